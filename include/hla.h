@@ -1,0 +1,215 @@
+/*
+ * hla.h -- C ABI of libhla.so: the B200 (sm_100a) hot path of Hilbert-guided
+ * local attention (arXiv 2511.05832).
+ *
+ * Citation convention: P:Lnnn = line nnn of the paper text.
+ *
+ * The method (P:L7):
+ *   1. image tokens of an H x W grid are reordered along a Hilbert curve
+ *      (hla_hilbert_perm; "the path can be precomputed and cached");
+ *   2. windows (HWA), slides (HSA) or neighborhoods (HNA) are formed on the
+ *      reordered 1D sequence; the N x N attention matrix is tiled into
+ *      b_q x b_k blocks that are full, partial or empty (hla_build_block_mask,
+ *      P:L85);
+ *   3. block-sparse attention skips empty blocks, runs full blocks unmasked and
+ *      masks partial blocks element-wise (hla_attn_fwd / hla_attn_bwd, P:L85,
+ *      P:L102 Eq. 1).
+ * The same kernels run the row-major baselines (WSA / SA / NA2D)
+ * and dense attention, selected by hla_pattern_desc.
+ *
+ * Conventions for every call:
+ *   - Tensor pointers are DEVICE pointers owned by the caller.  The library
+ *     allocates nothing and keeps no state between calls (thread-safe); the
+ *     only host-side state is a thread-local error string (hla_last_error).
+ *   - Calls are asynchronous on `stream` unless stated otherwise.
+ *   - Every argument check is host-side and synchronous; on any non-OK status
+ *     nothing has been launched.  No C++ exception crosses the ABI.
+ *   - Q, K, V, O, dO, dQ, dK, dV are bf16 tensors of layout [batch, N, heads,
+ *     head_dim] (head_dim contiguous), N = grid_h * grid_w, with token rows in
+ *     the sequence order of the pattern (Hilbert order for Hilbert patterns,
+ *     row-major grid order otherwise).  Base pointers must be 16-byte aligned.
+ *   - LSE / D are fp32 [batch, heads, N].
+ */
+#ifndef HLA_H_
+#define HLA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#if defined(__GNUC__)
+#define HLA_API __attribute__((visibility("default")))
+#else
+#define HLA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HLA_OK = 0,
+  HLA_ERR_INVALID = 1,      /* malformed arguments (window does not divide grid, N mismatch, ...) */
+  HLA_ERR_UNSUPPORTED = 2,  /* valid but outside the hot path's limits (head_dim, block, grid) */
+  HLA_ERR_CAPACITY = 3,     /* caller's CSR arrays too small; *nnz_out holds the needed size */
+  HLA_ERR_CUDA = 4          /* a CUDA runtime/driver call failed; see hla_last_error() */
+} hla_status;
+
+typedef enum {
+  HLA_ORDER_ROW_MAJOR = 0,  /* token t = row*W + col */
+  HLA_ORDER_HILBERT = 1     /* token s = position on the Hilbert curve */
+} hla_order;
+
+/* Pattern families.  With order = HILBERT they are the paper's HWA / HSA / HNA /
+ * HSWA, formed on the 1D Hilbert sequence with n = win_h*win_w tokens and
+ * r = n/2.  With order = ROW_MAJOR they are the
+ * conventional 2D baselines WSA / SA / NA2D.  Predicates (q, k
+ * are sequence positions; (rho, gamma) = (t / W, t % W)):
+ *   WINDOW        HWA : q/n == k/n                     WSA : rho_q/wh == rho_k/wh && gamma_q/ww == gamma_k/ww
+ *   SLIDE         HSA : |q-k| <= r                     SA  : |rho_q-rho_k| <= wh/2 && |gamma_q-gamma_k| <= ww/2
+ *   NEIGHBORHOOD  HNA : s <= k < s+2r+1,               NA2D: window of wh x ww cells whose start
+ *                       s = clamp(q-r, 0, N-2r-1)            is clamped into the grid
+ *   SHIFTED_WINDOW HSWA: floor((q-shift)/n) == floor((k-shift)/n)   (Hilbert order only)
+ *   DENSE         every pair (FlashAttention baseline)                               */
+typedef enum {
+  HLA_WINDOW = 0,
+  HLA_SLIDE = 1,
+  HLA_NEIGHBORHOOD = 2,
+  HLA_DENSE = 3,
+  HLA_SHIFTED_WINDOW = 4
+} hla_pattern;
+
+typedef enum {
+  HLA_TO_HILBERT = 0,       /* grid order  -> Hilbert order */
+  HLA_FROM_HILBERT = 1      /* Hilbert order -> grid order  */
+} hla_perm_dir;
+
+/* The problem statement of the paper: H x W token grid, window / neighborhood
+ * size, block size. */
+typedef struct {
+  int32_t grid_h, grid_w;   /* N = grid_h * grid_w */
+  int32_t order;            /* hla_order: sequence order the tensors are in */
+  int32_t pattern;          /* hla_pattern */
+  int32_t win_h, win_w;     /* window / kernel in cells; Hilbert patterns use n = win_h*win_w tokens */
+  int32_t shift;            /* HSWA 1D shift in tokens (0 <= shift < n); must be 0 otherwise */
+  int32_t block_q, block_k; /* tile shape b_q x b_k.  Mask builder: any >= 1.
+                               Attention: block_q == block_k == 128. */
+} hla_pattern_desc;
+
+/* Block mask in CSR form (caller-allocated DEVICE arrays).  Entry kinds:
+ * 1 = full (no element mask), 2 = partial (element-masked); empty tiles are not
+ * listed.  Lists are ascending.  Immutable after the build and shared
+ * read-only by every (batch, head) slice and every rank. */
+typedef struct {
+  int32_t n_qblocks, n_kblocks;  /* = ceil(N/block_q), ceil(N/block_k) */
+  int64_t capacity;              /* entries available in col_idx/kind and t_col_idx/t_kind */
+  int32_t* row_ptr;              /* [n_qblocks+1]  q-block -> kv-blocks (forward)  */
+  int32_t* col_idx;              /* [capacity]                                     */
+  uint8_t* kind;                 /* [capacity]                                     */
+  int32_t* t_row_ptr;            /* [n_kblocks+1]  kv-block -> q-blocks (backward) */
+  int32_t* t_col_idx;            /* [capacity]                                     */
+  uint8_t* t_kind;               /* [capacity]                                     */
+  int64_t* counts;               /* [4]: nnz, n_full, n_partial, n_empty           */
+} hla_block_mask;
+
+/* ---------------------------------------------------------------------------
+ * hla_hilbert_index -- the cached Hilbert path: seq_to_cell[s] = cell
+ * (row*W + col) of the s-th curve position, cell_to_seq = its inverse.  Either
+ * output may be NULL.  Curve: classic Hilbert d2xy with x = column, y = row,
+ * starting at (0,0) (reading R1).  grid must be square 2^k with
+ * 1 <= 2^k <= 32768, else HLA_ERR_UNSUPPORTED.
+ */
+HLA_API hla_status hla_hilbert_index(int32_t grid_h, int32_t grid_w,
+                             int32_t* seq_to_cell, int32_t* cell_to_seq,
+                             cudaStream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * hla_hilbert_perm -- reorder token rows between grid order and Hilbert order
+ * ("image tokens are first reordered along a Hilbert curve", P:L7; the
+ * "Reshape" step of P:L196).  Both directions are gathers:
+ *   TO_HILBERT  : dst[b, s, :] = src[b, seq_to_cell[s], :]
+ *   FROM_HILBERT: dst[b, t, :] = src[b, cell_to_seq[t], :]
+ * src, dst: HOST arrays of n_tensors (1..4) DEVICE pointers, each a tensor of
+ * [batch, N, row_bytes] bytes (bit-exact copy; any element type).  row_bytes
+ * must be a multiple of 16 and pointers 16-byte aligned.  src[i] != dst[i].
+ * seq_to_cell_out: optional device int32[N] export of the index table (NULL = skip).
+ * Grid must be square 2^k (else HLA_ERR_UNSUPPORTED).
+ */
+HLA_API hla_status hla_hilbert_perm(int32_t grid_h, int32_t grid_w, int32_t dir,
+                            int32_t batch, int32_t row_bytes, int32_t n_tensors,
+                            const void* const* src, void* const* dst,
+                            int32_t* seq_to_cell_out, cudaStream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * hla_build_block_mask -- classify every b_q x b_k tile as full / partial /
+ * empty and emit CSR lists, their transpose and counts.
+ * Sizing call: if m->col_idx == NULL, only row_ptr, t_row_ptr and counts are
+ * written; the call synchronises `stream` and writes nnz to *nnz_out.
+ * Fill call: all arrays written; if nnz > m->capacity returns HLA_ERR_CAPACITY
+ * with the needed nnz in *nnz_out (row_ptr/t_row_ptr/counts are then valid).
+ * The fill call also synchronises (it reads nnz back).  Any block >= 1 and any
+ * N are accepted (tiles with padding positions are never full).
+ * Not on the per-step path: built once per (shape, pattern, block), like the
+ * paper's cached path.
+ */
+HLA_API hla_status hla_build_block_mask(const hla_pattern_desc* d, hla_block_mask* m,
+                                int64_t* nnz_out, cudaStream_t stream);
+
+/* Host helper: the two sparsity ratios of a built mask from its integer counts
+ * (host copy of m->counts): empty_tile_ratio = n_empty / (Mq*Mk); sparsity =
+ * 1 - nnz*b_q*b_k / N^2, the paper's "Sparsity" column (DESIGN.md
+ * reading R7).  Either output may be NULL. */
+HLA_API hla_status hla_mask_ratios(const hla_pattern_desc* d, const int64_t counts[4],
+                           double* empty_tile_ratio, double* sparsity);
+
+/* ---------------------------------------------------------------------------
+ * hla_attn_fwd -- block-sparse attention forward:
+ *   for every (b, h, q-block i) and every listed kv-block j (ascending):
+ *     S = scale * Q_i K_j^T (tcgen05, fp32 in TMEM); mask only if kind == partial;
+ *     online softmax (exp2); O_i += P V_j.
+ *   O = O / l (bf16), LSE = m + ln(l) (fp32, natural log).
+ * q, k, v, o: bf16 [batch, N, heads, head_dim] in d->order.  lse: fp32
+ * [batch, heads, N].  scale <= 0 selects 1/sqrt(head_dim).
+ * Limits: head_dim in {32, 64}; block_q == block_k == 128; N % 128 == 0;
+ * mask built for the same descriptor (n_qblocks == N/128).
+ * tiles_visited: optional device int64 counter; when non-NULL the kernel adds
+ * the number of tiles it executed (must equal batch*heads*nnz: empty tiles are
+ * skipped).
+ */
+HLA_API hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_mask* m,
+                        int32_t batch, int32_t heads, int32_t head_dim, float scale,
+                        const void* q, const void* k, const void* v,
+                        void* o, float* lse, int64_t* tiles_visited,
+                        cudaStream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * hla_attn_bwd -- backward of hla_attn_fwd over the transposed lists.
+ *   P = exp(scale*S - LSE) (masked -> 0 on partial tiles), D = rowsum(dO o O),
+ *   dV = P^T dO, dS = P o (dO V^T - D), dK = scale dS^T Q, dQ = scale dS K.
+ * q, k, v, o, dout, dq, dk, dv: bf16 [batch, N, heads, head_dim]; lse from the
+ * forward.  workspace: device memory of at least hla_attn_bwd_workspace(...)
+ * bytes, 256-byte aligned (fp32 dQ accumulator + D); its contents need not be
+ * initialised.  dQ accumulation uses fp32 atomics (summation order is not
+ * deterministic; covered by the stated tolerance).  Same limits as the forward.
+ */
+HLA_API hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_mask* m,
+                        int32_t batch, int32_t heads, int32_t head_dim, float scale,
+                        const void* q, const void* k, const void* v, const void* o,
+                        const float* lse, const void* dout,
+                        void* dq, void* dk, void* dv,
+                        void* workspace, size_t workspace_bytes,
+                        int64_t* tiles_visited, cudaStream_t stream);
+
+HLA_API size_t hla_attn_bwd_workspace(int32_t batch, int32_t heads, int32_t n, int32_t head_dim);
+
+/* Thread-local message for the last non-OK status of this thread ("" if none). */
+HLA_API const char* hla_last_error(void);
+
+/* Library build identification (arch, version). */
+HLA_API const char* hla_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif  /* HLA_H_ */

@@ -1,0 +1,30 @@
+/*
+ * hla_debug.h -- bring-up entry points of libhla.so (not part of the hot path).
+ *
+ * hla_debug_umma: one CTA computes C[m][n] = sum_k A(m,k) * B(n,k) (fp32) with
+ * tcgen05.mma (M = 128, kind::f16, bf16 inputs), staging the operands in shared
+ * memory in the canonical SWIZZLE_128B layouts the attention kernels use, so the
+ * descriptor / instruction-descriptor encodings can be checked against a plain
+ * matmul.  A is stored [M][K] (a_major_mn = 0, K-major) or [K][M] (a_major_mn =
+ * 1, MN-major); B is stored [N][K] (b_major_mn = 0) or [K][N] (b_major_mn = 1).
+ * a_from_tmem = 1 stages A in tensor memory instead (then a_major_mn must be 0).
+ * Limits: M == 128, N in {64,128,192,256}, K in {64, 128}.  All pointers device;
+ * synchronous w.r.t. `stream` ordering only (asynchronous call).
+ */
+#ifndef HLA_DEBUG_H_
+#define HLA_DEBUG_H_
+
+#include "hla.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+HLA_API hla_status hla_debug_umma(const void* A, const void* B, float* C, int32_t M, int32_t N, int32_t K,
+                          int32_t a_major_mn, int32_t b_major_mn, int32_t a_from_tmem, cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HLA_DEBUG_H_ */

@@ -1,0 +1,175 @@
+"""Thin Python binding of libhla.so with the C ABI's names (argument marshalling only).
+
+Every step of the path runs in the CUDA kernels behind include/hla.h; PyTorch is
+used for device memory, streams and process groups only.  There is no CPU or
+PyTorch fallback: if libhla.so is missing, the first call raises.
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import BlockMaskC, PatternDesc, check, lib
+
+ORDER_ROW_MAJOR, ORDER_HILBERT = 0, 1
+WINDOW, SLIDE, NEIGHBORHOOD, DENSE, SHIFTED_WINDOW = 0, 1, 2, 3, 4
+TO_HILBERT, FROM_HILBERT = 0, 1
+
+# paper names -> (order, pattern family)   (HWA/HSA/HNA/HSWA: P:L39; WSA/SA/NA2D: P:L28)
+KINDS = {
+    "HWA": (ORDER_HILBERT, WINDOW), "HSA": (ORDER_HILBERT, SLIDE), "HNA": (ORDER_HILBERT, NEIGHBORHOOD),
+    "HSWA": (ORDER_HILBERT, SHIFTED_WINDOW), "WSA": (ORDER_ROW_MAJOR, WINDOW), "SA": (ORDER_ROW_MAJOR, SLIDE),
+    "NA2D": (ORDER_ROW_MAJOR, NEIGHBORHOOD), "DENSE": (ORDER_ROW_MAJOR, DENSE),
+}
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def pattern_desc(kind, grid_h, grid_w, win_h=1, win_w=1, block=128, shift=0):
+    order, pattern = KINDS[kind]
+    return PatternDesc(grid_h, grid_w, order, pattern, win_h, win_w, shift, block, block)
+
+
+def is_hilbert(desc):
+    return desc.order == ORDER_HILBERT
+
+
+@dataclass
+class BlockMask:
+    """Device CSR block mask (include/hla.h hla_block_mask) plus its host counts."""
+    desc: PatternDesc
+    row_ptr: torch.Tensor
+    col_idx: torch.Tensor
+    kind: torch.Tensor
+    t_row_ptr: torch.Tensor
+    t_col_idx: torch.Tensor
+    t_kind: torch.Tensor
+    counts: torch.Tensor          # device int64[4]: nnz, n_full, n_partial, n_empty
+    host_counts: tuple = None
+
+    @property
+    def c(self):
+        return BlockMaskC(self.row_ptr.numel() - 1, self.t_row_ptr.numel() - 1, self.col_idx.numel(),
+                          self.row_ptr.data_ptr(), self.col_idx.data_ptr(), self.kind.data_ptr(),
+                          self.t_row_ptr.data_ptr(), self.t_col_idx.data_ptr(), self.t_kind.data_ptr(),
+                          self.counts.data_ptr())
+
+    @property
+    def nnz(self):
+        return self.host_counts[0]
+
+    def ratios(self):
+        """(empty_tile_ratio, sparsity) computed by hla_mask_ratios from the integer counts."""
+        cnt = (ctypes.c_int64 * 4)(*self.host_counts)
+        e, s = ctypes.c_double(), ctypes.c_double()
+        check("hla_mask_ratios", lib().hla_mask_ratios(ctypes.byref(self.desc), cnt, ctypes.byref(e), ctypes.byref(s)))
+        return e.value, s.value
+
+
+def hla_hilbert_index(grid_h, grid_w, device="cuda", stream=None):
+    n = grid_h * grid_w
+    s2c = torch.empty(n, dtype=torch.int32, device=device)
+    c2s = torch.empty(n, dtype=torch.int32, device=device)
+    check("hla_hilbert_index", lib().hla_hilbert_index(grid_h, grid_w, _ptr(s2c), _ptr(c2s), _stream(stream)))
+    return s2c, c2s
+
+
+def hla_hilbert_perm(grid_h, grid_w, direction, srcs, dsts=None, stream=None):
+    """Permute token rows of up to 4 tensors [B, N, ...] between grid and Hilbert order."""
+    srcs = list(srcs)
+    if dsts is None:
+        dsts = [torch.empty_like(s) for s in srcs]
+    B, N = srcs[0].shape[0], srcs[0].shape[1]
+    row_bytes = srcs[0][0, 0].numel() * srcs[0].element_size()
+    for s, d in zip(srcs, dsts):
+        assert s.is_cuda and s.is_contiguous() and d.is_contiguous() and s.shape == d.shape
+        assert s.shape[0] == B and s.shape[1] == N and s[0, 0].numel() * s.element_size() == row_bytes
+    n = len(srcs)
+    src_arr = (ctypes.c_void_p * n)(*[s.data_ptr() for s in srcs])
+    dst_arr = (ctypes.c_void_p * n)(*[d.data_ptr() for d in dsts])
+    check("hla_hilbert_perm", lib().hla_hilbert_perm(grid_h, grid_w, direction, B, row_bytes, n, src_arr, dst_arr,
+                                                     None, _stream(stream)))
+    return dsts
+
+
+def hla_build_block_mask(desc, device="cuda", stream=None):
+    """Sizing call, then fill call (both synchronous; built once per shape)."""
+    N = desc.grid_h * desc.grid_w
+    mq = (N + desc.block_q - 1) // desc.block_q
+    mk = (N + desc.block_k - 1) // desc.block_k
+    i32 = dict(dtype=torch.int32, device=device)
+    m = BlockMask(desc, torch.zeros(mq + 1, **i32), torch.empty(0, **i32), torch.empty(0, dtype=torch.uint8, device=device),
+                  torch.zeros(mk + 1, **i32), torch.empty(0, **i32), torch.empty(0, dtype=torch.uint8, device=device),
+                  torch.zeros(4, dtype=torch.int64, device=device))
+    c = m.c
+    c.col_idx = None
+    nnz = ctypes.c_int64()
+    check("hla_build_block_mask", lib().hla_build_block_mask(ctypes.byref(desc), ctypes.byref(c), ctypes.byref(nnz),
+                                                             _stream(stream)))
+    cap = max(1, nnz.value)
+    m.col_idx = torch.empty(cap, **i32)
+    m.kind = torch.empty(cap, dtype=torch.uint8, device=device)
+    m.t_col_idx = torch.empty(cap, **i32)
+    m.t_kind = torch.empty(cap, dtype=torch.uint8, device=device)
+    c = m.c
+    check("hla_build_block_mask", lib().hla_build_block_mask(ctypes.byref(desc), ctypes.byref(c), ctypes.byref(nnz),
+                                                             _stream(stream)))
+    m.host_counts = tuple(int(x) for x in m.counts.cpu().tolist())
+    return m
+
+
+def hla_attn_fwd(desc, mask, q, k, v, scale=0.0, o=None, lse=None, tiles_visited=None, stream=None):
+    """q, k, v: bf16 [B, N, heads, d] in desc's sequence order -> (o, lse [B, heads, N] fp32)."""
+    B, N, H, D = q.shape
+    for t in (q, k, v):
+        assert t.dtype == torch.bfloat16 and t.is_cuda and t.is_contiguous() and t.shape == q.shape
+    if o is None:
+        o = torch.empty_like(q)
+    if lse is None:
+        lse = torch.empty(B, H, N, dtype=torch.float32, device=q.device)
+    mc = mask.c
+    check("hla_attn_fwd", lib().hla_attn_fwd(ctypes.byref(desc), ctypes.byref(mc), B, H, D, float(scale),
+                                             _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(tiles_visited),
+                                             _stream(stream)))
+    return o, lse
+
+
+def hla_attn_bwd_workspace(B, H, N, D):
+    return int(lib().hla_attn_bwd_workspace(B, H, N, D))
+
+
+def hla_attn_bwd(desc, mask, q, k, v, o, lse, dout, scale=0.0, dq=None, dk=None, dv=None, workspace=None,
+                 tiles_visited=None, stream=None):
+    B, N, H, D = q.shape
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    nbytes = hla_attn_bwd_workspace(B, H, N, D)
+    if workspace is None:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=q.device)
+    mc = mask.c
+    check("hla_attn_bwd", lib().hla_attn_bwd(ctypes.byref(desc), ctypes.byref(mc), B, H, D, float(scale),
+                                             _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(dout),
+                                             _ptr(dq), _ptr(dk), _ptr(dv), _ptr(workspace), workspace.numel(),
+                                             _ptr(tiles_visited), _stream(stream)))
+    return dq, dk, dv
+
+
+def hla_debug_umma(A, B, M, N, K, a_mn=False, b_mn=False, a_tmem=False, stream=None):
+    C = torch.empty(M, N, dtype=torch.float32, device=A.device)
+    check("hla_debug_umma", lib().hla_debug_umma(_ptr(A), _ptr(B), _ptr(C), M, N, K, int(a_mn), int(b_mn),
+                                                 int(a_tmem), _stream(stream)))
+    return C
+
+
+def version():
+    return lib().hla_version().decode()

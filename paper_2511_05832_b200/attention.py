@@ -1,0 +1,77 @@
+"""HilbertLocalAttention -- the public, allocation-free step API over the C ABI.
+
+One instance = one attention layer shape.  Construction does the once-per-shape
+work the paper caches ("the path can be precomputed and cached"): the
+block mask is built on the GPU and all intermediate buffers are allocated.
+forward() / backward() then only launch libhla kernels (capturable in a CUDA
+graph):
+
+  Hilbert patterns (HWA / HSA / HNA / HSWA), tensors given in grid order:
+    forward : perm(q,k,v -> Hilbert) ; hla_attn_fwd ; perm(o -> grid)
+    backward: perm(dO -> Hilbert) ; hla_attn_bwd ; perm(dq,dk,dv -> grid)
+  Row-major baselines (WSA / SA / NA2D / DENSE) run the same attention kernels
+  directly on grid order.
+"""
+
+import torch
+
+from . import api
+
+
+class HilbertLocalAttention:
+    def __init__(self, kind, grid_h, grid_w, win_h=1, win_w=1, batch=1, heads=1, head_dim=64, block=128,
+                 shift=0, scale=0.0, device="cuda"):
+        self.kind = kind
+        self.grid_h, self.grid_w = grid_h, grid_w
+        self.N = grid_h * grid_w
+        self.shape = (batch, self.N, heads, head_dim)
+        self.scale = float(scale)
+        self.desc = api.pattern_desc(kind, grid_h, grid_w, win_h, win_w, block, shift)
+        self.mask = api.hla_build_block_mask(self.desc, device)
+        self.hilbert = api.is_hilbert(self.desc)
+        bf = dict(dtype=torch.bfloat16, device=device)
+        e = lambda: torch.empty(self.shape, **bf)   # noqa: E731
+        self.o, self.dq, self.dk, self.dv = e(), e(), e(), e()
+        self.lse = torch.empty(batch, heads, self.N, dtype=torch.float32, device=device)
+        self.workspace = torch.empty(api.hla_attn_bwd_workspace(batch, heads, self.N, head_dim),
+                                     dtype=torch.uint8, device=device)
+        if self.hilbert:
+            self.qs, self.ks, self.vs, self.os = e(), e(), e(), e()
+            self.dos, self.dqs, self.dks, self.dvs = e(), e(), e(), e()
+        self._saved = None
+
+    # tiles executed per step, per (b, h): R (P:L102 r_i summed over q-blocks)
+    @property
+    def nnz(self):
+        return self.mask.nnz
+
+    def forward(self, q, k, v):
+        """q, k, v: bf16 [B, N, heads, d] in grid (row-major cell) order -> o (grid order)."""
+        if self.hilbert:
+            api.hla_hilbert_perm(self.grid_h, self.grid_w, api.TO_HILBERT, (q, k, v), (self.qs, self.ks, self.vs))
+            api.hla_attn_fwd(self.desc, self.mask, self.qs, self.ks, self.vs, self.scale, self.os, self.lse)
+            api.hla_hilbert_perm(self.grid_h, self.grid_w, api.FROM_HILBERT, (self.os,), (self.o,))
+            self._saved = (self.qs, self.ks, self.vs, self.os)
+        else:
+            api.hla_attn_fwd(self.desc, self.mask, q, k, v, self.scale, self.o, self.lse)
+            self._saved = (q, k, v, self.o)
+        return self.o
+
+    def backward(self, dout):
+        """dout: bf16 [B, N, heads, d] in grid order -> (dq, dk, dv) in grid order."""
+        q, k, v, o = self._saved
+        if self.hilbert:
+            api.hla_hilbert_perm(self.grid_h, self.grid_w, api.TO_HILBERT, (dout,), (self.dos,))
+            api.hla_attn_bwd(self.desc, self.mask, q, k, v, o, self.lse, self.dos, self.scale,
+                             self.dqs, self.dks, self.dvs, self.workspace)
+            api.hla_hilbert_perm(self.grid_h, self.grid_w, api.FROM_HILBERT, (self.dqs, self.dks, self.dvs),
+                                 (self.dq, self.dk, self.dv))
+        else:
+            api.hla_attn_bwd(self.desc, self.mask, q, k, v, o, self.lse, dout, self.scale,
+                             self.dq, self.dk, self.dv, self.workspace)
+        return self.dq, self.dk, self.dv
+
+    def step(self, q, k, v, dout):
+        """One pass of the whole hot path: forward then backward."""
+        self.forward(q, k, v)
+        return self.backward(dout)

@@ -1,0 +1,359 @@
+// K6: block-sparse attention forward on sm_100a (tcgen05 + TMEM + TMA).
+//
+// Paper: "Block-sparse attention tiles the N x N matrix into fixed-size blocks
+// ... empty blocks are skipped, full blocks run unmasked, partial blocks require
+// element-wise masking"; per CTA cost alpha + beta * r_i, where beta
+// covers "loading q block and k/v block, computing qk^T within the block, ...,
+// online softmax, and aggregation with value" (Eq. 1).
+//
+// One CTA per (q-block i, head h, batch b), 192 threads, 2 CTAs per SM:
+//   warp 0      TMA producer: Q_i once, then K_j / V_j of the listed kv-blocks
+//               into a 2-stage shared-memory ring (separate K and V barriers).
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:
+//                 S_t  = Q_i K_j^T   (SS MMA, 128x128x D, fp32 in TMEM cols [0,128))
+//                 O   += P_t V_j     (TS MMA, P bf16 in TMEM cols [128,192), O in [192,192+D))
+//   warps 2..5  softmax: thread = query row (TMEM lane); reads its S row with
+//               tcgen05.ld, applies the element mask only when the tile is
+//               partial, keeps the online max / sum in registers (lazy rescale:
+//               O is rescaled in TMEM only when the row max grows by > 2^8),
+//               writes P (bf16) to TMEM; epilogue O / l -> bf16, LSE.
+// The S region is reused by S_{t+1} only after the softmax of tile t has
+// released it (p_full); P has its own region, so S_{t+1} overlaps nothing the
+// PV MMA still reads.  Every commit tracks all earlier MMAs, so s_full(t) also
+// certifies that PV_{t-1} finished (O may then be rescaled safely).
+#include "predicates.cuh"
+#include "sm100.cuh"
+#include "tensor_map.cuh"
+
+namespace hla {
+namespace {
+
+constexpr int kBlock = 128;
+constexpr int kThreads = 192;
+constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kColS = 0, kColP = 128, kColO = 192;
+
+struct FwdParams {
+  Pattern pat;
+  int32_t N, heads, batch;
+  float scale_log2;
+  const int32_t* row_ptr;
+  const int32_t* col_idx;
+  const uint8_t* kind;
+  __nv_bfloat16* o;
+  float* lse;
+  unsigned long long* visited;
+};
+
+template <int D>
+struct FwdSmem {
+  static constexpr uint32_t kTileBytes = kBlock * D * 2;
+  alignas(1024) uint8_t q[kTileBytes];
+  alignas(1024) uint8_t k[2][kTileBytes];
+  alignas(1024) uint8_t v[2][kTileBytes];
+  uint64_t q_full, k_full[2], v_full[2], kv_empty[2], s_full, p_full, o_full;
+  uint32_t tmem_base;
+};
+
+template <int D>
+__device__ __forceinline__ uint64_t kmajor_desc(const uint8_t* tile, int kstep) {
+  // rows of D bf16 (= swizzle width), 8-row groups 8*2D bytes apart; K step = 16 elements = 32 B
+  constexpr uint32_t layout = D == 64 ? sm100::kSwizzle128B : sm100::kSwizzle64B;
+  return sm100::make_smem_desc(sm100::smem_u32(tile) + kstep * 32, 16, 8 * D * 2, layout);
+}
+template <int D>
+__device__ __forceinline__ uint64_t mnmajor_desc(const uint8_t* tile, int kstep) {
+  // V as the B operand of O = P V: N = D (one swizzle atom wide), K = kv rows;
+  // 8-row K groups 8*2D bytes apart; K step = 16 rows
+  constexpr uint32_t layout = D == 64 ? sm100::kSwizzle128B : sm100::kSwizzle64B;
+  return sm100::make_smem_desc(sm100::smem_u32(tile) + kstep * 16 * D * 2, kBlock * D * 2, 8 * D * 2, layout);
+}
+
+template <int D, bool kTwoD>
+__global__ void __launch_bounds__(kThreads, 2)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const FwdParams prm) {
+  extern __shared__ uint8_t smem_raw[];
+  FwdSmem<D>& sm = *reinterpret_cast<FwdSmem<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int32_t rs = __ldg(prm.row_ptr + qb), nt = __ldg(prm.row_ptr + qb + 1) - rs;
+  const int32_t row0 = b * prm.N + qb * kBlock;  // first token row of this q-block in [B*N]
+
+  if (warp == 0 && lane == 0) {
+    sm100::mbar_init(&sm.q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      sm100::mbar_init(&sm.k_full[s], 1);
+      sm100::mbar_init(&sm.v_full[s], 1);
+      sm100::mbar_init(&sm.kv_empty[s], 1);
+    }
+    sm100::mbar_init(&sm.s_full, 1);
+    sm100::mbar_init(&sm.p_full, 128);
+    sm100::mbar_init(&sm.o_full, 1);
+    sm100::fence_mbar_init();
+    sm100::tma_prefetch_desc(&tmQ);
+    sm100::tma_prefetch_desc(&tmK);
+    sm100::tma_prefetch_desc(&tmV);
+  }
+  if (warp == 1) {
+    sm100::tmem_alloc(&sm.tmem_base, kTmemCols);
+    sm100::tmem_relinquish();
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0 && nt > 0) {
+      const uint64_t pol_q = sm100::policy_evict_first();
+      const uint64_t pol_kv = sm100::policy_evict_last();
+      sm100::mbar_arrive_expect_tx(&sm.q_full, FwdSmem<D>::kTileBytes);
+      sm100::tma_load_3d(sm.q, &tmQ, &sm.q_full, 0, h, row0, pol_q);
+      for (int t = 0; t < nt; ++t) {
+        const int s = t & 1;
+        if (t >= 2) sm100::mbar_wait(&sm.kv_empty[s], ((t >> 1) - 1) & 1);
+        const int32_t krow = b * prm.N + __ldg(prm.col_idx + rs + t) * kBlock;
+        sm100::mbar_arrive_expect_tx(&sm.k_full[s], FwdSmem<D>::kTileBytes);
+        sm100::tma_load_3d(sm.k[s], &tmK, &sm.k_full[s], 0, h, krow, pol_kv);
+        sm100::mbar_arrive_expect_tx(&sm.v_full[s], FwdSmem<D>::kTileBytes);
+        sm100::tma_load_3d(sm.v[s], &tmV, &sm.v_full[s], 0, h, krow, pol_kv);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------- MMA issuer
+    if (lane == 0 && nt > 0) {
+      constexpr uint32_t idesc_s = sm100::make_idesc_bf16(kBlock, kBlock, false, false);
+      constexpr uint32_t idesc_o = sm100::make_idesc_bf16(kBlock, D, false, true);
+      const uint32_t tS = tmem + kColS, tP = tmem + kColP, tO = tmem + kColO;
+      auto issue_s = [&](int s) {
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          sm100::mma_ss(tS, kmajor_desc<D>(sm.q, kk), kmajor_desc<D>(sm.k[s], kk), idesc_s, kk > 0);
+        sm100::mma_commit(&sm.s_full);
+      };
+      sm100::mbar_wait(&sm.q_full, 0);
+      sm100::mbar_wait(&sm.k_full[0], 0);
+      sm100::tc_fence_after();
+      issue_s(0);
+      for (int t = 0; t < nt; ++t) {
+        const int s = t & 1;
+        sm100::mbar_wait(&sm.p_full, t & 1);
+        sm100::mbar_wait(&sm.v_full[s], (t >> 1) & 1);
+        sm100::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < kBlock / 16; ++kk)
+          sm100::mma_ts(tO, tP + kk * 8, mnmajor_desc<D>(sm.v[s], kk), idesc_o, (t > 0 || kk > 0) ? 1u : 0u);
+        sm100::mma_commit(&sm.kv_empty[s]);
+        if (t + 1 < nt) {
+          const int s2 = (t + 1) & 1;
+          sm100::mbar_wait(&sm.k_full[s2], ((t + 1) >> 1) & 1);
+          sm100::tc_fence_after();
+          issue_s(s2);
+        } else {
+          sm100::mma_commit(&sm.o_full);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------- softmax + epilogue
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const int32_t q = qb * kBlock + row;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const float sl2 = prm.scale_log2;
+    float m_ref = -INFINITY, l = 0.f;
+    RowBox box;
+    if (nt > 0) box = row_box(prm.pat, q);
+
+    for (int t = 0; t < nt; ++t) {
+      sm100::mbar_wait(&sm.s_full, t & 1);
+      sm100::tc_fence_after();
+      float s[kBlock];
+      {
+        uint32_t r[32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          sm100::tmem_ld32(tmem + lane_off + kColS + c * 32, r);
+          sm100::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(r[e]);
+        }
+      }
+      const uint8_t kd = __ldg(prm.kind + rs + t);
+      if (kd == 2) {
+        const int32_t k0 = __ldg(prm.col_idx + rs + t) * kBlock;
+        if (!kTwoD) {
+#pragma unroll
+          for (int c = 0; c < kBlock; ++c)
+            if ((uint32_t)(k0 + c - box.lo) >= (uint32_t)box.len) s[c] = -INFINITY;
+        } else if (prm.pat.log2W >= 0) {
+          const int sh = prm.pat.log2W;
+          const int32_t wm = prm.pat.W - 1;
+#pragma unroll
+          for (int c = 0; c < kBlock; ++c) {
+            const int32_t k = k0 + c;
+            const bool ok = ((uint32_t)((k >> sh) - box.lo) < (uint32_t)box.len) &&
+                            ((uint32_t)((k & wm) - box.c0) < (uint32_t)box.cn);
+            if (!ok) s[c] = -INFINITY;
+          }
+        } else {
+          const int32_t W = prm.pat.W;
+#pragma unroll
+          for (int c = 0; c < kBlock; ++c) {
+            const int32_t k = k0 + c;
+            const int32_t rk = k / W, ck = k - rk * W;
+            const bool ok = ((uint32_t)(rk - box.lo) < (uint32_t)box.len) &&
+                            ((uint32_t)(ck - box.c0) < (uint32_t)box.cn);
+            if (!ok) s[c] = -INFINITY;
+          }
+        }
+      }
+      float mx = s[0];
+#pragma unroll
+      for (int c = 1; c < kBlock; ++c) mx = fmaxf(mx, s[c]);
+      const float m_tile = mx * sl2;
+      // lazy rescale (exact): keep the reference max unless it grew by > 8 (x256)
+      const float m_new = (m_tile > m_ref + 8.f) ? m_tile : m_ref;
+      const float alpha = (m_new == m_ref) ? 1.f : sm100::ex2(m_ref - m_new);
+      if (__any_sync(0xffffffffu, t > 0 && alpha != 1.f)) {
+        uint32_t o[32];
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          sm100::tmem_ld32(tmem + lane_off + kColO + c * 32, o);
+          sm100::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+          sm100::tmem_st32(tmem + lane_off + kColO + c * 32, o);
+        }
+        sm100::tmem_wait_st();
+      }
+      m_ref = m_new;
+      l *= alpha;
+      const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        uint32_t pk[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const float p0 = sm100::ex2(fmaf(s[half * 64 + 2 * e], sl2, -m_use));
+          const float p1 = sm100::ex2(fmaf(s[half * 64 + 2 * e + 1], sl2, -m_use));
+          l += p0 + p1;
+          pk[e] = sm100::pack_bf16(p0, p1);
+        }
+        sm100::tmem_st32(tmem + lane_off + kColP + half * 32, pk);
+      }
+      sm100::tmem_wait_st();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&sm.p_full);
+    }
+
+    // epilogue: O / l -> bf16 row, LSE (natural log)
+    const int64_t orow = ((int64_t)b * prm.N + q) * prm.heads + h;
+    uint4* optr = reinterpret_cast<uint4*>(prm.o + orow * D);
+    const float inv_l = l > 0.f ? 1.f / l : 0.f;
+    if (nt > 0) {
+      sm100::mbar_wait(&sm.o_full, 0);
+      sm100::tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t o[32];
+        sm100::tmem_ld32(tmem + lane_off + kColO + c * 32, o);
+        sm100::tmem_wait_ld();
+#pragma unroll
+        for (int v4 = 0; v4 < 4; ++v4) {
+          uint4 w;
+          w.x = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 0]) * inv_l, __uint_as_float(o[v4 * 8 + 1]) * inv_l);
+          w.y = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 2]) * inv_l, __uint_as_float(o[v4 * 8 + 3]) * inv_l);
+          w.z = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 4]) * inv_l, __uint_as_float(o[v4 * 8 + 5]) * inv_l);
+          w.w = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 6]) * inv_l, __uint_as_float(o[v4 * 8 + 7]) * inv_l);
+          optr[c * 4 + v4] = w;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < D / 8; ++c) optr[c] = make_uint4(0, 0, 0, 0);
+    }
+    const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
+    prm.lse[((int64_t)b * prm.heads + h) * prm.N + q] =
+        l > 0.f ? (m_use + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+  }
+
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  if (warp == 1) sm100::tmem_dealloc(tmem, kTmemCols);
+  if (threadIdx.x == 0 && prm.visited != nullptr && nt > 0) atomicAdd(prm.visited, (unsigned long long)nt);
+}
+
+template <int D, bool kTwoD>
+hla_status launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const FwdParams& prm,
+                      int32_t n_qblocks, cudaStream_t stream) {
+  const size_t smem = sizeof(FwdSmem<D>) + 1024;
+  auto* fn = attn_fwd_kernel<D, kTwoD>;
+  HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid(n_qblocks, prm.heads, prm.batch);
+  fn<<<grid, kThreads, smem, stream>>>(mq, mk, mv, prm);
+  HLA_CUDA_TRY(cudaGetLastError());
+  return HLA_OK;
+}
+
+}  // namespace
+
+// shared argument validation of forward and backward (declared in attn_common.cuh)
+hla_status check_attn_args(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
+                           int32_t head_dim, Pattern* pat) {
+  hla_status st = make_pattern(d, pat);
+  if (st != HLA_OK) return st;
+  HLA_REQUIRE(m != nullptr && m->row_ptr && m->col_idx && m->kind, HLA_ERR_INVALID, "mask arrays missing");
+  HLA_REQUIRE(head_dim == 32 || head_dim == 64, HLA_ERR_UNSUPPORTED, "head_dim %d not in {32, 64}", head_dim);
+  HLA_REQUIRE(d->block_q == kBlock && d->block_k == kBlock, HLA_ERR_UNSUPPORTED,
+              "attention needs block_q == block_k == 128 (got %d, %d)", d->block_q, d->block_k);
+  HLA_REQUIRE(pat->N % kBlock == 0, HLA_ERR_UNSUPPORTED, "N=%d not a multiple of 128 (phantom padding is NEXT-4)",
+              pat->N);
+  HLA_REQUIRE(m->n_qblocks == pat->N / kBlock && m->n_kblocks == pat->N / kBlock, HLA_ERR_INVALID,
+              "mask built for a different N / block");
+  HLA_REQUIRE(batch >= 1 && batch <= 65535 && heads >= 1 && heads <= 65535, HLA_ERR_INVALID,
+              "batch %d / heads %d out of range", batch, heads);
+  return HLA_OK;
+}
+
+}  // namespace hla
+
+using namespace hla;
+
+extern "C" hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
+                                   int32_t head_dim, float scale, const void* q, const void* k, const void* v,
+                                   void* o, float* lse, int64_t* tiles_visited, cudaStream_t stream) {
+  clear_error();
+  Pattern pat;
+  hla_status st = check_attn_args(d, m, batch, heads, head_dim, &pat);
+  if (st != HLA_OK) return st;
+  HLA_REQUIRE(q && k && v && o && lse, HLA_ERR_INVALID, "null tensor pointer");
+  HLA_REQUIRE((((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)o) & 15) == 0, HLA_ERR_INVALID,
+              "tensors must be 16-byte aligned");
+  const float sc = scale > 0.f ? scale : 1.0f / sqrtf((float)head_dim);
+  FwdParams prm;
+  prm.pat = pat;
+  prm.N = pat.N;
+  prm.heads = heads;
+  prm.batch = batch;
+  prm.scale_log2 = sc * 1.4426950408889634f;
+  prm.row_ptr = m->row_ptr;
+  prm.col_idx = m->col_idx;
+  prm.kind = m->kind;
+  prm.o = reinterpret_cast<__nv_bfloat16*>(o);
+  prm.lse = lse;
+  prm.visited = reinterpret_cast<unsigned long long*>(tiles_visited);
+  const int64_t rows = (int64_t)batch * pat.N;
+  CUtensorMap mq, mk, mv;
+  if ((st = make_rows_map(&mq, q, rows, heads, head_dim, kBlock)) != HLA_OK) return st;
+  if ((st = make_rows_map(&mk, k, rows, heads, head_dim, kBlock)) != HLA_OK) return st;
+  if ((st = make_rows_map(&mv, v, rows, heads, head_dim, kBlock)) != HLA_OK) return st;
+  const bool two_d = pat.kind == K_WSA || pat.kind == K_SA || pat.kind == K_NA2D;
+  const int32_t mqb = pat.N / kBlock;
+  if (head_dim == 64)
+    return two_d ? launch_fwd<64, true>(mq, mk, mv, prm, mqb, stream) : launch_fwd<64, false>(mq, mk, mv, prm, mqb, stream);
+  return two_d ? launch_fwd<32, true>(mq, mk, mv, prm, mqb, stream) : launch_fwd<32, false>(mq, mk, mv, prm, mqb, stream);
+}

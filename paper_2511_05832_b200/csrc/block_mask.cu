@@ -1,0 +1,200 @@
+// K3-K5: block-mask builder.  Classifies every b_q x b_k tile of the N x N
+// attention matrix as full / partial / empty and emits CSR lists per
+// q-block (forward) and their transpose per kv-block (backward), plus counts.
+//
+// Method: brute-force predicate evaluation with warp ballots and early exit
+// (a tile is proven partial as soon as one allowed and one denied pair are
+// seen).  This is deliberately a different algorithm from the oracle's
+// interval counter.  One CTA per "line" (a q-block row or a kv-block column):
+// the line's tile kinds are staged in shared memory, then counted (sizing pass)
+// or compacted in ascending order (fill pass).  The library owns no scratch
+// memory, so lines are re-classified in each pass (not on the per-step path;
+// built once per shape like the cached Hilbert path).
+#include "predicates.cuh"
+
+namespace hla {
+
+constexpr int kLineThreads = 256;
+
+// Kind of tile (i, j): 0 empty, 1 full, 2 partial.  Warp-collective.
+__device__ uint8_t classify_tile(const Pattern& p, int32_t i, int32_t j, int32_t bq, int32_t bk) {
+  const int lane = threadIdx.x & 31;
+  const int32_t q0 = i * bq, k0 = j * bk;
+  const int32_t nq = min(bq, p.N - q0), nk = min(bk, p.N - k0);
+  const int64_t total = (int64_t)nq * nk;
+  // lane's (qq, kk) in the flattened tile, advanced by 32 per step
+  int32_t qq = lane / nk, kk = lane - qq * nk;
+  bool seen_allowed = false, seen_denied = false;
+  for (int64_t e0 = 0; e0 < total; e0 += 32) {
+    const bool valid = e0 + lane < total;
+    const bool a = valid && allowed(p, q0 + qq, k0 + kk);
+    const unsigned valid_mask = __ballot_sync(0xffffffffu, valid);
+    const unsigned allow_mask = __ballot_sync(0xffffffffu, a);
+    seen_allowed |= allow_mask != 0u;
+    seen_denied |= allow_mask != valid_mask;
+    if (seen_allowed && seen_denied) return 2;
+    kk += 32;
+    while (kk >= nk) { kk -= nk; ++qq; }
+  }
+  if (!seen_allowed) return 0;
+  return (nq == bq && nk == bk) ? 1 : 2;   // tiles with padding positions are never full
+}
+
+// MODE 0: count (sizing).  MODE 1: fill (ascending compaction).
+// Lines [0, Mq) are q-block rows, lines [Mq, Mq+Mk) are kv-block columns.
+template <int MODE>
+__global__ void __launch_bounds__(kLineThreads) classify_lines_kernel(
+    Pattern p, int32_t bq, int32_t bk, int32_t Mq, int32_t Mk,
+    int32_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx, uint8_t* __restrict__ kind,
+    int32_t* __restrict__ t_row_ptr, int32_t* __restrict__ t_col_idx, uint8_t* __restrict__ t_kind,
+    unsigned long long* __restrict__ counts) {
+  extern __shared__ uint8_t s_kind[];
+  __shared__ int32_t s_warp[kLineThreads / 32];
+  __shared__ int32_t s_total[3];
+  const bool is_row = blockIdx.x < (unsigned)Mq;
+  const int32_t line = is_row ? blockIdx.x : blockIdx.x - Mq;
+  const int32_t len = is_row ? Mk : Mq;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kWarps = kLineThreads / 32;
+
+  for (int32_t t = warp; t < len; t += kWarps) {
+    const uint8_t kd = is_row ? classify_tile(p, line, t, bq, bk) : classify_tile(p, t, line, bq, bk);
+    if (lane == 0) s_kind[t] = kd;
+  }
+  if (threadIdx.x < 3) s_total[threadIdx.x] = 0;
+  __syncthreads();
+
+  if (MODE == 0) {
+    int32_t nnz = 0, nfull = 0;
+    for (int32_t t = threadIdx.x; t < len; t += kLineThreads) {
+      nnz += s_kind[t] != 0;
+      nfull += s_kind[t] == 1;
+    }
+    atomicAdd(&s_total[0], nnz);
+    atomicAdd(&s_total[1], nfull);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (is_row) {
+        row_ptr[line + 1] = s_total[0];
+        atomicAdd(&counts[0], (unsigned long long)s_total[0]);
+        atomicAdd(&counts[1], (unsigned long long)s_total[1]);
+        atomicAdd(&counts[2], (unsigned long long)(s_total[0] - s_total[1]));
+      } else {
+        t_row_ptr[line + 1] = s_total[0];
+      }
+    }
+    return;
+  }
+
+  // MODE 1: ordered compaction of the non-empty tiles of this line
+  int32_t* out_idx = is_row ? col_idx : t_col_idx;
+  uint8_t* out_kind = is_row ? kind : t_kind;
+  int32_t base = is_row ? row_ptr[line] : t_row_ptr[line];
+  for (int32_t t0 = 0; t0 < len; t0 += kLineThreads) {
+    const int32_t t = t0 + threadIdx.x;
+    const uint8_t kd = t < len ? s_kind[t] : 0;
+    const unsigned ball = __ballot_sync(0xffffffffu, kd != 0);
+    if (lane == 0) s_warp[warp] = __popc(ball);
+    __syncthreads();
+    int32_t before = 0, chunk_total = 0;
+    for (int w = 0; w < kWarps; ++w) {
+      if (w < warp) before += s_warp[w];
+      chunk_total += s_warp[w];
+    }
+    if (kd != 0) {
+      const int32_t pos = base + before + __popc(ball & ((1u << lane) - 1u));
+      out_idx[pos] = t;
+      out_kind[pos] = kd;
+    }
+    base += chunk_total;
+    __syncthreads();
+  }
+}
+
+// row_ptr[0] = 0 and inclusive prefix sum of the counts in row_ptr[1..n]
+__global__ void __launch_bounds__(1024) scan_lines_kernel(int32_t* row_ptr, int32_t Mq, int32_t* t_row_ptr,
+                                                          int32_t Mk, unsigned long long* counts) {
+  int32_t* a = blockIdx.x == 0 ? row_ptr : t_row_ptr;
+  const int32_t n = blockIdx.x == 0 ? Mq : Mk;
+  __shared__ int32_t s_warp[32];
+  __shared__ int32_t s_carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) { s_carry = 0; a[0] = 0; }
+  __syncthreads();
+  for (int32_t c0 = 1; c0 <= n; c0 += 1024) {
+    const int32_t idx = c0 + threadIdx.x;
+    int32_t v = idx <= n ? a[idx] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    if (lane == 31) s_warp[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+      int32_t w = s_warp[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t u = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += u;
+      }
+      s_warp[lane] = w;
+    }
+    __syncthreads();
+    const int32_t incl = v + (warp > 0 ? s_warp[warp - 1] : 0) + s_carry;
+    if (idx <= n) a[idx] = incl;
+    __syncthreads();
+    if (threadIdx.x == 1023) s_carry = incl;
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) counts[3] = (unsigned long long)Mq * (unsigned long long)Mk - counts[0];
+}
+
+}  // namespace hla
+
+using namespace hla;
+
+extern "C" hla_status hla_build_block_mask(const hla_pattern_desc* d, hla_block_mask* m, int64_t* nnz_out,
+                                           cudaStream_t stream) {
+  clear_error();
+  Pattern p;
+  hla_status st = make_pattern(d, &p);
+  if (st != HLA_OK) return st;
+  HLA_REQUIRE(m != nullptr && nnz_out != nullptr, HLA_ERR_INVALID, "null mask or nnz_out");
+  const int32_t bq = d->block_q, bk = d->block_k;
+  const int64_t Mq = (p.N + (int64_t)bq - 1) / bq, Mk = (p.N + (int64_t)bk - 1) / bk;
+  HLA_REQUIRE(m->n_qblocks == Mq && m->n_kblocks == Mk, HLA_ERR_INVALID,
+              "mask n_qblocks/n_kblocks (%d,%d) != (%lld,%lld) for this descriptor", m->n_qblocks,
+              m->n_kblocks, (long long)Mq, (long long)Mk);
+  HLA_REQUIRE(Mq <= 65536 && Mk <= 65536, HLA_ERR_UNSUPPORTED, "more than 65536 blocks per line");
+  HLA_REQUIRE(m->row_ptr && m->t_row_ptr && m->counts, HLA_ERR_INVALID, "row_ptr/t_row_ptr/counts required");
+  const bool fill = m->col_idx != nullptr;
+  if (fill)
+    HLA_REQUIRE(m->kind && m->t_col_idx && m->t_kind, HLA_ERR_INVALID, "fill call needs all CSR arrays");
+
+  const size_t smem = (size_t)std::max(Mq, Mk);
+  auto* counts = reinterpret_cast<unsigned long long*>(m->counts);
+  HLA_CUDA_TRY(cudaMemsetAsync(m->counts, 0, 4 * sizeof(int64_t), stream));
+  HLA_CUDA_TRY(cudaFuncSetAttribute(classify_lines_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+  HLA_CUDA_TRY(cudaFuncSetAttribute(classify_lines_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+  const unsigned lines = (unsigned)(Mq + Mk);
+  classify_lines_kernel<0><<<lines, kLineThreads, smem, stream>>>(p, bq, bk, (int32_t)Mq, (int32_t)Mk, m->row_ptr,
+                                                                  nullptr, nullptr, m->t_row_ptr, nullptr, nullptr,
+                                                                  counts);
+  HLA_CUDA_TRY(cudaGetLastError());
+  scan_lines_kernel<<<2, 1024, 0, stream>>>(m->row_ptr, (int32_t)Mq, m->t_row_ptr, (int32_t)Mk, counts);
+  HLA_CUDA_TRY(cudaGetLastError());
+  int64_t nnz = 0;
+  HLA_CUDA_TRY(cudaMemcpyAsync(&nnz, m->counts, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+  HLA_CUDA_TRY(cudaStreamSynchronize(stream));
+  *nnz_out = nnz;
+  if (!fill) return HLA_OK;
+  HLA_REQUIRE(nnz <= m->capacity, HLA_ERR_CAPACITY, "capacity %lld < nnz %lld", (long long)m->capacity,
+              (long long)nnz);
+  classify_lines_kernel<1><<<lines, kLineThreads, smem, stream>>>(p, bq, bk, (int32_t)Mq, (int32_t)Mk, m->row_ptr,
+                                                                  m->col_idx, m->kind, m->t_row_ptr, m->t_col_idx,
+                                                                  m->t_kind, counts);
+  HLA_CUDA_TRY(cudaGetLastError());
+  HLA_CUDA_TRY(cudaStreamSynchronize(stream));
+  return HLA_OK;
+}

@@ -1,0 +1,61 @@
+// Shared host/device helpers of libhla (not exported).
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include "../../include/hla.h"
+
+namespace hla {
+
+// thread-local last error message (hla_last_error)
+void set_error(const char* fmt, ...);
+void clear_error();
+
+#define HLA_REQUIRE(cond, status, ...)      \
+  do {                                      \
+    if (!(cond)) {                          \
+      ::hla::set_error(__VA_ARGS__);        \
+      return (status);                      \
+    }                                       \
+  } while (0)
+
+#define HLA_CUDA_TRY(expr)                                                         \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess) {                                                       \
+      ::hla::set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e),     \
+                       __FILE__, __LINE__);                                        \
+      return HLA_ERR_CUDA;                                                         \
+    }                                                                              \
+  } while (0)
+
+// Internal pattern kinds (order x family), see include/hla.h.
+enum Kind : int32_t {
+  K_HWA = 0, K_HSA = 1, K_HNA = 2, K_HSWA = 3,
+  K_WSA = 4, K_SA = 5, K_NA2D = 6, K_DENSE = 7
+};
+
+// Device-side description of the allowed(q, k) predicate.
+struct Pattern {
+  int32_t kind;
+  int32_t N, H, W;
+  int32_t n, r, L, shift;   // 1D (Hilbert) parameters: window n, radius r, HNA length L
+  int32_t kh, kw;           // 2D (row-major) window / kernel
+  int32_t log2W;            // log2(W) if W is a power of two, else -1
+};
+
+hla_status make_pattern(const hla_pattern_desc* d, Pattern* p);
+
+// Argument checks shared by hla_attn_fwd / hla_attn_bwd (attn_fwd.cu).
+hla_status check_attn_args(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
+                           int32_t head_dim, Pattern* pat);
+
+inline bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+inline int ilog2(int64_t x) { int l = 0; while ((1ll << l) < x) ++l; return l; }
+
+}  // namespace hla

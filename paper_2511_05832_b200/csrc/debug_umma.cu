@@ -1,0 +1,124 @@
+// Bring-up microtest of the tcgen05 operand encodings (include/hla_debug.h).
+// Operands are written to shared memory by plain threads in the canonical
+// SWIZZLE_128B layouts (K-major: [K/64][rows][128 B]; MN-major: [MN/64][K][128 B]),
+// exactly the layouts TMA produces for the attention tiles, then one thread
+// issues the MMAs.
+#include "../../include/hla_debug.h"
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace hla {
+namespace {
+
+__global__ void __launch_bounds__(128) debug_umma_kernel(const __nv_bfloat16* __restrict__ A,
+                                                         const __nv_bfloat16* __restrict__ B, float* __restrict__ C,
+                                                         int N, int K, int a_mn, int b_mn, int a_tmem) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  constexpr int M = 128;
+  uint8_t* sA = base;                       // M*K*2 bytes
+  uint8_t* sB = base + M * K * 2;           // N*K*2 bytes
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5;
+
+  auto kmajor_off = [](int r, int k, int R) -> uint32_t {
+    return (uint32_t)((k / 64) * R * 128) + sm100::swz128((uint32_t)(r * 128 + (k % 64) * 2));
+  };
+  auto mnmajor_off = [](int r, int k, int Kt) -> uint32_t {
+    return (uint32_t)((r / 64) * Kt * 128) + sm100::swz128((uint32_t)(k * 128 + (r % 64) * 2));
+  };
+  for (int idx = tid; idx < M * K; idx += 128) {
+    const int m = idx / K, k = idx % K;
+    const __nv_bfloat16 v = a_mn ? A[k * M + m] : A[m * K + k];
+    *reinterpret_cast<__nv_bfloat16*>(sA + (a_mn ? mnmajor_off(m, k, K) : kmajor_off(m, k, M))) = v;
+  }
+  for (int idx = tid; idx < N * K; idx += 128) {
+    const int n = idx / K, k = idx % K;
+    const __nv_bfloat16 v = b_mn ? B[k * N + n] : B[n * K + k];
+    *reinterpret_cast<__nv_bfloat16*>(sB + (b_mn ? mnmajor_off(n, k, K) : kmajor_off(n, k, N))) = v;
+  }
+  if (warp == 0) {
+    sm100::tmem_alloc(&tmem_base, 512);
+    sm100::tmem_relinquish();
+  }
+  if (tid == 0) {
+    sm100::mbar_init(&bar, 1);
+    sm100::fence_mbar_init();
+  }
+  sm100::fence_proxy_async_smem();
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  const uint32_t tD = tmem, tA = tmem + 256;
+  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+  if (a_tmem) {
+    // thread m writes row m of A (bf16 pairs) into TMEM columns [256, 256 + K/2)
+    for (int c0 = 0; c0 < K / 2; c0 += 16) {
+      uint32_t r[16];
+      for (int e = 0; e < 16; ++e) {
+        const int k = 2 * (c0 + e);
+        const float lo = __bfloat162float(A[tid * K + k]), hi = __bfloat162float(A[tid * K + k + 1]);
+        r[e] = sm100::pack_bf16(lo, hi);
+      }
+      sm100::tmem_st16(tA + lane_off + c0, r);
+    }
+    sm100::tmem_wait_st();
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  if (tid == 0) {
+    const uint32_t idesc = sm100::make_idesc_bf16(M, N, a_mn != 0, b_mn != 0);
+    const uint32_t a_base = sm100::smem_u32(sA), b_base = sm100::smem_u32(sB);
+    for (int s = 0; s < K / 16; ++s) {
+      const uint32_t a_addr = a_mn ? a_base + s * 16 * 128 : a_base + (s / 4) * M * 128 + (s % 4) * 32;
+      const uint32_t b_addr = b_mn ? b_base + s * 16 * 128 : b_base + (s / 4) * N * 128 + (s % 4) * 32;
+      const uint64_t bdesc = sm100::make_smem_desc(b_addr, b_mn ? K * 128 : 16, 1024, sm100::kSwizzle128B);
+      if (a_tmem) {
+        sm100::mma_ts(tD, tA + s * 8, bdesc, idesc, s > 0);
+      } else {
+        const uint64_t adesc = sm100::make_smem_desc(a_addr, a_mn ? K * 128 : 16, 1024, sm100::kSwizzle128B);
+        sm100::mma_ss(tD, adesc, bdesc, idesc, s > 0);
+      }
+    }
+    sm100::mma_commit(&bar);
+  }
+  __syncwarp();
+  sm100::mbar_wait(&bar, 0);
+  sm100::tc_fence_after();
+  for (int c0 = 0; c0 < N; c0 += 32) {
+    uint32_t r[32];
+    sm100::tmem_ld32(tD + lane_off + c0, r);
+    sm100::tmem_wait_ld();
+    for (int e = 0; e < 32; ++e) C[tid * N + c0 + e] = __uint_as_float(r[e]);
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  if (warp == 0) sm100::tmem_dealloc(tmem, 512);
+}
+
+}  // namespace
+}  // namespace hla
+
+using namespace hla;
+
+extern "C" hla_status hla_debug_umma(const void* A, const void* B, float* C, int32_t M, int32_t N, int32_t K,
+                                     int32_t a_major_mn, int32_t b_major_mn, int32_t a_from_tmem,
+                                     cudaStream_t stream) {
+  clear_error();
+  HLA_REQUIRE(A && B && C, HLA_ERR_INVALID, "null pointer");
+  HLA_REQUIRE(M == 128, HLA_ERR_UNSUPPORTED, "M must be 128");
+  HLA_REQUIRE(N % 64 == 0 && N >= 64 && N <= 256, HLA_ERR_UNSUPPORTED, "N must be 64..256 step 64");
+  HLA_REQUIRE(K == 64 || K == 128, HLA_ERR_UNSUPPORTED, "K must be 64 or 128");
+  HLA_REQUIRE(!(a_from_tmem && a_major_mn), HLA_ERR_INVALID, "A in TMEM is K-major");
+  const size_t smem = 1024 + (size_t)(M + N) * K * 2;
+  HLA_CUDA_TRY(cudaFuncSetAttribute(debug_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  debug_umma_kernel<<<1, 128, smem, stream>>>(reinterpret_cast<const __nv_bfloat16*>(A),
+                                              reinterpret_cast<const __nv_bfloat16*>(B), C, N, K, a_major_mn,
+                                              b_major_mn, a_from_tmem);
+  HLA_CUDA_TRY(cudaGetLastError());
+  return HLA_OK;
+}

@@ -16,3 +16,12 @@ def pytest_configure(config):
 @pytest.fixture(scope="session")
 def golden_dir():
     return os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_sessionstart(session):
+    # libhla.so is a build artefact (git-ignored); build it if this checkout has none.
+    lib = os.path.join(ROOT, "paper_2511_05832_b200", "libhla.so")
+    if not os.path.exists(lib):
+        import subprocess
+        subprocess.run(["make", "-C", os.path.join(ROOT, "paper_2511_05832_b200", "csrc"), "-j8"], check=True,
+                       stdout=subprocess.DEVNULL)

@@ -1,0 +1,95 @@
+"""GPU tests of the non-attention kernels and of the tcgen05 operand encodings.
+
+Bar: bit-exact for the Hilbert index, the permutation, tile kinds, CSR lists,
+counts and ratios (north_star); tcgen05 microtest vs an fp32 matmul of the same
+bf16 operands (exact products, fp32 sums: tight tolerance)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2511_05832_b200 as hla
+from oracle import blocks, hilbert
+from oracle.patterns import Spec
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+@pytest.mark.parametrize("a_mn,b_mn,a_tmem", [(0, 0, 0), (0, 1, 0), (1, 0, 0), (1, 1, 0), (0, 0, 1), (0, 1, 1)])
+@pytest.mark.parametrize("N,K", [(128, 64), (64, 128), (256, 128)])
+def test_umma_encodings(a_mn, b_mn, a_tmem, N, K):
+    g = torch.Generator().manual_seed(N + K)
+    A = torch.randn(128, K, generator=g).bfloat16()
+    B = torch.randn(N, K, generator=g).bfloat16()
+    ref = A.float() @ B.float().T
+    A_dev = (A.T.contiguous() if a_mn else A).to(DEV)
+    B_dev = (B.T.contiguous() if b_mn else B).to(DEV)
+    C = hla.hla_debug_umma(A_dev, B_dev, 128, N, K, a_mn=bool(a_mn), b_mn=bool(b_mn), a_tmem=bool(a_tmem))
+    torch.cuda.synchronize()
+    assert torch.allclose(C.cpu(), ref, atol=1e-3, rtol=1e-4), (C.cpu() - ref).abs().max()
+
+
+@pytest.mark.parametrize("k", range(0, 9))
+def test_hilbert_index_bit_exact(k):
+    n = 1 << k
+    s2c, c2s = hla.hla_hilbert_index(n, n, DEV)
+    ref_s2c, ref_c2s = hilbert.hilbert_order(n, n)      # gilbert2d recursion (different algorithm)
+    assert np.array_equal(s2c.cpu().numpy(), ref_s2c)
+    assert np.array_equal(c2s.cpu().numpy(), ref_c2s)
+
+
+@pytest.mark.parametrize("n,B,heads,d", [(16, 1, 1, 32), (64, 3, 8, 64), (128, 2, 12, 64), (8, 2, 3, 8)])
+def test_hilbert_perm_bit_exact(n, B, heads, d):
+    N = n * n
+    g = torch.Generator().manual_seed(n)
+    xs = [torch.randn(B, N, heads, d, generator=g).bfloat16() for _ in range(3)]
+    dev = [x.to(DEV) for x in xs]
+    out = hla.hla_hilbert_perm(n, n, 0, dev)
+    s2c, _ = hilbert.hilbert_order(n, n)
+    for x, y in zip(xs, out):
+        assert torch.equal(y.cpu(), x[:, torch.from_numpy(s2c)])
+    back = hla.hla_hilbert_perm(n, n, 1, out)
+    for x, y in zip(xs, back):
+        assert torch.equal(y.cpu(), x)
+    # fp32 rows (dQ accumulator-like) and 4 tensors per launch
+    f = [torch.randn(B, N, heads * 4, generator=g).to(DEV) for _ in range(4)]
+    o = hla.hla_hilbert_perm(n, n, 0, f)
+    for x, y in zip(f, o):
+        assert torch.equal(y.cpu(), x.cpu()[:, torch.from_numpy(s2c)])
+
+
+MASK_CASES = [
+    # BASELINE configs (attention block 128; cfg1 classification at block 16)
+    ("HWA", 16, 16, 8, 8, 16), ("WSA", 16, 16, 8, 8, 16), ("HWA", 16, 16, 8, 8, 128),
+    ("HWA", 64, 64, 16, 16, 128), ("WSA", 64, 64, 16, 16, 128),
+    ("HSA", 64, 64, 16, 16, 128), ("SA", 64, 64, 16, 16, 128),
+    ("HNA", 128, 128, 7, 7, 128), ("NA2D", 128, 128, 7, 7, 128), ("DENSE", 64, 64, 1, 1, 128),
+    ("HWA", 64, 64, 8, 8, 64), ("WSA", 64, 64, 8, 8, 64),
+    # paper shapes incl. N % b != 0 and rectangular grids (masks are curve-independent)
+    ("HWA", 56, 56, 7, 7, 128), ("SA", 56, 56, 7, 7, 128), ("NA2D", 56, 56, 7, 7, 128), ("HNA", 56, 56, 7, 7, 128),
+    ("HSA", 96, 96, 17, 17, 128), ("HNA", 96, 96, 17, 17, 128), ("WSA", 128, 256, 16, 16, 128),
+    ("HWA", 160, 160, 20, 20, 128), ("HWA", 128, 128, 16, 16, 512), ("HSWA", 64, 64, 16, 16, 128),
+    ("HNA", 16, 16, 3, 3, 5), ("NA2D", 12, 20, 3, 5, 7),
+]
+
+
+@pytest.mark.parametrize("kind,H,W,wh,ww,b", MASK_CASES)
+def test_block_mask_bit_exact(kind, H, W, wh, ww, b):
+    shift = (wh * ww) // 2 if kind == "HSWA" else 0
+    spec = Spec(kind, H, W, wh, ww, shift=shift)
+    km = blocks.classify_spec(spec, b, b)
+    rp, ci, kd = blocks.csr(km)
+    trp, tci, tkd = blocks.csr_transpose(km)
+    st = blocks.stats(km, spec.n_tokens, b, b)
+    m = hla.hla_build_block_mask(hla.pattern_desc(kind, H, W, wh, ww, block=b, shift=shift), DEV)
+    nnz = st["nnz"]
+    assert m.host_counts == (nnz, st["n_full"], st["n_partial"], st["n_empty"])
+    assert np.array_equal(m.row_ptr.cpu().numpy(), rp)
+    assert np.array_equal(m.col_idx.cpu().numpy()[:nnz], ci)
+    assert np.array_equal(m.kind.cpu().numpy()[:nnz], kd)
+    assert np.array_equal(m.t_row_ptr.cpu().numpy(), trp)
+    assert np.array_equal(m.t_col_idx.cpu().numpy()[:nnz], tci)
+    assert np.array_equal(m.t_kind.cpu().numpy()[:nnz], tkd)
+    e, s = m.ratios()
+    assert e == st["empty_tile_ratio"] and s == st["sparsity"]

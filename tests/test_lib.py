@@ -1,0 +1,96 @@
+"""CPU-side checks of the C ABI library: it loads, exports every symbol the
+headers declare, validates arguments host-side (no GPU needed), and computes the
+sparsity ratios bit-exactly like the oracle.  Also: no product module imports
+the oracle, and the product path has no fallback when libhla.so is missing."""
+
+import ast
+import ctypes
+import glob
+import os
+import re
+
+import pytest
+
+from oracle import blocks
+from oracle.patterns import Spec
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        src = open(h).read()
+        names.update(re.findall(r"HLA_API\s+[\w\s\*]+?\b(hla_\w+)\s*\(", src))
+    return names
+
+
+def test_library_exports_header_symbols():
+    from paper_2511_05832_b200 import _lib
+    L = _lib.lib()
+    declared = _declared_symbols()
+    assert len(declared) >= 10
+    for name in declared:
+        assert hasattr(L, name), name
+    assert set(_lib.EXPORTED) == declared
+    assert "sm_100a" in L.hla_version().decode()
+
+
+def test_argument_validation_without_gpu():
+    from paper_2511_05832_b200 import _lib, api
+    L = _lib.lib()
+    n = 1
+    arr = (ctypes.c_void_p * n)(16)
+    # non-square grid -> UNSUPPORTED, checked before any CUDA call
+    assert L.hla_hilbert_perm(56, 64, 0, 1, 128, 1, arr, arr, None, None) == _lib.HLA_ERR_UNSUPPORTED
+    assert L.hla_hilbert_index(48, 48, None, None, None) == _lib.HLA_ERR_UNSUPPORTED
+    assert b"square" in L.hla_last_error()
+    # window not dividing the grid -> INVALID
+    d = api.pattern_desc("WSA", 64, 64, 7, 7)
+    m = _lib.BlockMaskC()
+    nnz = ctypes.c_int64()
+    assert L.hla_build_block_mask(ctypes.byref(d), ctypes.byref(m), ctypes.byref(nnz), None) == _lib.HLA_ERR_INVALID
+    # attention limits
+    d = api.pattern_desc("HWA", 64, 64, 16, 16, block=64)
+    m = _lib.BlockMaskC(64, 64, 1, 8, 8, 8, 8, 8, 8, 8)
+    st = L.hla_attn_fwd(ctypes.byref(d), ctypes.byref(m), 1, 1, 64, 0.0, 16, 16, 16, 16, 16, None, None)
+    assert st == _lib.HLA_ERR_UNSUPPORTED
+    d = api.pattern_desc("HWA", 64, 64, 16, 16)
+    m = _lib.BlockMaskC(32, 32, 1, 8, 8, 8, 8, 8, 8, 8)
+    st = L.hla_attn_fwd(ctypes.byref(d), ctypes.byref(m), 1, 1, 128, 0.0, 16, 16, 16, 16, 16, None, None)
+    assert st == _lib.HLA_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("kind,H,W,wh,ww,b", [("HWA", 56, 56, 7, 7, 128), ("SA", 56, 56, 7, 7, 128),
+                                             ("HNA", 128, 128, 17, 17, 128), ("WSA", 128, 128, 16, 16, 512),
+                                             ("HWA", 16, 16, 8, 8, 16)])
+def test_mask_ratios_match_oracle_bitwise(kind, H, W, wh, ww, b):
+    from paper_2511_05832_b200 import _lib, api
+    spec = Spec(kind, H, W, wh, ww)
+    st = blocks.stats(blocks.classify_spec(spec, b, b), spec.n_tokens, b, b)
+    d = api.pattern_desc(kind, H, W, wh, ww, block=b)
+    cnt = (ctypes.c_int64 * 4)(st["nnz"], st["n_full"], st["n_partial"], st["n_empty"])
+    e, s = ctypes.c_double(), ctypes.c_double()
+    assert _lib.lib().hla_mask_ratios(ctypes.byref(d), cnt, ctypes.byref(e), ctypes.byref(s)) == 0
+    assert e.value == st["empty_tile_ratio"] and s.value == st["sparsity"]
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2511_05832_b200")
+    for path in glob.glob(os.path.join(pkg, "**", "*.py"), recursive=True):
+        tree = ast.parse(open(path).read())
+        for node in ast.walk(tree):
+            if isinstance(node, ast.Import):
+                assert not any(a.name.split(".")[0] == "oracle" for a in node.names), path
+            if isinstance(node, ast.ImportFrom):
+                assert (node.module or "").split(".")[0] != "oracle", path
+    for path in glob.glob(os.path.join(pkg, "csrc", "*")):
+        assert not re.search(r'#include\s*["<][^">]*oracle', open(path, errors="ignore").read()), path
+
+
+def test_missing_library_fails_loudly(monkeypatch):
+    from paper_2511_05832_b200 import _lib
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", "/nonexistent/libhla.so")
+    with pytest.raises(ImportError):
+        _lib.lib()
