@@ -1,13 +1,476 @@
-// K7-K9: block-sparse attention backward (placeholder until the tcgen05 kernel lands).
-#include "common.cuh"
+// K7-K9: block-sparse attention backward on sm_100a (tcgen05 + TMEM + TMA).
+//
+// Gradients of masked softmax attention (the paper times this pass in the
+// "Backward" columns; skipping empty tiles is what makes it
+// cheaper):
+//   P = exp(scale S - LSE) (0 where masked),  D = rowsum(dO o O)
+//   dV = P^T dO,  dS = scale P o (dO V^T - D),  dK = dS^T Q,  dQ = dS K.
+//
+// K7 bwd_preprocess : D = rowsum(dO o O) (fp32) and zero the fp32 dQ accumulator.
+// K8 attn_bwd_kernel: one CTA per (kv-block j, head, batch), walking the
+//    transposed CSR list of q-blocks i (ascending).  320 threads, 1 CTA / SM:
+//    warp 0     TMA: K_j, V_j once; per q-block Q_i, dO_i (+ LSE_i, D_i via bulk
+//               copy) into a 2-stage ring;
+//    warp 1     TMEM allocator + single-thread tcgen05.mma issuer:
+//                 S^T  = K_j Q_i^T     (SS, TMEM cols [0,128))
+//                 dP^T = V_j dO_i^T    (SS, TMEM cols [128,256))
+//                 dV  += P^T dO_i      (TS, P^T bf16 in TMEM cols [256,320); acc [384,448))
+//                 dK  += dS^T Q_i      (SS, dS^T bf16 in smem, K-major view; acc [448,512))
+//                 dQ_i = dS K_j        (SS, same dS smem, MN-major view; TMEM [320,384))
+//    warps 2-5  thread = key row: P^T, dS^T from S^T, dP^T (mask only on partial
+//               tiles); final dK, dV -> bf16;
+//    warps 6-9  thread = query row: dQ_i partial -> red.global.add.v4.f32 into the
+//               fp32 accumulator (overlaps the next q-block's MMAs).
+// K9 dq_finalize    : fp32 accumulator -> bf16 dQ.
+#include "predicates.cuh"
+#include "sm100.cuh"
+#include "tensor_map.cuh"
 
-extern "C" size_t hla_attn_bwd_workspace(int32_t batch, int32_t heads, int32_t n, int32_t head_dim) {
-  return (size_t)batch * heads * n * head_dim * 4 + (size_t)batch * heads * n * 4 + 256;
+namespace hla {
+namespace {
+
+constexpr int kBlock = 128;
+constexpr int kThreads = 320;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kColS = 0, kColDP = 128, kColP = 256, kColDQ = 320, kColDV = 384, kColDK = 448;
+constexpr float kLog2e = 1.4426950408889634f;
+
+struct BwdParams {
+  Pattern pat;
+  int32_t N, heads, batch;
+  float scale, scale_log2;
+  const int32_t* t_row_ptr;
+  const int32_t* t_col_idx;
+  const uint8_t* t_kind;
+  const float* lse;        // [B, H, N]
+  const float* dsum;       // D, [B, H, N]
+  float* dq_acc;           // [B, N, H, Dh] fp32
+  __nv_bfloat16* dk;
+  __nv_bfloat16* dv;
+  unsigned long long* visited;
+};
+
+template <int D>
+struct BwdSmem {
+  static constexpr uint32_t kTileBytes = kBlock * D * 2;
+  alignas(1024) uint8_t k[kTileBytes];
+  alignas(1024) uint8_t v[kTileBytes];
+  alignas(1024) uint8_t q[2][kTileBytes];
+  alignas(1024) uint8_t dO[2][kTileBytes];
+  alignas(1024) uint8_t ds[2 * 128 * 128];   // dS^T bf16: [q/64][kv 128][64 q], SWIZZLE_128B
+  alignas(16) float lse[2][kBlock];
+  alignas(16) float dd[2][kBlock];
+  uint64_t kv_full, q_full[2], q_empty[2], s_full, ds_ready, dq_full, dq_free, dkv_full;
+  uint32_t tmem_base;
+};
+
+template <int D>
+__device__ __forceinline__ uint64_t kmajor_desc(const uint8_t* tile, int kstep) {
+  constexpr uint32_t layout = D == 64 ? sm100::kSwizzle128B : sm100::kSwizzle64B;
+  return sm100::make_smem_desc(sm100::smem_u32(tile) + kstep * 32, 16, 8 * D * 2, layout);
+}
+template <int D>
+__device__ __forceinline__ uint64_t mnmajor_desc(const uint8_t* tile, int kstep) {
+  constexpr uint32_t layout = D == 64 ? sm100::kSwizzle128B : sm100::kSwizzle64B;
+  return sm100::make_smem_desc(sm100::smem_u32(tile) + kstep * 16 * D * 2, kBlock * D * 2, 8 * D * 2, layout);
+}
+// dS^T smem tile viewed as K-major A (M = kv, K = q): K step = 16 q
+__device__ __forceinline__ uint64_t ds_kmajor_desc(const uint8_t* ds, int kstep) {
+  return sm100::make_smem_desc(sm100::smem_u32(ds) + (kstep >> 2) * 16384 + (kstep & 3) * 32, 16, 1024,
+                               sm100::kSwizzle128B);
+}
+// dS^T smem tile viewed as MN-major A of dQ = dS K (M = q, K = kv): K step = 16 kv rows
+__device__ __forceinline__ uint64_t ds_mnmajor_desc(const uint8_t* ds, int kstep) {
+  return sm100::make_smem_desc(sm100::smem_u32(ds) + kstep * 2048, 16384, 1024, sm100::kSwizzle128B);
 }
 
-extern "C" hla_status hla_attn_bwd(const hla_pattern_desc*, const hla_block_mask*, int32_t, int32_t, int32_t, float,
-                                   const void*, const void*, const void*, const void*, const float*, const void*,
-                                   void*, void*, void*, void*, size_t, int64_t*, cudaStream_t) {
-  hla::set_error("backward not built yet");
-  return HLA_ERR_UNSUPPORTED;
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+template <int D, bool kTwoD>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                    const BwdParams prm) {
+  extern __shared__ uint8_t smem_raw[];
+  BwdSmem<D>& sm = *reinterpret_cast<BwdSmem<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t kb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
+  const int64_t bh = (int64_t)b * prm.heads + h;
+
+  if (warp == 0 && lane == 0) {
+    sm100::mbar_init(&sm.kv_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      sm100::mbar_init(&sm.q_full[s], 1);
+      sm100::mbar_init(&sm.q_empty[s], 1);
+    }
+    sm100::mbar_init(&sm.s_full, 1);
+    sm100::mbar_init(&sm.ds_ready, 128);
+    sm100::mbar_init(&sm.dq_full, 1);
+    sm100::mbar_init(&sm.dq_free, 128);
+    sm100::mbar_init(&sm.dkv_full, 1);
+    sm100::fence_mbar_init();
+    sm100::tma_prefetch_desc(&tmQ);
+    sm100::tma_prefetch_desc(&tmK);
+    sm100::tma_prefetch_desc(&tmV);
+    sm100::tma_prefetch_desc(&tmDO);
+  }
+  if (warp == 1) {
+    sm100::tmem_alloc(&sm.tmem_base, kTmemCols);
+    sm100::tmem_relinquish();
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0 && nt > 0) {
+      const uint64_t pol_kv = sm100::policy_evict_first();
+      const uint64_t pol_q = sm100::policy_evict_last();
+      const int32_t krow = b * prm.N + kb * kBlock;
+      sm100::mbar_arrive_expect_tx(&sm.kv_full, 2 * BwdSmem<D>::kTileBytes);
+      sm100::tma_load_3d(sm.k, &tmK, &sm.kv_full, 0, h, krow, pol_kv);
+      sm100::tma_load_3d(sm.v, &tmV, &sm.kv_full, 0, h, krow, pol_kv);
+      for (int t = 0; t < nt; ++t) {
+        const int s = t & 1;
+        if (t >= 2) sm100::mbar_wait(&sm.q_empty[s], ((t >> 1) - 1) & 1);
+        const int32_t qblk = __ldg(prm.t_col_idx + rs + t);
+        const int32_t qrow = b * prm.N + qblk * kBlock;
+        sm100::mbar_arrive_expect_tx(&sm.q_full[s], 2 * BwdSmem<D>::kTileBytes + 2 * kBlock * 4);
+        sm100::tma_load_3d(sm.q[s], &tmQ, &sm.q_full[s], 0, h, qrow, pol_q);
+        sm100::tma_load_3d(sm.dO[s], &tmDO, &sm.q_full[s], 0, h, qrow, pol_q);
+        sm100::bulk_load(sm.lse[s], prm.lse + bh * prm.N + qblk * kBlock, kBlock * 4, &sm.q_full[s]);
+        sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * kBlock, kBlock * 4, &sm.q_full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------- MMA issuer
+    if (lane == 0 && nt > 0) {
+      constexpr uint32_t idesc_s = sm100::make_idesc_bf16(kBlock, kBlock, false, false);
+      constexpr uint32_t idesc_kv = sm100::make_idesc_bf16(kBlock, D, false, true);   // dV, dK
+      constexpr uint32_t idesc_q = sm100::make_idesc_bf16(kBlock, D, true, true);     // dQ
+      const uint32_t tS = tmem + kColS, tDP = tmem + kColDP, tP = tmem + kColP;
+      const uint32_t tDQ = tmem + kColDQ, tDV = tmem + kColDV, tDK = tmem + kColDK;
+      sm100::mbar_wait(&sm.kv_full, 0);
+      for (int t = 0; t < nt; ++t) {
+        const int s = t & 1;
+        sm100::mbar_wait(&sm.q_full[s], (t >> 1) & 1);
+        sm100::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          sm100::mma_ss(tS, kmajor_desc<D>(sm.k, kk), kmajor_desc<D>(sm.q[s], kk), idesc_s, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          sm100::mma_ss(tDP, kmajor_desc<D>(sm.v, kk), kmajor_desc<D>(sm.dO[s], kk), idesc_s, kk > 0);
+        sm100::mma_commit(&sm.s_full);
+        sm100::mbar_wait(&sm.ds_ready, t & 1);
+        sm100::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < kBlock / 16; ++kk)
+          sm100::mma_ts(tDV, tP + kk * 8, mnmajor_desc<D>(sm.dO[s], kk), idesc_kv, (t > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < kBlock / 16; ++kk)
+          sm100::mma_ss(tDK, ds_kmajor_desc(sm.ds, kk), mnmajor_desc<D>(sm.q[s], kk), idesc_kv,
+                        (t > 0 || kk > 0) ? 1u : 0u);
+        if (t > 0) {
+          sm100::mbar_wait(&sm.dq_free, (t - 1) & 1);
+          sm100::tc_fence_after();
+        }
+#pragma unroll
+        for (int kk = 0; kk < kBlock / 16; ++kk)
+          sm100::mma_ss(tDQ, ds_mnmajor_desc(sm.ds, kk), mnmajor_desc<D>(sm.k, kk), idesc_q, kk > 0);
+        sm100::mma_commit(&sm.q_empty[s]);
+        sm100::mma_commit(&sm.dq_full);
+      }
+      sm100::mma_commit(&sm.dkv_full);
+    }
+  } else if (warp < 6) {
+    // --------------------------------------------- P^T / dS^T (thread = key row)
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const int32_t kidx = kb * kBlock + row;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const float sl2 = prm.scale_log2, scale = prm.scale;
+    RowBox box;
+    if (nt > 0) box = col_box(prm.pat, kidx);
+    for (int t = 0; t < nt; ++t) {
+      const int s = t & 1;
+      sm100::mbar_wait(&sm.q_full[s], (t >> 1) & 1);
+      sm.lse[s][row] *= kLog2e;                     // LSE in the log2 domain
+      sm100::named_bar_sync(1, 128);
+      sm100::mbar_wait(&sm.s_full, t & 1);
+      sm100::tc_fence_after();
+      const uint8_t kd = __ldg(prm.t_kind + rs + t);
+      const int32_t q0 = __ldg(prm.t_col_idx + rs + t) * kBlock;
+      const float* lse2 = sm.lse[s];
+      const float* dd = sm.dd[s];
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t sr[32], dpr[32];
+        sm100::tmem_ld32(tmem + lane_off + kColS + c * 32, sr);
+        sm100::tmem_ld32(tmem + lane_off + kColDP + c * 32, dpr);
+        sm100::tmem_wait_ld();
+        float p[32], ds[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int qc = c * 32 + e;
+          p[e] = sm100::ex2(fmaf(__uint_as_float(sr[e]), sl2, -lse2[qc]));
+        }
+        if (kd == 2) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const int32_t qq = q0 + c * 32 + e;
+            bool ok;
+            if (!kTwoD) {
+              ok = (uint32_t)(qq - box.lo) < (uint32_t)box.len;
+            } else {
+              const int32_t rq = prm.pat.log2W >= 0 ? (qq >> prm.pat.log2W) : qq / prm.pat.W;
+              const int32_t cq = qq - rq * prm.pat.W;
+              ok = ((uint32_t)(rq - box.lo) < (uint32_t)box.len) && ((uint32_t)(cq - box.c0) < (uint32_t)box.cn);
+            }
+            if (!ok) p[e] = 0.f;
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 32; ++e) ds[e] = p[e] * scale * (__uint_as_float(dpr[e]) - dd[c * 32 + e]);
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) pk[e] = sm100::pack_bf16(p[2 * e], p[2 * e + 1]);
+        sm100::tmem_st16(tmem + lane_off + kColP + c * 16, pk);
+        // dS^T row -> smem [q/64][kv][64] with the 128B swizzle (16B chunks)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int qc = c * 32 + u * 8;               // first q column of this 16B chunk
+          uint4 w;
+          w.x = sm100::pack_bf16(ds[u * 8 + 0], ds[u * 8 + 1]);
+          w.y = sm100::pack_bf16(ds[u * 8 + 2], ds[u * 8 + 3]);
+          w.z = sm100::pack_bf16(ds[u * 8 + 4], ds[u * 8 + 5]);
+          w.w = sm100::pack_bf16(ds[u * 8 + 6], ds[u * 8 + 7]);
+          const uint32_t off = (uint32_t)(qc >> 6) * 16384u + sm100::swz128((uint32_t)row * 128u + (uint32_t)(qc & 63) * 2u);
+          *reinterpret_cast<uint4*>(sm.ds + off) = w;
+        }
+      }
+      sm100::tmem_wait_st();
+      sm100::fence_proxy_async_smem();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&sm.ds_ready);
+    }
+    // final dK, dV rows -> bf16 (dS already carries the softmax scale)
+    const int64_t grow = ((int64_t)b * prm.N + kidx) * prm.heads + h;
+    uint4* dkp = reinterpret_cast<uint4*>(prm.dk + grow * D);
+    uint4* dvp = reinterpret_cast<uint4*>(prm.dv + grow * D);
+    if (nt > 0) {
+      sm100::mbar_wait(&sm.dkv_full, 0);
+      sm100::tc_fence_after();
+#pragma unroll
+      for (int which = 0; which < 2; ++which) {
+        uint4* dst = which == 0 ? dvp : dkp;
+        const uint32_t col = which == 0 ? kColDV : kColDK;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t r[32];
+          sm100::tmem_ld32(tmem + lane_off + col + c * 32, r);
+          sm100::tmem_wait_ld();
+#pragma unroll
+          for (int v4 = 0; v4 < 4; ++v4) {
+            uint4 w;
+            w.x = sm100::pack_bf16(__uint_as_float(r[v4 * 8 + 0]), __uint_as_float(r[v4 * 8 + 1]));
+            w.y = sm100::pack_bf16(__uint_as_float(r[v4 * 8 + 2]), __uint_as_float(r[v4 * 8 + 3]));
+            w.z = sm100::pack_bf16(__uint_as_float(r[v4 * 8 + 4]), __uint_as_float(r[v4 * 8 + 5]));
+            w.w = sm100::pack_bf16(__uint_as_float(r[v4 * 8 + 6]), __uint_as_float(r[v4 * 8 + 7]));
+            dst[c * 4 + v4] = w;
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < D / 8; ++c) {
+        dkp[c] = make_uint4(0, 0, 0, 0);
+        dvp[c] = make_uint4(0, 0, 0, 0);
+      }
+    }
+  } else {
+    // ------------------------------------------ dQ partial -> fp32 accumulator
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    for (int t = 0; t < nt; ++t) {
+      sm100::mbar_wait(&sm.dq_full, t & 1);
+      sm100::tc_fence_after();
+      const int32_t qidx = __ldg(prm.t_col_idx + rs + t) * kBlock + row;
+      float* dst = prm.dq_acc + (((int64_t)b * prm.N + qidx) * prm.heads + h) * D;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t r[32];
+        sm100::tmem_ld32(tmem + lane_off + kColDQ + c * 32, r);
+        sm100::tmem_wait_ld();
+        if (c == D / 32 - 1) {
+          sm100::tc_fence_before();
+          sm100::mbar_arrive(&sm.dq_free);   // TMEM dQ tile may be overwritten
+        }
+#pragma unroll
+        for (int v4 = 0; v4 < 8; ++v4)
+          red_add_v4(dst + c * 32 + v4 * 4, __uint_as_float(r[v4 * 4 + 0]), __uint_as_float(r[v4 * 4 + 1]),
+                     __uint_as_float(r[v4 * 4 + 2]), __uint_as_float(r[v4 * 4 + 3]));
+      }
+    }
+  }
+
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  if (warp == 1) sm100::tmem_dealloc(tmem, kTmemCols);
+  if (threadIdx.x == 0 && prm.visited != nullptr && nt > 0) atomicAdd(prm.visited, (unsigned long long)nt);
+}
+
+// K7: D = rowsum(dO o O) per (b, q, h) row of head_dim bf16, fp32; dQ accumulator := 0
+template <int D>
+__global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
+                                                             const __nv_bfloat16* __restrict__ dout,
+                                                             float* __restrict__ dsum, float* __restrict__ dq_acc,
+                                                             int32_t N, int32_t heads, int64_t rows) {
+  constexpr int kLanes = D / 8;   // lanes per row, 16 B (8 bf16) each
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r = gid / kLanes;
+  const int part = (int)(gid % kLanes);
+  if (r >= rows) return;
+  const uint4 a = *reinterpret_cast<const uint4*>(o + r * D + part * 8);
+  const uint4 g = *reinterpret_cast<const uint4*>(dout + r * D + part * 8);
+  const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+  const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&g);
+  float acc = 0.f;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 x = __bfloat1622float2(a2[e]), y = __bfloat1622float2(g2[e]);
+    acc = fmaf(x.x, y.x, acc);
+    acc = fmaf(x.y, y.y, acc);
+  }
+#pragma unroll
+  for (int o2 = kLanes / 2; o2 > 0; o2 >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o2);
+  float4* z = reinterpret_cast<float4*>(dq_acc + r * D + part * 8);
+  z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+  z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (part == 0) {
+    // row r = (b * N + q) * heads + h  ->  D[b, h, q]
+    const int64_t hq = r % heads, bq = r / heads;
+    const int64_t q = bq % N, bb = bq / N;
+    dsum[(bb * heads + hq) * N + q] = acc;
+  }
+}
+
+// K9: dQ = bf16(accumulator)
+__global__ void __launch_bounds__(256) dq_finalize_kernel(const float4* __restrict__ acc, uint2* __restrict__ dq,
+                                                          int64_t n4) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = acc[i];
+    dq[i] = make_uint2(sm100::pack_bf16(v.x, v.y), sm100::pack_bf16(v.z, v.w));
+  }
+}
+
+template <int D, bool kTwoD>
+hla_status launch_bwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mdo,
+                      const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream) {
+  const size_t smem = sizeof(BwdSmem<D>) + 1024;
+  auto* fn = attn_bwd_kernel<D, kTwoD>;
+  HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid(n_kblocks, prm.heads, prm.batch);
+  fn<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mdo, prm);
+  HLA_CUDA_TRY(cudaGetLastError());
+  return HLA_OK;
+}
+
+}  // namespace
+}  // namespace hla
+
+using namespace hla;
+
+extern "C" size_t hla_attn_bwd_workspace(int32_t batch, int32_t heads, int32_t n, int32_t head_dim) {
+  const size_t acc = (size_t)batch * n * heads * head_dim * 4;
+  const size_t dsum = (size_t)batch * heads * n * 4;
+  return ((acc + 255) / 256) * 256 + ((dsum + 255) / 256) * 256;
+}
+
+extern "C" hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
+                                   int32_t head_dim, float scale, const void* q, const void* k, const void* v,
+                                   const void* o, const float* lse, const void* dout, void* dq, void* dk, void* dv,
+                                   void* workspace, size_t workspace_bytes, int64_t* tiles_visited,
+                                   cudaStream_t stream) {
+  clear_error();
+  Pattern pat;
+  hla_status st = check_attn_args(d, m, batch, heads, head_dim, &pat);
+  if (st != HLA_OK) return st;
+  HLA_REQUIRE(m->t_row_ptr && m->t_col_idx && m->t_kind, HLA_ERR_INVALID, "transposed mask arrays missing");
+  HLA_REQUIRE(q && k && v && o && lse && dout && dq && dk && dv && workspace, HLA_ERR_INVALID, "null pointer");
+  HLA_REQUIRE(((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)o | (uintptr_t)dout | (uintptr_t)dq |
+               (uintptr_t)dk | (uintptr_t)dv) % 16 == 0 && (uintptr_t)lse % 16 == 0,
+              HLA_ERR_INVALID, "tensors must be 16-byte aligned");
+  HLA_REQUIRE((uintptr_t)workspace % 256 == 0, HLA_ERR_INVALID, "workspace must be 256-byte aligned");
+  const size_t need = hla_attn_bwd_workspace(batch, heads, pat.N, head_dim);
+  HLA_REQUIRE(workspace_bytes >= need, HLA_ERR_INVALID, "workspace %zu < %zu bytes", workspace_bytes, need);
+  const int64_t rows = (int64_t)batch * pat.N * heads;
+  float* dq_acc = reinterpret_cast<float*>(workspace);
+  float* dsum = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) +
+                                         (((size_t)rows * head_dim * 4 + 255) / 256) * 256);
+  const float sc = scale > 0.f ? scale : 1.0f / sqrtf((float)head_dim);
+
+  // K7
+  {
+    const int64_t threads = rows * (head_dim / 8);
+    const unsigned blocks = (unsigned)((threads + 255) / 256);
+    if (head_dim == 64)
+      bwd_preprocess_kernel<64><<<blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
+                                                            reinterpret_cast<const __nv_bfloat16*>(dout), dsum,
+                                                            dq_acc, pat.N, heads, rows);
+    else
+      bwd_preprocess_kernel<32><<<blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
+                                                            reinterpret_cast<const __nv_bfloat16*>(dout), dsum,
+                                                            dq_acc, pat.N, heads, rows);
+    HLA_CUDA_TRY(cudaGetLastError());
+  }
+  // K8
+  BwdParams prm;
+  prm.pat = pat;
+  prm.N = pat.N;
+  prm.heads = heads;
+  prm.batch = batch;
+  prm.scale = sc;
+  prm.scale_log2 = sc * kLog2e;
+  prm.t_row_ptr = m->t_row_ptr;
+  prm.t_col_idx = m->t_col_idx;
+  prm.t_kind = m->t_kind;
+  prm.lse = lse;
+  prm.dsum = dsum;
+  prm.dq_acc = dq_acc;
+  prm.dk = reinterpret_cast<__nv_bfloat16*>(dk);
+  prm.dv = reinterpret_cast<__nv_bfloat16*>(dv);
+  prm.visited = reinterpret_cast<unsigned long long*>(tiles_visited);
+  const int64_t tok = (int64_t)batch * pat.N;
+  CUtensorMap mq, mk, mv, mdo;
+  if ((st = make_rows_map(&mq, q, tok, heads, head_dim, kBlock)) != HLA_OK) return st;
+  if ((st = make_rows_map(&mk, k, tok, heads, head_dim, kBlock)) != HLA_OK) return st;
+  if ((st = make_rows_map(&mv, v, tok, heads, head_dim, kBlock)) != HLA_OK) return st;
+  if ((st = make_rows_map(&mdo, dout, tok, heads, head_dim, kBlock)) != HLA_OK) return st;
+  const bool two_d = pat.kind == K_WSA || pat.kind == K_SA || pat.kind == K_NA2D;
+  const int32_t mkb = pat.N / kBlock;
+  if (head_dim == 64)
+    st = two_d ? launch_bwd<64, true>(mq, mk, mv, mdo, prm, mkb, stream)
+               : launch_bwd<64, false>(mq, mk, mv, mdo, prm, mkb, stream);
+  else
+    st = two_d ? launch_bwd<32, true>(mq, mk, mv, mdo, prm, mkb, stream)
+               : launch_bwd<32, false>(mq, mk, mv, mdo, prm, mkb, stream);
+  if (st != HLA_OK) return st;
+  // K9
+  {
+    const int64_t n4 = rows * head_dim / 4;
+    const unsigned blocks = (unsigned)std::min<int64_t>((n4 + 255) / 256, 148 * 16);
+    dq_finalize_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const float4*>(dq_acc),
+                                                   reinterpret_cast<uint2*>(dq), n4);
+    HLA_CUDA_TRY(cudaGetLastError());
+  }
+  return HLA_OK;
 }

@@ -71,4 +71,36 @@ __device__ __forceinline__ RowBox row_box(const Pattern& p, int32_t q) {
   }
 }
 
+// Transposed form for the backward pass (thread = key k, columns = queries q):
+// the set {q : allowed(q, k)} as a box of the same shape.  For the symmetric
+// patterns it equals row_box(k); HNA / NA2D clamp their windows, so the query
+// range of a key is derived from the monotone window start s(q) = clamp(q - a, 0, n - L):
+//   s(q) <= k        <=>  q <= k + a            (or every q if k >= n - L)
+//   s(q) >= k - L + 1 <=> q >= k - L + 1 + a    (or every q if k - L + 1 <= 0)
+__device__ __forceinline__ void clamped_col_range(int32_t k, int32_t a, int32_t L, int32_t n, int32_t* lo,
+                                                  int32_t* len) {
+  const int32_t q0 = (k - L + 1 <= 0) ? 0 : k - L + 1 + a;
+  const int32_t q1 = (k >= n - L) ? n - 1 : k + a;
+  *lo = q0;
+  *len = q1 - q0 + 1;
+}
+
+__device__ __forceinline__ RowBox col_box(const Pattern& p, int32_t k) {
+  if (p.kind == K_HNA) {
+    RowBox b;
+    clamped_col_range(k, p.r, p.L, p.N, &b.lo, &b.len);
+    b.c0 = 0;
+    b.cn = 0;
+    return b;
+  }
+  if (p.kind == K_NA2D) {
+    RowBox b;
+    const int32_t rk = k / p.W, ck = k - rk * p.W;
+    clamped_col_range(rk, p.kh / 2, p.kh, p.H, &b.lo, &b.len);
+    clamped_col_range(ck, p.kw / 2, p.kw, p.W, &b.c0, &b.cn);
+    return b;
+  }
+  return row_box(p, k);  // symmetric patterns
+}
+
 }  // namespace hla

@@ -111,3 +111,56 @@ def test_fwd_full_size_sampled(case):
         assert_close("%s O[b=%d,h=%d]" % (name, b, h), got, O_ref)
         got_lse = to_np(layer.lse[b, h])[rows]        # LSE stays in sequence order
         assert_close("%s LSE" % name, got_lse, L_ref, max_abs=LSE_MAX_ABS, mean_abs=LSE_MAX_ABS)
+
+
+@pytest.mark.parametrize("case", SMALL, ids=lambda c: "%s_%dx%d_w%dx%d_d%d" % (c[0], c[1], c[2], c[3], c[4], c[7]))
+@pytest.mark.parametrize("sharp", [False, True])
+def test_bwd_small(case, sharp):
+    kind, gh, gw, wh, ww, B, H, d = case
+    shift = (wh * ww) // 2 if kind == "HSWA" else 0
+    N = gh * gw
+    q, k, v, do = _inputs(B, N, H, d, seed=7, sharp=sharp)
+    desc = hla.pattern_desc(kind, gh, gw, wh, ww, shift=shift)
+    m = hla.hla_build_block_mask(desc, DEV)
+    o, lse = hla.hla_attn_fwd(desc, m, q, k, v)
+    visited = torch.zeros(1, dtype=torch.int64, device=DEV)
+    dq, dk, dv = hla.hla_attn_bwd(desc, m, q, k, v, o, lse, do, tiles_visited=visited)
+    torch.cuda.synchronize()
+    spec = Spec(kind, gh, gw, wh, ww, shift=shift)
+    dQ, dK, dV = oatt.attn_bwd(to_np(q), to_np(k), to_np(v), to_np(do), spec)
+    assert_close("dQ", to_np(dq), dQ)
+    assert_close("dK", to_np(dk), dK)
+    assert_close("dV", to_np(dv), dV)
+    assert int(visited.item()) == B * H * m.nnz
+
+
+FULL_BWD = [c for c in FULL if c[0] in ("cfg2", "cfg2-rm", "cfg3", "cfg3-rm", "cfg4", "cfg4-rm")]
+
+
+@pytest.mark.parametrize("case", FULL_BWD, ids=lambda c: c[0])
+def test_step_full_size_sampled(case):
+    """Full hot-path step through the public layer API (perm -> fwd -> unperm ->
+    perm dO -> bwd -> unperm), exactly what bench.py times; one (b, h) slice is
+    checked completely against the fp64 oracle and every slice against the
+    backward invariants sum_k dK = 0 and sum_k dV = sum_q dO."""
+    name, kind, gh, gw, wh, ww, B, H, d = case
+    N = gh * gw
+    q, k, v, do = _inputs(B, N, H, d, seed=0)
+    layer = hla.HilbertLocalAttention(kind, gh, gw, wh, ww, B, H, d, device=DEV)
+    dq, dk, dv = layer.step(q, k, v, do)
+    torch.cuda.synchronize()
+    for t in (dq, dk, dv):
+        assert torch.isfinite(t.float()).all()
+    # invariants on every slice (tolerance: bf16 rounding of N values of size ~1e-2)
+    sdk = dk.float().sum(1)
+    assert sdk.abs().max().item() < 0.05 * max(1.0, N / 4096), sdk.abs().max().item()
+    err = (dv.float().sum(1) - do.float().sum(1)).abs().max().item()
+    assert err < 0.05 * max(1.0, N / 4096), err
+    spec = Spec(kind, gh, gw, wh, ww)
+    s2c = hilbert.hilbert_order(gh, gw)[0] if layer.hilbert else np.arange(N)
+    b, h = B - 1, H // 2
+    Q, K, V, DO = (to_np(t[b, :, h])[s2c] for t in (q, k, v, do))
+    dQ, dK, dV, _, _ = oatt.attn_bwd_slice(Q, K, V, DO, spec, chunk=512)
+    assert_close("%s dQ" % name, to_np(dq[b, :, h])[s2c], dQ)
+    assert_close("%s dK" % name, to_np(dk[b, :, h])[s2c], dK)
+    assert_close("%s dV" % name, to_np(dv[b, :, h])[s2c], dV)
