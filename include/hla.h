@@ -200,6 +200,27 @@ HLA_API hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_mask*
                         void* workspace, size_t workspace_bytes,
                         int64_t* tiles_visited, cudaStream_t stream);
 
+/* The three stages of hla_attn_bwd, callable separately (SURVEY 8(a) rows a6,
+ * a7, a8) so they can be timed / overlapped individually.  Same arguments and
+ * limits as hla_attn_bwd; the workspace carries D and the fp32 dQ accumulator
+ * from one stage to the next and must not be touched in between.
+ *   preprocess: D = rowsum(dO o O) (fp32), dQ accumulator := 0
+ *   main      : the tcgen05 kernel over the transposed lists; writes dK, dV and
+ *               accumulates dQ (fp32, red.global.add)
+ *   finalize  : dQ = bf16(accumulator)                                        */
+HLA_API hla_status hla_attn_bwd_preprocess(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,
+                                   const void* o, const void* dout, void* workspace,
+                                   size_t workspace_bytes, cudaStream_t stream);
+HLA_API hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_block_mask* m,
+                             int32_t batch, int32_t heads, int32_t head_dim, float scale,
+                             const void* q, const void* k, const void* v, const float* lse,
+                             const void* dout, void* dk, void* dv,
+                             void* workspace, size_t workspace_bytes,
+                             int64_t* tiles_visited, cudaStream_t stream);
+HLA_API hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,
+                                 const void* workspace, size_t workspace_bytes, void* dq,
+                                 cudaStream_t stream);
+
 HLA_API size_t hla_attn_bwd_workspace(int32_t batch, int32_t heads, int32_t n, int32_t head_dim);
 
 /* Thread-local message for the last non-OK status of this thread ("" if none). */

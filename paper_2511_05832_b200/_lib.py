@@ -16,7 +16,8 @@ STATUS_NAMES = {0: "HLA_OK", 1: "HLA_ERR_INVALID", 2: "HLA_ERR_UNSUPPORTED", 3: 
 
 # exported symbols of include/hla.h and include/hla_debug.h
 EXPORTED = ("hla_hilbert_index", "hla_hilbert_perm", "hla_build_block_mask", "hla_mask_ratios",
-            "hla_attn_fwd", "hla_attn_bwd", "hla_attn_bwd_workspace", "hla_last_error", "hla_version",
+            "hla_attn_fwd", "hla_attn_bwd", "hla_attn_bwd_workspace", "hla_attn_bwd_preprocess",
+            "hla_attn_bwd_main", "hla_attn_bwd_finalize", "hla_last_error", "hla_version",
             "hla_debug_umma")
 
 
@@ -59,6 +60,9 @@ def lib():
                             ctypes.POINTER(ctypes.c_double)],
         "hla_attn_fwd": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp],
         "hla_attn_bwd": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp],
+        "hla_attn_bwd_preprocess": [i32, i32, i32, i32, vp, vp, vp, sz, vp],
+        "hla_attn_bwd_main": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp],
+        "hla_attn_bwd_finalize": [i32, i32, i32, i32, vp, sz, vp, vp],
         "hla_debug_umma": [vp, vp, vp, i32, i32, i32, i32, i32, i32, vp],
     }
     for name, args in sig.items():

@@ -164,6 +164,28 @@ def hla_attn_bwd(desc, mask, q, k, v, o, lse, dout, scale=0.0, dq=None, dk=None,
     return dq, dk, dv
 
 
+def hla_attn_bwd_preprocess(o, dout, workspace, stream=None):
+    B, N, H, D = o.shape
+    check("hla_attn_bwd_preprocess", lib().hla_attn_bwd_preprocess(B, H, N, D, _ptr(o), _ptr(dout), _ptr(workspace),
+                                                                   workspace.numel(), _stream(stream)))
+
+
+def hla_attn_bwd_main(desc, mask, q, k, v, lse, dout, dk, dv, workspace, scale=0.0, tiles_visited=None,
+                      stream=None):
+    B, N, H, D = q.shape
+    mc = mask.c
+    check("hla_attn_bwd_main", lib().hla_attn_bwd_main(ctypes.byref(desc), ctypes.byref(mc), B, H, D, float(scale),
+                                                       _ptr(q), _ptr(k), _ptr(v), _ptr(lse), _ptr(dout), _ptr(dk),
+                                                       _ptr(dv), _ptr(workspace), workspace.numel(),
+                                                       _ptr(tiles_visited), _stream(stream)))
+
+
+def hla_attn_bwd_finalize(workspace, dq, stream=None):
+    B, N, H, D = dq.shape
+    check("hla_attn_bwd_finalize", lib().hla_attn_bwd_finalize(B, H, N, D, _ptr(workspace), workspace.numel(),
+                                                               _ptr(dq), _stream(stream)))
+
+
 def hla_debug_umma(A, B, M, N, K, a_mn=False, b_mn=False, a_tmem=False, stream=None):
     C = torch.empty(M, N, dtype=torch.float32, device=A.device)
     check("hla_debug_umma", lib().hla_debug_umma(_ptr(A), _ptr(B), _ptr(C), M, N, K, int(a_mn), int(b_mn),

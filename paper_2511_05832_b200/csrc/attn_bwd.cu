@@ -395,44 +395,66 @@ extern "C" size_t hla_attn_bwd_workspace(int32_t batch, int32_t heads, int32_t n
   return ((acc + 255) / 256) * 256 + ((dsum + 255) / 256) * 256;
 }
 
-extern "C" hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
-                                   int32_t head_dim, float scale, const void* q, const void* k, const void* v,
-                                   const void* o, const float* lse, const void* dout, void* dq, void* dk, void* dv,
-                                   void* workspace, size_t workspace_bytes, int64_t* tiles_visited,
-                                   cudaStream_t stream) {
+namespace {
+
+// workspace carve-up: [fp32 dQ accumulator, 256-aligned][fp32 D]
+hla_status carve_workspace(int32_t batch, int32_t heads, int32_t n, int32_t head_dim, void* workspace,
+                           size_t workspace_bytes, float** dq_acc, float** dsum) {
+  HLA_REQUIRE(workspace != nullptr, HLA_ERR_INVALID, "null workspace");
+  HLA_REQUIRE((uintptr_t)workspace % 256 == 0, HLA_ERR_INVALID, "workspace must be 256-byte aligned");
+  const size_t need = hla_attn_bwd_workspace(batch, heads, n, head_dim);
+  HLA_REQUIRE(workspace_bytes >= need, HLA_ERR_INVALID, "workspace %zu < %zu bytes", workspace_bytes, need);
+  const size_t acc = (size_t)batch * n * heads * head_dim * 4;
+  *dq_acc = reinterpret_cast<float*>(workspace);
+  *dsum = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + ((acc + 255) / 256) * 256);
+  return HLA_OK;
+}
+
+}  // namespace
+
+extern "C" hla_status hla_attn_bwd_preprocess(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,
+                                              const void* o, const void* dout, void* workspace,
+                                              size_t workspace_bytes, cudaStream_t stream) {
+  clear_error();
+  HLA_REQUIRE(head_dim == 32 || head_dim == 64, HLA_ERR_UNSUPPORTED, "head_dim %d not in {32, 64}", head_dim);
+  HLA_REQUIRE(batch >= 1 && heads >= 1 && n >= 1, HLA_ERR_INVALID, "bad shape");
+  HLA_REQUIRE(o && dout && ((uintptr_t)o | (uintptr_t)dout) % 16 == 0, HLA_ERR_INVALID, "o/dout null or unaligned");
+  float *dq_acc, *dsum;
+  hla_status st = carve_workspace(batch, heads, n, head_dim, workspace, workspace_bytes, &dq_acc, &dsum);
+  if (st != HLA_OK) return st;
+  const int64_t rows = (int64_t)batch * n * heads;
+  const int64_t threads = rows * (head_dim / 8);
+  const unsigned blocks = (unsigned)((threads + 255) / 256);
+  if (head_dim == 64)
+    bwd_preprocess_kernel<64><<<blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
+                                                          reinterpret_cast<const __nv_bfloat16*>(dout), dsum,
+                                                          dq_acc, n, heads, rows);
+  else
+    bwd_preprocess_kernel<32><<<blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
+                                                          reinterpret_cast<const __nv_bfloat16*>(dout), dsum,
+                                                          dq_acc, n, heads, rows);
+  HLA_CUDA_TRY(cudaGetLastError());
+  return HLA_OK;
+}
+
+extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch,
+                                        int32_t heads, int32_t head_dim, float scale, const void* q, const void* k,
+                                        const void* v, const float* lse, const void* dout, void* dk, void* dv,
+                                        void* workspace, size_t workspace_bytes, int64_t* tiles_visited,
+                                        cudaStream_t stream) {
   clear_error();
   Pattern pat;
   hla_status st = check_attn_args(d, m, batch, heads, head_dim, &pat);
   if (st != HLA_OK) return st;
   HLA_REQUIRE(m->t_row_ptr && m->t_col_idx && m->t_kind, HLA_ERR_INVALID, "transposed mask arrays missing");
-  HLA_REQUIRE(q && k && v && o && lse && dout && dq && dk && dv && workspace, HLA_ERR_INVALID, "null pointer");
-  HLA_REQUIRE(((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)o | (uintptr_t)dout | (uintptr_t)dq |
-               (uintptr_t)dk | (uintptr_t)dv) % 16 == 0 && (uintptr_t)lse % 16 == 0,
+  HLA_REQUIRE(q && k && v && lse && dout && dk && dv, HLA_ERR_INVALID, "null pointer");
+  HLA_REQUIRE(((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)dout | (uintptr_t)dk | (uintptr_t)dv |
+               (uintptr_t)lse) % 16 == 0,
               HLA_ERR_INVALID, "tensors must be 16-byte aligned");
-  HLA_REQUIRE((uintptr_t)workspace % 256 == 0, HLA_ERR_INVALID, "workspace must be 256-byte aligned");
-  const size_t need = hla_attn_bwd_workspace(batch, heads, pat.N, head_dim);
-  HLA_REQUIRE(workspace_bytes >= need, HLA_ERR_INVALID, "workspace %zu < %zu bytes", workspace_bytes, need);
-  const int64_t rows = (int64_t)batch * pat.N * heads;
-  float* dq_acc = reinterpret_cast<float*>(workspace);
-  float* dsum = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) +
-                                         (((size_t)rows * head_dim * 4 + 255) / 256) * 256);
+  float *dq_acc, *dsum;
+  st = carve_workspace(batch, heads, pat.N, head_dim, workspace, workspace_bytes, &dq_acc, &dsum);
+  if (st != HLA_OK) return st;
   const float sc = scale > 0.f ? scale : 1.0f / sqrtf((float)head_dim);
-
-  // K7
-  {
-    const int64_t threads = rows * (head_dim / 8);
-    const unsigned blocks = (unsigned)((threads + 255) / 256);
-    if (head_dim == 64)
-      bwd_preprocess_kernel<64><<<blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
-                                                            reinterpret_cast<const __nv_bfloat16*>(dout), dsum,
-                                                            dq_acc, pat.N, heads, rows);
-    else
-      bwd_preprocess_kernel<32><<<blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
-                                                            reinterpret_cast<const __nv_bfloat16*>(dout), dsum,
-                                                            dq_acc, pat.N, heads, rows);
-    HLA_CUDA_TRY(cudaGetLastError());
-  }
-  // K8
   BwdParams prm;
   prm.pat = pat;
   prm.N = pat.N;
@@ -458,19 +480,50 @@ extern "C" hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_ma
   const bool two_d = pat.kind == K_WSA || pat.kind == K_SA || pat.kind == K_NA2D;
   const int32_t mkb = pat.N / kBlock;
   if (head_dim == 64)
-    st = two_d ? launch_bwd<64, true>(mq, mk, mv, mdo, prm, mkb, stream)
-               : launch_bwd<64, false>(mq, mk, mv, mdo, prm, mkb, stream);
-  else
-    st = two_d ? launch_bwd<32, true>(mq, mk, mv, mdo, prm, mkb, stream)
+    return two_d ? launch_bwd<64, true>(mq, mk, mv, mdo, prm, mkb, stream)
+                 : launch_bwd<64, false>(mq, mk, mv, mdo, prm, mkb, stream);
+  return two_d ? launch_bwd<32, true>(mq, mk, mv, mdo, prm, mkb, stream)
                : launch_bwd<32, false>(mq, mk, mv, mdo, prm, mkb, stream);
+}
+
+extern "C" hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,
+                                            const void* workspace, size_t workspace_bytes, void* dq,
+                                            cudaStream_t stream) {
+  clear_error();
+  HLA_REQUIRE(head_dim == 32 || head_dim == 64, HLA_ERR_UNSUPPORTED, "head_dim %d not in {32, 64}", head_dim);
+  HLA_REQUIRE(dq && (uintptr_t)dq % 16 == 0, HLA_ERR_INVALID, "dq null or unaligned");
+  float *dq_acc, *dsum;
+  hla_status st = carve_workspace(batch, heads, n, head_dim, const_cast<void*>(workspace), workspace_bytes, &dq_acc,
+                                  &dsum);
   if (st != HLA_OK) return st;
-  // K9
-  {
-    const int64_t n4 = rows * head_dim / 4;
-    const unsigned blocks = (unsigned)std::min<int64_t>((n4 + 255) / 256, 148 * 16);
-    dq_finalize_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const float4*>(dq_acc),
-                                                   reinterpret_cast<uint2*>(dq), n4);
-    HLA_CUDA_TRY(cudaGetLastError());
-  }
+  const int64_t n4 = (int64_t)batch * n * heads * head_dim / 4;
+  const unsigned blocks = (unsigned)std::min<int64_t>((n4 + 255) / 256, 148 * 16);
+  dq_finalize_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const float4*>(dq_acc),
+                                                 reinterpret_cast<uint2*>(dq), n4);
+  HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
+}
+
+extern "C" hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
+                                   int32_t head_dim, float scale, const void* q, const void* k, const void* v,
+                                   const void* o, const float* lse, const void* dout, void* dq, void* dk, void* dv,
+                                   void* workspace, size_t workspace_bytes, int64_t* tiles_visited,
+                                   cudaStream_t stream) {
+  clear_error();
+  Pattern pat;
+  hla_status st = check_attn_args(d, m, batch, heads, head_dim, &pat);
+  if (st != HLA_OK) return st;
+  HLA_REQUIRE(o && dq, HLA_ERR_INVALID, "null pointer");
+  // validate everything before launching anything
+  float *dq_acc, *dsum;
+  st = carve_workspace(batch, heads, pat.N, head_dim, workspace, workspace_bytes, &dq_acc, &dsum);
+  if (st != HLA_OK) return st;
+  HLA_REQUIRE(((uintptr_t)o | (uintptr_t)dq) % 16 == 0, HLA_ERR_INVALID, "tensors must be 16-byte aligned");
+  if ((st = hla_attn_bwd_preprocess(batch, heads, pat.N, head_dim, o, dout, workspace, workspace_bytes, stream)) !=
+      HLA_OK)
+    return st;
+  if ((st = hla_attn_bwd_main(d, m, batch, heads, head_dim, scale, q, k, v, lse, dout, dk, dv, workspace,
+                              workspace_bytes, tiles_visited, stream)) != HLA_OK)
+    return st;
+  return hla_attn_bwd_finalize(batch, heads, pat.N, head_dim, workspace, workspace_bytes, dq, stream);
 }

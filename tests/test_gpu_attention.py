@@ -128,9 +128,13 @@ def test_bwd_small(case, sharp):
     torch.cuda.synchronize()
     spec = Spec(kind, gh, gw, wh, ww, shift=shift)
     dQ, dK, dV = oatt.attn_bwd(to_np(q), to_np(k), to_np(v), to_np(do), spec)
-    assert_close("dQ", to_np(dq), dQ)
-    assert_close("dK", to_np(dk), dK)
-    assert_close("dV", to_np(dv), dV)
+    for name, got, ref in (("dQ", dq, dQ), ("dK", dk, dK), ("dV", dv, dV)):
+        # DESIGN.md reading R16: the north_star bound is absolute for the workload
+        # recipe (unit-variance inputs).  The sharp stress input (Q x 4) scales the
+        # gradients up to ~5x; its bound scales with the reference RMS relative to
+        # the nominal gradient RMS (0.25), i.e. the same relative accuracy.
+        f = max(1.0, float(np.sqrt((ref ** 2).mean())) / 0.25) if sharp else 1.0
+        assert_close(name, to_np(got), ref, max_abs=2e-2 * f, mean_abs=2e-3 * f)
     assert int(visited.item()) == B * H * m.nnz
 
 
@@ -151,11 +155,12 @@ def test_step_full_size_sampled(case):
     torch.cuda.synchronize()
     for t in (dq, dk, dv):
         assert torch.isfinite(t.float()).all()
-    # invariants on every slice (tolerance: bf16 rounding of N values of size ~1e-2)
-    sdk = dk.float().sum(1)
-    assert sdk.abs().max().item() < 0.05 * max(1.0, N / 4096), sdk.abs().max().item()
-    err = (dv.float().sum(1) - do.float().sum(1)).abs().max().item()
-    assert err < 0.05 * max(1.0, N / 4096), err
+    # invariants on every slice: sum_k dK = 0, sum_k dV = sum_q dO (exact for the
+    # fp64 oracle).  On the GPU, bf16 rounding of the dS / P MMA operands leaves a
+    # residual ~ sqrt(N) * rms * 2^-8 per column; bound it at 8x that.
+    tol = 8 * np.sqrt(N) * float(dk.float().pow(2).mean().sqrt()) * 2 ** -8
+    assert dk.float().sum(1).abs().max().item() <= tol
+    assert (dv.float().sum(1) - do.float().sum(1)).abs().max().item() <= tol
     spec = Spec(kind, gh, gw, wh, ww)
     s2c = hilbert.hilbert_order(gh, gw)[0] if layer.hilbert else np.arange(N)
     b, h = B - 1, H // 2
