@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""bench.py -- Hilbert-guided local attention hot path on B200 (driver contract).
+
+One STEP = one pass of the whole hot path over one batch:
+  perm(Q,K,V -> Hilbert) ; block-sparse fwd ; perm(O -> grid) ;
+  perm(dO -> Hilbert) ; bwd preprocess ; block-sparse bwd ; dQ finalize ;
+  perm(dQ,dK,dV -> grid)
+The block mask and the Hilbert path are built once per shape, before timing
+(the paper caches them).  Workload (N=1): BASELINE.json configs[1]
+("cfg2": 64x64 grid, 8 heads, head_dim 64, HWA 256 tokens vs row-major 16x16
+windows, block 128), batch 16 (the paper's batch).
+
+metric "fwd+bwd ms ...": value = step time per batch of work for the whole job
+= (max-over-ranks device time of one step) / (batches processed per step by all
+ranks).  Each rank processes its own batch (weak scaling, no collective on the
+hot path; NCCL only for the barrier and the max-reduction of timings).
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+"""
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fwd+bwd ms and tensor-pipe % vs row-major + dense FA, 1/2/4/8 B200"
+CONFIGS = {
+    # name: Hilbert pattern, row-major baseline, grid side, window (cells), batch, heads, head_dim
+    "cfg1": dict(kind="HWA", rm="WSA", grid=16, win=8, B=1, H=1, d=32,
+                 text="16x16 grid, HWA 64 tokens vs WSA 8x8, 1 head, d32, batch 1"),
+    "cfg2": dict(kind="HWA", rm="WSA", grid=64, win=16, B=16, H=8, d=64,
+                 text="64x64 grid, HWA 256 tokens vs WSA 16x16, 8 heads, d64, block 128, batch 16"),
+    "cfg3": dict(kind="HSA", rm="SA", grid=64, win=16, B=16, H=8, d=64,
+                 text="64x64 grid, HSA 256 tokens vs SA 16x16, 8 heads, d64, block 128, batch 16"),
+    "cfg4": dict(kind="HNA", rm="NA2D", grid=128, win=7, B=16, H=12, d=64,
+                 text="128x128 grid, HNA 49 tokens vs NA2D 7x7, 12 heads, d64, block 128, batch 16"),
+}
+# paper's row-major-block-sparse -> Hilbert fwd+bwd speedup on the nearest shape (RTX 3080)
+PAPER_SPEEDUP = {"cfg2": (2.70, "WSA(Flex)->HWA 64x64 W8, P:L150-151"),
+                 "cfg3": (1.62, "SA(Flex)->HSA 64x64 K9, P:L495-496"),
+                 "cfg4": (1.58, "NA2D(Flex)->HNA 56x56 K7, P:L490-491")}
+L2_FLUSH_BYTES = 512 << 20
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-variants", action="store_true", help="skip the row-major / dense comparison runs")
+    p.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            pk = json.load(f)
+        return {"hbm": pk["hbm_gbs"], "tf": pk["bf16_tflops"], "tf_sus": pk.get("bf16_tflops_sustained", pk["bf16_tflops"]),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm": 6650.0, "tf": 1590.0, "tf_sus": 1400.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.out = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.out, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.out.flush()
+        self.out.seek(0)
+        sms, mx, reasons = [], None, set()
+        for line in self.out.read().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm, smax = float(f[1]), float(f[2])
+            except ValueError:
+                continue
+            mx = smax
+            names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+            for name, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+            if sm > 300:       # under load
+                sms.append(sm)
+        if not sms:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(sms), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# ---------------------------------------------------------- oracle (CPU) leg
+def oracle_step_sample(cfg, n_slices, seed=0):
+    """The oracle as it stands on a bounded sample: Hilbert reorder (numpy
+    indexing) + fp64 fwd+bwd of `n_slices` (b, h) slices.  Returns seconds."""
+    import numpy as np
+
+    import hla_synth
+    from oracle import attention as oatt
+    from oracle import hilbert as ohil
+    from oracle.patterns import Spec
+    g, B, H, d = cfg["grid"], cfg["B"], cfg["H"], cfg["d"]
+    N = g * g
+    spec = Spec(cfg["kind"], g, g, cfg["win"], cfg["win"])
+    s2c, _ = ohil.hilbert_order(g, g)
+    shape = (1, N, 1, d)
+    t0 = time.perf_counter()
+    for i in range(n_slices):
+        q, k, v, do = (hla_synth.uniform_np(shape, seed + i, tid) for tid in (1, 2, 3, 4))
+        qs, ks, vs, dos = (ohil.to_sequence(x, s2c)[0, :, 0].astype(np.float64) for x in (q, k, v, do))
+        dQ, dK, dV, O, _ = oatt.attn_bwd_slice(qs, ks, vs, dos, spec, chunk=512)
+        for x in (dQ, dK, dV, O):
+            ohil.to_grid(x[None], s2c)
+    return time.perf_counter() - t0
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(cfg, budget_s=15.0):
+    slices_total = cfg["B"] * cfg["H"]
+    t1 = oracle_step_sample(cfg, 1)
+    n = int(max(1, min(slices_total, budget_s / max(t1, 1e-3))))
+    t = oracle_step_sample(cfg, n, seed=1) if n > 1 else t1
+    per_slice = t / n
+    return {"value": round(per_slice * slices_total * 1e3, 3), "unit": "ms", "cores": blas_threads(),
+            "kind": "oracle",
+            "sample": "%d of %d (b,h) slices of one step (Hilbert reorder + fp64 fwd+bwd, numpy), "
+                      "extrapolated x%d" % (n, slices_total, slices_total // max(n, 1))}
+
+
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    slices_total = cfg["B"] * cfg["H"]
+    for _ in range(args.warmup):
+        oracle_step_sample(cfg, 1)
+    times = [oracle_step_sample(cfg, 1, seed=s) for s in range(args.steps)]
+    ms = statistics.mean(times) * slices_total * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": round(ms, 3), "unit": "ms", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (hla_synth)",
+            "config": {"workload": args.config + ": " + cfg["text"], "global_batch": cfg["B"],
+                       "seq_len": cfg["grid"] ** 2, "parallelism": "host cores (numpy BLAS)"},
+            "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": blas_threads(), "kind": "oracle",
+                             "sample": "each step = 1 of %d (b,h) slices (Hilbert reorder + fp64 fwd+bwd), "
+                                       "extrapolated x%d" % (slices_total, slices_total)},
+            "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- GPU leg
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import hla_synth
+    import paper_2511_05832_b200 as hla
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    peaks = load_peaks()
+
+    g, B, H, d, win = cfg["grid"], cfg["B"], cfg["H"], cfg["d"], cfg["win"]
+    N = g * g
+    # each rank: its own batch shard (weak scaling); inputs resident in HBM before timing
+    q, k, v, do = hla_synth.attention_inputs(B, N, H, d, seed=rank, device=dev)
+    layer = hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, B, H, d, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+
+    def timed(lay, steps, warmup, with_marks=True, sampler=None):
+        for _ in range(warmup):
+            lay.step(q, k, v, do)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.start()
+        rec = []
+        for _ in range(steps):
+            flush.zero_()                       # L2 flush between timed steps (untimed)
+            ev = [("start", torch.cuda.Event(enable_timing=True))]
+            ev[0][1].record()
+
+            def mark(name, ev=ev):
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                ev.append((name, e))
+            lay.step(q, k, v, do, mark if with_marks else None)
+            if not with_marks:
+                mark("end")
+            rec.append(ev)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clocks = sampler.stop() if sampler else None
+        total = [ev[0][1].elapsed_time(ev[-1][1]) for ev in rec]
+        stages = {}
+        for ev in rec:
+            for (_, a), (name, b) in zip(ev[:-1], ev[1:]):
+                stages.setdefault(name, []).append(a.elapsed_time(b))
+        return total, {kk: statistics.mean(vv) for kk, vv in stages.items()}, clocks
+
+    sampler = ClockSampler(local)
+    total, stages, clocks = timed(layer, args.steps, args.warmup, True, sampler)
+    my_ms = statistics.mean(total)
+    t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms = float(t.item())
+    value = step_ms / world            # ms per batch of work for the whole job
+
+    # --- row-major baseline and dense FA on the same shape (same kernels) ---
+    variants = {}
+    if not args.no_variants:
+        vsteps = max(3, min(args.steps, 10))
+        for name, kind in (("row_major", cfg["rm"]), ("dense", "DENSE")):
+            lay = hla.HilbertLocalAttention(kind, g, g, win, win, B, H, d, device=dev)
+            tot, st, _ = timed(lay, vsteps, 2, True)
+            variants[name] = {"pattern": kind, "ms_per_step": round(statistics.mean(tot), 4),
+                              "fwd_ms": round(st["fwd"], 4), "bwd_ms": round(st["bwd_pre"] + st["bwd"] + st["bwd_fin"], 4),
+                              "tiles_per_bh": lay.nnz}
+            exec_flops = 14 * 128 * 128 * d * lay.nnz * B * H
+            variants[name]["tensor_pct_executed"] = round(
+                100 * exec_flops / ((st["fwd"] + st["bwd"]) * 1e-3) / (peaks["tf_sus"] * 1e12), 2)
+            del lay
+        ours_attn = stages["fwd"] + stages["bwd_pre"] + stages["bwd"] + stages["bwd_fin"]
+        rm = variants["row_major"]
+        rm_attn = rm["fwd_ms"] + rm["bwd_ms"]
+        variants["speedup_attn_vs_row_major"] = round(rm_attn / ours_attn, 3)
+        variants["speedup_step_vs_row_major"] = round(rm["ms_per_step"] / step_ms, 3)
+        variants["speedup_attn_vs_dense"] = round((variants["dense"]["fwd_ms"] + variants["dense"]["bwd_ms"]) / ours_attn, 3)
+        if args.config in PAPER_SPEEDUP:
+            variants["paper_speedup_fwd_bwd"] = {"value": PAPER_SPEEDUP[args.config][0],
+                                                 "source": PAPER_SPEEDUP[args.config][1] + " (RTX 3080, context)"}
+
+    # --- end to end through the public API: host -> device -> step -> host ---
+    e2e = None
+    if not args.no_e2e:
+        hin = [x.cpu().pin_memory() for x in (q, k, v, do)]
+        dq_in = [torch.empty_like(x) for x in (q, k, v, do)]
+        hout = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (q, q, q, q)]
+        esteps = max(2, min(args.steps, 5))
+        for it in range(esteps + 1):
+            if it == 1:
+                torch.cuda.synchronize()
+                if world > 1:
+                    dist.barrier()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+            for dst, src in zip(dq_in, hin):
+                dst.copy_(src, non_blocking=True)
+            o = layer.forward(*dq_in[:3])
+            hout[0].copy_(o, non_blocking=True)
+            dqq, dkk, dvv = layer.backward(dq_in[3])
+            for dst, src in zip(hout[1:], (dqq, dkk, dvv)):
+                dst.copy_(src, non_blocking=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1) / esteps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        nbytes = sum(x.numel() * x.element_size() for x in hin)
+        e2e = {"value": round(float(te.item()) / world, 4), "unit": "ms", "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes, "path": "pinned host -> HilbertLocalAttention.forward/backward -> pinned host"}
+
+    # --- roofline of the dominant kernel (share of the step) ---
+    T = B * H * N                               # token-heads per launch
+    tiles = layer.nnz * B * H
+    kern = {
+        "fwd": {"bytes": T * (8 * d + 4), "flops": 4 * 128 * 128 * d * tiles, "name": "attn_fwd_kernel"},
+        "bwd": {"bytes": T * (20 * d + 8), "flops": 10 * 128 * 128 * d * tiles, "name": "attn_bwd_kernel"},
+        "perm_qkv": {"bytes": 3 * 2 * T * d * 2, "flops": 0, "name": "hilbert_perm_kernel"},
+        "perm_grads": {"bytes": 3 * 2 * T * d * 2, "flops": 0, "name": "hilbert_perm_kernel"},
+    }
+    dom = max((kk for kk in kern if kk in stages), key=lambda kk: stages[kk])
+    ms_dom = stages[dom]
+    kd = kern[dom]
+    ridge = peaks["tf_sus"] * 1e12 / (peaks["hbm"] * 1e9)
+    ai = kd["flops"] / kd["bytes"] if kd["bytes"] else 0
+    if ai < ridge:
+        ach = kd["bytes"] / (ms_dom * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm"], "unit": "GB/s",
+                "frac": round(ach / peaks["hbm"], 4)}
+    else:
+        ach = kd["flops"] / (ms_dom * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": round(ach, 1), "peak": peaks["tf_sus"], "unit": "TFLOP/s",
+                "frac": round(ach / peaks["tf_sus"], 4)}
+    roof.update({"kernel": kd["name"], "stage": dom, "share_of_step": round(ms_dom / my_ms, 4),
+                 "ms_per_launch": round(ms_dom, 5), "algorithmic_bytes_per_launch": kd["bytes"],
+                 "algorithmic_flops_per_launch": kd["flops"], "arith_intensity": round(ai, 1),
+                 "peak_source": peaks["source"], "traffic": None})
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f).get(args.config, {}).get(dom)
+        if tr:
+            roof["traffic"] = tr
+    except Exception:
+        pass
+
+    attn_ms = stages["fwd"] + stages["bwd_pre"] + stages["bwd"] + stages["bwd_fin"]
+    exec_flops = 14 * 128 * 128 * d * tiles
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(cfg)
+
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "ms", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic: hla_synth splitmix64 uniform, unit variance, bf16 (no dataset)",
+        "config": {"workload": args.config + ": " + cfg["text"], "global_batch": B * world, "seq_len": N,
+                   "parallelism": "dp%d (batch shards, no collective on the hot path)" % world,
+                   "l2": "flushed between timed steps (%d MiB write, untimed)" % (L2_FLUSH_BYTES >> 20),
+                   "step": "perm(qkv)+fwd+perm(o)+perm(dO)+bwd_pre+bwd+bwd_fin+perm(dq,dk,dv)",
+                   "mask": "built once before timing (%d of %d tiles per (b,h) executed)" % (layer.nnz, (N // 128) ** 2)},
+        "clocks": clocks, "e2e": e2e, "gpu_launches": layer.launches_per_step * args.steps,
+        "roofline": roof, "cpu_baseline": cpu,
+        "breakdown_ms": {kk: round(vv, 5) for kk, vv in stages.items()},
+        "attn_ms": round(attn_ms, 4),
+        "tensor_pct_executed": round(100 * exec_flops / (attn_ms * 1e-3) / (peaks["tf_sus"] * 1e12), 2),
+        "variants": variants,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

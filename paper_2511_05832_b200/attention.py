@@ -45,33 +45,57 @@ class HilbertLocalAttention:
     def nnz(self):
         return self.mask.nnz
 
-    def forward(self, q, k, v):
-        """q, k, v: bf16 [B, N, heads, d] in grid (row-major cell) order -> o (grid order)."""
+    def forward(self, q, k, v, mark=None):
+        """q, k, v: bf16 [B, N, heads, d] in grid (row-major cell) order -> o (grid order).
+
+        mark: optional callable(name) invoked after each launch (bench timing hook)."""
+        mark = mark or _nop
         if self.hilbert:
             api.hla_hilbert_perm(self.grid_h, self.grid_w, api.TO_HILBERT, (q, k, v), (self.qs, self.ks, self.vs))
+            mark("perm_qkv")
             api.hla_attn_fwd(self.desc, self.mask, self.qs, self.ks, self.vs, self.scale, self.os, self.lse)
+            mark("fwd")
             api.hla_hilbert_perm(self.grid_h, self.grid_w, api.FROM_HILBERT, (self.os,), (self.o,))
+            mark("perm_o")
             self._saved = (self.qs, self.ks, self.vs, self.os)
         else:
             api.hla_attn_fwd(self.desc, self.mask, q, k, v, self.scale, self.o, self.lse)
+            mark("fwd")
             self._saved = (q, k, v, self.o)
         return self.o
 
-    def backward(self, dout):
+    def backward(self, dout, mark=None):
         """dout: bf16 [B, N, heads, d] in grid order -> (dq, dk, dv) in grid order."""
+        mark = mark or _nop
         q, k, v, o = self._saved
         if self.hilbert:
             api.hla_hilbert_perm(self.grid_h, self.grid_w, api.TO_HILBERT, (dout,), (self.dos,))
-            api.hla_attn_bwd(self.desc, self.mask, q, k, v, o, self.lse, self.dos, self.scale,
-                             self.dqs, self.dks, self.dvs, self.workspace)
+            mark("perm_do")
+            dout_s, dq, dk, dv = self.dos, self.dqs, self.dks, self.dvs
+        else:
+            dout_s, dq, dk, dv = dout, self.dq, self.dk, self.dv
+        api.hla_attn_bwd_preprocess(o, dout_s, self.workspace)
+        mark("bwd_pre")
+        api.hla_attn_bwd_main(self.desc, self.mask, q, k, v, self.lse, dout_s, dk, dv, self.workspace, self.scale)
+        mark("bwd")
+        api.hla_attn_bwd_finalize(self.workspace, dq)
+        mark("bwd_fin")
+        if self.hilbert:
             api.hla_hilbert_perm(self.grid_h, self.grid_w, api.FROM_HILBERT, (self.dqs, self.dks, self.dvs),
                                  (self.dq, self.dk, self.dv))
-        else:
-            api.hla_attn_bwd(self.desc, self.mask, q, k, v, o, self.lse, dout, self.scale,
-                             self.dq, self.dk, self.dv, self.workspace)
+            mark("perm_grads")
         return self.dq, self.dk, self.dv
 
-    def step(self, q, k, v, dout):
+    # kernel launches per step (forward + backward)
+    @property
+    def launches_per_step(self):
+        return 8 if self.hilbert else 4
+
+    def step(self, q, k, v, dout, mark=None):
         """One pass of the whole hot path: forward then backward."""
-        self.forward(q, k, v)
-        return self.backward(dout)
+        self.forward(q, k, v, mark)
+        return self.backward(dout, mark)
+
+
+def _nop(_name):
+    pass
