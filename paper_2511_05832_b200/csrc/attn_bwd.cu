@@ -53,14 +53,14 @@ struct BwdParams {
 template <int D>
 struct BwdSmem {
   static constexpr uint32_t kTileBytes = kBlock * D * 2;
-  alignas(1024) uint8_t k[kTileBytes];
-  alignas(1024) uint8_t v[kTileBytes];
+  alignas(1024) uint8_t k[2][kTileBytes];
+  alignas(1024) uint8_t v[2][kTileBytes];
   alignas(1024) uint8_t q[2][kTileBytes];
   alignas(1024) uint8_t dO[2][kTileBytes];
   alignas(1024) uint8_t ds[2 * 128 * 128];   // dS^T bf16: [q/64][kv 128][64 q], SWIZZLE_128B
   alignas(16) float lse[2][kBlock];
   alignas(16) float dd[2][kBlock];
-  uint64_t kv_full, q_full[2], q_empty[2], s_full, ds_ready, dq_full, dq_free, dkv_full;
+  uint64_t kv_full[2], kv_empty[2], q_full[2], q_empty[2], s_full, ds_ready, dq_full, dq_free, dkv_full;
   uint32_t tmem_base;
 };
 
@@ -89,6 +89,11 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
                : "memory");
 }
 
+// Persistent: CTA c processes kv-block work units c, c + G, ... (unit = kv-block,
+// head, batch; kv-block fastest).  K/V are double-buffered across units, so the
+// next unit's K/V (and first Q/dO) stream in while the current unit computes;
+// the dK/dV epilogue of a unit overlaps the first S/dP MMAs of the next one.
+// Phase counters: n = units with nt > 0 so far, g = (q-block) tiles so far.
 template <int D, bool kTwoD>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -97,13 +102,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   BwdSmem<D>& sm = *reinterpret_cast<BwdSmem<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t kb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
-  const int64_t bh = (int64_t)b * prm.heads + h;
+  const int32_t mk = prm.N / kBlock;
+  const int32_t units = mk * prm.heads * prm.batch;
 
   if (warp == 0 && lane == 0) {
-    sm100::mbar_init(&sm.kv_full, 1);
     for (int s = 0; s < 2; ++s) {
+      sm100::mbar_init(&sm.kv_full[s], 1);
+      sm100::mbar_init(&sm.kv_empty[s], 1);
       sm100::mbar_init(&sm.q_full[s], 1);
       sm100::mbar_init(&sm.q_empty[s], 1);
     }
@@ -126,197 +131,230 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
+  unsigned long long tiles_done = 0;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0 && nt > 0) {
+    if (lane == 0) {
       const uint64_t pol_kv = sm100::policy_evict_first();
       const uint64_t pol_q = sm100::policy_evict_last();
-      const int32_t krow = b * prm.N + kb * kBlock;
-      sm100::mbar_arrive_expect_tx(&sm.kv_full, 2 * BwdSmem<D>::kTileBytes);
-      sm100::tma_load_3d(sm.k, &tmK, &sm.kv_full, 0, h, krow, pol_kv);
-      sm100::tma_load_3d(sm.v, &tmV, &sm.kv_full, 0, h, krow, pol_kv);
-      for (int t = 0; t < nt; ++t) {
-        const int s = t & 1;
-        if (t >= 2) sm100::mbar_wait(&sm.q_empty[s], ((t >> 1) - 1) & 1);
-        const int32_t qblk = __ldg(prm.t_col_idx + rs + t);
-        const int32_t qrow = b * prm.N + qblk * kBlock;
-        sm100::mbar_arrive_expect_tx(&sm.q_full[s], 2 * BwdSmem<D>::kTileBytes + 2 * kBlock * 4);
-        sm100::tma_load_3d(sm.q[s], &tmQ, &sm.q_full[s], 0, h, qrow, pol_q);
-        sm100::tma_load_3d(sm.dO[s], &tmDO, &sm.q_full[s], 0, h, qrow, pol_q);
-        sm100::bulk_load(sm.lse[s], prm.lse + bh * prm.N + qblk * kBlock, kBlock * 4, &sm.q_full[s]);
-        sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * kBlock, kBlock * 4, &sm.q_full[s]);
+      uint32_t n = 0, g = 0;
+      for (int32_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
+        const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
+        if (nt == 0) continue;
+        const int64_t bh = (int64_t)b * prm.heads + h;
+        const int kvs = n & 1;
+        if (n >= 2) sm100::mbar_wait(&sm.kv_empty[kvs], ((n >> 1) - 1) & 1);
+        const int32_t krow = b * prm.N + kb * kBlock;
+        sm100::mbar_arrive_expect_tx(&sm.kv_full[kvs], 2 * BwdSmem<D>::kTileBytes);
+        sm100::tma_load_3d(sm.k[kvs], &tmK, &sm.kv_full[kvs], 0, h, krow, pol_kv);
+        sm100::tma_load_3d(sm.v[kvs], &tmV, &sm.kv_full[kvs], 0, h, krow, pol_kv);
+        for (int t = 0; t < nt; ++t, ++g) {
+          const int s = g & 1;
+          if (g >= 2) sm100::mbar_wait(&sm.q_empty[s], ((g >> 1) - 1) & 1);
+          const int32_t qblk = __ldg(prm.t_col_idx + rs + t);
+          const int32_t qrow = b * prm.N + qblk * kBlock;
+          sm100::mbar_arrive_expect_tx(&sm.q_full[s], 2 * BwdSmem<D>::kTileBytes + 2 * kBlock * 4);
+          sm100::tma_load_3d(sm.q[s], &tmQ, &sm.q_full[s], 0, h, qrow, pol_q);
+          sm100::tma_load_3d(sm.dO[s], &tmDO, &sm.q_full[s], 0, h, qrow, pol_q);
+          sm100::bulk_load(sm.lse[s], prm.lse + bh * prm.N + qblk * kBlock, kBlock * 4, &sm.q_full[s]);
+          sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * kBlock, kBlock * 4, &sm.q_full[s]);
+        }
+        ++n;
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------- MMA issuer
-    if (lane == 0 && nt > 0) {
+    if (lane == 0) {
       constexpr uint32_t idesc_s = sm100::make_idesc_bf16(kBlock, kBlock, false, false);
       constexpr uint32_t idesc_kv = sm100::make_idesc_bf16(kBlock, D, false, true);   // dV, dK
       constexpr uint32_t idesc_q = sm100::make_idesc_bf16(kBlock, D, true, true);     // dQ
       const uint32_t tS = tmem + kColS, tDP = tmem + kColDP, tP = tmem + kColP;
       const uint32_t tDQ = tmem + kColDQ, tDV = tmem + kColDV, tDK = tmem + kColDK;
-      sm100::mbar_wait(&sm.kv_full, 0);
-      for (int t = 0; t < nt; ++t) {
-        const int s = t & 1;
-        sm100::mbar_wait(&sm.q_full[s], (t >> 1) & 1);
-        sm100::tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          sm100::mma_ss(tS, kmajor_desc<D>(sm.k, kk), kmajor_desc<D>(sm.q[s], kk), idesc_s, kk > 0);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          sm100::mma_ss(tDP, kmajor_desc<D>(sm.v, kk), kmajor_desc<D>(sm.dO[s], kk), idesc_s, kk > 0);
-        sm100::mma_commit(&sm.s_full);
-        sm100::mbar_wait(&sm.ds_ready, t & 1);
-        sm100::tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < kBlock / 16; ++kk)
-          sm100::mma_ts(tDV, tP + kk * 8, mnmajor_desc<D>(sm.dO[s], kk), idesc_kv, (t > 0 || kk > 0) ? 1u : 0u);
-#pragma unroll
-        for (int kk = 0; kk < kBlock / 16; ++kk)
-          sm100::mma_ss(tDK, ds_kmajor_desc(sm.ds, kk), mnmajor_desc<D>(sm.q[s], kk), idesc_kv,
-                        (t > 0 || kk > 0) ? 1u : 0u);
-        if (t > 0) {
-          sm100::mbar_wait(&sm.dq_free, (t - 1) & 1);
+      uint32_t n = 0, g = 0;
+      for (int32_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int32_t kb = u % mk;
+        const int32_t nt = __ldg(prm.t_row_ptr + kb + 1) - __ldg(prm.t_row_ptr + kb);
+        if (nt == 0) continue;
+        const int kvs = n & 1;
+        const uint8_t* sk = sm.k[kvs];
+        const uint8_t* sv = sm.v[kvs];
+        sm100::mbar_wait(&sm.kv_full[kvs], (n >> 1) & 1);
+        for (int t = 0; t < nt; ++t, ++g) {
+          const int s = g & 1;
+          sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1);
           sm100::tc_fence_after();
-        }
 #pragma unroll
-        for (int kk = 0; kk < kBlock / 16; ++kk)
-          sm100::mma_ss(tDQ, ds_mnmajor_desc(sm.ds, kk), mnmajor_desc<D>(sm.k, kk), idesc_q, kk > 0);
-        sm100::mma_commit(&sm.q_empty[s]);
-        sm100::mma_commit(&sm.dq_full);
+          for (int kk = 0; kk < D / 16; ++kk)
+            sm100::mma_ss(tS, kmajor_desc<D>(sk, kk), kmajor_desc<D>(sm.q[s], kk), idesc_s, kk > 0);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            sm100::mma_ss(tDP, kmajor_desc<D>(sv, kk), kmajor_desc<D>(sm.dO[s], kk), idesc_s, kk > 0);
+          sm100::mma_commit(&sm.s_full);
+          sm100::mbar_wait(&sm.ds_ready, g & 1);
+          sm100::tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < kBlock / 16; ++kk)
+            sm100::mma_ts(tDV, tP + kk * 8, mnmajor_desc<D>(sm.dO[s], kk), idesc_kv, (t > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+          for (int kk = 0; kk < kBlock / 16; ++kk)
+            sm100::mma_ss(tDK, ds_kmajor_desc(sm.ds, kk), mnmajor_desc<D>(sm.q[s], kk), idesc_kv,
+                          (t > 0 || kk > 0) ? 1u : 0u);
+          if (g > 0) {
+            sm100::mbar_wait(&sm.dq_free, (g - 1) & 1);
+            sm100::tc_fence_after();
+          }
+#pragma unroll
+          for (int kk = 0; kk < kBlock / 16; ++kk)
+            sm100::mma_ss(tDQ, ds_mnmajor_desc(sm.ds, kk), mnmajor_desc<D>(sk, kk), idesc_q, kk > 0);
+          sm100::mma_commit(&sm.q_empty[s]);
+          sm100::mma_commit(&sm.dq_full);
+        }
+        sm100::mma_commit(&sm.kv_empty[kvs]);
+        sm100::mma_commit(&sm.dkv_full);
+        ++n;
       }
-      sm100::mma_commit(&sm.dkv_full);
     }
   } else if (warp < 6) {
     // --------------------------------------------- P^T / dS^T (thread = key row)
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
-    const int32_t kidx = kb * kBlock + row;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = prm.scale_log2, scale = prm.scale;
-    RowBox box;
-    if (nt > 0) box = col_box(prm.pat, kidx);
-    for (int t = 0; t < nt; ++t) {
-      const int s = t & 1;
-      sm100::mbar_wait(&sm.q_full[s], (t >> 1) & 1);
-      sm.lse[s][row] *= kLog2e;                     // LSE in the log2 domain
-      sm100::named_bar_sync(1, 128);
-      sm100::mbar_wait(&sm.s_full, t & 1);
-      sm100::tc_fence_after();
-      const uint8_t kd = __ldg(prm.t_kind + rs + t);
-      const int32_t q0 = __ldg(prm.t_col_idx + rs + t) * kBlock;
-      const float* lse2 = sm.lse[s];
-      const float* dd = sm.dd[s];
+    uint32_t n = 0, g = 0;
+    for (int32_t u = blockIdx.x; u < units; u += gridDim.x) {
+      const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
+      const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
+      const int32_t kidx = kb * kBlock + row;
+      const RowBox box = col_box(prm.pat, kidx);
+      for (int t = 0; t < nt; ++t, ++g) {
+        const int s = g & 1;
+        sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1);
+        sm.lse[s][row] *= kLog2e;                     // LSE in the log2 domain
+        sm100::named_bar_sync(1, 128);
+        sm100::mbar_wait(&sm.s_full, g & 1);
+        sm100::tc_fence_after();
+        const uint8_t kd = __ldg(prm.t_kind + rs + t);
+        const int32_t q0 = __ldg(prm.t_col_idx + rs + t) * kBlock;
+        const float* lse2 = sm.lse[s];
+        const float* dd = sm.dd[s];
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t sr[32], dpr[32];
-        sm100::tmem_ld32(tmem + lane_off + kColS + c * 32, sr);
-        sm100::tmem_ld32(tmem + lane_off + kColDP + c * 32, dpr);
-        sm100::tmem_wait_ld();
-        float p[32], ds[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int qc = c * 32 + e;
-          p[e] = sm100::ex2(fmaf(__uint_as_float(sr[e]), sl2, -lse2[qc]));
-        }
-        if (kd == 2) {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int32_t qq = q0 + c * 32 + e;
-            bool ok;
-            if (!kTwoD) {
-              ok = (uint32_t)(qq - box.lo) < (uint32_t)box.len;
-            } else {
-              const int32_t rq = prm.pat.log2W >= 0 ? (qq >> prm.pat.log2W) : qq / prm.pat.W;
-              const int32_t cq = qq - rq * prm.pat.W;
-              ok = ((uint32_t)(rq - box.lo) < (uint32_t)box.len) && ((uint32_t)(cq - box.c0) < (uint32_t)box.cn);
-            }
-            if (!ok) p[e] = 0.f;
-          }
-        }
-#pragma unroll
-        for (int e = 0; e < 32; ++e) ds[e] = p[e] * scale * (__uint_as_float(dpr[e]) - dd[c * 32 + e]);
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) pk[e] = sm100::pack_bf16(p[2 * e], p[2 * e + 1]);
-        sm100::tmem_st16(tmem + lane_off + kColP + c * 16, pk);
-        // dS^T row -> smem [q/64][kv][64] with the 128B swizzle (16B chunks)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int qc = c * 32 + u * 8;               // first q column of this 16B chunk
-          uint4 w;
-          w.x = sm100::pack_bf16(ds[u * 8 + 0], ds[u * 8 + 1]);
-          w.y = sm100::pack_bf16(ds[u * 8 + 2], ds[u * 8 + 3]);
-          w.z = sm100::pack_bf16(ds[u * 8 + 4], ds[u * 8 + 5]);
-          w.w = sm100::pack_bf16(ds[u * 8 + 6], ds[u * 8 + 7]);
-          const uint32_t off = (uint32_t)(qc >> 6) * 16384u + sm100::swz128((uint32_t)row * 128u + (uint32_t)(qc & 63) * 2u);
-          *reinterpret_cast<uint4*>(sm.ds + off) = w;
-        }
-      }
-      sm100::tmem_wait_st();
-      sm100::fence_proxy_async_smem();
-      sm100::tc_fence_before();
-      sm100::mbar_arrive(&sm.ds_ready);
-    }
-    // final dK, dV rows -> bf16 (dS already carries the softmax scale)
-    const int64_t grow = ((int64_t)b * prm.N + kidx) * prm.heads + h;
-    uint4* dkp = reinterpret_cast<uint4*>(prm.dk + grow * D);
-    uint4* dvp = reinterpret_cast<uint4*>(prm.dv + grow * D);
-    if (nt > 0) {
-      sm100::mbar_wait(&sm.dkv_full, 0);
-      sm100::tc_fence_after();
-#pragma unroll
-      for (int which = 0; which < 2; ++which) {
-        uint4* dst = which == 0 ? dvp : dkp;
-        const uint32_t col = which == 0 ? kColDV : kColDK;
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t r[32];
-          sm100::tmem_ld32(tmem + lane_off + col + c * 32, r);
+        for (int c = 0; c < 4; ++c) {
+          uint32_t sr[32], dpr[32];
+          sm100::tmem_ld32(tmem + lane_off + kColS + c * 32, sr);
+          sm100::tmem_ld32(tmem + lane_off + kColDP + c * 32, dpr);
           sm100::tmem_wait_ld();
+          float p[32];
 #pragma unroll
-          for (int v4 = 0; v4 < 4; ++v4) {
+          for (int e = 0; e < 32; ++e) p[e] = sm100::ex2(fmaf(__uint_as_float(sr[e]), sl2, -lse2[c * 32 + e]));
+          if (kd == 2) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              const int32_t qq = q0 + c * 32 + e;
+              bool ok;
+              if (!kTwoD) {
+                ok = (uint32_t)(qq - box.lo) < (uint32_t)box.len;
+              } else {
+                const int32_t rq = prm.pat.log2W >= 0 ? (qq >> prm.pat.log2W) : qq / prm.pat.W;
+                const int32_t cq = qq - rq * prm.pat.W;
+                ok = ((uint32_t)(rq - box.lo) < (uint32_t)box.len) && ((uint32_t)(cq - box.c0) < (uint32_t)box.cn);
+              }
+              if (!ok) p[e] = 0.f;
+            }
+          }
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) pk[e] = sm100::pack_bf16(p[2 * e], p[2 * e + 1]);
+          sm100::tmem_st16(tmem + lane_off + kColP + c * 16, pk);
+          // dS^T row -> smem [q/64][kv][64] with the 128B swizzle (16B chunks)
+#pragma unroll
+          for (int u4 = 0; u4 < 4; ++u4) {
+            const int qc = c * 32 + u4 * 8;             // first q column of this 16B chunk
+            float ds[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              ds[e] = p[u4 * 8 + e] * scale * (__uint_as_float(dpr[u4 * 8 + e]) - dd[qc + e]);
             uint4 w;
-            w.x = sm100::pack_bf16(__uint_as_float(r[v4 * 8 + 0]), __uint_as_float(r[v4 * 8 + 1]));
-            w.y = sm100::pack_bf16(__uint_as_float(r[v4 * 8 + 2]), __uint_as_float(r[v4 * 8 + 3]));
-            w.z = sm100::pack_bf16(__uint_as_float(r[v4 * 8 + 4]), __uint_as_float(r[v4 * 8 + 5]));
-            w.w = sm100::pack_bf16(__uint_as_float(r[v4 * 8 + 6]), __uint_as_float(r[v4 * 8 + 7]));
-            dst[c * 4 + v4] = w;
+            w.x = sm100::pack_bf16(ds[0], ds[1]);
+            w.y = sm100::pack_bf16(ds[2], ds[3]);
+            w.z = sm100::pack_bf16(ds[4], ds[5]);
+            w.w = sm100::pack_bf16(ds[6], ds[7]);
+            const uint32_t off =
+                (uint32_t)(qc >> 6) * 16384u + sm100::swz128((uint32_t)row * 128u + (uint32_t)(qc & 63) * 2u);
+            *reinterpret_cast<uint4*>(sm.ds + off) = w;
           }
         }
+        sm100::tmem_wait_st();
+        sm100::fence_proxy_async_smem();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&sm.ds_ready);
       }
-    } else {
+      // final dK, dV rows -> bf16 (dS already carries the softmax scale)
+      const int64_t grow = ((int64_t)b * prm.N + kidx) * prm.heads + h;
+      uint4* dkp = reinterpret_cast<uint4*>(prm.dk + grow * D);
+      uint4* dvp = reinterpret_cast<uint4*>(prm.dv + grow * D);
+      if (nt > 0) {
+        sm100::mbar_wait(&sm.dkv_full, n & 1);
+        sm100::tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < D / 8; ++c) {
-        dkp[c] = make_uint4(0, 0, 0, 0);
-        dvp[c] = make_uint4(0, 0, 0, 0);
+        for (int which = 0; which < 2; ++which) {
+          uint4* dst = which == 0 ? dvp : dkp;
+          const uint32_t col = which == 0 ? kColDV : kColDK;
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t r[32];
+            sm100::tmem_ld32(tmem + lane_off + col + c * 32, r);
+            sm100::tmem_wait_ld();
+#pragma unroll
+            for (int v4 = 0; v4 < 4; ++v4) {
+              uint4 w;
+              w.x = sm100::pack_bf16(__uint_as_float(r[v4 * 8 + 0]), __uint_as_float(r[v4 * 8 + 1]));
+              w.y = sm100::pack_bf16(__uint_as_float(r[v4 * 8 + 2]), __uint_as_float(r[v4 * 8 + 3]));
+              w.z = sm100::pack_bf16(__uint_as_float(r[v4 * 8 + 4]), __uint_as_float(r[v4 * 8 + 5]));
+              w.w = sm100::pack_bf16(__uint_as_float(r[v4 * 8 + 6]), __uint_as_float(r[v4 * 8 + 7]));
+              dst[c * 4 + v4] = w;
+            }
+          }
+        }
+        ++n;
+      } else {
+#pragma unroll
+        for (int c = 0; c < D / 8; ++c) {
+          dkp[c] = make_uint4(0, 0, 0, 0);
+          dvp[c] = make_uint4(0, 0, 0, 0);
+        }
       }
+      tiles_done += nt;
     }
   } else {
     // ------------------------------------------ dQ partial -> fp32 accumulator
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    for (int t = 0; t < nt; ++t) {
-      sm100::mbar_wait(&sm.dq_full, t & 1);
-      sm100::tc_fence_after();
-      const int32_t qidx = __ldg(prm.t_col_idx + rs + t) * kBlock + row;
-      float* dst = prm.dq_acc + (((int64_t)b * prm.N + qidx) * prm.heads + h) * D;
+    uint32_t g = 0;
+    for (int32_t u = blockIdx.x; u < units; u += gridDim.x) {
+      const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
+      const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
+      for (int t = 0; t < nt; ++t, ++g) {
+        sm100::mbar_wait(&sm.dq_full, g & 1);
+        sm100::tc_fence_after();
+        const int32_t qidx = __ldg(prm.t_col_idx + rs + t) * kBlock + row;
+        float* dst = prm.dq_acc + (((int64_t)b * prm.N + qidx) * prm.heads + h) * D;
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t r[32];
-        sm100::tmem_ld32(tmem + lane_off + kColDQ + c * 32, r);
-        sm100::tmem_wait_ld();
-        if (c == D / 32 - 1) {
-          sm100::tc_fence_before();
-          sm100::mbar_arrive(&sm.dq_free);   // TMEM dQ tile may be overwritten
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t r[32];
+          sm100::tmem_ld32(tmem + lane_off + kColDQ + c * 32, r);
+          sm100::tmem_wait_ld();
+          if (c == D / 32 - 1) {
+            sm100::tc_fence_before();
+            sm100::mbar_arrive(&sm.dq_free);   // TMEM dQ tile may be overwritten
+          }
+#pragma unroll
+          for (int v4 = 0; v4 < 8; ++v4)
+            red_add_v4(dst + c * 32 + v4 * 4, __uint_as_float(r[v4 * 4 + 0]), __uint_as_float(r[v4 * 4 + 1]),
+                       __uint_as_float(r[v4 * 4 + 2]), __uint_as_float(r[v4 * 4 + 3]));
         }
-#pragma unroll
-        for (int v4 = 0; v4 < 8; ++v4)
-          red_add_v4(dst + c * 32 + v4 * 4, __uint_as_float(r[v4 * 4 + 0]), __uint_as_float(r[v4 * 4 + 1]),
-                     __uint_as_float(r[v4 * 4 + 2]), __uint_as_float(r[v4 * 4 + 3]));
       }
     }
   }
@@ -325,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   sm100::tc_fence_after();
   if (warp == 1) sm100::tmem_dealloc(tmem, kTmemCols);
-  if (threadIdx.x == 0 && prm.visited != nullptr && nt > 0) atomicAdd(prm.visited, (unsigned long long)nt);
+  if (warp == 2 && lane == 0 && prm.visited != nullptr && tiles_done > 0) atomicAdd(prm.visited, tiles_done);
 }
 
 // K7: D = rowsum(dO o O) per (b, q, h) row of head_dim bf16, fp32; dQ accumulator := 0
@@ -378,7 +416,8 @@ hla_status launch_bwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtens
   const size_t smem = sizeof(BwdSmem<D>) + 1024;
   auto* fn = attn_bwd_kernel<D, kTwoD>;
   HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid(n_kblocks, prm.heads, prm.batch);
+  const int64_t units = (int64_t)n_kblocks * prm.heads * prm.batch;
+  const int grid = (int)std::min<int64_t>(units, (int64_t)num_sms());
   fn<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mdo, prm);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;

@@ -51,7 +51,7 @@ struct FwdSmem {
   alignas(1024) uint8_t q[kTileBytes];
   alignas(1024) uint8_t k[2][kTileBytes];
   alignas(1024) uint8_t v[2][kTileBytes];
-  uint64_t q_full, k_full[2], v_full[2], kv_empty[2], s_full, p_full, o_full;
+  uint64_t q_full, q_empty, k_full[2], v_full[2], kv_empty[2], s_full, p_full, o_full;
   uint32_t tmem_base;
 };
 
@@ -69,6 +69,42 @@ __device__ __forceinline__ uint64_t mnmajor_desc(const uint8_t* tile, int kstep)
   return sm100::make_smem_desc(sm100::smem_u32(tile) + kstep * 16 * D * 2, kBlock * D * 2, 8 * D * 2, layout);
 }
 
+// Element mask of a partial tile for query row q (box = row_box(q)), keys k0 .. k0+127.
+template <bool kTwoD>
+__device__ __forceinline__ void apply_row_mask(float (&s)[kBlock], const Pattern& pat, const RowBox& box,
+                                               int32_t k0) {
+  if (!kTwoD) {
+#pragma unroll
+    for (int c = 0; c < kBlock; ++c)
+      if ((uint32_t)(k0 + c - box.lo) >= (uint32_t)box.len) s[c] = -INFINITY;
+  } else if (pat.log2W >= 0) {
+    const int sh = pat.log2W;
+    const int32_t wm = pat.W - 1;
+#pragma unroll
+    for (int c = 0; c < kBlock; ++c) {
+      const int32_t k = k0 + c;
+      const bool ok = ((uint32_t)((k >> sh) - box.lo) < (uint32_t)box.len) &&
+                      ((uint32_t)((k & wm) - box.c0) < (uint32_t)box.cn);
+      if (!ok) s[c] = -INFINITY;
+    }
+  } else {
+    const int32_t W = pat.W;
+#pragma unroll
+    for (int c = 0; c < kBlock; ++c) {
+      const int32_t k = k0 + c;
+      const int32_t rk = k / W, ck = k - rk * W;
+      const bool ok = ((uint32_t)(rk - box.lo) < (uint32_t)box.len) &&
+                      ((uint32_t)(ck - box.c0) < (uint32_t)box.cn);
+      if (!ok) s[c] = -INFINITY;
+    }
+  }
+}
+
+// Persistent: CTA c processes work units c, c + G, c + 2G, ... (unit = q-block,
+// head, batch with the q-block fastest so that CTAs running side by side share
+// K/V tiles in L2).  Barrier phases run on per-CTA counters: n = units with
+// nt > 0 processed so far, g = tiles processed so far.  The next unit's Q and
+// first K/V loads and its first S MMA overlap the current unit's epilogue.
 template <int D, bool kTwoD>
 __global__ void __launch_bounds__(kThreads, 2)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -76,12 +112,12 @@ __global__ void __launch_bounds__(kThreads, 2)
   extern __shared__ uint8_t smem_raw[];
   FwdSmem<D>& sm = *reinterpret_cast<FwdSmem<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int32_t rs = __ldg(prm.row_ptr + qb), nt = __ldg(prm.row_ptr + qb + 1) - rs;
-  const int32_t row0 = b * prm.N + qb * kBlock;  // first token row of this q-block in [B*N]
+  const int32_t mq = prm.N / kBlock;
+  const int32_t units = mq * prm.heads * prm.batch;
 
   if (warp == 0 && lane == 0) {
     sm100::mbar_init(&sm.q_full, 1);
+    sm100::mbar_init(&sm.q_empty, 1);
     for (int s = 0; s < 2; ++s) {
       sm100::mbar_init(&sm.k_full[s], 1);
       sm100::mbar_init(&sm.v_full[s], 1);
@@ -103,27 +139,36 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
+  unsigned long long tiles_done = 0;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0 && nt > 0) {
+    if (lane == 0) {
       const uint64_t pol_q = sm100::policy_evict_first();
       const uint64_t pol_kv = sm100::policy_evict_last();
-      sm100::mbar_arrive_expect_tx(&sm.q_full, FwdSmem<D>::kTileBytes);
-      sm100::tma_load_3d(sm.q, &tmQ, &sm.q_full, 0, h, row0, pol_q);
-      for (int t = 0; t < nt; ++t) {
-        const int s = t & 1;
-        if (t >= 2) sm100::mbar_wait(&sm.kv_empty[s], ((t >> 1) - 1) & 1);
-        const int32_t krow = b * prm.N + __ldg(prm.col_idx + rs + t) * kBlock;
-        sm100::mbar_arrive_expect_tx(&sm.k_full[s], FwdSmem<D>::kTileBytes);
-        sm100::tma_load_3d(sm.k[s], &tmK, &sm.k_full[s], 0, h, krow, pol_kv);
-        sm100::mbar_arrive_expect_tx(&sm.v_full[s], FwdSmem<D>::kTileBytes);
-        sm100::tma_load_3d(sm.v[s], &tmV, &sm.v_full[s], 0, h, krow, pol_kv);
+      uint32_t n = 0, g = 0;
+      for (int32_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int32_t qb = u % mq, h = (u / mq) % prm.heads, b = u / (mq * prm.heads);
+        const int32_t rs = __ldg(prm.row_ptr + qb), nt = __ldg(prm.row_ptr + qb + 1) - rs;
+        if (nt == 0) continue;
+        if (n > 0) sm100::mbar_wait(&sm.q_empty, (n - 1) & 1);
+        sm100::mbar_arrive_expect_tx(&sm.q_full, FwdSmem<D>::kTileBytes);
+        sm100::tma_load_3d(sm.q, &tmQ, &sm.q_full, 0, h, b * prm.N + qb * kBlock, pol_q);
+        for (int t = 0; t < nt; ++t, ++g) {
+          const int s = g & 1;
+          if (g >= 2) sm100::mbar_wait(&sm.kv_empty[s], ((g >> 1) - 1) & 1);
+          const int32_t krow = b * prm.N + __ldg(prm.col_idx + rs + t) * kBlock;
+          sm100::mbar_arrive_expect_tx(&sm.k_full[s], FwdSmem<D>::kTileBytes);
+          sm100::tma_load_3d(sm.k[s], &tmK, &sm.k_full[s], 0, h, krow, pol_kv);
+          sm100::mbar_arrive_expect_tx(&sm.v_full[s], FwdSmem<D>::kTileBytes);
+          sm100::tma_load_3d(sm.v[s], &tmV, &sm.v_full[s], 0, h, krow, pol_kv);
+        }
+        ++n;
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------- MMA issuer
-    if (lane == 0 && nt > 0) {
+    if (lane == 0) {
       constexpr uint32_t idesc_s = sm100::make_idesc_bf16(kBlock, kBlock, false, false);
       constexpr uint32_t idesc_o = sm100::make_idesc_bf16(kBlock, D, false, true);
       const uint32_t tS = tmem + kColS, tP = tmem + kColP, tO = tmem + kColO;
@@ -133,158 +178,152 @@ __global__ void __launch_bounds__(kThreads, 2)
           sm100::mma_ss(tS, kmajor_desc<D>(sm.q, kk), kmajor_desc<D>(sm.k[s], kk), idesc_s, kk > 0);
         sm100::mma_commit(&sm.s_full);
       };
-      sm100::mbar_wait(&sm.q_full, 0);
-      sm100::mbar_wait(&sm.k_full[0], 0);
-      sm100::tc_fence_after();
-      issue_s(0);
-      for (int t = 0; t < nt; ++t) {
-        const int s = t & 1;
-        sm100::mbar_wait(&sm.p_full, t & 1);
-        sm100::mbar_wait(&sm.v_full[s], (t >> 1) & 1);
+      uint32_t n = 0, g = 0;
+      for (int32_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int32_t qb = u % mq;
+        const int32_t nt = __ldg(prm.row_ptr + qb + 1) - __ldg(prm.row_ptr + qb);
+        if (nt == 0) continue;
+        sm100::mbar_wait(&sm.q_full, n & 1);
+        sm100::mbar_wait(&sm.k_full[g & 1], (g >> 1) & 1);
         sm100::tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < kBlock / 16; ++kk)
-          sm100::mma_ts(tO, tP + kk * 8, mnmajor_desc<D>(sm.v[s], kk), idesc_o, (t > 0 || kk > 0) ? 1u : 0u);
-        sm100::mma_commit(&sm.kv_empty[s]);
-        if (t + 1 < nt) {
-          const int s2 = (t + 1) & 1;
-          sm100::mbar_wait(&sm.k_full[s2], ((t + 1) >> 1) & 1);
+        issue_s(g & 1);
+        for (int t = 0; t < nt; ++t, ++g) {
+          const int s = g & 1;
+          sm100::mbar_wait(&sm.p_full, g & 1);
+          sm100::mbar_wait(&sm.v_full[s], (g >> 1) & 1);
           sm100::tc_fence_after();
-          issue_s(s2);
-        } else {
-          sm100::mma_commit(&sm.o_full);
+#pragma unroll
+          for (int kk = 0; kk < kBlock / 16; ++kk)
+            sm100::mma_ts(tO, tP + kk * 8, mnmajor_desc<D>(sm.v[s], kk), idesc_o, (t > 0 || kk > 0) ? 1u : 0u);
+          sm100::mma_commit(&sm.kv_empty[s]);
+          if (t + 1 < nt) {
+            const uint32_t g2 = g + 1;
+            sm100::mbar_wait(&sm.k_full[g2 & 1], (g2 >> 1) & 1);
+            sm100::tc_fence_after();
+            issue_s(g2 & 1);
+          } else {
+            sm100::mma_commit(&sm.q_empty);
+            sm100::mma_commit(&sm.o_full);
+          }
         }
+        ++n;
       }
     }
   } else {
     // ------------------------------------------------- softmax + epilogue
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
-    const int32_t q = qb * kBlock + row;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = prm.scale_log2;
-    float m_ref = -INFINITY, l = 0.f;
-    RowBox box;
-    if (nt > 0) box = row_box(prm.pat, q);
-
-    for (int t = 0; t < nt; ++t) {
-      sm100::mbar_wait(&sm.s_full, t & 1);
-      sm100::tc_fence_after();
-      float s[kBlock];
-      {
-        uint32_t r[32];
+    uint32_t n = 0, g = 0;
+    for (int32_t u = blockIdx.x; u < units; u += gridDim.x) {
+      const int32_t qb = u % mq, h = (u / mq) % prm.heads, b = u / (mq * prm.heads);
+      const int32_t rs = __ldg(prm.row_ptr + qb), nt = __ldg(prm.row_ptr + qb + 1) - rs;
+      const int32_t q = qb * kBlock + row;
+      float m_ref = -INFINITY, l = 0.f;
+      const RowBox box = row_box(prm.pat, q);
+      for (int t = 0; t < nt; ++t, ++g) {
+        sm100::mbar_wait(&sm.s_full, g & 1);
+        sm100::tc_fence_after();
+        float s[kBlock];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
+          uint32_t r[32];
           sm100::tmem_ld32(tmem + lane_off + kColS + c * 32, r);
           sm100::tmem_wait_ld();
 #pragma unroll
           for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(r[e]);
         }
-      }
-      const uint8_t kd = __ldg(prm.kind + rs + t);
-      if (kd == 2) {
-        const int32_t k0 = __ldg(prm.col_idx + rs + t) * kBlock;
-        if (!kTwoD) {
+        if (__ldg(prm.kind + rs + t) == 2)
+          apply_row_mask<kTwoD>(s, prm.pat, box, __ldg(prm.col_idx + rs + t) * kBlock);
+        // row max with 8 independent chains (a single dependent chain costs ~4 cycles x 128)
+        float m8[8];
 #pragma unroll
-          for (int c = 0; c < kBlock; ++c)
-            if ((uint32_t)(k0 + c - box.lo) >= (uint32_t)box.len) s[c] = -INFINITY;
-        } else if (prm.pat.log2W >= 0) {
-          const int sh = prm.pat.log2W;
-          const int32_t wm = prm.pat.W - 1;
+        for (int j = 0; j < 8; ++j) m8[j] = s[j];
 #pragma unroll
-          for (int c = 0; c < kBlock; ++c) {
-            const int32_t k = k0 + c;
-            const bool ok = ((uint32_t)((k >> sh) - box.lo) < (uint32_t)box.len) &&
-                            ((uint32_t)((k & wm) - box.c0) < (uint32_t)box.cn);
-            if (!ok) s[c] = -INFINITY;
-          }
-        } else {
-          const int32_t W = prm.pat.W;
+        for (int c = 8; c < kBlock; ++c) m8[c & 7] = fmaxf(m8[c & 7], s[c]);
 #pragma unroll
-          for (int c = 0; c < kBlock; ++c) {
-            const int32_t k = k0 + c;
-            const int32_t rk = k / W, ck = k - rk * W;
-            const bool ok = ((uint32_t)(rk - box.lo) < (uint32_t)box.len) &&
-                            ((uint32_t)(ck - box.c0) < (uint32_t)box.cn);
-            if (!ok) s[c] = -INFINITY;
+        for (int j = 4; j > 0; j >>= 1)
+#pragma unroll
+          for (int i = 0; i < j; ++i) m8[i] = fmaxf(m8[i], m8[i + j]);
+        const float m_tile = m8[0] * sl2;
+        // lazy rescale (exact): keep the reference max unless it grew by > 8 (x256)
+        const float m_new = (m_tile > m_ref + 8.f) ? m_tile : m_ref;
+        const float alpha = (m_new == m_ref) ? 1.f : sm100::ex2(m_ref - m_new);
+        if (__any_sync(0xffffffffu, t > 0 && alpha != 1.f)) {
+          // O of the previous tiles is final in TMEM: s_full(t) was committed after PV(t-1)
+#pragma unroll
+          for (int c = 0; c < D / 16; ++c) {
+            uint32_t o[16];
+            sm100::tmem_ld16(tmem + lane_off + kColO + c * 16, o);
+            sm100::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            sm100::tmem_st16(tmem + lane_off + kColO + c * 16, o);
           }
         }
-      }
-      float mx = s[0];
+        m_ref = m_new;
+        l *= alpha;
+        const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
+        float l4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int c = 1; c < kBlock; ++c) mx = fmaxf(mx, s[c]);
-      const float m_tile = mx * sl2;
-      // lazy rescale (exact): keep the reference max unless it grew by > 8 (x256)
-      const float m_new = (m_tile > m_ref + 8.f) ? m_tile : m_ref;
-      const float alpha = (m_new == m_ref) ? 1.f : sm100::ex2(m_ref - m_new);
-      if (__any_sync(0xffffffffu, t > 0 && alpha != 1.f)) {
-        uint32_t o[32];
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float p0 = sm100::ex2(fmaf(s[c * 32 + 2 * e], sl2, -m_use));
+            const float p1 = sm100::ex2(fmaf(s[c * 32 + 2 * e + 1], sl2, -m_use));
+            l4[e & 3] += p0 + p1;
+            pk[e] = sm100::pack_bf16(p0, p1);
+          }
+          sm100::tmem_st16(tmem + lane_off + kColP + c * 16, pk);
+        }
+        l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
+        sm100::tmem_wait_st();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&sm.p_full);
+      }
+
+      // epilogue: O / l -> bf16 row, LSE (natural log)
+      const int64_t orow = ((int64_t)b * prm.N + q) * prm.heads + h;
+      uint4* optr = reinterpret_cast<uint4*>(prm.o + orow * D);
+      const float inv_l = l > 0.f ? 1.f / l : 0.f;
+      if (nt > 0) {
+        sm100::mbar_wait(&sm.o_full, n & 1);
+        sm100::tc_fence_after();
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
+          uint32_t o[32];
           sm100::tmem_ld32(tmem + lane_off + kColO + c * 32, o);
           sm100::tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-          sm100::tmem_st32(tmem + lane_off + kColO + c * 32, o);
+          for (int v4 = 0; v4 < 4; ++v4) {
+            uint4 w;
+            w.x = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 0]) * inv_l, __uint_as_float(o[v4 * 8 + 1]) * inv_l);
+            w.y = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 2]) * inv_l, __uint_as_float(o[v4 * 8 + 3]) * inv_l);
+            w.z = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 4]) * inv_l, __uint_as_float(o[v4 * 8 + 5]) * inv_l);
+            w.w = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 6]) * inv_l, __uint_as_float(o[v4 * 8 + 7]) * inv_l);
+            optr[c * 4 + v4] = w;
+          }
         }
-        sm100::tmem_wait_st();
+        // TMEM O may now be overwritten by the next unit's first PV (it waits p_full)
+        ++n;
+      } else {
+#pragma unroll
+        for (int c = 0; c < D / 8; ++c) optr[c] = make_uint4(0, 0, 0, 0);
       }
-      m_ref = m_new;
-      l *= alpha;
       const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        uint32_t pk[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const float p0 = sm100::ex2(fmaf(s[half * 64 + 2 * e], sl2, -m_use));
-          const float p1 = sm100::ex2(fmaf(s[half * 64 + 2 * e + 1], sl2, -m_use));
-          l += p0 + p1;
-          pk[e] = sm100::pack_bf16(p0, p1);
-        }
-        sm100::tmem_st32(tmem + lane_off + kColP + half * 32, pk);
-      }
-      sm100::tmem_wait_st();
-      sm100::tc_fence_before();
-      sm100::mbar_arrive(&sm.p_full);
+      prm.lse[((int64_t)b * prm.heads + h) * prm.N + q] =
+          l > 0.f ? (m_use + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+      tiles_done += nt;
     }
-
-    // epilogue: O / l -> bf16 row, LSE (natural log)
-    const int64_t orow = ((int64_t)b * prm.N + q) * prm.heads + h;
-    uint4* optr = reinterpret_cast<uint4*>(prm.o + orow * D);
-    const float inv_l = l > 0.f ? 1.f / l : 0.f;
-    if (nt > 0) {
-      sm100::mbar_wait(&sm.o_full, 0);
-      sm100::tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t o[32];
-        sm100::tmem_ld32(tmem + lane_off + kColO + c * 32, o);
-        sm100::tmem_wait_ld();
-#pragma unroll
-        for (int v4 = 0; v4 < 4; ++v4) {
-          uint4 w;
-          w.x = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 0]) * inv_l, __uint_as_float(o[v4 * 8 + 1]) * inv_l);
-          w.y = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 2]) * inv_l, __uint_as_float(o[v4 * 8 + 3]) * inv_l);
-          w.z = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 4]) * inv_l, __uint_as_float(o[v4 * 8 + 5]) * inv_l);
-          w.w = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 6]) * inv_l, __uint_as_float(o[v4 * 8 + 7]) * inv_l);
-          optr[c * 4 + v4] = w;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int c = 0; c < D / 8; ++c) optr[c] = make_uint4(0, 0, 0, 0);
-    }
-    const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
-    prm.lse[((int64_t)b * prm.heads + h) * prm.N + q] =
-        l > 0.f ? (m_use + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
   }
 
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
   if (warp == 1) sm100::tmem_dealloc(tmem, kTmemCols);
-  if (threadIdx.x == 0 && prm.visited != nullptr && nt > 0) atomicAdd(prm.visited, (unsigned long long)nt);
+  if (warp == 2 && lane == 0 && prm.visited != nullptr && tiles_done > 0) atomicAdd(prm.visited, tiles_done);
 }
 
 template <int D, bool kTwoD>
@@ -293,7 +332,8 @@ hla_status launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtens
   const size_t smem = sizeof(FwdSmem<D>) + 1024;
   auto* fn = attn_fwd_kernel<D, kTwoD>;
   HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid(n_qblocks, prm.heads, prm.batch);
+  const int64_t units = (int64_t)n_qblocks * prm.heads * prm.batch;
+  const int grid = (int)std::min<int64_t>(units, 2 * (int64_t)num_sms());
   fn<<<grid, kThreads, smem, stream>>>(mq, mk, mv, prm);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;

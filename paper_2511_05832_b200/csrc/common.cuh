@@ -55,6 +55,18 @@ hla_status make_pattern(const hla_pattern_desc* d, Pattern* p);
 hla_status check_attn_args(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
                            int32_t head_dim, Pattern* pat);
 
+// number of SMs of the current device (cached per process; B200: 148)
+inline int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 inline bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
 inline int ilog2(int64_t x) { int l = 0; while ((1ll << l) < x) ++l; return l; }
 
