@@ -175,12 +175,19 @@ HLA_API hla_status hla_mask_ratios(const hla_pattern_desc* d, const int64_t coun
  * tiles_visited: optional device int64 counter; when non-NULL the kernel adds
  * the number of tiles it executed (must equal batch*heads*nnz: empty tiles are
  * skipped).
+ * seq_to_cell: NULL -> q, k, v, o are in the sequence order of d->order.
+ * Non-NULL (Hilbert patterns only; 16-byte aligned device int32[N] from
+ * hla_hilbert_index) -> FUSED REORDER: q, k, v, o are in GRID (row-major cell)
+ * order; the kernel gathers each 128-token Hilbert tile with TMA .tile::gather4
+ * row loads and writes O rows back to their grid cells, so the separate
+ * "Reshape" passes of P:L196 disappear.  LSE stays in
+ * sequence order.
  */
 HLA_API hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_mask* m,
                         int32_t batch, int32_t heads, int32_t head_dim, float scale,
                         const void* q, const void* k, const void* v,
-                        void* o, float* lse, int64_t* tiles_visited,
-                        cudaStream_t stream);
+                        void* o, float* lse, const int32_t* seq_to_cell,
+                        int64_t* tiles_visited, cudaStream_t stream);
 
 /* ---------------------------------------------------------------------------
  * hla_attn_bwd -- backward of hla_attn_fwd over the transposed lists.
@@ -191,12 +198,13 @@ HLA_API hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_mask*
  * bytes, 256-byte aligned (fp32 dQ accumulator + D); its contents need not be
  * initialised.  dQ accumulation uses fp32 atomics (summation order is not
  * deterministic; covered by the stated tolerance).  Same limits as the forward.
+ * seq_to_cell: as in hla_attn_fwd (fused reorder: every bf16 tensor in grid order).
  */
 HLA_API hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_mask* m,
                         int32_t batch, int32_t heads, int32_t head_dim, float scale,
                         const void* q, const void* k, const void* v, const void* o,
                         const float* lse, const void* dout,
-                        void* dq, void* dk, void* dv,
+                        void* dq, void* dk, void* dv, const int32_t* seq_to_cell,
                         void* workspace, size_t workspace_bytes,
                         int64_t* tiles_visited, cudaStream_t stream);
 
@@ -209,12 +217,12 @@ HLA_API hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_mask*
  *               accumulates dQ (fp32, red.global.add)
  *   finalize  : dQ = bf16(accumulator)                                        */
 HLA_API hla_status hla_attn_bwd_preprocess(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,
-                                   const void* o, const void* dout, void* workspace,
-                                   size_t workspace_bytes, cudaStream_t stream);
+                                   const void* o, const void* dout, const int32_t* seq_to_cell,
+                                   void* workspace, size_t workspace_bytes, cudaStream_t stream);
 HLA_API hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_block_mask* m,
                              int32_t batch, int32_t heads, int32_t head_dim, float scale,
                              const void* q, const void* k, const void* v, const float* lse,
-                             const void* dout, void* dk, void* dv,
+                             const void* dout, void* dk, void* dv, const int32_t* seq_to_cell,
                              void* workspace, size_t workspace_bytes,
                              int64_t* tiles_visited, cudaStream_t stream);
 HLA_API hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,

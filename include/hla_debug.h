@@ -23,6 +23,14 @@ extern "C" {
 HLA_API hla_status hla_debug_umma(const void* A, const void* B, float* C, int32_t M, int32_t N, int32_t K,
                           int32_t a_major_mn, int32_t b_major_mn, int32_t a_from_tmem, cudaStream_t stream);
 
+/* hla_debug_gather4: 128 token rows idx[0..127] (row = batch*N + token) of head `head`
+ * of a bf16 [rows, heads, head_dim] tensor, loaded with TMA .tile::gather4 into a
+ * swizzled shared-memory tile and written back unswizzled to out[128][head_dim].
+ * box_h: second box dimension of the 2-D tensor map (bring-up parameter). */
+HLA_API hla_status hla_debug_gather4(const void* src, int64_t rows, int32_t heads, int32_t head_dim,
+                                     const int32_t* idx, int32_t head, int32_t box_h, void* out,
+                                     cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

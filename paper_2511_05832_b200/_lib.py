@@ -18,7 +18,7 @@ STATUS_NAMES = {0: "HLA_OK", 1: "HLA_ERR_INVALID", 2: "HLA_ERR_UNSUPPORTED", 3: 
 EXPORTED = ("hla_hilbert_index", "hla_hilbert_perm", "hla_build_block_mask", "hla_mask_ratios",
             "hla_attn_fwd", "hla_attn_bwd", "hla_attn_bwd_workspace", "hla_attn_bwd_preprocess",
             "hla_attn_bwd_main", "hla_attn_bwd_finalize", "hla_last_error", "hla_version",
-            "hla_debug_umma")
+            "hla_debug_umma", "hla_debug_gather4")
 
 
 class PatternDesc(ctypes.Structure):
@@ -58,12 +58,13 @@ def lib():
         "hla_build_block_mask": [pdesc, pmask, ctypes.POINTER(i64), vp],
         "hla_mask_ratios": [pdesc, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double),
                             ctypes.POINTER(ctypes.c_double)],
-        "hla_attn_fwd": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp],
-        "hla_attn_bwd": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp],
-        "hla_attn_bwd_preprocess": [i32, i32, i32, i32, vp, vp, vp, sz, vp],
-        "hla_attn_bwd_main": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp],
+        "hla_attn_fwd": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp],
+        "hla_attn_bwd": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp],
+        "hla_attn_bwd_preprocess": [i32, i32, i32, i32, vp, vp, vp, vp, sz, vp],
+        "hla_attn_bwd_main": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp],
         "hla_attn_bwd_finalize": [i32, i32, i32, i32, vp, sz, vp, vp],
         "hla_debug_umma": [vp, vp, vp, i32, i32, i32, i32, i32, i32, vp],
+        "hla_debug_gather4": [vp, i64, i32, i32, vp, i32, i32, vp, vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)

@@ -127,8 +127,10 @@ def hla_build_block_mask(desc, device="cuda", stream=None):
     return m
 
 
-def hla_attn_fwd(desc, mask, q, k, v, scale=0.0, o=None, lse=None, tiles_visited=None, stream=None):
-    """q, k, v: bf16 [B, N, heads, d] in desc's sequence order -> (o, lse [B, heads, N] fp32)."""
+def hla_attn_fwd(desc, mask, q, k, v, scale=0.0, o=None, lse=None, tiles_visited=None, seq_to_cell=None,
+                 stream=None):
+    """q, k, v: bf16 [B, N, heads, d] in desc's sequence order -> (o, lse [B, heads, N] fp32).
+    seq_to_cell (int32 [N] from hla_hilbert_index): fused reorder -- q, k, v, o in grid order."""
     B, N, H, D = q.shape
     for t in (q, k, v):
         assert t.dtype == torch.bfloat16 and t.is_cuda and t.is_contiguous() and t.shape == q.shape
@@ -138,8 +140,8 @@ def hla_attn_fwd(desc, mask, q, k, v, scale=0.0, o=None, lse=None, tiles_visited
         lse = torch.empty(B, H, N, dtype=torch.float32, device=q.device)
     mc = mask.c
     check("hla_attn_fwd", lib().hla_attn_fwd(ctypes.byref(desc), ctypes.byref(mc), B, H, D, float(scale),
-                                             _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(tiles_visited),
-                                             _stream(stream)))
+                                             _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(seq_to_cell),
+                                             _ptr(tiles_visited), _stream(stream)))
     return o, lse
 
 
@@ -148,7 +150,7 @@ def hla_attn_bwd_workspace(B, H, N, D):
 
 
 def hla_attn_bwd(desc, mask, q, k, v, o, lse, dout, scale=0.0, dq=None, dk=None, dv=None, workspace=None,
-                 tiles_visited=None, stream=None):
+                 tiles_visited=None, seq_to_cell=None, stream=None):
     B, N, H, D = q.shape
     dq = torch.empty_like(q) if dq is None else dq
     dk = torch.empty_like(k) if dk is None else dk
@@ -159,25 +161,26 @@ def hla_attn_bwd(desc, mask, q, k, v, o, lse, dout, scale=0.0, dq=None, dk=None,
     mc = mask.c
     check("hla_attn_bwd", lib().hla_attn_bwd(ctypes.byref(desc), ctypes.byref(mc), B, H, D, float(scale),
                                              _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(dout),
-                                             _ptr(dq), _ptr(dk), _ptr(dv), _ptr(workspace), workspace.numel(),
-                                             _ptr(tiles_visited), _stream(stream)))
+                                             _ptr(dq), _ptr(dk), _ptr(dv), _ptr(seq_to_cell), _ptr(workspace),
+                                             workspace.numel(), _ptr(tiles_visited), _stream(stream)))
     return dq, dk, dv
 
 
-def hla_attn_bwd_preprocess(o, dout, workspace, stream=None):
+def hla_attn_bwd_preprocess(o, dout, workspace, seq_to_cell=None, stream=None):
     B, N, H, D = o.shape
-    check("hla_attn_bwd_preprocess", lib().hla_attn_bwd_preprocess(B, H, N, D, _ptr(o), _ptr(dout), _ptr(workspace),
-                                                                   workspace.numel(), _stream(stream)))
+    check("hla_attn_bwd_preprocess", lib().hla_attn_bwd_preprocess(B, H, N, D, _ptr(o), _ptr(dout), _ptr(seq_to_cell),
+                                                                   _ptr(workspace), workspace.numel(),
+                                                                   _stream(stream)))
 
 
 def hla_attn_bwd_main(desc, mask, q, k, v, lse, dout, dk, dv, workspace, scale=0.0, tiles_visited=None,
-                      stream=None):
+                      seq_to_cell=None, stream=None):
     B, N, H, D = q.shape
     mc = mask.c
     check("hla_attn_bwd_main", lib().hla_attn_bwd_main(ctypes.byref(desc), ctypes.byref(mc), B, H, D, float(scale),
                                                        _ptr(q), _ptr(k), _ptr(v), _ptr(lse), _ptr(dout), _ptr(dk),
-                                                       _ptr(dv), _ptr(workspace), workspace.numel(),
-                                                       _ptr(tiles_visited), _stream(stream)))
+                                                       _ptr(dv), _ptr(seq_to_cell), _ptr(workspace),
+                                                       workspace.numel(), _ptr(tiles_visited), _stream(stream)))
 
 
 def hla_attn_bwd_finalize(workspace, dq, stream=None):
@@ -191,6 +194,15 @@ def hla_debug_umma(A, B, M, N, K, a_mn=False, b_mn=False, a_tmem=False, stream=N
     check("hla_debug_umma", lib().hla_debug_umma(_ptr(A), _ptr(B), _ptr(C), M, N, K, int(a_mn), int(b_mn),
                                                  int(a_tmem), _stream(stream)))
     return C
+
+
+def hla_debug_gather4(src, idx, head, box_h=1, stream=None):
+    """src: bf16 [rows, heads, d]; idx: int32[128] row indices -> bf16 [128, d] (TMA gather4 bring-up)."""
+    rows, heads, d = src.shape
+    out = torch.empty(128, d, dtype=torch.bfloat16, device=src.device)
+    check("hla_debug_gather4", lib().hla_debug_gather4(_ptr(src), rows, heads, d, _ptr(idx), head, box_h, _ptr(out),
+                                                       _stream(stream)))
+    return out
 
 
 def version():

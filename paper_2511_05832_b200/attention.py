@@ -11,6 +11,13 @@ graph):
     backward: perm(dO -> Hilbert) ; hla_attn_bwd ; perm(dq,dk,dv -> grid)
   Row-major baselines (WSA / SA / NA2D / DENSE) run the same attention kernels
   directly on grid order.
+
+With fused=True (default for Hilbert patterns) the reorder is fused into the
+attention kernels: they gather Hilbert tiles straight from
+the grid-order tensors (TMA .tile::gather4 through the cached seq_to_cell path)
+and scatter O / dK / dV / dQ rows back to their grid cells, so a step is
+fwd ; bwd_pre ; bwd ; bwd_fin with no permutation passes.  fused=False keeps the
+explicit hla_hilbert_perm passes (the paper's "Reshape" step).
 """
 
 import torch
@@ -20,7 +27,7 @@ from . import api
 
 class HilbertLocalAttention:
     def __init__(self, kind, grid_h, grid_w, win_h=1, win_w=1, batch=1, heads=1, head_dim=64, block=128,
-                 shift=0, scale=0.0, device="cuda"):
+                 shift=0, scale=0.0, device="cuda", fused=True):
         self.kind = kind
         self.grid_h, self.grid_w = grid_h, grid_w
         self.N = grid_h * grid_w
@@ -35,7 +42,11 @@ class HilbertLocalAttention:
         self.lse = torch.empty(batch, heads, self.N, dtype=torch.float32, device=device)
         self.workspace = torch.empty(api.hla_attn_bwd_workspace(batch, heads, self.N, head_dim),
                                      dtype=torch.uint8, device=device)
-        if self.hilbert:
+        self.fused = bool(fused) and self.hilbert
+        self.s2c = None
+        if self.fused:
+            self.s2c, _ = api.hla_hilbert_index(grid_h, grid_w, device)     # the cached path
+        elif self.hilbert:
             self.qs, self.ks, self.vs, self.os = e(), e(), e(), e()
             self.dos, self.dqs, self.dks, self.dvs = e(), e(), e(), e()
         self._saved = None
@@ -50,7 +61,11 @@ class HilbertLocalAttention:
 
         mark: optional callable(name) invoked after each launch (bench timing hook)."""
         mark = mark or _nop
-        if self.hilbert:
+        if self.fused:
+            api.hla_attn_fwd(self.desc, self.mask, q, k, v, self.scale, self.o, self.lse, seq_to_cell=self.s2c)
+            mark("fwd")
+            self._saved = (q, k, v, self.o)
+        elif self.hilbert:
             api.hla_hilbert_perm(self.grid_h, self.grid_w, api.TO_HILBERT, (q, k, v), (self.qs, self.ks, self.vs))
             mark("perm_qkv")
             api.hla_attn_fwd(self.desc, self.mask, self.qs, self.ks, self.vs, self.scale, self.os, self.lse)
@@ -68,19 +83,20 @@ class HilbertLocalAttention:
         """dout: bf16 [B, N, heads, d] in grid order -> (dq, dk, dv) in grid order."""
         mark = mark or _nop
         q, k, v, o = self._saved
-        if self.hilbert:
+        if self.hilbert and not self.fused:
             api.hla_hilbert_perm(self.grid_h, self.grid_w, api.TO_HILBERT, (dout,), (self.dos,))
             mark("perm_do")
             dout_s, dq, dk, dv = self.dos, self.dqs, self.dks, self.dvs
         else:
             dout_s, dq, dk, dv = dout, self.dq, self.dk, self.dv
-        api.hla_attn_bwd_preprocess(o, dout_s, self.workspace)
+        api.hla_attn_bwd_preprocess(o, dout_s, self.workspace, seq_to_cell=self.s2c)
         mark("bwd_pre")
-        api.hla_attn_bwd_main(self.desc, self.mask, q, k, v, self.lse, dout_s, dk, dv, self.workspace, self.scale)
+        api.hla_attn_bwd_main(self.desc, self.mask, q, k, v, self.lse, dout_s, dk, dv, self.workspace, self.scale,
+                              seq_to_cell=self.s2c)
         mark("bwd")
         api.hla_attn_bwd_finalize(self.workspace, dq)
         mark("bwd_fin")
-        if self.hilbert:
+        if self.hilbert and not self.fused:
             api.hla_hilbert_perm(self.grid_h, self.grid_w, api.FROM_HILBERT, (self.dqs, self.dks, self.dvs),
                                  (self.dq, self.dk, self.dv))
             mark("perm_grads")
@@ -89,7 +105,7 @@ class HilbertLocalAttention:
     # kernel launches per step (forward + backward)
     @property
     def launches_per_step(self):
-        return 8 if self.hilbert else 4
+        return 8 if (self.hilbert and not self.fused) else 4
 
     def step(self, q, k, v, dout, mark=None):
         """One pass of the whole hot path: forward then backward."""

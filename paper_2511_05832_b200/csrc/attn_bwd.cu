@@ -44,7 +44,8 @@ struct BwdParams {
   const uint8_t* t_kind;
   const float* lse;        // [B, H, N]
   const float* dsum;       // D, [B, H, N]
-  float* dq_acc;           // [B, N, H, Dh] fp32
+  float* dq_acc;           // [B, N, H, Dh] fp32 (grid order when s2c != null)
+  const int32_t* s2c;      // fused reorder: seq_to_cell table (tensors in grid order), else null
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;
   unsigned long long* visited;
@@ -84,6 +85,21 @@ __device__ __forceinline__ uint64_t ds_mnmajor_desc(const uint8_t* ds, int kstep
   return sm100::make_smem_desc(sm100::smem_u32(ds) + kstep * 2048, 16384, 1024, sm100::kSwizzle128B);
 }
 
+// Load the 128 token rows [seq0, seq0 + 128) (sequence order) of head h, batch b;
+// see attn_fwd.cu load_rows (kGather = fused reorder through s2c with .tile::gather4).
+template <int D, bool kGather>
+__device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int32_t h,
+                                          int32_t b, int32_t N, int32_t seq0, const int32_t* s2c, uint64_t pol,
+                                          int lane) {
+  if (kGather) {
+    const int4 c = __ldg(reinterpret_cast<const int4*>(s2c + seq0) + lane);
+    const int32_t base = b * N;
+    sm100::tma_gather4(dst + lane * 4 * D * 2, map, bar, h * D, base + c.x, base + c.y, base + c.z, base + c.w, pol);
+  } else if (lane == 0) {
+    sm100::tma_load_3d(dst, map, bar, 0, h, b * N + seq0, pol);
+  }
+}
+
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
                : "memory");
@@ -94,7 +110,7 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
 // next unit's K/V (and first Q/dO) stream in while the current unit computes;
 // the dK/dV epilogue of a unit overlaps the first S/dP MMAs of the next one.
 // Phase counters: n = units with nt > 0 so far, g = (q-block) tiles so far.
-template <int D, bool kTwoD>
+template <int D, bool kTwoD, bool kGather>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -135,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
+    {
       const uint64_t pol_kv = sm100::policy_evict_first();
       const uint64_t pol_q = sm100::policy_evict_last();
       uint32_t n = 0, g = 0;
@@ -146,20 +162,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t bh = (int64_t)b * prm.heads + h;
         const int kvs = n & 1;
         if (n >= 2) sm100::mbar_wait(&sm.kv_empty[kvs], ((n >> 1) - 1) & 1);
-        const int32_t krow = b * prm.N + kb * kBlock;
-        sm100::mbar_arrive_expect_tx(&sm.kv_full[kvs], 2 * BwdSmem<D>::kTileBytes);
-        sm100::tma_load_3d(sm.k[kvs], &tmK, &sm.kv_full[kvs], 0, h, krow, pol_kv);
-        sm100::tma_load_3d(sm.v[kvs], &tmV, &sm.kv_full[kvs], 0, h, krow, pol_kv);
+        if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.kv_full[kvs], 2 * BwdSmem<D>::kTileBytes);
+        __syncwarp();
+        load_rows<D, kGather>(sm.k[kvs], &tmK, &sm.kv_full[kvs], h, b, prm.N, kb * kBlock, prm.s2c, pol_kv, lane);
+        load_rows<D, kGather>(sm.v[kvs], &tmV, &sm.kv_full[kvs], h, b, prm.N, kb * kBlock, prm.s2c, pol_kv, lane);
         for (int t = 0; t < nt; ++t, ++g) {
           const int s = g & 1;
           if (g >= 2) sm100::mbar_wait(&sm.q_empty[s], ((g >> 1) - 1) & 1);
           const int32_t qblk = __ldg(prm.t_col_idx + rs + t);
-          const int32_t qrow = b * prm.N + qblk * kBlock;
-          sm100::mbar_arrive_expect_tx(&sm.q_full[s], 2 * BwdSmem<D>::kTileBytes + 2 * kBlock * 4);
-          sm100::tma_load_3d(sm.q[s], &tmQ, &sm.q_full[s], 0, h, qrow, pol_q);
-          sm100::tma_load_3d(sm.dO[s], &tmDO, &sm.q_full[s], 0, h, qrow, pol_q);
-          sm100::bulk_load(sm.lse[s], prm.lse + bh * prm.N + qblk * kBlock, kBlock * 4, &sm.q_full[s]);
-          sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * kBlock, kBlock * 4, &sm.q_full[s]);
+          if (lane == 0) {
+            sm100::mbar_arrive_expect_tx(&sm.q_full[s], 2 * BwdSmem<D>::kTileBytes + 2 * kBlock * 4);
+            sm100::bulk_load(sm.lse[s], prm.lse + bh * prm.N + qblk * kBlock, kBlock * 4, &sm.q_full[s]);
+            sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * kBlock, kBlock * 4, &sm.q_full[s]);
+          }
+          __syncwarp();
+          load_rows<D, kGather>(sm.q[s], &tmQ, &sm.q_full[s], h, b, prm.N, qblk * kBlock, prm.s2c, pol_q, lane);
+          load_rows<D, kGather>(sm.dO[s], &tmDO, &sm.q_full[s], h, b, prm.N, qblk * kBlock, prm.s2c, pol_q, lane);
         }
         ++n;
       }
@@ -291,7 +309,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         sm100::mbar_arrive(&sm.ds_ready);
       }
       // final dK, dV rows -> bf16 (dS already carries the softmax scale)
-      const int64_t grow = ((int64_t)b * prm.N + kidx) * prm.heads + h;
+      const int32_t kcell = kGather ? __ldg(prm.s2c + kidx) : kidx;   // fused inverse reorder of dK, dV
+      const int64_t grow = ((int64_t)b * prm.N + kcell) * prm.heads + h;
       uint4* dkp = reinterpret_cast<uint4*>(prm.dk + grow * D);
       uint4* dvp = reinterpret_cast<uint4*>(prm.dv + grow * D);
       if (nt > 0) {
@@ -340,7 +359,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         sm100::mbar_wait(&sm.dq_full, g & 1);
         sm100::tc_fence_after();
         const int32_t qidx = __ldg(prm.t_col_idx + rs + t) * kBlock + row;
-        float* dst = prm.dq_acc + (((int64_t)b * prm.N + qidx) * prm.heads + h) * D;
+        const int32_t qcell = kGather ? __ldg(prm.s2c + qidx) : qidx;   // dQ accumulated in grid order
+        float* dst = prm.dq_acc + (((int64_t)b * prm.N + qcell) * prm.heads + h) * D;
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
           uint32_t r[32];
@@ -366,19 +386,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2 && lane == 0 && prm.visited != nullptr && tiles_done > 0) atomicAdd(prm.visited, tiles_done);
 }
 
-// K7: D = rowsum(dO o O) per (b, q, h) row of head_dim bf16, fp32; dQ accumulator := 0
+// K7: D = rowsum(dO o O) per (b, s, h) row of head_dim bf16, fp32, in sequence order s
+// (rows read at grid cell s2c[s] under the fused reorder); dQ accumulator := 0
 template <int D>
 __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
                                                              const __nv_bfloat16* __restrict__ dout,
                                                              float* __restrict__ dsum, float* __restrict__ dq_acc,
-                                                             int32_t N, int32_t heads, int64_t rows) {
+                                                             const int32_t* __restrict__ s2c, int32_t N,
+                                                             int32_t heads, int64_t rows) {
   constexpr int kLanes = D / 8;   // lanes per row, 16 B (8 bf16) each
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t r = gid / kLanes;
+  const int64_t r = gid / kLanes;             // sequence-order row (b * N + s) * heads + h
   const int part = (int)(gid % kLanes);
   if (r >= rows) return;
-  const uint4 a = *reinterpret_cast<const uint4*>(o + r * D + part * 8);
-  const uint4 g = *reinterpret_cast<const uint4*>(dout + r * D + part * 8);
+  const int64_t hq = r % heads, bs = r / heads;
+  const int64_t s = bs % N, bb = bs / N;
+  const int64_t src = s2c ? ((bb * N + __ldg(s2c + s)) * heads + hq) : r;
+  const uint4 a = *reinterpret_cast<const uint4*>(o + src * D + part * 8);
+  const uint4 g = *reinterpret_cast<const uint4*>(dout + src * D + part * 8);
   const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
   const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&g);
   float acc = 0.f;
@@ -390,15 +415,10 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
   }
 #pragma unroll
   for (int o2 = kLanes / 2; o2 > 0; o2 >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o2);
-  float4* z = reinterpret_cast<float4*>(dq_acc + r * D + part * 8);
+  float4* z = reinterpret_cast<float4*>(dq_acc + r * D + part * 8);   // zeroing is layout-agnostic
   z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
   z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (part == 0) {
-    // row r = (b * N + q) * heads + h  ->  D[b, h, q]
-    const int64_t hq = r % heads, bq = r / heads;
-    const int64_t q = bq % N, bb = bq / N;
-    dsum[(bb * heads + hq) * N + q] = acc;
-  }
+  if (part == 0) dsum[(bb * heads + hq) * N + s] = acc;
 }
 
 // K9: dQ = bf16(accumulator)
@@ -410,11 +430,11 @@ __global__ void __launch_bounds__(256) dq_finalize_kernel(const float4* __restri
   }
 }
 
-template <int D, bool kTwoD>
+template <int D, bool kTwoD, bool kGather>
 hla_status launch_bwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mdo,
                       const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream) {
   const size_t smem = sizeof(BwdSmem<D>) + 1024;
-  auto* fn = attn_bwd_kernel<D, kTwoD>;
+  auto* fn = attn_bwd_kernel<D, kTwoD, kGather>;
   HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t units = (int64_t)n_kblocks * prm.heads * prm.batch;
   const int grid = (int)std::min<int64_t>(units, (int64_t)num_sms());
@@ -452,8 +472,8 @@ hla_status carve_workspace(int32_t batch, int32_t heads, int32_t n, int32_t head
 }  // namespace
 
 extern "C" hla_status hla_attn_bwd_preprocess(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,
-                                              const void* o, const void* dout, void* workspace,
-                                              size_t workspace_bytes, cudaStream_t stream) {
+                                              const void* o, const void* dout, const int32_t* seq_to_cell,
+                                              void* workspace, size_t workspace_bytes, cudaStream_t stream) {
   clear_error();
   HLA_REQUIRE(head_dim == 32 || head_dim == 64, HLA_ERR_UNSUPPORTED, "head_dim %d not in {32, 64}", head_dim);
   HLA_REQUIRE(batch >= 1 && heads >= 1 && n >= 1, HLA_ERR_INVALID, "bad shape");
@@ -467,11 +487,11 @@ extern "C" hla_status hla_attn_bwd_preprocess(int32_t batch, int32_t heads, int3
   if (head_dim == 64)
     bwd_preprocess_kernel<64><<<blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
                                                           reinterpret_cast<const __nv_bfloat16*>(dout), dsum,
-                                                          dq_acc, n, heads, rows);
+                                                          dq_acc, seq_to_cell, n, heads, rows);
   else
     bwd_preprocess_kernel<32><<<blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
                                                           reinterpret_cast<const __nv_bfloat16*>(dout), dsum,
-                                                          dq_acc, n, heads, rows);
+                                                          dq_acc, seq_to_cell, n, heads, rows);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
 }
@@ -479,8 +499,8 @@ extern "C" hla_status hla_attn_bwd_preprocess(int32_t batch, int32_t heads, int3
 extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch,
                                         int32_t heads, int32_t head_dim, float scale, const void* q, const void* k,
                                         const void* v, const float* lse, const void* dout, void* dk, void* dv,
-                                        void* workspace, size_t workspace_bytes, int64_t* tiles_visited,
-                                        cudaStream_t stream) {
+                                        const int32_t* seq_to_cell, void* workspace, size_t workspace_bytes,
+                                        int64_t* tiles_visited, cudaStream_t stream) {
   clear_error();
   Pattern pat;
   hla_status st = check_attn_args(d, m, batch, heads, head_dim, &pat);
@@ -510,19 +530,30 @@ extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_blo
   prm.dk = reinterpret_cast<__nv_bfloat16*>(dk);
   prm.dv = reinterpret_cast<__nv_bfloat16*>(dv);
   prm.visited = reinterpret_cast<unsigned long long*>(tiles_visited);
+  prm.s2c = seq_to_cell;
+  const bool gather = seq_to_cell != nullptr;
+  HLA_REQUIRE(!gather || d->order == HLA_ORDER_HILBERT, HLA_ERR_INVALID,
+              "seq_to_cell (fused reorder) is only meaningful for Hilbert-order patterns");
+  HLA_REQUIRE(!gather || ((uintptr_t)seq_to_cell & 15) == 0, HLA_ERR_INVALID, "seq_to_cell must be 16-byte aligned");
   const int64_t tok = (int64_t)batch * pat.N;
   CUtensorMap mq, mk, mv, mdo;
-  if ((st = make_rows_map(&mq, q, tok, heads, head_dim, kBlock)) != HLA_OK) return st;
-  if ((st = make_rows_map(&mk, k, tok, heads, head_dim, kBlock)) != HLA_OK) return st;
-  if ((st = make_rows_map(&mv, v, tok, heads, head_dim, kBlock)) != HLA_OK) return st;
-  if ((st = make_rows_map(&mdo, dout, tok, heads, head_dim, kBlock)) != HLA_OK) return st;
+  auto mk_map = [&](CUtensorMap* mp, const void* base) {
+    return gather ? make_gather_map(mp, base, tok, heads, head_dim) : make_rows_map(mp, base, tok, heads, head_dim, kBlock);
+  };
+  if ((st = mk_map(&mq, q)) != HLA_OK) return st;
+  if ((st = mk_map(&mk, k)) != HLA_OK) return st;
+  if ((st = mk_map(&mv, v)) != HLA_OK) return st;
+  if ((st = mk_map(&mdo, dout)) != HLA_OK) return st;
   const bool two_d = pat.kind == K_WSA || pat.kind == K_SA || pat.kind == K_NA2D;
   const int32_t mkb = pat.N / kBlock;
-  if (head_dim == 64)
-    return two_d ? launch_bwd<64, true>(mq, mk, mv, mdo, prm, mkb, stream)
-                 : launch_bwd<64, false>(mq, mk, mv, mdo, prm, mkb, stream);
-  return two_d ? launch_bwd<32, true>(mq, mk, mv, mdo, prm, mkb, stream)
-               : launch_bwd<32, false>(mq, mk, mv, mdo, prm, mkb, stream);
+  if (head_dim == 64) {
+    if (gather) return launch_bwd<64, false, true>(mq, mk, mv, mdo, prm, mkb, stream);
+    return two_d ? launch_bwd<64, true, false>(mq, mk, mv, mdo, prm, mkb, stream)
+                 : launch_bwd<64, false, false>(mq, mk, mv, mdo, prm, mkb, stream);
+  }
+  if (gather) return launch_bwd<32, false, true>(mq, mk, mv, mdo, prm, mkb, stream);
+  return two_d ? launch_bwd<32, true, false>(mq, mk, mv, mdo, prm, mkb, stream)
+               : launch_bwd<32, false, false>(mq, mk, mv, mdo, prm, mkb, stream);
 }
 
 extern "C" hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,
@@ -546,8 +577,8 @@ extern "C" hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_
 extern "C" hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
                                    int32_t head_dim, float scale, const void* q, const void* k, const void* v,
                                    const void* o, const float* lse, const void* dout, void* dq, void* dk, void* dv,
-                                   void* workspace, size_t workspace_bytes, int64_t* tiles_visited,
-                                   cudaStream_t stream) {
+                                   const int32_t* seq_to_cell, void* workspace, size_t workspace_bytes,
+                                   int64_t* tiles_visited, cudaStream_t stream) {
   clear_error();
   Pattern pat;
   hla_status st = check_attn_args(d, m, batch, heads, head_dim, &pat);
@@ -558,11 +589,11 @@ extern "C" hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_ma
   st = carve_workspace(batch, heads, pat.N, head_dim, workspace, workspace_bytes, &dq_acc, &dsum);
   if (st != HLA_OK) return st;
   HLA_REQUIRE(((uintptr_t)o | (uintptr_t)dq) % 16 == 0, HLA_ERR_INVALID, "tensors must be 16-byte aligned");
-  if ((st = hla_attn_bwd_preprocess(batch, heads, pat.N, head_dim, o, dout, workspace, workspace_bytes, stream)) !=
-      HLA_OK)
+  if ((st = hla_attn_bwd_preprocess(batch, heads, pat.N, head_dim, o, dout, seq_to_cell, workspace,
+                                    workspace_bytes, stream)) != HLA_OK)
     return st;
-  if ((st = hla_attn_bwd_main(d, m, batch, heads, head_dim, scale, q, k, v, lse, dout, dk, dv, workspace,
-                              workspace_bytes, tiles_visited, stream)) != HLA_OK)
+  if ((st = hla_attn_bwd_main(d, m, batch, heads, head_dim, scale, q, k, v, lse, dout, dk, dv, seq_to_cell,
+                              workspace, workspace_bytes, tiles_visited, stream)) != HLA_OK)
     return st;
   return hla_attn_bwd_finalize(batch, heads, pat.N, head_dim, workspace, workspace_bytes, dq, stream);
 }

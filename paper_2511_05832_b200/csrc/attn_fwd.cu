@@ -40,6 +40,7 @@ struct FwdParams {
   const int32_t* row_ptr;
   const int32_t* col_idx;
   const uint8_t* kind;
+  const int32_t* s2c;        // fused reorder: seq_to_cell table (tensors in grid order), else null
   __nv_bfloat16* o;
   float* lse;
   unsigned long long* visited;
@@ -67,6 +68,23 @@ __device__ __forceinline__ uint64_t mnmajor_desc(const uint8_t* tile, int kstep)
   // 8-row K groups 8*2D bytes apart; K step = 16 rows
   constexpr uint32_t layout = D == 64 ? sm100::kSwizzle128B : sm100::kSwizzle64B;
   return sm100::make_smem_desc(sm100::smem_u32(tile) + kstep * 16 * D * 2, kBlock * D * 2, 8 * D * 2, layout);
+}
+
+// Load the 128 token rows [seq0, seq0 + 128) (sequence order) of head h, batch b.
+// kGather (fused reorder): the tensor is in grid order; the warp gathers the rows of
+// cells s2c[seq0 ..] with 32 TMA .tile::gather4 ops (4 rows each); otherwise one 3-D
+// TMA box.  Called by all 32 lanes of the producer warp after lane 0 armed `bar`.
+template <int D, bool kGather>
+__device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int32_t h,
+                                          int32_t b, int32_t N, int32_t seq0, const int32_t* s2c, uint64_t pol,
+                                          int lane) {
+  if (kGather) {
+    const int4 c = __ldg(reinterpret_cast<const int4*>(s2c + seq0) + lane);
+    const int32_t base = b * N;
+    sm100::tma_gather4(dst + lane * 4 * D * 2, map, bar, h * D, base + c.x, base + c.y, base + c.z, base + c.w, pol);
+  } else if (lane == 0) {
+    sm100::tma_load_3d(dst, map, bar, 0, h, b * N + seq0, pol);
+  }
 }
 
 // Element mask of a partial tile for query row q (box = row_box(q)), keys k0 .. k0+127.
@@ -105,7 +123,7 @@ __device__ __forceinline__ void apply_row_mask(float (&s)[kBlock], const Pattern
 // K/V tiles in L2).  Barrier phases run on per-CTA counters: n = units with
 // nt > 0 processed so far, g = tiles processed so far.  The next unit's Q and
 // first K/V loads and its first S MMA overlap the current unit's epilogue.
-template <int D, bool kTwoD>
+template <int D, bool kTwoD, bool kGather>
 __global__ void __launch_bounds__(kThreads, 2)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const FwdParams prm) {
@@ -143,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
+    {
       const uint64_t pol_q = sm100::policy_evict_first();
       const uint64_t pol_kv = sm100::policy_evict_last();
       uint32_t n = 0, g = 0;
@@ -152,16 +170,20 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int32_t rs = __ldg(prm.row_ptr + qb), nt = __ldg(prm.row_ptr + qb + 1) - rs;
         if (nt == 0) continue;
         if (n > 0) sm100::mbar_wait(&sm.q_empty, (n - 1) & 1);
-        sm100::mbar_arrive_expect_tx(&sm.q_full, FwdSmem<D>::kTileBytes);
-        sm100::tma_load_3d(sm.q, &tmQ, &sm.q_full, 0, h, b * prm.N + qb * kBlock, pol_q);
+        if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.q_full, FwdSmem<D>::kTileBytes);
+        __syncwarp();
+        load_rows<D, kGather>(sm.q, &tmQ, &sm.q_full, h, b, prm.N, qb * kBlock, prm.s2c, pol_q, lane);
         for (int t = 0; t < nt; ++t, ++g) {
           const int s = g & 1;
           if (g >= 2) sm100::mbar_wait(&sm.kv_empty[s], ((g >> 1) - 1) & 1);
-          const int32_t krow = b * prm.N + __ldg(prm.col_idx + rs + t) * kBlock;
-          sm100::mbar_arrive_expect_tx(&sm.k_full[s], FwdSmem<D>::kTileBytes);
-          sm100::tma_load_3d(sm.k[s], &tmK, &sm.k_full[s], 0, h, krow, pol_kv);
-          sm100::mbar_arrive_expect_tx(&sm.v_full[s], FwdSmem<D>::kTileBytes);
-          sm100::tma_load_3d(sm.v[s], &tmV, &sm.v_full[s], 0, h, krow, pol_kv);
+          const int32_t k0 = __ldg(prm.col_idx + rs + t) * kBlock;
+          if (lane == 0) {
+            sm100::mbar_arrive_expect_tx(&sm.k_full[s], FwdSmem<D>::kTileBytes);
+            sm100::mbar_arrive_expect_tx(&sm.v_full[s], FwdSmem<D>::kTileBytes);
+          }
+          __syncwarp();
+          load_rows<D, kGather>(sm.k[s], &tmK, &sm.k_full[s], h, b, prm.N, k0, prm.s2c, pol_kv, lane);
+          load_rows<D, kGather>(sm.v[s], &tmV, &sm.v_full[s], h, b, prm.N, k0, prm.s2c, pol_kv, lane);
         }
         ++n;
       }
@@ -285,7 +307,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
 
       // epilogue: O / l -> bf16 row, LSE (natural log)
-      const int64_t orow = ((int64_t)b * prm.N + q) * prm.heads + h;
+      const int32_t ocell = kGather ? __ldg(prm.s2c + q) : q;   // fused inverse reorder of O
+      const int64_t orow = ((int64_t)b * prm.N + ocell) * prm.heads + h;
       uint4* optr = reinterpret_cast<uint4*>(prm.o + orow * D);
       const float inv_l = l > 0.f ? 1.f / l : 0.f;
       if (nt > 0) {
@@ -326,11 +349,11 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (warp == 2 && lane == 0 && prm.visited != nullptr && tiles_done > 0) atomicAdd(prm.visited, tiles_done);
 }
 
-template <int D, bool kTwoD>
+template <int D, bool kTwoD, bool kGather>
 hla_status launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const FwdParams& prm,
                       int32_t n_qblocks, cudaStream_t stream) {
   const size_t smem = sizeof(FwdSmem<D>) + 1024;
-  auto* fn = attn_fwd_kernel<D, kTwoD>;
+  auto* fn = attn_fwd_kernel<D, kTwoD, kGather>;
   HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t units = (int64_t)n_qblocks * prm.heads * prm.batch;
   const int grid = (int)std::min<int64_t>(units, 2 * (int64_t)num_sms());
@@ -365,7 +388,8 @@ using namespace hla;
 
 extern "C" hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
                                    int32_t head_dim, float scale, const void* q, const void* k, const void* v,
-                                   void* o, float* lse, int64_t* tiles_visited, cudaStream_t stream) {
+                                   void* o, float* lse, const int32_t* seq_to_cell, int64_t* tiles_visited,
+                                   cudaStream_t stream) {
   clear_error();
   Pattern pat;
   hla_status st = check_attn_args(d, m, batch, heads, head_dim, &pat);
@@ -385,15 +409,31 @@ extern "C" hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_ma
   prm.kind = m->kind;
   prm.o = reinterpret_cast<__nv_bfloat16*>(o);
   prm.lse = lse;
+  prm.s2c = seq_to_cell;
   prm.visited = reinterpret_cast<unsigned long long*>(tiles_visited);
+  const bool two_d = pat.kind == K_WSA || pat.kind == K_SA || pat.kind == K_NA2D;
+  const bool gather = seq_to_cell != nullptr;
+  HLA_REQUIRE(!gather || d->order == HLA_ORDER_HILBERT, HLA_ERR_INVALID,
+              "seq_to_cell (fused reorder) is only meaningful for Hilbert-order patterns");
+  HLA_REQUIRE(!gather || ((uintptr_t)seq_to_cell & 15) == 0, HLA_ERR_INVALID, "seq_to_cell must be 16-byte aligned");
   const int64_t rows = (int64_t)batch * pat.N;
   CUtensorMap mq, mk, mv;
-  if ((st = make_rows_map(&mq, q, rows, heads, head_dim, kBlock)) != HLA_OK) return st;
-  if ((st = make_rows_map(&mk, k, rows, heads, head_dim, kBlock)) != HLA_OK) return st;
-  if ((st = make_rows_map(&mv, v, rows, heads, head_dim, kBlock)) != HLA_OK) return st;
-  const bool two_d = pat.kind == K_WSA || pat.kind == K_SA || pat.kind == K_NA2D;
+  if (gather) {
+    if ((st = make_gather_map(&mq, q, rows, heads, head_dim)) != HLA_OK) return st;
+    if ((st = make_gather_map(&mk, k, rows, heads, head_dim)) != HLA_OK) return st;
+    if ((st = make_gather_map(&mv, v, rows, heads, head_dim)) != HLA_OK) return st;
+  } else {
+    if ((st = make_rows_map(&mq, q, rows, heads, head_dim, kBlock)) != HLA_OK) return st;
+    if ((st = make_rows_map(&mk, k, rows, heads, head_dim, kBlock)) != HLA_OK) return st;
+    if ((st = make_rows_map(&mv, v, rows, heads, head_dim, kBlock)) != HLA_OK) return st;
+  }
   const int32_t mqb = pat.N / kBlock;
-  if (head_dim == 64)
-    return two_d ? launch_fwd<64, true>(mq, mk, mv, prm, mqb, stream) : launch_fwd<64, false>(mq, mk, mv, prm, mqb, stream);
-  return two_d ? launch_fwd<32, true>(mq, mk, mv, prm, mqb, stream) : launch_fwd<32, false>(mq, mk, mv, prm, mqb, stream);
+  if (head_dim == 64) {
+    if (gather) return launch_fwd<64, false, true>(mq, mk, mv, prm, mqb, stream);
+    return two_d ? launch_fwd<64, true, false>(mq, mk, mv, prm, mqb, stream)
+                 : launch_fwd<64, false, false>(mq, mk, mv, prm, mqb, stream);
+  }
+  if (gather) return launch_fwd<32, false, true>(mq, mk, mv, prm, mqb, stream);
+  return two_d ? launch_fwd<32, true, false>(mq, mk, mv, prm, mqb, stream)
+               : launch_fwd<32, false, false>(mq, mk, mv, prm, mqb, stream);
 }

@@ -6,6 +6,7 @@
 #include "../../include/hla_debug.h"
 #include "common.cuh"
 #include "sm100.cuh"
+#include "tensor_map.cuh"
 
 namespace hla {
 namespace {
@@ -100,10 +101,54 @@ __global__ void __launch_bounds__(128) debug_umma_kernel(const __nv_bfloat16* __
   if (warp == 0) sm100::tmem_dealloc(tmem, 512);
 }
 
+// 128 token rows (indices idx[0..127]) of head h gathered with .tile::gather4 into a
+// SWIZZLE_<2d> tile, then read back through the swizzle into out[128][d].
+template <int D>
+__global__ void __launch_bounds__(128) debug_gather_kernel(const __grid_constant__ CUtensorMap map,
+                                                           const int32_t* __restrict__ idx, int h,
+                                                           __nv_bfloat16* __restrict__ out) {
+  __shared__ alignas(1024) uint8_t tile[128 * D * 2];
+  __shared__ uint64_t bar;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    sm100::mbar_init(&bar, 1);
+    sm100::fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid < 32) {
+    if (tid == 0) sm100::mbar_arrive_expect_tx(&bar, 128 * D * 2);
+    __syncwarp();
+    const int4 r = *reinterpret_cast<const int4*>(idx + 4 * tid);
+    sm100::tma_gather4(tile + 4 * tid * D * 2, &map, &bar, h * D, r.x, r.y, r.z, r.w, sm100::policy_evict_normal());
+  }
+  sm100::mbar_wait(&bar, 0);
+  for (int e = 0; e < D; ++e) {
+    const uint32_t off = (uint32_t)(tid * D * 2 + e * 2);
+    const uint32_t phys = D == 64 ? sm100::swz128(off) : sm100::swz64(off);
+    out[tid * D + e] = *reinterpret_cast<const __nv_bfloat16*>(tile + phys);
+  }
+}
+
 }  // namespace
 }  // namespace hla
 
 using namespace hla;
+
+extern "C" hla_status hla_debug_gather4(const void* src, int64_t rows, int32_t heads, int32_t head_dim,
+                                        const int32_t* idx, int32_t head, int32_t box_h, void* out,
+                                        cudaStream_t stream) {
+  clear_error();
+  HLA_REQUIRE(head_dim == 32 || head_dim == 64, HLA_ERR_UNSUPPORTED, "head_dim");
+  CUtensorMap map;
+  hla_status st = make_gather_map(&map, src, rows, heads, head_dim, box_h);
+  if (st != HLA_OK) return st;
+  if (head_dim == 64)
+    debug_gather_kernel<64><<<1, 128, 0, stream>>>(map, idx, head, reinterpret_cast<__nv_bfloat16*>(out));
+  else
+    debug_gather_kernel<32><<<1, 128, 0, stream>>>(map, idx, head, reinterpret_cast<__nv_bfloat16*>(out));
+  HLA_CUDA_TRY(cudaGetLastError());
+  return HLA_OK;
+}
 
 extern "C" hla_status hla_debug_umma(const void* A, const void* B, float* C, int32_t M, int32_t N, int32_t K,
                                      int32_t a_major_mn, int32_t b_major_mn, int32_t a_from_tmem,

@@ -48,4 +48,25 @@ inline hla_status make_rows_map(CUtensorMap* map, const void* base, int64_t rows
   return HLA_OK;
 }
 
+// bf16 tensor [rows_total, heads * head_dim] viewed as 2-D (heads*head_dim, rows) for
+// .tile::gather4 loads of single token rows: box = (head_dim, box_h).
+inline hla_status make_gather_map(CUtensorMap* map, const void* base, int64_t rows_total, int heads, int head_dim,
+                                  int box_h = 1) {
+  EncodeTiledFn enc;
+  hla_status st = get_encode_fn(&enc);
+  if (st != HLA_OK) return st;
+  cuuint64_t dims[2] = {(cuuint64_t)heads * head_dim, (cuuint64_t)rows_total};
+  cuuint64_t strides[1] = {(cuuint64_t)heads * head_dim * 2};
+  cuuint32_t box[2] = {(cuuint32_t)head_dim, (cuuint32_t)box_h};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMapSwizzle swz = head_dim * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                           : head_dim * 2 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                : CU_TENSOR_MAP_SWIZZLE_32B;
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  HLA_REQUIRE(r == CUDA_SUCCESS, HLA_ERR_CUDA, "cuTensorMapEncodeTiled (gather) failed (%d)", (int)r);
+  return HLA_OK;
+}
+
 }  // namespace hla

@@ -141,6 +141,27 @@ def test_bwd_small(case, sharp):
 FULL_BWD = [c for c in FULL if c[0] in ("cfg2", "cfg2-rm", "cfg3", "cfg3-rm", "cfg4", "cfg4-rm")]
 
 
+@pytest.mark.parametrize("kind,g,w,B,H,d", [("HWA", 64, 16, 4, 8, 64), ("HSA", 64, 16, 2, 3, 64),
+                                             ("HNA", 128, 7, 1, 4, 64), ("HWA", 16, 8, 1, 1, 32),
+                                             ("HNA", 32, 5, 2, 2, 32), ("HSWA", 32, 8, 2, 2, 64)])
+def test_fused_reorder_matches_explicit_permutation(kind, g, w, B, H, d):
+    """Fused reorder (TMA gather4 loads + scattered epilogues) == explicit
+    hla_hilbert_perm passes: O, dK, dV bit-identical (same tiles, same order);
+    dQ within atomics-order rounding."""
+    q, k, v, do = _inputs(B, g * g, H, d, seed=11)
+    shift = (w * w) // 2 if kind == "HSWA" else 0
+    fused = hla.HilbertLocalAttention(kind, g, g, w, w, B, H, d, shift=shift, device=DEV, fused=True)
+    plain = hla.HilbertLocalAttention(kind, g, g, w, w, B, H, d, shift=shift, device=DEV, fused=False)
+    r1 = [t.clone() for t in (fused.forward(q, k, v),) + fused.backward(do)]
+    r2 = [t.clone() for t in (plain.forward(q, k, v),) + plain.backward(do)]
+    torch.cuda.synchronize()
+    assert fused.launches_per_step == 4 and plain.launches_per_step == 8
+    assert torch.equal(r1[0], r2[0])                       # O
+    assert torch.equal(fused.lse, plain.lse)
+    assert torch.equal(r1[2], r2[2]) and torch.equal(r1[3], r2[3])   # dK, dV
+    assert (r1[1].float() - r2[1].float()).abs().max().item() <= 2e-3   # dQ (fp32 atomics order)
+
+
 @pytest.mark.parametrize("case", FULL_BWD, ids=lambda c: c[0])
 def test_step_full_size_sampled(case):
     """Full hot-path step through the public layer API (perm -> fwd -> unperm ->

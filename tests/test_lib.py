@@ -53,11 +53,11 @@ def test_argument_validation_without_gpu():
     # attention limits
     d = api.pattern_desc("HWA", 64, 64, 16, 16, block=64)
     m = _lib.BlockMaskC(64, 64, 1, 8, 8, 8, 8, 8, 8, 8)
-    st = L.hla_attn_fwd(ctypes.byref(d), ctypes.byref(m), 1, 1, 64, 0.0, 16, 16, 16, 16, 16, None, None)
+    st = L.hla_attn_fwd(ctypes.byref(d), ctypes.byref(m), 1, 1, 64, 0.0, 16, 16, 16, 16, 16, None, None, None)
     assert st == _lib.HLA_ERR_UNSUPPORTED
     d = api.pattern_desc("HWA", 64, 64, 16, 16)
     m = _lib.BlockMaskC(32, 32, 1, 8, 8, 8, 8, 8, 8, 8)
-    st = L.hla_attn_fwd(ctypes.byref(d), ctypes.byref(m), 1, 1, 128, 0.0, 16, 16, 16, 16, 16, None, None)
+    st = L.hla_attn_fwd(ctypes.byref(d), ctypes.byref(m), 1, 1, 128, 0.0, 16, 16, 16, 16, 16, None, None, None)
     assert st == _lib.HLA_ERR_UNSUPPORTED
 
 
