@@ -34,6 +34,7 @@ constexpr int kThreads = 320;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColS = 0, kColDP = 128, kColP = 256, kColDQ = 320, kColDV = 384, kColDK = 448;
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kHalf = 64;   // q-columns per pipeline half
 
 struct BwdParams {
   Pattern pat;
@@ -58,10 +59,10 @@ struct BwdSmem {
   alignas(1024) uint8_t v[2][kTileBytes];
   alignas(1024) uint8_t q[2][kTileBytes];
   alignas(1024) uint8_t dO[2][kTileBytes];
-  alignas(1024) uint8_t ds[2 * 128 * 128];   // dS^T bf16: [q/64][kv 128][64 q], SWIZZLE_128B
+  alignas(1024) uint8_t ds[2][2 * 128 * 128];   // dS^T bf16 x2 (tile parity): [q/64][kv 128][64 q], SWIZZLE_128B
   alignas(16) float lse[2][kBlock];
   alignas(16) float dd[2][kBlock];
-  uint64_t kv_full[2], kv_empty[2], q_full[2], q_empty[2], s_full, ds_ready, dq_full, dq_free, dkv_full;
+  uint64_t kv_full[2], kv_empty[2], q_full[2], q_empty[2], s_full[2], ds_ready[2], dq_full, dq_free, dkv_full;
   uint32_t tmem_base;
 };
 
@@ -84,6 +85,31 @@ __device__ __forceinline__ uint64_t ds_kmajor_desc(const uint8_t* ds, int kstep)
 __device__ __forceinline__ uint64_t ds_mnmajor_desc(const uint8_t* ds, int kstep) {
   return sm100::make_smem_desc(sm100::smem_u32(ds) + kstep * 2048, 16384, 1024, sm100::kSwizzle128B);
 }
+
+// Iterator over the flattened (work unit, q-block tile) sequence of this CTA,
+// skipping units without tiles.  n = ordinal of the current non-empty unit.
+struct TileIter {
+  int32_t u, t, nt;
+  uint32_t n;
+  bool valid;
+  __device__ void seek(const int32_t* t_row_ptr, int32_t mk, int32_t units) {
+    for (; u < units; u += gridDim.x) {
+      const int32_t kb = u % mk;
+      nt = __ldg(t_row_ptr + kb + 1) - __ldg(t_row_ptr + kb);
+      if (nt > 0) { valid = true; return; }
+    }
+    valid = false;
+  }
+  __device__ void init(const int32_t* t_row_ptr, int32_t mk, int32_t units) {
+    u = blockIdx.x; t = 0; n = 0;
+    seek(t_row_ptr, mk, units);
+  }
+  __device__ void advance(const int32_t* t_row_ptr, int32_t mk, int32_t units) {
+    if (++t < nt) return;
+    t = 0; ++n; u += gridDim.x;
+    seek(t_row_ptr, mk, units);
+  }
+};
 
 // Load the 128 token rows [seq0, seq0 + 128) (sequence order) of head h, batch b;
 // see attn_fwd.cu load_rows (kGather = fused reorder through s2c with .tile::gather4).
@@ -128,8 +154,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::mbar_init(&sm.q_full[s], 1);
       sm100::mbar_init(&sm.q_empty[s], 1);
     }
-    sm100::mbar_init(&sm.s_full, 1);
-    sm100::mbar_init(&sm.ds_ready, 128);
+    for (int hh = 0; hh < 2; ++hh) {
+      sm100::mbar_init(&sm.s_full[hh], 1);
+      sm100::mbar_init(&sm.ds_ready[hh], 128);
+    }
     sm100::mbar_init(&sm.dq_full, 1);
     sm100::mbar_init(&sm.dq_free, 128);
     sm100::mbar_init(&sm.dkv_full, 1);
@@ -184,54 +212,82 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------- MMA issuer
+    // Half-tile software pipeline over the flattened (unit, q-block) sequence:
+    //   S_A,dP_A(g) S_B,dP_B(g) | dV_A dK_A(g) S_A,dP_A(g+1) | dV_B dK_B dQ(g) S_B,dP_B(g+1) | ...
+    // so the tensor core works on one q-half while the compute warps process the other.
     if (lane == 0) {
-      constexpr uint32_t idesc_s = sm100::make_idesc_bf16(kBlock, kBlock, false, false);
-      constexpr uint32_t idesc_kv = sm100::make_idesc_bf16(kBlock, D, false, true);   // dV, dK
-      constexpr uint32_t idesc_q = sm100::make_idesc_bf16(kBlock, D, true, true);     // dQ
-      const uint32_t tS = tmem + kColS, tDP = tmem + kColDP, tP = tmem + kColP;
-      const uint32_t tDQ = tmem + kColDQ, tDV = tmem + kColDV, tDK = tmem + kColDK;
-      uint32_t n = 0, g = 0;
-      for (int32_t u = blockIdx.x; u < units; u += gridDim.x) {
-        const int32_t kb = u % mk;
-        const int32_t nt = __ldg(prm.t_row_ptr + kb + 1) - __ldg(prm.t_row_ptr + kb);
-        if (nt == 0) continue;
-        const int kvs = n & 1;
-        const uint8_t* sk = sm.k[kvs];
-        const uint8_t* sv = sm.v[kvs];
-        sm100::mbar_wait(&sm.kv_full[kvs], (n >> 1) & 1);
-        for (int t = 0; t < nt; ++t, ++g) {
-          const int s = g & 1;
-          sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1);
-          sm100::tc_fence_after();
+      constexpr uint32_t idesc_h = sm100::make_idesc_bf16(kBlock, kHalf, false, false);  // S^T, dP^T halves
+      constexpr uint32_t idesc_kv = sm100::make_idesc_bf16(kBlock, D, false, true);      // dV, dK
+      constexpr uint32_t idesc_q = sm100::make_idesc_bf16(kBlock, D, true, true);        // dQ
+      const uint32_t tP = tmem + kColP, tDQ = tmem + kColDQ, tDV = tmem + kColDV, tDK = tmem + kColDK;
+      TileIter cur;
+      cur.init(prm.t_row_ptr, mk, units);
+      uint32_t g = 0;
+      auto issue_sdp = [&](const TileIter& it, uint32_t gg, int half) {
+        const int s = gg & 1;
+        const uint8_t* sk = sm.k[it.n & 1];
+        const uint8_t* sv = sm.v[it.n & 1];
+        const uint32_t qoff = half * kHalf * D * 2;   // first row of this q half
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)
-            sm100::mma_ss(tS, kmajor_desc<D>(sk, kk), kmajor_desc<D>(sm.q[s], kk), idesc_s, kk > 0);
+        for (int kk = 0; kk < D / 16; ++kk)
+          sm100::mma_ss(tmem + kColS + half * kHalf, kmajor_desc<D>(sk, kk), kmajor_desc<D>(sm.q[s] + qoff, kk),
+                        idesc_h, kk > 0);
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)
-            sm100::mma_ss(tDP, kmajor_desc<D>(sv, kk), kmajor_desc<D>(sm.dO[s], kk), idesc_s, kk > 0);
-          sm100::mma_commit(&sm.s_full);
-          sm100::mbar_wait(&sm.ds_ready, g & 1);
-          sm100::tc_fence_after();
+        for (int kk = 0; kk < D / 16; ++kk)
+          sm100::mma_ss(tmem + kColDP + half * kHalf, kmajor_desc<D>(sv, kk), kmajor_desc<D>(sm.dO[s] + qoff, kk),
+                        idesc_h, kk > 0);
+        sm100::mma_commit(&sm.s_full[half]);
+      };
+      auto issue_dvdk = [&](uint32_t gg, int half, bool first_tile) {
+        const int s = gg & 1;
+        const uint8_t* ds = sm.ds[gg & 1];
 #pragma unroll
-          for (int kk = 0; kk < kBlock / 16; ++kk)
-            sm100::mma_ts(tDV, tP + kk * 8, mnmajor_desc<D>(sm.dO[s], kk), idesc_kv, (t > 0 || kk > 0) ? 1u : 0u);
-#pragma unroll
-          for (int kk = 0; kk < kBlock / 16; ++kk)
-            sm100::mma_ss(tDK, ds_kmajor_desc(sm.ds, kk), mnmajor_desc<D>(sm.q[s], kk), idesc_kv,
-                          (t > 0 || kk > 0) ? 1u : 0u);
-          if (g > 0) {
-            sm100::mbar_wait(&sm.dq_free, (g - 1) & 1);
-            sm100::tc_fence_after();
-          }
-#pragma unroll
-          for (int kk = 0; kk < kBlock / 16; ++kk)
-            sm100::mma_ss(tDQ, ds_mnmajor_desc(sm.ds, kk), mnmajor_desc<D>(sk, kk), idesc_q, kk > 0);
-          sm100::mma_commit(&sm.q_empty[s]);
-          sm100::mma_commit(&sm.dq_full);
+        for (int kk = half * 4; kk < half * 4 + 4; ++kk) {
+          const uint32_t acc = (!first_tile || kk > 0) ? 1u : 0u;
+          sm100::mma_ts(tDV, tP + kk * 8, mnmajor_desc<D>(sm.dO[s], kk), idesc_kv, acc);
+          sm100::mma_ss(tDK, ds_kmajor_desc(ds, kk), mnmajor_desc<D>(sm.q[s], kk), idesc_kv, acc);
         }
-        sm100::mma_commit(&sm.kv_empty[kvs]);
-        sm100::mma_commit(&sm.dkv_full);
-        ++n;
+      };
+      if (cur.valid) {
+        sm100::mbar_wait(&sm.kv_full[cur.n & 1], (cur.n >> 1) & 1);
+        sm100::mbar_wait(&sm.q_full[0], 0);
+        sm100::tc_fence_after();
+        issue_sdp(cur, 0, 0);
+        issue_sdp(cur, 0, 1);
+      }
+      while (cur.valid) {
+        TileIter nxt = cur;
+        nxt.advance(prm.t_row_ptr, mk, units);
+        const int kvs = cur.n & 1;
+        const bool last_of_unit = cur.t == cur.nt - 1;
+        // half A of tile g
+        sm100::mbar_wait(&sm.ds_ready[0], g & 1);
+        sm100::tc_fence_after();
+        issue_dvdk(g, 0, cur.t == 0);
+        if (nxt.valid) {
+          if (nxt.t == 0) sm100::mbar_wait(&sm.kv_full[nxt.n & 1], (nxt.n >> 1) & 1);
+          sm100::mbar_wait(&sm.q_full[(g + 1) & 1], ((g + 1) >> 1) & 1);
+          sm100::tc_fence_after();
+          issue_sdp(nxt, g + 1, 0);
+        }
+        // half B of tile g, then dQ (needs both halves of dS)
+        sm100::mbar_wait(&sm.ds_ready[1], g & 1);
+        sm100::tc_fence_after();
+        issue_dvdk(g, 1, false);
+        if (last_of_unit) sm100::mma_commit(&sm.dkv_full);
+        if (g > 0) {
+          sm100::mbar_wait(&sm.dq_free, (g - 1) & 1);
+          sm100::tc_fence_after();
+        }
+#pragma unroll
+        for (int kk = 0; kk < kBlock / 16; ++kk)
+          sm100::mma_ss(tDQ, ds_mnmajor_desc(sm.ds[g & 1], kk), mnmajor_desc<D>(sm.k[kvs], kk), idesc_q, kk > 0);
+        sm100::mma_commit(&sm.q_empty[g & 1]);
+        sm100::mma_commit(&sm.dq_full);
+        if (last_of_unit) sm100::mma_commit(&sm.kv_empty[kvs]);
+        if (nxt.valid) issue_sdp(nxt, g + 1, 1);
+        cur = nxt;
+        ++g;
       }
     }
   } else if (warp < 6) {
@@ -251,62 +307,66 @@ __global__ void __launch_bounds__(kThreads, 1)
         sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1);
         sm.lse[s][row] *= kLog2e;                     // LSE in the log2 domain
         sm100::named_bar_sync(1, 128);
-        sm100::mbar_wait(&sm.s_full, g & 1);
-        sm100::tc_fence_after();
         const uint8_t kd = __ldg(prm.t_kind + rs + t);
         const int32_t q0 = __ldg(prm.t_col_idx + rs + t) * kBlock;
         const float* lse2 = sm.lse[s];
         const float* dd = sm.dd[s];
+        uint8_t* dsbuf = sm.ds[g & 1];
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t sr[32], dpr[32];
-          sm100::tmem_ld32(tmem + lane_off + kColS + c * 32, sr);
-          sm100::tmem_ld32(tmem + lane_off + kColDP + c * 32, dpr);
-          sm100::tmem_wait_ld();
-          float p[32];
+        for (int half = 0; half < 2; ++half) {
+          sm100::mbar_wait(&sm.s_full[half], g & 1);
+          sm100::tc_fence_after();
+#pragma unroll 1
+          for (int c = 2 * half; c < 2 * half + 2; ++c) {
+            uint32_t sr[32], dpr[32];
+            sm100::tmem_ld32(tmem + lane_off + kColS + c * 32, sr);
+            sm100::tmem_ld32(tmem + lane_off + kColDP + c * 32, dpr);
+            sm100::tmem_wait_ld();
+            float p[32];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) p[e] = sm100::ex2(fmaf(__uint_as_float(sr[e]), sl2, -lse2[c * 32 + e]));
-          if (kd == 2) {
+            for (int e = 0; e < 32; ++e) p[e] = sm100::ex2(fmaf(__uint_as_float(sr[e]), sl2, -lse2[c * 32 + e]));
+            if (kd == 2) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
-              const int32_t qq = q0 + c * 32 + e;
-              bool ok;
-              if (!kTwoD) {
-                ok = (uint32_t)(qq - box.lo) < (uint32_t)box.len;
-              } else {
-                const int32_t rq = prm.pat.log2W >= 0 ? (qq >> prm.pat.log2W) : qq / prm.pat.W;
-                const int32_t cq = qq - rq * prm.pat.W;
-                ok = ((uint32_t)(rq - box.lo) < (uint32_t)box.len) && ((uint32_t)(cq - box.c0) < (uint32_t)box.cn);
+              for (int e = 0; e < 32; ++e) {
+                const int32_t qq = q0 + c * 32 + e;
+                bool ok;
+                if (!kTwoD) {
+                  ok = (uint32_t)(qq - box.lo) < (uint32_t)box.len;
+                } else {
+                  const int32_t rq = prm.pat.log2W >= 0 ? (qq >> prm.pat.log2W) : qq / prm.pat.W;
+                  const int32_t cq = qq - rq * prm.pat.W;
+                  ok = ((uint32_t)(rq - box.lo) < (uint32_t)box.len) && ((uint32_t)(cq - box.c0) < (uint32_t)box.cn);
+                }
+                if (!ok) p[e] = 0.f;
               }
-              if (!ok) p[e] = 0.f;
+            }
+            uint32_t pk[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) pk[e] = sm100::pack_bf16(p[2 * e], p[2 * e + 1]);
+            sm100::tmem_st16(tmem + lane_off + kColP + c * 16, pk);
+            // dS^T row -> smem [q/64][kv][64] with the 128B swizzle (16B chunks)
+#pragma unroll
+            for (int u4 = 0; u4 < 4; ++u4) {
+              const int qc = c * 32 + u4 * 8;             // first q column of this 16B chunk
+              float ds[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                ds[e] = p[u4 * 8 + e] * scale * (__uint_as_float(dpr[u4 * 8 + e]) - dd[qc + e]);
+              uint4 w;
+              w.x = sm100::pack_bf16(ds[0], ds[1]);
+              w.y = sm100::pack_bf16(ds[2], ds[3]);
+              w.z = sm100::pack_bf16(ds[4], ds[5]);
+              w.w = sm100::pack_bf16(ds[6], ds[7]);
+              const uint32_t off =
+                  (uint32_t)(qc >> 6) * 16384u + sm100::swz128((uint32_t)row * 128u + (uint32_t)(qc & 63) * 2u);
+              *reinterpret_cast<uint4*>(dsbuf + off) = w;
             }
           }
-          uint32_t pk[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) pk[e] = sm100::pack_bf16(p[2 * e], p[2 * e + 1]);
-          sm100::tmem_st16(tmem + lane_off + kColP + c * 16, pk);
-          // dS^T row -> smem [q/64][kv][64] with the 128B swizzle (16B chunks)
-#pragma unroll
-          for (int u4 = 0; u4 < 4; ++u4) {
-            const int qc = c * 32 + u4 * 8;             // first q column of this 16B chunk
-            float ds[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              ds[e] = p[u4 * 8 + e] * scale * (__uint_as_float(dpr[u4 * 8 + e]) - dd[qc + e]);
-            uint4 w;
-            w.x = sm100::pack_bf16(ds[0], ds[1]);
-            w.y = sm100::pack_bf16(ds[2], ds[3]);
-            w.z = sm100::pack_bf16(ds[4], ds[5]);
-            w.w = sm100::pack_bf16(ds[6], ds[7]);
-            const uint32_t off =
-                (uint32_t)(qc >> 6) * 16384u + sm100::swz128((uint32_t)row * 128u + (uint32_t)(qc & 63) * 2u);
-            *reinterpret_cast<uint4*>(sm.ds + off) = w;
-          }
+          sm100::tmem_wait_st();
+          sm100::fence_proxy_async_smem();
+          sm100::tc_fence_before();
+          sm100::mbar_arrive(&sm.ds_ready[half]);
         }
-        sm100::tmem_wait_st();
-        sm100::fence_proxy_async_smem();
-        sm100::tc_fence_before();
-        sm100::mbar_arrive(&sm.ds_ready);
       }
       // final dK, dV rows -> bf16 (dS already carries the softmax scale)
       const int32_t kcell = kGather ? __ldg(prm.s2c + kidx) : kidx;   // fused inverse reorder of dK, dV
