@@ -196,8 +196,8 @@ HLA_API hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_mask*
  * q, k, v, o, dout, dq, dk, dv: bf16 [batch, N, heads, head_dim]; lse from the
  * forward.  workspace: device memory of at least hla_attn_bwd_workspace(...)
  * bytes, 256-byte aligned (fp32 dQ accumulator + D); its contents need not be
- * initialised.  dQ accumulation uses fp32 atomics (summation order is not
- * deterministic; covered by the stated tolerance).  Same limits as the forward.
+ * initialised.  dQ accumulation uses fp32 TMA reduce-adds (summation order is
+ * not deterministic; covered by the stated tolerance).  Same limits as the forward.
  * seq_to_cell: as in hla_attn_fwd (fused reorder: every bf16 tensor in grid order).
  */
 HLA_API hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_mask* m,
@@ -214,8 +214,9 @@ HLA_API hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_mask*
  * from one stage to the next and must not be touched in between.
  *   preprocess: D = rowsum(dO o O) (fp32), dQ accumulator := 0
  *   main      : the tcgen05 kernel over the transposed lists; writes dK, dV and
- *               accumulates dQ (fp32, red.global.add)
- *   finalize  : dQ = bf16(accumulator)                                        */
+ *               accumulates dQ (fp32, TMA reduce-add, sequence order)
+ *   finalize  : dQ = bf16(accumulator), written to grid cells when seq_to_cell
+ *               is given (fused inverse reorder)                              */
 HLA_API hla_status hla_attn_bwd_preprocess(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,
                                    const void* o, const void* dout, const int32_t* seq_to_cell,
                                    void* workspace, size_t workspace_bytes, cudaStream_t stream);
@@ -227,7 +228,7 @@ HLA_API hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_block_
                              int64_t* tiles_visited, cudaStream_t stream);
 HLA_API hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,
                                  const void* workspace, size_t workspace_bytes, void* dq,
-                                 cudaStream_t stream);
+                                 const int32_t* seq_to_cell, cudaStream_t stream);
 
 HLA_API size_t hla_attn_bwd_workspace(int32_t batch, int32_t heads, int32_t n, int32_t head_dim);
 

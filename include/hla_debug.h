@@ -31,6 +31,11 @@ HLA_API hla_status hla_debug_gather4(const void* src, int64_t rows, int32_t head
                                      const int32_t* idx, int32_t head, int32_t box_h, void* out,
                                      cudaStream_t stream);
 
+/* hla_debug_mma_rate: `iters` back-to-back tcgen05.mma (M=128, N, K=16) from one CTA;
+ * out_cycles (device int64[1]) = SM cycles from first issue to commit completion. */
+HLA_API hla_status hla_debug_mma_rate(int32_t N, int32_t iters, int32_t a_major_mn, int32_t b_major_mn,
+                                      int32_t a_from_tmem, long long* out_cycles, cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

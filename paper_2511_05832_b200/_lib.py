@@ -8,7 +8,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhla.so")
+LIB_PATH = os.path.join(_HERE, os.environ.get("HLA_LIB_NAME", "libhla.so"))   # HLA_LIB_NAME: dev trace build
 
 HLA_OK, HLA_ERR_INVALID, HLA_ERR_UNSUPPORTED, HLA_ERR_CAPACITY, HLA_ERR_CUDA = range(5)
 STATUS_NAMES = {0: "HLA_OK", 1: "HLA_ERR_INVALID", 2: "HLA_ERR_UNSUPPORTED", 3: "HLA_ERR_CAPACITY",
@@ -18,7 +18,7 @@ STATUS_NAMES = {0: "HLA_OK", 1: "HLA_ERR_INVALID", 2: "HLA_ERR_UNSUPPORTED", 3: 
 EXPORTED = ("hla_hilbert_index", "hla_hilbert_perm", "hla_build_block_mask", "hla_mask_ratios",
             "hla_attn_fwd", "hla_attn_bwd", "hla_attn_bwd_workspace", "hla_attn_bwd_preprocess",
             "hla_attn_bwd_main", "hla_attn_bwd_finalize", "hla_last_error", "hla_version",
-            "hla_debug_umma", "hla_debug_gather4")
+            "hla_debug_umma", "hla_debug_gather4", "hla_debug_mma_rate")
 
 
 class PatternDesc(ctypes.Structure):
@@ -62,9 +62,10 @@ def lib():
         "hla_attn_bwd": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp],
         "hla_attn_bwd_preprocess": [i32, i32, i32, i32, vp, vp, vp, vp, sz, vp],
         "hla_attn_bwd_main": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp],
-        "hla_attn_bwd_finalize": [i32, i32, i32, i32, vp, sz, vp, vp],
+        "hla_attn_bwd_finalize": [i32, i32, i32, i32, vp, sz, vp, vp, vp],
         "hla_debug_umma": [vp, vp, vp, i32, i32, i32, i32, i32, i32, vp],
         "hla_debug_gather4": [vp, i64, i32, i32, vp, i32, i32, vp, vp],
+        "hla_debug_mma_rate": [i32, i32, i32, i32, i32, vp, vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)

@@ -183,10 +183,10 @@ def hla_attn_bwd_main(desc, mask, q, k, v, lse, dout, dk, dv, workspace, scale=0
                                                        workspace.numel(), _ptr(tiles_visited), _stream(stream)))
 
 
-def hla_attn_bwd_finalize(workspace, dq, stream=None):
+def hla_attn_bwd_finalize(workspace, dq, seq_to_cell=None, stream=None):
     B, N, H, D = dq.shape
     check("hla_attn_bwd_finalize", lib().hla_attn_bwd_finalize(B, H, N, D, _ptr(workspace), workspace.numel(),
-                                                               _ptr(dq), _stream(stream)))
+                                                               _ptr(dq), _ptr(seq_to_cell), _stream(stream)))
 
 
 def hla_debug_umma(A, B, M, N, K, a_mn=False, b_mn=False, a_tmem=False, stream=None):

@@ -94,7 +94,7 @@ class HilbertLocalAttention:
         api.hla_attn_bwd_main(self.desc, self.mask, q, k, v, self.lse, dout_s, dk, dv, self.workspace, self.scale,
                               seq_to_cell=self.s2c)
         mark("bwd")
-        api.hla_attn_bwd_finalize(self.workspace, dq)
+        api.hla_attn_bwd_finalize(self.workspace, dq, seq_to_cell=self.s2c)
         mark("bwd_fin")
         if self.hilbert and not self.fused:
             api.hla_hilbert_perm(self.grid_h, self.grid_w, api.FROM_HILBERT, (self.dqs, self.dks, self.dvs),

@@ -91,6 +91,21 @@ hla_status make_pattern(const hla_pattern_desc* d, Pattern* p) {
 
 }  // namespace hla
 
+#ifdef HLA_TRACE
+namespace hla {
+__device__ unsigned long long g_hla_trace[8 * 1024 * 2];
+}  // namespace hla
+// dev-only: copy the whole trace area (8 roles x 1024 (tag, clock) pairs) to host and clear it
+extern "C" __attribute__((visibility("default"))) int hla_debug_trace_dump(unsigned long long* host, int max_events) {
+  cudaDeviceSynchronize();
+  const int n = max_events < 8 * 1024 ? max_events : 8 * 1024;
+  cudaMemcpyFromSymbol(host, hla::g_hla_trace, (size_t)n * 2 * sizeof(unsigned long long));
+  static unsigned long long zeros[8 * 1024 * 2];
+  cudaMemcpyToSymbol(hla::g_hla_trace, zeros, sizeof(zeros));
+  return n;
+}
+#endif
+
 extern "C" const char* hla_last_error(void) { return hla::g_err; }
 
 extern "C" const char* hla_version(void) { return "libhla 0.1 (sm_100a, tcgen05/TMEM/TMA)"; }

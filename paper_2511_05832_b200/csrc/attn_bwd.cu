@@ -17,10 +17,11 @@
 //                 dV  += P^T dO_i      (TS, P^T bf16 in TMEM cols [256,320); acc [384,448))
 //                 dK  += dS^T Q_i      (SS, dS^T bf16 in smem, K-major view; acc [448,512))
 //                 dQ_i = dS K_j        (SS, same dS smem, MN-major view; TMEM [320,384))
-//    warps 2-5  thread = key row: P^T, dS^T from S^T, dP^T (mask only on partial
-//               tiles); final dK, dV -> bf16;
-//    warps 6-9  thread = query row: dQ_i partial -> red.global.add.v4.f32 into the
-//               fp32 accumulator (overlaps the next q-block's MMAs).
+//    warps 2-9  thread = key row (two warps per TMEM lane quarter, one 32-column
+//               chunk each): P^T, dS^T from S^T, dP^T (mask only on partial
+//               tiles); final dK (warps 6-9), dV (warps 2-5) -> bf16;
+//    warps 10-13 thread = query row: dQ_i partial -> smem -> TMA reduce-add into
+//               the fp32 accumulator (overlaps the next q-block's MMAs).
 // K9 dq_finalize    : fp32 accumulator -> bf16 dQ.
 #include "predicates.cuh"
 #include "sm100.cuh"
@@ -30,7 +31,7 @@ namespace hla {
 namespace {
 
 constexpr int kBlock = 128;
-constexpr int kThreads = 320;
+constexpr int kThreads = 448;   // 14 warps: TMA, MMA, 8 x P/dS, 4 x dQ
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColS = 0, kColDP = 128, kColP = 256, kColDQ = 320, kColDV = 384, kColDK = 448;
 constexpr float kLog2e = 1.4426950408889634f;
@@ -60,9 +61,11 @@ struct BwdSmem {
   alignas(1024) uint8_t q[2][kTileBytes];
   alignas(1024) uint8_t dO[2][kTileBytes];
   alignas(1024) uint8_t ds[2][2 * 128 * 128];   // dS^T bf16 x2 (tile parity): [q/64][kv 128][64 q], SWIZZLE_128B
+  alignas(1024) float dq_stage[kBlock * 32];    // fp32 dQ half tile [128][32], SWIZZLE_128B
   alignas(16) float lse[2][kBlock];
   alignas(16) float dd[2][kBlock];
   uint64_t kv_full[2], kv_empty[2], q_full[2], q_empty[2], s_full[2], ds_ready[2], dq_full, dq_free, dkv_full;
+  uint64_t dbg_bar;
   uint32_t tmem_base;
 };
 
@@ -140,7 +143,7 @@ template <int D, bool kTwoD, bool kGather>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                    const BwdParams prm) {
+                    const __grid_constant__ CUtensorMap tmDQ, const BwdParams prm) {
   extern __shared__ uint8_t smem_raw[];
   BwdSmem<D>& sm = *reinterpret_cast<BwdSmem<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -156,11 +159,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int hh = 0; hh < 2; ++hh) {
       sm100::mbar_init(&sm.s_full[hh], 1);
-      sm100::mbar_init(&sm.ds_ready[hh], 128);
+      sm100::mbar_init(&sm.ds_ready[hh], 256);
     }
     sm100::mbar_init(&sm.dq_full, 1);
     sm100::mbar_init(&sm.dq_free, 128);
     sm100::mbar_init(&sm.dkv_full, 1);
+    sm100::mbar_init(&sm.dbg_bar, 1);
     sm100::fence_mbar_init();
     sm100::tma_prefetch_desc(&tmQ);
     sm100::tma_prefetch_desc(&tmK);
@@ -176,6 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   sm100::tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
   unsigned long long tiles_done = 0;
+  HLA_TR_DECL;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -190,6 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t bh = (int64_t)b * prm.heads + h;
         const int kvs = n & 1;
         if (n >= 2) sm100::mbar_wait(&sm.kv_empty[kvs], ((n >> 1) - 1) & 1);
+        if (lane == 0) HLA_TR((3 << 24) | ((1) << 16) | (n));
         if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.kv_full[kvs], 2 * BwdSmem<D>::kTileBytes);
         __syncwarp();
         load_rows<D, kGather>(sm.k[kvs], &tmK, &sm.kv_full[kvs], h, b, prm.N, kb * kBlock, prm.s2c, pol_kv, lane);
@@ -197,6 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = 0; t < nt; ++t, ++g) {
           const int s = g & 1;
           if (g >= 2) sm100::mbar_wait(&sm.q_empty[s], ((g >> 1) - 1) & 1);
+          if (lane == 0) HLA_TR((3 << 24) | ((2) << 16) | (g));
           const int32_t qblk = __ldg(prm.t_col_idx + rs + t);
           if (lane == 0) {
             sm100::mbar_arrive_expect_tx(&sm.q_full[s], 2 * BwdSmem<D>::kTileBytes + 2 * kBlock * 4);
@@ -248,6 +255,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           sm100::mma_ss(tDK, ds_kmajor_desc(ds, kk), mnmajor_desc<D>(sm.q[s], kk), idesc_kv, acc);
         }
       };
+#ifdef HLA_TRACE
+      uint32_t dbg_phase = 0;
+      // trace builds: serialise after each MMA group and record its tensor-core time
+      auto mma_probe = [&](int ev, uint32_t gg) {
+        sm100::mma_commit(&sm.dbg_bar);
+        sm100::mbar_wait(&sm.dbg_bar, dbg_phase);
+        dbg_phase ^= 1;
+        HLA_TR((5 << 24) | (ev << 16) | gg);
+      };
+#else
+      auto mma_probe = [](int, uint32_t) {};
+#endif
       if (cur.valid) {
         sm100::mbar_wait(&sm.kv_full[cur.n & 1], (cur.n >> 1) & 1);
         sm100::mbar_wait(&sm.q_full[0], 0);
@@ -262,37 +281,55 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool last_of_unit = cur.t == cur.nt - 1;
         // half A of tile g
         sm100::mbar_wait(&sm.ds_ready[0], g & 1);
+        HLA_TR((1 << 24) | ((1) << 16) | (g));
         sm100::tc_fence_after();
+        HLA_TR((5 << 24) | (0 << 16) | g);
         issue_dvdk(g, 0, cur.t == 0);
+        mma_probe(1, g);
         if (nxt.valid) {
           if (nxt.t == 0) sm100::mbar_wait(&sm.kv_full[nxt.n & 1], (nxt.n >> 1) & 1);
           sm100::mbar_wait(&sm.q_full[(g + 1) & 1], ((g + 1) >> 1) & 1);
+          HLA_TR((1 << 24) | ((4) << 16) | (g));
           sm100::tc_fence_after();
+          HLA_TR((5 << 24) | (0 << 16) | g);
           issue_sdp(nxt, g + 1, 0);
+          mma_probe(2, g);
         }
         // half B of tile g, then dQ (needs both halves of dS)
         sm100::mbar_wait(&sm.ds_ready[1], g & 1);
+        HLA_TR((1 << 24) | ((2) << 16) | (g));
         sm100::tc_fence_after();
+        HLA_TR((5 << 24) | (0 << 16) | g);
         issue_dvdk(g, 1, false);
+        mma_probe(3, g);
+        sm100::mma_commit(&sm.q_empty[g & 1]);   // Q_g / dO_g no longer read (dQ needs only dS and K)
         if (last_of_unit) sm100::mma_commit(&sm.dkv_full);
         if (g > 0) {
           sm100::mbar_wait(&sm.dq_free, (g - 1) & 1);
+          HLA_TR((1 << 24) | ((3) << 16) | (g));
           sm100::tc_fence_after();
         }
 #pragma unroll
         for (int kk = 0; kk < kBlock / 16; ++kk)
           sm100::mma_ss(tDQ, ds_mnmajor_desc(sm.ds[g & 1], kk), mnmajor_desc<D>(sm.k[kvs], kk), idesc_q, kk > 0);
-        sm100::mma_commit(&sm.q_empty[g & 1]);
+        mma_probe(4, g);
         sm100::mma_commit(&sm.dq_full);
         if (last_of_unit) sm100::mma_commit(&sm.kv_empty[kvs]);
-        if (nxt.valid) issue_sdp(nxt, g + 1, 1);
+        if (nxt.valid) {
+          HLA_TR((5 << 24) | (0 << 16) | g);
+          issue_sdp(nxt, g + 1, 1);
+          mma_probe(5, g);
+        }
         cur = nxt;
         ++g;
       }
     }
-  } else if (warp < 6) {
+  } else if (warp < 10) {
     // --------------------------------------------- P^T / dS^T (thread = key row)
+    // two warp sets (cset 0: warps 2-5, cset 1: warps 6-9) share every TMEM lane
+    // quarter; within each q-half, cset c processes the 32-column chunk 2*half + c.
     const int quarter = warp & 3;
+    const int cset = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = prm.scale_log2, scale = prm.scale;
@@ -305,67 +342,72 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = 0; t < nt; ++t, ++g) {
         const int s = g & 1;
         sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1);
-        sm.lse[s][row] *= kLog2e;                     // LSE in the log2 domain
-        sm100::named_bar_sync(1, 128);
+        if (row == 0 && cset == 0) HLA_TR((2 << 24) | ((1) << 16) | (g));
+        if (cset == 0) {  // LSE -> log2 domain, in place (thread `row` converts entry `row`)
+          const uint32_t a = sm100::smem_u32(&sm.lse[s][row]);
+          sm100::sts_f32(a, sm100::lds_f32(a) * kLog2e);
+        }
+        sm100::named_bar_sync(1, 256);
         const uint8_t kd = __ldg(prm.t_kind + rs + t);
         const int32_t q0 = __ldg(prm.t_col_idx + rs + t) * kBlock;
-        const float* lse2 = sm.lse[s];
-        const float* dd = sm.dd[s];
-        uint8_t* dsbuf = sm.ds[g & 1];
+        const uint32_t lse2 = sm100::smem_u32(sm.lse[s]);
+        const uint32_t dd = sm100::smem_u32(sm.dd[s]);
+        const uint32_t dsbuf = sm100::smem_u32(sm.ds[g & 1]);
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
           sm100::mbar_wait(&sm.s_full[half], g & 1);
+          if (row == 0 && cset == 0) HLA_TR((2 << 24) | ((2 + 2 * half) << 16) | (g));
           sm100::tc_fence_after();
-#pragma unroll 1
-          for (int c = 2 * half; c < 2 * half + 2; ++c) {
+          {
+            const int c = 2 * half + cset;
             uint32_t sr[32], dpr[32];
             sm100::tmem_ld32(tmem + lane_off + kColS + c * 32, sr);
             sm100::tmem_ld32(tmem + lane_off + kColDP + c * 32, dpr);
             sm100::tmem_wait_ld();
-            float p[32];
-#pragma unroll
-            for (int e = 0; e < 32; ++e) p[e] = sm100::ex2(fmaf(__uint_as_float(sr[e]), sl2, -lse2[c * 32 + e]));
-            if (kd == 2) {
-#pragma unroll
-              for (int e = 0; e < 32; ++e) {
-                const int32_t qq = q0 + c * 32 + e;
-                bool ok;
-                if (!kTwoD) {
-                  ok = (uint32_t)(qq - box.lo) < (uint32_t)box.len;
-                } else {
-                  const int32_t rq = prm.pat.log2W >= 0 ? (qq >> prm.pat.log2W) : qq / prm.pat.W;
-                  const int32_t cq = qq - rq * prm.pat.W;
-                  ok = ((uint32_t)(rq - box.lo) < (uint32_t)box.len) && ((uint32_t)(cq - box.c0) < (uint32_t)box.cn);
-                }
-                if (!ok) p[e] = 0.f;
-              }
-            }
             uint32_t pk[16];
 #pragma unroll
-            for (int e = 0; e < 16; ++e) pk[e] = sm100::pack_bf16(p[2 * e], p[2 * e + 1]);
-            sm100::tmem_st16(tmem + lane_off + kColP + c * 16, pk);
-            // dS^T row -> smem [q/64][kv][64] with the 128B swizzle (16B chunks)
+            for (int u4 = 0; u4 < 4; ++u4) {   // 8 query columns (one 16B dS chunk) at a time
+              const int qc = c * 32 + u4 * 8;
+              const float4 la = sm100::lds_f4(lse2 + qc * 4), lb = sm100::lds_f4(lse2 + qc * 4 + 16);
+              const float4 da = sm100::lds_f4(dd + qc * 4), db = sm100::lds_f4(dd + qc * 4 + 16);
+              const float lv[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
+              const float dv[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
+              float p[8];
 #pragma unroll
-            for (int u4 = 0; u4 < 4; ++u4) {
-              const int qc = c * 32 + u4 * 8;             // first q column of this 16B chunk
+              for (int e = 0; e < 8; ++e) p[e] = sm100::ex2(fmaf(__uint_as_float(sr[u4 * 8 + e]), sl2, -lv[e]));
+              if (kd == 2) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  const int32_t qq = q0 + qc + e;
+                  bool ok;
+                  if (!kTwoD) {
+                    ok = (uint32_t)(qq - box.lo) < (uint32_t)box.len;
+                  } else {
+                    const int32_t rq = prm.pat.log2W >= 0 ? (qq >> prm.pat.log2W) : qq / prm.pat.W;
+                    const int32_t cq = qq - rq * prm.pat.W;
+                    ok = ((uint32_t)(rq - box.lo) < (uint32_t)box.len) && ((uint32_t)(cq - box.c0) < (uint32_t)box.cn);
+                  }
+                  if (!ok) p[e] = 0.f;
+                }
+              }
               float ds[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e)
-                ds[e] = p[u4 * 8 + e] * scale * (__uint_as_float(dpr[u4 * 8 + e]) - dd[qc + e]);
-              uint4 w;
-              w.x = sm100::pack_bf16(ds[0], ds[1]);
-              w.y = sm100::pack_bf16(ds[2], ds[3]);
-              w.z = sm100::pack_bf16(ds[4], ds[5]);
-              w.w = sm100::pack_bf16(ds[6], ds[7]);
+              for (int e = 0; e < 8; ++e) ds[e] = p[e] * scale * (__uint_as_float(dpr[u4 * 8 + e]) - dv[e]);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) pk[u4 * 4 + e] = sm100::pack_bf16(p[2 * e], p[2 * e + 1]);
+              // dS^T row -> smem [q/64][kv][64] with the 128B swizzle (16B chunks)
               const uint32_t off =
                   (uint32_t)(qc >> 6) * 16384u + sm100::swz128((uint32_t)row * 128u + (uint32_t)(qc & 63) * 2u);
-              *reinterpret_cast<uint4*>(dsbuf + off) = w;
+              sm100::sts_u4(dsbuf + off, sm100::pack_bf16(ds[0], ds[1]), sm100::pack_bf16(ds[2], ds[3]),
+                            sm100::pack_bf16(ds[4], ds[5]), sm100::pack_bf16(ds[6], ds[7]));
             }
+            sm100::tmem_st16(tmem + lane_off + kColP + c * 16, pk);
           }
           sm100::tmem_wait_st();
           sm100::fence_proxy_async_smem();
           sm100::tc_fence_before();
           sm100::mbar_arrive(&sm.ds_ready[half]);
+          if (row == 0 && cset == 0) HLA_TR((2 << 24) | ((3 + 2 * half) << 16) | (g));
         }
       }
       // final dK, dV rows -> bf16 (dS already carries the softmax scale)
@@ -375,11 +417,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint4* dvp = reinterpret_cast<uint4*>(prm.dv + grow * D);
       if (nt > 0) {
         sm100::mbar_wait(&sm.dkv_full, n & 1);
+        if (row == 0 && cset == 0) HLA_TR((2 << 24) | ((6) << 16) | (n));
         sm100::tc_fence_after();
-#pragma unroll
-        for (int which = 0; which < 2; ++which) {
-          uint4* dst = which == 0 ? dvp : dkp;
-          const uint32_t col = which == 0 ? kColDV : kColDK;
+        {  // cset 0 writes dV, cset 1 writes dK
+          uint4* dst = cset == 0 ? dvp : dkp;
+          const uint32_t col = cset == 0 ? kColDV : kColDK;
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
             uint32_t r[32];
@@ -396,47 +438,59 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
+        if (row == 0 && cset == 0) HLA_TR((2 << 24) | ((7) << 16) | (n));
         ++n;
       } else {
 #pragma unroll
-        for (int c = 0; c < D / 8; ++c) {
-          dkp[c] = make_uint4(0, 0, 0, 0);
-          dvp[c] = make_uint4(0, 0, 0, 0);
-        }
+        for (int c = 0; c < D / 8; ++c) (cset == 0 ? dvp : dkp)[c] = make_uint4(0, 0, 0, 0);
       }
       tiles_done += nt;
     }
   } else {
     // ------------------------------------------ dQ partial -> fp32 accumulator
+    // thread = query row: drain the dQ_i tile from TMEM (then release it), stage it
+    // in shared memory (two 32-column halves, 128B swizzle) and let the TMA engine
+    // add it into the fp32 accumulator (cp.reduce.async.bulk.tensor ... add) -- no
+    // per-thread atomics, so the LSU stays free for the compute warps.
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const bool leader = warp == 10 && lane == 0;
     uint32_t g = 0;
     for (int32_t u = blockIdx.x; u < units; u += gridDim.x) {
       const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
       const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
       for (int t = 0; t < nt; ++t, ++g) {
         sm100::mbar_wait(&sm.dq_full, g & 1);
+        if (leader) HLA_TR((4 << 24) | ((1) << 16) | (g));
         sm100::tc_fence_after();
-        const int32_t qidx = __ldg(prm.t_col_idx + rs + t) * kBlock + row;
-        const int32_t qcell = kGather ? __ldg(prm.s2c + qidx) : qidx;   // dQ accumulated in grid order
-        float* dst = prm.dq_acc + (((int64_t)b * prm.N + qcell) * prm.heads + h) * D;
+        const int32_t qrow = b * prm.N + __ldg(prm.t_col_idx + rs + t) * kBlock;   // sequence order
+        uint32_t r[D];
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t r[32];
-          sm100::tmem_ld32(tmem + lane_off + kColDQ + c * 32, r);
-          sm100::tmem_wait_ld();
-          if (c == D / 32 - 1) {
-            sm100::tc_fence_before();
-            sm100::mbar_arrive(&sm.dq_free);   // TMEM dQ tile may be overwritten
+        for (int c = 0; c < D / 32; ++c) sm100::tmem_ld32(tmem + lane_off + kColDQ + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
+        sm100::tmem_wait_ld();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&sm.dq_free);     // the TMEM dQ tile may now be overwritten
+#pragma unroll
+        for (int hh = 0; hh < D / 32; ++hh) {
+          if (leader) sm100::bulk_wait_group_read0();   // previous reduce finished reading the stage
+          sm100::named_bar_sync(2, 128);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t off = sm100::swz128((uint32_t)row * 128u + (uint32_t)j * 16u);
+            sm100::sts_u4(sm100::smem_u32(sm.dq_stage) + off, r[hh * 32 + 4 * j], r[hh * 32 + 4 * j + 1],
+                          r[hh * 32 + 4 * j + 2], r[hh * 32 + 4 * j + 3]);
           }
-#pragma unroll
-          for (int v4 = 0; v4 < 8; ++v4)
-            red_add_v4(dst + c * 32 + v4 * 4, __uint_as_float(r[v4 * 4 + 0]), __uint_as_float(r[v4 * 4 + 1]),
-                       __uint_as_float(r[v4 * 4 + 2]), __uint_as_float(r[v4 * 4 + 3]));
+          sm100::fence_proxy_async_smem();
+          sm100::named_bar_sync(2, 128);
+          if (leader) {
+            sm100::tma_reduce_add_3d(&tmDQ, sm.dq_stage, hh * 32, h, qrow);
+            sm100::bulk_commit_group();
+          }
         }
       }
     }
+    if (leader) sm100::bulk_wait_group0();
   }
 
   sm100::tc_fence_before();
@@ -481,24 +535,33 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
   if (part == 0) dsum[(bb * heads + hq) * N + s] = acc;
 }
 
-// K9: dQ = bf16(accumulator)
+// K9: dQ = bf16(accumulator) -- the accumulator is in sequence order; under the
+// fused reorder each row is written to its grid cell s2c[s] (SURVEY 8(a) a8:
+// "dQ finalize + inverse permutation").
 __global__ void __launch_bounds__(256) dq_finalize_kernel(const float4* __restrict__ acc, uint2* __restrict__ dq,
-                                                          int64_t n4) {
+                                                          const int32_t* __restrict__ s2c, int32_t N,
+                                                          int32_t row_f4, int64_t n4) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     const float4 v = acc[i];
-    dq[i] = make_uint2(sm100::pack_bf16(v.x, v.y), sm100::pack_bf16(v.z, v.w));
+    int64_t o = i;
+    if (s2c) {   // i = ((b * N + s) * row_f4 + part) with row_f4 = heads * D / 4
+      const int64_t part = i % row_f4, bs = i / row_f4;
+      const int64_t s = bs % N, b = bs / N;
+      o = (b * N + __ldg(s2c + s)) * row_f4 + part;
+    }
+    dq[o] = make_uint2(sm100::pack_bf16(v.x, v.y), sm100::pack_bf16(v.z, v.w));
   }
 }
 
 template <int D, bool kTwoD, bool kGather>
 hla_status launch_bwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mdo,
-                      const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream) {
+                      const CUtensorMap& mdq, const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream) {
   const size_t smem = sizeof(BwdSmem<D>) + 1024;
   auto* fn = attn_bwd_kernel<D, kTwoD, kGather>;
   HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t units = (int64_t)n_kblocks * prm.heads * prm.batch;
   const int grid = (int)std::min<int64_t>(units, (int64_t)num_sms());
-  fn<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mdo, prm);
+  fn<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mdo, mdq, prm);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
 }
@@ -604,21 +667,23 @@ extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_blo
   if ((st = mk_map(&mk, k)) != HLA_OK) return st;
   if ((st = mk_map(&mv, v)) != HLA_OK) return st;
   if ((st = mk_map(&mdo, dout)) != HLA_OK) return st;
+  CUtensorMap mdq;   // fp32 dQ accumulator, sequence order, 32-float (128 B) boxes for the TMA reduce-add
+  if ((st = make_f32_rows_map(&mdq, dq_acc, tok, heads, head_dim, 32, kBlock)) != HLA_OK) return st;
   const bool two_d = pat.kind == K_WSA || pat.kind == K_SA || pat.kind == K_NA2D;
   const int32_t mkb = pat.N / kBlock;
   if (head_dim == 64) {
-    if (gather) return launch_bwd<64, false, true>(mq, mk, mv, mdo, prm, mkb, stream);
-    return two_d ? launch_bwd<64, true, false>(mq, mk, mv, mdo, prm, mkb, stream)
-                 : launch_bwd<64, false, false>(mq, mk, mv, mdo, prm, mkb, stream);
+    if (gather) return launch_bwd<64, false, true>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
+    return two_d ? launch_bwd<64, true, false>(mq, mk, mv, mdo, mdq, prm, mkb, stream)
+                 : launch_bwd<64, false, false>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
   }
-  if (gather) return launch_bwd<32, false, true>(mq, mk, mv, mdo, prm, mkb, stream);
-  return two_d ? launch_bwd<32, true, false>(mq, mk, mv, mdo, prm, mkb, stream)
-               : launch_bwd<32, false, false>(mq, mk, mv, mdo, prm, mkb, stream);
+  if (gather) return launch_bwd<32, false, true>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
+  return two_d ? launch_bwd<32, true, false>(mq, mk, mv, mdo, mdq, prm, mkb, stream)
+               : launch_bwd<32, false, false>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
 }
 
 extern "C" hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,
                                             const void* workspace, size_t workspace_bytes, void* dq,
-                                            cudaStream_t stream) {
+                                            const int32_t* seq_to_cell, cudaStream_t stream) {
   clear_error();
   HLA_REQUIRE(head_dim == 32 || head_dim == 64, HLA_ERR_UNSUPPORTED, "head_dim %d not in {32, 64}", head_dim);
   HLA_REQUIRE(dq && (uintptr_t)dq % 16 == 0, HLA_ERR_INVALID, "dq null or unaligned");
@@ -629,7 +694,8 @@ extern "C" hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_
   const int64_t n4 = (int64_t)batch * n * heads * head_dim / 4;
   const unsigned blocks = (unsigned)std::min<int64_t>((n4 + 255) / 256, 148 * 16);
   dq_finalize_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const float4*>(dq_acc),
-                                                 reinterpret_cast<uint2*>(dq), n4);
+                                                 reinterpret_cast<uint2*>(dq), seq_to_cell, n,
+                                                 heads * head_dim / 4, n4);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
 }
@@ -655,5 +721,5 @@ extern "C" hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_ma
   if ((st = hla_attn_bwd_main(d, m, batch, heads, head_dim, scale, q, k, v, lse, dout, dk, dv, seq_to_cell,
                               workspace, workspace_bytes, tiles_visited, stream)) != HLA_OK)
     return st;
-  return hla_attn_bwd_finalize(batch, heads, pat.N, head_dim, workspace, workspace_bytes, dq, stream);
+  return hla_attn_bwd_finalize(batch, heads, pat.N, head_dim, workspace, workspace_bytes, dq, seq_to_cell, stream);
 }

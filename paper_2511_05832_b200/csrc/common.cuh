@@ -3,6 +3,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include <cuda_runtime.h>
@@ -69,5 +70,28 @@ inline int num_sms() {
 
 inline bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
 inline int ilog2(int64_t x) { int l = 0; while ((1ll << l) < x) ++l; return l; }
+
+// ---- optional device-side event trace (dev builds only: make TRACE=1) ----------
+// CTA 0 only; every tracing thread keeps its own counter (HLA_TR_DECL) and writes
+// (tag, clock) pairs into the region of its role (tag >> 24), no atomics.
+#ifdef HLA_TRACE
+extern __device__ unsigned long long g_hla_trace[8 * 1024 * 2];
+#define HLA_TR_DECL unsigned int _hla_tr = 0
+#define HLA_TR(tag)                                                                       \
+  do {                                                                                    \
+    if (blockIdx.x == 0 && _hla_tr < 1024) {                                              \
+      const unsigned int _s = (((unsigned int)(tag) >> 24) & 7u) * 1024u + _hla_tr++;     \
+      ::hla::g_hla_trace[2 * _s] = (unsigned long long)(tag);                             \
+      ::hla::g_hla_trace[2 * _s + 1] = clock64();                                         \
+    }                                                                                     \
+  } while (0)
+#else
+#define HLA_TR_DECL \
+  do {              \
+  } while (0)
+#define HLA_TR(tag) \
+  do {              \
+  } while (0)
+#endif
 
 }  // namespace hla

@@ -101,6 +101,55 @@ __global__ void __launch_bounds__(128) debug_umma_kernel(const __nv_bfloat16* __
   if (warp == 0) sm100::tmem_dealloc(tmem, 512);
 }
 
+// Tensor-core rate probe: `iters` back-to-back tcgen05.mma (M=128, N, K=16 each) on
+// operands already in shared memory / TMEM (contents irrelevant), one commit at the
+// end; returns elapsed SM cycles in out[0].
+__global__ void __launch_bounds__(128) debug_mma_rate_kernel(int N, int iters, int a_mn, int b_mn, int a_tmem,
+                                                             long long* out) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) {
+    sm100::tmem_alloc(&tmem_base, 512);
+    sm100::tmem_relinquish();
+  }
+  if (tid == 0) {
+    sm100::mbar_init(&bar, 1);
+    sm100::fence_mbar_init();
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  if (tid == 0) {
+    const uint32_t idesc = sm100::make_idesc_bf16(128, N, a_mn != 0, b_mn != 0);
+    const uint32_t a_base = sm100::smem_u32(base), b_base = sm100::smem_u32(base + 128 * 128 * 2);
+    const uint64_t adesc0 = sm100::make_smem_desc(a_base, a_mn ? 128 * 128 : 16, 1024, sm100::kSwizzle128B);
+    const uint64_t bdesc0 = sm100::make_smem_desc(b_base, b_mn ? 128 * 128 : 16, 1024, sm100::kSwizzle128B);
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      const int s = i & 3;   // cycle over 4 k-steps of a 64-wide K atom
+      const uint64_t ad = adesc0 + (uint64_t)((a_mn ? s * 2048 : s * 32) >> 4);
+      const uint64_t bd = bdesc0 + (uint64_t)((b_mn ? s * 2048 : s * 32) >> 4);
+      // a_tmem bit 1 (value 2/3): alternate between two independent accumulators
+      const uint32_t dcol = (a_tmem & 2) ? (uint32_t)((i & 1) * (N <= 128 ? 128 : 0)) : 0u;
+      if (a_tmem & 1)
+        sm100::mma_ts(tmem + dcol, tmem + 256 + s * 8, bd, idesc, 1);
+      else
+        sm100::mma_ss(tmem + dcol, ad, bd, idesc, 1);
+    }
+    sm100::mma_commit(&bar);
+    sm100::mbar_wait(&bar, 0);
+    out[0] = clock64() - t0;
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  if (warp == 0) sm100::tmem_dealloc(tmem, 512);
+}
+
 // 128 token rows (indices idx[0..127]) of head h gathered with .tile::gather4 into a
 // SWIZZLE_<2d> tile, then read back through the swizzle into out[128][d].
 template <int D>
@@ -133,6 +182,17 @@ __global__ void __launch_bounds__(128) debug_gather_kernel(const __grid_constant
 }  // namespace hla
 
 using namespace hla;
+
+extern "C" hla_status hla_debug_mma_rate(int32_t N, int32_t iters, int32_t a_major_mn, int32_t b_major_mn,
+                                         int32_t a_from_tmem, long long* out_cycles, cudaStream_t stream) {
+  clear_error();
+  HLA_REQUIRE(N % 16 == 0 && N >= 16 && N <= 256 && iters > 0, HLA_ERR_INVALID, "bad N/iters");
+  const size_t smem = 1024 + 2 * 128 * 256 * 2;
+  HLA_CUDA_TRY(cudaFuncSetAttribute(debug_mma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  debug_mma_rate_kernel<<<1, 128, smem, stream>>>(N, iters, a_major_mn, b_major_mn, a_from_tmem, out_cycles);
+  HLA_CUDA_TRY(cudaGetLastError());
+  return HLA_OK;
+}
 
 extern "C" hla_status hla_debug_gather4(const void* src, int64_t rows, int32_t heads, int32_t head_dim,
                                         const int32_t* idx, int32_t head, int32_t box_h, void* out,

@@ -69,4 +69,22 @@ inline hla_status make_gather_map(CUtensorMap* map, const void* base, int64_t ro
   return HLA_OK;
 }
 
+// fp32 tensor [rows_total, heads, head_dim] as 3-D (head_dim, heads, rows); box =
+// (box_cols, 1, box_rows), SWIZZLE_128B (box_cols * 4 == 128).
+inline hla_status make_f32_rows_map(CUtensorMap* map, const void* base, int64_t rows_total, int heads, int head_dim,
+                                    int box_cols, int box_rows) {
+  EncodeTiledFn enc;
+  hla_status st = get_encode_fn(&enc);
+  if (st != HLA_OK) return st;
+  cuuint64_t dims[3] = {(cuuint64_t)head_dim, (cuuint64_t)heads, (cuuint64_t)rows_total};
+  cuuint64_t strides[2] = {(cuuint64_t)head_dim * 4, (cuuint64_t)heads * head_dim * 4};
+  cuuint32_t box[3] = {(cuuint32_t)box_cols, 1, (cuuint32_t)box_rows};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  HLA_REQUIRE(r == CUDA_SUCCESS, HLA_ERR_CUDA, "cuTensorMapEncodeTiled (f32) failed (%d)", (int)r);
+  return HLA_OK;
+}
+
 }  // namespace hla
