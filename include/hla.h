@@ -212,17 +212,19 @@ HLA_API hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_mask*
  * a7, a8) so they can be timed / overlapped individually.  Same arguments and
  * limits as hla_attn_bwd; the workspace carries D and the fp32 dQ accumulator
  * from one stage to the next and must not be touched in between.
- *   preprocess: D = rowsum(dO o O) (fp32), dQ accumulator := 0
+ *   preprocess: D = rowsum(dO o O) (fp32, stored x scale), LSE -> log2 domain,
+ *               dQ accumulator := 0 (all into the workspace)
  *   main      : the tcgen05 kernel over the transposed lists; writes dK, dV and
  *               accumulates dQ (fp32, TMA reduce-add, sequence order)
  *   finalize  : dQ = bf16(accumulator), written to grid cells when seq_to_cell
  *               is given (fused inverse reorder)                              */
 HLA_API hla_status hla_attn_bwd_preprocess(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,
-                                   const void* o, const void* dout, const int32_t* seq_to_cell,
+                                   float scale, const void* o, const void* dout, const float* lse,
+                                   const int32_t* seq_to_cell,
                                    void* workspace, size_t workspace_bytes, cudaStream_t stream);
 HLA_API hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_block_mask* m,
                              int32_t batch, int32_t heads, int32_t head_dim, float scale,
-                             const void* q, const void* k, const void* v, const float* lse,
+                             const void* q, const void* k, const void* v,
                              const void* dout, void* dk, void* dv, const int32_t* seq_to_cell,
                              void* workspace, size_t workspace_bytes,
                              int64_t* tiles_visited, cudaStream_t stream);

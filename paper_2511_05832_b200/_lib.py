@@ -60,8 +60,8 @@ def lib():
                             ctypes.POINTER(ctypes.c_double)],
         "hla_attn_fwd": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp],
         "hla_attn_bwd": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp],
-        "hla_attn_bwd_preprocess": [i32, i32, i32, i32, vp, vp, vp, vp, sz, vp],
-        "hla_attn_bwd_main": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp],
+        "hla_attn_bwd_preprocess": [i32, i32, i32, i32, f32, vp, vp, vp, vp, vp, sz, vp],
+        "hla_attn_bwd_main": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp],
         "hla_attn_bwd_finalize": [i32, i32, i32, i32, vp, sz, vp, vp, vp],
         "hla_debug_umma": [vp, vp, vp, i32, i32, i32, i32, i32, i32, vp],
         "hla_debug_gather4": [vp, i64, i32, i32, vp, i32, i32, vp, vp],

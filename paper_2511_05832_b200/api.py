@@ -166,19 +166,20 @@ def hla_attn_bwd(desc, mask, q, k, v, o, lse, dout, scale=0.0, dq=None, dk=None,
     return dq, dk, dv
 
 
-def hla_attn_bwd_preprocess(o, dout, workspace, seq_to_cell=None, stream=None):
+def hla_attn_bwd_preprocess(o, dout, lse, workspace, scale=0.0, seq_to_cell=None, stream=None):
     B, N, H, D = o.shape
-    check("hla_attn_bwd_preprocess", lib().hla_attn_bwd_preprocess(B, H, N, D, _ptr(o), _ptr(dout), _ptr(seq_to_cell),
-                                                                   _ptr(workspace), workspace.numel(),
-                                                                   _stream(stream)))
+    check("hla_attn_bwd_preprocess", lib().hla_attn_bwd_preprocess(B, H, N, D, float(scale), _ptr(o), _ptr(dout),
+                                                                   _ptr(lse), _ptr(seq_to_cell), _ptr(workspace),
+                                                                   workspace.numel(), _stream(stream)))
 
 
-def hla_attn_bwd_main(desc, mask, q, k, v, lse, dout, dk, dv, workspace, scale=0.0, tiles_visited=None,
+def hla_attn_bwd_main(desc, mask, q, k, v, dout, dk, dv, workspace, scale=0.0, tiles_visited=None,
                       seq_to_cell=None, stream=None):
+    """Requires hla_attn_bwd_preprocess to have filled `workspace` (D, LSE in log2 domain)."""
     B, N, H, D = q.shape
     mc = mask.c
     check("hla_attn_bwd_main", lib().hla_attn_bwd_main(ctypes.byref(desc), ctypes.byref(mc), B, H, D, float(scale),
-                                                       _ptr(q), _ptr(k), _ptr(v), _ptr(lse), _ptr(dout), _ptr(dk),
+                                                       _ptr(q), _ptr(k), _ptr(v), _ptr(dout), _ptr(dk),
                                                        _ptr(dv), _ptr(seq_to_cell), _ptr(workspace),
                                                        workspace.numel(), _ptr(tiles_visited), _stream(stream)))
 

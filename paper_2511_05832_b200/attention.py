@@ -89,9 +89,9 @@ class HilbertLocalAttention:
             dout_s, dq, dk, dv = self.dos, self.dqs, self.dks, self.dvs
         else:
             dout_s, dq, dk, dv = dout, self.dq, self.dk, self.dv
-        api.hla_attn_bwd_preprocess(o, dout_s, self.workspace, seq_to_cell=self.s2c)
+        api.hla_attn_bwd_preprocess(o, dout_s, self.lse, self.workspace, self.scale, seq_to_cell=self.s2c)
         mark("bwd_pre")
-        api.hla_attn_bwd_main(self.desc, self.mask, q, k, v, self.lse, dout_s, dk, dv, self.workspace, self.scale,
+        api.hla_attn_bwd_main(self.desc, self.mask, q, k, v, dout_s, dk, dv, self.workspace, self.scale,
                               seq_to_cell=self.s2c)
         mark("bwd")
         api.hla_attn_bwd_finalize(self.workspace, dq, seq_to_cell=self.s2c)

@@ -44,8 +44,8 @@ struct BwdParams {
   const int32_t* t_row_ptr;
   const int32_t* t_col_idx;
   const uint8_t* t_kind;
-  const float* lse;        // [B, H, N]
-  const float* dsum;       // D, [B, H, N]
+  const float* lse2;       // LSE * log2(e), [B, H, N] (workspace, from the preprocess)
+  const float* dsum;       // D * scale, [B, H, N] (workspace, from the preprocess)
   float* dq_acc;           // [B, N, H, Dh] fp32 (grid order when s2c != null)
   const int32_t* s2c;      // fused reorder: seq_to_cell table (tensors in grid order), else null
   __nv_bfloat16* dk;
@@ -89,14 +89,23 @@ __device__ __forceinline__ uint64_t ds_mnmajor_desc(const uint8_t* ds, int kstep
   return sm100::make_smem_desc(sm100::smem_u32(ds) + kstep * 2048, 16384, 1024, sm100::kSwizzle128B);
 }
 
+// k-th work unit of this CTA: pairs of consecutive kv-blocks (2p, 2p+1), pairs
+// strided over the grid.  Consecutive kv-blocks share q-blocks (the producer then
+// skips reloading a Q/dO stage), while all CTAs stay on nearby units (L2 reuse).
+__device__ __forceinline__ int32_t unit_at(int32_t k) {
+  return 2 * ((int32_t)blockIdx.x + (k >> 1) * (int32_t)gridDim.x) + (k & 1);
+}
+
 // Iterator over the flattened (work unit, q-block tile) sequence of this CTA,
 // skipping units without tiles.  n = ordinal of the current non-empty unit.
 struct TileIter {
-  int32_t u, t, nt;
+  int32_t k, u, t, nt;
   uint32_t n;
   bool valid;
   __device__ void seek(const int32_t* t_row_ptr, int32_t mk, int32_t units) {
-    for (; u < units; u += gridDim.x) {
+    for (;; ++k) {
+      u = unit_at(k);
+      if (u >= units) break;
       const int32_t kb = u % mk;
       nt = __ldg(t_row_ptr + kb + 1) - __ldg(t_row_ptr + kb);
       if (nt > 0) { valid = true; return; }
@@ -104,12 +113,12 @@ struct TileIter {
     valid = false;
   }
   __device__ void init(const int32_t* t_row_ptr, int32_t mk, int32_t units) {
-    u = blockIdx.x; t = 0; n = 0;
+    k = 0; t = 0; n = 0;
     seek(t_row_ptr, mk, units);
   }
   __device__ void advance(const int32_t* t_row_ptr, int32_t mk, int32_t units) {
     if (++t < nt) return;
-    t = 0; ++n; u += gridDim.x;
+    t = 0; ++n; ++k;
     seek(t_row_ptr, mk, units);
   }
 };
@@ -188,7 +197,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_kv = sm100::policy_evict_first();
       const uint64_t pol_q = sm100::policy_evict_last();
       uint32_t n = 0, g = 0;
-      for (int32_t u = blockIdx.x; u < units; u += gridDim.x) {
+      int64_t stage_tag0 = -1, stage_tag1 = -1;   // (b, h, q-block) held by stage 0 / 1
+      for (int32_t kq = 0;; ++kq) {
+        const int32_t u = unit_at(kq);
+        if (u >= units) break;
         const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
         const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
         if (nt == 0) continue;
@@ -205,9 +217,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (g >= 2) sm100::mbar_wait(&sm.q_empty[s], ((g >> 1) - 1) & 1);
           if (lane == 0) HLA_TR((3 << 24) | ((2) << 16) | (g));
           const int32_t qblk = __ldg(prm.t_col_idx + rs + t);
+          const int64_t tag = bh * prm.N + qblk;     // (b, h, q-block) held by the stage
+          if (tag == (s ? stage_tag1 : stage_tag0)) {
+            // the stage already holds this q-block (consecutive kv-blocks share
+            // q-blocks): no reload, just publish it again
+            if (lane == 0) sm100::mbar_arrive(&sm.q_full[s]);
+            continue;
+          }
+          if (s) stage_tag1 = tag; else stage_tag0 = tag;
           if (lane == 0) {
             sm100::mbar_arrive_expect_tx(&sm.q_full[s], 2 * BwdSmem<D>::kTileBytes + 2 * kBlock * 4);
-            sm100::bulk_load(sm.lse[s], prm.lse + bh * prm.N + qblk * kBlock, kBlock * 4, &sm.q_full[s]);
+            sm100::bulk_load(sm.lse[s], prm.lse2 + bh * prm.N + qblk * kBlock, kBlock * 4, &sm.q_full[s]);
             sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * kBlock, kBlock * 4, &sm.q_full[s]);
           }
           __syncwarp();
@@ -334,7 +354,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = prm.scale_log2, scale = prm.scale;
     uint32_t n = 0, g = 0;
-    for (int32_t u = blockIdx.x; u < units; u += gridDim.x) {
+    for (int32_t kq = 0;; ++kq) {
+        const int32_t u = unit_at(kq);
+        if (u >= units) break;
       const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
       const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
       const int32_t kidx = kb * kBlock + row;
@@ -343,11 +365,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = g & 1;
         sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1);
         if (row == 0 && cset == 0) HLA_TR((2 << 24) | ((1) << 16) | (g));
-        if (cset == 0) {  // LSE -> log2 domain, in place (thread `row` converts entry `row`)
-          const uint32_t a = sm100::smem_u32(&sm.lse[s][row]);
-          sm100::sts_f32(a, sm100::lds_f32(a) * kLog2e);
-        }
-        sm100::named_bar_sync(1, 256);
         const uint8_t kd = __ldg(prm.t_kind + rs + t);
         const int32_t q0 = __ldg(prm.t_col_idx + rs + t) * kBlock;
         const uint32_t lse2 = sm100::smem_u32(sm.lse[s]);
@@ -392,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
               float ds[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) ds[e] = p[e] * scale * (__uint_as_float(dpr[u4 * 8 + e]) - dv[e]);
+              for (int e = 0; e < 8; ++e) ds[e] = p[e] * fmaf(__uint_as_float(dpr[u4 * 8 + e]), scale, -dv[e]);
 #pragma unroll
               for (int e = 0; e < 4; ++e) pk[u4 * 4 + e] = sm100::pack_bf16(p[2 * e], p[2 * e + 1]);
               // dS^T row -> smem [q/64][kv][64] with the 128B swizzle (16B chunks)
@@ -457,7 +474,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const bool leader = warp == 10 && lane == 0;
     uint32_t g = 0;
-    for (int32_t u = blockIdx.x; u < units; u += gridDim.x) {
+    for (int32_t kq = 0;; ++kq) {
+        const int32_t u = unit_at(kq);
+        if (u >= units) break;
       const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
       const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
       for (int t = 0; t < nt; ++t, ++g) {
@@ -501,11 +520,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // K7: D = rowsum(dO o O) per (b, s, h) row of head_dim bf16, fp32, in sequence order s
-// (rows read at grid cell s2c[s] under the fused reorder); dQ accumulator := 0
+// (rows read at grid cell s2c[s] under the fused reorder), stored pre-multiplied by
+// the softmax scale; LSE converted to the log2 domain; dQ accumulator := 0
 template <int D>
 __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
                                                              const __nv_bfloat16* __restrict__ dout,
-                                                             float* __restrict__ dsum, float* __restrict__ dq_acc,
+                                                             const float* __restrict__ lse, float scale,
+                                                             float* __restrict__ dsum, float* __restrict__ lse2,
+                                                             float* __restrict__ dq_acc,
                                                              const int32_t* __restrict__ s2c, int32_t N,
                                                              int32_t heads, int64_t rows) {
   constexpr int kLanes = D / 8;   // lanes per row, 16 B (8 bf16) each
@@ -532,7 +554,11 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
   float4* z = reinterpret_cast<float4*>(dq_acc + r * D + part * 8);   // zeroing is layout-agnostic
   z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
   z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (part == 0) dsum[(bb * heads + hq) * N + s] = acc;
+  if (part == 0) {
+    const int64_t i = (bb * heads + hq) * N + s;
+    dsum[i] = acc * scale;                       // D * scale (dS = P o (dP * scale - D * scale))
+    lse2[i] = __ldg(lse + i) * kLog2e;           // LSE in the log2 domain
+  }
 }
 
 // K9: dQ = bf16(accumulator) -- the accumulator is in sequence order; under the
@@ -560,7 +586,7 @@ hla_status launch_bwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtens
   auto* fn = attn_bwd_kernel<D, kTwoD, kGather>;
   HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t units = (int64_t)n_kblocks * prm.heads * prm.batch;
-  const int grid = (int)std::min<int64_t>(units, (int64_t)num_sms());
+  const int grid = (int)std::min<int64_t>((units + 1) / 2, (int64_t)num_sms());   // pairs of units
   fn<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mdo, mdq, prm);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
@@ -573,55 +599,60 @@ using namespace hla;
 
 extern "C" size_t hla_attn_bwd_workspace(int32_t batch, int32_t heads, int32_t n, int32_t head_dim) {
   const size_t acc = (size_t)batch * n * heads * head_dim * 4;
-  const size_t dsum = (size_t)batch * heads * n * 4;
-  return ((acc + 255) / 256) * 256 + ((dsum + 255) / 256) * 256;
+  const size_t row = (size_t)batch * heads * n * 4;
+  return ((acc + 255) / 256) * 256 + 2 * ((row + 255) / 256) * 256;
 }
 
 namespace {
 
-// workspace carve-up: [fp32 dQ accumulator, 256-aligned][fp32 D]
+// workspace carve-up: [fp32 dQ accumulator][fp32 D*scale][fp32 LSE*log2e], 256-aligned regions
 hla_status carve_workspace(int32_t batch, int32_t heads, int32_t n, int32_t head_dim, void* workspace,
-                           size_t workspace_bytes, float** dq_acc, float** dsum) {
+                           size_t workspace_bytes, float** dq_acc, float** dsum, float** lse2 = nullptr) {
   HLA_REQUIRE(workspace != nullptr, HLA_ERR_INVALID, "null workspace");
   HLA_REQUIRE((uintptr_t)workspace % 256 == 0, HLA_ERR_INVALID, "workspace must be 256-byte aligned");
   const size_t need = hla_attn_bwd_workspace(batch, heads, n, head_dim);
   HLA_REQUIRE(workspace_bytes >= need, HLA_ERR_INVALID, "workspace %zu < %zu bytes", workspace_bytes, need);
   const size_t acc = (size_t)batch * n * heads * head_dim * 4;
   *dq_acc = reinterpret_cast<float*>(workspace);
+  const size_t row = (size_t)batch * heads * n * 4;
   *dsum = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + ((acc + 255) / 256) * 256);
+  if (lse2) *lse2 = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(*dsum) + ((row + 255) / 256) * 256);
   return HLA_OK;
 }
 
 }  // namespace
 
 extern "C" hla_status hla_attn_bwd_preprocess(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,
-                                              const void* o, const void* dout, const int32_t* seq_to_cell,
-                                              void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+                                              float scale, const void* o, const void* dout, const float* lse,
+                                              const int32_t* seq_to_cell, void* workspace, size_t workspace_bytes,
+                                              cudaStream_t stream) {
   clear_error();
   HLA_REQUIRE(head_dim == 32 || head_dim == 64, HLA_ERR_UNSUPPORTED, "head_dim %d not in {32, 64}", head_dim);
   HLA_REQUIRE(batch >= 1 && heads >= 1 && n >= 1, HLA_ERR_INVALID, "bad shape");
   HLA_REQUIRE(o && dout && ((uintptr_t)o | (uintptr_t)dout) % 16 == 0, HLA_ERR_INVALID, "o/dout null or unaligned");
-  float *dq_acc, *dsum;
-  hla_status st = carve_workspace(batch, heads, n, head_dim, workspace, workspace_bytes, &dq_acc, &dsum);
+  HLA_REQUIRE(lse != nullptr, HLA_ERR_INVALID, "null lse");
+  float *dq_acc, *dsum, *lse2;
+  hla_status st = carve_workspace(batch, heads, n, head_dim, workspace, workspace_bytes, &dq_acc, &dsum, &lse2);
   if (st != HLA_OK) return st;
+  const float sc = scale > 0.f ? scale : 1.0f / sqrtf((float)head_dim);
   const int64_t rows = (int64_t)batch * n * heads;
   const int64_t threads = rows * (head_dim / 8);
   const unsigned blocks = (unsigned)((threads + 255) / 256);
   if (head_dim == 64)
     bwd_preprocess_kernel<64><<<blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
-                                                          reinterpret_cast<const __nv_bfloat16*>(dout), dsum,
-                                                          dq_acc, seq_to_cell, n, heads, rows);
+                                                          reinterpret_cast<const __nv_bfloat16*>(dout), lse, sc,
+                                                          dsum, lse2, dq_acc, seq_to_cell, n, heads, rows);
   else
     bwd_preprocess_kernel<32><<<blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
-                                                          reinterpret_cast<const __nv_bfloat16*>(dout), dsum,
-                                                          dq_acc, seq_to_cell, n, heads, rows);
+                                                          reinterpret_cast<const __nv_bfloat16*>(dout), lse, sc,
+                                                          dsum, lse2, dq_acc, seq_to_cell, n, heads, rows);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
 }
 
 extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch,
                                         int32_t heads, int32_t head_dim, float scale, const void* q, const void* k,
-                                        const void* v, const float* lse, const void* dout, void* dk, void* dv,
+                                        const void* v, const void* dout, void* dk, void* dv,
                                         const int32_t* seq_to_cell, void* workspace, size_t workspace_bytes,
                                         int64_t* tiles_visited, cudaStream_t stream) {
   clear_error();
@@ -629,12 +660,11 @@ extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_blo
   hla_status st = check_attn_args(d, m, batch, heads, head_dim, &pat);
   if (st != HLA_OK) return st;
   HLA_REQUIRE(m->t_row_ptr && m->t_col_idx && m->t_kind, HLA_ERR_INVALID, "transposed mask arrays missing");
-  HLA_REQUIRE(q && k && v && lse && dout && dk && dv, HLA_ERR_INVALID, "null pointer");
-  HLA_REQUIRE(((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)dout | (uintptr_t)dk | (uintptr_t)dv |
-               (uintptr_t)lse) % 16 == 0,
+  HLA_REQUIRE(q && k && v && dout && dk && dv, HLA_ERR_INVALID, "null pointer");
+  HLA_REQUIRE(((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)dout | (uintptr_t)dk | (uintptr_t)dv) % 16 == 0,
               HLA_ERR_INVALID, "tensors must be 16-byte aligned");
-  float *dq_acc, *dsum;
-  st = carve_workspace(batch, heads, pat.N, head_dim, workspace, workspace_bytes, &dq_acc, &dsum);
+  float *dq_acc, *dsum, *lse2;
+  st = carve_workspace(batch, heads, pat.N, head_dim, workspace, workspace_bytes, &dq_acc, &dsum, &lse2);
   if (st != HLA_OK) return st;
   const float sc = scale > 0.f ? scale : 1.0f / sqrtf((float)head_dim);
   BwdParams prm;
@@ -647,7 +677,7 @@ extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_blo
   prm.t_row_ptr = m->t_row_ptr;
   prm.t_col_idx = m->t_col_idx;
   prm.t_kind = m->t_kind;
-  prm.lse = lse;
+  prm.lse2 = lse2;
   prm.dsum = dsum;
   prm.dq_acc = dq_acc;
   prm.dk = reinterpret_cast<__nv_bfloat16*>(dk);
@@ -715,10 +745,10 @@ extern "C" hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_ma
   st = carve_workspace(batch, heads, pat.N, head_dim, workspace, workspace_bytes, &dq_acc, &dsum);
   if (st != HLA_OK) return st;
   HLA_REQUIRE(((uintptr_t)o | (uintptr_t)dq) % 16 == 0, HLA_ERR_INVALID, "tensors must be 16-byte aligned");
-  if ((st = hla_attn_bwd_preprocess(batch, heads, pat.N, head_dim, o, dout, seq_to_cell, workspace,
+  if ((st = hla_attn_bwd_preprocess(batch, heads, pat.N, head_dim, scale, o, dout, lse, seq_to_cell, workspace,
                                     workspace_bytes, stream)) != HLA_OK)
     return st;
-  if ((st = hla_attn_bwd_main(d, m, batch, heads, head_dim, scale, q, k, v, lse, dout, dk, dv, seq_to_cell,
+  if ((st = hla_attn_bwd_main(d, m, batch, heads, head_dim, scale, q, k, v, dout, dk, dv, seq_to_cell,
                               workspace, workspace_bytes, tiles_visited, stream)) != HLA_OK)
     return st;
   return hla_attn_bwd_finalize(batch, heads, pat.N, head_dim, workspace, workspace_bytes, dq, seq_to_cell, stream);
