@@ -36,6 +36,11 @@ HLA_API hla_status hla_debug_gather4(const void* src, int64_t rows, int32_t head
 HLA_API hla_status hla_debug_mma_rate(int32_t N, int32_t iters, int32_t a_major_mn, int32_t b_major_mn,
                                       int32_t a_from_tmem, long long* out_cycles, cudaStream_t stream);
 
+/* hla_debug_tmem_rate: nwarps warps each issue `iters` tcgen05.ld (mode 0) / .st (mode 1)
+ * 32x32b.x32 (4 KB per warp-instruction), waiting every `batch`; out_cycles = SM cycles. */
+HLA_API hla_status hla_debug_tmem_rate(int32_t nwarps, int32_t iters, int32_t mode, int32_t batch,
+                                       long long* out_cycles, cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,7 +18,8 @@ STATUS_NAMES = {0: "HLA_OK", 1: "HLA_ERR_INVALID", 2: "HLA_ERR_UNSUPPORTED", 3: 
 EXPORTED = ("hla_hilbert_index", "hla_hilbert_perm", "hla_build_block_mask", "hla_mask_ratios",
             "hla_attn_fwd", "hla_attn_bwd", "hla_attn_bwd_workspace", "hla_attn_bwd_preprocess",
             "hla_attn_bwd_main", "hla_attn_bwd_finalize", "hla_last_error", "hla_version",
-            "hla_debug_umma", "hla_debug_gather4", "hla_debug_mma_rate")
+            "hla_debug_umma", "hla_debug_gather4", "hla_debug_mma_rate",
+            "hla_debug_tmem_rate")
 
 
 class PatternDesc(ctypes.Structure):
@@ -66,6 +67,7 @@ def lib():
         "hla_debug_umma": [vp, vp, vp, i32, i32, i32, i32, i32, i32, vp],
         "hla_debug_gather4": [vp, i64, i32, i32, vp, i32, i32, vp, vp],
         "hla_debug_mma_rate": [i32, i32, i32, i32, i32, vp, vp],
+        "hla_debug_tmem_rate": [i32, i32, i32, i32, vp, vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)

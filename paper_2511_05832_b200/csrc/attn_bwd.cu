@@ -64,7 +64,7 @@ struct BwdSmem {
   alignas(1024) float dq_stage[kBlock * 32];    // fp32 dQ half tile [128][32], SWIZZLE_128B
   alignas(16) float lse[2][kBlock];
   alignas(16) float dd[2][kBlock];
-  uint64_t kv_full[2], kv_empty[2], q_full[2], q_empty[2], s_full[2], ds_ready[2], dq_full, dq_free, dkv_full;
+  uint64_t kv_full[2], kv_empty[2], q_full[2], q_empty[2], s_full[2], ds_ready[2], dq_full, dq_free, dkv_full, epi_done;
   uint64_t dbg_bar;
   uint32_t tmem_base;
 };
@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     sm100::mbar_init(&sm.dq_full, 1);
     sm100::mbar_init(&sm.dq_free, 128);
     sm100::mbar_init(&sm.dkv_full, 1);
+    sm100::mbar_init(&sm.epi_done, 128);
     sm100::mbar_init(&sm.dbg_bar, 1);
     sm100::fence_mbar_init();
     sm100::tma_prefetch_desc(&tmQ);
@@ -304,16 +305,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         HLA_TR((1 << 24) | ((1) << 16) | (g));
         sm100::tc_fence_after();
         HLA_TR((5 << 24) | (0 << 16) | g);
+        if (cur.t == 0 && cur.n > 0) {
+          // the previous unit's dV / dK must have been drained from TMEM
+          sm100::mbar_wait(&sm.epi_done, (cur.n - 1) & 1);
+          sm100::tc_fence_after();
+        }
         issue_dvdk(g, 0, cur.t == 0);
         mma_probe(1, g);
-        if (nxt.valid) {
-          if (nxt.t == 0) sm100::mbar_wait(&sm.kv_full[nxt.n & 1], (nxt.n >> 1) & 1);
-          sm100::mbar_wait(&sm.q_full[(g + 1) & 1], ((g + 1) >> 1) & 1);
+        // S_A / dP_A of the next tile now if its operands already landed (never block
+        // here: the B half of this tile must not wait behind the next tile's loads)
+        bool next_a_issued = false;
+        if (nxt.valid && (nxt.t != 0 || sm100::mbar_test_wait(&sm.kv_full[nxt.n & 1], (nxt.n >> 1) & 1)) &&
+            sm100::mbar_test_wait(&sm.q_full[(g + 1) & 1], ((g + 1) >> 1) & 1)) {
           HLA_TR((1 << 24) | ((4) << 16) | (g));
           sm100::tc_fence_after();
-          HLA_TR((5 << 24) | (0 << 16) | g);
           issue_sdp(nxt, g + 1, 0);
-          mma_probe(2, g);
+          next_a_issued = true;
         }
         // half B of tile g, then dQ (needs both halves of dS)
         sm100::mbar_wait(&sm.ds_ready[1], g & 1);
@@ -336,6 +343,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         sm100::mma_commit(&sm.dq_full);
         if (last_of_unit) sm100::mma_commit(&sm.kv_empty[kvs]);
         if (nxt.valid) {
+          if (!next_a_issued) {
+            if (nxt.t == 0) sm100::mbar_wait(&sm.kv_full[nxt.n & 1], (nxt.n >> 1) & 1);
+            sm100::mbar_wait(&sm.q_full[(g + 1) & 1], ((g + 1) >> 1) & 1);
+            HLA_TR((1 << 24) | ((4) << 16) | (g));
+            sm100::tc_fence_after();
+            issue_sdp(nxt, g + 1, 0);
+          }
           HLA_TR((5 << 24) | (0 << 16) | g);
           issue_sdp(nxt, g + 1, 1);
           mma_probe(5, g);
@@ -427,40 +441,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (row == 0 && cset == 0) HLA_TR((2 << 24) | ((3 + 2 * half) << 16) | (g));
         }
       }
-      // final dK, dV rows -> bf16 (dS already carries the softmax scale)
-      const int32_t kcell = kGather ? __ldg(prm.s2c + kidx) : kidx;   // fused inverse reorder of dK, dV
-      const int64_t grow = ((int64_t)b * prm.N + kcell) * prm.heads + h;
-      uint4* dkp = reinterpret_cast<uint4*>(prm.dk + grow * D);
-      uint4* dvp = reinterpret_cast<uint4*>(prm.dv + grow * D);
-      if (nt > 0) {
-        sm100::mbar_wait(&sm.dkv_full, n & 1);
-        if (row == 0 && cset == 0) HLA_TR((2 << 24) | ((6) << 16) | (n));
-        sm100::tc_fence_after();
-        {  // cset 0 writes dV, cset 1 writes dK
-          uint4* dst = cset == 0 ? dvp : dkp;
-          const uint32_t col = cset == 0 ? kColDV : kColDK;
-#pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t r[32];
-            sm100::tmem_ld32(tmem + lane_off + col + c * 32, r);
-            sm100::tmem_wait_ld();
-#pragma unroll
-            for (int v4 = 0; v4 < 4; ++v4) {
-              uint4 w;
-              w.x = sm100::pack_bf16(__uint_as_float(r[v4 * 8 + 0]), __uint_as_float(r[v4 * 8 + 1]));
-              w.y = sm100::pack_bf16(__uint_as_float(r[v4 * 8 + 2]), __uint_as_float(r[v4 * 8 + 3]));
-              w.z = sm100::pack_bf16(__uint_as_float(r[v4 * 8 + 4]), __uint_as_float(r[v4 * 8 + 5]));
-              w.w = sm100::pack_bf16(__uint_as_float(r[v4 * 8 + 6]), __uint_as_float(r[v4 * 8 + 7]));
-              dst[c * 4 + v4] = w;
-            }
-          }
-        }
-        if (row == 0 && cset == 0) HLA_TR((2 << 24) | ((7) << 16) | (n));
-        ++n;
-      } else {
-#pragma unroll
-        for (int c = 0; c < D / 8; ++c) (cset == 0 ? dvp : dkp)[c] = make_uint4(0, 0, 0, 0);
-      }
       tiles_done += nt;
     }
   } else {
@@ -473,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const bool leader = warp == 10 && lane == 0;
-    uint32_t g = 0;
+    uint32_t g = 0, n = 0;
     for (int32_t kq = 0;; ++kq) {
         const int32_t u = unit_at(kq);
         if (u >= units) break;
@@ -506,6 +486,47 @@ __global__ void __launch_bounds__(kThreads, 1)
             sm100::tma_reduce_add_3d(&tmDQ, sm.dq_stage, hh * 32, h, qrow);
             sm100::bulk_commit_group();
           }
+        }
+      }
+      // final dK, dV rows of this unit -> bf16 (thread = key row; dS already carries
+      // the softmax scale).  Done here, off the compute warps' critical path; the
+      // next unit's first dV/dK MMA waits for epi_done.
+      const int32_t kidx = kb * kBlock + row;
+      const int32_t kcell = kGather ? __ldg(prm.s2c + kidx) : kidx;   // fused inverse reorder of dK, dV
+      const int64_t grow = ((int64_t)b * prm.N + kcell) * prm.heads + h;
+      uint4* dkp = reinterpret_cast<uint4*>(prm.dk + grow * D);
+      uint4* dvp = reinterpret_cast<uint4*>(prm.dv + grow * D);
+      if (nt > 0) {
+        sm100::mbar_wait(&sm.dkv_full, n & 1);
+        if (leader) HLA_TR((2 << 24) | ((6) << 16) | (n));
+        sm100::tc_fence_after();
+        uint32_t rv[D], rk[D];
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          sm100::tmem_ld32(tmem + lane_off + kColDV + c * 32, *reinterpret_cast<uint32_t(*)[32]>(rv + c * 32));
+          sm100::tmem_ld32(tmem + lane_off + kColDK + c * 32, *reinterpret_cast<uint32_t(*)[32]>(rk + c * 32));
+        }
+        sm100::tmem_wait_ld();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&sm.epi_done);      // dV / dK accumulators may now be reset
+#pragma unroll
+        for (int v4 = 0; v4 < D / 8; ++v4) {
+          dvp[v4] = make_uint4(sm100::pack_bf16(__uint_as_float(rv[v4 * 8 + 0]), __uint_as_float(rv[v4 * 8 + 1])),
+                               sm100::pack_bf16(__uint_as_float(rv[v4 * 8 + 2]), __uint_as_float(rv[v4 * 8 + 3])),
+                               sm100::pack_bf16(__uint_as_float(rv[v4 * 8 + 4]), __uint_as_float(rv[v4 * 8 + 5])),
+                               sm100::pack_bf16(__uint_as_float(rv[v4 * 8 + 6]), __uint_as_float(rv[v4 * 8 + 7])));
+          dkp[v4] = make_uint4(sm100::pack_bf16(__uint_as_float(rk[v4 * 8 + 0]), __uint_as_float(rk[v4 * 8 + 1])),
+                               sm100::pack_bf16(__uint_as_float(rk[v4 * 8 + 2]), __uint_as_float(rk[v4 * 8 + 3])),
+                               sm100::pack_bf16(__uint_as_float(rk[v4 * 8 + 4]), __uint_as_float(rk[v4 * 8 + 5])),
+                               sm100::pack_bf16(__uint_as_float(rk[v4 * 8 + 6]), __uint_as_float(rk[v4 * 8 + 7])));
+        }
+        if (leader) HLA_TR((2 << 24) | ((7) << 16) | (n));
+        ++n;
+      } else {
+#pragma unroll
+        for (int c = 0; c < D / 8; ++c) {
+          dvp[c] = make_uint4(0, 0, 0, 0);
+          dkp[c] = make_uint4(0, 0, 0, 0);
         }
       }
     }

@@ -150,6 +150,49 @@ __global__ void __launch_bounds__(128) debug_mma_rate_kernel(int N, int iters, i
   if (warp == 0) sm100::tmem_dealloc(tmem, 512);
 }
 
+// TMEM read/write rate probe: nwarps (multiple of 4) warps each issue `iters`
+// tcgen05.ld (mode 0) or tcgen05.st (mode 1) of 32 lanes x 32 columns, waiting
+// after every `batch` of them; returns SM cycles of warp 0 in out[0].
+__global__ void debug_tmem_rate_kernel(int iters, int mode, int batch, long long* out) {
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    sm100::tmem_alloc(&tmem_base, 512);
+    sm100::tmem_relinquish();
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) & 3) * 128;
+  uint32_t r[32];
+  for (int e = 0; e < 32; ++e) r[e] = e;
+  uint32_t acc = 0;
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; i += batch) {
+    for (int j = 0; j < batch; ++j) {
+      const uint32_t col = (uint32_t)(((i + j) & 3) * 32);
+      if (mode == 0) {
+        sm100::tmem_ld32(tmem + col, r);
+      } else {
+        sm100::tmem_st32(tmem + col, r);
+      }
+    }
+    if (mode == 0) {
+      sm100::tmem_wait_ld();
+      acc += r[0] + r[31];
+    } else {
+      sm100::tmem_wait_st();
+    }
+  }
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) out[0] = t1 - t0 + (acc == 0xFFFFFFFF ? 1 : 0);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  if (warp == 0) sm100::tmem_dealloc(tmem_base, 512);
+}
+
 // 128 token rows (indices idx[0..127]) of head h gathered with .tile::gather4 into a
 // SWIZZLE_<2d> tile, then read back through the swizzle into out[128][d].
 template <int D>
@@ -190,6 +233,15 @@ extern "C" hla_status hla_debug_mma_rate(int32_t N, int32_t iters, int32_t a_maj
   const size_t smem = 1024 + 2 * 128 * 256 * 2;
   HLA_CUDA_TRY(cudaFuncSetAttribute(debug_mma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   debug_mma_rate_kernel<<<1, 128, smem, stream>>>(N, iters, a_major_mn, b_major_mn, a_from_tmem, out_cycles);
+  HLA_CUDA_TRY(cudaGetLastError());
+  return HLA_OK;
+}
+
+extern "C" hla_status hla_debug_tmem_rate(int32_t nwarps, int32_t iters, int32_t mode, int32_t batch,
+                                          long long* out_cycles, cudaStream_t stream) {
+  clear_error();
+  HLA_REQUIRE(nwarps % 4 == 0 && nwarps >= 4 && nwarps <= 16 && iters > 0 && batch >= 1, HLA_ERR_INVALID, "bad args");
+  debug_tmem_rate_kernel<<<1, nwarps * 32, 0, stream>>>(iters, mode, batch, out_cycles);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
 }
