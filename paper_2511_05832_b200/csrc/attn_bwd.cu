@@ -395,44 +395,51 @@ __global__ void __launch_bounds__(kThreads, 1)
             sm100::tmem_ld32(tmem + lane_off + kColS + c * 32, sr);
             sm100::tmem_ld32(tmem + lane_off + kColDP + c * 32, dpr);
             sm100::tmem_wait_ld();
-            uint32_t pk[16];
+            // P first (so its TMEM store is in flight while dS is formed)
+            float p[32];
 #pragma unroll
-            for (int u4 = 0; u4 < 4; ++u4) {   // 8 query columns (one 16B dS chunk) at a time
+            for (int u4 = 0; u4 < 4; ++u4) {
               const int qc = c * 32 + u4 * 8;
               const float4 la = sm100::lds_f4(lse2 + qc * 4), lb = sm100::lds_f4(lse2 + qc * 4 + 16);
-              const float4 da = sm100::lds_f4(dd + qc * 4), db = sm100::lds_f4(dd + qc * 4 + 16);
               const float lv[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
-              const float dv[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
-              float p[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) p[e] = sm100::ex2(fmaf(__uint_as_float(sr[u4 * 8 + e]), sl2, -lv[e]));
-              if (kd == 2) {
+              for (int e = 0; e < 8; ++e) p[u4 * 8 + e] = sm100::ex2(fmaf(__uint_as_float(sr[u4 * 8 + e]), sl2, -lv[e]));
+            }
+            if (kd == 2) {
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                  const int32_t qq = q0 + qc + e;
-                  bool ok;
-                  if (!kTwoD) {
-                    ok = (uint32_t)(qq - box.lo) < (uint32_t)box.len;
-                  } else {
-                    const int32_t rq = prm.pat.log2W >= 0 ? (qq >> prm.pat.log2W) : qq / prm.pat.W;
-                    const int32_t cq = qq - rq * prm.pat.W;
-                    ok = ((uint32_t)(rq - box.lo) < (uint32_t)box.len) && ((uint32_t)(cq - box.c0) < (uint32_t)box.cn);
-                  }
-                  if (!ok) p[e] = 0.f;
+              for (int e = 0; e < 32; ++e) {
+                const int32_t qq = q0 + c * 32 + e;
+                bool ok;
+                if (!kTwoD) {
+                  ok = (uint32_t)(qq - box.lo) < (uint32_t)box.len;
+                } else {
+                  const int32_t rq = prm.pat.log2W >= 0 ? (qq >> prm.pat.log2W) : qq / prm.pat.W;
+                  const int32_t cq = qq - rq * prm.pat.W;
+                  ok = ((uint32_t)(rq - box.lo) < (uint32_t)box.len) && ((uint32_t)(cq - box.c0) < (uint32_t)box.cn);
                 }
+                if (!ok) p[e] = 0.f;
               }
+            }
+            {
+              uint32_t pk[16];
+#pragma unroll
+              for (int e = 0; e < 16; ++e) pk[e] = sm100::pack_bf16(p[2 * e], p[2 * e + 1]);
+              sm100::tmem_st16(tmem + lane_off + kColP + c * 16, pk);
+            }
+#pragma unroll
+            for (int u4 = 0; u4 < 4; ++u4) {   // dS, 8 query columns (one 16B chunk) at a time
+              const int qc = c * 32 + u4 * 8;
+              const float4 da = sm100::lds_f4(dd + qc * 4), db = sm100::lds_f4(dd + qc * 4 + 16);
+              const float dv[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
               float ds[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) ds[e] = p[e] * fmaf(__uint_as_float(dpr[u4 * 8 + e]), scale, -dv[e]);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) pk[u4 * 4 + e] = sm100::pack_bf16(p[2 * e], p[2 * e + 1]);
+              for (int e = 0; e < 8; ++e) ds[e] = p[u4 * 8 + e] * fmaf(__uint_as_float(dpr[u4 * 8 + e]), scale, -dv[e]);
               // dS^T row -> smem [q/64][kv][64] with the 128B swizzle (16B chunks)
               const uint32_t off =
                   (uint32_t)(qc >> 6) * 16384u + sm100::swz128((uint32_t)row * 128u + (uint32_t)(qc & 63) * 2u);
               sm100::sts_u4(dsbuf + off, sm100::pack_bf16(ds[0], ds[1]), sm100::pack_bf16(ds[2], ds[3]),
                             sm100::pack_bf16(ds[4], ds[5]), sm100::pack_bf16(ds[6], ds[7]));
             }
-            sm100::tmem_st16(tmem + lane_off + kColP + c * 16, pk);
           }
           sm100::tmem_wait_st();
           sm100::fence_proxy_async_smem();

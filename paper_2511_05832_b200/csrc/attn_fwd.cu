@@ -6,13 +6,13 @@
 // covers "loading q block and k/v block, computing qk^T within the block, ...,
 // online softmax, and aggregation with value" (Eq. 1).
 //
-// One CTA per (q-block i, head h, batch b), 192 threads, 2 CTAs per SM:
+// Persistent CTAs (2 per SM), 256 threads:
 //   warp 0      TMA producer: Q_i once, then K_j / V_j of the listed kv-blocks
 //               into a 2-stage shared-memory ring (separate K and V barriers).
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:
 //                 S_t  = Q_i K_j^T   (SS MMA, 128x128x D, fp32 in TMEM cols [0,128))
 //                 O   += P_t V_j     (TS MMA, P bf16 in TMEM cols [128,192), O in [192,192+D))
-//   warps 2..5  softmax: thread = query row (TMEM lane); reads its S row with
+//   warps 4..7  softmax: thread = query row (TMEM lane); reads its S row with
 //               tcgen05.ld, applies the element mask only when the tile is
 //               partial, keeps the online max / sum in registers (lazy rescale:
 //               O is rescaled in TMEM only when the row max grows by > 2^8),
@@ -29,7 +29,7 @@ namespace hla {
 namespace {
 
 constexpr int kBlock = 128;
-constexpr int kThreads = 192;
+constexpr int kThreads = 256;   // warpgroup 0: TMA, MMA, 2 idle; warpgroup 1: softmax
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kColS = 0, kColP = 128, kColO = 192;
 
@@ -49,10 +49,10 @@ struct FwdParams {
 template <int D>
 struct FwdSmem {
   static constexpr uint32_t kTileBytes = kBlock * D * 2;
-  alignas(1024) uint8_t q[kTileBytes];
+  alignas(1024) uint8_t q[2][kTileBytes];
   alignas(1024) uint8_t k[2][kTileBytes];
   alignas(1024) uint8_t v[2][kTileBytes];
-  uint64_t q_full, q_empty, k_full[2], v_full[2], kv_empty[2], s_full, p_full, o_full;
+  uint64_t q_full[2], q_empty[2], k_full[2], v_full[2], kv_empty[2], s_full, s_free, p_full, pv_done, o_full;
   uint32_t tmem_base;
 };
 
@@ -118,11 +118,47 @@ __device__ __forceinline__ void apply_row_mask(float (&s)[kBlock], const Pattern
   }
 }
 
-// Persistent: CTA c processes work units c, c + G, c + 2G, ... (unit = q-block,
-// head, batch with the q-block fastest so that CTAs running side by side share
-// K/V tiles in L2).  Barrier phases run on per-CTA counters: n = units with
-// nt > 0 processed so far, g = tiles processed so far.  The next unit's Q and
-// first K/V loads and its first S MMA overlap the current unit's epilogue.
+// k-th work unit of this CTA: pairs of consecutive q-blocks (2p, 2p+1) of one
+// (b, h), pairs strided over the grid.  Neighbouring q-blocks list the same
+// kv-blocks (HWA: exactly), so the producer can skip reloading a K/V stage.
+__device__ __forceinline__ int32_t fwd_unit_at(int32_t k) {
+  return 2 * ((int32_t)blockIdx.x + (k >> 1) * (int32_t)gridDim.x) + (k & 1);
+}
+
+// Flattened (unit, kv-tile) iterator of this CTA, skipping units without tiles.
+struct FwdIter {
+  int32_t k, u, t, nt, rs;
+  uint32_t n;   // ordinal of the current non-empty unit
+  bool valid;
+  __device__ void seek(const int32_t* row_ptr, int32_t mq, int32_t units) {
+    for (;; ++k) {
+      u = fwd_unit_at(k);
+      if (u >= units) break;
+      const int32_t qb = u % mq;
+      rs = __ldg(row_ptr + qb);
+      nt = __ldg(row_ptr + qb + 1) - rs;
+      if (nt > 0) { valid = true; return; }
+    }
+    valid = false;
+  }
+  __device__ void init(const int32_t* row_ptr, int32_t mq, int32_t units) {
+    k = 0; t = 0; n = 0;
+    seek(row_ptr, mq, units);
+  }
+  __device__ void advance(const int32_t* row_ptr, int32_t mq, int32_t units) {
+    if (++t < nt) return;
+    t = 0; ++n; ++k;
+    seek(row_ptr, mq, units);
+  }
+};
+
+// Persistent CTAs (2 per SM).  Pipeline over the flattened tile sequence g:
+//   TMA     : Q of unit n into stage n&1 (double-buffered); K/V of tile g into
+//             stage g&1 (skipped when the stage already holds that kv-block)
+//   MMA     : S(g+1) as soon as the softmax has pulled S(g) into registers
+//             (s_free), then PV(g) after P(g) is in TMEM (p_full)
+//   softmax : S(g) -> registers -> s_free -> mask / max / exp; before writing
+//             P(g) (and before rescaling O) it waits pv_done(g-1)
 template <int D, bool kTwoD, bool kGather>
 __global__ void __launch_bounds__(kThreads, 2)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -134,15 +170,17 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int32_t units = mq * prm.heads * prm.batch;
 
   if (warp == 0 && lane == 0) {
-    sm100::mbar_init(&sm.q_full, 1);
-    sm100::mbar_init(&sm.q_empty, 1);
     for (int s = 0; s < 2; ++s) {
+      sm100::mbar_init(&sm.q_full[s], 1);
+      sm100::mbar_init(&sm.q_empty[s], 1);
       sm100::mbar_init(&sm.k_full[s], 1);
       sm100::mbar_init(&sm.v_full[s], 1);
       sm100::mbar_init(&sm.kv_empty[s], 1);
     }
     sm100::mbar_init(&sm.s_full, 1);
+    sm100::mbar_init(&sm.s_free, 128);
     sm100::mbar_init(&sm.p_full, 128);
+    sm100::mbar_init(&sm.pv_done, 1);
     sm100::mbar_init(&sm.o_full, 1);
     sm100::fence_mbar_init();
     sm100::tma_prefetch_desc(&tmQ);
@@ -158,106 +196,135 @@ __global__ void __launch_bounds__(kThreads, 2)
   sm100::tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
   unsigned long long tiles_done = 0;
+  HLA_TR_DECL;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    {
+  // register split (setmaxnreg acts per warpgroup): the control warpgroup gives its
+  // registers to the softmax warpgroup (one thread per row keeps a 128-wide S row)
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
+    if (warp == 0) {
+      // ---------------------------------------------------------- TMA producer
       const uint64_t pol_q = sm100::policy_evict_first();
       const uint64_t pol_kv = sm100::policy_evict_last();
-      uint32_t n = 0, g = 0;
-      for (int32_t u = blockIdx.x; u < units; u += gridDim.x) {
-        const int32_t qb = u % mq, h = (u / mq) % prm.heads, b = u / (mq * prm.heads);
-        const int32_t rs = __ldg(prm.row_ptr + qb), nt = __ldg(prm.row_ptr + qb + 1) - rs;
-        if (nt == 0) continue;
-        if (n > 0) sm100::mbar_wait(&sm.q_empty, (n - 1) & 1);
-        if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.q_full, FwdSmem<D>::kTileBytes);
+      int64_t tag0 = -1, tag1 = -1;   // (b, h, kv-block) held by K/V stage 0 / 1
+      uint32_t g = 0;
+      FwdIter it;
+      it.init(prm.row_ptr, mq, units);
+      while (it.valid) {
+        const int32_t qb = it.u % mq, h = (it.u / mq) % prm.heads, b = it.u / (mq * prm.heads);
+        const int64_t bh = (int64_t)b * prm.heads + h;
+        const int qs = it.n & 1;
+        if (it.n >= 2) sm100::mbar_wait(&sm.q_empty[qs], ((it.n >> 1) - 1) & 1);
+        if (lane == 0) HLA_TR((3 << 24) | (1 << 16) | it.n);
+        if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.q_full[qs], FwdSmem<D>::kTileBytes);
         __syncwarp();
-        load_rows<D, kGather>(sm.q, &tmQ, &sm.q_full, h, b, prm.N, qb * kBlock, prm.s2c, pol_q, lane);
-        for (int t = 0; t < nt; ++t, ++g) {
+        load_rows<D, kGather>(sm.q[qs], &tmQ, &sm.q_full[qs], h, b, prm.N, qb * kBlock, prm.s2c, pol_q, lane);
+        for (int t = 0; t < it.nt; ++t, ++g) {
           const int s = g & 1;
           if (g >= 2) sm100::mbar_wait(&sm.kv_empty[s], ((g >> 1) - 1) & 1);
-          const int32_t k0 = __ldg(prm.col_idx + rs + t) * kBlock;
+          if (lane == 0) HLA_TR((3 << 24) | (2 << 16) | g);
+          const int32_t kvb = __ldg(prm.col_idx + it.rs + t);
+          const int64_t tag = bh * mq + kvb;
+          if (tag == (s ? tag1 : tag0)) {   // stage already holds this K/V tile
+            if (lane == 0) {
+              sm100::mbar_arrive(&sm.k_full[s]);
+              sm100::mbar_arrive(&sm.v_full[s]);
+            }
+            continue;
+          }
+          if (s) tag1 = tag; else tag0 = tag;
           if (lane == 0) {
             sm100::mbar_arrive_expect_tx(&sm.k_full[s], FwdSmem<D>::kTileBytes);
             sm100::mbar_arrive_expect_tx(&sm.v_full[s], FwdSmem<D>::kTileBytes);
           }
           __syncwarp();
-          load_rows<D, kGather>(sm.k[s], &tmK, &sm.k_full[s], h, b, prm.N, k0, prm.s2c, pol_kv, lane);
-          load_rows<D, kGather>(sm.v[s], &tmV, &sm.v_full[s], h, b, prm.N, k0, prm.s2c, pol_kv, lane);
+          load_rows<D, kGather>(sm.k[s], &tmK, &sm.k_full[s], h, b, prm.N, kvb * kBlock, prm.s2c, pol_kv, lane);
+          load_rows<D, kGather>(sm.v[s], &tmV, &sm.v_full[s], h, b, prm.N, kvb * kBlock, prm.s2c, pol_kv, lane);
         }
-        ++n;
+        it.t = it.nt - 1;
+        it.advance(prm.row_ptr, mq, units);
       }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
+    } else if (warp == 1 && lane == 0) {
+      // ----------------------------------------------------------- MMA issuer
       constexpr uint32_t idesc_s = sm100::make_idesc_bf16(kBlock, kBlock, false, false);
       constexpr uint32_t idesc_o = sm100::make_idesc_bf16(kBlock, D, false, true);
       const uint32_t tS = tmem + kColS, tP = tmem + kColP, tO = tmem + kColO;
-      auto issue_s = [&](int s) {
+      auto issue_s = [&](const FwdIter& x, uint32_t gg) {
+        const uint8_t* q = sm.q[x.n & 1];
+        const uint8_t* k = sm.k[gg & 1];
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          sm100::mma_ss(tS, kmajor_desc<D>(sm.q, kk), kmajor_desc<D>(sm.k[s], kk), idesc_s, kk > 0);
+          sm100::mma_ss(tS, kmajor_desc<D>(q, kk), kmajor_desc<D>(k, kk), idesc_s, kk > 0);
         sm100::mma_commit(&sm.s_full);
       };
-      uint32_t n = 0, g = 0;
-      for (int32_t u = blockIdx.x; u < units; u += gridDim.x) {
-        const int32_t qb = u % mq;
-        const int32_t nt = __ldg(prm.row_ptr + qb + 1) - __ldg(prm.row_ptr + qb);
-        if (nt == 0) continue;
-        sm100::mbar_wait(&sm.q_full, n & 1);
-        sm100::mbar_wait(&sm.k_full[g & 1], (g >> 1) & 1);
+      FwdIter cur;
+      cur.init(prm.row_ptr, mq, units);
+      uint32_t g = 0;
+      if (cur.valid) {
+        sm100::mbar_wait(&sm.q_full[0], 0);
+        sm100::mbar_wait(&sm.k_full[0], 0);
         sm100::tc_fence_after();
-        issue_s(g & 1);
-        for (int t = 0; t < nt; ++t, ++g) {
-          const int s = g & 1;
-          sm100::mbar_wait(&sm.p_full, g & 1);
-          sm100::mbar_wait(&sm.v_full[s], (g >> 1) & 1);
+        issue_s(cur, 0);
+      }
+      while (cur.valid) {
+        FwdIter nxt = cur;
+        nxt.advance(prm.row_ptr, mq, units);
+        if (nxt.valid) {
+          // S(g+1) overwrites S(g): only after the softmax pulled S(g) into registers
+          sm100::mbar_wait(&sm.s_free, g & 1);
+          if (nxt.t == 0) sm100::mbar_wait(&sm.q_full[nxt.n & 1], (nxt.n >> 1) & 1);
+          sm100::mbar_wait(&sm.k_full[(g + 1) & 1], ((g + 1) >> 1) & 1);
           sm100::tc_fence_after();
-#pragma unroll
-          for (int kk = 0; kk < kBlock / 16; ++kk)
-            sm100::mma_ts(tO, tP + kk * 8, mnmajor_desc<D>(sm.v[s], kk), idesc_o, (t > 0 || kk > 0) ? 1u : 0u);
-          sm100::mma_commit(&sm.kv_empty[s]);
-          if (t + 1 < nt) {
-            const uint32_t g2 = g + 1;
-            sm100::mbar_wait(&sm.k_full[g2 & 1], (g2 >> 1) & 1);
-            sm100::tc_fence_after();
-            issue_s(g2 & 1);
-          } else {
-            sm100::mma_commit(&sm.q_empty);
-            sm100::mma_commit(&sm.o_full);
-          }
+          issue_s(nxt, g + 1);
         }
-        ++n;
+        sm100::mbar_wait(&sm.p_full, g & 1);
+        HLA_TR((1 << 24) | (2 << 16) | g);
+        sm100::mbar_wait(&sm.v_full[g & 1], (g >> 1) & 1);
+        sm100::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < kBlock / 16; ++kk)
+          sm100::mma_ts(tO, tP + kk * 8, mnmajor_desc<D>(sm.v[g & 1], kk), idesc_o,
+                        (cur.t > 0 || kk > 0) ? 1u : 0u);
+        sm100::mma_commit(&sm.kv_empty[g & 1]);
+        sm100::mma_commit(&sm.pv_done);
+        if (cur.t == cur.nt - 1) {
+          sm100::mma_commit(&sm.q_empty[cur.n & 1]);
+          sm100::mma_commit(&sm.o_full);
+        }
+        cur = nxt;
+        ++g;
       }
     }
   } else {
-    // ------------------------------------------------- softmax + epilogue
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;" ::: "memory");
+    // --------------------------------------------------- softmax + epilogue
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = prm.scale_log2;
-    uint32_t n = 0, g = 0;
-    for (int32_t u = blockIdx.x; u < units; u += gridDim.x) {
-      const int32_t qb = u % mq, h = (u / mq) % prm.heads, b = u / (mq * prm.heads);
-      const int32_t rs = __ldg(prm.row_ptr + qb), nt = __ldg(prm.row_ptr + qb + 1) - rs;
+    uint32_t g = 0;
+    FwdIter it;
+    it.init(prm.row_ptr, mq, units);
+    while (it.valid) {
+      const int32_t qb = it.u % mq, h = (it.u / mq) % prm.heads, b = it.u / (mq * prm.heads);
       const int32_t q = qb * kBlock + row;
       float m_ref = -INFINITY, l = 0.f;
       const RowBox box = row_box(prm.pat, q);
-      for (int t = 0; t < nt; ++t, ++g) {
+      for (int t = 0; t < it.nt; ++t, ++g) {
         sm100::mbar_wait(&sm.s_full, g & 1);
+        if (row == 0) HLA_TR((2 << 24) | (1 << 16) | g);
         sm100::tc_fence_after();
-        float s[kBlock];
+        // the whole S row: four loads in flight, one wait (TMEM round trip ~200 cycles)
+        uint32_t sr[kBlock];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t r[32];
-          sm100::tmem_ld32(tmem + lane_off + kColS + c * 32, r);
-          sm100::tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(r[e]);
-        }
-        if (__ldg(prm.kind + rs + t) == 2)
-          apply_row_mask<kTwoD>(s, prm.pat, box, __ldg(prm.col_idx + rs + t) * kBlock);
+        for (int c = 0; c < 4; ++c)
+          sm100::tmem_ld32(tmem + lane_off + kColS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(sr + c * 32));
+        sm100::tmem_wait_ld();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&sm.s_free);          // the MMA may overwrite S with S(g+1)
+        float (&s)[kBlock] = *reinterpret_cast<float(*)[kBlock]>(sr);
+        if (__ldg(prm.kind + it.rs + t) == 2)
+          apply_row_mask<kTwoD>(s, prm.pat, box, __ldg(prm.col_idx + it.rs + t) * kBlock);
         // row max with 8 independent chains (a single dependent chain costs ~4 cycles x 128)
         float m8[8];
 #pragma unroll
@@ -272,38 +339,43 @@ __global__ void __launch_bounds__(kThreads, 2)
         // lazy rescale (exact): keep the reference max unless it grew by > 8 (x256)
         const float m_new = (m_tile > m_ref + 8.f) ? m_tile : m_ref;
         const float alpha = (m_new == m_ref) ? 1.f : sm100::ex2(m_ref - m_new);
-        if (__any_sync(0xffffffffu, t > 0 && alpha != 1.f)) {
-          // O of the previous tiles is final in TMEM: s_full(t) was committed after PV(t-1)
-#pragma unroll
-          for (int c = 0; c < D / 16; ++c) {
-            uint32_t o[16];
-            sm100::tmem_ld16(tmem + lane_off + kColO + c * 16, o);
-            sm100::tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            sm100::tmem_st16(tmem + lane_off + kColO + c * 16, o);
-          }
-        }
         m_ref = m_new;
         l *= alpha;
         const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
         float l4[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t pk[64];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const float p0 = sm100::ex2(fmaf(s[c * 32 + 2 * e], sl2, -m_use));
-            const float p1 = sm100::ex2(fmaf(s[c * 32 + 2 * e + 1], sl2, -m_use));
-            l4[e & 3] += p0 + p1;
-            pk[e] = sm100::pack_bf16(p0, p1);
-          }
-          sm100::tmem_st16(tmem + lane_off + kColP + c * 16, pk);
+        for (int e = 0; e < 64; ++e) {
+          const float p0 = sm100::ex2(fmaf(s[2 * e], sl2, -m_use));
+          const float p1 = sm100::ex2(fmaf(s[2 * e + 1], sl2, -m_use));
+          l4[e & 3] += p0 + p1;
+          pk[e] = sm100::pack_bf16(p0, p1);
         }
         l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
+        // P(g-1) / O are read by PV(g-1): wait for it before writing P(g) or rescaling O
+        if (g > 0) {
+          sm100::mbar_wait(&sm.pv_done, (g - 1) & 1);
+          sm100::tc_fence_after();
+        }
+        if (__any_sync(0xffffffffu, t > 0 && alpha != 1.f)) {
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            sm100::tmem_ld16(tmem + lane_off + kColO + c * 32, o);
+            sm100::tmem_ld16(tmem + lane_off + kColO + c * 32 + 16, o + 16);
+            sm100::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            sm100::tmem_st16(tmem + lane_off + kColO + c * 32, o);
+            sm100::tmem_st16(tmem + lane_off + kColO + c * 32 + 16, o + 16);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sm100::tmem_st16(tmem + lane_off + kColP + c * 16, pk + c * 16);
         sm100::tmem_wait_st();
         sm100::tc_fence_before();
         sm100::mbar_arrive(&sm.p_full);
+        if (row == 0) HLA_TR((2 << 24) | (2 << 16) | g);
       }
 
       // epilogue: O / l -> bf16 row, LSE (natural log)
@@ -311,34 +383,31 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int64_t orow = ((int64_t)b * prm.N + ocell) * prm.heads + h;
       uint4* optr = reinterpret_cast<uint4*>(prm.o + orow * D);
       const float inv_l = l > 0.f ? 1.f / l : 0.f;
-      if (nt > 0) {
-        sm100::mbar_wait(&sm.o_full, n & 1);
-        sm100::tc_fence_after();
+      sm100::mbar_wait(&sm.o_full, it.n & 1);
+      if (row == 0) HLA_TR((2 << 24) | (3 << 16) | it.n);
+      sm100::tc_fence_after();
+      uint32_t o[D];
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t o[32];
-          sm100::tmem_ld32(tmem + lane_off + kColO + c * 32, o);
-          sm100::tmem_wait_ld();
+      for (int c = 0; c < D / 32; ++c)
+        sm100::tmem_ld32(tmem + lane_off + kColO + c * 32, *reinterpret_cast<uint32_t(*)[32]>(o + c * 32));
+      sm100::tmem_wait_ld();
+      // TMEM O may now be overwritten by the next unit's first PV (it waits p_full)
 #pragma unroll
-          for (int v4 = 0; v4 < 4; ++v4) {
-            uint4 w;
-            w.x = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 0]) * inv_l, __uint_as_float(o[v4 * 8 + 1]) * inv_l);
-            w.y = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 2]) * inv_l, __uint_as_float(o[v4 * 8 + 3]) * inv_l);
-            w.z = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 4]) * inv_l, __uint_as_float(o[v4 * 8 + 5]) * inv_l);
-            w.w = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 6]) * inv_l, __uint_as_float(o[v4 * 8 + 7]) * inv_l);
-            optr[c * 4 + v4] = w;
-          }
-        }
-        // TMEM O may now be overwritten by the next unit's first PV (it waits p_full)
-        ++n;
-      } else {
-#pragma unroll
-        for (int c = 0; c < D / 8; ++c) optr[c] = make_uint4(0, 0, 0, 0);
+      for (int v4 = 0; v4 < D / 8; ++v4) {
+        uint4 w;
+        w.x = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 0]) * inv_l, __uint_as_float(o[v4 * 8 + 1]) * inv_l);
+        w.y = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 2]) * inv_l, __uint_as_float(o[v4 * 8 + 3]) * inv_l);
+        w.z = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 4]) * inv_l, __uint_as_float(o[v4 * 8 + 5]) * inv_l);
+        w.w = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 6]) * inv_l, __uint_as_float(o[v4 * 8 + 7]) * inv_l);
+        optr[v4] = w;
       }
+      if (row == 0) HLA_TR((2 << 24) | (4 << 16) | it.n);
       const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
       prm.lse[((int64_t)b * prm.heads + h) * prm.N + q] =
           l > 0.f ? (m_use + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
-      tiles_done += nt;
+      tiles_done += it.nt;
+      it.t = it.nt - 1;
+      it.advance(prm.row_ptr, mq, units);
     }
   }
 
@@ -346,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   sm100::tc_fence_after();
   if (warp == 1) sm100::tmem_dealloc(tmem, kTmemCols);
-  if (warp == 2 && lane == 0 && prm.visited != nullptr && tiles_done > 0) atomicAdd(prm.visited, tiles_done);
+  if (warp == 4 && lane == 0 && prm.visited != nullptr && tiles_done > 0) atomicAdd(prm.visited, tiles_done);
 }
 
 template <int D, bool kTwoD, bool kGather>
@@ -356,7 +425,7 @@ hla_status launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtens
   auto* fn = attn_fwd_kernel<D, kTwoD, kGather>;
   HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t units = (int64_t)n_qblocks * prm.heads * prm.batch;
-  const int grid = (int)std::min<int64_t>(units, 2 * (int64_t)num_sms());
+  const int grid = (int)std::min<int64_t>((units + 1) / 2, 2 * (int64_t)num_sms());   // pairs of units
   fn<<<grid, kThreads, smem, stream>>>(mq, mk, mv, prm);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
