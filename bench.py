@@ -1,10 +1,13 @@
 #!/usr/bin/env python
 """bench.py -- Hilbert-guided local attention hot path on B200 (driver contract).
 
-One STEP = one pass of the whole hot path over one batch:
-  perm(Q,K,V -> Hilbert) ; block-sparse fwd ; perm(O -> grid) ;
-  perm(dO -> Hilbert) ; bwd preprocess ; block-sparse bwd ; dQ finalize ;
-  perm(dQ,dK,dV -> grid)
+One STEP = one pass of the whole hot path over one batch, grid-order
+tensors in and out, through the public HilbertLocalAttention API:
+  block-sparse fwd (Hilbert gather of Q,K,V + scatter of O fused into the kernel) ;
+  bwd preprocess (D, LSE2; gather of O,dO) ; block-sparse bwd (gathers, scatter of
+  dK,dV) ; dQ finalize (+ inverse reorder)
+(with HilbertLocalAttention(fused=False) the reorder runs as separate
+hla_hilbert_perm passes instead, the paper's "Reshape" step).
 The block mask and the Hilbert path are built once per shape, before timing
 (the paper caches them).  Workload (N=1): BASELINE.json configs[1]
 ("cfg2": 64x64 grid, 8 heads, head_dim 64, HWA 256 tokens vs row-major 16x16
@@ -65,6 +68,21 @@ def parse():
 
 
 # ------------------------------------------------------------------ helpers
+def reduce_max_ms(ms, dist=None, device=None):
+    """Max of a per-rank time over all ranks (the contract's max-over-ranks rule)."""
+    import torch
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    if dist is not None and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_value(step_ms, world):
+    """Weak scaling: every rank processes one batch per step, so the whole job does
+    `world` batches in step_ms (max over ranks) -> ms per batch of work."""
+    return step_ms / world
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -264,11 +282,8 @@ def main():
     sampler = ClockSampler(local)
     total, stages, clocks = timed(layer, args.steps, args.warmup, True, sampler)
     my_ms = statistics.mean(total)
-    t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    step_ms = float(t.item())
-    value = step_ms / world            # ms per batch of work for the whole job
+    step_ms = reduce_max_ms(my_ms, dist if world > 1 else None, dev)
+    value = job_value(step_ms, world)   # ms per batch of work for the whole job
 
     # --- row-major baseline and dense FA on the same shape (same kernels) ---
     variants = {}
@@ -318,11 +333,9 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record()
         torch.cuda.synchronize()
-        te = torch.tensor([e0.elapsed_time(e1) / esteps], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        te = reduce_max_ms(e0.elapsed_time(e1) / esteps, dist if world > 1 else None, dev)
         nbytes = sum(x.numel() * x.element_size() for x in hin)
-        e2e = {"value": round(float(te.item()) / world, 4), "unit": "ms", "h2d_bytes_per_step": nbytes,
+        e2e = {"value": round(job_value(te, world), 4), "unit": "ms", "h2d_bytes_per_step": nbytes,
                "d2h_bytes_per_step": nbytes, "path": "pinned host -> HilbertLocalAttention.forward/backward -> pinned host"}
 
     # --- roofline of the dominant kernel (share of the step) ---
@@ -373,7 +386,8 @@ def main():
         "config": {"workload": args.config + ": " + cfg["text"], "global_batch": B * world, "seq_len": N,
                    "parallelism": "dp%d (batch shards, no collective on the hot path)" % world,
                    "l2": "flushed between timed steps (%d MiB write, untimed)" % (L2_FLUSH_BYTES >> 20),
-                   "step": "perm(qkv)+fwd+perm(o)+perm(dO)+bwd_pre+bwd+bwd_fin+perm(dq,dk,dv)",
+                   "step": ("fwd+bwd_pre+bwd+bwd_fin (Hilbert reorder fused into the kernels)" if layer.fused else
+                            "perm(qkv)+fwd+perm(o)+perm(dO)+bwd_pre+bwd+bwd_fin+perm(dq,dk,dv)"),
                    "mask": "built once before timing (%d of %d tiles per (b,h) executed)" % (layer.nnz, (N // 128) ** 2)},
         "clocks": clocks, "e2e": e2e, "gpu_launches": layer.launches_per_step * args.steps,
         "roofline": roof, "cpu_baseline": cpu,
