@@ -130,7 +130,8 @@ __device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* map, 
                                           int32_t b, int32_t N, int32_t seq0, const int32_t* s2c, uint64_t pol,
                                           int lane) {
   if (kGather) {
-    const int4 c = __ldg(reinterpret_cast<const int4*>(s2c + seq0) + lane);
+    // rows past N (ragged last tile) gather cell 0: their values are masked / discarded
+    const int4 c = seq0 + 4 * lane < N ? __ldg(reinterpret_cast<const int4*>(s2c + seq0) + lane) : make_int4(0, 0, 0, 0);
     const int32_t base = b * N;
     sm100::tma_gather4(dst + lane * 4 * D * 2, map, bar, h * D, base + c.x, base + c.y, base + c.z, base + c.w, pol);
   } else if (lane == 0) {
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   BwdSmem<D>& sm = *reinterpret_cast<BwdSmem<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t mk = prm.N / kBlock;
+  const int32_t mk = (prm.N + kBlock - 1) / kBlock;   // last kv-block may be ragged
   const int32_t units = mk * prm.heads * prm.batch;
 
   if (warp == 0 && lane == 0) {
@@ -227,9 +228,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (s) stage_tag1 = tag; else stage_tag0 = tag;
           if (lane == 0) {
-            sm100::mbar_arrive_expect_tx(&sm.q_full[s], 2 * BwdSmem<D>::kTileBytes + 2 * kBlock * 4);
-            sm100::bulk_load(sm.lse[s], prm.lse2 + bh * prm.N + qblk * kBlock, kBlock * 4, &sm.q_full[s]);
-            sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * kBlock, kBlock * 4, &sm.q_full[s]);
+            // LSE / D of the real rows only (ragged last tile: N % 4 == 0, so 16-B multiples)
+            const uint32_t vbytes = (uint32_t)min(kBlock, prm.N - qblk * kBlock) * 4u;
+            sm100::mbar_arrive_expect_tx(&sm.q_full[s], 2 * BwdSmem<D>::kTileBytes + 2 * vbytes);
+            sm100::bulk_load(sm.lse[s], prm.lse2 + bh * prm.N + qblk * kBlock, vbytes, &sm.q_full[s]);
+            sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * kBlock, vbytes, &sm.q_full[s]);
           }
           __syncwarp();
           load_rows<D, kGather>(sm.q[s], &tmQ, &sm.q_full[s], h, b, prm.N, qblk * kBlock, prm.s2c, pol_q, lane);
@@ -374,7 +377,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
       const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
       const int32_t kidx = kb * kBlock + row;
-      const RowBox box = col_box(prm.pat, kidx);
+      RowBox box = clip_box<kTwoD>(prm.pat, col_box(prm.pat, kidx));
+      if (kidx >= prm.N) box.len = 0;   // phantom key row of a ragged tile: nothing allowed
       for (int t = 0; t < nt; ++t, ++g) {
         const int s = g & 1;
         sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1);
@@ -405,6 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int e = 0; e < 8; ++e) p[u4 * 8 + e] = sm100::ex2(fmaf(__uint_as_float(sr[u4 * 8 + e]), sl2, -lv[e]));
             }
+            uint32_t okbits = 0xffffffffu;   // element mask of this chunk (partial tiles only)
             if (kd == 2) {
 #pragma unroll
               for (int e = 0; e < 32; ++e) {
@@ -417,7 +422,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const int32_t cq = qq - rq * prm.pat.W;
                   ok = ((uint32_t)(rq - box.lo) < (uint32_t)box.len) && ((uint32_t)(cq - box.c0) < (uint32_t)box.cn);
                 }
-                if (!ok) p[e] = 0.f;
+                if (!ok) {
+                  p[e] = 0.f;
+                  okbits &= ~(1u << e);
+                }
               }
             }
             {
@@ -433,7 +441,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float dv[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
               float ds[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) ds[e] = p[u4 * 8 + e] * fmaf(__uint_as_float(dpr[u4 * 8 + e]), scale, -dv[e]);
+              for (int e = 0; e < 8; ++e) {
+                ds[e] = p[u4 * 8 + e] * fmaf(__uint_as_float(dpr[u4 * 8 + e]), scale, -dv[e]);
+                // masked: exactly 0 (the D / LSE of phantom query columns may be stale, 0 * NaN = NaN)
+                if (!((okbits >> (u4 * 8 + e)) & 1u)) ds[e] = 0.f;
+              }
               // dS^T row -> smem [q/64][kv][64] with the 128B swizzle (16B chunks)
               const uint32_t off =
                   (uint32_t)(qc >> 6) * 16384u + sm100::swz128((uint32_t)row * 128u + (uint32_t)(qc & 63) * 2u);
@@ -499,7 +511,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // the softmax scale).  Done here, off the compute warps' critical path; the
       // next unit's first dV/dK MMA waits for epi_done.
       const int32_t kidx = kb * kBlock + row;
-      const int32_t kcell = kGather ? __ldg(prm.s2c + kidx) : kidx;   // fused inverse reorder of dK, dV
+      const bool real = kidx < prm.N;   // phantom key rows of a ragged tile write nothing
+      const int32_t kcell = kGather ? (real ? __ldg(prm.s2c + kidx) : 0) : kidx;   // fused inverse reorder of dK, dV
       const int64_t grow = ((int64_t)b * prm.N + kcell) * prm.heads + h;
       uint4* dkp = reinterpret_cast<uint4*>(prm.dk + grow * D);
       uint4* dvp = reinterpret_cast<uint4*>(prm.dv + grow * D);
@@ -517,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         sm100::tc_fence_before();
         sm100::mbar_arrive(&sm.epi_done);      // dV / dK accumulators may now be reset
 #pragma unroll
-        for (int v4 = 0; v4 < D / 8; ++v4) {
+        for (int v4 = 0; v4 < D / 8 && real; ++v4) {
           dvp[v4] = make_uint4(sm100::pack_bf16(__uint_as_float(rv[v4 * 8 + 0]), __uint_as_float(rv[v4 * 8 + 1])),
                                sm100::pack_bf16(__uint_as_float(rv[v4 * 8 + 2]), __uint_as_float(rv[v4 * 8 + 3])),
                                sm100::pack_bf16(__uint_as_float(rv[v4 * 8 + 4]), __uint_as_float(rv[v4 * 8 + 5])),
@@ -531,7 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++n;
       } else {
 #pragma unroll
-        for (int c = 0; c < D / 8; ++c) {
+        for (int c = 0; c < D / 8 && real; ++c) {
           dvp[c] = make_uint4(0, 0, 0, 0);
           dkp[c] = make_uint4(0, 0, 0, 0);
         }
@@ -728,7 +741,7 @@ extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_blo
   CUtensorMap mdq;   // fp32 dQ accumulator, sequence order, 32-float (128 B) boxes for the TMA reduce-add
   if ((st = make_f32_rows_map(&mdq, dq_acc, tok, heads, head_dim, 32, kBlock)) != HLA_OK) return st;
   const bool two_d = pat.kind == K_WSA || pat.kind == K_SA || pat.kind == K_NA2D;
-  const int32_t mkb = pat.N / kBlock;
+  const int32_t mkb = (pat.N + kBlock - 1) / kBlock;
   if (head_dim == 64) {
     if (gather) return launch_bwd<64, false, true>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
     return two_d ? launch_bwd<64, true, false>(mq, mk, mv, mdo, mdq, prm, mkb, stream)

@@ -79,7 +79,8 @@ __device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* map, 
                                           int32_t b, int32_t N, int32_t seq0, const int32_t* s2c, uint64_t pol,
                                           int lane) {
   if (kGather) {
-    const int4 c = __ldg(reinterpret_cast<const int4*>(s2c + seq0) + lane);
+    // rows past N (ragged last tile) gather cell 0: their values are masked / discarded
+    const int4 c = seq0 + 4 * lane < N ? __ldg(reinterpret_cast<const int4*>(s2c + seq0) + lane) : make_int4(0, 0, 0, 0);
     const int32_t base = b * N;
     sm100::tma_gather4(dst + lane * 4 * D * 2, map, bar, h * D, base + c.x, base + c.y, base + c.z, base + c.w, pol);
   } else if (lane == 0) {
@@ -89,8 +90,9 @@ __device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* map, 
 
 // Element mask of a partial tile for query row q (box = row_box(q)), keys k0 .. k0+127.
 template <bool kTwoD>
-__device__ __forceinline__ void apply_row_mask(float (&s)[kBlock], const Pattern& pat, const RowBox& box,
+__device__ __forceinline__ void apply_row_mask(float (&s)[kBlock], const Pattern& pat, const RowBox& box_in,
                                                int32_t k0) {
+  const RowBox box = clip_box<kTwoD>(pat, box_in);   // phantom keys (k >= N) are never allowed
   if (!kTwoD) {
 #pragma unroll
     for (int c = 0; c < kBlock; ++c)
@@ -166,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   extern __shared__ uint8_t smem_raw[];
   FwdSmem<D>& sm = *reinterpret_cast<FwdSmem<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t mq = prm.N / kBlock;
+  const int32_t mq = (prm.N + kBlock - 1) / kBlock;   // last q-block may be ragged
   const int32_t units = mq * prm.heads * prm.batch;
 
   if (warp == 0 && lane == 0) {
@@ -378,8 +380,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (row == 0) HLA_TR((2 << 24) | (2 << 16) | g);
       }
 
-      // epilogue: O / l -> bf16 row, LSE (natural log)
-      const int32_t ocell = kGather ? __ldg(prm.s2c + q) : q;   // fused inverse reorder of O
+      // epilogue: O / l -> bf16 row, LSE (natural log); phantom rows (q >= N) write nothing
+      const bool real = q < prm.N;
+      const int32_t ocell = kGather ? (real ? __ldg(prm.s2c + q) : 0) : q;   // fused inverse reorder of O
       const int64_t orow = ((int64_t)b * prm.N + ocell) * prm.heads + h;
       uint4* optr = reinterpret_cast<uint4*>(prm.o + orow * D);
       const float inv_l = l > 0.f ? 1.f / l : 0.f;
@@ -392,19 +395,22 @@ __global__ void __launch_bounds__(kThreads, 2)
         sm100::tmem_ld32(tmem + lane_off + kColO + c * 32, *reinterpret_cast<uint32_t(*)[32]>(o + c * 32));
       sm100::tmem_wait_ld();
       // TMEM O may now be overwritten by the next unit's first PV (it waits p_full)
+      if (real) {
 #pragma unroll
-      for (int v4 = 0; v4 < D / 8; ++v4) {
-        uint4 w;
-        w.x = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 0]) * inv_l, __uint_as_float(o[v4 * 8 + 1]) * inv_l);
-        w.y = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 2]) * inv_l, __uint_as_float(o[v4 * 8 + 3]) * inv_l);
-        w.z = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 4]) * inv_l, __uint_as_float(o[v4 * 8 + 5]) * inv_l);
-        w.w = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 6]) * inv_l, __uint_as_float(o[v4 * 8 + 7]) * inv_l);
-        optr[v4] = w;
+        for (int v4 = 0; v4 < D / 8; ++v4) {
+          uint4 w;
+          w.x = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 0]) * inv_l, __uint_as_float(o[v4 * 8 + 1]) * inv_l);
+          w.y = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 2]) * inv_l, __uint_as_float(o[v4 * 8 + 3]) * inv_l);
+          w.z = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 4]) * inv_l, __uint_as_float(o[v4 * 8 + 5]) * inv_l);
+          w.w = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 6]) * inv_l, __uint_as_float(o[v4 * 8 + 7]) * inv_l);
+          optr[v4] = w;
+        }
       }
       if (row == 0) HLA_TR((2 << 24) | (4 << 16) | it.n);
       const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
-      prm.lse[((int64_t)b * prm.heads + h) * prm.N + q] =
-          l > 0.f ? (m_use + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+      if (real)
+        prm.lse[((int64_t)b * prm.heads + h) * prm.N + q] =
+            l > 0.f ? (m_use + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
       tiles_done += it.nt;
       it.t = it.nt - 1;
       it.advance(prm.row_ptr, mq, units);
@@ -442,9 +448,9 @@ hla_status check_attn_args(const hla_pattern_desc* d, const hla_block_mask* m, i
   HLA_REQUIRE(head_dim == 32 || head_dim == 64, HLA_ERR_UNSUPPORTED, "head_dim %d not in {32, 64}", head_dim);
   HLA_REQUIRE(d->block_q == kBlock && d->block_k == kBlock, HLA_ERR_UNSUPPORTED,
               "attention needs block_q == block_k == 128 (got %d, %d)", d->block_q, d->block_k);
-  HLA_REQUIRE(pat->N % kBlock == 0, HLA_ERR_UNSUPPORTED, "N=%d not a multiple of 128 (phantom padding is NEXT-4)",
-              pat->N);
-  HLA_REQUIRE(m->n_qblocks == pat->N / kBlock && m->n_kblocks == pat->N / kBlock, HLA_ERR_INVALID,
+  HLA_REQUIRE(pat->N % 4 == 0, HLA_ERR_UNSUPPORTED, "N=%d not a multiple of 4", pat->N);
+  const int32_t nb = (pat->N + kBlock - 1) / kBlock;   // ragged last block: phantom rows masked / not written
+  HLA_REQUIRE(m->n_qblocks == nb && m->n_kblocks == nb, HLA_ERR_INVALID,
               "mask built for a different N / block");
   HLA_REQUIRE(batch >= 1 && batch <= 65535 && heads >= 1 && heads <= 65535, HLA_ERR_INVALID,
               "batch %d / heads %d out of range", batch, heads);
@@ -496,7 +502,7 @@ extern "C" hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_ma
     if ((st = make_rows_map(&mk, k, rows, heads, head_dim, kBlock)) != HLA_OK) return st;
     if ((st = make_rows_map(&mv, v, rows, heads, head_dim, kBlock)) != HLA_OK) return st;
   }
-  const int32_t mqb = pat.N / kBlock;
+  const int32_t mqb = (pat.N + kBlock - 1) / kBlock;
   if (head_dim == 64) {
     if (gather) return launch_fwd<64, false, true>(mq, mk, mv, prm, mqb, stream);
     return two_d ? launch_fwd<64, true, false>(mq, mk, mv, prm, mqb, stream)

@@ -103,4 +103,17 @@ __device__ __forceinline__ RowBox col_box(const Pattern& p, int32_t k) {
   return row_box(p, k);  // symmetric patterns
 }
 
+// Intersect a row / column box with the real sequence (ragged last tile): 1D
+// intervals with [0, N), 2D row ranges with [0, H) (columns are inside [0, W) by
+// construction of the 2D boxes, and rows < H imply k < N).
+template <bool kTwoD>
+__device__ __forceinline__ RowBox clip_box(const Pattern& p, RowBox b) {
+  const int32_t lim = kTwoD ? p.H : p.N;
+  const int32_t lo = b.lo < 0 ? 0 : b.lo;
+  const int32_t hi = min(b.lo + b.len, lim);
+  b.lo = lo;
+  b.len = hi > lo ? hi - lo : 0;
+  return b;
+}
+
 }  // namespace hla

@@ -42,6 +42,14 @@ SMALL = [
     ("DENSE", 16, 32, 1, 1, 1, 2, 64),
     ("NA2D", 24, 16, 5, 3, 1, 1, 32),      # non-power-of-two width
     ("WSA", 48, 16, 4, 8, 1, 1, 64),
+    # ragged N (N % 128 != 0): phantom rows / columns of the last tile
+    ("HWA", 8, 8, 8, 8, 2, 3, 32),         # cfg5 stage 4 (7x7 padded to 8x8: N = 64 < one tile)
+    ("HNA", 8, 8, 3, 3, 1, 2, 64),
+    ("HSA", 4, 4, 3, 3, 1, 1, 32),         # N = 16
+    ("WSA", 56, 56, 7, 7, 1, 2, 64),       # paper shape 56x56, W7 (N = 3136 = 24.5 tiles), row-major
+    ("SA", 56, 56, 7, 7, 1, 1, 64),
+    ("NA2D", 56, 56, 7, 7, 1, 1, 32),
+    ("DENSE", 10, 20, 1, 1, 1, 2, 64),     # N = 200
 ]
 
 
@@ -136,6 +144,29 @@ def test_bwd_small(case, sharp):
         f = max(1.0, float(np.sqrt((ref ** 2).mean())) / 0.25) if sharp else 1.0
         assert_close(name, to_np(got), ref, max_abs=2e-2 * f, mean_abs=2e-3 * f)
     assert int(visited.item()) == B * H * m.nnz
+
+
+CFG5 = [(64, 3), (32, 6), (16, 12), (8, 24)]   # HWT-T stages: grid (56/28/14/7 padded), heads
+
+
+@pytest.mark.parametrize("g,H", CFG5, ids=lambda v: str(v))
+def test_cfg5_stage(g, H):
+    """BASELINE cfg5: HWT-T stack stage (window 49 -> 64 tokens = 8x8, d32), forward and
+    backward through the layer API (fused reorder), one slice checked in full."""
+    B, d = 4, 32
+    N = g * g
+    q, k, v, do = _inputs(B, N, H, d, seed=21)
+    layer = hla.HilbertLocalAttention("HWA", g, g, 8, 8, B, H, d, device=DEV)
+    o = layer.forward(q, k, v).clone()
+    dq, dk, dv = (t.clone() for t in layer.backward(do))
+    torch.cuda.synchronize()
+    spec = Spec("HWA", g, g, 8, 8)
+    s2c = hilbert.hilbert_order(g, g)[0]
+    b, h = B - 1, H - 1
+    Q, K, V, DO = (to_np(t[b, :, h])[s2c] for t in (q, k, v, do))
+    dQ, dK, dV, O, _ = oatt.attn_bwd_slice(Q, K, V, DO, spec)
+    for name, got, ref in (("O", o, O), ("dQ", dq, dQ), ("dK", dk, dK), ("dV", dv, dV)):
+        assert_close("cfg5 g%d %s" % (g, name), to_np(got[b, :, h])[s2c], ref)
 
 
 FULL_BWD = [c for c in FULL if c[0] in ("cfg2", "cfg2-rm", "cfg3", "cfg3-rm", "cfg4", "cfg4-rm")]
