@@ -41,6 +41,16 @@ HLA_API hla_status hla_debug_mma_rate(int32_t N, int32_t iters, int32_t a_major_
 HLA_API hla_status hla_debug_tmem_rate(int32_t nwarps, int32_t iters, int32_t mode, int32_t batch,
                                        long long* out_cycles, cudaStream_t stream);
 
+/* hla_debug_ex2_rate: one CTA of `threads` threads, each `iters` x 16 independent
+ * ex2.approx.f32; out_cycles = SM cycles (MUFU throughput probe). */
+HLA_API hla_status hla_debug_ex2_rate(int32_t threads, int32_t iters, long long* out_cycles, float* sink,
+                                      cudaStream_t stream);
+
+/* hla_debug_softmax_rate: `blocks` CTAs x 128 threads run the forward softmax inner
+ * loop (128 exps per thread) `iters` times; out_cycles[block] = SM cycles. */
+HLA_API hla_status hla_debug_softmax_rate(int32_t blocks, int32_t iters, long long* out_cycles, uint32_t* sink,
+                                          cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,7 +19,8 @@ EXPORTED = ("hla_hilbert_index", "hla_hilbert_perm", "hla_build_block_mask", "hl
             "hla_attn_fwd", "hla_attn_bwd", "hla_attn_bwd_workspace", "hla_attn_bwd_preprocess",
             "hla_attn_bwd_main", "hla_attn_bwd_finalize", "hla_last_error", "hla_version",
             "hla_debug_umma", "hla_debug_gather4", "hla_debug_mma_rate",
-            "hla_debug_tmem_rate")
+            "hla_debug_tmem_rate", "hla_debug_ex2_rate",
+            "hla_debug_softmax_rate")
 
 
 class PatternDesc(ctypes.Structure):
@@ -68,6 +69,8 @@ def lib():
         "hla_debug_gather4": [vp, i64, i32, i32, vp, i32, i32, vp, vp],
         "hla_debug_mma_rate": [i32, i32, i32, i32, i32, vp, vp],
         "hla_debug_tmem_rate": [i32, i32, i32, i32, vp, vp],
+        "hla_debug_ex2_rate": [i32, i32, vp, vp, vp],
+        "hla_debug_softmax_rate": [i32, i32, vp, vp, vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)

@@ -271,13 +271,17 @@ __global__ void __launch_bounds__(kThreads, 2)
       while (cur.valid) {
         FwdIter nxt = cur;
         nxt.advance(prm.row_ptr, mq, units);
+        bool next_s_issued = false;
         if (nxt.valid) {
-          // S(g+1) overwrites S(g): only after the softmax pulled S(g) into registers
+          // S(g+1) overwrites S(g): only after the softmax pulled S(g) into registers.
+          // Its operands may still be in flight (next unit's Q, K): then PV(g) goes first.
           sm100::mbar_wait(&sm.s_free, g & 1);
-          if (nxt.t == 0) sm100::mbar_wait(&sm.q_full[nxt.n & 1], (nxt.n >> 1) & 1);
-          sm100::mbar_wait(&sm.k_full[(g + 1) & 1], ((g + 1) >> 1) & 1);
-          sm100::tc_fence_after();
-          issue_s(nxt, g + 1);
+          if ((nxt.t != 0 || sm100::mbar_test_wait(&sm.q_full[nxt.n & 1], (nxt.n >> 1) & 1)) &&
+              sm100::mbar_test_wait(&sm.k_full[(g + 1) & 1], ((g + 1) >> 1) & 1)) {
+            sm100::tc_fence_after();
+            issue_s(nxt, g + 1);
+            next_s_issued = true;
+          }
         }
         sm100::mbar_wait(&sm.p_full, g & 1);
         HLA_TR((1 << 24) | (2 << 16) | g);
@@ -292,6 +296,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (cur.t == cur.nt - 1) {
           sm100::mma_commit(&sm.q_empty[cur.n & 1]);
           sm100::mma_commit(&sm.o_full);
+        }
+        if (nxt.valid && !next_s_issued) {
+          if (nxt.t == 0) sm100::mbar_wait(&sm.q_full[nxt.n & 1], (nxt.n >> 1) & 1);
+          sm100::mbar_wait(&sm.k_full[(g + 1) & 1], ((g + 1) >> 1) & 1);
+          sm100::tc_fence_after();
+          issue_s(nxt, g + 1);
         }
         cur = nxt;
         ++g;
@@ -322,6 +332,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int c = 0; c < 4; ++c)
           sm100::tmem_ld32(tmem + lane_off + kColS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(sr + c * 32));
         sm100::tmem_wait_ld();
+        if (row == 0) HLA_TR((6 << 24) | (1 << 16) | g);
         sm100::tc_fence_before();
         sm100::mbar_arrive(&sm.s_free);          // the MMA may overwrite S with S(g+1)
         float (&s)[kBlock] = *reinterpret_cast<float(*)[kBlock]>(sr);
@@ -338,6 +349,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
           for (int i = 0; i < j; ++i) m8[i] = fmaxf(m8[i], m8[i + j]);
         const float m_tile = m8[0] * sl2;
+        if (row == 0) HLA_TR((6 << 24) | (2 << 16) | g);
         // lazy rescale (exact): keep the reference max unless it grew by > 8 (x256)
         const float m_new = (m_tile > m_ref + 8.f) ? m_tile : m_ref;
         const float alpha = (m_new == m_ref) ? 1.f : sm100::ex2(m_ref - m_new);
@@ -354,11 +366,13 @@ __global__ void __launch_bounds__(kThreads, 2)
           pk[e] = sm100::pack_bf16(p0, p1);
         }
         l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
+        if (row == 0) HLA_TR((6 << 24) | (3 << 16) | g);
         // P(g-1) / O are read by PV(g-1): wait for it before writing P(g) or rescaling O
         if (g > 0) {
           sm100::mbar_wait(&sm.pv_done, (g - 1) & 1);
           sm100::tc_fence_after();
         }
+        if (row == 0) HLA_TR((6 << 24) | (4 << 16) | g);
         if (__any_sync(0xffffffffu, t > 0 && alpha != 1.f)) {
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {

@@ -193,6 +193,55 @@ __global__ void debug_tmem_rate_kernel(int iters, int mode, int batch, long long
   if (warp == 0) sm100::tmem_dealloc(tmem_base, 512);
 }
 
+// MUFU.EX2 throughput probe: every thread runs `iters` x 16 independent ex2.approx;
+// out[0] = SM cycles of the block.
+__global__ void debug_ex2_rate_kernel(int iters, float seed, long long* out, float* sink) {
+  float x[16];
+  for (int i = 0; i < 16; ++i) x[i] = seed * (float)(threadIdx.x + i) * 1e-6f;
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = sm100::ex2(x[i]) - 1.0f;
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  float s = 0.f;
+  for (int i = 0; i < 16; ++i) s += x[i];
+  if (s == 12345.f) sink[0] = s;
+  if (threadIdx.x == 0) out[0] = t1 - t0;
+}
+
+// Softmax inner-loop probe: each thread exponentiates a 128-wide row `iters` times
+// exactly like attn_fwd_kernel (FFMA + ex2 + row sum + bf16 pack); out[blockIdx] = cycles.
+__global__ void __launch_bounds__(128) debug_softmax_rate_kernel(int iters, float sl2, long long* out, uint32_t* sink) {
+  uint32_t sr[128];
+  for (int i = 0; i < 128; ++i) sr[i] = __float_as_uint((float)((threadIdx.x * 7 + i * 13) % 97) * 0.01f);
+  float l = 0.f, m_use = 0.5f;
+  uint32_t acc = 0;
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    float l4[4] = {0.f, 0.f, 0.f, 0.f};
+    uint32_t pk[64];
+#pragma unroll
+    for (int e = 0; e < 64; ++e) {
+      const float p0 = sm100::ex2(fmaf(__uint_as_float(sr[2 * e]), sl2, -m_use));
+      const float p1 = sm100::ex2(fmaf(__uint_as_float(sr[2 * e + 1]), sl2, -m_use));
+      l4[e & 3] += p0 + p1;
+      pk[e] = sm100::pack_bf16(p0, p1);
+    }
+    l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
+#pragma unroll
+    for (int e = 0; e < 64; ++e) acc ^= pk[e];
+    m_use += 1e-7f;
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  if (acc == 0x12345678u && l == 1.f) sink[0] = acc;
+  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+}
+
 // 128 token rows (indices idx[0..127]) of head h gathered with .tile::gather4 into a
 // SWIZZLE_<2d> tile, then read back through the swizzle into out[128][d].
 template <int D>
@@ -242,6 +291,22 @@ extern "C" hla_status hla_debug_tmem_rate(int32_t nwarps, int32_t iters, int32_t
   clear_error();
   HLA_REQUIRE(nwarps % 4 == 0 && nwarps >= 4 && nwarps <= 16 && iters > 0 && batch >= 1, HLA_ERR_INVALID, "bad args");
   debug_tmem_rate_kernel<<<1, nwarps * 32, 0, stream>>>(iters, mode, batch, out_cycles);
+  HLA_CUDA_TRY(cudaGetLastError());
+  return HLA_OK;
+}
+
+extern "C" hla_status hla_debug_ex2_rate(int32_t threads, int32_t iters, long long* out_cycles, float* sink,
+                                         cudaStream_t stream) {
+  clear_error();
+  debug_ex2_rate_kernel<<<1, threads, 0, stream>>>(iters, 1.0f, out_cycles, sink);
+  HLA_CUDA_TRY(cudaGetLastError());
+  return HLA_OK;
+}
+
+extern "C" hla_status hla_debug_softmax_rate(int32_t blocks, int32_t iters, long long* out_cycles, uint32_t* sink,
+                                             cudaStream_t stream) {
+  clear_error();
+  debug_softmax_rate_kernel<<<blocks, 128, 0, stream>>>(iters, 0.18f, out_cycles, sink);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
 }
