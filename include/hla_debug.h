@@ -46,6 +46,12 @@ HLA_API hla_status hla_debug_tmem_rate(int32_t nwarps, int32_t iters, int32_t mo
 HLA_API hla_status hla_debug_ex2_rate(int32_t threads, int32_t iters, long long* out_cycles, float* sink,
                                       cudaStream_t stream);
 
+/* hla_debug_load_rate: `ctas` CTAs (one per SM) each stream `tiles` 16 KB tiles (128
+ * token rows x 64 bf16 of one head of a [rows, heads, 64] tensor) through a `stages`-deep
+ * shared-memory ring; mode 0 = one 3-D TMA box, 1 = 32 TMA gather4, 2 = cp.async by 128
+ * threads, 3 = one 16 KB contiguous bulk copy.  out_cycles[cta] = clock64 span. */
+HLA_API hla_status hla_debug_load_rate(const void* src, int64_t rows, int32_t heads, int32_t mode, int32_t stages,
+                                       int32_t ctas, int32_t tiles, long long* out_cycles, cudaStream_t stream);
 /* hla_debug_softmax_rate: `blocks` CTAs x 128 threads run the forward softmax inner
  * loop (128 exps per thread) `iters` times; out_cycles[block] = SM cycles. */
 HLA_API hla_status hla_debug_softmax_rate(int32_t blocks, int32_t iters, long long* out_cycles, uint32_t* sink,

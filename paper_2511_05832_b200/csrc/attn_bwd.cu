@@ -31,7 +31,7 @@ namespace hla {
 namespace {
 
 constexpr int kBlock = 128;
-constexpr int kThreads = 448;   // 14 warps: TMA, MMA, 8 x P/dS, 4 x dQ
+constexpr int kThreads = 512;   // 16 warps: TMA, MMA, 8 x P/dS, 4 x dQ, 2 x TMA
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColS = 0, kColDP = 128, kColP = 256, kColDQ = 320, kColDV = 384, kColDK = 448;
 constexpr float kLog2e = 1.4426950408889634f;
@@ -162,9 +162,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < 2; ++s) {
-      sm100::mbar_init(&sm.kv_full[s], 1);
+      sm100::mbar_init(&sm.kv_full[s], 2);    // producer warps 0 (K), 14 (V)
       sm100::mbar_init(&sm.kv_empty[s], 1);
-      sm100::mbar_init(&sm.q_full[s], 1);
+      sm100::mbar_init(&sm.q_full[s], 3);     // producer warps 0 (LSE, D), 14 (Q), 15 (dO)
       sm100::mbar_init(&sm.q_empty[s], 1);
     }
     for (int hh = 0; hh < 2; ++hh) {
@@ -193,11 +193,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned long long tiles_done = 0;
   HLA_TR_DECL;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+  if (warp == 0 || warp >= 14) {
+    // ----------------------------------------------------------- TMA producers
+    // Three warps run the same schedule and split the loads (a CTA's TMA gather4
+    // throughput grows with the number of issuing warps): warp 0 K + LSE / D,
+    // warp 14 V + Q, warp 15 dO.  Every warp arrives (with its own byte count) on
+    // the barriers it feeds, so no expect_tx has to precede another warp's copy.
     {
       const uint64_t pol_kv = sm100::policy_evict_first();
       const uint64_t pol_q = sm100::policy_evict_last();
+      const int role = warp == 0 ? 0 : warp - 13;   // 0, 1, 2
+      constexpr uint32_t kTile = BwdSmem<D>::kTileBytes;
       uint32_t n = 0, g = 0;
       int64_t stage_tag0 = -1, stage_tag1 = -1;   // (b, h, q-block) held by stage 0 / 1
       for (int32_t kq = 0;; ++kq) {
@@ -208,16 +214,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (nt == 0) continue;
         const int64_t bh = (int64_t)b * prm.heads + h;
         const int kvs = n & 1;
-        if (n >= 2) sm100::mbar_wait(&sm.kv_empty[kvs], ((n >> 1) - 1) & 1);
-        if (lane == 0) HLA_TR((3 << 24) | ((1) << 16) | (n));
-        if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.kv_full[kvs], 2 * BwdSmem<D>::kTileBytes);
-        __syncwarp();
-        load_rows<D, kGather>(sm.k[kvs], &tmK, &sm.kv_full[kvs], h, b, prm.N, kb * kBlock, prm.s2c, pol_kv, lane);
-        load_rows<D, kGather>(sm.v[kvs], &tmV, &sm.kv_full[kvs], h, b, prm.N, kb * kBlock, prm.s2c, pol_kv, lane);
+        if (role < 2) {
+          if (n >= 2) sm100::mbar_wait(&sm.kv_empty[kvs], ((n >> 1) - 1) & 1);
+          if (lane == 0) HLA_TR((3 << 24) | ((1) << 16) | (n));
+          if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.kv_full[kvs], kTile);
+          __syncwarp();
+          load_rows<D, kGather>(role == 0 ? sm.k[kvs] : sm.v[kvs], role == 0 ? &tmK : &tmV, &sm.kv_full[kvs], h, b,
+                                prm.N, kb * kBlock, prm.s2c, pol_kv, lane);
+        }
         for (int t = 0; t < nt; ++t, ++g) {
           const int s = g & 1;
           if (g >= 2) sm100::mbar_wait(&sm.q_empty[s], ((g >> 1) - 1) & 1);
-          if (lane == 0) HLA_TR((3 << 24) | ((2) << 16) | (g));
+          if (lane == 0 && role == 0) HLA_TR((3 << 24) | ((2) << 16) | (g));
           const int32_t qblk = __ldg(prm.t_col_idx + rs + t);
           const int64_t tag = bh * prm.N + qblk;     // (b, h, q-block) held by the stage
           if (tag == (s ? stage_tag1 : stage_tag0)) {
@@ -227,16 +235,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             continue;
           }
           if (s) stage_tag1 = tag; else stage_tag0 = tag;
-          if (lane == 0) {
-            // LSE / D of the real rows only (ragged last tile: N % 4 == 0, so 16-B multiples)
-            const uint32_t vbytes = (uint32_t)min(kBlock, prm.N - qblk * kBlock) * 4u;
-            sm100::mbar_arrive_expect_tx(&sm.q_full[s], 2 * BwdSmem<D>::kTileBytes + 2 * vbytes);
-            sm100::bulk_load(sm.lse[s], prm.lse2 + bh * prm.N + qblk * kBlock, vbytes, &sm.q_full[s]);
-            sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * kBlock, vbytes, &sm.q_full[s]);
+          if (role == 0) {
+            if (lane == 0) {
+              // LSE / D of the real rows only (ragged last tile: N % 4 == 0, so 16-B multiples)
+              const uint32_t vbytes = (uint32_t)min(kBlock, prm.N - qblk * kBlock) * 4u;
+              sm100::mbar_arrive_expect_tx(&sm.q_full[s], 2 * vbytes);
+              sm100::bulk_load(sm.lse[s], prm.lse2 + bh * prm.N + qblk * kBlock, vbytes, &sm.q_full[s]);
+              sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * kBlock, vbytes, &sm.q_full[s]);
+            }
+          } else {
+            if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.q_full[s], kTile);
+            __syncwarp();
+            load_rows<D, kGather>(role == 1 ? sm.q[s] : sm.dO[s], role == 1 ? &tmQ : &tmDO, &sm.q_full[s], h, b,
+                                  prm.N, qblk * kBlock, prm.s2c, pol_q, lane);
           }
-          __syncwarp();
-          load_rows<D, kGather>(sm.q[s], &tmQ, &sm.q_full[s], h, b, prm.N, qblk * kBlock, prm.s2c, pol_q, lane);
-          load_rows<D, kGather>(sm.dO[s], &tmDO, &sm.q_full[s], h, b, prm.N, qblk * kBlock, prm.s2c, pol_q, lane);
         }
         ++n;
       }
@@ -462,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tiles_done += nt;
     }
-  } else {
+  } else if (warp < 14) {
     // ------------------------------------------ dQ partial -> fp32 accumulator
     // thread = query row: drain the dQ_i tile from TMEM (then release it), stage it
     // in shared memory (two 32-column halves, 128B swizzle) and let the TMA engine
@@ -520,25 +532,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         sm100::mbar_wait(&sm.dkv_full, n & 1);
         if (leader) HLA_TR((2 << 24) | ((6) << 16) | (n));
         sm100::tc_fence_after();
-        uint32_t rv[D], rk[D];
+        // dV then dK, each packed to bf16 right away (64 live registers, not 128)
+        uint32_t pv[D / 2], pk[D / 2];
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          sm100::tmem_ld32(tmem + lane_off + kColDV + c * 32, *reinterpret_cast<uint32_t(*)[32]>(rv + c * 32));
-          sm100::tmem_ld32(tmem + lane_off + kColDK + c * 32, *reinterpret_cast<uint32_t(*)[32]>(rk + c * 32));
+        for (int which = 0; which < 2; ++which) {
+          uint32_t r[D];
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c)
+            sm100::tmem_ld32(tmem + lane_off + (which ? kColDK : kColDV) + c * 32,
+                             *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
+          sm100::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < D / 2; ++e) {
+            const uint32_t w = sm100::pack_bf16(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
+            if (which) pk[e] = w; else pv[e] = w;
+          }
         }
-        sm100::tmem_wait_ld();
         sm100::tc_fence_before();
         sm100::mbar_arrive(&sm.epi_done);      // dV / dK accumulators may now be reset
 #pragma unroll
         for (int v4 = 0; v4 < D / 8 && real; ++v4) {
-          dvp[v4] = make_uint4(sm100::pack_bf16(__uint_as_float(rv[v4 * 8 + 0]), __uint_as_float(rv[v4 * 8 + 1])),
-                               sm100::pack_bf16(__uint_as_float(rv[v4 * 8 + 2]), __uint_as_float(rv[v4 * 8 + 3])),
-                               sm100::pack_bf16(__uint_as_float(rv[v4 * 8 + 4]), __uint_as_float(rv[v4 * 8 + 5])),
-                               sm100::pack_bf16(__uint_as_float(rv[v4 * 8 + 6]), __uint_as_float(rv[v4 * 8 + 7])));
-          dkp[v4] = make_uint4(sm100::pack_bf16(__uint_as_float(rk[v4 * 8 + 0]), __uint_as_float(rk[v4 * 8 + 1])),
-                               sm100::pack_bf16(__uint_as_float(rk[v4 * 8 + 2]), __uint_as_float(rk[v4 * 8 + 3])),
-                               sm100::pack_bf16(__uint_as_float(rk[v4 * 8 + 4]), __uint_as_float(rk[v4 * 8 + 5])),
-                               sm100::pack_bf16(__uint_as_float(rk[v4 * 8 + 6]), __uint_as_float(rk[v4 * 8 + 7])));
+          dvp[v4] = make_uint4(pv[v4 * 4 + 0], pv[v4 * 4 + 1], pv[v4 * 4 + 2], pv[v4 * 4 + 3]);
+          dkp[v4] = make_uint4(pk[v4 * 4 + 0], pk[v4 * 4 + 1], pk[v4 * 4 + 2], pk[v4 * 4 + 3]);
         }
         if (leader) HLA_TR((2 << 24) | ((7) << 16) | (n));
         ++n;

@@ -203,9 +203,11 @@ __global__ void __launch_bounds__(kThreads, 2)
   // register split (setmaxnreg acts per warpgroup): the control warpgroup gives its
   // registers to the softmax warpgroup (one thread per row keeps a 128-wide S row)
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
-    if (warp == 0) {
-      // ---------------------------------------------------------- TMA producer
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
+    if (warp != 1) {
+      // ---------------------------------------------------------- TMA producers
+      // warp 0 loads Q, warp 2 K, warp 3 V: a CTA's TMA row / gather4 throughput grows
+      // with the number of issuing warps (one warp alone caps gather4 at ~6 B/clk)
       const uint64_t pol_q = sm100::policy_evict_first();
       const uint64_t pol_kv = sm100::policy_evict_last();
       int64_t tag0 = -1, tag1 = -1;   // (b, h, kv-block) held by K/V stage 0 / 1
@@ -215,33 +217,31 @@ __global__ void __launch_bounds__(kThreads, 2)
       while (it.valid) {
         const int32_t qb = it.u % mq, h = (it.u / mq) % prm.heads, b = it.u / (mq * prm.heads);
         const int64_t bh = (int64_t)b * prm.heads + h;
-        const int qs = it.n & 1;
-        if (it.n >= 2) sm100::mbar_wait(&sm.q_empty[qs], ((it.n >> 1) - 1) & 1);
-        if (lane == 0) HLA_TR((3 << 24) | (1 << 16) | it.n);
-        if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.q_full[qs], FwdSmem<D>::kTileBytes);
-        __syncwarp();
-        load_rows<D, kGather>(sm.q[qs], &tmQ, &sm.q_full[qs], h, b, prm.N, qb * kBlock, prm.s2c, pol_q, lane);
-        for (int t = 0; t < it.nt; ++t, ++g) {
-          const int s = g & 1;
-          if (g >= 2) sm100::mbar_wait(&sm.kv_empty[s], ((g >> 1) - 1) & 1);
-          if (lane == 0) HLA_TR((3 << 24) | (2 << 16) | g);
-          const int32_t kvb = __ldg(prm.col_idx + it.rs + t);
-          const int64_t tag = bh * mq + kvb;
-          if (tag == (s ? tag1 : tag0)) {   // stage already holds this K/V tile
-            if (lane == 0) {
-              sm100::mbar_arrive(&sm.k_full[s]);
-              sm100::mbar_arrive(&sm.v_full[s]);
-            }
-            continue;
-          }
-          if (s) tag1 = tag; else tag0 = tag;
-          if (lane == 0) {
-            sm100::mbar_arrive_expect_tx(&sm.k_full[s], FwdSmem<D>::kTileBytes);
-            sm100::mbar_arrive_expect_tx(&sm.v_full[s], FwdSmem<D>::kTileBytes);
-          }
+        if (warp == 0) {
+          const int qs = it.n & 1;
+          if (it.n >= 2) sm100::mbar_wait(&sm.q_empty[qs], ((it.n >> 1) - 1) & 1);
+          if (lane == 0) HLA_TR((3 << 24) | (1 << 16) | it.n);
+          if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.q_full[qs], FwdSmem<D>::kTileBytes);
           __syncwarp();
-          load_rows<D, kGather>(sm.k[s], &tmK, &sm.k_full[s], h, b, prm.N, kvb * kBlock, prm.s2c, pol_kv, lane);
-          load_rows<D, kGather>(sm.v[s], &tmV, &sm.v_full[s], h, b, prm.N, kvb * kBlock, prm.s2c, pol_kv, lane);
+          load_rows<D, kGather>(sm.q[qs], &tmQ, &sm.q_full[qs], h, b, prm.N, qb * kBlock, prm.s2c, pol_q, lane);
+        } else {
+          const bool is_k = warp == 2;
+          for (int t = 0; t < it.nt; ++t, ++g) {
+            const int s = g & 1;
+            uint64_t* full = is_k ? &sm.k_full[s] : &sm.v_full[s];
+            if (g >= 2) sm100::mbar_wait(&sm.kv_empty[s], ((g >> 1) - 1) & 1);
+            const int32_t kvb = __ldg(prm.col_idx + it.rs + t);
+            const int64_t tag = bh * mq + kvb;
+            if (tag == (s ? tag1 : tag0)) {   // stage already holds this K/V tile
+              if (lane == 0) sm100::mbar_arrive(full);
+              continue;
+            }
+            if (s) tag1 = tag; else tag0 = tag;
+            if (lane == 0) sm100::mbar_arrive_expect_tx(full, FwdSmem<D>::kTileBytes);
+            __syncwarp();
+            load_rows<D, kGather>(is_k ? sm.k[s] : sm.v[s], is_k ? &tmK : &tmV, full, h, b, prm.N, kvb * kBlock,
+                                  prm.s2c, pol_kv, lane);
+          }
         }
         it.t = it.nt - 1;
         it.advance(prm.row_ptr, mq, units);
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
     // --------------------------------------------------- softmax + epilogue
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;

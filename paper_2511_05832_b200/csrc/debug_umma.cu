@@ -311,6 +311,109 @@ extern "C" hla_status hla_debug_softmax_rate(int32_t blocks, int32_t iters, long
   return HLA_OK;
 }
 
+// ---- load-rate probe: how fast can a CTA stream 16 KB K/V-like tiles (128 token
+// rows x 64 bf16 of one head, rows heads*128 B apart) into shared memory?
+// mode = base | (issuing warps W << 4) | (one barrier per issuing warp << 8);
+// base 0 = 3-D TMA box (128 / W rows per warp), 1 = gather4 (32 / W per warp),
+// 2 = cp.async by 128 threads (W = 4), 3 = 16 KB contiguous bulk copy (W = 1).
+constexpr int kLoadStagesMax = 8;
+
+__global__ void debug_load_kernel(const __grid_constant__ CUtensorMap m3, const __grid_constant__ CUtensorMap mg,
+                                  const __nv_bfloat16* src, int64_t rows, int32_t heads, int32_t mode,
+                                  int32_t stages, int32_t tiles, long long* out_cycles) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t (*tile)[16384] = reinterpret_cast<uint8_t(*)[16384]>(base);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + stages * 16384);   // [stage][8]
+  uint64_t* empty = full + kLoadStagesMax * 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kind = mode & 15, W = (mode >> 4) & 15, nb = (mode >> 8) & 1 ? W : 1;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < stages; ++i) {
+      for (int j = 0; j < nb; ++j) sm100::mbar_init(&full[i * 8 + j], kind == 2 ? 128 / nb : 1);
+      sm100::mbar_init(&empty[i * 8], 1);
+    }
+    sm100::fence_mbar_init();
+  }
+  __syncthreads();
+  const long long t0 = clock64();
+  const int64_t nrb = rows / 128;
+  if (warp < W) {
+    const int my_bar = nb > 1 ? warp : 0;
+    const uint32_t part = 16384 / nb;
+    for (int i = 0; i < tiles; ++i) {
+      const int s = i % stages;
+      if (i >= stages) sm100::mbar_wait(&empty[s * 8], ((i / stages) - 1) & 1);
+      const int64_t t = (int64_t)blockIdx.x * tiles + i;
+      const int32_t head = (int32_t)(t % heads);
+      const int64_t r0 = ((t / heads) % nrb) * 128;
+      uint8_t* dst = tile[s];
+      uint64_t* bar = &full[s * 8 + my_bar];
+      if (kind == 0) {
+        if (lane == 0) {
+          if (nb > 1 || warp == 0) sm100::mbar_arrive_expect_tx(bar, nb > 1 ? part : 16384);
+        }
+        if (W > 1) asm volatile("bar.sync 1, %0;" ::"r"(W * 32) : "memory");
+        if (lane == 0) {
+          const int rw = 128 / W;
+          sm100::tma_load_3d(dst + warp * rw * 128, &m3, bar, 0, head, (int32_t)r0 + warp * rw,
+                             sm100::policy_evict_first());
+        }
+      } else if (kind == 1) {
+        if (lane == 0 && (nb > 1 || warp == 0)) sm100::mbar_arrive_expect_tx(bar, nb > 1 ? part : 16384);
+        if (W > 1) asm volatile("bar.sync 1, %0;" ::"r"(W * 32) : "memory");
+        const int per = 32 / W;
+        if (lane < per) {
+          const int gi = warp * per + lane;
+          const int32_t y = (int32_t)r0 + 4 * gi;
+          sm100::tma_gather4(dst + gi * 512, &mg, bar, head * 64, y, y + 1, y + 2, y + 3,
+                             sm100::policy_evict_first());
+        }
+      } else if (kind == 2) {
+        const int j = threadIdx.x;   // row
+        const char* g = reinterpret_cast<const char*>(src + ((r0 + j) * heads + head) * 64);
+        const uint32_t d = sm100::smem_u32(dst + j * 128);
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + c * 16), "l"(g + c * 16) : "memory");
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(sm100::smem_u32(bar)) : "memory");
+      } else if (lane == 0) {
+        const int64_t nt = rows * heads * 128 / 16384;
+        sm100::mbar_arrive_expect_tx(bar, 16384);
+        sm100::bulk_load(dst, reinterpret_cast<const char*>(src) + (t % nt) * 16384, 16384, bar);
+      }
+    }
+  } else if (warp == W && lane == 0) {
+    for (int i = 0; i < tiles; ++i) {
+      const int s = i % stages;
+      for (int j = 0; j < nb; ++j) sm100::mbar_wait(&full[s * 8 + j], (i / stages) & 1);
+      sm100::mbar_arrive(&empty[s * 8]);
+    }
+    out_cycles[blockIdx.x] = clock64() - t0;
+  }
+}
+
+extern "C" hla_status hla_debug_load_rate(const void* src, int64_t rows, int32_t heads, int32_t mode,
+                                          int32_t stages, int32_t ctas, int32_t tiles, long long* out_cycles,
+                                          cudaStream_t stream) {
+  clear_error();
+  const int kind = mode & 15, W = (mode >> 4) & 15;
+  HLA_REQUIRE(src && out_cycles && kind <= 3 && W >= 1 && W <= 8 && 32 % W == 0 && (kind != 2 || W == 4) &&
+                  stages >= 1 && stages <= kLoadStagesMax && rows % 128 == 0,
+              HLA_ERR_INVALID, "bad load-rate probe arguments");
+  CUtensorMap m3, mg;
+  hla_status st = make_rows_map(&m3, src, rows, heads, 64, kind == 0 ? 128 / W : 128);
+  if (st != HLA_OK) return st;
+  st = make_gather_map(&mg, src, rows, heads, 64, 1);
+  if (st != HLA_OK) return st;
+  const size_t smem = (size_t)stages * 16384 + 2 * kLoadStagesMax * 8 * 8 + 1024;
+  HLA_CUDA_TRY(cudaFuncSetAttribute(debug_load_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  debug_load_kernel<<<ctas, 32 * (W + 1), smem, stream>>>(m3, mg, reinterpret_cast<const __nv_bfloat16*>(src),
+                                                          rows, heads, mode, stages, tiles, out_cycles);
+  HLA_CUDA_TRY(cudaGetLastError());
+  return HLA_OK;
+}
+
 extern "C" hla_status hla_debug_gather4(const void* src, int64_t rows, int32_t heads, int32_t head_dim,
                                         const int32_t* idx, int32_t head, int32_t box_h, void* out,
                                         cudaStream_t stream) {
