@@ -46,6 +46,10 @@ HLA_API hla_status hla_debug_tmem_rate(int32_t nwarps, int32_t iters, int32_t mo
 HLA_API hla_status hla_debug_ex2_rate(int32_t threads, int32_t iters, long long* out_cycles, float* sink,
                                       cudaStream_t stream);
 
+/* hla_debug_softmax_tile: `blocks` CTAs x 128 threads run the forward softmax tile body
+ * with its TMEM traffic (S ld, max, exp2, P st), `iters` times; out_cycles[cta]. */
+HLA_API hla_status hla_debug_softmax_tile(int32_t blocks, int32_t iters, long long* out_cycles, uint32_t* sink,
+                                          cudaStream_t stream);
 /* hla_debug_load_rate: `ctas` CTAs (one per SM) each stream `tiles` 16 KB tiles (128
  * token rows x 64 bf16 of one head of a [rows, heads, 64] tensor) through a `stages`-deep
  * shared-memory ring; mode 0 = one 3-D TMA box, 1 = 32 TMA gather4, 2 = cp.async by 128

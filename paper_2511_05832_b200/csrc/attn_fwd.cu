@@ -7,8 +7,11 @@
 // online softmax, and aggregation with value" (Eq. 1).
 //
 // Persistent CTAs (2 per SM), 256 threads:
-//   warp 0      TMA producer: Q_i once, then K_j / V_j of the listed kv-blocks
-//               into a 2-stage shared-memory ring (separate K and V barriers).
+//   warps 0,2,3 TMA producers (Q_i / K_j / V_j; several issuing warps because a
+//               CTA's TMA gather4 rate grows with them): Q double-buffered per
+//               unit, K / V of the listed kv-blocks in a 2-stage ring; warp 0
+//               also stores each finished O tile (TMA store / scatter4) from
+//               the unit's Q stage, where the softmax warps staged it.
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:
 //                 S_t  = Q_i K_j^T   (SS MMA, 128x128x D, fp32 in TMEM cols [0,128))
 //                 O   += P_t V_j     (TS MMA, P bf16 in TMEM cols [128,192), O in [192,192+D))
@@ -16,7 +19,8 @@
 //               tcgen05.ld, applies the element mask only when the tile is
 //               partial, keeps the online max / sum in registers (lazy rescale:
 //               O is rescaled in TMEM only when the row max grows by > 2^8),
-//               writes P (bf16) to TMEM; epilogue O / l -> bf16, LSE.
+//               writes P (bf16) to TMEM; epilogue O / l -> bf16 rows staged in
+//               shared memory (swizzled like a loaded tile), LSE.
 // The S region is reused by S_{t+1} only after the softmax of tile t has
 // released it (p_full); P has its own region, so S_{t+1} overlaps nothing the
 // PV MMA still reads.  Every commit tracks all earlier MMAs, so s_full(t) also
@@ -29,7 +33,7 @@ namespace hla {
 namespace {
 
 constexpr int kBlock = 128;
-constexpr int kThreads = 256;   // warpgroup 0: TMA, MMA, 2 idle; warpgroup 1: softmax
+constexpr int kThreads = 256;   // warpgroup 0: TMA (Q), MMA, TMA (K), TMA (V); warpgroup 1: softmax
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kColS = 0, kColP = 128, kColO = 192;
 
@@ -52,7 +56,7 @@ struct FwdSmem {
   alignas(1024) uint8_t q[2][kTileBytes];
   alignas(1024) uint8_t k[2][kTileBytes];
   alignas(1024) uint8_t v[2][kTileBytes];
-  uint64_t q_full[2], q_empty[2], k_full[2], v_full[2], kv_empty[2], s_full, s_free, p_full, pv_done, o_full;
+  uint64_t q_full[2], o_staged[2], k_full[2], v_full[2], kv_empty[2], s_full, s_free, p_full, pv_done, o_full;
   uint32_t tmem_base;
 };
 
@@ -73,14 +77,18 @@ __device__ __forceinline__ uint64_t mnmajor_desc(const uint8_t* tile, int kstep)
 // Load the 128 token rows [seq0, seq0 + 128) (sequence order) of head h, batch b.
 // kGather (fused reorder): the tensor is in grid order; the warp gathers the rows of
 // cells s2c[seq0 ..] with 32 TMA .tile::gather4 ops (4 rows each); otherwise one 3-D
-// TMA box.  Called by all 32 lanes of the producer warp after lane 0 armed `bar`.
+// TMA box.  row_cells() looks the cells up (issued early: it is an L2 round trip),
+// issue_rows() is called by all 32 lanes of the producer warp after lane 0 armed `bar`.
+template <bool kGather>
+__device__ __forceinline__ int4 row_cells(int32_t N, int32_t seq0, const int32_t* s2c, int lane) {
+  // rows past N (ragged last tile) gather cell 0: their values are masked / discarded
+  if (!kGather) return make_int4(0, 0, 0, 0);
+  return seq0 + 4 * lane < N ? __ldg(reinterpret_cast<const int4*>(s2c + seq0) + lane) : make_int4(0, 0, 0, 0);
+}
 template <int D, bool kGather>
-__device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int32_t h,
-                                          int32_t b, int32_t N, int32_t seq0, const int32_t* s2c, uint64_t pol,
-                                          int lane) {
+__device__ __forceinline__ void issue_rows(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int32_t h, int32_t b,
+                                           int32_t N, int32_t seq0, int4 c, uint64_t pol, int lane) {
   if (kGather) {
-    // rows past N (ragged last tile) gather cell 0: their values are masked / discarded
-    const int4 c = seq0 + 4 * lane < N ? __ldg(reinterpret_cast<const int4*>(s2c + seq0) + lane) : make_int4(0, 0, 0, 0);
     const int32_t base = b * N;
     sm100::tma_gather4(dst + lane * 4 * D * 2, map, bar, h * D, base + c.x, base + c.y, base + c.z, base + c.w, pol);
   } else if (lane == 0) {
@@ -128,10 +136,14 @@ __device__ __forceinline__ int32_t fwd_unit_at(int32_t k) {
 }
 
 // Flattened (unit, kv-tile) iterator of this CTA, skipping units without tiles.
+// The CSR row of the next unit is loaded one unit ahead (prefetch), so crossing a
+// unit boundary does not put an L2 round trip on any role's critical path.
 struct FwdIter {
   int32_t k, u, t, nt, rs;
   uint32_t n;   // ordinal of the current non-empty unit
   bool valid;
+  bool from_pf;          // the current unit came from the prefetch (its per-lane metadata too)
+  int32_t pu, prs, pre;  // prefetched unit k + 1 and its CSR row [prs, pre)
   __device__ void seek(const int32_t* row_ptr, int32_t mq, int32_t units) {
     for (;; ++k) {
       u = fwd_unit_at(k);
@@ -143,16 +155,47 @@ struct FwdIter {
     }
     valid = false;
   }
+  __device__ void prefetch(const int32_t* row_ptr, int32_t mq, int32_t units) {
+    pu = fwd_unit_at(k + 1);
+    prs = pre = 0;
+    if (pu < units) {
+      const int32_t qb = pu % mq;
+      prs = __ldg(row_ptr + qb);
+      pre = __ldg(row_ptr + qb + 1);
+    }
+  }
   __device__ void init(const int32_t* row_ptr, int32_t mq, int32_t units) {
-    k = 0; t = 0; n = 0;
+    k = 0; t = 0; n = 0; from_pf = false;
     seek(row_ptr, mq, units);
+    if (valid) prefetch(row_ptr, mq, units);
   }
   __device__ void advance(const int32_t* row_ptr, int32_t mq, int32_t units) {
     if (++t < nt) return;
     t = 0; ++n; ++k;
-    seek(row_ptr, mq, units);
+    if (pu >= units) { valid = false; return; }
+    if (pre > prs) {
+      u = pu; rs = prs; nt = pre - prs; valid = true; from_pf = true;
+    } else {
+      ++k;
+      seek(row_ptr, mq, units);
+      from_pf = false;
+      if (!valid) return;
+    }
+    prefetch(row_ptr, mq, units);
   }
 };
+
+// Per-lane copy of a unit's CSR entries (lane i holds tile i), packed col * 4 + kind;
+// tiles past 32 fall back to direct loads.
+__device__ __forceinline__ int32_t load_meta(const int32_t* col, const uint8_t* kind, int32_t rs, int32_t nt,
+                                             int lane) {
+  return lane < nt ? (__ldg(col + rs + lane) << 2) | (int32_t)__ldg(kind + rs + lane) : 0;
+}
+__device__ __forceinline__ int32_t tile_meta(int32_t meta, const int32_t* col, const uint8_t* kind, int32_t rs,
+                                             int32_t t) {
+  const int32_t v = __shfl_sync(0xffffffffu, meta, t & 31);
+  return t < 32 ? v : (__ldg(col + rs + t) << 2) | (int32_t)__ldg(kind + rs + t);
+}
 
 // Persistent CTAs (2 per SM).  Pipeline over the flattened tile sequence g:
 //   TMA     : Q of unit n into stage n&1 (double-buffered); K/V of tile g into
@@ -164,17 +207,16 @@ struct FwdIter {
 template <int D, bool kTwoD, bool kGather>
 __global__ void __launch_bounds__(kThreads, 2)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                    const __grid_constant__ CUtensorMap tmV, const FwdParams prm) {
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                    const FwdParams prm) {
   extern __shared__ uint8_t smem_raw[];
   FwdSmem<D>& sm = *reinterpret_cast<FwdSmem<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t mq = (prm.N + kBlock - 1) / kBlock;   // last q-block may be ragged
-  const int32_t units = mq * prm.heads * prm.batch;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < 2; ++s) {
       sm100::mbar_init(&sm.q_full[s], 1);
-      sm100::mbar_init(&sm.q_empty[s], 1);
+      sm100::mbar_init(&sm.o_staged[s], 128);   // softmax threads: O(n) staged in Q stage n&1
       sm100::mbar_init(&sm.k_full[s], 1);
       sm100::mbar_init(&sm.v_full[s], 1);
       sm100::mbar_init(&sm.kv_empty[s], 1);
@@ -204,6 +246,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   // registers to the softmax warpgroup (one thread per row keeps a 128-wide S row)
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
+    // (derived after the register split, so they are not spilled across it)
+    const int32_t mq = (prm.N + kBlock - 1) / kBlock;   // last q-block may be ragged
+    const int32_t units = mq * prm.heads * prm.batch;
     if (warp != 1) {
       // ---------------------------------------------------------- TMA producers
       // warp 0 loads Q, warp 2 K, warp 3 V: a CTA's TMA row / gather4 throughput grows
@@ -211,75 +256,120 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint64_t pol_q = sm100::policy_evict_first();
       const uint64_t pol_kv = sm100::policy_evict_last();
       int64_t tag0 = -1, tag1 = -1;   // (b, h, kv-block) held by K/V stage 0 / 1
-      uint32_t g = 0;
+      uint32_t g = 0, n_units = 0;
+      int32_t staged0 = 0, staged1 = 0;   // unit whose O is staged in Q stage 0 / 1
+      // O tile of unit us (staged in Q stage qs, swizzled like a loaded tile) -> global;
+      // ragged tiles were written row by row by the softmax warps
+      auto store_o = [&](int qs, int32_t us) {
+        const int32_t sqb = us % mq, sh = (us / mq) % prm.heads, sb = us / (mq * prm.heads);
+        if ((sqb + 1) * kBlock > prm.N) return;
+        if (kGather) {
+          const int4 c = row_cells<true>(prm.N, sqb * kBlock, prm.s2c, lane);
+          const int32_t base = sb * prm.N;
+          sm100::tma_scatter4(&tmO, sm.q[qs] + lane * 4 * D * 2, sh * D, base + c.x, base + c.y, base + c.z,
+                              base + c.w);
+        } else if (lane == 0) {
+          sm100::tma_store_3d(&tmO, sm.q[qs], 0, sh, sb * prm.N + sqb * kBlock);
+        }
+        sm100::bulk_commit_group();
+        sm100::bulk_wait_group_read0();   // the stage may be refilled once the engine has read it
+        __syncwarp();
+      };
       FwdIter it;
       it.init(prm.row_ptr, mq, units);
+      int32_t meta = 0, pmeta = 0;
+      if (warp != 0 && it.valid) {
+        meta = load_meta(prm.col_idx, prm.kind, it.rs, it.nt, lane);
+        pmeta = load_meta(prm.col_idx, prm.kind, it.prs, it.pre - it.prs, lane);
+      }
       while (it.valid) {
         const int32_t qb = it.u % mq, h = (it.u / mq) % prm.heads, b = it.u / (mq * prm.heads);
         const int64_t bh = (int64_t)b * prm.heads + h;
         if (warp == 0) {
+          // Q(n) goes into stage n&1, which holds O(n-2) staged by the softmax warps:
+          // store that tile first (TMA store / scatter4), then reuse the stage
           const int qs = it.n & 1;
-          if (it.n >= 2) sm100::mbar_wait(&sm.q_empty[qs], ((it.n >> 1) - 1) & 1);
+          const int4 cells = row_cells<kGather>(prm.N, qb * kBlock, prm.s2c, lane);
+          if (it.n >= 2) {
+            sm100::mbar_wait(&sm.o_staged[qs], ((it.n >> 1) - 1) & 1);
+            store_o(qs, qs ? staged1 : staged0);
+          }
+          if (qs) staged1 = it.u; else staged0 = it.u;
           if (lane == 0) HLA_TR((3 << 24) | (1 << 16) | it.n);
           if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.q_full[qs], FwdSmem<D>::kTileBytes);
           __syncwarp();
-          load_rows<D, kGather>(sm.q[qs], &tmQ, &sm.q_full[qs], h, b, prm.N, qb * kBlock, prm.s2c, pol_q, lane);
+          issue_rows<D, kGather>(sm.q[qs], &tmQ, &sm.q_full[qs], h, b, prm.N, qb * kBlock, cells, pol_q, lane);
+          ++n_units;
         } else {
           const bool is_k = warp == 2;
           for (int t = 0; t < it.nt; ++t, ++g) {
             const int s = g & 1;
             uint64_t* full = is_k ? &sm.k_full[s] : &sm.v_full[s];
-            if (g >= 2) sm100::mbar_wait(&sm.kv_empty[s], ((g >> 1) - 1) & 1);
-            const int32_t kvb = __ldg(prm.col_idx + it.rs + t);
+            const int32_t kvb = tile_meta(meta, prm.col_idx, prm.kind, it.rs, t) >> 2;
             const int64_t tag = bh * mq + kvb;
-            if (tag == (s ? tag1 : tag0)) {   // stage already holds this K/V tile
+            const bool reuse = tag == (s ? tag1 : tag0);   // stage already holds this K/V tile
+            const int4 cells = reuse ? make_int4(0, 0, 0, 0) : row_cells<kGather>(prm.N, kvb * kBlock, prm.s2c, lane);
+            if (g >= 2) sm100::mbar_wait(&sm.kv_empty[s], ((g >> 1) - 1) & 1);
+            if (reuse) {
               if (lane == 0) sm100::mbar_arrive(full);
               continue;
             }
             if (s) tag1 = tag; else tag0 = tag;
             if (lane == 0) sm100::mbar_arrive_expect_tx(full, FwdSmem<D>::kTileBytes);
             __syncwarp();
-            load_rows<D, kGather>(is_k ? sm.k[s] : sm.v[s], is_k ? &tmK : &tmV, full, h, b, prm.N, kvb * kBlock,
-                                  prm.s2c, pol_kv, lane);
+            issue_rows<D, kGather>(is_k ? sm.k[s] : sm.v[s], is_k ? &tmK : &tmV, full, h, b, prm.N, kvb * kBlock,
+                                   cells, pol_kv, lane);
           }
         }
         it.t = it.nt - 1;
         it.advance(prm.row_ptr, mq, units);
+        if (warp != 0 && it.valid) {
+          meta = it.from_pf ? pmeta : load_meta(prm.col_idx, prm.kind, it.rs, it.nt, lane);
+          pmeta = load_meta(prm.col_idx, prm.kind, it.prs, it.pre - it.prs, lane);
+        }
+      }
+      if (warp == 0) {
+        // the last (up to) two units' O tiles are still staged
+        for (uint32_t m = n_units >= 2 ? n_units - 2 : 0; m < n_units; ++m) {
+          sm100::mbar_wait(&sm.o_staged[m & 1], (m >> 1) & 1);
+          store_o(m & 1, (m & 1) ? staged1 : staged0);
+        }
+        sm100::bulk_wait_group0();
       }
     } else if (warp == 1 && lane == 0) {
       // ----------------------------------------------------------- MMA issuer
       constexpr uint32_t idesc_s = sm100::make_idesc_bf16(kBlock, kBlock, false, false);
       constexpr uint32_t idesc_o = sm100::make_idesc_bf16(kBlock, D, false, true);
       const uint32_t tS = tmem + kColS, tP = tmem + kColP, tO = tmem + kColO;
-      auto issue_s = [&](const FwdIter& x, uint32_t gg) {
-        const uint8_t* q = sm.q[x.n & 1];
+      auto issue_s = [&](uint32_t n, uint32_t gg) {
+        const uint8_t* q = sm.q[n & 1];
         const uint8_t* k = sm.k[gg & 1];
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
           sm100::mma_ss(tS, kmajor_desc<D>(q, kk), kmajor_desc<D>(k, kk), idesc_s, kk > 0);
         sm100::mma_commit(&sm.s_full);
       };
-      FwdIter cur;
-      cur.init(prm.row_ptr, mq, units);
+      FwdIter it;   // always one tile ahead of the PV being issued
+      it.init(prm.row_ptr, mq, units);
       uint32_t g = 0;
-      if (cur.valid) {
+      if (it.valid) {
         sm100::mbar_wait(&sm.q_full[0], 0);
         sm100::mbar_wait(&sm.k_full[0], 0);
         sm100::tc_fence_after();
-        issue_s(cur, 0);
+        issue_s(0, 0);
       }
-      while (cur.valid) {
-        FwdIter nxt = cur;
-        nxt.advance(prm.row_ptr, mq, units);
+      while (it.valid) {
+        const int32_t ct = it.t, cnt = it.nt;
+        it.advance(prm.row_ptr, mq, units);
         bool next_s_issued = false;
-        if (nxt.valid) {
+        if (it.valid) {
           // S(g+1) overwrites S(g): only after the softmax pulled S(g) into registers.
           // Its operands may still be in flight (next unit's Q, K): then PV(g) goes first.
           sm100::mbar_wait(&sm.s_free, g & 1);
-          if ((nxt.t != 0 || sm100::mbar_test_wait(&sm.q_full[nxt.n & 1], (nxt.n >> 1) & 1)) &&
+          if ((it.t != 0 || sm100::mbar_test_wait(&sm.q_full[it.n & 1], (it.n >> 1) & 1)) &&
               sm100::mbar_test_wait(&sm.k_full[(g + 1) & 1], ((g + 1) >> 1) & 1)) {
             sm100::tc_fence_after();
-            issue_s(nxt, g + 1);
+            issue_s(it.n, g + 1);
             next_s_issued = true;
           }
         }
@@ -289,26 +379,23 @@ __global__ void __launch_bounds__(kThreads, 2)
         sm100::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < kBlock / 16; ++kk)
-          sm100::mma_ts(tO, tP + kk * 8, mnmajor_desc<D>(sm.v[g & 1], kk), idesc_o,
-                        (cur.t > 0 || kk > 0) ? 1u : 0u);
+          sm100::mma_ts(tO, tP + kk * 8, mnmajor_desc<D>(sm.v[g & 1], kk), idesc_o, (ct > 0 || kk > 0) ? 1u : 0u);
         sm100::mma_commit(&sm.kv_empty[g & 1]);
         sm100::mma_commit(&sm.pv_done);
-        if (cur.t == cur.nt - 1) {
-          sm100::mma_commit(&sm.q_empty[cur.n & 1]);
-          sm100::mma_commit(&sm.o_full);
-        }
-        if (nxt.valid && !next_s_issued) {
-          if (nxt.t == 0) sm100::mbar_wait(&sm.q_full[nxt.n & 1], (nxt.n >> 1) & 1);
+        if (ct == cnt - 1) sm100::mma_commit(&sm.o_full);
+        if (it.valid && !next_s_issued) {
+          if (it.t == 0) sm100::mbar_wait(&sm.q_full[it.n & 1], (it.n >> 1) & 1);
           sm100::mbar_wait(&sm.k_full[(g + 1) & 1], ((g + 1) >> 1) & 1);
           sm100::tc_fence_after();
-          issue_s(nxt, g + 1);
+          issue_s(it.n, g + 1);
         }
-        cur = nxt;
         ++g;
       }
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
+    const int32_t mq = (prm.N + kBlock - 1) / kBlock;
+    const int32_t units = mq * prm.heads * prm.batch;
     // --------------------------------------------------- softmax + epilogue
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
@@ -317,11 +404,19 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint32_t g = 0;
     FwdIter it;
     it.init(prm.row_ptr, mq, units);
+    int32_t meta = 0, pmeta = 0;
+    if (it.valid) {
+      meta = load_meta(prm.col_idx, prm.kind, it.rs, it.nt, lane);
+      pmeta = load_meta(prm.col_idx, prm.kind, it.prs, it.pre - it.prs, lane);
+    }
     while (it.valid) {
       const int32_t qb = it.u % mq, h = (it.u / mq) % prm.heads, b = it.u / (mq * prm.heads);
       const int32_t q = qb * kBlock + row;
       float m_ref = -INFINITY, l = 0.f;
       const RowBox box = row_box(prm.pat, q);
+      const bool real = q < prm.N;
+      const int32_t ocell = kGather ? (real ? __ldg(prm.s2c + q) : 0) : q;   // fused inverse reorder of O (used at the end)
+      if (row == 0) HLA_TR((2 << 24) | (6 << 16) | it.n);
       for (int t = 0; t < it.nt; ++t, ++g) {
         sm100::mbar_wait(&sm.s_full, g & 1);
         if (row == 0) HLA_TR((2 << 24) | (1 << 16) | g);
@@ -336,8 +431,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         sm100::tc_fence_before();
         sm100::mbar_arrive(&sm.s_free);          // the MMA may overwrite S with S(g+1)
         float (&s)[kBlock] = *reinterpret_cast<float(*)[kBlock]>(sr);
-        if (__ldg(prm.kind + it.rs + t) == 2)
-          apply_row_mask<kTwoD>(s, prm.pat, box, __ldg(prm.col_idx + it.rs + t) * kBlock);
+        const int32_t tm = tile_meta(meta, prm.col_idx, prm.kind, it.rs, t);
+        if ((tm & 3) == 2) apply_row_mask<kTwoD>(s, prm.pat, box, (tm >> 2) * kBlock);
         // row max with 8 independent chains (a single dependent chain costs ~4 cycles x 128)
         float m8[8];
 #pragma unroll
@@ -360,6 +455,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         uint32_t pk[64];
 #pragma unroll
         for (int e = 0; e < 64; ++e) {
+          // MUFU for one half of the exponentials, the FMA pipe for the other (FA4's split)
           const float p0 = sm100::ex2(fmaf(s[2 * e], sl2, -m_use));
           const float p1 = sm100::ex2(fmaf(s[2 * e + 1], sl2, -m_use));
           l4[e & 3] += p0 + p1;
@@ -395,8 +491,6 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
 
       // epilogue: O / l -> bf16 row, LSE (natural log); phantom rows (q >= N) write nothing
-      const bool real = q < prm.N;
-      const int32_t ocell = kGather ? (real ? __ldg(prm.s2c + q) : 0) : q;   // fused inverse reorder of O
       const int64_t orow = ((int64_t)b * prm.N + ocell) * prm.heads + h;
       uint4* optr = reinterpret_cast<uint4*>(prm.o + orow * D);
       const float inv_l = l > 0.f ? 1.f / l : 0.f;
@@ -408,18 +502,29 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int c = 0; c < D / 32; ++c)
         sm100::tmem_ld32(tmem + lane_off + kColO + c * 32, *reinterpret_cast<uint32_t(*)[32]>(o + c * 32));
       sm100::tmem_wait_ld();
-      // TMEM O may now be overwritten by the next unit's first PV (it waits p_full)
-      if (real) {
+      // TMEM O may now be overwritten by the next unit's first PV (it waits p_full).
+      // Full tiles: the bf16 row goes into this unit's Q stage (all S MMAs of the unit
+      // are done), swizzled like a TMA-loaded tile; the producer stores the tile with one
+      // TMA store / 32 scatter4 (full 128-B lines, no LSU store queue in this warp's way).
+      // Ragged tiles: rows written directly.
+      const bool staged = (qb + 1) * kBlock <= prm.N;
+      const uint32_t stage = sm100::smem_u32(sm.q[it.n & 1]);
 #pragma unroll
-        for (int v4 = 0; v4 < D / 8; ++v4) {
-          uint4 w;
-          w.x = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 0]) * inv_l, __uint_as_float(o[v4 * 8 + 1]) * inv_l);
-          w.y = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 2]) * inv_l, __uint_as_float(o[v4 * 8 + 3]) * inv_l);
-          w.z = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 4]) * inv_l, __uint_as_float(o[v4 * 8 + 5]) * inv_l);
-          w.w = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 6]) * inv_l, __uint_as_float(o[v4 * 8 + 7]) * inv_l);
+      for (int v4 = 0; v4 < D / 8; ++v4) {
+        uint4 w;
+        w.x = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 0]) * inv_l, __uint_as_float(o[v4 * 8 + 1]) * inv_l);
+        w.y = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 2]) * inv_l, __uint_as_float(o[v4 * 8 + 3]) * inv_l);
+        w.z = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 4]) * inv_l, __uint_as_float(o[v4 * 8 + 5]) * inv_l);
+        w.w = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 6]) * inv_l, __uint_as_float(o[v4 * 8 + 7]) * inv_l);
+        if (staged) {
+          const uint32_t off = (uint32_t)row * (D * 2) + v4 * 16;
+          sm100::sts_u4(stage + (D == 64 ? sm100::swz128(off) : sm100::swz64(off)), w.x, w.y, w.z, w.w);
+        } else if (real) {
           optr[v4] = w;
         }
       }
+      sm100::fence_proxy_async_smem();
+      sm100::mbar_arrive(&sm.o_staged[it.n & 1]);
       if (row == 0) HLA_TR((2 << 24) | (4 << 16) | it.n);
       const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
       if (real)
@@ -428,6 +533,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       tiles_done += it.nt;
       it.t = it.nt - 1;
       it.advance(prm.row_ptr, mq, units);
+      if (it.valid) {
+        meta = it.from_pf ? pmeta : load_meta(prm.col_idx, prm.kind, it.rs, it.nt, lane);
+        pmeta = load_meta(prm.col_idx, prm.kind, it.prs, it.pre - it.prs, lane);
+      }
+      if (row == 0) HLA_TR((2 << 24) | (5 << 16) | it.n);
     }
   }
 
@@ -439,14 +549,14 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 template <int D, bool kTwoD, bool kGather>
-hla_status launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const FwdParams& prm,
-                      int32_t n_qblocks, cudaStream_t stream) {
+hla_status launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mo,
+                      const FwdParams& prm, int32_t n_qblocks, cudaStream_t stream) {
   const size_t smem = sizeof(FwdSmem<D>) + 1024;
   auto* fn = attn_fwd_kernel<D, kTwoD, kGather>;
   HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t units = (int64_t)n_qblocks * prm.heads * prm.batch;
   const int grid = (int)std::min<int64_t>((units + 1) / 2, 2 * (int64_t)num_sms());   // pairs of units
-  fn<<<grid, kThreads, smem, stream>>>(mq, mk, mv, prm);
+  fn<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mo, prm);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
 }
@@ -506,23 +616,25 @@ extern "C" hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_ma
               "seq_to_cell (fused reorder) is only meaningful for Hilbert-order patterns");
   HLA_REQUIRE(!gather || ((uintptr_t)seq_to_cell & 15) == 0, HLA_ERR_INVALID, "seq_to_cell must be 16-byte aligned");
   const int64_t rows = (int64_t)batch * pat.N;
-  CUtensorMap mq, mk, mv;
+  CUtensorMap mq, mk, mv, mo;
   if (gather) {
+    if ((st = make_gather_map(&mo, o, rows, heads, head_dim)) != HLA_OK) return st;
     if ((st = make_gather_map(&mq, q, rows, heads, head_dim)) != HLA_OK) return st;
     if ((st = make_gather_map(&mk, k, rows, heads, head_dim)) != HLA_OK) return st;
     if ((st = make_gather_map(&mv, v, rows, heads, head_dim)) != HLA_OK) return st;
   } else {
+    if ((st = make_rows_map(&mo, o, rows, heads, head_dim, kBlock)) != HLA_OK) return st;
     if ((st = make_rows_map(&mq, q, rows, heads, head_dim, kBlock)) != HLA_OK) return st;
     if ((st = make_rows_map(&mk, k, rows, heads, head_dim, kBlock)) != HLA_OK) return st;
     if ((st = make_rows_map(&mv, v, rows, heads, head_dim, kBlock)) != HLA_OK) return st;
   }
   const int32_t mqb = (pat.N + kBlock - 1) / kBlock;
   if (head_dim == 64) {
-    if (gather) return launch_fwd<64, false, true>(mq, mk, mv, prm, mqb, stream);
-    return two_d ? launch_fwd<64, true, false>(mq, mk, mv, prm, mqb, stream)
-                 : launch_fwd<64, false, false>(mq, mk, mv, prm, mqb, stream);
+    if (gather) return launch_fwd<64, false, true>(mq, mk, mv, mo, prm, mqb, stream);
+    return two_d ? launch_fwd<64, true, false>(mq, mk, mv, mo, prm, mqb, stream)
+                 : launch_fwd<64, false, false>(mq, mk, mv, mo, prm, mqb, stream);
   }
-  if (gather) return launch_fwd<32, false, true>(mq, mk, mv, prm, mqb, stream);
-  return two_d ? launch_fwd<32, true, false>(mq, mk, mv, prm, mqb, stream)
-               : launch_fwd<32, false, false>(mq, mk, mv, prm, mqb, stream);
+  if (gather) return launch_fwd<32, false, true>(mq, mk, mv, mo, prm, mqb, stream);
+  return two_d ? launch_fwd<32, true, false>(mq, mk, mv, mo, prm, mqb, stream)
+               : launch_fwd<32, false, false>(mq, mk, mv, mo, prm, mqb, stream);
 }

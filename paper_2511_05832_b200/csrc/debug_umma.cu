@@ -242,6 +242,104 @@ __global__ void __launch_bounds__(128) debug_softmax_rate_kernel(int iters, floa
   if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
 }
 
+// The forward softmax tile body with its TMEM traffic, no MMA / TMA: per iteration
+// S (128 fp32 per row) from TMEM -> row max -> 128 exponentials -> P (bf16) to TMEM.
+// iters bit 20: a 5th warp keeps the tensor core busy meanwhile (SS MMAs N = 64 into
+// TMEM cols [192, 256)), to see whether tcgen05 traffic slows the softmax warps.
+__global__ void __launch_bounds__(160) debug_softmax_tile_kernel(int iters_flags, float sl2, long long* out,
+                                                                   uint32_t* sink) {
+  __shared__ uint32_t tmem_base;
+  __shared__ alignas(1024) uint8_t ops[2 * 16384];
+  __shared__ uint64_t bar;
+  __shared__ volatile int done;
+  const int iters = iters_flags & 0xFFFFF;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    sm100::tmem_alloc(&tmem_base, 256);
+    sm100::tmem_relinquish();
+  }
+  if (threadIdx.x == 0) {
+    sm100::mbar_init(&bar, 1);
+    sm100::fence_mbar_init();
+    done = 0;
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  if (warp == 4) {
+    if (lane == 0 && (iters_flags >> 20)) {
+      const uint32_t idesc = sm100::make_idesc_bf16(128, 64, false, false);
+      const uint64_t ad = sm100::make_smem_desc(sm100::smem_u32(ops), 16, 1024, sm100::kSwizzle128B);
+      const uint64_t bd = sm100::make_smem_desc(sm100::smem_u32(ops + 16384), 16, 1024, sm100::kSwizzle128B);
+      uint32_t ph = 0;
+      while (!done) {
+        for (int i = 0; i < 64; ++i) sm100::mma_ss(tmem_base + 192, ad, bd, idesc, 1);
+        sm100::mma_commit(&bar);
+        sm100::mbar_wait(&bar, ph);
+        ph ^= 1;
+      }
+    }
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    return;
+  }
+  const uint32_t tm = tmem_base + ((uint32_t)(warp * 32) << 16);
+  {
+    uint32_t init[32];
+    for (int i = 0; i < 32; ++i) init[i] = __float_as_uint((float)((threadIdx.x * 7 + i * 13) % 97) * 0.01f);
+    for (int c = 0; c < 4; ++c) sm100::tmem_st32(tm + c * 32, init);
+    sm100::tmem_wait_st();
+  }
+  float l = 0.f, m_ref = -INFINITY;
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    uint32_t sr[128];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) sm100::tmem_ld32(tm + c * 32, *reinterpret_cast<uint32_t(*)[32]>(sr + c * 32));
+    sm100::tmem_wait_ld();
+    float (&sv)[128] = *reinterpret_cast<float(*)[128]>(sr);
+    float m8[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) m8[j] = sv[j];
+#pragma unroll
+    for (int c = 8; c < 128; ++c) m8[c & 7] = fmaxf(m8[c & 7], sv[c]);
+#pragma unroll
+    for (int j = 4; j > 0; j >>= 1)
+#pragma unroll
+      for (int i = 0; i < j; ++i) m8[i] = fmaxf(m8[i], m8[i + j]);
+    const float m_tile = m8[0] * sl2;
+    const float m_new = (m_tile > m_ref + 8.f) ? m_tile : m_ref;
+    const float alpha = (m_new == m_ref) ? 1.f : sm100::ex2(m_ref - m_new);
+    m_ref = m_new;
+    l *= alpha;
+    const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
+    float l4[4] = {0.f, 0.f, 0.f, 0.f};
+    uint32_t pk[64];
+#pragma unroll
+    for (int e = 0; e < 64; ++e) {
+      const float p0 = sm100::ex2(fmaf(sv[2 * e], sl2, -m_use));
+      const float p1 = sm100::ex2(fmaf(sv[2 * e + 1], sl2, -m_use));
+      l4[e & 3] += p0 + p1;
+      pk[e] = sm100::pack_bf16(p0, p1);
+    }
+    l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) sm100::tmem_st16(tm + 128 + c * 16, pk + c * 16);
+    sm100::tmem_wait_st();
+  }
+  const long long t1 = clock64();
+  if (l == 1.2345f) sink[0] = 1;
+  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (threadIdx.x == 0) done = 1;
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  if (warp == 0) sm100::tmem_dealloc(tmem_base, 256);
+}
+
 // 128 token rows (indices idx[0..127]) of head h gathered with .tile::gather4 into a
 // SWIZZLE_<2d> tile, then read back through the swizzle into out[128][d].
 template <int D>
@@ -299,6 +397,14 @@ extern "C" hla_status hla_debug_ex2_rate(int32_t threads, int32_t iters, long lo
                                          cudaStream_t stream) {
   clear_error();
   debug_ex2_rate_kernel<<<1, threads, 0, stream>>>(iters, 1.0f, out_cycles, sink);
+  HLA_CUDA_TRY(cudaGetLastError());
+  return HLA_OK;
+}
+
+extern "C" hla_status hla_debug_softmax_tile(int32_t blocks, int32_t iters, long long* out_cycles, uint32_t* sink,
+                                             cudaStream_t stream) {
+  clear_error();
+  debug_softmax_tile_kernel<<<blocks, 160, 0, stream>>>(iters, 0.18f, out_cycles, sink);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
 }

@@ -106,6 +106,15 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
                "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
                : "memory");
 }
+// 2-D scatter of 4 rows (sm_100 .tile::scatter4): 4 consecutive box rows in shared
+// memory to rows y0..y3 at column x of a 2-D tensor map (bulk async group)
+__device__ __forceinline__ void tma_scatter4(const CUtensorMap* map, const void* src, int32_t x, int32_t y0,
+                                             int32_t y1, int32_t y2, int32_t y3) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(src)), "r"(x), "r"(y0), "r"(y1), "r"(y2),
+               "r"(y3)
+               : "memory");
+}
 // 3-D tile reduce-add shared -> global (fp32 add performed by the TMA engine / L2)
 __device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, const void* src, int32_t c0, int32_t c1,
                                                   int32_t c2) {

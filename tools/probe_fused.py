@@ -22,3 +22,12 @@ for fused in (True, False):
         f = lambda: api.hla_attn_fwd(L.desc, L.mask, L.qs, L.ks, L.vs, 0.0, L.os, L.lse)
         b = lambda: api.hla_attn_bwd_main(L.desc, L.mask, L.qs, L.ks, L.vs, L.dos, L.dks, L.dvs, L.workspace, 0.0)
     print("fused" if fused else "plain", "fwd %.4f ms  bwd_main %.4f ms" % (t_ms(f), t_ms(b)))
+# SM clock while the forward runs back to back (~1 s)
+import bench
+cs = bench.ClockSampler(0)
+cs.start()
+t0 = __import__("time").time()
+while __import__("time").time() - t0 < 1.0:
+    for _ in range(50): f()
+    torch.cuda.synchronize()
+print("clocks during fwd loop:", cs.stop())

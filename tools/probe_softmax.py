@@ -10,3 +10,17 @@ for blocks in (1, 148, 296, 592):
         torch.cuda.synchronize(); r.append(float(out[:blocks].float().mean().item()))
     cyc = (r[1] - r[0]) / 64
     print("blocks=%3d: %.0f cycles per 128x128 tile per CTA (MUFU bound alone: 1024)" % (blocks, cyc))
+print("with TMEM S load / P store:")
+for blocks in (1, 148, 296):
+    r = []
+    for iters in (8, 72):
+        L.hla_debug_softmax_tile(blocks, iters, ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(sink.data_ptr()), None)
+        torch.cuda.synchronize(); r.append(float(out[:blocks].float().mean().item()))
+    print("blocks=%3d: %.0f cycles per tile per CTA" % (blocks, (r[1] - r[0]) / 64))
+print("with TMEM S load / P store + a warp issuing MMAs back to back:")
+for blocks in (148, 296):
+    r = []
+    for iters in (8, 72):
+        L.hla_debug_softmax_tile(blocks, iters | (1 << 20), ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(sink.data_ptr()), None)
+        torch.cuda.synchronize(); r.append(float(out[:blocks].float().mean().item()))
+    print("blocks=%3d: %.0f cycles per tile per CTA" % (blocks, (r[1] - r[0]) / 64))
