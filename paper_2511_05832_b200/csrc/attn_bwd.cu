@@ -585,17 +585,18 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
                                                              float* __restrict__ dsum, float* __restrict__ lse2,
                                                              float* __restrict__ dq_acc,
                                                              const int32_t* __restrict__ s2c, int32_t N,
-                                                             int32_t heads, int64_t rows) {
-  constexpr int kLanes = D / 8;   // lanes per row, 16 B (8 bf16) each
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t r = gid / kLanes;             // sequence-order row (b * N + s) * heads + h
-  const int part = (int)(gid % kLanes);
+                                                             int32_t heads, int32_t rows) {
+  // one thread per 8 elements (16 B of O and of dO); 32-bit index math (rows * D / 8 < 2^31)
+  constexpr int kLanes = D / 8;   // lanes per row
+  const int32_t gid = (int32_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int32_t r = gid / kLanes;             // sequence-order row (b * N + s) * heads + h
+  const int part = gid - r * kLanes;
   if (r >= rows) return;
-  const int64_t hq = r % heads, bs = r / heads;
-  const int64_t s = bs % N, bb = bs / N;
-  const int64_t src = s2c ? ((bb * N + __ldg(s2c + s)) * heads + hq) : r;
-  const uint4 a = *reinterpret_cast<const uint4*>(o + src * D + part * 8);
-  const uint4 g = *reinterpret_cast<const uint4*>(dout + src * D + part * 8);
+  const int32_t bs = r / heads, hq = r - bs * heads;
+  const int32_t bb = bs / N, s = bs - bb * N;
+  const int64_t src = s2c ? ((int64_t)(bb * N + __ldg(s2c + s)) * heads + hq) : (int64_t)r;
+  const uint4 a = __ldg(reinterpret_cast<const uint4*>(o + src * D + part * 8));
+  const uint4 g = __ldg(reinterpret_cast<const uint4*>(dout + src * D + part * 8));
   const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
   const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&g);
   float acc = 0.f;
@@ -607,11 +608,11 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
   }
 #pragma unroll
   for (int o2 = kLanes / 2; o2 > 0; o2 >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o2);
-  float4* z = reinterpret_cast<float4*>(dq_acc + r * D + part * 8);   // zeroing is layout-agnostic
+  float4* z = reinterpret_cast<float4*>(dq_acc + (int64_t)r * D + part * 8);   // zeroing is layout-agnostic
   z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
   z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
   if (part == 0) {
-    const int64_t i = (bb * heads + hq) * N + s;
+    const int64_t i = (int64_t)(bb * heads + hq) * N + s;
     dsum[i] = acc * scale;                       // D * scale (dS = P o (dP * scale - D * scale))
     lse2[i] = __ldg(lse + i) * kLog2e;           // LSE in the log2 domain
   }
@@ -619,20 +620,21 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
 
 // K9: dQ = bf16(accumulator) -- the accumulator is in sequence order; under the
 // fused reorder each row is written to its grid cell s2c[s] (SURVEY 8(a) a8:
-// "dQ finalize + inverse permutation").
-__global__ void __launch_bounds__(256) dq_finalize_kernel(const float4* __restrict__ acc, uint2* __restrict__ dq,
+// "dQ finalize + inverse permutation").  One thread per 8 elements (32 B in, 16 B out).
+__global__ void __launch_bounds__(256) dq_finalize_kernel(const float4* __restrict__ acc, uint4* __restrict__ dq,
                                                           const int32_t* __restrict__ s2c, int32_t N,
-                                                          int32_t row_f4, int64_t n4) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-    const float4 v = acc[i];
-    int64_t o = i;
-    if (s2c) {   // i = ((b * N + s) * row_f4 + part) with row_f4 = heads * D / 4
-      const int64_t part = i % row_f4, bs = i / row_f4;
-      const int64_t s = bs % N, b = bs / N;
-      o = (b * N + __ldg(s2c + s)) * row_f4 + part;
-    }
-    dq[o] = make_uint2(sm100::pack_bf16(v.x, v.y), sm100::pack_bf16(v.z, v.w));
+                                                          int32_t row_v, int32_t n_v) {
+  const int32_t t = (int32_t)blockIdx.x * blockDim.x + threadIdx.x;   // n_v = B * N * row_v < 2^31
+  if (t >= n_v) return;
+  const float4 v0 = __ldcs(acc + 2 * (int64_t)t), v1 = __ldcs(acc + 2 * (int64_t)t + 1);
+  int64_t o = t;
+  if (s2c) {   // t = (b * N + s) * row_v + part, row_v = heads * D / 8
+    const int32_t bs = t / row_v, part = t - bs * row_v;
+    const int32_t b = bs / N, s = bs - b * N;
+    o = (int64_t)(b * N + __ldg(s2c + s)) * row_v + part;
   }
+  dq[o] = make_uint4(sm100::pack_bf16(v0.x, v0.y), sm100::pack_bf16(v0.z, v0.w), sm100::pack_bf16(v1.x, v1.y),
+                     sm100::pack_bf16(v1.z, v1.w));
 }
 
 template <int D, bool kTwoD, bool kGather>
@@ -693,15 +695,16 @@ extern "C" hla_status hla_attn_bwd_preprocess(int32_t batch, int32_t heads, int3
   const float sc = scale > 0.f ? scale : 1.0f / sqrtf((float)head_dim);
   const int64_t rows = (int64_t)batch * n * heads;
   const int64_t threads = rows * (head_dim / 8);
+  HLA_REQUIRE(threads < (1ll << 31), HLA_ERR_UNSUPPORTED, "B * N * heads * head_dim too large");
   const unsigned blocks = (unsigned)((threads + 255) / 256);
   if (head_dim == 64)
     bwd_preprocess_kernel<64><<<blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
                                                           reinterpret_cast<const __nv_bfloat16*>(dout), lse, sc,
-                                                          dsum, lse2, dq_acc, seq_to_cell, n, heads, rows);
+                                                          dsum, lse2, dq_acc, seq_to_cell, n, heads, (int32_t)rows);
   else
     bwd_preprocess_kernel<32><<<blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
                                                           reinterpret_cast<const __nv_bfloat16*>(dout), lse, sc,
-                                                          dsum, lse2, dq_acc, seq_to_cell, n, heads, rows);
+                                                          dsum, lse2, dq_acc, seq_to_cell, n, heads, (int32_t)rows);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
 }
@@ -777,11 +780,12 @@ extern "C" hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_
   hla_status st = carve_workspace(batch, heads, n, head_dim, const_cast<void*>(workspace), workspace_bytes, &dq_acc,
                                   &dsum);
   if (st != HLA_OK) return st;
-  const int64_t n4 = (int64_t)batch * n * heads * head_dim / 4;
-  const unsigned blocks = (unsigned)std::min<int64_t>((n4 + 255) / 256, 148 * 16);
+  const int64_t n_v = (int64_t)batch * n * heads * head_dim / 8;
+  HLA_REQUIRE(n_v < (1ll << 31), HLA_ERR_UNSUPPORTED, "B * N * heads * head_dim too large");
+  const unsigned blocks = (unsigned)((n_v + 255) / 256);
   dq_finalize_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const float4*>(dq_acc),
-                                                 reinterpret_cast<uint2*>(dq), seq_to_cell, n,
-                                                 heads * head_dim / 4, n4);
+                                                 reinterpret_cast<uint4*>(dq), seq_to_cell, n,
+                                                 heads * head_dim / 8, (int32_t)n_v);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
 }
