@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = 0; t < nt; ++t, ++g) {
           const int s = g & 1;
           if (g >= 2) sm100::mbar_wait(&sm.q_empty[s], ((g >> 1) - 1) & 1);
-          if (lane == 0 && role == 0) HLA_TR((3 << 24) | ((2) << 16) | (g));
+          if (lane == 0 && role == 1) HLA_TR((7 << 24) | ((2) << 16) | (g));
           const int32_t qblk = __ldg(prm.t_col_idx + rs + t);
           const int64_t tag = bh * prm.N + qblk;     // (b, h, q-block) held by the stage
           if (tag == (s ? stage_tag1 : stage_tag0)) {
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           sm100::mma_ss(tDK, ds_kmajor_desc(ds, kk), mnmajor_desc<D>(sm.q[s], kk), idesc_kv, acc);
         }
       };
-#ifdef HLA_TRACE
+#if defined(HLA_TRACE) && defined(HLA_TRACE_MMA)
       uint32_t dbg_phase = 0;
       // trace builds: serialise after each MMA group and record its tensor-core time
       auto mma_probe = [&](int ev, uint32_t gg) {
@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint4* dvp = reinterpret_cast<uint4*>(prm.dv + grow * D);
       if (nt > 0) {
         sm100::mbar_wait(&sm.dkv_full, n & 1);
-        if (leader) HLA_TR((2 << 24) | ((6) << 16) | (n));
+        if (leader) HLA_TR((4 << 24) | ((6) << 16) | (n));
         sm100::tc_fence_after();
         // dV then dK, each packed to bf16 right away (64 live registers, not 128)
         uint32_t pv[D / 2], pk[D / 2];
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           dvp[v4] = make_uint4(pv[v4 * 4 + 0], pv[v4 * 4 + 1], pv[v4 * 4 + 2], pv[v4 * 4 + 3]);
           dkp[v4] = make_uint4(pk[v4 * 4 + 0], pk[v4 * 4 + 1], pk[v4 * 4 + 2], pk[v4 * 4 + 3]);
         }
-        if (leader) HLA_TR((2 << 24) | ((7) << 16) | (n));
+        if (leader) HLA_TR((4 << 24) | ((7) << 16) | (n));
         ++n;
       } else {
 #pragma unroll

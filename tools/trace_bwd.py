@@ -28,7 +28,7 @@ torch.cuda.synchronize()
 n = lib.hla_debug_trace_dump(buf, 8192)
 ev = sorted((buf[2 * i + 1], buf[2 * i]) for i in range(n) if buf[2 * i + 1])
 t0 = ev[0][0]
-names = {1: "MMA", 2: "CMP", 3: "TMA", 4: "DQW", 5: "TC ", 6: "SM1"}
+names = {1: "MMA", 2: "CMP", 3: "TMA", 4: "DQW", 5: "TC ", 6: "SM1", 7: "TMQ"}
 for t, tag in ev[:400]:
     role, e, gg = tag >> 24, (tag >> 16) & 0xFF, tag & 0xFFFF
     print("%8d  %s ev%d g%d" % (t - t0, names.get(role, role), e, gg))
