@@ -425,6 +425,7 @@ extern "C" hla_status hla_debug_softmax_rate(int32_t blocks, int32_t iters, long
 constexpr int kLoadStagesMax = 8;
 
 __global__ void debug_load_kernel(const __grid_constant__ CUtensorMap m3, const __grid_constant__ CUtensorMap mg,
+                                  const __grid_constant__ CUtensorMap m3b, const __grid_constant__ CUtensorMap mgb,
                                   const __nv_bfloat16* src, int64_t rows, int32_t heads, int32_t mode,
                                   int32_t stages, int32_t tiles, long long* out_cycles) {
   extern __shared__ uint8_t smem_raw[];
@@ -455,6 +456,20 @@ __global__ void debug_load_kernel(const __grid_constant__ CUtensorMap m3, const 
       const int64_t r0 = ((t / heads) % nrb) * 128;
       uint8_t* dst = tile[s];
       uint64_t* bar = &full[s * 8 + my_bar];
+      if ((mode >> 10) & 1) {   // L2 prefetch of tile i + 8
+        const int64_t tp = (int64_t)blockIdx.x * tiles + i + 8;
+        const int32_t hp = (int32_t)(tp % heads);
+        const int64_t rp = ((tp / heads) % nrb) * 128;
+        if (kind == 0) {
+          if (lane == 0 && warp == 0) sm100::tma_prefetch_3d(&m3, 0, hp, (int32_t)rp);
+        } else if (kind == 1) {
+          const int per = 32 / W;
+          if (lane < per) {
+            const int32_t y = (int32_t)rp + 4 * (warp * per + lane);
+            sm100::tma_prefetch_gather4(&mg, hp * 64, y, y + 1, y + 2, y + 3);
+          }
+        }
+      }
       if (kind == 0) {
         if (lane == 0) {
           if (nb > 1 || warp == 0) sm100::mbar_arrive_expect_tx(bar, nb > 1 ? part : 16384);
@@ -462,7 +477,7 @@ __global__ void debug_load_kernel(const __grid_constant__ CUtensorMap m3, const 
         if (W > 1) asm volatile("bar.sync 1, %0;" ::"r"(W * 32) : "memory");
         if (lane == 0) {
           const int rw = 128 / W;
-          sm100::tma_load_3d(dst + warp * rw * 128, &m3, bar, 0, head, (int32_t)r0 + warp * rw,
+          sm100::tma_load_3d(dst + warp * rw * 128, ((mode >> 9) & 1) && (warp & 1) ? &m3b : &m3, bar, 0, head, (int32_t)r0 + warp * rw,
                              sm100::policy_evict_first());
         }
       } else if (kind == 1) {
@@ -472,7 +487,7 @@ __global__ void debug_load_kernel(const __grid_constant__ CUtensorMap m3, const 
         if (lane < per) {
           const int gi = warp * per + lane;
           const int32_t y = (int32_t)r0 + 4 * gi;
-          sm100::tma_gather4(dst + gi * 512, &mg, bar, head * 64, y, y + 1, y + 2, y + 3,
+          sm100::tma_gather4(dst + gi * 512, ((mode >> 9) & 1) && (warp & 1) ? &mgb : &mg, bar, head * 64, y, y + 1, y + 2, y + 3,
                              sm100::policy_evict_first());
         }
       } else if (kind == 2) {
@@ -507,14 +522,17 @@ extern "C" hla_status hla_debug_load_rate(const void* src, int64_t rows, int32_t
   HLA_REQUIRE(src && out_cycles && kind <= 3 && W >= 1 && W <= 8 && 32 % W == 0 && (kind != 2 || W == 4) &&
                   stages >= 1 && stages <= kLoadStagesMax && rows % 128 == 0,
               HLA_ERR_INVALID, "bad load-rate probe arguments");
-  CUtensorMap m3, mg;
+  CUtensorMap m3, mg, m3b, mgb;
   hla_status st = make_rows_map(&m3, src, rows, heads, 64, kind == 0 ? 128 / W : 128);
   if (st != HLA_OK) return st;
   st = make_gather_map(&mg, src, rows, heads, 64, 1);
   if (st != HLA_OK) return st;
+  // mode bit 9: odd warps use a second (identical) tensor map
+  if ((st = make_rows_map(&m3b, src, rows, heads, 64, kind == 0 ? 128 / W : 128)) != HLA_OK) return st;
+  if ((st = make_gather_map(&mgb, src, rows, heads, 64, 1)) != HLA_OK) return st;
   const size_t smem = (size_t)stages * 16384 + 2 * kLoadStagesMax * 8 * 8 + 1024;
   HLA_CUDA_TRY(cudaFuncSetAttribute(debug_load_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  debug_load_kernel<<<ctas, 32 * (W + 1), smem, stream>>>(m3, mg, reinterpret_cast<const __nv_bfloat16*>(src),
+  debug_load_kernel<<<ctas, 32 * (W + 1), smem, stream>>>(m3, mg, m3b, mgb, reinterpret_cast<const __nv_bfloat16*>(src),
                                                           rows, heads, mode, stages, tiles, out_cycles);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;

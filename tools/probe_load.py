@@ -9,8 +9,11 @@ src = torch.randn(rows, heads, 64, device="cuda").to(torch.bfloat16)
 ctas = torch.cuda.get_device_properties(0).multi_processor_count
 cyc = torch.zeros(4 * ctas, dtype=torch.int64, device="cuda")
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-def M(kind, W=1, nb=0): return kind | (W << 4) | (nb << 8)
-cases = [("tma3d W1", M(0), 4, 1), ("tma3d W1 2cta", M(0), 4, 2), ("tma3d W4", M(0, 4), 4, 1),
+def M(kind, W=1, nb=0, two=0, pf=0): return kind | (W << 4) | (nb << 8) | (two << 9) | (pf << 10)
+cases = [("tma3d W1 pf", M(0, 1, 0, 0, 1), 4, 1), ("tma3d W1 pf 2cta", M(0, 1, 0, 0, 1), 4, 2),
+         ("g4 W1 pf", M(1, 1, 0, 0, 1), 4, 1), ("g4 W4 pf", M(1, 4, 0, 0, 1), 4, 1), ("g4 W8 nb pf", M(1, 8, 1, 0, 1), 4, 1), ("tma3d W2", M(0, 2), 4, 1), ("tma3d W2 2maps", M(0, 2, 0, 1), 4, 1), ("tma3d W4 2maps", M(0, 4, 0, 1), 4, 1),
+         ("g4 W2", M(1, 2), 4, 1), ("g4 W2 2maps", M(1, 2, 0, 1), 4, 1), ("g4 W4 2maps", M(1, 4, 0, 1), 4, 1),
+         ("tma3d W1 st8", M(0), 8, 1), ("tma3d W2 st8 2maps", M(0, 2, 0, 1), 8, 1), ("tma3d W1", M(0), 4, 1), ("tma3d W1 2cta", M(0), 4, 2), ("tma3d W4", M(0, 4), 4, 1),
          ("tma3d W4 nb", M(0, 4, 1), 4, 1), ("g4 W1", M(1), 4, 1), ("g4 W1 2cta", M(1), 4, 2),
          ("g4 W4", M(1, 4), 4, 1), ("g4 W4 nb", M(1, 4, 1), 4, 1), ("g4 W8 nb", M(1, 8, 1), 4, 1),
          ("g4 W8 nb 2cta", M(1, 8, 1), 4, 2), ("g4 W4 nb 8st", M(1, 4, 1), 8, 1),
