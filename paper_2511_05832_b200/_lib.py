@@ -75,6 +75,8 @@ def lib():
         "hla_debug_load_rate": [vp, i64, i32, i32, i32, i32, i32, vp, vp],
     }
     for name, args in sig.items():
+        if name.startswith("hla_debug_") and not hasattr(L, name):
+            continue   # bring-up probes are optional (e.g. an older dev build under HLA_LIB_NAME)
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = ctypes.c_int

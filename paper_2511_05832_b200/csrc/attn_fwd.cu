@@ -361,33 +361,35 @@ __global__ void __launch_bounds__(kThreads, 2)
       while (it.valid) {
         const int32_t ct = it.t, cnt = it.nt;
         it.advance(prm.row_ptr, mq, units);
-        bool next_s_issued = false;
-        if (it.valid) {
-          // S(g+1) overwrites S(g): only after the softmax pulled S(g) into registers.
-          // Its operands may still be in flight (next unit's Q, K): then PV(g) goes first.
-          sm100::mbar_wait(&sm.s_free, g & 1);
-          if ((it.t != 0 || sm100::mbar_test_wait(&sm.q_full[it.n & 1], (it.n >> 1) & 1)) &&
+        // Two independent issues: S(g+1) (needs the softmax to have pulled S(g) into
+        // registers, and the next Q / K landed) and PV(g) (needs P(g)).  Whichever is
+        // ready first goes first: waiting for one in a fixed order stalls the other
+        // (S first stalls PV behind late K loads; PV first stalls S behind the softmax).
+        bool s_pending = it.valid, pv_pending = true;
+        if (s_pending) sm100::mbar_wait(&sm.s_free, g & 1);
+        while (s_pending || pv_pending) {
+          if (s_pending && (it.t != 0 || sm100::mbar_test_wait(&sm.q_full[it.n & 1], (it.n >> 1) & 1)) &&
               sm100::mbar_test_wait(&sm.k_full[(g + 1) & 1], ((g + 1) >> 1) & 1)) {
             sm100::tc_fence_after();
             issue_s(it.n, g + 1);
-            next_s_issued = true;
+            s_pending = false;
+            continue;
           }
-        }
-        sm100::mbar_wait(&sm.p_full, g & 1);
-        HLA_TR((1 << 24) | (2 << 16) | g);
-        sm100::mbar_wait(&sm.v_full[g & 1], (g >> 1) & 1);
-        sm100::tc_fence_after();
+          if (pv_pending && sm100::mbar_test_wait(&sm.p_full, g & 1)) {
+            HLA_TR((1 << 24) | (2 << 16) | g);
+            sm100::mbar_wait(&sm.v_full[g & 1], (g >> 1) & 1);
+            sm100::tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < kBlock / 16; ++kk)
-          sm100::mma_ts(tO, tP + kk * 8, mnmajor_desc<D>(sm.v[g & 1], kk), idesc_o, (ct > 0 || kk > 0) ? 1u : 0u);
-        sm100::mma_commit(&sm.kv_empty[g & 1]);
-        sm100::mma_commit(&sm.pv_done);
-        if (ct == cnt - 1) sm100::mma_commit(&sm.o_full);
-        if (it.valid && !next_s_issued) {
-          if (it.t == 0) sm100::mbar_wait(&sm.q_full[it.n & 1], (it.n >> 1) & 1);
-          sm100::mbar_wait(&sm.k_full[(g + 1) & 1], ((g + 1) >> 1) & 1);
-          sm100::tc_fence_after();
-          issue_s(it.n, g + 1);
+            for (int kk = 0; kk < kBlock / 16; ++kk)
+              sm100::mma_ts(tO, tP + kk * 8, mnmajor_desc<D>(sm.v[g & 1], kk), idesc_o,
+                            (ct > 0 || kk > 0) ? 1u : 0u);
+            sm100::mma_commit(&sm.kv_empty[g & 1]);
+            sm100::mma_commit(&sm.pv_done);
+            if (ct == cnt - 1) sm100::mma_commit(&sm.o_full);
+            pv_pending = false;
+            continue;
+          }
+          __nanosleep(32);
         }
         ++g;
       }
