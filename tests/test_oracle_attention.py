@@ -151,3 +151,92 @@ def test_zero_upstream_gradient():
     Q, K, V = (_rand((N, d), s) for s in (40, 41, 42))
     dQ, dK, dV, _, _ = attention.attn_bwd_slice(Q, K, V, np.zeros((N, d)), spec)
     assert not dQ.any() and not dK.any() and not dV.any()
+
+
+# ------------------------------------------------------------- global RPB (R19)
+# bias = table[h, dr + H - 1, dc + W - 1] with (dr, dc)
+# the 2D cell offset cell(q) - cell(k) recovered through the ordering's cell map.
+
+def test_rpb_hand_example():
+    # 2x2 grid.  Hilbert path (gilbert2d): seq 0..3 -> cells (0,0) (1,0) (1,1) (0,1);
+    # row-major: (0,0) (0,1) (1,0) (1,1).  Table T[i][j] = 3i + j, i = dr + 1, j = dc + 1.
+    T = np.arange(9.0).reshape(3, 3)
+    hil = np.array([[4, 1, 0, 3], [7, 4, 3, 6], [8, 5, 4, 7], [5, 2, 1, 4]], dtype=float)
+    rm = np.array([[4, 3, 1, 0], [5, 4, 2, 1], [7, 6, 4, 3], [8, 7, 5, 4]], dtype=float)
+    assert np.array_equal(attention.rpb_bias(Spec("HWA", 2, 2, 2, 2), T, np.arange(4)), hil)
+    assert np.array_equal(attention.rpb_bias(Spec("WSA", 2, 2, 2, 2), T, np.arange(4)), rm)
+
+
+def test_rpb_depends_on_cells_not_order():
+    # the same (q, k) cell pair under row-major and Hilbert order -> same bias
+    H, W = 8, 12
+    T = _rand((2 * H - 1, 2 * W - 1), 50)
+    s2c, c2s = hilbert.hilbert_order(H, W)
+    bh = attention.rpb_bias(Spec("HWA", H, W, 2, 2), T, np.arange(H * W))
+    brm = attention.rpb_bias(Spec("WSA", H, W, 2, 2), T, np.arange(H * W))
+    assert np.array_equal(bh[np.ix_(c2s, c2s)], brm)
+
+
+def test_rpb_zero_table_is_identity():
+    spec = Spec("HSWA", 8, 8, 4, 4, shift=8)
+    N, d = 64, 8
+    Q, K, V, dO = (_rand((N, d), s) for s in (51, 52, 53, 54))
+    Z = np.zeros((15, 15))
+    O0, L0 = attention.attn_fwd_slice(Q, K, V, spec)
+    O1, L1 = attention.attn_fwd_slice(Q, K, V, spec, rpb=Z)
+    assert np.array_equal(O0, O1) and np.array_equal(L0, L1)
+    g0 = attention.attn_bwd_slice(Q, K, V, dO, spec)
+    g1 = attention.attn_bwd_slice(Q, K, V, dO, spec, rpb=Z)
+    for a, b in zip(g0[:3], g1[:3]):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("spec", [Spec("HWA", 8, 8, 4, 4), Spec("HSWA", 8, 8, 4, 4, shift=8),
+                                  Spec("HNA", 8, 8, 3, 3), Spec("WSA", 8, 8, 4, 4)],
+                         ids=lambda s: s.kind)
+def test_rpb_matches_autograd_sdpa(spec):
+    # library pin: SDPA fp64 with an additive float mask (bias where allowed, -inf
+    # elsewhere); the table gradient comes from torch autograd through a gather
+    H, W = spec.grid_h, spec.grid_w
+    N, d = H * W, 8
+    Q, K, V, dO = (_rand((N, d), s) for s in (60, 61, 62, 63))
+    T = _rand((2 * H - 1, 2 * W - 1), 64)
+    dQ, dK, dV, O, LSE, dT = attention.attn_bwd_slice(Q, K, V, dO, spec, chunk=9, rpb=T)
+    r, c = attention.seq_cells(spec)
+    ir = torch.from_numpy(r[:, None] - r[None, :] + H - 1)
+    ic = torch.from_numpy(c[:, None] - c[None, :] + W - 1)
+    tT = torch.from_numpy(T).requires_grad_(True)
+    tq, tk, tv = (torch.from_numpy(a).requires_grad_(True) for a in (Q, K, V))
+    M = torch.from_numpy(patterns.materialize(spec))
+    bias = torch.where(M, tT[ir, ic], torch.tensor(-np.inf, dtype=torch.float64))
+    out = torch.nn.functional.scaled_dot_product_attention(tq[None], tk[None], tv[None], attn_mask=bias[None],
+                                                           scale=1 / np.sqrt(d))[0]
+    out.backward(torch.from_numpy(dO))
+    assert np.allclose(O, out.detach().numpy(), atol=1e-12)
+    for mine, ref in ((dQ, tq.grad), (dK, tk.grad), (dV, tv.grad), (dT, tT.grad)):
+        assert np.allclose(mine, ref.numpy(), rtol=0, atol=1e-11)
+    # sum over the table gradient = sum of dS = 0 (rows of dS sum to zero)
+    assert abs(dT.sum()) < 1e-11
+
+
+def test_rpb_finite_differences():
+    # S:L279 extended to the table: fp64 central differences, h = 1e-5, rel <= 1e-6
+    spec = Spec("HSA", 4, 4, 3, 3)
+    N, d, h = 16, 4, 1e-5
+    Q, K, V, dO = (_rand((N, d), s) for s in (70, 71, 72, 73))
+    T = _rand((7, 7), 74)
+    dT = attention.attn_bwd_slice(Q, K, V, dO, spec, rpb=T)[5]
+
+    def loss(T_):
+        O, _ = attention.attn_fwd_slice(Q, K, V, spec, rpb=T_)
+        return float((O * dO).sum())
+
+    num = np.zeros_like(T)
+    for i in range(7):
+        for j in range(7):
+            Tp, Tm = T.copy(), T.copy()
+            Tp[i, j] += h
+            Tm[i, j] -= h
+            num[i, j] = (loss(Tp) - loss(Tm)) / (2 * h)
+    rel = np.abs(num - dT).max() / np.abs(dT).max()
+    assert rel <= 1e-6, rel
