@@ -163,6 +163,32 @@ HLA_API hla_status hla_mask_ratios(const hla_pattern_desc* d, const int64_t coun
                            double* empty_tile_ratio, double* sparsity);
 
 /* ---------------------------------------------------------------------------
+ * Score modification (SPEC ScoreMod {none, global-RPB}).
+ * HLA_SCORE_GLOBAL_RPB ("HWT enlarges the window to the full feature map,
+ * enabling a global relative position bias"; reading R19):
+ *   score(q, k) = scale * <q, k> + rpb[h][dr + grid_h - 1][dc + grid_w - 1],
+ *   (dr, dc) = cell(q) - cell(k), the 2D grid offset of the pair,
+ * added before the mask (masked pairs stay excluded).
+ *   rpb         device fp32 [heads][2*grid_h-1][2*grid_w-1], read only.
+ *   drpb        backward only: device fp32, same shape; the table gradient
+ *               sum_{b, pairs with that offset} dL/dscore is ACCUMULATED into it
+ *               (zero it first; fp32 atomics, summation order not deterministic).
+ *   seq_to_cell device int32[N]: grid cell of every sequence position of d->order
+ *               (hla_hilbert_index for Hilbert orders; NULL = identity, only
+ *               valid for row-major patterns).  Independent of the fused-reorder
+ *               seq_to_cell argument (which describes the TENSOR layout).
+ * Passing NULL (or kind == HLA_SCORE_NONE) as the score_mod argument disables it.
+ */
+typedef enum { HLA_SCORE_NONE = 0, HLA_SCORE_GLOBAL_RPB = 1 } hla_score_kind;
+
+typedef struct {
+  int32_t kind;                 /* hla_score_kind */
+  const float* rpb;
+  float* drpb;
+  const int32_t* seq_to_cell;
+} hla_score_mod;
+
+/* ---------------------------------------------------------------------------
  * hla_attn_fwd -- block-sparse attention forward:
  *   for every (b, h, q-block i) and every listed kv-block j (ascending):
  *     S = scale * Q_i K_j^T (tcgen05, fp32 in TMEM); mask only if kind == partial;
@@ -187,6 +213,7 @@ HLA_API hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_mask*
                         int32_t batch, int32_t heads, int32_t head_dim, float scale,
                         const void* q, const void* k, const void* v,
                         void* o, float* lse, const int32_t* seq_to_cell,
+                        const hla_score_mod* score_mod,
                         int64_t* tiles_visited, cudaStream_t stream);
 
 /* ---------------------------------------------------------------------------
@@ -199,12 +226,16 @@ HLA_API hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_mask*
  * initialised.  dQ accumulation uses fp32 TMA reduce-adds (summation order is
  * not deterministic; covered by the stated tolerance).  Same limits as the forward.
  * seq_to_cell: as in hla_attn_fwd (fused reorder: every bf16 tensor in grid order).
+ * score_mod: as in hla_attn_fwd (same table); with global RPB, drpb receives the
+ * table gradient (accumulated; hla_attn_bwd zeroes it first, hla_attn_bwd_main
+ * does not).
  */
 HLA_API hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_mask* m,
                         int32_t batch, int32_t heads, int32_t head_dim, float scale,
                         const void* q, const void* k, const void* v, const void* o,
                         const float* lse, const void* dout,
                         void* dq, void* dk, void* dv, const int32_t* seq_to_cell,
+                        const hla_score_mod* score_mod,
                         void* workspace, size_t workspace_bytes,
                         int64_t* tiles_visited, cudaStream_t stream);
 
@@ -226,6 +257,7 @@ HLA_API hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_block_
                              int32_t batch, int32_t heads, int32_t head_dim, float scale,
                              const void* q, const void* k, const void* v,
                              const void* dout, void* dk, void* dv, const int32_t* seq_to_cell,
+                             const hla_score_mod* score_mod,
                              void* workspace, size_t workspace_bytes,
                              int64_t* tiles_visited, cudaStream_t stream);
 HLA_API hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,

@@ -29,6 +29,12 @@ class PatternDesc(ctypes.Structure):
                 ("shift", ctypes.c_int32), ("block_q", ctypes.c_int32), ("block_k", ctypes.c_int32)]
 
 
+class ScoreModC(ctypes.Structure):
+    """hla_score_mod (include/hla.h): kind 1 = global RPB."""
+    _fields_ = [("kind", ctypes.c_int32), ("rpb", ctypes.c_void_p), ("drpb", ctypes.c_void_p),
+                ("seq_to_cell", ctypes.c_void_p)]
+
+
 class BlockMaskC(ctypes.Structure):
     _fields_ = [("n_qblocks", ctypes.c_int32), ("n_kblocks", ctypes.c_int32), ("capacity", ctypes.c_int64),
                 ("row_ptr", ctypes.c_void_p), ("col_idx", ctypes.c_void_p), ("kind", ctypes.c_void_p),
@@ -60,10 +66,11 @@ def lib():
         "hla_build_block_mask": [pdesc, pmask, ctypes.POINTER(i64), vp],
         "hla_mask_ratios": [pdesc, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double),
                             ctypes.POINTER(ctypes.c_double)],
-        "hla_attn_fwd": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp],
-        "hla_attn_bwd": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp],
+        "hla_attn_fwd": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp],
+        "hla_attn_bwd": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp,
+                         vp],
         "hla_attn_bwd_preprocess": [i32, i32, i32, i32, f32, vp, vp, vp, vp, vp, sz, vp],
-        "hla_attn_bwd_main": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp],
+        "hla_attn_bwd_main": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp],
         "hla_attn_bwd_finalize": [i32, i32, i32, i32, vp, sz, vp, vp, vp],
         "hla_debug_umma": [vp, vp, vp, i32, i32, i32, i32, i32, i32, vp],
         "hla_debug_gather4": [vp, i64, i32, i32, vp, i32, i32, vp, vp],

@@ -127,10 +127,28 @@ def hla_build_block_mask(desc, device="cuda", stream=None):
     return m
 
 
+def score_mod(rpb=None, drpb=None, cells=None):
+    """hla_score_mod for the global RPB (reading R19): rpb fp32 [heads, 2H-1, 2W-1],
+    drpb its gradient buffer (backward), cells = int32 [N] grid cell of every sequence
+    position (hla_hilbert_index for Hilbert patterns; None = row-major identity).
+    None when rpb is None (no score modification)."""
+    if rpb is None:
+        return None
+    assert rpb.dtype == torch.float32 and rpb.is_cuda and rpb.is_contiguous()
+    if drpb is not None:
+        assert drpb.dtype == torch.float32 and drpb.shape == rpb.shape and drpb.is_contiguous()
+    return _lib.ScoreModC(1, _ptr(rpb), _ptr(drpb), _ptr(cells))
+
+
+def _sm(mod):
+    return ctypes.byref(mod) if mod is not None else None
+
+
 def hla_attn_fwd(desc, mask, q, k, v, scale=0.0, o=None, lse=None, tiles_visited=None, seq_to_cell=None,
-                 stream=None):
+                 stream=None, mod=None):
     """q, k, v: bf16 [B, N, heads, d] in desc's sequence order -> (o, lse [B, heads, N] fp32).
-    seq_to_cell (int32 [N] from hla_hilbert_index): fused reorder -- q, k, v, o in grid order."""
+    seq_to_cell (int32 [N] from hla_hilbert_index): fused reorder -- q, k, v, o in grid order.
+    mod: optional score_mod(...) (global RPB)."""
     B, N, H, D = q.shape
     for t in (q, k, v):
         assert t.dtype == torch.bfloat16 and t.is_cuda and t.is_contiguous() and t.shape == q.shape
@@ -141,7 +159,7 @@ def hla_attn_fwd(desc, mask, q, k, v, scale=0.0, o=None, lse=None, tiles_visited
     mc = mask.c
     check("hla_attn_fwd", lib().hla_attn_fwd(ctypes.byref(desc), ctypes.byref(mc), B, H, D, float(scale),
                                              _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(seq_to_cell),
-                                             _ptr(tiles_visited), _stream(stream)))
+                                             _sm(mod), _ptr(tiles_visited), _stream(stream)))
     return o, lse
 
 
@@ -150,7 +168,7 @@ def hla_attn_bwd_workspace(B, H, N, D):
 
 
 def hla_attn_bwd(desc, mask, q, k, v, o, lse, dout, scale=0.0, dq=None, dk=None, dv=None, workspace=None,
-                 tiles_visited=None, seq_to_cell=None, stream=None):
+                 tiles_visited=None, seq_to_cell=None, stream=None, mod=None):
     B, N, H, D = q.shape
     dq = torch.empty_like(q) if dq is None else dq
     dk = torch.empty_like(k) if dk is None else dk
@@ -161,8 +179,9 @@ def hla_attn_bwd(desc, mask, q, k, v, o, lse, dout, scale=0.0, dq=None, dk=None,
     mc = mask.c
     check("hla_attn_bwd", lib().hla_attn_bwd(ctypes.byref(desc), ctypes.byref(mc), B, H, D, float(scale),
                                              _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(dout),
-                                             _ptr(dq), _ptr(dk), _ptr(dv), _ptr(seq_to_cell), _ptr(workspace),
-                                             workspace.numel(), _ptr(tiles_visited), _stream(stream)))
+                                             _ptr(dq), _ptr(dk), _ptr(dv), _ptr(seq_to_cell), _sm(mod),
+                                             _ptr(workspace), workspace.numel(), _ptr(tiles_visited),
+                                             _stream(stream)))
     return dq, dk, dv
 
 
@@ -174,13 +193,14 @@ def hla_attn_bwd_preprocess(o, dout, lse, workspace, scale=0.0, seq_to_cell=None
 
 
 def hla_attn_bwd_main(desc, mask, q, k, v, dout, dk, dv, workspace, scale=0.0, tiles_visited=None,
-                      seq_to_cell=None, stream=None):
-    """Requires hla_attn_bwd_preprocess to have filled `workspace` (D, LSE in log2 domain)."""
+                      seq_to_cell=None, stream=None, mod=None):
+    """Requires hla_attn_bwd_preprocess to have filled `workspace` (D, LSE in log2 domain).
+    With a global-RPB mod, the table gradient is ACCUMULATED into mod's drpb."""
     B, N, H, D = q.shape
     mc = mask.c
     check("hla_attn_bwd_main", lib().hla_attn_bwd_main(ctypes.byref(desc), ctypes.byref(mc), B, H, D, float(scale),
                                                        _ptr(q), _ptr(k), _ptr(v), _ptr(dout), _ptr(dk),
-                                                       _ptr(dv), _ptr(seq_to_cell), _ptr(workspace),
+                                                       _ptr(dv), _ptr(seq_to_cell), _sm(mod), _ptr(workspace),
                                                        workspace.numel(), _ptr(tiles_visited), _stream(stream)))
 
 

@@ -18,6 +18,11 @@ the grid-order tensors (TMA .tile::gather4 through the cached seq_to_cell path)
 and scatter O / dK / dV / dQ rows back to their grid cells, so a step is
 fwd ; bwd_pre ; bwd ; bwd_fin with no permutation passes.  fused=False keeps the
 explicit hla_hilbert_perm passes (the paper's "Reshape" step).
+
+rpb=True adds HWT's global relative position bias (reading R19): a table
+`self.rpb` fp32 [heads, 2H-1, 2W-1] (zero-initialised; set it as a parameter)
+whose gradient is written to `self.drpb` by backward() (one memset + the
+backward kernel's accumulation; launches_per_step counts the memset).
 """
 
 import torch
@@ -27,7 +32,7 @@ from . import api
 
 class HilbertLocalAttention:
     def __init__(self, kind, grid_h, grid_w, win_h=1, win_w=1, batch=1, heads=1, head_dim=64, block=128,
-                 shift=0, scale=0.0, device="cuda", fused=True):
+                 shift=0, scale=0.0, device="cuda", fused=True, rpb=False):
         self.kind = kind
         self.grid_h, self.grid_w = grid_h, grid_w
         self.N = grid_h * grid_w
@@ -50,6 +55,16 @@ class HilbertLocalAttention:
             self.qs, self.ks, self.vs, self.os = e(), e(), e(), e()
             self.dos, self.dqs, self.dks, self.dvs = e(), e(), e(), e()
         self._saved = None
+        self.rpb = self.drpb = self.mod = None
+        if rpb:
+            shape = (heads, 2 * grid_h - 1, 2 * grid_w - 1)
+            self.rpb = torch.zeros(shape, dtype=torch.float32, device=device)
+            self.drpb = torch.zeros(shape, dtype=torch.float32, device=device)
+            cells = None
+            if self.hilbert:     # 2D offsets need the sequence -> cell map of the order
+                cells = self.s2c if self.s2c is not None else api.hla_hilbert_index(grid_h, grid_w, device)[0]
+            self._cells = cells
+            self.mod = api.score_mod(self.rpb, self.drpb, cells)
 
     # tiles executed per step, per (b, h): R (P:L102 r_i summed over q-blocks)
     @property
@@ -62,19 +77,21 @@ class HilbertLocalAttention:
         mark: optional callable(name) invoked after each launch (bench timing hook)."""
         mark = mark or _nop
         if self.fused:
-            api.hla_attn_fwd(self.desc, self.mask, q, k, v, self.scale, self.o, self.lse, seq_to_cell=self.s2c)
+            api.hla_attn_fwd(self.desc, self.mask, q, k, v, self.scale, self.o, self.lse, seq_to_cell=self.s2c,
+                             mod=self.mod)
             mark("fwd")
             self._saved = (q, k, v, self.o)
         elif self.hilbert:
             api.hla_hilbert_perm(self.grid_h, self.grid_w, api.TO_HILBERT, (q, k, v), (self.qs, self.ks, self.vs))
             mark("perm_qkv")
-            api.hla_attn_fwd(self.desc, self.mask, self.qs, self.ks, self.vs, self.scale, self.os, self.lse)
+            api.hla_attn_fwd(self.desc, self.mask, self.qs, self.ks, self.vs, self.scale, self.os, self.lse,
+                             mod=self.mod)
             mark("fwd")
             api.hla_hilbert_perm(self.grid_h, self.grid_w, api.FROM_HILBERT, (self.os,), (self.o,))
             mark("perm_o")
             self._saved = (self.qs, self.ks, self.vs, self.os)
         else:
-            api.hla_attn_fwd(self.desc, self.mask, q, k, v, self.scale, self.o, self.lse)
+            api.hla_attn_fwd(self.desc, self.mask, q, k, v, self.scale, self.o, self.lse, mod=self.mod)
             mark("fwd")
             self._saved = (q, k, v, self.o)
         return self.o
@@ -90,9 +107,11 @@ class HilbertLocalAttention:
         else:
             dout_s, dq, dk, dv = dout, self.dq, self.dk, self.dv
         api.hla_attn_bwd_preprocess(o, dout_s, self.lse, self.workspace, self.scale, seq_to_cell=self.s2c)
+        if self.drpb is not None:
+            self.drpb.zero_()      # the kernel accumulates the table gradient
         mark("bwd_pre")
         api.hla_attn_bwd_main(self.desc, self.mask, q, k, v, dout_s, dk, dv, self.workspace, self.scale,
-                              seq_to_cell=self.s2c)
+                              seq_to_cell=self.s2c, mod=self.mod)
         mark("bwd")
         api.hla_attn_bwd_finalize(self.workspace, dq, seq_to_cell=self.s2c)
         mark("bwd_fin")
@@ -105,7 +124,7 @@ class HilbertLocalAttention:
     # kernel launches per step (forward + backward)
     @property
     def launches_per_step(self):
-        return 8 if (self.hilbert and not self.fused) else 4
+        return (8 if (self.hilbert and not self.fused) else 4) + (1 if self.rpb is not None else 0)
 
     def step(self, q, k, v, dout, mark=None):
         """One pass of the whole hot path: forward then backward."""

@@ -40,7 +40,7 @@ constexpr int kHalf = 64;   // q-columns per pipeline half
 struct BwdParams {
   Pattern pat;
   int32_t N, heads, batch;
-  float scale, scale_log2;
+  float scale, scale_log2, inv_scale;
   const int32_t* t_row_ptr;
   const int32_t* t_col_idx;
   const uint8_t* t_kind;
@@ -48,12 +48,18 @@ struct BwdParams {
   const float* dsum;       // D * scale, [B, H, N] (workspace, from the preprocess)
   float* dq_acc;           // [B, N, H, Dh] fp32 (grid order when s2c != null)
   const int32_t* s2c;      // fused reorder: seq_to_cell table (tensors in grid order), else null
+  const float* rpb;        // global RPB table [heads][2H-1][2W-1] (kBias)
+  float* drpb;             // its gradient (accumulated)
+  const int32_t* cells;    // grid cell of each sequence position (null: identity)
+  int32_t grid_h, grid_w, rpb_w, rpb_hw;
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;
   unsigned long long* visited;
 };
 
-template <int D>
+constexpr int kRpbWin = 2048;   // fp32 entries of the per-tile dRPB window (offset box) in shared memory
+
+template <int D, bool kBias = false>
 struct BwdSmem {
   static constexpr uint32_t kTileBytes = kBlock * D * 2;
   alignas(1024) uint8_t k[2][kTileBytes];
@@ -67,6 +73,7 @@ struct BwdSmem {
   uint64_t kv_full[2], kv_empty[2], q_full[2], q_empty[2], s_full[2], ds_ready[2], dq_full, dq_free, dkv_full, epi_done;
   uint64_t dbg_bar;
   uint32_t tmem_base;
+  float rpb_win[kBias ? kRpbWin : 1];   // dRPB of the current tile's offset box (compute warps)
 };
 
 template <int D>
@@ -149,13 +156,44 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
 // next unit's K/V (and first Q/dO) stream in while the current unit computes;
 // the dK/dV epilogue of a unit overlaps the first S/dP MMAs of the next one.
 // Phase counters: n = units with nt > 0 so far, g = (q-block) tiles so far.
-template <int D, bool kTwoD, bool kGather>
+// cell -> (row << 16) | col (RPB offsets; grid sides < 2^15)
+__device__ __forceinline__ int32_t rpb_cell_rc(const int32_t* cells, int32_t seq, int32_t N, int32_t W) {
+  const int32_t cell = seq < N ? (cells ? __ldg(cells + seq) : seq) : 0;
+  const int32_t r = cell / W;
+  return (r << 16) | (cell - r * W);
+}
+// min / max of the rows and columns of the cells of sequence block [s0, s0 + 128)
+// (phantom positions >= N ignored); identical in every lane.
+struct CellBox { int32_t r0, r1, c0, c1; };
+__device__ __forceinline__ CellBox rpb_block_box(const int32_t* cells, int32_t s0, int32_t N, int32_t W, int lane) {
+  CellBox bx{1 << 30, -(1 << 30), 1 << 30, -(1 << 30)};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int32_t sq = s0 + 32 * j + lane;
+    if (sq < N) {
+      const int32_t rc = rpb_cell_rc(cells, sq, N, W);
+      const int32_t r = rc >> 16, c = rc & 0xffff;
+      bx.r0 = min(bx.r0, r); bx.r1 = max(bx.r1, r); bx.c0 = min(bx.c0, c); bx.c1 = max(bx.c1, c);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    bx.r0 = min(bx.r0, __shfl_xor_sync(0xffffffffu, bx.r0, o));
+    bx.r1 = max(bx.r1, __shfl_xor_sync(0xffffffffu, bx.r1, o));
+    bx.c0 = min(bx.c0, __shfl_xor_sync(0xffffffffu, bx.c0, o));
+    bx.c1 = max(bx.c1, __shfl_xor_sync(0xffffffffu, bx.c1, o));
+  }
+  return bx;
+}
+
+template <int D, bool kTwoD, bool kGather, bool kBias>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                     const __grid_constant__ CUtensorMap tmDQ, const BwdParams prm) {
   extern __shared__ uint8_t smem_raw[];
-  BwdSmem<D>& sm = *reinterpret_cast<BwdSmem<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  using Smem = BwdSmem<D, kBias>;
+  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t mk = (prm.N + kBlock - 1) / kBlock;   // last kv-block may be ragged
   const int32_t units = mk * prm.heads * prm.batch;
@@ -203,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_kv = sm100::policy_evict_first();
       const uint64_t pol_q = sm100::policy_evict_last();
       const int role = warp == 0 ? 0 : warp - 13;   // 0, 1, 2
-      constexpr uint32_t kTile = BwdSmem<D>::kTileBytes;
+      constexpr uint32_t kTile = Smem::kTileBytes;
       uint32_t n = 0, g = 0;
       int64_t stage_tag0 = -1, stage_tag1 = -1;   // (b, h, q-block) held by stage 0 / 1
       for (int32_t kq = 0;; ++kq) {
@@ -382,6 +420,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = prm.scale_log2, scale = prm.scale;
+    if (kBias) {   // the dRPB window starts (and is left after every flush) zeroed
+      for (int i = (warp - 2) * 32 + lane; i < kRpbWin; i += 256) sm.rpb_win[i] = 0.f;
+      sm100::named_bar_sync(3, 256);
+    }
     uint32_t n = 0, g = 0;
     for (int32_t kq = 0;; ++kq) {
         const int32_t u = unit_at(kq);
@@ -391,12 +433,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int32_t kidx = kb * kBlock + row;
       RowBox box = clip_box<kTwoD>(prm.pat, col_box(prm.pat, kidx));
       if (kidx >= prm.N) box.len = 0;   // phantom key row of a ragged tile: nothing allowed
+      // RPB: this key row's cell, the key block's cell box, the head's table / gradient
+      int32_t k_r = 0, k_c = 0;
+      CellBox kbox{0, 0, 0, 0};
+      const float* rpbh = nullptr;
+      float* drpbh = nullptr;
+      if (kBias) {
+        const int32_t rc = rpb_cell_rc(prm.cells, kidx, prm.N, prm.grid_w);
+        k_r = rc >> 16;
+        k_c = rc & 0xffff;
+        kbox = rpb_block_box(prm.cells, kb * kBlock, prm.N, prm.grid_w, lane);
+        rpbh = prm.rpb + (int64_t)h * prm.rpb_hw;
+        drpbh = prm.drpb + (int64_t)h * prm.rpb_hw;
+      }
       for (int t = 0; t < nt; ++t, ++g) {
         const int s = g & 1;
-        sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1);
-        if (row == 0 && cset == 0) HLA_TR((2 << 24) | ((1) << 16) | (g));
         const uint8_t kd = __ldg(prm.t_kind + rs + t);
         const int32_t q0 = __ldg(prm.t_col_idx + rs + t) * kBlock;
+        // RPB: cells of this warp set's two query chunks (lane e: column 32c + e), the
+        // tile's offset box (dr, dc) = q box - key box, and whether it fits the window
+        int32_t qrc[2] = {0, 0};
+        int32_t dr0 = 0, dc0 = 0, wc = 0;
+        bool win = false;
+        if (kBias) {
+          qrc[0] = rpb_cell_rc(prm.cells, q0 + 32 * cset + lane, prm.N, prm.grid_w);
+          qrc[1] = rpb_cell_rc(prm.cells, q0 + 32 * (2 + cset) + lane, prm.N, prm.grid_w);
+          const CellBox qbox = rpb_block_box(prm.cells, q0, prm.N, prm.grid_w, lane);
+          dr0 = qbox.r0 - kbox.r1;
+          dc0 = qbox.c0 - kbox.c1;
+          wc = qbox.c1 - kbox.c0 - dc0 + 1;
+          win = (qbox.r1 - kbox.r0 - dr0 + 1) * wc <= kRpbWin;
+        }
+        sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1);
+        if (row == 0 && cset == 0) HLA_TR((2 << 24) | ((1) << 16) | (g));
         const uint32_t lse2 = sm100::smem_u32(sm.lse[s]);
         const uint32_t dd = sm100::smem_u32(sm.dd[s]);
         const uint32_t dsbuf = sm100::smem_u32(sm.ds[g & 1]);
@@ -407,6 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           sm100::tc_fence_after();
           {
             const int c = 2 * half + cset;
+            const int32_t q_rc = half ? qrc[1] : qrc[0];   // RPB: cell of query column 32c + lane
             uint32_t sr[32], dpr[32];
             sm100::tmem_ld32(tmem + lane_off + kColS + c * 32, sr);
             sm100::tmem_ld32(tmem + lane_off + kColDP + c * 32, dpr);
@@ -419,7 +489,15 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float4 la = sm100::lds_f4(lse2 + qc * 4), lb = sm100::lds_f4(lse2 + qc * 4 + 16);
               const float lv[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
 #pragma unroll
-              for (int e = 0; e < 8; ++e) p[u4 * 8 + e] = sm100::ex2(fmaf(__uint_as_float(sr[u4 * 8 + e]), sl2, -lv[e]));
+              for (int e = 0; e < 8; ++e) {
+                float x = fmaf(__uint_as_float(sr[u4 * 8 + e]), sl2, -lv[e]);
+                if (kBias) {   // + bias * log2(e), bias = table[h][dr + H - 1][dc + W - 1]
+                  const int32_t rc = __shfl_sync(0xffffffffu, q_rc, u4 * 8 + e);
+                  const int32_t ti = ((rc >> 16) - k_r + prm.grid_h - 1) * prm.rpb_w + ((rc & 0xffff) - k_c + prm.grid_w - 1);
+                  x = fmaf(__ldg(rpbh + ti), 1.4426950408889634f, x);
+                }
+                p[u4 * 8 + e] = sm100::ex2(x);
+              }
             }
             uint32_t okbits = 0xffffffffu;   // element mask of this chunk (partial tiles only)
             if (kd == 2) {
@@ -458,6 +536,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // masked: exactly 0 (the D / LSE of phantom query columns may be stale, 0 * NaN = NaN)
                 if (!((okbits >> (u4 * 8 + e)) & 1u)) ds[e] = 0.f;
               }
+              if (kBias) {
+                // dRPB[offset] += dL/dscore = dS / scale: into the tile's shared-memory
+                // offset window (flushed once per tile), else straight to global
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  const int32_t rc = __shfl_sync(0xffffffffu, q_rc, u4 * 8 + e);
+                  if (!((okbits >> (u4 * 8 + e)) & 1u)) continue;
+                  const int32_t dr = (rc >> 16) - k_r, dc = (rc & 0xffff) - k_c;
+                  const float gv = ds[e] * prm.inv_scale;
+                  if (win)
+                    atomicAdd(&sm.rpb_win[(dr - dr0) * wc + (dc - dc0)], gv);
+                  else
+                    atomicAdd(drpbh + (dr + prm.grid_h - 1) * prm.rpb_w + (dc + prm.grid_w - 1), gv);
+                }
+              }
               // dS^T row -> smem [q/64][kv][64] with the 128B swizzle (16B chunks)
               const uint32_t off =
                   (uint32_t)(qc >> 6) * 16384u + sm100::swz128((uint32_t)row * 128u + (uint32_t)(qc & 63) * 2u);
@@ -470,6 +563,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           sm100::tc_fence_before();
           sm100::mbar_arrive(&sm.ds_ready[half]);
           if (row == 0 && cset == 0) HLA_TR((2 << 24) | ((3 + 2 * half) << 16) | (g));
+        }
+        if (kBias && win) {
+          // flush the tile's dRPB window to global (and re-zero it) -- all 256 compute threads
+          sm100::named_bar_sync(3, 256);
+          const int tid = (warp - 2) * 32 + lane;
+          const int wr = kRpbWin / wc;
+          for (int i = tid; i < wr * wc; i += 256) {
+            const float v = sm.rpb_win[i];
+            if (v != 0.f) {
+              const int32_t dr = dr0 + i / wc, dc = dc0 + i % wc;
+              atomicAdd(drpbh + (dr + prm.grid_h - 1) * prm.rpb_w + (dc + prm.grid_w - 1), v);
+              sm.rpb_win[i] = 0.f;
+            }
+          }
+          sm100::named_bar_sync(3, 256);
         }
       }
       tiles_done += nt;
@@ -637,17 +745,33 @@ __global__ void __launch_bounds__(256) dq_finalize_kernel(const float4* __restri
                      sm100::pack_bf16(v1.z, v1.w));
 }
 
-template <int D, bool kTwoD, bool kGather>
+template <int D, bool kTwoD, bool kGather, bool kBias>
 hla_status launch_bwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mdo,
                       const CUtensorMap& mdq, const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream) {
-  const size_t smem = sizeof(BwdSmem<D>) + 1024;
-  auto* fn = attn_bwd_kernel<D, kTwoD, kGather>;
+  const size_t smem = sizeof(BwdSmem<D, kBias>) + 1024;
+  auto* fn = attn_bwd_kernel<D, kTwoD, kGather, kBias>;
   HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t units = (int64_t)n_kblocks * prm.heads * prm.batch;
   const int grid = (int)std::min<int64_t>((units + 1) / 2, (int64_t)num_sms());   // pairs of units
   fn<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mdo, mdq, prm);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
+}
+
+static_assert(sizeof(BwdSmem<64, true>) + 1024 <= 227 * 1024, "bwd shared memory (d = 64, RPB) exceeds 227 KB");
+
+template <bool kBias>
+hla_status dispatch_bwd(int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
+                        const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm,
+                        int32_t mkb, cudaStream_t stream) {
+  if (head_dim == 64) {
+    if (gather) return launch_bwd<64, false, true, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
+    return two_d ? launch_bwd<64, true, false, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream)
+                 : launch_bwd<64, false, false, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
+  }
+  if (gather) return launch_bwd<32, false, true, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
+  return two_d ? launch_bwd<32, true, false, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream)
+               : launch_bwd<32, false, false, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
 }
 
 }  // namespace
@@ -712,8 +836,9 @@ extern "C" hla_status hla_attn_bwd_preprocess(int32_t batch, int32_t heads, int3
 extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch,
                                         int32_t heads, int32_t head_dim, float scale, const void* q, const void* k,
                                         const void* v, const void* dout, void* dk, void* dv,
-                                        const int32_t* seq_to_cell, void* workspace, size_t workspace_bytes,
-                                        int64_t* tiles_visited, cudaStream_t stream) {
+                                        const int32_t* seq_to_cell, const hla_score_mod* score_mod,
+                                        void* workspace, size_t workspace_bytes, int64_t* tiles_visited,
+                                        cudaStream_t stream) {
   clear_error();
   Pattern pat;
   hla_status st = check_attn_args(d, m, batch, heads, head_dim, &pat);
@@ -743,6 +868,12 @@ extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_blo
   prm.dv = reinterpret_cast<__nv_bfloat16*>(dv);
   prm.visited = reinterpret_cast<unsigned long long*>(tiles_visited);
   prm.s2c = seq_to_cell;
+  if ((st = parse_score_mod(d, score_mod, true, &prm.rpb, &prm.drpb, &prm.cells)) != HLA_OK) return st;
+  prm.grid_h = pat.H;
+  prm.grid_w = pat.W;
+  prm.rpb_w = 2 * pat.W - 1;
+  prm.rpb_hw = (2 * pat.H - 1) * prm.rpb_w;
+  prm.inv_scale = 1.f / sc;
   const bool gather = seq_to_cell != nullptr;
   HLA_REQUIRE(!gather || d->order == HLA_ORDER_HILBERT, HLA_ERR_INVALID,
               "seq_to_cell (fused reorder) is only meaningful for Hilbert-order patterns");
@@ -760,14 +891,8 @@ extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_blo
   if ((st = make_f32_rows_map(&mdq, dq_acc, tok, heads, head_dim, 32, kBlock)) != HLA_OK) return st;
   const bool two_d = pat.kind == K_WSA || pat.kind == K_SA || pat.kind == K_NA2D;
   const int32_t mkb = (pat.N + kBlock - 1) / kBlock;
-  if (head_dim == 64) {
-    if (gather) return launch_bwd<64, false, true>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
-    return two_d ? launch_bwd<64, true, false>(mq, mk, mv, mdo, mdq, prm, mkb, stream)
-                 : launch_bwd<64, false, false>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
-  }
-  if (gather) return launch_bwd<32, false, true>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
-  return two_d ? launch_bwd<32, true, false>(mq, mk, mv, mdo, mdq, prm, mkb, stream)
-               : launch_bwd<32, false, false>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
+  return prm.rpb ? dispatch_bwd<true>(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, mkb, stream)
+                 : dispatch_bwd<false>(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, mkb, stream);
 }
 
 extern "C" hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,
@@ -793,8 +918,8 @@ extern "C" hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_
 extern "C" hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
                                    int32_t head_dim, float scale, const void* q, const void* k, const void* v,
                                    const void* o, const float* lse, const void* dout, void* dq, void* dk, void* dv,
-                                   const int32_t* seq_to_cell, void* workspace, size_t workspace_bytes,
-                                   int64_t* tiles_visited, cudaStream_t stream) {
+                                   const int32_t* seq_to_cell, const hla_score_mod* score_mod, void* workspace,
+                                   size_t workspace_bytes, int64_t* tiles_visited, cudaStream_t stream) {
   clear_error();
   Pattern pat;
   hla_status st = check_attn_args(d, m, batch, heads, head_dim, &pat);
@@ -805,10 +930,16 @@ extern "C" hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_ma
   st = carve_workspace(batch, heads, pat.N, head_dim, workspace, workspace_bytes, &dq_acc, &dsum);
   if (st != HLA_OK) return st;
   HLA_REQUIRE(((uintptr_t)o | (uintptr_t)dq) % 16 == 0, HLA_ERR_INVALID, "tensors must be 16-byte aligned");
+  const float* rpb;
+  float* drpb;
+  const int32_t* cells;
+  if ((st = parse_score_mod(d, score_mod, true, &rpb, &drpb, &cells)) != HLA_OK) return st;
+  if (drpb)   // the table gradient is accumulated: start from zero
+    HLA_CUDA_TRY(cudaMemsetAsync(drpb, 0, sizeof(float) * heads * (2 * pat.H - 1) * (2 * pat.W - 1), stream));
   if ((st = hla_attn_bwd_preprocess(batch, heads, pat.N, head_dim, scale, o, dout, lse, seq_to_cell, workspace,
                                     workspace_bytes, stream)) != HLA_OK)
     return st;
-  if ((st = hla_attn_bwd_main(d, m, batch, heads, head_dim, scale, q, k, v, dout, dk, dv, seq_to_cell,
+  if ((st = hla_attn_bwd_main(d, m, batch, heads, head_dim, scale, q, k, v, dout, dk, dv, seq_to_cell, score_mod,
                               workspace, workspace_bytes, tiles_visited, stream)) != HLA_OK)
     return st;
   return hla_attn_bwd_finalize(batch, heads, pat.N, head_dim, workspace, workspace_bytes, dq, seq_to_cell, stream);

@@ -45,6 +45,10 @@ struct FwdParams {
   const int32_t* col_idx;
   const uint8_t* kind;
   const int32_t* s2c;        // fused reorder: seq_to_cell table (tensors in grid order), else null
+  const float* rpb;          // global RPB table [heads][2H-1][2W-1] (kBias), else null
+  const int32_t* cells;      // grid cell of each sequence position for the RPB offsets (null: identity)
+  int32_t grid_w, rpb_w, rpb_hw;   // W, 2W-1, (2H-1)(2W-1)
+  int32_t rpb_a0;                  // (H-1)(2W-1) + (W-1): index of the zero offset
   __nv_bfloat16* o;
   float* lse;
   unsigned long long* visited;
@@ -204,7 +208,24 @@ __device__ __forceinline__ int32_t tile_meta(int32_t meta, const int32_t* col, c
 //             (s_free), then PV(g) after P(g) is in TMEM (p_full)
 //   softmax : S(g) -> registers -> s_free -> mask / max / exp; before writing
 //             P(g) (and before rescaling O) it waits pv_done(g-1)
-template <int D, bool kTwoD, bool kGather>
+// Global RPB (reading R19): the table index of the pair (q, k) is
+// A_q - B_k with A_q = (qr + H - 1)(2W - 1) + qc + W - 1, B_k = kr (2W - 1) + kc.
+__device__ __forceinline__ int32_t rpb_cell_off(const int32_t* cells, int32_t seq, int32_t N, int32_t W, int32_t rw) {
+  const int32_t cell = seq < N ? (cells ? __ldg(cells + seq) : seq) : 0;
+  const int32_t r = cell / W;
+  return r * rw + (cell - r * W);
+}
+// B_k of the 4 keys k0 + 4 lane .. + 3 of a kv tile (lane-distributed; 16-B loads)
+__device__ __forceinline__ int4 rpb_key_offs(const int32_t* cells, int32_t k0, int32_t N, int32_t W, int32_t rw,
+                                             int lane) {
+  const int32_t k = k0 + 4 * lane;
+  int4 c = make_int4(0, 0, 0, 0);
+  if (k < N) c = cells ? __ldg(reinterpret_cast<const int4*>(cells + k0) + lane) : make_int4(k, k + 1, k + 2, k + 3);
+  auto off = [&](int32_t cell) { const int32_t r = cell / W; return r * rw + (cell - r * W); };
+  return make_int4(off(c.x), off(c.y), off(c.z), off(c.w));
+}
+
+template <int D, bool kTwoD, bool kGather, bool kBias>
 __global__ void __launch_bounds__(kThreads, 2)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
@@ -411,6 +432,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       meta = load_meta(prm.col_idx, prm.kind, it.rs, it.nt, lane);
       pmeta = load_meta(prm.col_idx, prm.kind, it.prs, it.pre - it.prs, lane);
     }
+    // RPB: key offsets of the next tile, loaded one tile ahead
+    int4 bk_next = make_int4(0, 0, 0, 0);
+    if (kBias && it.valid)
+      bk_next = rpb_key_offs(prm.cells, (tile_meta(meta, prm.col_idx, prm.kind, it.rs, 0) >> 2) * kBlock, prm.N,
+                             prm.grid_w, prm.rpb_w, lane);
     while (it.valid) {
       const int32_t qb = it.u % mq, h = (it.u / mq) % prm.heads, b = it.u / (mq * prm.heads);
       const int32_t q = qb * kBlock + row;
@@ -418,6 +444,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       const RowBox box = row_box(prm.pat, q);
       const bool real = q < prm.N;
       const int32_t ocell = kGather ? (real ? __ldg(prm.s2c + q) : 0) : q;   // fused inverse reorder of O (used at the end)
+      const float* rpbh = kBias ? prm.rpb + (int64_t)h * prm.rpb_hw : nullptr;
+      const int32_t a_q = kBias ? prm.rpb_a0 + rpb_cell_off(prm.cells, q, prm.N, prm.grid_w, prm.rpb_w) : 0;
       if (row == 0) HLA_TR((2 << 24) | (6 << 16) | it.n);
       for (int t = 0; t < it.nt; ++t, ++g) {
         sm100::mbar_wait(&sm.s_full, g & 1);
@@ -434,6 +462,22 @@ __global__ void __launch_bounds__(kThreads, 2)
         sm100::mbar_arrive(&sm.s_free);          // the MMA may overwrite S with S(g+1)
         float (&s)[kBlock] = *reinterpret_cast<float(*)[kBlock]>(sr);
         const int32_t tm = tile_meta(meta, prm.col_idx, prm.kind, it.rs, t);
+        // kBias: scores move to the log2 domain here (s = S * scale * log2e + bias * log2e)
+        // so that the mask, the max and the exponentials see the biased score
+        const float sl2e = kBias ? 1.f : sl2;
+        if (kBias) {
+          const int4 bk = bk_next;
+          // the next tile's key offsets (this unit's next tile, else the next unit's first)
+          const int32_t nt_kvb = (t + 1 < it.nt) ? (tile_meta(meta, prm.col_idx, prm.kind, it.rs, t + 1) >> 2)
+                                                 : (__shfl_sync(0xffffffffu, pmeta, 0) >> 2);
+          bk_next = rpb_key_offs(prm.cells, nt_kvb * kBlock, prm.N, prm.grid_w, prm.rpb_w, lane);
+          const int32_t bkr[4] = {bk.x, bk.y, bk.z, bk.w};
+#pragma unroll
+          for (int c = 0; c < kBlock; ++c) {
+            const int32_t b_k = __shfl_sync(0xffffffffu, bkr[c & 3], c >> 2);
+            s[c] = fmaf(s[c], sl2, __ldg(rpbh + (a_q - b_k)) * 1.4426950408889634f);
+          }
+        }
         if ((tm & 3) == 2) apply_row_mask<kTwoD>(s, prm.pat, box, (tm >> 2) * kBlock);
         // row max with 8 independent chains (a single dependent chain costs ~4 cycles x 128)
         float m8[8];
@@ -445,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int j = 4; j > 0; j >>= 1)
 #pragma unroll
           for (int i = 0; i < j; ++i) m8[i] = fmaxf(m8[i], m8[i + j]);
-        const float m_tile = m8[0] * sl2;
+        const float m_tile = m8[0] * sl2e;
         if (row == 0) HLA_TR((6 << 24) | (2 << 16) | g);
         // lazy rescale (exact): keep the reference max unless it grew by > 8 (x256)
         const float m_new = (m_tile > m_ref + 8.f) ? m_tile : m_ref;
@@ -458,8 +502,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int e = 0; e < 64; ++e) {
           // MUFU for one half of the exponentials, the FMA pipe for the other (FA4's split)
-          const float p0 = sm100::ex2(fmaf(s[2 * e], sl2, -m_use));
-          const float p1 = sm100::ex2(fmaf(s[2 * e + 1], sl2, -m_use));
+          const float p0 = sm100::ex2(fmaf(s[2 * e], sl2e, -m_use));
+          const float p1 = sm100::ex2(fmaf(s[2 * e + 1], sl2e, -m_use));
           l4[e & 3] += p0 + p1;
           pk[e] = sm100::pack_bf16(p0, p1);
         }
@@ -550,17 +594,31 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (warp == 4 && lane == 0 && prm.visited != nullptr && tiles_done > 0) atomicAdd(prm.visited, tiles_done);
 }
 
-template <int D, bool kTwoD, bool kGather>
+template <int D, bool kTwoD, bool kGather, bool kBias>
 hla_status launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mo,
                       const FwdParams& prm, int32_t n_qblocks, cudaStream_t stream) {
   const size_t smem = sizeof(FwdSmem<D>) + 1024;
-  auto* fn = attn_fwd_kernel<D, kTwoD, kGather>;
+  auto* fn = attn_fwd_kernel<D, kTwoD, kGather, kBias>;
   HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t units = (int64_t)n_qblocks * prm.heads * prm.batch;
   const int grid = (int)std::min<int64_t>((units + 1) / 2, 2 * (int64_t)num_sms());   // pairs of units
   fn<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mo, prm);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
+}
+
+template <bool kBias>
+hla_status dispatch_fwd(int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
+                        const CUtensorMap& mv, const CUtensorMap& mo, const FwdParams& prm, int32_t mqb,
+                        cudaStream_t stream) {
+  if (head_dim == 64) {
+    if (gather) return launch_fwd<64, false, true, kBias>(mq, mk, mv, mo, prm, mqb, stream);
+    return two_d ? launch_fwd<64, true, false, kBias>(mq, mk, mv, mo, prm, mqb, stream)
+                 : launch_fwd<64, false, false, kBias>(mq, mk, mv, mo, prm, mqb, stream);
+  }
+  if (gather) return launch_fwd<32, false, true, kBias>(mq, mk, mv, mo, prm, mqb, stream);
+  return two_d ? launch_fwd<32, true, false, kBias>(mq, mk, mv, mo, prm, mqb, stream)
+               : launch_fwd<32, false, false, kBias>(mq, mk, mv, mo, prm, mqb, stream);
 }
 
 }  // namespace
@@ -583,14 +641,32 @@ hla_status check_attn_args(const hla_pattern_desc* d, const hla_block_mask* m, i
   return HLA_OK;
 }
 
+hla_status parse_score_mod(const hla_pattern_desc* d, const hla_score_mod* mod, bool bwd, const float** rpb,
+                           float** drpb, const int32_t** cells) {
+  *rpb = nullptr;
+  *cells = nullptr;
+  if (drpb) *drpb = nullptr;
+  if (mod == nullptr || mod->kind == HLA_SCORE_NONE) return HLA_OK;
+  HLA_REQUIRE(mod->kind == HLA_SCORE_GLOBAL_RPB, HLA_ERR_UNSUPPORTED, "score_mod kind %d not supported", mod->kind);
+  HLA_REQUIRE(mod->rpb != nullptr, HLA_ERR_INVALID, "score_mod: rpb table is null");
+  HLA_REQUIRE(d->order != HLA_ORDER_HILBERT || mod->seq_to_cell != nullptr, HLA_ERR_INVALID,
+              "score_mod: Hilbert order needs seq_to_cell for the 2D offsets");
+  HLA_REQUIRE(((uintptr_t)mod->seq_to_cell & 15) == 0, HLA_ERR_INVALID, "score_mod: seq_to_cell must be 16-byte aligned");
+  HLA_REQUIRE(!bwd || mod->drpb != nullptr, HLA_ERR_INVALID, "score_mod: drpb (table gradient) is null");
+  *rpb = mod->rpb;
+  *cells = mod->seq_to_cell;
+  if (drpb) *drpb = mod->drpb;
+  return HLA_OK;
+}
+
 }  // namespace hla
 
 using namespace hla;
 
 extern "C" hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
                                    int32_t head_dim, float scale, const void* q, const void* k, const void* v,
-                                   void* o, float* lse, const int32_t* seq_to_cell, int64_t* tiles_visited,
-                                   cudaStream_t stream) {
+                                   void* o, float* lse, const int32_t* seq_to_cell,
+                                   const hla_score_mod* score_mod, int64_t* tiles_visited, cudaStream_t stream) {
   clear_error();
   Pattern pat;
   hla_status st = check_attn_args(d, m, batch, heads, head_dim, &pat);
@@ -611,6 +687,11 @@ extern "C" hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_ma
   prm.o = reinterpret_cast<__nv_bfloat16*>(o);
   prm.lse = lse;
   prm.s2c = seq_to_cell;
+  if ((st = parse_score_mod(d, score_mod, false, &prm.rpb, nullptr, &prm.cells)) != HLA_OK) return st;
+  prm.grid_w = pat.W;
+  prm.rpb_w = 2 * pat.W - 1;
+  prm.rpb_hw = (2 * pat.H - 1) * prm.rpb_w;
+  prm.rpb_a0 = (pat.H - 1) * prm.rpb_w + (pat.W - 1);
   prm.visited = reinterpret_cast<unsigned long long*>(tiles_visited);
   const bool two_d = pat.kind == K_WSA || pat.kind == K_SA || pat.kind == K_NA2D;
   const bool gather = seq_to_cell != nullptr;
@@ -631,12 +712,6 @@ extern "C" hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_ma
     if ((st = make_rows_map(&mv, v, rows, heads, head_dim, kBlock)) != HLA_OK) return st;
   }
   const int32_t mqb = (pat.N + kBlock - 1) / kBlock;
-  if (head_dim == 64) {
-    if (gather) return launch_fwd<64, false, true>(mq, mk, mv, mo, prm, mqb, stream);
-    return two_d ? launch_fwd<64, true, false>(mq, mk, mv, mo, prm, mqb, stream)
-                 : launch_fwd<64, false, false>(mq, mk, mv, mo, prm, mqb, stream);
-  }
-  if (gather) return launch_fwd<32, false, true>(mq, mk, mv, mo, prm, mqb, stream);
-  return two_d ? launch_fwd<32, true, false>(mq, mk, mv, mo, prm, mqb, stream)
-               : launch_fwd<32, false, false>(mq, mk, mv, mo, prm, mqb, stream);
+  return prm.rpb ? dispatch_fwd<true>(head_dim, gather, two_d, mq, mk, mv, mo, prm, mqb, stream)
+                 : dispatch_fwd<false>(head_dim, gather, two_d, mq, mk, mv, mo, prm, mqb, stream);
 }

@@ -56,6 +56,11 @@ hla_status make_pattern(const hla_pattern_desc* d, Pattern* p);
 hla_status check_attn_args(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
                            int32_t head_dim, Pattern* pat);
 
+// Validates an optional hla_score_mod (attn_fwd.cu): outputs stay null when the
+// score modification is off; drpb may be null for the forward.
+hla_status parse_score_mod(const hla_pattern_desc* d, const hla_score_mod* mod, bool bwd, const float** rpb,
+                           float** drpb, const int32_t** cells);
+
 // number of SMs of the current device (cached per process; B200: 148)
 inline int num_sms() {
   static int n = 0;

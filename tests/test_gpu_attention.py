@@ -221,3 +221,59 @@ def test_step_full_size_sampled(case):
     assert_close("%s dQ" % name, to_np(dq[b, :, h])[s2c], dQ)
     assert_close("%s dK" % name, to_np(dk[b, :, h])[s2c], dK)
     assert_close("%s dV" % name, to_np(dv[b, :, h])[s2c], dV)
+
+
+# ------------------------------------------------------------- global RPB (R19, R20)
+RPB_CASES = [
+    # kind, grid, window, B, heads, d, fused
+    ("HWA", 32, 8, 2, 2, 64, True),
+    ("HSWA", 32, 8, 1, 3, 32, True),       # HWT's second block of a pair, d32 (cfg5 family)
+    ("HNA", 32, 5, 1, 2, 64, False),       # explicit permutation path
+    ("WSA", 32, 8, 2, 2, 64, True),        # row-major: identity cell map
+    ("WSA", 56, 7, 1, 1, 32, True),        # 56x56 (paper shape), ragged last tile
+]
+
+
+@pytest.mark.parametrize("case", RPB_CASES, ids=lambda c: "%s%d_d%d" % (c[0], c[1], c[5]))
+def test_rpb_fwd_bwd_vs_oracle(case):
+    """HWT's global relative position bias: O, LSE,
+    dQ, dK, dV under the north_star bound; the table gradient (a sum over up to
+    B*N pairs per offset) under a relative L2 bound (reading R20)."""
+    kind, g, w, B, H, d, fused = case
+    N = g * g
+    shift = (w * w) // 2 if kind == "HSWA" else 0
+    q, k, v, do = _inputs(B, N, H, d, seed=21)
+    layer = hla.HilbertLocalAttention(kind, g, g, w, w, B, H, d, shift=shift, device=DEV, fused=fused, rpb=True)
+    table = torch.rand(layer.rpb.shape, generator=torch.Generator().manual_seed(5), dtype=torch.float64)
+    layer.rpb.copy_((2 * table - 1).float())            # U(-1, 1): the bias moves the softmax
+    o = layer.forward(q, k, v)
+    dq, dk, dv = layer.backward(do)
+    torch.cuda.synchronize()
+    spec = Spec(kind, g, g, w, w, shift=shift)
+    s2c = hilbert.hilbert_order(g, g)[0] if spec.order == "hilbert" else np.arange(N)
+    seq = lambda t: hilbert.to_sequence(to_np(t), s2c)   # noqa: E731  grid -> sequence order
+    T = layer.rpb.double().cpu().numpy()
+    O_ref, L_ref = oatt.attn_fwd(seq(q), seq(k), seq(v), spec, rpb=T)
+    dQ_ref, dK_ref, dV_ref, dT_ref = oatt.attn_bwd(seq(q), seq(k), seq(v), seq(do), spec, rpb=T)
+    assert_close("rpb O", seq(o), O_ref)
+    assert np.abs(to_np(layer.lse) - L_ref).max() <= LSE_MAX_ABS
+    for name, got, ref in (("dQ", dq, dQ_ref), ("dK", dk, dK_ref), ("dV", dv, dV_ref)):
+        assert_close("rpb " + name, seq(got), ref)
+    dT = layer.drpb.double().cpu().numpy()
+    rel = np.linalg.norm(dT - dT_ref) / np.linalg.norm(dT_ref)
+    assert rel <= 2e-2, rel
+    assert abs(dT.sum()) <= 1e-3 * np.abs(dT_ref).sum() + 1e-3   # rows of dS sum to zero
+
+
+def test_rpb_zero_table_matches_no_bias():
+    """A zero table leaves O / gradients at the no-bias result (same tiles, same
+    arithmetic up to the log2-domain reassociation of the score)."""
+    g, w, B, H, d = 32, 8, 1, 2, 64
+    q, k, v, do = _inputs(B, g * g, H, d, seed=22)
+    a = hla.HilbertLocalAttention("HWA", g, g, w, w, B, H, d, device=DEV)
+    b = hla.HilbertLocalAttention("HWA", g, g, w, w, B, H, d, device=DEV, rpb=True)
+    ra = [t.clone() for t in (a.forward(q, k, v),) + a.backward(do)]
+    rb = [t.clone() for t in (b.forward(q, k, v),) + b.backward(do)]
+    torch.cuda.synchronize()
+    for x, y in zip(ra, rb):
+        assert (x.float() - y.float()).abs().max().item() <= 2e-2

@@ -53,12 +53,26 @@ def test_argument_validation_without_gpu():
     # attention limits
     d = api.pattern_desc("HWA", 64, 64, 16, 16, block=64)
     m = _lib.BlockMaskC(64, 64, 1, 8, 8, 8, 8, 8, 8, 8)
-    st = L.hla_attn_fwd(ctypes.byref(d), ctypes.byref(m), 1, 1, 64, 0.0, 16, 16, 16, 16, 16, None, None, None)
+    st = L.hla_attn_fwd(ctypes.byref(d), ctypes.byref(m), 1, 1, 64, 0.0, 16, 16, 16, 16, 16, None, None, None,
+                        None)
     assert st == _lib.HLA_ERR_UNSUPPORTED
     d = api.pattern_desc("HWA", 64, 64, 16, 16)
     m = _lib.BlockMaskC(32, 32, 1, 8, 8, 8, 8, 8, 8, 8)
-    st = L.hla_attn_fwd(ctypes.byref(d), ctypes.byref(m), 1, 1, 128, 0.0, 16, 16, 16, 16, 16, None, None, None)
+    st = L.hla_attn_fwd(ctypes.byref(d), ctypes.byref(m), 1, 1, 128, 0.0, 16, 16, 16, 16, 16, None, None, None,
+                        None)
     assert st == _lib.HLA_ERR_UNSUPPORTED
+    # score_mod validation (global RPB, reading R19): unknown kind, missing table,
+    # Hilbert order without the cell map, backward without a gradient buffer
+    for mod, want in ((_lib.ScoreModC(7, 16, 16, 16), _lib.HLA_ERR_UNSUPPORTED),
+                      (_lib.ScoreModC(1, None, 16, 16), _lib.HLA_ERR_INVALID),
+                      (_lib.ScoreModC(1, 16, 16, None), _lib.HLA_ERR_INVALID)):
+        st = L.hla_attn_fwd(ctypes.byref(d), ctypes.byref(m), 1, 1, 64, 0.0, 16, 16, 16, 16, 16, None,
+                            ctypes.byref(mod), None, None)
+        assert st == want, (mod.kind, st)
+    mod = _lib.ScoreModC(1, 16, None, 16)
+    st = L.hla_attn_bwd_main(ctypes.byref(d), ctypes.byref(m), 1, 1, 64, 0.0, 16, 16, 16, 16, 16, 16, None,
+                             ctypes.byref(mod), 256, 1 << 30, None, None)
+    assert st == _lib.HLA_ERR_INVALID and b"drpb" in L.hla_last_error()
 
 
 @pytest.mark.parametrize("kind,H,W,wh,ww,b", [("HWA", 56, 56, 7, 7, 128), ("SA", 56, 56, 7, 7, 128),
