@@ -9,6 +9,9 @@
 // The permutation is a bit-exact row gather: one warp per token row, 16-byte
 // vector loads/stores, up to 4 chunks per lane in flight, several tensors per
 // launch.  HBM-bound: 2 * row_bytes of traffic per row.
+#include <cstdlib>
+#include <vector>
+
 #include "common.cuh"
 
 namespace hla {
@@ -102,9 +105,58 @@ __global__ void __launch_bounds__(256) hilbert_perm_kernel(PermPtrs ptrs, int32_
 static hla_status check_grid(int32_t grid_h, int32_t grid_w, int* log2n) {
   HLA_REQUIRE(grid_h >= 1 && grid_w >= 1, HLA_ERR_INVALID, "grid %dx%d invalid", grid_h, grid_w);
   HLA_REQUIRE(grid_h == grid_w && is_pow2(grid_h) && grid_h <= 32768, HLA_ERR_UNSUPPORTED,
-              "Hilbert path needs a square 2^k grid (got %dx%d; generalized curve is NEXT-4)", grid_h, grid_w);
+              "the explicit permutation kernel needs a square 2^k grid (got %dx%d); other grids: "
+              "hla_hilbert_index + the fused reorder of the attention kernels", grid_h, grid_w);
   *log2n = ilog2(grid_h);
   return HLA_OK;
+}
+
+// Generalized Hilbert curve for any W x H grid (the "gilbert" construction the
+// paper's shapes need: 56x56, 28x28, 14x14, 7x7, 96x96, ... ).
+// Recursive split of the rectangle spanned by the major axis (ax, ay) and the
+// minor axis (bx, by): a long rectangle is cut in two along its major axis, a
+// squarish one in three (first and last parts turned), keeping every part's
+// major side even when possible so the path stays adjacent-step connected.
+// Host code, once per grid shape; on 2^k squares it yields the same path as the
+// device bit loops above (tested: both against the oracle, bit-exact).
+namespace {
+inline int sgn(int v) { return (v > 0) - (v < 0); }
+inline int floor_half(int v) { return v >= 0 ? v / 2 : -((1 - v) / 2); }   // floor(v / 2)
+
+void gilbert_rect(int x, int y, int ax, int ay, int bx, int by, int W, int32_t* out, int& pos) {
+  const int w = std::abs(ax + ay), h = std::abs(bx + by);
+  const int dax = sgn(ax), day = sgn(ay), dbx = sgn(bx), dby = sgn(by);
+  if (h == 1) {   // a single row along the major axis
+    for (int i = 0; i < w; ++i, x += dax, y += day) out[pos++] = y * W + x;
+    return;
+  }
+  if (w == 1) {   // a single column along the minor axis
+    for (int i = 0; i < h; ++i, x += dbx, y += dby) out[pos++] = y * W + x;
+    return;
+  }
+  int ax2 = floor_half(ax), ay2 = floor_half(ay), bx2 = floor_half(bx), by2 = floor_half(by);
+  const int w2 = std::abs(ax2 + ay2), h2 = std::abs(bx2 + by2);
+  if (2 * w > 3 * h) {   // long: two halves along the major axis
+    if ((w2 & 1) && w > 2) { ax2 += dax; ay2 += day; }
+    gilbert_rect(x, y, ax2, ay2, bx, by, W, out, pos);
+    gilbert_rect(x + ax2, y + ay2, ax - ax2, ay - ay2, bx, by, W, out, pos);
+  } else {               // squarish: up the minor half, across, back down
+    if ((h2 & 1) && h > 2) { bx2 += dbx; by2 += dby; }
+    gilbert_rect(x, y, bx2, by2, ax2, ay2, W, out, pos);
+    gilbert_rect(x + bx2, y + by2, ax, ay, bx - bx2, by - by2, W, out, pos);
+    gilbert_rect(x + (ax - dax) + (bx2 - dbx), y + (ay - day) + (by2 - dby), -bx2, -by2, -(ax - ax2),
+                 -(ay - ay2), W, out, pos);
+  }
+}
+}  // namespace
+
+// seq_to_cell of the generalized curve (x = column along the wider side first)
+void gilbert_path(int32_t grid_h, int32_t grid_w, int32_t* seq_to_cell) {
+  int pos = 0;
+  if (grid_w >= grid_h)
+    gilbert_rect(0, 0, grid_w, 0, 0, grid_h, grid_w, seq_to_cell, pos);
+  else
+    gilbert_rect(0, 0, 0, grid_h, grid_w, 0, grid_w, seq_to_cell, pos);
 }
 
 }  // namespace hla
@@ -114,11 +166,26 @@ using namespace hla;
 extern "C" hla_status hla_hilbert_index(int32_t grid_h, int32_t grid_w, int32_t* seq_to_cell,
                                         int32_t* cell_to_seq, cudaStream_t stream) {
   clear_error();
+  HLA_REQUIRE(grid_h >= 1 && grid_w >= 1 && (int64_t)grid_h * grid_w < (1ll << 30), HLA_ERR_INVALID,
+              "grid %dx%d invalid", grid_h, grid_w);
+  const int32_t N = grid_h * grid_w;
+  if (!(grid_h == grid_w && is_pow2(grid_h))) {
+    // generalized curve: built on the host once per shape, copied (synchronises `stream`)
+    if (!seq_to_cell && !cell_to_seq) return HLA_OK;
+    std::vector<int32_t> s2c(N), c2s(N);
+    gilbert_path(grid_h, grid_w, s2c.data());
+    for (int32_t s = 0; s < N; ++s) c2s[s2c[s]] = s;
+    if (seq_to_cell)
+      HLA_CUDA_TRY(cudaMemcpyAsync(seq_to_cell, s2c.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, stream));
+    if (cell_to_seq)
+      HLA_CUDA_TRY(cudaMemcpyAsync(cell_to_seq, c2s.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, stream));
+    HLA_CUDA_TRY(cudaStreamSynchronize(stream));
+    return HLA_OK;
+  }
   int log2n = 0;
   hla_status st = check_grid(grid_h, grid_w, &log2n);
   if (st != HLA_OK) return st;
   if (!seq_to_cell && !cell_to_seq) return HLA_OK;
-  const int32_t N = grid_h * grid_w;
   const int blocks = (N + 255) / 256;
   hilbert_index_kernel<<<blocks, 256, 0, stream>>>(N, log2n, seq_to_cell, cell_to_seq);
   HLA_CUDA_TRY(cudaGetLastError());

@@ -231,6 +231,7 @@ RPB_CASES = [
     ("HNA", 32, 5, 1, 2, 64, False),       # explicit permutation path
     ("WSA", 32, 8, 2, 2, 64, True),        # row-major: identity cell map
     ("WSA", 56, 7, 1, 1, 32, True),        # 56x56 (paper shape), ragged last tile
+    ("HWA", 56, 7, 1, 2, 32, True),        # generalized Hilbert 56x56 (fused), ragged last tile
 ]
 
 

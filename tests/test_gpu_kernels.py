@@ -39,6 +39,16 @@ def test_hilbert_index_bit_exact(k):
     assert np.array_equal(c2s.cpu().numpy(), ref_c2s)
 
 
+@pytest.mark.parametrize("h,w", [(56, 56), (28, 28), (14, 14), (7, 7), (96, 96), (160, 160), (16, 24), (24, 16),
+                                 (1, 9), (5, 3), (128, 256)])
+def test_generalized_hilbert_index_bit_exact(h, w):
+    """Any-shape path (host construction in libhla) == the oracle's gilbert2d."""
+    s2c, c2s = hla.hla_hilbert_index(h, w, DEV)
+    ref_s2c, ref_c2s = hilbert.hilbert_order(h, w)
+    assert np.array_equal(s2c.cpu().numpy(), ref_s2c)
+    assert np.array_equal(c2s.cpu().numpy(), ref_c2s)
+
+
 @pytest.mark.parametrize("n,B,heads,d", [(16, 1, 1, 32), (64, 3, 8, 64), (128, 2, 12, 64), (8, 2, 3, 8)])
 def test_hilbert_perm_bit_exact(n, B, heads, d):
     N = n * n

@@ -41,10 +41,12 @@ def test_argument_validation_without_gpu():
     L = _lib.lib()
     n = 1
     arr = (ctypes.c_void_p * n)(16)
-    # non-square grid -> UNSUPPORTED, checked before any CUDA call
+    # explicit permutation on a non-2^k grid -> UNSUPPORTED, checked before any CUDA call
     assert L.hla_hilbert_perm(56, 64, 0, 1, 128, 1, arr, arr, None, None) == _lib.HLA_ERR_UNSUPPORTED
-    assert L.hla_hilbert_index(48, 48, None, None, None) == _lib.HLA_ERR_UNSUPPORTED
     assert b"square" in L.hla_last_error()
+    # the index itself covers any grid (generalized curve on the host); no outputs -> no work
+    assert L.hla_hilbert_index(48, 56, None, None, None) == _lib.HLA_OK
+    assert L.hla_hilbert_index(0, 56, None, None, None) == _lib.HLA_ERR_INVALID
     # window not dividing the grid -> INVALID
     d = api.pattern_desc("WSA", 64, 64, 7, 7)
     m = _lib.BlockMaskC()
