@@ -47,6 +47,14 @@ CONFIGS = {
     "cfg4": dict(kind="HNA", rm="NA2D", grid=128, win=7, B=16, H=12, d=64,
                  text="128x128 grid, HNA 49 tokens vs NA2D 7x7, 12 heads, d64, block 128, batch 16"),
 }
+# cfg5: the HWT-T attention stack (SURVEY 8 cfg5 + 8(f) NEXT-1): Swin-T-like stages on the paper's
+# feature-map sizes (generalized Hilbert path, ragged N), HWA / HSWA blocks alternating (HWT
+# blocks come in pairs), each with HWT's global RPB, 7x7 = 49-token windows
+STACK = {"cfg5": dict(B=128, d=32, stages=[(56, 3, 2, 7), (28, 6, 2, 7), (14, 12, 6, 7), (8, 24, 2, 8)],
+                      text="HWT-T attention stack: stages 56x56/28x28/14x14/7x7->8x8 padded (N % 4 == 0 kernel "
+                           "limit) (generalized Hilbert, ragged N), "
+                           "heads 3/6/12/24, depths 2/2/6/2, B128, d32, 49-token windows (64 at the padded 8x8 stage), "
+                           "HWA/HSWA alternating (shift = half a window), global RPB, block 128")}
 # paper's row-major-block-sparse -> Hilbert fwd+bwd speedup on the nearest shape (RTX 3080)
 PAPER_SPEEDUP = {"cfg2": (2.70, "WSA(Flex)->HWA 64x64 W8, P:L150-151"),
                  "cfg3": (1.62, "SA(Flex)->HSA 64x64 K9, P:L495-496"),
@@ -59,7 +67,7 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
-    p.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    p.add_argument("--config", default="cfg2", choices=sorted(CONFIGS) + sorted(STACK))
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-variants", action="store_true", help="skip the row-major / dense comparison runs")
     p.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
@@ -230,8 +238,106 @@ def run_reference(args, cfg):
 
 
 # ------------------------------------------------------------- GPU leg
+def run_stack(args):
+    """--config cfg5: one step = fwd + bwd of every attention layer of the HWT-T stack."""
+    import torch
+    import torch.distributed as dist
+
+    import hla_synth
+    import paper_2511_05832_b200 as hla
+
+    sc = STACK[args.config]
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    B, d = sc["B"], sc["d"]
+    layers = []   # (layer, inputs) in execution order
+    for si, (g, H, depth, w) in enumerate(sc["stages"]):
+        N = g * g
+        ins = hla_synth.attention_inputs(B, N, H, d, seed=100 * rank + si, device=dev)
+        pair = [hla.HilbertLocalAttention(kind, g, g, w, w, B, H, d, shift=(w * w) // 2 if kind == "HSWA" else 0,
+                                          device=dev, rpb=True) for kind in ("HWA", "HSWA")]
+        gen = torch.Generator().manual_seed(si)
+        for lay in pair:
+            lay.rpb.copy_(torch.rand(lay.rpb.shape, generator=gen) * 2 - 1)
+        for i in range(depth):
+            layers.append((pair[i % 2], ins))
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+
+    def one_step(rec=None):
+        for lay, (q, k, v, do) in layers:
+            lay.step(q, k, v, do, rec)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    totals, per = [], {}
+    for _ in range(args.steps):
+        flush.zero_()
+        ev = [("start", torch.cuda.Event(enable_timing=True))]
+        ev[0][1].record()
+
+        def mark(name, ev=ev):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            ev.append((name, e))
+        one_step(mark)
+        totals.append(ev)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    step = []
+    for ev in totals:
+        step.append(ev[0][1].elapsed_time(ev[-1][1]))
+        for (_, a), (name, b) in zip(ev[:-1], ev[1:]):
+            per[name] = per.get(name, 0.0) + a.elapsed_time(b) / args.steps
+    step_ms = reduce_max_ms(statistics.mean(step), dist if world > 1 else None, dev)
+    peaks = load_peaks()
+    # roofline of the stack's dominant kernel (sum over layers): algorithmic bytes / summed time
+    tb = {"fwd": 0, "bwd": 0}
+    for lay, (q, _, _, _) in layers:
+        T = q.shape[0] * q.shape[1] * q.shape[2]
+        tb["fwd"] += T * (8 * d + 4)
+        tb["bwd"] += T * (20 * d + 8)
+    dom = max(("fwd", "bwd"), key=lambda kk: per[kk])
+    ach = tb[dom] / (per[dom] * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm"], "unit": "GB/s",
+            "frac": round(ach / peaks["hbm"], 4), "kernel": "attn_%s_kernel" % dom, "stage": dom,
+            "share_of_step": round(per[dom] / statistics.mean(step), 4), "traffic": None,
+            "note": "summed over the %d attention layers of the stack" % len(layers), "peak_source": peaks["source"]}
+    line = {"metric": METRIC, "value": round(job_value(step_ms, world), 4), "unit": "ms", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic: hla_synth splitmix64 uniform, unit variance, bf16 (no dataset)",
+            "config": {"workload": args.config + ": " + sc["text"], "global_batch": B * world,
+                       "layers": len(layers), "parallelism": "dp%d" % world,
+                       "l2": "flushed between timed steps (%d MiB write, untimed)" % (L2_FLUSH_BYTES >> 20)},
+            "clocks": clocks, "e2e": None,
+            "gpu_launches": sum(lay.launches_per_step for lay, _ in layers) * args.steps,
+            "roofline": roof, "cpu_baseline": None,
+            "breakdown_ms": {kk: round(vv, 4) for kk, vv in per.items()}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
+    if args.config in STACK:
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "the oracle leg covers cfg1-cfg4 only"}))
+            return
+        run_stack(args)
+        return
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
@@ -312,6 +418,14 @@ def main():
             variants[name]["tensor_pct_executed"] = round(
                 100 * exec_flops / ((st["fwd"] + st["bwd"]) * 1e-3) / (peaks["tf_sus"] * 1e12), 2)
             del lay
+        # HWT's global relative position bias on the same layer (reading R19)
+        lay = hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, B, H, d, device=dev, rpb=True)
+        lay.rpb.copy_(torch.rand(lay.rpb.shape, generator=torch.Generator().manual_seed(1)) * 2 - 1)
+        tot, st, _ = timed(lay, vsteps, 2, True)
+        variants["global_rpb"] = {"pattern": cfg["kind"] + " + global RPB score_mod",
+                                  "ms_per_step": round(statistics.mean(tot), 4), "fwd_ms": round(st["fwd"], 4),
+                                  "bwd_ms": round(st["bwd_pre"] + st["bwd"] + st["bwd_fin"], 4)}
+        del lay
         ours_attn = stages["fwd"] + stages["bwd_pre"] + stages["bwd"] + stages["bwd_fin"]
         rm = variants["row_major"]
         rm_attn = rm["fwd_ms"] + rm["bwd_ms"]

@@ -57,7 +57,13 @@ struct BwdParams {
   unsigned long long* visited;
 };
 
-constexpr int kRpbWin = 2048;   // fp32 entries of the per-tile dRPB window (offset box) in shared memory
+constexpr int kRpbWin = 2048;   // entries of the per-tile dRPB window (offset box) in shared memory
+// The window accumulates in 32-bit fixed point: shared-memory fp32 atomics are
+// compare-and-swap loops on sm_100 (ATOMS.CAST.SPIN, measured in SASS) while
+// integer ATOMS.ADD is native.  Resolution 2^-16 (absolute; dS values are
+// O(1e-2..1)), each addend saturated at +-2^14 so a tile's sum per offset (at most
+// 128 pairs) cannot overflow; converted back to fp32 when the window is flushed.
+constexpr float kRpbFix = 65536.f;
 
 template <int D, bool kBias = false>
 struct BwdSmem {
@@ -73,7 +79,7 @@ struct BwdSmem {
   uint64_t kv_full[2], kv_empty[2], q_full[2], q_empty[2], s_full[2], ds_ready[2], dq_full, dq_free, dkv_full, epi_done;
   uint64_t dbg_bar;
   uint32_t tmem_base;
-  float rpb_win[kBias ? kRpbWin : 1];   // dRPB of the current tile's offset box (compute warps)
+  int32_t rpb_win[kBias ? kRpbWin : 1];   // dRPB of the current tile's offset box, fixed point (compute warps)
 };
 
 template <int D>
@@ -421,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = prm.scale_log2, scale = prm.scale;
     if (kBias) {   // the dRPB window starts (and is left after every flush) zeroed
-      for (int i = (warp - 2) * 32 + lane; i < kRpbWin; i += 256) sm.rpb_win[i] = 0.f;
+      for (int i = (warp - 2) * 32 + lane; i < kRpbWin; i += 256) sm.rpb_win[i] = 0;
       sm100::named_bar_sync(3, 256);
     }
     uint32_t n = 0, g = 0;
@@ -545,10 +551,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                   if (!((okbits >> (u4 * 8 + e)) & 1u)) continue;
                   const int32_t dr = (rc >> 16) - k_r, dc = (rc & 0xffff) - k_c;
                   const float gv = ds[e] * prm.inv_scale;
-                  if (win)
-                    atomicAdd(&sm.rpb_win[(dr - dr0) * wc + (dc - dc0)], gv);
-                  else
+                  if (win) {
+                    const int32_t fx = __float2int_rn(fminf(fmaxf(gv, -16384.f), 16384.f) * kRpbFix);
+                    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(sm100::smem_u32(&sm.rpb_win[(dr - dr0) * wc + (dc - dc0)])),
+                                 "r"(fx)
+                                 : "memory");
+                  } else {
                     atomicAdd(drpbh + (dr + prm.grid_h - 1) * prm.rpb_w + (dc + prm.grid_w - 1), gv);
+                  }
                 }
               }
               // dS^T row -> smem [q/64][kv][64] with the 128B swizzle (16B chunks)
@@ -570,11 +580,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int tid = (warp - 2) * 32 + lane;
           const int wr = kRpbWin / wc;
           for (int i = tid; i < wr * wc; i += 256) {
-            const float v = sm.rpb_win[i];
-            if (v != 0.f) {
+            const int32_t v = sm.rpb_win[i];
+            if (v != 0) {
               const int32_t dr = dr0 + i / wc, dc = dc0 + i % wc;
-              atomicAdd(drpbh + (dr + prm.grid_h - 1) * prm.rpb_w + (dc + prm.grid_w - 1), v);
-              sm.rpb_win[i] = 0.f;
+              atomicAdd(drpbh + (dr + prm.grid_h - 1) * prm.rpb_w + (dc + prm.grid_w - 1), (float)v * (1.f / kRpbFix));
+              sm.rpb_win[i] = 0;
             }
           }
           sm100::named_bar_sync(3, 256);
