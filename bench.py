@@ -76,6 +76,15 @@ def parse():
 
 
 # ------------------------------------------------------------------ helpers
+def bwd_bytes(T, d, mask):
+    """Algorithmic HBM bytes of attn_bwd_kernel per launch: read Q, K, V, dO (8d per token-head),
+    LSE, D (8); write dK, dV (4d); dQ: bf16 write (2d) for the q-blocks the dQ plan keeps
+    local, one fp32 read + write of the accumulator (8d, TMA reduce-add) for the others."""
+    mq = mask.row_ptr.numel() - 1
+    nl = mq if mask.n_dq_nonlocal < 0 else mask.n_dq_nonlocal
+    return int(T * (12 * d + 8) + T * (2 * d * (mq - nl) + 8 * d * nl) // mq)
+
+
 def reduce_max_ms(ms, dist=None, device=None):
     """Max of a per-rank time over all ranks (the contract's max-over-ranks rule)."""
     import torch
@@ -305,7 +314,7 @@ def run_stack(args):
     for lay, (q, _, _, _) in layers:
         T = q.shape[0] * q.shape[1] * q.shape[2]
         tb["fwd"] += T * (8 * d + 4)
-        tb["bwd"] += T * (20 * d + 8)
+        tb["bwd"] += bwd_bytes(T, d, lay.mask)
     dom = max(("fwd", "bwd"), key=lambda kk: per[kk])
     ach = tb[dom] / (per[dom] * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm"], "unit": "GB/s",
@@ -470,7 +479,7 @@ def main():
     tiles = layer.nnz * B * H
     kern = {
         "fwd": {"bytes": T * (8 * d + 4), "flops": 4 * 128 * 128 * d * tiles, "name": "attn_fwd_kernel"},
-        "bwd": {"bytes": T * (20 * d + 8), "flops": 10 * 128 * 128 * d * tiles, "name": "attn_bwd_kernel"},
+        "bwd": {"bytes": bwd_bytes(T, d, layer.mask), "flops": 10 * 128 * 128 * d * tiles, "name": "attn_bwd_kernel"},
         "perm_qkv": {"bytes": 3 * 2 * T * d * 2, "flops": 0, "name": "hilbert_perm_kernel"},
         "perm_grads": {"bytes": 3 * 2 * T * d * 2, "flops": 0, "name": "hilbert_perm_kernel"},
     }

@@ -110,7 +110,25 @@ typedef struct {
   int32_t* t_col_idx;            /* [capacity]                                     */
   uint8_t* t_kind;               /* [capacity]                                     */
   int64_t* counts;               /* [4]: nnz, n_full, n_partial, n_empty           */
+  /* Optional backward dQ plan (hla_build_bwd_plan).  In effect only when t_dq and
+     q_dq_local are non-NULL and n_dq_nonlocal >= 0 (zero-initialised = no plan). */
+  uint8_t* t_dq;                 /* [capacity] per transposed entry: HLA_DQ_* bits  */
+  uint8_t* q_dq_local;           /* [n_qblocks] 1 = dQ rows written by bwd_main     */
+  int32_t n_dq_nonlocal;         /* host: q-blocks with q_dq_local == 0 (-1: none)  */
 } hla_block_mask;
+
+/* Bits of hla_block_mask.t_dq.  The backward walks the transposed lists in work
+ * units of two kv-blocks (2p, 2p+1) of one (batch, head); inside a unit the dQ_i
+ * partial products of consecutive tiles with the same q-block i are chained in
+ * one of two TMEM accumulators instead of being reduced into the fp32 workspace
+ * one tile at a time.  A chain that covers q-block i's whole forward list is
+ * the finished dQ_i and is written to dq directly (bf16). */
+enum {
+  HLA_DQ_BUF = 1,       /* TMEM dQ accumulator (0 / 1) of the tile's chain          */
+  HLA_DQ_NEW = 2,       /* first tile of its chain (the dQ MMA overwrites)          */
+  HLA_DQ_DRAIN = 4,     /* last tile of its chain (the accumulator is drained)      */
+  HLA_DQ_LOCAL = 8      /* drained chain = complete dQ_i: written to dq as bf16     */
+};
 
 /* ---------------------------------------------------------------------------
  * hla_hilbert_index -- the cached Hilbert path: seq_to_cell[s] = cell
@@ -154,6 +172,20 @@ HLA_API hla_status hla_hilbert_perm(int32_t grid_h, int32_t grid_w, int32_t dir,
  */
 HLA_API hla_status hla_build_block_mask(const hla_pattern_desc* d, hla_block_mask* m,
                                 int64_t* nnz_out, cudaStream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * hla_build_bwd_plan -- the backward's dQ chaining plan of a filled mask (fill
+ * call of hla_build_block_mask done; block_q == block_k).  Writes m->t_dq
+ * ([capacity] bytes, HLA_DQ_* bits per transposed entry) and m->q_dq_local
+ * ([n_qblocks] bytes), both caller-allocated device arrays, and sets the host
+ * field m->n_dq_nonlocal.  Synchronises `stream`.  Not on the per-step path
+ * (built once per mask).  The plan changes only how dQ partial products are
+ * summed (fewer fp32 reductions; P:L85 block-sparse structure), never which
+ * products are summed.  Chains never cross a work unit; within a unit each
+ * accumulator holds one chain at a time (a chain that would need a busy
+ * accumulator is drained early through the fp32 workspace instead).
+ */
+HLA_API hla_status hla_build_bwd_plan(hla_block_mask* m, cudaStream_t stream);
 
 /* Host helper: the two sparsity ratios of a built mask from its integer counts
  * (host copy of m->counts): empty_tile_ratio = n_empty / (Mq*Mk); sparsity =
@@ -224,7 +256,9 @@ HLA_API hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_mask*
  * forward.  workspace: device memory of at least hla_attn_bwd_workspace(...)
  * bytes, 256-byte aligned (fp32 dQ accumulator + D); its contents need not be
  * initialised.  dQ accumulation uses fp32 TMA reduce-adds (summation order is
- * not deterministic; covered by the stated tolerance).  Same limits as the forward.
+ * not deterministic; covered by the stated tolerance), except for the q-blocks
+ * the mask's optional dQ plan (hla_build_bwd_plan) marks local, whose dQ is
+ * summed in TMEM and written directly.  Same limits as the forward.
  * seq_to_cell: as in hla_attn_fwd (fused reorder: every bf16 tensor in grid order).
  * score_mod: as in hla_attn_fwd (same table); with global RPB, drpb receives the
  * table gradient (accumulated; hla_attn_bwd zeroes it first, hla_attn_bwd_main
@@ -242,27 +276,32 @@ HLA_API hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_mask*
 /* The three stages of hla_attn_bwd, callable separately (SURVEY 8(a) rows a6,
  * a7, a8) so they can be timed / overlapped individually.  Same arguments and
  * limits as hla_attn_bwd; the workspace carries D and the fp32 dQ accumulator
- * from one stage to the next and must not be touched in between.
+ * from one stage to the next and must not be touched in between.  All three
+ * must see the same mask plan (plan_mask = the mask given to main; NULL or a
+ * mask without plan = every q-block through the fp32 accumulator).
  *   preprocess: D = rowsum(dO o O) (fp32, stored x scale), LSE -> log2 domain,
- *               dQ accumulator := 0 (all into the workspace)
- *   main      : the tcgen05 kernel over the transposed lists; writes dK, dV and
- *               accumulates dQ (fp32, TMA reduce-add, sequence order)
- *   finalize  : dQ = bf16(accumulator), written to grid cells when seq_to_cell
- *               is given (fused inverse reorder)                              */
+ *               dQ accumulator := 0 for the q-blocks that are not local
+ *   main      : the tcgen05 kernel over the transposed lists; writes dK, dV,
+ *               writes dQ of local q-blocks (bf16) and accumulates the others
+ *               (fp32, TMA reduce-add, sequence order)
+ *   finalize  : dQ = bf16(accumulator) of the non-local q-blocks, written to
+ *               grid cells when seq_to_cell is given (fused inverse reorder);
+ *               launches nothing when the plan has no non-local q-block      */
 HLA_API hla_status hla_attn_bwd_preprocess(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,
                                    float scale, const void* o, const void* dout, const float* lse,
-                                   const int32_t* seq_to_cell,
+                                   const int32_t* seq_to_cell, const hla_block_mask* plan_mask,
                                    void* workspace, size_t workspace_bytes, cudaStream_t stream);
 HLA_API hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_block_mask* m,
                              int32_t batch, int32_t heads, int32_t head_dim, float scale,
                              const void* q, const void* k, const void* v,
-                             const void* dout, void* dk, void* dv, const int32_t* seq_to_cell,
+                             const void* dout, void* dq, void* dk, void* dv, const int32_t* seq_to_cell,
                              const hla_score_mod* score_mod,
                              void* workspace, size_t workspace_bytes,
                              int64_t* tiles_visited, cudaStream_t stream);
 HLA_API hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,
                                  const void* workspace, size_t workspace_bytes, void* dq,
-                                 const int32_t* seq_to_cell, cudaStream_t stream);
+                                 const int32_t* seq_to_cell, const hla_block_mask* plan_mask,
+                                 cudaStream_t stream);
 
 HLA_API size_t hla_attn_bwd_workspace(int32_t batch, int32_t heads, int32_t n, int32_t head_dim);
 

@@ -17,7 +17,7 @@ STATUS_NAMES = {0: "HLA_OK", 1: "HLA_ERR_INVALID", 2: "HLA_ERR_UNSUPPORTED", 3: 
 # exported symbols of include/hla.h and include/hla_debug.h
 EXPORTED = ("hla_hilbert_index", "hla_hilbert_perm", "hla_build_block_mask", "hla_mask_ratios",
             "hla_attn_fwd", "hla_attn_bwd", "hla_attn_bwd_workspace", "hla_attn_bwd_preprocess",
-            "hla_attn_bwd_main", "hla_attn_bwd_finalize", "hla_last_error", "hla_version",
+            "hla_attn_bwd_main", "hla_attn_bwd_finalize", "hla_build_bwd_plan", "hla_last_error", "hla_version",
             "hla_debug_umma", "hla_debug_gather4", "hla_debug_mma_rate",
             "hla_debug_tmem_rate", "hla_debug_ex2_rate",
             "hla_debug_softmax_rate", "hla_debug_softmax_tile", "hla_debug_load_rate")
@@ -39,7 +39,8 @@ class BlockMaskC(ctypes.Structure):
     _fields_ = [("n_qblocks", ctypes.c_int32), ("n_kblocks", ctypes.c_int32), ("capacity", ctypes.c_int64),
                 ("row_ptr", ctypes.c_void_p), ("col_idx", ctypes.c_void_p), ("kind", ctypes.c_void_p),
                 ("t_row_ptr", ctypes.c_void_p), ("t_col_idx", ctypes.c_void_p), ("t_kind", ctypes.c_void_p),
-                ("counts", ctypes.c_void_p)]
+                ("counts", ctypes.c_void_p),
+                ("t_dq", ctypes.c_void_p), ("q_dq_local", ctypes.c_void_p), ("n_dq_nonlocal", ctypes.c_int32)]
 
 
 class HlaError(RuntimeError):
@@ -69,9 +70,10 @@ def lib():
         "hla_attn_fwd": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp],
         "hla_attn_bwd": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp,
                          vp],
-        "hla_attn_bwd_preprocess": [i32, i32, i32, i32, f32, vp, vp, vp, vp, vp, sz, vp],
-        "hla_attn_bwd_main": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp],
-        "hla_attn_bwd_finalize": [i32, i32, i32, i32, vp, sz, vp, vp, vp],
+        "hla_attn_bwd_preprocess": [i32, i32, i32, i32, f32, vp, vp, vp, vp, pmask, vp, sz, vp],
+        "hla_attn_bwd_main": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp],
+        "hla_attn_bwd_finalize": [i32, i32, i32, i32, vp, sz, vp, vp, pmask, vp],
+        "hla_build_bwd_plan": [pmask, vp],
         "hla_debug_umma": [vp, vp, vp, i32, i32, i32, i32, i32, i32, vp],
         "hla_debug_gather4": [vp, i64, i32, i32, vp, i32, i32, vp, vp],
         "hla_debug_mma_rate": [i32, i32, i32, i32, i32, vp, vp],

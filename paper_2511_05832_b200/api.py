@@ -55,13 +55,16 @@ class BlockMask:
     t_kind: torch.Tensor
     counts: torch.Tensor          # device int64[4]: nnz, n_full, n_partial, n_empty
     host_counts: tuple = None
+    t_dq: torch.Tensor = None     # backward dQ plan (hla_build_bwd_plan): uint8 per transposed entry
+    q_dq_local: torch.Tensor = None   # uint8 per q-block: 1 = dQ written by the main backward kernel
+    n_dq_nonlocal: int = -1
 
     @property
     def c(self):
         return BlockMaskC(self.row_ptr.numel() - 1, self.t_row_ptr.numel() - 1, self.col_idx.numel(),
                           self.row_ptr.data_ptr(), self.col_idx.data_ptr(), self.kind.data_ptr(),
                           self.t_row_ptr.data_ptr(), self.t_col_idx.data_ptr(), self.t_kind.data_ptr(),
-                          self.counts.data_ptr())
+                          self.counts.data_ptr(), _dp(self.t_dq), _dp(self.q_dq_local), self.n_dq_nonlocal)
 
     @property
     def nnz(self):
@@ -73,6 +76,10 @@ class BlockMask:
         e, s = ctypes.c_double(), ctypes.c_double()
         check("hla_mask_ratios", lib().hla_mask_ratios(ctypes.byref(self.desc), cnt, ctypes.byref(e), ctypes.byref(s)))
         return e.value, s.value
+
+
+def _dp(t):
+    return t.data_ptr() if t is not None else None
 
 
 def hla_hilbert_index(grid_h, grid_w, device="cuda", stream=None):
@@ -101,8 +108,9 @@ def hla_hilbert_perm(grid_h, grid_w, direction, srcs, dsts=None, stream=None):
     return dsts
 
 
-def hla_build_block_mask(desc, device="cuda", stream=None):
-    """Sizing call, then fill call (both synchronous; built once per shape)."""
+def hla_build_block_mask(desc, device="cuda", stream=None, plan=True):
+    """Sizing call, then fill call (both synchronous; built once per shape); then
+    (plan=True, square tiles) the backward's dQ plan."""
     N = desc.grid_h * desc.grid_w
     mq = (N + desc.block_q - 1) // desc.block_q
     mk = (N + desc.block_k - 1) // desc.block_k
@@ -124,7 +132,20 @@ def hla_build_block_mask(desc, device="cuda", stream=None):
     check("hla_build_block_mask", lib().hla_build_block_mask(ctypes.byref(desc), ctypes.byref(c), ctypes.byref(nnz),
                                                              _stream(stream)))
     m.host_counts = tuple(int(x) for x in m.counts.cpu().tolist())
+    if plan and desc.block_q == desc.block_k:
+        hla_build_bwd_plan(m, stream)
     return m
+
+
+def hla_build_bwd_plan(mask, stream=None):
+    """The backward's dQ chaining plan of a filled mask (synchronous; once per mask)."""
+    dev = mask.row_ptr.device
+    mask.t_dq = torch.zeros(max(1, mask.col_idx.numel()), dtype=torch.uint8, device=dev)
+    mask.q_dq_local = torch.zeros(mask.row_ptr.numel() - 1, dtype=torch.uint8, device=dev)
+    c = mask.c
+    check("hla_build_bwd_plan", lib().hla_build_bwd_plan(ctypes.byref(c), _stream(stream)))
+    mask.n_dq_nonlocal = int(c.n_dq_nonlocal)
+    return mask
 
 
 def score_mod(rpb=None, drpb=None, cells=None):
@@ -185,29 +206,39 @@ def hla_attn_bwd(desc, mask, q, k, v, o, lse, dout, scale=0.0, dq=None, dk=None,
     return dq, dk, dv
 
 
-def hla_attn_bwd_preprocess(o, dout, lse, workspace, scale=0.0, seq_to_cell=None, stream=None):
+def _pm(mask):
+    return ctypes.byref(mask.c) if mask is not None else None
+
+
+def hla_attn_bwd_preprocess(o, dout, lse, workspace, scale=0.0, seq_to_cell=None, stream=None, mask=None):
+    """mask: the mask whose dQ plan hla_attn_bwd_main will use (None = no plan)."""
     B, N, H, D = o.shape
     check("hla_attn_bwd_preprocess", lib().hla_attn_bwd_preprocess(B, H, N, D, float(scale), _ptr(o), _ptr(dout),
-                                                                   _ptr(lse), _ptr(seq_to_cell), _ptr(workspace),
-                                                                   workspace.numel(), _stream(stream)))
+                                                                   _ptr(lse), _ptr(seq_to_cell), _pm(mask),
+                                                                   _ptr(workspace), workspace.numel(),
+                                                                   _stream(stream)))
 
 
-def hla_attn_bwd_main(desc, mask, q, k, v, dout, dk, dv, workspace, scale=0.0, tiles_visited=None,
+def hla_attn_bwd_main(desc, mask, q, k, v, dout, dq, dk, dv, workspace, scale=0.0, tiles_visited=None,
                       seq_to_cell=None, stream=None, mod=None):
     """Requires hla_attn_bwd_preprocess to have filled `workspace` (D, LSE in log2 domain).
-    With a global-RPB mod, the table gradient is ACCUMULATED into mod's drpb."""
+    dq receives the rows of the q-blocks the mask's dQ plan marks local (the others come
+    from hla_attn_bwd_finalize).  With a global-RPB mod, the table gradient is ACCUMULATED
+    into mod's drpb."""
     B, N, H, D = q.shape
     mc = mask.c
     check("hla_attn_bwd_main", lib().hla_attn_bwd_main(ctypes.byref(desc), ctypes.byref(mc), B, H, D, float(scale),
-                                                       _ptr(q), _ptr(k), _ptr(v), _ptr(dout), _ptr(dk),
+                                                       _ptr(q), _ptr(k), _ptr(v), _ptr(dout), _ptr(dq), _ptr(dk),
                                                        _ptr(dv), _ptr(seq_to_cell), _sm(mod), _ptr(workspace),
                                                        workspace.numel(), _ptr(tiles_visited), _stream(stream)))
 
 
-def hla_attn_bwd_finalize(workspace, dq, seq_to_cell=None, stream=None):
+def hla_attn_bwd_finalize(workspace, dq, seq_to_cell=None, stream=None, mask=None):
+    """mask: the mask whose dQ plan hla_attn_bwd_main used (None = no plan)."""
     B, N, H, D = dq.shape
     check("hla_attn_bwd_finalize", lib().hla_attn_bwd_finalize(B, H, N, D, _ptr(workspace), workspace.numel(),
-                                                               _ptr(dq), _ptr(seq_to_cell), _stream(stream)))
+                                                               _ptr(dq), _ptr(seq_to_cell), _pm(mask),
+                                                               _stream(stream)))
 
 
 def hla_debug_umma(A, B, M, N, K, a_mn=False, b_mn=False, a_tmem=False, stream=None):

@@ -19,6 +19,11 @@ and scatter O / dK / dV / dQ rows back to their grid cells, so a step is
 fwd ; bwd_pre ; bwd ; bwd_fin with no permutation passes.  fused=False keeps the
 explicit hla_hilbert_perm passes (the paper's "Reshape" step).
 
+dq_plan=True (default) also builds the backward's dQ chaining plan with the mask
+(hla_build_bwd_plan): dQ partials of a kv-block pair are summed in TMEM, and q-blocks
+whose whole kv list lies in one pair get their dQ written by the main backward kernel
+(no fp32 accumulator traffic, no finalize pass when that holds for all of them).
+
 rpb=True adds HWT's global relative position bias (reading R19): a table
 `self.rpb` fp32 [heads, 2H-1, 2W-1] (zero-initialised; set it as a parameter)
 whose gradient is written to `self.drpb` by backward() (one memset + the
@@ -32,14 +37,14 @@ from . import api
 
 class HilbertLocalAttention:
     def __init__(self, kind, grid_h, grid_w, win_h=1, win_w=1, batch=1, heads=1, head_dim=64, block=128,
-                 shift=0, scale=0.0, device="cuda", fused=True, rpb=False):
+                 shift=0, scale=0.0, device="cuda", fused=True, rpb=False, dq_plan=True):
         self.kind = kind
         self.grid_h, self.grid_w = grid_h, grid_w
         self.N = grid_h * grid_w
         self.shape = (batch, self.N, heads, head_dim)
         self.scale = float(scale)
         self.desc = api.pattern_desc(kind, grid_h, grid_w, win_h, win_w, block, shift)
-        self.mask = api.hla_build_block_mask(self.desc, device)
+        self.mask = api.hla_build_block_mask(self.desc, device, plan=dq_plan)   # + the backward's dQ plan
         self.hilbert = api.is_hilbert(self.desc)
         bf = dict(dtype=torch.bfloat16, device=device)
         e = lambda: torch.empty(self.shape, **bf)   # noqa: E731
@@ -106,14 +111,15 @@ class HilbertLocalAttention:
             dout_s, dq, dk, dv = self.dos, self.dqs, self.dks, self.dvs
         else:
             dout_s, dq, dk, dv = dout, self.dq, self.dk, self.dv
-        api.hla_attn_bwd_preprocess(o, dout_s, self.lse, self.workspace, self.scale, seq_to_cell=self.s2c)
+        api.hla_attn_bwd_preprocess(o, dout_s, self.lse, self.workspace, self.scale, seq_to_cell=self.s2c,
+                                    mask=self.mask)
         if self.drpb is not None:
             self.drpb.zero_()      # the kernel accumulates the table gradient
         mark("bwd_pre")
-        api.hla_attn_bwd_main(self.desc, self.mask, q, k, v, dout_s, dk, dv, self.workspace, self.scale,
+        api.hla_attn_bwd_main(self.desc, self.mask, q, k, v, dout_s, dq, dk, dv, self.workspace, self.scale,
                               seq_to_cell=self.s2c, mod=self.mod)
         mark("bwd")
-        api.hla_attn_bwd_finalize(self.workspace, dq, seq_to_cell=self.s2c)
+        api.hla_attn_bwd_finalize(self.workspace, dq, seq_to_cell=self.s2c, mask=self.mask)
         mark("bwd_fin")
         if self.hilbert and not self.fused:
             api.hla_hilbert_perm(self.grid_h, self.grid_w, api.FROM_HILBERT, (self.dqs, self.dks, self.dvs),
@@ -124,7 +130,8 @@ class HilbertLocalAttention:
     # kernel launches per step (forward + backward)
     @property
     def launches_per_step(self):
-        return (8 if (self.hilbert and not self.fused) else 4) + (1 if self.rpb is not None else 0)
+        fin = 0 if self.mask.n_dq_nonlocal == 0 else 1   # the finalize launches nothing when every dQ is local
+        return 3 + fin + (4 if (self.hilbert and not self.fused) else 0) + (1 if self.rpb is not None else 0)
 
     def step(self, q, k, v, dout, mark=None):
         """One pass of the whole hot path: forward then backward."""

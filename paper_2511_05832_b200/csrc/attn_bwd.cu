@@ -14,14 +14,17 @@
 //    warp 1     TMEM allocator + single-thread tcgen05.mma issuer:
 //                 S^T  = K_j Q_i^T     (SS, TMEM cols [0,128))
 //                 dP^T = V_j dO_i^T    (SS, TMEM cols [128,256))
-//                 dV  += P^T dO_i      (TS, P^T bf16 in TMEM cols [256,320); acc [384,448))
+//                 dV  += P^T dO_i      (TS, P^T bf16 written over the first 16 columns of
+//                                       each 32-column S^T chunk; acc [384,448))
 //                 dK  += dS^T Q_i      (SS, dS^T bf16 in smem, K-major view; acc [448,512))
-//                 dQ_i = dS K_j        (SS, same dS smem, MN-major view; TMEM [320,384))
+//                 dQ_i (+)= dS K_j     (SS, same dS smem, MN-major view; two accumulators
+//                                       [256,320) / [320,384) chained by the mask's dQ plan)
 //    warps 2-9  thread = key row (two warps per TMEM lane quarter, one 32-column
 //               chunk each): P^T, dS^T from S^T, dP^T (mask only on partial
 //               tiles); final dK (warps 6-9), dV (warps 2-5) -> bf16;
-//    warps 10-13 thread = query row: dQ_i partial -> smem -> TMA reduce-add into
-//               the fp32 accumulator (overlaps the next q-block's MMAs).
+//    warps 10-13 thread = query row: at the end of a dQ chain, dQ_i -> bf16 dq rows
+//               (complete chains) or -> smem -> TMA reduce-add into the fp32
+//               accumulator (overlaps the next q-block's MMAs).
 // K9 dq_finalize    : fp32 accumulator -> bf16 dQ.
 #include "predicates.cuh"
 #include "sm100.cuh"
@@ -33,7 +36,7 @@ namespace {
 constexpr int kBlock = 128;
 constexpr int kThreads = 512;   // 16 warps: TMA, MMA, 8 x P/dS, 4 x dQ, 2 x TMA
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kColS = 0, kColDP = 128, kColP = 256, kColDQ = 320, kColDV = 384, kColDK = 448;
+constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256, kColDV = 384, kColDK = 448;   // dQ: 2 x 64 columns
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kHalf = 64;   // q-columns per pipeline half
 
@@ -44,6 +47,7 @@ struct BwdParams {
   const int32_t* t_row_ptr;
   const int32_t* t_col_idx;
   const uint8_t* t_kind;
+  const uint8_t* t_dq;     // dQ chaining plan per transposed entry (HLA_DQ_*; null = one chain per tile)
   const float* lse2;       // LSE * log2(e), [B, H, N] (workspace, from the preprocess)
   const float* dsum;       // D * scale, [B, H, N] (workspace, from the preprocess)
   float* dq_acc;           // [B, N, H, Dh] fp32 (grid order when s2c != null)
@@ -54,6 +58,7 @@ struct BwdParams {
   int32_t grid_h, grid_w, rpb_w, rpb_hw;
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;
+  __nv_bfloat16* dq;       // dQ rows of LOCAL chains (bf16, same layout as dk)
   unsigned long long* visited;
 };
 
@@ -76,7 +81,8 @@ struct BwdSmem {
   alignas(1024) float dq_stage[kBlock * 32];    // fp32 dQ half tile [128][32], SWIZZLE_128B
   alignas(16) float lse[2][kBlock];
   alignas(16) float dd[2][kBlock];
-  uint64_t kv_full[2], kv_empty[2], q_full[2], q_empty[2], s_full[2], ds_ready[2], dq_full, dq_free, dkv_full, epi_done;
+  uint64_t kv_full[2], kv_empty[2], q_full[2], q_empty[2], s_full[2], ds_ready[2], dq_full[2], dq_free[2], dkv_full,
+      epi_done;
   uint64_t dbg_bar;
   uint32_t tmem_base;
   int32_t rpb_win[kBias ? kRpbWin : 1];   // dRPB of the current tile's offset box, fixed point (compute warps)
@@ -102,39 +108,58 @@ __device__ __forceinline__ uint64_t ds_mnmajor_desc(const uint8_t* ds, int kstep
   return sm100::make_smem_desc(sm100::smem_u32(ds) + kstep * 2048, 16384, 1024, sm100::kSwizzle128B);
 }
 
-// k-th work unit of this CTA: pairs of consecutive kv-blocks (2p, 2p+1), pairs
-// strided over the grid.  Consecutive kv-blocks share q-blocks (the producer then
-// skips reloading a Q/dO stage), while all CTAs stay on nearby units (L2 reuse).
-__device__ __forceinline__ int32_t unit_at(int32_t k) {
-  return 2 * ((int32_t)blockIdx.x + (k >> 1) * (int32_t)gridDim.x) + (k & 1);
+// Work units are pairs (2p, 2p+1) of kv-blocks of one (b, h) -- the unit of the dQ
+// plan (hla_build_bwd_plan) -- strided over the grid.  Consecutive kv-blocks share
+// q-blocks (the producer then skips reloading a Q/dO stage, and dQ partials chain in
+// TMEM), while all CTAs stay on nearby units (L2 reuse).
+constexpr int32_t kUnitEnd = 0x7fffffff, kUnitSkip = -1;
+struct UnitGeom {
+  int32_t mk, ppb, pairs;   // kv-blocks per (b, h), pairs per (b, h), pairs in total
+};
+// k-th kv-block of this CTA: flattened u = (b * heads + h) * mk + kb, kUnitSkip for
+// the missing second block of a ragged last pair, kUnitEnd past the last pair
+__device__ __forceinline__ int32_t unit_at(int32_t k, const UnitGeom& ug) {
+  const int32_t P = (int32_t)blockIdx.x + (k >> 1) * (int32_t)gridDim.x;
+  if (P >= ug.pairs) return kUnitEnd;
+  const int32_t bh = P / ug.ppb;
+  const int32_t kb = 2 * (P - bh * ug.ppb) + (k & 1);
+  return kb < ug.mk ? bh * ug.mk + kb : kUnitSkip;
 }
 
 // Iterator over the flattened (work unit, q-block tile) sequence of this CTA,
 // skipping units without tiles.  n = ordinal of the current non-empty unit.
 struct TileIter {
-  int32_t k, u, t, nt;
+  int32_t k, u, t, nt, rs;
   uint32_t n;
   bool valid;
-  __device__ void seek(const int32_t* t_row_ptr, int32_t mk, int32_t units) {
+  __device__ void seek(const int32_t* t_row_ptr, const UnitGeom& ug) {
     for (;; ++k) {
-      u = unit_at(k);
-      if (u >= units) break;
-      const int32_t kb = u % mk;
-      nt = __ldg(t_row_ptr + kb + 1) - __ldg(t_row_ptr + kb);
+      u = unit_at(k, ug);
+      if (u == kUnitEnd) break;
+      if (u < 0) continue;
+      const int32_t kb = u % ug.mk;
+      rs = __ldg(t_row_ptr + kb);
+      nt = __ldg(t_row_ptr + kb + 1) - rs;
       if (nt > 0) { valid = true; return; }
     }
     valid = false;
   }
-  __device__ void init(const int32_t* t_row_ptr, int32_t mk, int32_t units) {
+  __device__ void init(const int32_t* t_row_ptr, const UnitGeom& ug) {
     k = 0; t = 0; n = 0;
-    seek(t_row_ptr, mk, units);
+    seek(t_row_ptr, ug);
   }
-  __device__ void advance(const int32_t* t_row_ptr, int32_t mk, int32_t units) {
+  __device__ void advance(const int32_t* t_row_ptr, const UnitGeom& ug) {
     if (++t < nt) return;
     t = 0; ++n; ++k;
-    seek(t_row_ptr, mk, units);
+    seek(t_row_ptr, ug);
   }
 };
+
+// dQ plan bits of the g-th tile (transposed entry e); without a plan every tile is
+// its own chain, alternating between the two accumulators
+__device__ __forceinline__ uint32_t dq_plan(const uint8_t* t_dq, int32_t e, uint32_t g) {
+  return t_dq ? (uint32_t)__ldg(t_dq + e) : ((g & 1u) | HLA_DQ_NEW | HLA_DQ_DRAIN);
+}
 
 // Load the 128 token rows [seq0, seq0 + 128) (sequence order) of head h, batch b;
 // see attn_fwd.cu load_rows (kGather = fused reorder through s2c with .tile::gather4).
@@ -201,8 +226,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   using Smem = BwdSmem<D, kBias>;
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t mk = (prm.N + kBlock - 1) / kBlock;   // last kv-block may be ragged
-  const int32_t units = mk * prm.heads * prm.batch;
+  UnitGeom ug;
+  ug.mk = (prm.N + kBlock - 1) / kBlock;   // last kv-block may be ragged
+  ug.ppb = (ug.mk + 1) / 2;
+  ug.pairs = ug.ppb * prm.heads * prm.batch;
+  const int32_t mk = ug.mk;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < 2; ++s) {
@@ -215,8 +243,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::mbar_init(&sm.s_full[hh], 1);
       sm100::mbar_init(&sm.ds_ready[hh], 256);
     }
-    sm100::mbar_init(&sm.dq_full, 1);
-    sm100::mbar_init(&sm.dq_free, 128);
+    for (int bb = 0; bb < 2; ++bb) {
+      sm100::mbar_init(&sm.dq_full[bb], 1);
+      sm100::mbar_init(&sm.dq_free[bb], 128);
+    }
     sm100::mbar_init(&sm.dkv_full, 1);
     sm100::mbar_init(&sm.epi_done, 128);
     sm100::mbar_init(&sm.dbg_bar, 1);
@@ -251,8 +281,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t n = 0, g = 0;
       int64_t stage_tag0 = -1, stage_tag1 = -1;   // (b, h, q-block) held by stage 0 / 1
       for (int32_t kq = 0;; ++kq) {
-        const int32_t u = unit_at(kq);
-        if (u >= units) break;
+        const int32_t u = unit_at(kq, ug);
+        if (u == kUnitEnd) break;
+        if (u < 0) continue;
         const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
         const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
         if (nt == 0) continue;
@@ -306,10 +337,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc_h = sm100::make_idesc_bf16(kBlock, kHalf, false, false);  // S^T, dP^T halves
       constexpr uint32_t idesc_kv = sm100::make_idesc_bf16(kBlock, D, false, true);      // dV, dK
       constexpr uint32_t idesc_q = sm100::make_idesc_bf16(kBlock, D, true, true);        // dQ
-      const uint32_t tP = tmem + kColP, tDQ = tmem + kColDQ, tDV = tmem + kColDV, tDK = tmem + kColDK;
+      const uint32_t tDQ = tmem + kColDQ, tDV = tmem + kColDV, tDK = tmem + kColDK;
       TileIter cur;
-      cur.init(prm.t_row_ptr, mk, units);
+      cur.init(prm.t_row_ptr, ug);
       uint32_t g = 0;
+      uint32_t dq_started0 = 0, dq_started1 = 0;   // chains begun per dQ accumulator
       auto issue_sdp = [&](const TileIter& it, uint32_t gg, int half) {
         const int s = gg & 1;
         const uint8_t* sk = sm.k[it.n & 1];
@@ -331,7 +363,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int kk = half * 4; kk < half * 4 + 4; ++kk) {
           const uint32_t acc = (!first_tile || kk > 0) ? 1u : 0u;
-          sm100::mma_ts(tDV, tP + kk * 8, mnmajor_desc<D>(sm.dO[s], kk), idesc_kv, acc);
+          // P^T of q-columns [16kk, 16kk + 16): 8 packed columns at the start of S^T chunk kk/2
+          sm100::mma_ts(tDV, tmem + kColS + (kk >> 1) * 32 + (kk & 1) * 8, mnmajor_desc<D>(sm.dO[s], kk), idesc_kv,
+                        acc);
           sm100::mma_ss(tDK, ds_kmajor_desc(ds, kk), mnmajor_desc<D>(sm.q[s], kk), idesc_kv, acc);
         }
       };
@@ -356,7 +390,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       while (cur.valid) {
         TileIter nxt = cur;
-        nxt.advance(prm.t_row_ptr, mk, units);
+        nxt.advance(prm.t_row_ptr, ug);
+        const uint32_t fdq = dq_plan(prm.t_dq, cur.rs + cur.t, g);
         const int kvs = cur.n & 1;
         const bool last_of_unit = cur.t == cur.nt - 1;
         // half A of tile g
@@ -390,16 +425,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_probe(3, g);
         sm100::mma_commit(&sm.q_empty[g & 1]);   // Q_g / dO_g no longer read (dQ needs only dS and K)
         if (last_of_unit) sm100::mma_commit(&sm.dkv_full);
-        if (g > 0) {
-          sm100::mbar_wait(&sm.dq_free, (g - 1) & 1);
-          HLA_TR((1 << 24) | ((3) << 16) | (g));
-          sm100::tc_fence_after();
+        const int dqb = (int)(fdq & HLA_DQ_BUF);
+        const bool dq_new = (fdq & HLA_DQ_NEW) != 0;
+        if (dq_new) {
+          // a new chain: the accumulator's previous chain must have been drained
+          const uint32_t c = dqb ? dq_started1++ : dq_started0++;
+          if (c > 0) {
+            sm100::mbar_wait(&sm.dq_free[dqb], (c - 1) & 1);
+            HLA_TR((1 << 24) | ((3) << 16) | (g));
+            sm100::tc_fence_after();
+          }
         }
 #pragma unroll
         for (int kk = 0; kk < kBlock / 16; ++kk)
-          sm100::mma_ss(tDQ, ds_mnmajor_desc(sm.ds[g & 1], kk), mnmajor_desc<D>(sm.k[kvs], kk), idesc_q, kk > 0);
+          sm100::mma_ss(tDQ + dqb * 64, ds_mnmajor_desc(sm.ds[g & 1], kk), mnmajor_desc<D>(sm.k[kvs], kk), idesc_q,
+                        (kk > 0 || !dq_new) ? 1u : 0u);
         mma_probe(4, g);
-        sm100::mma_commit(&sm.dq_full);
+        if (fdq & HLA_DQ_DRAIN) sm100::mma_commit(&sm.dq_full[dqb]);
         if (last_of_unit) sm100::mma_commit(&sm.kv_empty[kvs]);
         if (nxt.valid) {
           if (!next_a_issued) {
@@ -432,8 +474,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     uint32_t n = 0, g = 0;
     for (int32_t kq = 0;; ++kq) {
-        const int32_t u = unit_at(kq);
-        if (u >= units) break;
+      const int32_t u = unit_at(kq, ug);
+      if (u == kUnitEnd) break;
+      if (u < 0) continue;
       const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
       const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
       const int32_t kidx = kb * kBlock + row;
@@ -528,7 +571,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               uint32_t pk[16];
 #pragma unroll
               for (int e = 0; e < 16; ++e) pk[e] = sm100::pack_bf16(p[2 * e], p[2 * e + 1]);
-              sm100::tmem_st16(tmem + lane_off + kColP + c * 16, pk);
+              // over the first 16 columns of this thread's own S^T chunk (already in registers)
+              sm100::tmem_st16(tmem + lane_off + kColS + c * 32, pk);
             }
 #pragma unroll
             for (int u4 = 0; u4 < 4; ++u4) {   // dS, 8 query columns (one 16B chunk) at a time
@@ -603,22 +647,45 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const bool leader = warp == 10 && lane == 0;
     uint32_t g = 0, n = 0;
+    uint32_t dq_drained0 = 0, dq_drained1 = 0;   // chains drained per dQ accumulator
     for (int32_t kq = 0;; ++kq) {
-        const int32_t u = unit_at(kq);
-        if (u >= units) break;
+      const int32_t u = unit_at(kq, ug);
+      if (u == kUnitEnd) break;
+      if (u < 0) continue;
       const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
       const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
       for (int t = 0; t < nt; ++t, ++g) {
-        sm100::mbar_wait(&sm.dq_full, g & 1);
+        const uint32_t fdq = dq_plan(prm.t_dq, rs + t, g);
+        if (!(fdq & HLA_DQ_DRAIN)) continue;   // the chain continues in TMEM
+        const int dqb = (int)(fdq & HLA_DQ_BUF);
+        sm100::mbar_wait(&sm.dq_full[dqb], (dqb ? dq_drained1++ : dq_drained0++) & 1);
         if (leader) HLA_TR((4 << 24) | ((1) << 16) | (g));
         sm100::tc_fence_after();
-        const int32_t qrow = b * prm.N + __ldg(prm.t_col_idx + rs + t) * kBlock;   // sequence order
+        const int32_t qblk = __ldg(prm.t_col_idx + rs + t);
+        const int32_t qrow = b * prm.N + qblk * kBlock;   // sequence order
         uint32_t r[D];
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) sm100::tmem_ld32(tmem + lane_off + kColDQ + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
+        for (int c = 0; c < D / 32; ++c)
+          sm100::tmem_ld32(tmem + lane_off + kColDQ + dqb * 64 + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
         sm100::tmem_wait_ld();
         sm100::tc_fence_before();
-        sm100::mbar_arrive(&sm.dq_free);     // the TMEM dQ tile may now be overwritten
+        sm100::mbar_arrive(&sm.dq_free[dqb]);     // the TMEM dQ accumulator may now be overwritten
+        if (fdq & HLA_DQ_LOCAL) {
+          // complete dQ_i (dS carries the softmax scale): bf16 rows straight to dq, to the
+          // grid cell under the fused reorder; phantom rows of a ragged tile write nothing
+          const int32_t qs = qblk * kBlock + row;
+          if (qs < prm.N) {
+            const int32_t qcell = kGather ? __ldg(prm.s2c + qs) : qs;
+            uint4* dqp = reinterpret_cast<uint4*>(prm.dq + (((int64_t)b * prm.N + qcell) * prm.heads + h) * D);
+#pragma unroll
+            for (int v4 = 0; v4 < D / 8; ++v4)
+              dqp[v4] = make_uint4(sm100::pack_bf16(__uint_as_float(r[8 * v4 + 0]), __uint_as_float(r[8 * v4 + 1])),
+                                   sm100::pack_bf16(__uint_as_float(r[8 * v4 + 2]), __uint_as_float(r[8 * v4 + 3])),
+                                   sm100::pack_bf16(__uint_as_float(r[8 * v4 + 4]), __uint_as_float(r[8 * v4 + 5])),
+                                   sm100::pack_bf16(__uint_as_float(r[8 * v4 + 6]), __uint_as_float(r[8 * v4 + 7])));
+          }
+          continue;
+        }
 #pragma unroll
         for (int hh = 0; hh < D / 32; ++hh) {
           if (leader) sm100::bulk_wait_group_read0();   // previous reduce finished reading the stage
@@ -695,14 +762,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // K7: D = rowsum(dO o O) per (b, s, h) row of head_dim bf16, fp32, in sequence order s
 // (rows read at grid cell s2c[s] under the fused reorder), stored pre-multiplied by
-// the softmax scale; LSE converted to the log2 domain; dQ accumulator := 0
+// the softmax scale; LSE converted to the log2 domain; dQ accumulator := 0 (rows of
+// q-blocks whose dQ the main kernel writes directly -- q_local -- are skipped)
 template <int D>
 __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
                                                              const __nv_bfloat16* __restrict__ dout,
                                                              const float* __restrict__ lse, float scale,
                                                              float* __restrict__ dsum, float* __restrict__ lse2,
                                                              float* __restrict__ dq_acc,
-                                                             const int32_t* __restrict__ s2c, int32_t N,
+                                                             const int32_t* __restrict__ s2c,
+                                                             const uint8_t* __restrict__ q_local, int32_t N,
                                                              int32_t heads, int32_t rows) {
   // one thread per 8 elements (16 B of O and of dO); 32-bit index math (rows * D / 8 < 2^31)
   constexpr int kLanes = D / 8;   // lanes per row
@@ -726,9 +795,11 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
   }
 #pragma unroll
   for (int o2 = kLanes / 2; o2 > 0; o2 >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o2);
-  float4* z = reinterpret_cast<float4*>(dq_acc + (int64_t)r * D + part * 8);   // zeroing is layout-agnostic
-  z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-  z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (!(q_local && __ldg(q_local + (s >> 7)))) {
+    float4* z = reinterpret_cast<float4*>(dq_acc + (int64_t)r * D + part * 8);   // zeroing is layout-agnostic
+    z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   if (part == 0) {
     const int64_t i = (int64_t)(bb * heads + hq) * N + s;
     dsum[i] = acc * scale;                       // D * scale (dS = P o (dP * scale - D * scale))
@@ -739,18 +810,21 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
 // K9: dQ = bf16(accumulator) -- the accumulator is in sequence order; under the
 // fused reorder each row is written to its grid cell s2c[s] (SURVEY 8(a) a8:
 // "dQ finalize + inverse permutation").  One thread per 8 elements (32 B in, 16 B out).
+// Rows of local q-blocks (q_local: written by the main kernel) are left alone.
 __global__ void __launch_bounds__(256) dq_finalize_kernel(const float4* __restrict__ acc, uint4* __restrict__ dq,
-                                                          const int32_t* __restrict__ s2c, int32_t N,
+                                                          const int32_t* __restrict__ s2c,
+                                                          const uint8_t* __restrict__ q_local, int32_t N,
                                                           int32_t row_v, int32_t n_v) {
   const int32_t t = (int32_t)blockIdx.x * blockDim.x + threadIdx.x;   // n_v = B * N * row_v < 2^31
   if (t >= n_v) return;
-  const float4 v0 = __ldcs(acc + 2 * (int64_t)t), v1 = __ldcs(acc + 2 * (int64_t)t + 1);
   int64_t o = t;
-  if (s2c) {   // t = (b * N + s) * row_v + part, row_v = heads * D / 8
+  if (s2c || q_local) {   // t = (b * N + s) * row_v + part, row_v = heads * D / 8
     const int32_t bs = t / row_v, part = t - bs * row_v;
     const int32_t b = bs / N, s = bs - b * N;
-    o = (int64_t)(b * N + __ldg(s2c + s)) * row_v + part;
+    if (q_local && __ldg(q_local + (s >> 7))) return;
+    if (s2c) o = (int64_t)(b * N + __ldg(s2c + s)) * row_v + part;
   }
+  const float4 v0 = __ldcs(acc + 2 * (int64_t)t), v1 = __ldcs(acc + 2 * (int64_t)t + 1);
   dq[o] = make_uint4(sm100::pack_bf16(v0.x, v0.y), sm100::pack_bf16(v0.z, v0.w), sm100::pack_bf16(v1.x, v1.y),
                      sm100::pack_bf16(v1.z, v1.w));
 }
@@ -761,8 +835,8 @@ hla_status launch_bwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtens
   const size_t smem = sizeof(BwdSmem<D, kBias>) + 1024;
   auto* fn = attn_bwd_kernel<D, kTwoD, kGather, kBias>;
   HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t units = (int64_t)n_kblocks * prm.heads * prm.batch;
-  const int grid = (int)std::min<int64_t>((units + 1) / 2, (int64_t)num_sms());   // pairs of units
+  const int64_t pairs = (int64_t)((n_kblocks + 1) / 2) * prm.heads * prm.batch;   // work units (kv-block pairs)
+  const int grid = (int)std::min<int64_t>(pairs, (int64_t)num_sms());
   fn<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mdo, mdq, prm);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
@@ -797,6 +871,12 @@ extern "C" size_t hla_attn_bwd_workspace(int32_t batch, int32_t heads, int32_t n
 
 namespace {
 
+// q_dq_local of a mask with a complete dQ plan (else null: every q-block via the accumulator)
+const uint8_t* plan_of(const hla_block_mask* m, int32_t n) {
+  if (!m || !m->t_dq || !m->q_dq_local || m->n_dq_nonlocal < 0) return nullptr;
+  return m->n_qblocks == (n + kBlock - 1) / kBlock ? m->q_dq_local : nullptr;
+}
+
 // workspace carve-up: [fp32 dQ accumulator][fp32 D*scale][fp32 LSE*log2e], 256-aligned regions
 hla_status carve_workspace(int32_t batch, int32_t heads, int32_t n, int32_t head_dim, void* workspace,
                            size_t workspace_bytes, float** dq_acc, float** dsum, float** lse2 = nullptr) {
@@ -816,11 +896,12 @@ hla_status carve_workspace(int32_t batch, int32_t heads, int32_t n, int32_t head
 
 extern "C" hla_status hla_attn_bwd_preprocess(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,
                                               float scale, const void* o, const void* dout, const float* lse,
-                                              const int32_t* seq_to_cell, void* workspace, size_t workspace_bytes,
-                                              cudaStream_t stream) {
+                                              const int32_t* seq_to_cell, const hla_block_mask* plan_mask,
+                                              void* workspace, size_t workspace_bytes, cudaStream_t stream) {
   clear_error();
   HLA_REQUIRE(head_dim == 32 || head_dim == 64, HLA_ERR_UNSUPPORTED, "head_dim %d not in {32, 64}", head_dim);
   HLA_REQUIRE(batch >= 1 && heads >= 1 && n >= 1, HLA_ERR_INVALID, "bad shape");
+  const uint8_t* q_local = plan_of(plan_mask, n);
   HLA_REQUIRE(o && dout && ((uintptr_t)o | (uintptr_t)dout) % 16 == 0, HLA_ERR_INVALID, "o/dout null or unaligned");
   HLA_REQUIRE(lse != nullptr, HLA_ERR_INVALID, "null lse");
   float *dq_acc, *dsum, *lse2;
@@ -834,18 +915,20 @@ extern "C" hla_status hla_attn_bwd_preprocess(int32_t batch, int32_t heads, int3
   if (head_dim == 64)
     bwd_preprocess_kernel<64><<<blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
                                                           reinterpret_cast<const __nv_bfloat16*>(dout), lse, sc,
-                                                          dsum, lse2, dq_acc, seq_to_cell, n, heads, (int32_t)rows);
+                                                          dsum, lse2, dq_acc, seq_to_cell, q_local, n, heads,
+                                                          (int32_t)rows);
   else
     bwd_preprocess_kernel<32><<<blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
                                                           reinterpret_cast<const __nv_bfloat16*>(dout), lse, sc,
-                                                          dsum, lse2, dq_acc, seq_to_cell, n, heads, (int32_t)rows);
+                                                          dsum, lse2, dq_acc, seq_to_cell, q_local, n, heads,
+                                                          (int32_t)rows);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
 }
 
 extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch,
                                         int32_t heads, int32_t head_dim, float scale, const void* q, const void* k,
-                                        const void* v, const void* dout, void* dk, void* dv,
+                                        const void* v, const void* dout, void* dq, void* dk, void* dv,
                                         const int32_t* seq_to_cell, const hla_score_mod* score_mod,
                                         void* workspace, size_t workspace_bytes, int64_t* tiles_visited,
                                         cudaStream_t stream) {
@@ -855,7 +938,9 @@ extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_blo
   if (st != HLA_OK) return st;
   HLA_REQUIRE(m->t_row_ptr && m->t_col_idx && m->t_kind, HLA_ERR_INVALID, "transposed mask arrays missing");
   HLA_REQUIRE(q && k && v && dout && dk && dv, HLA_ERR_INVALID, "null pointer");
-  HLA_REQUIRE(((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)dout | (uintptr_t)dk | (uintptr_t)dv) % 16 == 0,
+  HLA_REQUIRE(dq || !plan_of(m, pat.N), HLA_ERR_INVALID, "dq required: the mask's dQ plan writes local q-blocks");
+  HLA_REQUIRE(((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)dout | (uintptr_t)dk | (uintptr_t)dv |
+               (uintptr_t)dq) % 16 == 0,
               HLA_ERR_INVALID, "tensors must be 16-byte aligned");
   float *dq_acc, *dsum, *lse2;
   st = carve_workspace(batch, heads, pat.N, head_dim, workspace, workspace_bytes, &dq_acc, &dsum, &lse2);
@@ -871,6 +956,8 @@ extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_blo
   prm.t_row_ptr = m->t_row_ptr;
   prm.t_col_idx = m->t_col_idx;
   prm.t_kind = m->t_kind;
+  prm.t_dq = plan_of(m, pat.N) ? m->t_dq : nullptr;
+  prm.dq = reinterpret_cast<__nv_bfloat16*>(dq);
   prm.lse2 = lse2;
   prm.dsum = dsum;
   prm.dq_acc = dq_acc;
@@ -907,7 +994,8 @@ extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_blo
 
 extern "C" hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,
                                             const void* workspace, size_t workspace_bytes, void* dq,
-                                            const int32_t* seq_to_cell, cudaStream_t stream) {
+                                            const int32_t* seq_to_cell, const hla_block_mask* plan_mask,
+                                            cudaStream_t stream) {
   clear_error();
   HLA_REQUIRE(head_dim == 32 || head_dim == 64, HLA_ERR_UNSUPPORTED, "head_dim %d not in {32, 64}", head_dim);
   HLA_REQUIRE(dq && (uintptr_t)dq % 16 == 0, HLA_ERR_INVALID, "dq null or unaligned");
@@ -917,9 +1005,11 @@ extern "C" hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_
   if (st != HLA_OK) return st;
   const int64_t n_v = (int64_t)batch * n * heads * head_dim / 8;
   HLA_REQUIRE(n_v < (1ll << 31), HLA_ERR_UNSUPPORTED, "B * N * heads * head_dim too large");
+  const uint8_t* q_local = plan_of(plan_mask, n);
+  if (q_local && plan_mask->n_dq_nonlocal == 0) return HLA_OK;   // every dQ row written by the main kernel
   const unsigned blocks = (unsigned)((n_v + 255) / 256);
   dq_finalize_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const float4*>(dq_acc),
-                                                 reinterpret_cast<uint4*>(dq), seq_to_cell, n,
+                                                 reinterpret_cast<uint4*>(dq), seq_to_cell, q_local, n,
                                                  heads * head_dim / 8, (int32_t)n_v);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
@@ -946,11 +1036,12 @@ extern "C" hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_ma
   if ((st = parse_score_mod(d, score_mod, true, &rpb, &drpb, &cells)) != HLA_OK) return st;
   if (drpb)   // the table gradient is accumulated: start from zero
     HLA_CUDA_TRY(cudaMemsetAsync(drpb, 0, sizeof(float) * heads * (2 * pat.H - 1) * (2 * pat.W - 1), stream));
-  if ((st = hla_attn_bwd_preprocess(batch, heads, pat.N, head_dim, scale, o, dout, lse, seq_to_cell, workspace,
+  if ((st = hla_attn_bwd_preprocess(batch, heads, pat.N, head_dim, scale, o, dout, lse, seq_to_cell, m, workspace,
                                     workspace_bytes, stream)) != HLA_OK)
     return st;
-  if ((st = hla_attn_bwd_main(d, m, batch, heads, head_dim, scale, q, k, v, dout, dk, dv, seq_to_cell, score_mod,
-                              workspace, workspace_bytes, tiles_visited, stream)) != HLA_OK)
+  if ((st = hla_attn_bwd_main(d, m, batch, heads, head_dim, scale, q, k, v, dout, dq, dk, dv, seq_to_cell,
+                              score_mod, workspace, workspace_bytes, tiles_visited, stream)) != HLA_OK)
     return st;
-  return hla_attn_bwd_finalize(batch, heads, pat.N, head_dim, workspace, workspace_bytes, dq, seq_to_cell, stream);
+  return hla_attn_bwd_finalize(batch, heads, pat.N, head_dim, workspace, workspace_bytes, dq, seq_to_cell, m,
+                               stream);
 }

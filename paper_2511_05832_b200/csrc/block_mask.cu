@@ -10,6 +10,8 @@
 // or compacted in ascending order (fill pass).  The library owns no scratch
 // memory, so lines are re-classified in each pass (not on the per-step path;
 // built once per shape like the cached Hilbert path).
+#include <vector>
+
 #include "predicates.cuh"
 
 namespace hla {
@@ -150,9 +152,106 @@ __global__ void __launch_bounds__(1024) scan_lines_kernel(int32_t* row_ptr, int3
   if (blockIdx.x == 0 && threadIdx.x == 0) counts[3] = (unsigned long long)Mq * (unsigned long long)Mk - counts[0];
 }
 
+// Backward dQ plan (hla_build_bwd_plan): one thread per work unit = kv-block pair
+// (2p, 2p+1).  Walks the unit's tiles in the order the backward kernel executes them
+// (list(2p) ascending, then list(2p+1) ascending) and assigns dQ chains to the two
+// TMEM accumulators: a q-block listed by both kv-blocks is held across the pair;
+// a new chain takes a free accumulator (alternating), and if both are held the
+// older hold is cut (its first tile drains through the fp32 workspace instead).
+__global__ void bwd_plan_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ t_row_ptr,
+                                const int32_t* __restrict__ t_col_idx, int32_t Mk, uint8_t* __restrict__ t_dq) {
+  const int32_t p = (int32_t)(blockIdx.x * blockDim.x + threadIdx.x);
+  const int32_t j0 = 2 * p, j1 = 2 * p + 1;
+  if (j0 >= Mk) return;
+  const int32_t a0 = t_row_ptr[j0], a1 = t_row_ptr[j0 + 1];
+  const int32_t b0 = j1 < Mk ? t_row_ptr[j1] : 0, b1 = j1 < Mk ? t_row_ptr[j1 + 1] : 0;
+  auto row_len = [&](int32_t i) { return row_ptr[i + 1] - row_ptr[i]; };
+  int32_t held_q[2] = {-1, -1}, held_e[2] = {-1, -1};
+  int nb = 0;
+  // a new chain's accumulator: prefer the alternate one, take the other if only it is
+  // free, cut the hold of the alternate one if both are held
+  auto take = [&]() {
+    int b = nb;
+    if (held_q[b] >= 0 && held_q[b ^ 1] < 0) b ^= 1;
+    if (held_q[b] >= 0) {
+      t_dq[held_e[b]] |= HLA_DQ_DRAIN;   // cut: drained (partial) at its first tile
+      held_q[b] = -1;
+    }
+    nb = b ^ 1;
+    return b;
+  };
+  int32_t e1 = b0;
+  for (int32_t e = a0; e < a1; ++e) {
+    const int32_t i = t_col_idx[e];
+    while (e1 < b1 && t_col_idx[e1] < i) ++e1;
+    const bool in1 = e1 < b1 && t_col_idx[e1] == i;
+    const int b = take();
+    uint8_t f = (uint8_t)(b | HLA_DQ_NEW);
+    if (in1) {
+      held_q[b] = i;
+      held_e[b] = e;
+    } else {
+      f |= HLA_DQ_DRAIN | (row_len(i) == 1 ? HLA_DQ_LOCAL : 0);
+    }
+    t_dq[e] = f;
+  }
+  for (int32_t e = b0; e < b1; ++e) {
+    const int32_t i = t_col_idx[e];
+    int b = held_q[0] == i ? 0 : (held_q[1] == i ? 1 : -1);
+    if (b >= 0) {   // continues the chain held since kv-block 2p: complete iff row i = {2p, 2p+1}
+      t_dq[e] = (uint8_t)(b | HLA_DQ_DRAIN | (row_len(i) == 2 ? HLA_DQ_LOCAL : 0));
+      held_q[b] = -1;
+    } else {
+      b = take();
+      t_dq[e] = (uint8_t)(b | HLA_DQ_NEW | HLA_DQ_DRAIN | (row_len(i) == 1 ? HLA_DQ_LOCAL : 0));
+    }
+  }
+}
+
+// q_dq_local[i] = 1 iff q-block i's dQ is completed inside one work unit, read off
+// the plan: the entry of i in the list of its last kv-block carries LOCAL (a chain
+// is LOCAL only if it covers i's whole forward list)
+__global__ void bwd_plan_local_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                                      const int32_t* __restrict__ t_row_ptr, const int32_t* __restrict__ t_col_idx,
+                                      const uint8_t* __restrict__ t_dq, int32_t Mq, uint8_t* __restrict__ q_local) {
+  const int32_t i = (int32_t)(blockIdx.x * blockDim.x + threadIdx.x);
+  if (i >= Mq) return;
+  uint8_t loc = 0;
+  const int32_t r0 = row_ptr[i], r1 = row_ptr[i + 1];
+  if (r1 > r0) {
+    const int32_t jl = col_idx[r1 - 1];
+    for (int32_t e = t_row_ptr[jl]; e < t_row_ptr[jl + 1]; ++e)
+      if (t_col_idx[e] == i) { loc = (t_dq[e] & HLA_DQ_LOCAL) ? 1 : 0; break; }
+  }
+  q_local[i] = loc;
+}
+
 }  // namespace hla
 
 using namespace hla;
+
+extern "C" hla_status hla_build_bwd_plan(hla_block_mask* m, cudaStream_t stream) {
+  clear_error();
+  HLA_REQUIRE(m != nullptr, HLA_ERR_INVALID, "null mask");
+  HLA_REQUIRE(m->row_ptr && m->col_idx && m->t_row_ptr && m->t_col_idx, HLA_ERR_INVALID,
+              "the mask must be filled (hla_build_block_mask fill call) before its plan");
+  HLA_REQUIRE(m->t_dq && m->q_dq_local, HLA_ERR_INVALID, "t_dq / q_dq_local arrays required");
+  HLA_REQUIRE(m->n_qblocks == m->n_kblocks, HLA_ERR_UNSUPPORTED, "dQ plan needs block_q == block_k");
+  const int32_t Mq = m->n_qblocks, Mk = m->n_kblocks;
+  HLA_REQUIRE(Mq >= 1 && Mq <= 65536, HLA_ERR_INVALID, "bad n_qblocks");
+  const int32_t pairs = (Mk + 1) / 2;
+  bwd_plan_kernel<<<(pairs + 127) / 128, 128, 0, stream>>>(m->row_ptr, m->t_row_ptr, m->t_col_idx, Mk, m->t_dq);
+  bwd_plan_local_kernel<<<(Mq + 127) / 128, 128, 0, stream>>>(m->row_ptr, m->col_idx, m->t_row_ptr, m->t_col_idx,
+                                                              m->t_dq, Mq, m->q_dq_local);
+  HLA_CUDA_TRY(cudaGetLastError());
+  std::vector<uint8_t> loc((size_t)Mq);
+  HLA_CUDA_TRY(cudaMemcpyAsync(loc.data(), m->q_dq_local, (size_t)Mq, cudaMemcpyDeviceToHost, stream));
+  HLA_CUDA_TRY(cudaStreamSynchronize(stream));
+  int32_t n = 0;
+  for (uint8_t x : loc) n += x ? 0 : 1;
+  m->n_dq_nonlocal = n;
+  return HLA_OK;
+}
 
 extern "C" hla_status hla_build_block_mask(const hla_pattern_desc* d, hla_block_mask* m, int64_t* nnz_out,
                                            cudaStream_t stream) {

@@ -186,7 +186,7 @@ def test_fused_reorder_matches_explicit_permutation(kind, g, w, B, H, d):
     r1 = [t.clone() for t in (fused.forward(q, k, v),) + fused.backward(do)]
     r2 = [t.clone() for t in (plain.forward(q, k, v),) + plain.backward(do)]
     torch.cuda.synchronize()
-    assert fused.launches_per_step == 4 and plain.launches_per_step == 8
+    assert plain.launches_per_step == fused.launches_per_step + 4 and fused.launches_per_step in (3, 4)
     assert torch.equal(r1[0], r2[0])                       # O
     assert torch.equal(fused.lse, plain.lse)
     assert torch.equal(r1[2], r2[2]) and torch.equal(r1[3], r2[3])   # dK, dV
@@ -280,3 +280,27 @@ def test_rpb_zero_table_matches_no_bias():
     torch.cuda.synchronize()
     for x, y in zip(ra, rb):
         assert (x.float() - y.float()).abs().max().item() <= 2e-2
+
+
+@pytest.mark.parametrize("kind,g,w,B,H,d", [("HWA", 64, 16, 2, 4, 64), ("HSA", 64, 16, 2, 3, 64),
+                                             ("HNA", 32, 5, 2, 2, 32), ("DENSE", 16, 1, 1, 2, 64),
+                                             ("HWA", 56, 7, 2, 3, 32), ("HSWA", 32, 8, 2, 2, 64),
+                                             ("WSA", 32, 8, 2, 2, 64)])
+@pytest.mark.parametrize("fused", [True, False])
+def test_dq_plan_matches_no_plan(kind, g, w, B, H, d, fused):
+    """The backward's dQ plan (TMEM chaining, direct bf16 dQ for local q-blocks) changes
+    only the summation of dQ partials: dK, dV bit-identical, dQ within fp32-order
+    rounding of the same products, both against a mask without plan."""
+    if not fused and kind.startswith("H") and g & (g - 1):
+        pytest.skip("the explicit permutation kernel needs a 2^k grid")
+    q, k, v, do = _inputs(B, g * g, H, d, seed=5)
+    shift = (w * w) // 2 if kind == "HSWA" else 0
+    a = hla.HilbertLocalAttention(kind, g, g, w, w, B, H, d, shift=shift, device=DEV, fused=fused)
+    b = hla.HilbertLocalAttention(kind, g, g, w, w, B, H, d, shift=shift, device=DEV, fused=fused, dq_plan=False)
+    assert a.mask.n_dq_nonlocal >= 0 and b.mask.n_dq_nonlocal == -1
+    r1 = [t.clone() for t in (a.forward(q, k, v),) + a.backward(do)]
+    r2 = [t.clone() for t in (b.forward(q, k, v),) + b.backward(do)]
+    torch.cuda.synchronize()
+    assert torch.equal(r1[0], r2[0])
+    assert torch.equal(r1[2], r2[2]) and torch.equal(r1[3], r2[3])
+    assert (r1[1].float() - r2[1].float()).abs().max().item() <= 2e-3

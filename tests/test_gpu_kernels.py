@@ -103,3 +103,62 @@ def test_block_mask_bit_exact(kind, H, W, wh, ww, b):
     assert np.array_equal(m.t_kind.cpu().numpy()[:nnz], tkd)
     e, s = m.ratios()
     assert e == st["empty_tile_ratio"] and s == st["sparsity"]
+
+
+def _check_bwd_plan(m):
+    """Replays the backward's dQ plan the way attn_bwd_kernel executes it (work units =
+    kv-block pairs (2p, 2p+1), tiles in list order) and checks that it is executable and
+    exact: a new chain only takes an accumulator whose previous chain was drained; a
+    continuing tile extends a live chain of the same q-block in the same unit; every tile
+    of the mask is in exactly one chain; LOCAL exactly when the chain is q-block i's whole
+    forward list; q_dq_local / n_dq_nonlocal agree with the LOCAL chains."""
+    NEW, DRAIN, LOCAL = 2, 4, 8
+    rp, ci = m.row_ptr.cpu().numpy(), m.col_idx.cpu().numpy()
+    trp, tci = m.t_row_ptr.cpu().numpy(), m.t_col_idx.cpu().numpy()
+    f = m.t_dq.cpu().numpy()
+    mq, mk = len(rp) - 1, len(trp) - 1
+    rows = [set(ci[rp[i]:rp[i + 1]].tolist()) for i in range(mq)]
+    covered = set()
+    local = np.zeros(mq, dtype=np.uint8)
+    for p in range(0, mk, 2):
+        live = [None, None]          # per accumulator: (q-block, kv-blocks of the chain) or None
+        for j in (p, p + 1):
+            if j >= mk:
+                continue
+            for e in range(trp[j], trp[j + 1]):
+                i, b = int(tci[e]), int(f[e] & 1)
+                if f[e] & NEW:
+                    assert live[b] is None, "accumulator %d still holds a chain (kv %d, q %d)" % (b, j, i)
+                    live[b] = (i, [j])
+                else:
+                    assert live[b] is not None and live[b][0] == i, "continuation of a chain not held (kv %d, q %d)" % (j, i)
+                    live[b][1].append(j)
+                assert (j, i) not in covered
+                covered.add((j, i))
+                if f[e] & DRAIN:
+                    whole = set(live[b][1]) == rows[i]
+                    assert bool(f[e] & LOCAL) == whole, (j, i, f[e])
+                    if whole:
+                        local[i] = 1
+                    live[b] = None
+                else:
+                    assert not f[e] & LOCAL
+        assert live == [None, None], "chain left open at the end of unit %d" % p
+    assert len(covered) == m.nnz
+    assert np.array_equal(m.q_dq_local.cpu().numpy(), local)
+    assert m.n_dq_nonlocal == int((local == 0).sum())
+
+
+PLAN_CASES = [("HWA", 64, 64, 16, 16), ("HSA", 64, 64, 16, 16), ("HNA", 128, 128, 7, 7), ("HWA", 16, 16, 8, 8),
+              ("WSA", 64, 64, 16, 16), ("SA", 64, 64, 16, 16), ("NA2D", 56, 56, 7, 7), ("DENSE", 16, 32, 1, 1),
+              ("DENSE", 64, 64, 1, 1), ("HSWA", 64, 64, 16, 16), ("HWA", 56, 56, 7, 7), ("HWA", 28, 28, 7, 7),
+              ("HWA", 14, 14, 7, 7), ("HSA", 4, 4, 3, 3), ("HWA", 40, 40, 8, 8)]
+
+
+@pytest.mark.parametrize("kind,H,W,wh,ww", PLAN_CASES)
+def test_bwd_plan_executable_and_exact(kind, H, W, wh, ww):
+    shift = (wh * ww) // 2 if kind == "HSWA" else 0
+    m = hla.hla_build_block_mask(hla.pattern_desc(kind, H, W, wh, ww, block=128, shift=shift), DEV)
+    _check_bwd_plan(m)
+    if kind == "HWA" and (wh * ww) % 256 == 0:
+        assert m.n_dq_nonlocal == 0      # windows of whole kv-block pairs: every dQ finishes in TMEM

@@ -72,9 +72,16 @@ def test_argument_validation_without_gpu():
                             ctypes.byref(mod), None, None)
         assert st == want, (mod.kind, st)
     mod = _lib.ScoreModC(1, 16, None, 16)
-    st = L.hla_attn_bwd_main(ctypes.byref(d), ctypes.byref(m), 1, 1, 64, 0.0, 16, 16, 16, 16, 16, 16, None,
+    st = L.hla_attn_bwd_main(ctypes.byref(d), ctypes.byref(m), 1, 1, 64, 0.0, 16, 16, 16, 16, 16, 16, 16, None,
                              ctypes.byref(mod), 256, 1 << 30, None, None)
     assert st == _lib.HLA_ERR_INVALID and b"drpb" in L.hla_last_error()
+    # backward dQ plan: needs a filled mask and its two plan arrays; square tiles only
+    m = _lib.BlockMaskC(32, 32, 1, 8, None, 8, 8, 8, 8, 8, 16, 16, -1)
+    assert L.hla_build_bwd_plan(ctypes.byref(m), None) == _lib.HLA_ERR_INVALID and b"filled" in L.hla_last_error()
+    m = _lib.BlockMaskC(32, 32, 1, 8, 8, 8, 8, 8, 8, 8, None, 16, -1)
+    assert L.hla_build_bwd_plan(ctypes.byref(m), None) == _lib.HLA_ERR_INVALID
+    m = _lib.BlockMaskC(32, 16, 1, 8, 8, 8, 8, 8, 8, 8, 16, 16, -1)
+    assert L.hla_build_bwd_plan(ctypes.byref(m), None) == _lib.HLA_ERR_UNSUPPORTED
 
 
 @pytest.mark.parametrize("kind,H,W,wh,ww,b", [("HWA", 56, 56, 7, 7, 128), ("SA", 56, 56, 7, 7, 128),

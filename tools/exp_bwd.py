@@ -8,7 +8,7 @@ for kind, w in (("HWA",16),("WSA",16)):
     L.forward(q,k,v); L.backward(do); torch.cuda.synchronize()
     s2c = L.s2c
     def run():
-        hla.api.hla_attn_bwd_main(L.desc, L.mask, q, k, v, do, L.dk, L.dv, L.workspace, 0.0, seq_to_cell=s2c)
+        hla.api.hla_attn_bwd_main(L.desc, L.mask, q, k, v, do, L.dq, L.dk, L.dv, L.workspace, 0.0, seq_to_cell=s2c)
     for _ in range(3): run()
     torch.cuda.synchronize()
     e0,e1=torch.cuda.Event(enable_timing=True),torch.cuda.Event(enable_timing=True)

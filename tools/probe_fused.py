@@ -17,10 +17,10 @@ for fused in (True, False):
     L.forward(q, k, v); L.backward(do)
     if fused:
         f = lambda: api.hla_attn_fwd(L.desc, L.mask, q, k, v, 0.0, L.o, L.lse, seq_to_cell=L.s2c)
-        b = lambda: api.hla_attn_bwd_main(L.desc, L.mask, q, k, v, do, L.dk, L.dv, L.workspace, 0.0, seq_to_cell=L.s2c)
+        b = lambda: api.hla_attn_bwd_main(L.desc, L.mask, q, k, v, do, L.dq, L.dk, L.dv, L.workspace, 0.0, seq_to_cell=L.s2c)
     else:
         f = lambda: api.hla_attn_fwd(L.desc, L.mask, L.qs, L.ks, L.vs, 0.0, L.os, L.lse)
-        b = lambda: api.hla_attn_bwd_main(L.desc, L.mask, L.qs, L.ks, L.vs, L.dos, L.dks, L.dvs, L.workspace, 0.0)
+        b = lambda: api.hla_attn_bwd_main(L.desc, L.mask, L.qs, L.ks, L.vs, L.dos, L.dqs, L.dks, L.dvs, L.workspace, 0.0)
     print("fused" if fused else "plain", "fwd %.4f ms  bwd_main %.4f ms" % (t_ms(f), t_ms(b)))
 # SM clock while the forward runs back to back (~1 s)
 import bench

@@ -21,9 +21,9 @@ for kind in ("HWA", "WSA", "DENSE"):
     L.forward(q, k, v); L.backward(do)
     if kind == "HWA":
         f = lambda: api.hla_attn_fwd(L.desc, L.mask, q, k, v, 0.0, L.o, L.lse, seq_to_cell=L.s2c)
-        b = lambda: api.hla_attn_bwd_main(L.desc, L.mask, q, k, v, do, L.dk, L.dv, L.workspace, 0.0, seq_to_cell=L.s2c)
+        b = lambda: api.hla_attn_bwd_main(L.desc, L.mask, q, k, v, do, L.dq, L.dk, L.dv, L.workspace, 0.0, seq_to_cell=L.s2c)
     else:
         f = lambda: api.hla_attn_fwd(L.desc, L.mask, q, k, v, 0.0, L.o, L.lse)
-        b = lambda: api.hla_attn_bwd_main(L.desc, L.mask, q, k, v, do, L.dk, L.dv, L.workspace, 0.0)
+        b = lambda: api.hla_attn_bwd_main(L.desc, L.mask, q, k, v, do, L.dq, L.dk, L.dv, L.workspace, 0.0)
     out.append("%s fwd %.4f bwd %.4f" % (kind, t_ms(f), t_ms(b)))
 print(os.environ.get("HLA_LIB_NAME", "libhla.so"), " | ".join(out))

@@ -19,7 +19,7 @@ lib.hla_debug_trace_dump.argtypes = [ctypes.c_void_p, ctypes.c_int]
 buf = (ctypes.c_ulonglong * 16384)()
 lib.hla_debug_trace_dump(buf, 8192)   # reset
 if which == "bwd":
-    hla.api.hla_attn_bwd_main(L.desc, L.mask, q, k, v, do, L.dk, L.dv, L.workspace, 0.0, seq_to_cell=L.s2c)
+    hla.api.hla_attn_bwd_main(L.desc, L.mask, q, k, v, do, L.dq, L.dk, L.dv, L.workspace, 0.0, seq_to_cell=L.s2c)
 elif which == "fwdplain":
     hla.api.hla_attn_fwd(L.desc, L.mask, L.qs, L.ks, L.vs, 0.0, L.os, L.lse)
 else:
