@@ -773,14 +773,17 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
                                                              const int32_t* __restrict__ s2c,
                                                              const uint8_t* __restrict__ q_local, int32_t N,
                                                              int32_t heads, int32_t rows) {
-  // one thread per 8 elements (16 B of O and of dO); 32-bit index math (rows * D / 8 < 2^31)
+  // one thread per 8 elements (16 B of O and of dO); 32-bit index math (rows * D / 8 < 2^31).
+  // Threads walk the OUTPUT order (b, h, s): D / LSE are written as contiguous runs (in
+  // token order the 4-byte results of one warp land in `heads` different sectors).
   constexpr int kLanes = D / 8;   // lanes per row
   const int32_t gid = (int32_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int32_t r = gid / kLanes;             // sequence-order row (b * N + s) * heads + h
-  const int part = gid - r * kLanes;
-  if (r >= rows) return;
-  const int32_t bs = r / heads, hq = r - bs * heads;
-  const int32_t bb = bs / N, s = bs - bb * N;
+  const int32_t i = gid / kLanes;             // (b * heads + h) * N + s
+  const int part = gid - i * kLanes;
+  if (i >= rows) return;
+  const int32_t bh = i / N, s = i - bh * N;
+  const int32_t bb = bh / heads, hq = bh - bb * heads;
+  const int32_t r = (bb * N + s) * heads + hq;   // sequence-order row (b * N + s) * heads + h
   const int64_t src = s2c ? ((int64_t)(bb * N + __ldg(s2c + s)) * heads + hq) : (int64_t)r;
   const uint4 a = __ldg(reinterpret_cast<const uint4*>(o + src * D + part * 8));
   const uint4 g = __ldg(reinterpret_cast<const uint4*>(dout + src * D + part * 8));
@@ -801,7 +804,6 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
     z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   if (part == 0) {
-    const int64_t i = (int64_t)(bb * heads + hq) * N + s;
     dsum[i] = acc * scale;                       // D * scale (dS = P o (dP * scale - D * scale))
     lse2[i] = __ldg(lse + i) * kLog2e;           // LSE in the log2 domain
   }
