@@ -46,6 +46,12 @@ HLA_API hla_status hla_debug_tmem_rate(int32_t nwarps, int32_t iters, int32_t mo
 HLA_API hla_status hla_debug_ex2_rate(int32_t threads, int32_t iters, long long* out_cycles, float* sink,
                                       cudaStream_t stream);
 
+/* hla_debug_xu_rate: one CTA of `threads` threads, each `iters` x 16 independent instances of
+ * one XU-pipe instruction form (mode 0 ex2.f32, 1 ex2.bf16x2, 2 ex2.f16x2, 3 cvt.rn.bf16x2.f32,
+ * 4/5/6 softmax pair-loop variants, see debug_umma.cu); out_cycles[0] = SM cycles. */
+HLA_API hla_status hla_debug_xu_rate(int32_t mode, int32_t threads, int32_t iters, long long* out_cycles,
+                                     uint32_t* sink, cudaStream_t stream);
+
 /* hla_debug_softmax_tile: `blocks` CTAs x 128 threads run the forward softmax tile body
  * with its TMEM traffic (S ld, max, exp2, P st), `iters` times; out_cycles[cta]. */
 HLA_API hla_status hla_debug_softmax_tile(int32_t blocks, int32_t iters, long long* out_cycles, uint32_t* sink,

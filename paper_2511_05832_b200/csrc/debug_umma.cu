@@ -212,6 +212,84 @@ __global__ void debug_ex2_rate_kernel(int iters, float seed, long long* out, flo
   if (threadIdx.x == 0) out[0] = t1 - t0;
 }
 
+// XU / MUFU instruction-mix probe: `threads` threads of one CTA run `iters` x 16
+// independent instances of one instruction form (mode):
+//   0 ex2.approx.ftz.f32      1 ex2.approx.ftz.bf16x2   2 ex2.approx.f16x2
+//   3 cvt.rn.bf16x2.f32       4 softmax pair loop as in attn_fwd (2 FFMA, 2 ex2.f32, FADD, cvt)
+//   5 softmax pair loop with one ex2.bf16x2 per pair (FFMA x2 in fp32, ALU round + PRMT pack,
+//     ex2.bf16x2, unpack + FADD for the row sum)
+//   6 = 5 with the pack by cvt.rn.bf16x2.f32 instead of the ALU rounding
+__device__ __forceinline__ uint32_t xu_ex2_bf16x2(uint32_t x) {
+  uint32_t y;
+  asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t xu_ex2_f16x2(uint32_t x) {
+  uint32_t y;
+  asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t xu_pack_round(float lo, float hi) {
+  // round-half-up of the fp32 bits to bf16, both halves packed by one PRMT
+  const uint32_t a = __float_as_uint(lo) + 0x8000u, b = __float_as_uint(hi) + 0x8000u;
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__global__ void debug_xu_rate_kernel(int mode, int iters, long long* out, uint32_t* sink) {
+  uint32_t r[16];
+  float f[16];
+  for (int i = 0; i < 16; ++i) {
+    f[i] = -(float)((threadIdx.x * 7 + i * 13) % 97) * 0.01f;
+    r[i] = 0xBF00BF00u ^ (i << 3);
+  }
+  float l = 0.f;
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    if (mode == 0) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) f[i] = sm100::ex2(f[i]) - 1.0f;
+    } else if (mode == 1) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) r[i] = xu_ex2_bf16x2(r[i]) ^ 0x80008000u;
+    } else if (mode == 2) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) r[i] = xu_ex2_f16x2(r[i]) ^ 0x80008000u;
+    } else if (mode == 3) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) r[i] = sm100::pack_bf16(f[i], __uint_as_float(r[i]));
+    } else if (mode == 4) {
+      float l4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float p0 = sm100::ex2(fmaf(f[2 * e], 0.18f, -l));
+        const float p1 = sm100::ex2(fmaf(f[2 * e + 1], 0.18f, -l));
+        l4[e & 3] += p0 + p1;
+        r[e] ^= sm100::pack_bf16(p0, p1);
+      }
+      l += 1e-7f * ((l4[0] + l4[1]) + (l4[2] + l4[3]));
+    } else {
+      float l4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float x0 = fmaf(f[2 * e], 0.18f, -l), x1 = fmaf(f[2 * e + 1], 0.18f, -l);
+        const uint32_t xp = mode == 5 ? xu_pack_round(x0, x1) : sm100::pack_bf16(x0, x1);
+        const uint32_t p = xu_ex2_bf16x2(xp);
+        l4[e & 3] += __uint_as_float(p << 16) + __uint_as_float(p & 0xFFFF0000u);
+        r[e] ^= p;
+      }
+      l += 1e-7f * ((l4[0] + l4[1]) + (l4[2] + l4[3]));
+    }
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  uint32_t acc = __float_as_uint(l);
+  for (int i = 0; i < 16; ++i) acc ^= r[i] ^ __float_as_uint(f[i]);
+  if (acc == 0x12345678u) sink[0] = acc;
+  if (threadIdx.x == 0) out[0] = t1 - t0;
+}
+
 // Softmax inner-loop probe: each thread exponentiates a 128-wide row `iters` times
 // exactly like attn_fwd_kernel (FFMA + ex2 + row sum + bf16 pack); out[blockIdx] = cycles.
 __global__ void __launch_bounds__(128) debug_softmax_rate_kernel(int iters, float sl2, long long* out, uint32_t* sink) {
@@ -397,6 +475,14 @@ extern "C" hla_status hla_debug_ex2_rate(int32_t threads, int32_t iters, long lo
                                          cudaStream_t stream) {
   clear_error();
   debug_ex2_rate_kernel<<<1, threads, 0, stream>>>(iters, 1.0f, out_cycles, sink);
+  HLA_CUDA_TRY(cudaGetLastError());
+  return HLA_OK;
+}
+
+extern "C" hla_status hla_debug_xu_rate(int32_t mode, int32_t threads, int32_t iters, long long* out_cycles,
+                                        uint32_t* sink, cudaStream_t stream) {
+  clear_error();
+  debug_xu_rate_kernel<<<1, threads, 0, stream>>>(mode, iters, out_cycles, sink);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
 }
