@@ -530,10 +530,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             sm100::tmem_ld32(tmem + lane_off + kColS + c * 32, sr);
             sm100::tmem_ld32(tmem + lane_off + kColDP + c * 32, dpr);
             sm100::tmem_wait_ld();
+            // [ulo, uhi): 8-column groups of this chunk that hold an allowed query of some
+            // key row of this warp (partial tiles of 1D patterns: each key row's queries are
+            // one interval); the other groups are all masked, their exponentials skipped
+            // (warp-uniform) and P = 0 there.  Full tiles / 2D patterns: all 4 groups.
+            int ulo = 0, uhi = 4;
+            if (kd == 2 && !kTwoD) {
+              const int32_t base = q0 + c * 32;
+              const int32_t lo = min(max(box.lo - base, 0), 32), hi = min(max(box.lo + box.len - base, 0), 32);
+              const bool any = hi > lo;
+              ulo = __reduce_min_sync(0xffffffffu, any ? lo : 32) >> 3;
+              uhi = (__reduce_max_sync(0xffffffffu, any ? hi : 0) + 7) >> 3;
+            }
             // P first (so its TMEM store is in flight while dS is formed)
             float p[32];
 #pragma unroll
             for (int u4 = 0; u4 < 4; ++u4) {
+              if (u4 < ulo || u4 >= uhi) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) p[u4 * 8 + e] = 0.f;
+                continue;
+              }
               const int qc = c * 32 + u4 * 8;
               const float4 la = sm100::lds_f4(lse2 + qc * 4), lb = sm100::lds_f4(lse2 + qc * 4 + 16);
               const float lv[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
