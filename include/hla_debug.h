@@ -52,6 +52,11 @@ HLA_API hla_status hla_debug_ex2_rate(int32_t threads, int32_t iters, long long*
 HLA_API hla_status hla_debug_xu_rate(int32_t mode, int32_t threads, int32_t iters, long long* out_cycles,
                                      uint32_t* sink, cudaStream_t stream);
 
+/* hla_debug_sync_latency: one CTA; out_cycles[0] = SM cycles per round trip of mode 0
+ * tcgen05.commit -> mbarrier -> wait (no MMA), 1 one 128x128x16 MMA + commit -> wait, 2 warp <-> warp
+ * mbarrier ping-pong (one arrive each way), 3 as 2 with 32 arriving threads on the way back. */
+HLA_API hla_status hla_debug_sync_latency(int32_t mode, int32_t iters, long long* out_cycles, cudaStream_t stream);
+
 /* hla_debug_softmax_tile: `blocks` CTAs x 128 threads run the forward softmax tile body
  * with its TMEM traffic (S ld, max, exp2, P st), `iters` times; out_cycles[cta]. */
 HLA_API hla_status hla_debug_softmax_tile(int32_t blocks, int32_t iters, long long* out_cycles, uint32_t* sink,

@@ -19,7 +19,7 @@ EXPORTED = ("hla_hilbert_index", "hla_hilbert_perm", "hla_build_block_mask", "hl
             "hla_attn_fwd", "hla_attn_bwd", "hla_attn_bwd_workspace", "hla_attn_bwd_preprocess",
             "hla_attn_bwd_main", "hla_attn_bwd_finalize", "hla_build_bwd_plan", "hla_last_error", "hla_version",
             "hla_debug_umma", "hla_debug_gather4", "hla_debug_mma_rate",
-            "hla_debug_tmem_rate", "hla_debug_ex2_rate", "hla_debug_xu_rate",
+            "hla_debug_tmem_rate", "hla_debug_ex2_rate", "hla_debug_xu_rate", "hla_debug_sync_latency",
             "hla_debug_softmax_rate", "hla_debug_softmax_tile", "hla_debug_load_rate")
 
 
@@ -80,6 +80,7 @@ def lib():
         "hla_debug_tmem_rate": [i32, i32, i32, i32, vp, vp],
         "hla_debug_ex2_rate": [i32, i32, vp, vp, vp],
         "hla_debug_xu_rate": [i32, i32, i32, vp, vp, vp],
+        "hla_debug_sync_latency": [i32, i32, vp, vp],
         "hla_debug_softmax_rate": [i32, i32, vp, vp, vp],
         "hla_debug_softmax_tile": [i32, i32, vp, vp, vp],
         "hla_debug_load_rate": [vp, i64, i32, i32, i32, i32, i32, vp, vp],

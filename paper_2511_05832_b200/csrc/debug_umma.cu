@@ -290,6 +290,66 @@ __global__ void debug_xu_rate_kernel(int mode, int iters, long long* out, uint32
   if (threadIdx.x == 0) out[0] = t1 - t0;
 }
 
+// Synchronisation latency probe (one CTA, 64 threads; out[0] = cycles per round trip):
+//   mode 0: one thread: tcgen05.commit (no MMA in flight) -> mbarrier -> wait, repeated
+//   mode 1: one thread: one 128x128x16 SS MMA + commit -> wait, repeated
+//   mode 2: ping-pong between warp 0 and warp 1 through two mbarriers (one arrive each way)
+//   mode 3: as 2, warp 1 = 32 threads arriving (count 32) -- the softmax-style handoff
+__global__ void __launch_bounds__(64) debug_sync_latency_kernel(int mode, int iters, long long* out) {
+  __shared__ alignas(8) uint64_t bars[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ alignas(1024) uint8_t tile[2][128 * 64 * 2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    sm100::mbar_init(&bars[0], 1);
+    sm100::mbar_init(&bars[1], mode == 3 ? 32 : 1);
+    sm100::fence_mbar_init();
+  }
+  if (warp == 0) {
+    sm100::tmem_alloc(&tmem_base, 128);
+    sm100::tmem_relinquish();
+  }
+  for (int i = threadIdx.x; i < 2 * 128 * 64 * 2 / 4; i += 64) reinterpret_cast<uint32_t*>(tile)[i] = 0;
+  sm100::fence_proxy_async_smem();
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  long long t0 = 0, t1 = 0;
+  if (mode <= 1) {
+    if (threadIdx.x == 0) {
+      const uint32_t idesc = sm100::make_idesc_bf16(128, 128, false, false);
+      const uint64_t da = sm100::make_smem_desc(sm100::smem_u32(tile[0]), 16, 1024, sm100::kSwizzle128B);
+      const uint64_t db = sm100::make_smem_desc(sm100::smem_u32(tile[1]), 16, 1024, sm100::kSwizzle128B);
+      t0 = clock64();
+      for (int it = 0; it < iters; ++it) {
+        if (mode == 1) sm100::mma_ss(tmem, da, db, idesc, 0u);
+        sm100::mma_commit(&bars[0]);
+        sm100::mbar_wait(&bars[0], it & 1);
+      }
+      t1 = clock64();
+    }
+  } else {
+    if (warp == 0 && lane == 0) {
+      t0 = clock64();
+      for (int it = 0; it < iters; ++it) {
+        sm100::mbar_arrive(&bars[0]);
+        sm100::mbar_wait(&bars[1], it & 1);
+      }
+      t1 = clock64();
+    } else if (warp == 1 && (mode == 3 || lane == 0)) {
+      for (int it = 0; it < iters; ++it) {
+        sm100::mbar_wait(&bars[0], it & 1);
+        sm100::mbar_arrive(&bars[1]);
+      }
+    }
+  }
+  if (threadIdx.x == 0) out[0] = (t1 - t0) / (iters > 0 ? iters : 1);
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) sm100::tmem_dealloc(tmem, 128);
+}
+
 // Softmax inner-loop probe: each thread exponentiates a 128-wide row `iters` times
 // exactly like attn_fwd_kernel (FFMA + ex2 + row sum + bf16 pack); out[blockIdx] = cycles.
 __global__ void __launch_bounds__(128) debug_softmax_rate_kernel(int iters, float sl2, long long* out, uint32_t* sink) {
@@ -483,6 +543,13 @@ extern "C" hla_status hla_debug_xu_rate(int32_t mode, int32_t threads, int32_t i
                                         uint32_t* sink, cudaStream_t stream) {
   clear_error();
   debug_xu_rate_kernel<<<1, threads, 0, stream>>>(mode, iters, out_cycles, sink);
+  HLA_CUDA_TRY(cudaGetLastError());
+  return HLA_OK;
+}
+
+extern "C" hla_status hla_debug_sync_latency(int32_t mode, int32_t iters, long long* out_cycles, cudaStream_t stream) {
+  clear_error();
+  debug_sync_latency_kernel<<<1, 64, 0, stream>>>(mode, iters, out_cycles);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
 }
