@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // one interval); the other groups are all masked, their exponentials skipped
             // (warp-uniform) and P = 0 there.  Full tiles / 2D patterns: all 4 groups.
             int ulo = 0, uhi = 4;
-            if (kd == 2 && !kTwoD) {
+            if (!kBias && kd == 2 && !kTwoD) {   // (with the RPB gather the branchy loop measured slower: cfg5 +6%)
               const int32_t base = q0 + c * 32;
               const int32_t lo = min(max(box.lo - base, 0), 32), hi = min(max(box.lo + box.len - base, 0), 32);
               const bool any = hi > lo;
