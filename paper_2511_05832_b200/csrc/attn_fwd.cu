@@ -9,10 +9,9 @@
 // Persistent CTAs (2 per SM), 256 threads:
 //   warps 0,2,3 TMA producers (Q_i / K_j / V_j; several issuing warps because a
 //               CTA's TMA gather4 rate grows with them): Q double-buffered per
-//               unit (a stage is reloaded once every S MMA of its unit retired:
-//               q_empty), K / V of the listed kv-blocks in a 2-stage ring; warp 0
-//               also stores each finished O tile (TMA store / 32 scatter4) from the
-//               dedicated staging tile the softmax warps filled.
+//               unit, K / V of the listed kv-blocks in a 2-stage ring; warp 0
+//               also stores each finished O tile (TMA store / scatter4) from
+//               the unit's Q stage, where the softmax warps staged it.
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:
 //                 S_t  = Q_i K_j^T   (SS MMA, 128x128x D, fp32 in TMEM cols [0,128))
 //                 O   += P_t V_j     (TS MMA, P bf16 in TMEM cols [128,192), O in [192,192+D))
@@ -21,7 +20,7 @@
 //               partial, keeps the online max / sum in registers (lazy rescale:
 //               O is rescaled in TMEM only when the row max grows by > 2^8),
 //               writes P (bf16) to TMEM; epilogue O / l -> bf16 rows staged in
-//               a dedicated shared-memory tile (swizzled like a loaded tile); LSE.
+//               shared memory (swizzled like a loaded tile), LSE.
 // The S region is reused by S_{t+1} only after the softmax of tile t has
 // released it (p_full); P has its own region, so S_{t+1} overlaps nothing the
 // PV MMA still reads.  Every commit tracks all earlier MMAs, so s_full(t) also
@@ -61,9 +60,7 @@ struct FwdSmem {
   alignas(1024) uint8_t q[2][kTileBytes];
   alignas(1024) uint8_t k[2][kTileBytes];
   alignas(1024) uint8_t v[2][kTileBytes];
-  alignas(1024) uint8_t ostage[kTileBytes];   // O tile staged for its TMA store (swizzled like a loaded tile)
-  uint64_t q_full[2], q_empty[2], k_full[2], v_full[2], kv_empty[2], s_full, s_free, p_full, pv_done, o_full,
-      o_staged, o_free;
+  uint64_t q_full[2], o_staged[2], k_full[2], v_full[2], kv_empty[2], s_full, s_free, p_full, pv_done, o_full;
   uint32_t tmem_base;
 };
 
@@ -234,16 +231,13 @@ __global__ void __launch_bounds__(kThreads, 2)
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                     const FwdParams prm) {
   extern __shared__ uint8_t smem_raw[];
-  // the swizzled tiles need a 1024-byte aligned base; the dynamic window starts after the
-  // CTA's 1 KB reserved region, so no alignment slack is allocated (checked, fails loudly)
-  if ((sm100::smem_u32(smem_raw) & 1023u) != 0) __trap();
-  FwdSmem<D>& sm = *reinterpret_cast<FwdSmem<D>*>(smem_raw);
+  FwdSmem<D>& sm = *reinterpret_cast<FwdSmem<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < 2; ++s) {
       sm100::mbar_init(&sm.q_full[s], 1);
-      sm100::mbar_init(&sm.q_empty[s], 1);      // MMA commit: every S MMA of the stage's unit retired
+      sm100::mbar_init(&sm.o_staged[s], 128);   // softmax threads: O(n) staged in Q stage n&1
       sm100::mbar_init(&sm.k_full[s], 1);
       sm100::mbar_init(&sm.v_full[s], 1);
       sm100::mbar_init(&sm.kv_empty[s], 1);
@@ -253,8 +247,6 @@ __global__ void __launch_bounds__(kThreads, 2)
     sm100::mbar_init(&sm.p_full, 128);
     sm100::mbar_init(&sm.pv_done, 1);
     sm100::mbar_init(&sm.o_full, 1);
-    sm100::mbar_init(&sm.o_staged, 128);   // softmax threads: O(n) staged in sm.ostage
-    sm100::mbar_init(&sm.o_free, 1);       // warp 0: the TMA store of O(n) has read sm.ostage
     sm100::fence_mbar_init();
     sm100::tma_prefetch_desc(&tmQ);
     sm100::tma_prefetch_desc(&tmK);
@@ -286,27 +278,24 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint64_t pol_kv = sm100::policy_evict_last();
       int64_t tag0 = -1, tag1 = -1;   // (b, h, kv-block) held by K/V stage 0 / 1
       uint32_t g = 0, n_units = 0;
-      // O tile of unit us (staged in sm.ostage by the softmax warps) -> global, then
-      // release the staging tile; ragged tiles were written row by row by the softmax warps
-      auto store_o = [&](uint32_t m, int32_t us) {
-        sm100::mbar_wait(&sm.o_staged, m & 1);
+      int32_t staged0 = 0, staged1 = 0;   // unit whose O is staged in Q stage 0 / 1
+      // O tile of unit us (staged in Q stage qs, swizzled like a loaded tile) -> global;
+      // ragged tiles were written row by row by the softmax warps
+      auto store_o = [&](int qs, int32_t us) {
         const int32_t sqb = us % mq, sh = (us / mq) % prm.heads, sb = us / (mq * prm.heads);
-        if ((sqb + 1) * kBlock <= prm.N) {
-          if (kGather) {
-            const int4 c = row_cells<true>(prm.N, sqb * kBlock, prm.s2c, lane);
-            const int32_t base = sb * prm.N;
-            sm100::tma_scatter4(&tmO, sm.ostage + lane * 4 * D * 2, sh * D, base + c.x, base + c.y, base + c.z,
-                                base + c.w);
-          } else if (lane == 0) {
-            sm100::tma_store_3d(&tmO, sm.ostage, 0, sh, sb * prm.N + sqb * kBlock);
-          }
-          sm100::bulk_commit_group();
-          sm100::bulk_wait_group_read0();
+        if ((sqb + 1) * kBlock > prm.N) return;
+        if (kGather) {
+          const int4 c = row_cells<true>(prm.N, sqb * kBlock, prm.s2c, lane);
+          const int32_t base = sb * prm.N;
+          sm100::tma_scatter4(&tmO, sm.q[qs] + lane * 4 * D * 2, sh * D, base + c.x, base + c.y, base + c.z,
+                              base + c.w);
+        } else if (lane == 0) {
+          sm100::tma_store_3d(&tmO, sm.q[qs], 0, sh, sb * prm.N + sqb * kBlock);
         }
+        sm100::bulk_commit_group();
+        sm100::bulk_wait_group_read0();   // the stage may be refilled once the engine has read it
         __syncwarp();
-        if (lane == 0) sm100::mbar_arrive(&sm.o_free);
       };
-      int32_t prev_u = 0;
       FwdIter it;
       it.init(prm.row_ptr, mq, units);
       int32_t meta = 0, pmeta = 0;
@@ -318,18 +307,19 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int32_t qb = it.u % mq, h = (it.u / mq) % prm.heads, b = it.u / (mq * prm.heads);
         const int64_t bh = (int64_t)b * prm.heads + h;
         if (warp == 0) {
-          // Q(n) goes into stage n&1 once every S MMA of unit n-2 has retired
+          // Q(n) goes into stage n&1, which holds O(n-2) staged by the softmax warps:
+          // store that tile first (TMA store / scatter4), then reuse the stage
           const int qs = it.n & 1;
           const int4 cells = row_cells<kGather>(prm.N, qb * kBlock, prm.s2c, lane);
-          if (it.n >= 2) sm100::mbar_wait(&sm.q_empty[qs], ((it.n >> 1) - 1) & 1);
+          if (it.n >= 2) {
+            sm100::mbar_wait(&sm.o_staged[qs], ((it.n >> 1) - 1) & 1);
+            store_o(qs, qs ? staged1 : staged0);
+          }
+          if (qs) staged1 = it.u; else staged0 = it.u;
           if (lane == 0) HLA_TR((3 << 24) | (1 << 16) | it.n);
           if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.q_full[qs], FwdSmem<D>::kTileBytes);
           __syncwarp();
           issue_rows<D, kGather>(sm.q[qs], &tmQ, &sm.q_full[qs], h, b, prm.N, qb * kBlock, cells, pol_q, lane);
-          // then the previous unit's O tile (its S MMAs are done long before its epilogue;
-          // Q(n + 1) waits behind this store, with one unit of slack)
-          if (it.n >= 1) store_o(it.n - 1, prev_u);
-          prev_u = it.u;
           ++n_units;
         } else {
           const bool is_k = warp == 2;
@@ -359,8 +349,12 @@ __global__ void __launch_bounds__(kThreads, 2)
           pmeta = load_meta(prm.col_idx, prm.kind, it.prs, it.pre - it.prs, lane);
         }
       }
-      if (warp == 0 && n_units > 0) {
-        store_o(n_units - 1, prev_u);
+      if (warp == 0) {
+        // the last (up to) two units' O tiles are still staged
+        for (uint32_t m = n_units >= 2 ? n_units - 2 : 0; m < n_units; ++m) {
+          sm100::mbar_wait(&sm.o_staged[m & 1], (m >> 1) & 1);
+          store_o(m & 1, (m & 1) ? staged1 : staged0);
+        }
         sm100::bulk_wait_group0();
       }
     } else if (warp == 1 && lane == 0) {
@@ -368,14 +362,13 @@ __global__ void __launch_bounds__(kThreads, 2)
       constexpr uint32_t idesc_s = sm100::make_idesc_bf16(kBlock, kBlock, false, false);
       constexpr uint32_t idesc_o = sm100::make_idesc_bf16(kBlock, D, false, true);
       const uint32_t tS = tmem + kColS, tP = tmem + kColP, tO = tmem + kColO;
-      auto issue_s = [&](uint32_t n, uint32_t gg, bool last_of_unit) {
+      auto issue_s = [&](uint32_t n, uint32_t gg) {
         const uint8_t* q = sm.q[n & 1];
         const uint8_t* k = sm.k[gg & 1];
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
           sm100::mma_ss(tS, kmajor_desc<D>(q, kk), kmajor_desc<D>(k, kk), idesc_s, kk > 0);
         sm100::mma_commit(&sm.s_full);
-        if (last_of_unit) sm100::mma_commit(&sm.q_empty[n & 1]);   // Q stage free for unit n + 2
       };
       FwdIter it;   // always one tile ahead of the PV being issued
       it.init(prm.row_ptr, mq, units);
@@ -384,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         sm100::mbar_wait(&sm.q_full[0], 0);
         sm100::mbar_wait(&sm.k_full[0], 0);
         sm100::tc_fence_after();
-        issue_s(0, 0, it.nt == 1);
+        issue_s(0, 0);
       }
       while (it.valid) {
         const int32_t ct = it.t, cnt = it.nt;
@@ -399,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           if (s_pending && (it.t != 0 || sm100::mbar_test_wait(&sm.q_full[it.n & 1], (it.n >> 1) & 1)) &&
               sm100::mbar_test_wait(&sm.k_full[(g + 1) & 1], ((g + 1) >> 1) & 1)) {
             sm100::tc_fence_after();
-            issue_s(it.n, g + 1, it.t == it.nt - 1);
+            issue_s(it.n, g + 1);
             s_pending = false;
             continue;
           }
@@ -561,9 +554,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       // TMA store / 32 scatter4 (full 128-B lines, no LSU store queue in this warp's way).
       // Ragged tiles: rows written directly.
       const bool staged = (qb + 1) * kBlock <= prm.N;
-      const uint32_t stage = sm100::smem_u32(sm.ostage);
-      // the previous unit's O store must have read the staging tile
-      if (it.n >= 1) sm100::mbar_wait(&sm.o_free, (it.n - 1) & 1);
+      const uint32_t stage = sm100::smem_u32(sm.q[it.n & 1]);
 #pragma unroll
       for (int v4 = 0; v4 < D / 8; ++v4) {
         uint4 w;
@@ -579,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
       sm100::fence_proxy_async_smem();
-      sm100::mbar_arrive(&sm.o_staged);
+      sm100::mbar_arrive(&sm.o_staged[it.n & 1]);
       if (row == 0) HLA_TR((2 << 24) | (4 << 16) | it.n);
       const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
       if (real)
@@ -606,7 +597,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 template <int D, bool kTwoD, bool kGather, bool kBias>
 hla_status launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mo,
                       const FwdParams& prm, int32_t n_qblocks, cudaStream_t stream) {
-  const size_t smem = sizeof(FwdSmem<D>);   // 2 CTAs per SM at d = 64: 2 x (113 KB + 1 KB reserved)
+  const size_t smem = sizeof(FwdSmem<D>) + 1024;
   auto* fn = attn_fwd_kernel<D, kTwoD, kGather, kBias>;
   HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t units = (int64_t)n_qblocks * prm.heads * prm.batch;
