@@ -4,6 +4,7 @@ Bar: bit-exact for the Hilbert index, the permutation, tile kinds, CSR lists,
 counts and ratios (north_star); tcgen05 microtest vs an fp32 matmul of the same
 bf16 operands (exact products, fp32 sums: tight tolerance)."""
 
+import os
 import numpy as np
 import pytest
 import torch
@@ -162,3 +163,19 @@ def test_bwd_plan_executable_and_exact(kind, H, W, wh, ww):
     _check_bwd_plan(m)
     if kind == "HWA" and (wh * ww) % 256 == 0:
         assert m.n_dq_nonlocal == 0      # windows of whole kv-block pairs: every dQ finishes in TMEM
+
+
+@pytest.mark.gpu
+def test_compute_sanitizer_memcheck_clean():
+    """SURVEY 4.2 tier T3: memcheck over small fwd + bwd workloads (tools/sanitize.py) reports no errors."""
+    import shutil
+    import subprocess
+    import sys
+    exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(exe):
+        pytest.skip("compute-sanitizer not installed")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([exe, "--tool", "memcheck", "--error-exitcode", "3", sys.executable,
+                        os.path.join(root, "tools", "sanitize.py")], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "ERROR SUMMARY: 0 errors" in r.stdout + r.stderr
