@@ -284,27 +284,35 @@ def run_stack(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+
+    def run(steps, marks):
+        recs = []
+        for _ in range(steps):
+            flush.zero_()
+            ev = [("start", torch.cuda.Event(enable_timing=True))]
+            ev[0][1].record()
+
+            def mark(name, ev=ev):
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                ev.append((name, e))
+            one_step(mark if marks else None)
+            if not marks:
+                mark("end")
+            recs.append(ev)
+        torch.cuda.synchronize()
+        return recs
+
+    # the step: one start / end event pair; the per-stage sums: a second, instrumented run
     sampler = ClockSampler(local)
     sampler.start()
-    totals, per = [], {}
-    for _ in range(args.steps):
-        flush.zero_()
-        ev = [("start", torch.cuda.Event(enable_timing=True))]
-        ev[0][1].record()
-
-        def mark(name, ev=ev):
-            e = torch.cuda.Event(enable_timing=True)
-            e.record()
-            ev.append((name, e))
-        one_step(mark)
-        totals.append(ev)
-    torch.cuda.synchronize()
+    totals = run(args.steps, False)
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
-    step = []
-    for ev in totals:
-        step.append(ev[0][1].elapsed_time(ev[-1][1]))
+    step = [ev[0][1].elapsed_time(ev[-1][1]) for ev in totals]
+    per = {}
+    for ev in run(args.steps, True):
         for (_, a), (name, b) in zip(ev[:-1], ev[1:]):
             per[name] = per.get(name, 0.0) + a.elapsed_time(b) / args.steps
     step_ms = reduce_max_ms(statistics.mean(step), dist if world > 1 else None, dev)
