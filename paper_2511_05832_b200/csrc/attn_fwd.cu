@@ -65,6 +65,7 @@ struct FwdSmem {
   // kBias, D = 32: the tile's bias window (offset box of q-block cells minus kv-block
   // cells, table values * log2 e), double-buffered by tile parity
   float bias_win[2][kBias && D == 32 ? 2048 : 1];
+  alignas(16) int32_t key_off[2][kBias && D == 32 ? 128 : 4];   // 4 * B'_k of the tile's keys (same parity)
 };
 
 template <int D>
@@ -528,6 +529,10 @@ __global__ void __launch_bounds__(kThreads, 2)
             w_aq = ((q_rc >> 16) - dr0) * wc + ((q_rc & 0xffff) - dc0);
             w_bk = make_int4((kr4[0] >> 16) * wc + (kr4[0] & 0xffff), (kr4[1] >> 16) * wc + (kr4[1] & 0xffff),
                              (kr4[2] >> 16) * wc + (kr4[2] & 0xffff), (kr4[3] >> 16) * wc + (kr4[3] & 0xffff));
+            // byte offsets of the 128 keys, read back as warp-uniform (broadcast) 16-B loads
+            if (quarter == 0)
+              sm100::sts_u4(sm100::smem_u32(sm.key_off[g & 1]) + 16u * lane, 4 * w_bk.x, 4 * w_bk.y, 4 * w_bk.z,
+                            4 * w_bk.w);
           } else {
             // direct table index A_q - B_k (B_k = kr (2W - 1) + kc)
             w_aq = prm.rpb_a0 + (q_rc >> 16) * prm.rpb_w + (q_rc & 0xffff);
@@ -574,10 +579,14 @@ __global__ void __launch_bounds__(kThreads, 2)
           const int32_t bkr[4] = {w_bk.x, w_bk.y, w_bk.z, w_bk.w};
           if (win) {
             const uint32_t wb = sm100::smem_u32(sm.bias_win[g & 1]) + 4u * (uint32_t)w_aq;
+            const uint32_t ko = sm100::smem_u32(sm.key_off[g & 1]);
 #pragma unroll
-            for (int c = 0; c < kBlock; ++c) {
-              const int32_t b_k = __shfl_sync(0xffffffffu, bkr[c & 3], c >> 2);
-              s[c] = fmaf(s[c], sl2, sm100::lds_f32(wb - 4u * (uint32_t)b_k));
+            for (int c4 = 0; c4 < kBlock / 4; ++c4) {
+              const float4 o = sm100::lds_f4(ko + 16u * c4);
+              const uint32_t ov[4] = {__float_as_uint(o.x), __float_as_uint(o.y), __float_as_uint(o.z),
+                                      __float_as_uint(o.w)};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) s[4 * c4 + j] = fmaf(s[4 * c4 + j], sl2, sm100::lds_f32(wb - ov[j]));
             }
           } else {
 #pragma unroll
