@@ -81,6 +81,7 @@ struct BwdSmem {
   alignas(1024) float dq_stage[kBlock * 32];    // fp32 dQ half tile [128][32], SWIZZLE_128B
   alignas(16) float lse[2][kBlock];
   alignas(16) float dd[2][kBlock];
+  alignas(16) int32_t qa[2][kBias ? kBlock : 4];   // kBias: A_q of the stage's query columns (RPB table index = A_q - B_k)
   uint64_t kv_full[2], kv_empty[2], q_full[2], q_empty[2], s_full[2], ds_ready[2], dq_full[2], dq_free[2], dkv_full,
       epi_done;
   uint64_t dbg_bar;
@@ -311,6 +312,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (s) stage_tag1 = tag; else stage_tag0 = tag;
           if (role == 0) {
+            if (kBias) {
+              // A_q = (qr + H - 1)(2W - 1) + qc + W - 1 of the q-block's 128 columns (phantom: cell 0),
+              // read by the compute warps as warp-uniform 16-B loads next to LSE / D
+              const int4 rc = make_int4(rpb_cell_rc(prm.cells, qblk * kBlock + 4 * lane, prm.N, prm.grid_w),
+                                        rpb_cell_rc(prm.cells, qblk * kBlock + 4 * lane + 1, prm.N, prm.grid_w),
+                                        rpb_cell_rc(prm.cells, qblk * kBlock + 4 * lane + 2, prm.N, prm.grid_w),
+                                        rpb_cell_rc(prm.cells, qblk * kBlock + 4 * lane + 3, prm.N, prm.grid_w));
+              const int32_t a0 = (prm.grid_h - 1) * prm.rpb_w + prm.grid_w - 1;
+              auto a_of = [&](int32_t v) { return a0 + (v >> 16) * prm.rpb_w + (v & 0xffff); };
+              sm100::sts_u4(sm100::smem_u32(sm.qa[s]) + 16u * lane, a_of(rc.x), a_of(rc.y), a_of(rc.z), a_of(rc.w));
+              __syncwarp();   // every lane's A_q is written before lane 0 arrives on q_full
+            }
             if (lane == 0) {
               // LSE / D of the real rows only (ragged last tile: N % 4 == 0, so 16-B multiples)
               const uint32_t vbytes = (uint32_t)min(kBlock, prm.N - qblk * kBlock) * 4u;
@@ -483,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       RowBox box = clip_box<kTwoD>(prm.pat, col_box(prm.pat, kidx));
       if (kidx >= prm.N) box.len = 0;   // phantom key row of a ragged tile: nothing allowed
       // RPB: this key row's cell, the key block's cell box, the head's table / gradient
-      int32_t k_r = 0, k_c = 0;
+      int32_t k_r = 0, k_c = 0, k_b = 0;
       CellBox kbox{0, 0, 0, 0};
       const float* rpbh = nullptr;
       float* drpbh = nullptr;
@@ -491,6 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int32_t rc = rpb_cell_rc(prm.cells, kidx, prm.N, prm.grid_w);
         k_r = rc >> 16;
         k_c = rc & 0xffff;
+        k_b = k_r * prm.rpb_w + k_c;
         kbox = rpb_block_box(prm.cells, kb * kBlock, prm.N, prm.grid_w, lane);
         rpbh = prm.rpb + (int64_t)h * prm.rpb_hw;
         drpbh = prm.drpb + (int64_t)h * prm.rpb_hw;
@@ -517,6 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (row == 0 && cset == 0) HLA_TR((2 << 24) | ((1) << 16) | (g));
         const uint32_t lse2 = sm100::smem_u32(sm.lse[s]);
         const uint32_t dd = sm100::smem_u32(sm.dd[s]);
+        const uint32_t qa = sm100::smem_u32(sm.qa[s]);
         const uint32_t dsbuf = sm100::smem_u32(sm.ds[g & 1]);
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
@@ -554,14 +569,18 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int qc = c * 32 + u4 * 8;
               const float4 la = sm100::lds_f4(lse2 + qc * 4), lb = sm100::lds_f4(lse2 + qc * 4 + 16);
               const float lv[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
+              int32_t av[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+              if (kBias) {
+                const float4 xa = sm100::lds_f4(qa + qc * 4), xb = sm100::lds_f4(qa + qc * 4 + 16);
+                av[0] = __float_as_int(xa.x); av[1] = __float_as_int(xa.y); av[2] = __float_as_int(xa.z);
+                av[3] = __float_as_int(xa.w); av[4] = __float_as_int(xb.x); av[5] = __float_as_int(xb.y);
+                av[6] = __float_as_int(xb.z); av[7] = __float_as_int(xb.w);
+              }
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
                 float x = fmaf(__uint_as_float(sr[u4 * 8 + e]), sl2, -lv[e]);
-                if (kBias) {   // + bias * log2(e), bias = table[h][dr + H - 1][dc + W - 1]
-                  const int32_t rc = __shfl_sync(0xffffffffu, q_rc, u4 * 8 + e);
-                  const int32_t ti = ((rc >> 16) - k_r + prm.grid_h - 1) * prm.rpb_w + ((rc & 0xffff) - k_c + prm.grid_w - 1);
-                  x = fmaf(__ldg(rpbh + ti), 1.4426950408889634f, x);
-                }
+                if (kBias)   // + bias * log2(e), bias = table[h][dr + H - 1][dc + W - 1] = table[A_q - B_k]
+                  x = fmaf(__ldg(rpbh + (av[e] - k_b)), 1.4426950408889634f, x);
                 p[u4 * 8 + e] = sm100::ex2(x);
               }
             }
