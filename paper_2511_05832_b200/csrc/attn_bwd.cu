@@ -62,7 +62,10 @@ struct BwdParams {
   unsigned long long* visited;
 };
 
-constexpr int kRpbWin = 2048;   // entries of the per-tile dRPB window (offset box) in shared memory
+// entries of the per-tile dRPB window (offset rows of the tile's box, full table row stride
+// 2W - 1) in shared memory; more at D = 32, where the smaller tiles leave room
+template <int D>
+constexpr int rpb_win_cap() { return D == 32 ? 4096 : 2048; }
 // The window accumulates in 32-bit fixed point: shared-memory fp32 atomics are
 // compare-and-swap loops on sm_100 (ATOMS.CAST.SPIN, measured in SASS) while
 // integer ATOMS.ADD is native.  Resolution 2^-16 (absolute; dS values are
@@ -86,7 +89,7 @@ struct BwdSmem {
       epi_done;
   uint64_t dbg_bar;
   uint32_t tmem_base;
-  int32_t rpb_win[kBias ? kRpbWin : 1];   // dRPB of the current tile's offset box, fixed point (compute warps)
+  int32_t rpb_win[kBias ? rpb_win_cap<D>() : 1];   // dRPB of the current tile's offset box, fixed point (compute warps)
 };
 
 template <int D>
@@ -482,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = prm.scale_log2, scale = prm.scale;
     if (kBias) {   // the dRPB window starts (and is left after every flush) zeroed
-      for (int i = (warp - 2) * 32 + lane; i < kRpbWin; i += 256) sm.rpb_win[i] = 0;
+      for (int i = (warp - 2) * 32 + lane; i < rpb_win_cap<D>(); i += 256) sm.rpb_win[i] = 0;
       sm100::named_bar_sync(3, 256);
     }
     uint32_t n = 0, g = 0;
@@ -513,19 +516,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = g & 1;
         const uint8_t kd = __ldg(prm.t_kind + rs + t);
         const int32_t q0 = __ldg(prm.t_col_idx + rs + t) * kBlock;
-        // RPB: cells of this warp set's two query chunks (lane e: column 32c + e), the
-        // tile's offset box (dr, dc) = q box - key box, and whether it fits the window
-        int32_t qrc[2] = {0, 0};
-        int32_t dr0 = 0, dc0 = 0, wc = 0;
+        // RPB: the tile's offset box (dr, dc) = q box - key box and whether its rows fit
+        // the shared-memory dRPB window (query offsets A_q come staged with LSE / D)
+        int32_t dr0 = 0, dc0 = 0, wc = 0, wrows = 0, kwb = 0;
         bool win = false;
         if (kBias) {
-          qrc[0] = rpb_cell_rc(prm.cells, q0 + 32 * cset + lane, prm.N, prm.grid_w);
-          qrc[1] = rpb_cell_rc(prm.cells, q0 + 32 * (2 + cset) + lane, prm.N, prm.grid_w);
           const CellBox qbox = rpb_block_box(prm.cells, q0, prm.N, prm.grid_w, lane);
           dr0 = qbox.r0 - kbox.r1;
           dc0 = qbox.c0 - kbox.c1;
-          wc = qbox.c1 - kbox.c0 - dc0 + 1;
-          win = (qbox.r1 - kbox.r0 - dr0 + 1) * wc <= kRpbWin;
+          // window = the box's offset rows at the table's own row stride, so that the element
+          // index (dr - dr0) * wc + (dc - dc0) = A_q - kwb (A_q staged per q-block)
+          wc = prm.rpb_w;
+          wrows = qbox.r1 - kbox.r0 - dr0 + 1;
+          win = wrows * wc <= rpb_win_cap<D>();
+          kwb = (prm.grid_h - 1) * prm.rpb_w + prm.grid_w - 1 + k_b + dr0 * wc + dc0;
         }
         sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1);
         if (row == 0 && cset == 0) HLA_TR((2 << 24) | ((1) << 16) | (g));
@@ -540,7 +544,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           sm100::tc_fence_after();
           {
             const int c = 2 * half + cset;
-            const int32_t q_rc = half ? qrc[1] : qrc[0];   // RPB: cell of query column 32c + lane
             uint32_t sr[32], dpr[32];
             sm100::tmem_ld32(tmem + lane_off + kColS + c * 32, sr);
             sm100::tmem_ld32(tmem + lane_off + kColDP + c * 32, dpr);
@@ -625,19 +628,21 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (kBias) {
                 // dRPB[offset] += dL/dscore = dS / scale: into the tile's shared-memory
                 // offset window (flushed once per tile), else straight to global
+                const float4 xa = sm100::lds_f4(qa + qc * 4), xb = sm100::lds_f4(qa + qc * 4 + 16);
+                const int32_t av[8] = {__float_as_int(xa.x), __float_as_int(xa.y), __float_as_int(xa.z),
+                                       __float_as_int(xa.w), __float_as_int(xb.x), __float_as_int(xb.y),
+                                       __float_as_int(xb.z), __float_as_int(xb.w)};
+                const uint32_t wbase = sm100::smem_u32(sm.rpb_win);
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                  const int32_t rc = __shfl_sync(0xffffffffu, q_rc, u4 * 8 + e);
                   if (!((okbits >> (u4 * 8 + e)) & 1u)) continue;
-                  const int32_t dr = (rc >> 16) - k_r, dc = (rc & 0xffff) - k_c;
                   const float gv = ds[e] * prm.inv_scale;
-                  if (win) {
+                  if (win) {   // window index (dr - dr0) * (2W - 1) + (dc - dc0) = A_q - kwb
                     const int32_t fx = __float2int_rn(fminf(fmaxf(gv, -16384.f), 16384.f) * kRpbFix);
-                    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(sm100::smem_u32(&sm.rpb_win[(dr - dr0) * wc + (dc - dc0)])),
-                                 "r"(fx)
+                    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(wbase + 4u * (uint32_t)(av[e] - kwb)), "r"(fx)
                                  : "memory");
-                  } else {
-                    atomicAdd(drpbh + (dr + prm.grid_h - 1) * prm.rpb_w + (dc + prm.grid_w - 1), gv);
+                  } else {     // table index A_q - B_k
+                    atomicAdd(drpbh + (av[e] - k_b), gv);
                   }
                 }
               }
@@ -658,8 +663,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // flush the tile's dRPB window to global (and re-zero it) -- all 256 compute threads
           sm100::named_bar_sync(3, 256);
           const int tid = (warp - 2) * 32 + lane;
-          const int wr = kRpbWin / wc;
-          for (int i = tid; i < wr * wc; i += 256) {
+          for (int i = tid; i < wrows * wc; i += 256) {
             const int32_t v = sm.rpb_win[i];
             if (v != 0) {
               const int32_t dr = dr0 + i / wc, dc = dc0 + i % wc;
