@@ -66,6 +66,9 @@ struct FwdSmem {
   // cells, table values * log2 e), double-buffered by tile parity
   float bias_win[2][kBias && D == 32 ? 2048 : 1];
   alignas(16) int32_t key_off[2][kBias && D == 32 ? 128 : 4];   // 4 * B'_k of the tile's keys (same parity)
+  // kBias, D = 64: table offsets B_k of the keys of K/V stage s, written by the K producer
+  // before it arms k_full[s] (read by the softmax after waiting on the same phase)
+  alignas(16) int32_t key_b[2][kBias && D == 64 ? 128 : 4];
 };
 
 template <int D>
@@ -369,6 +372,11 @@ __global__ void __launch_bounds__(kThreads, 2)
               continue;
             }
             if (s) tag1 = tag; else tag0 = tag;
+            if (kBias && D == 64 && is_k) {
+              const int4 bk = rpb_key_offs(prm.cells, kvb * kBlock, prm.N, prm.grid_w, prm.rpb_w, lane);
+              sm100::sts_u4(sm100::smem_u32(sm.key_b[s]) + 16u * lane, bk.x, bk.y, bk.z, bk.w);
+              __syncwarp();   // every lane's offsets are written before lane 0 arms k_full
+            }
             if (lane == 0) sm100::mbar_arrive_expect_tx(full, FwdSmem<D, kBias>::kTileBytes);
             __syncwarp();
             issue_rows<D, kGather>(is_k ? sm.k[s] : sm.v[s], is_k ? &tmK : &tmV, full, h, b, prm.N, kvb * kBlock,
@@ -471,11 +479,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     // blocks being cheaper than the per-tile fill + barrier)
     constexpr int32_t kWin = D == 32 ? 2048 : 0;
     int4 krc_next = make_int4(-1, -1, -1, -1);   // kWin > 0
-    int4 bk_next = make_int4(0, 0, 0, 0);         // kWin == 0: key offsets B_k of the next tile
     if (kBias && it.valid) {
       const int32_t k0 = (tile_meta(meta, prm.col_idx, prm.kind, it.rs, 0) >> 2) * kBlock;
       if constexpr (kWin > 0) krc_next = rpb_rc4(prm.cells, k0, prm.N, prm.grid_w, lane);
-      else bk_next = rpb_key_offs(prm.cells, k0, prm.N, prm.grid_w, prm.rpb_w, lane);
+
     }
     while (it.valid) {
       const int32_t qb = it.u % mq, h = (it.u / mq) % prm.heads, b = it.u / (mq * prm.heads);
@@ -563,16 +570,17 @@ __global__ void __launch_bounds__(kThreads, 2)
         // so that the mask, the max and the exponentials see the biased score
         const float sl2e = kBias ? 1.f : sl2;
         if constexpr (kBias && kWin == 0) {
-          const int4 bk = bk_next;
-          // the next tile's key offsets (this unit's next tile, else the next unit's first)
-          const int32_t nt_kvb = (t + 1 < it.nt) ? (tile_meta(meta, prm.col_idx, prm.kind, it.rs, t + 1) >> 2)
-                                                 : (__shfl_sync(0xffffffffu, pmeta, 0) >> 2);
-          bk_next = rpb_key_offs(prm.cells, nt_kvb * kBlock, prm.N, prm.grid_w, prm.rpb_w, lane);
-          const int32_t bkr[4] = {bk.x, bk.y, bk.z, bk.w};
+          // key offsets B_k staged with K (warp-uniform 16-B loads); the k_full phase of this
+          // tile is complete (S used it) -- the wait makes the producer's writes visible
+          sm100::mbar_wait(&sm.k_full[g & 1], (g >> 1) & 1);
+          const uint32_t kbo = sm100::smem_u32(sm.key_b[g & 1]);
 #pragma unroll
-          for (int c = 0; c < kBlock; ++c) {
-            const int32_t b_k = __shfl_sync(0xffffffffu, bkr[c & 3], c >> 2);
-            s[c] = fmaf(s[c], sl2, __ldg(rpbh + (a_q - b_k)) * 1.4426950408889634f);
+          for (int c4 = 0; c4 < kBlock / 4; ++c4) {
+            const float4 o = sm100::lds_f4(kbo + 16u * c4);
+            const int32_t ov[4] = {__float_as_int(o.x), __float_as_int(o.y), __float_as_int(o.z), __float_as_int(o.w)};
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              s[4 * c4 + j] = fmaf(s[4 * c4 + j], sl2, __ldg(rpbh + (a_q - ov[j])) * 1.4426950408889634f);
           }
         }
         if constexpr (kBias && kWin > 0) {
