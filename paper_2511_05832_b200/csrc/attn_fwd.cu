@@ -62,13 +62,9 @@ struct FwdSmem {
   alignas(1024) uint8_t v[2][kTileBytes];
   uint64_t q_full[2], o_staged[2], k_full[2], v_full[2], kv_empty[2], s_full, s_free, p_full, pv_done, o_full;
   uint32_t tmem_base;
-  // kBias, D = 32: the tile's bias window (offset box of q-block cells minus kv-block
-  // cells, table values * log2 e), double-buffered by tile parity
-  float bias_win[2][kBias && D == 32 ? 2048 : 1];
-  alignas(16) int32_t key_off[2][kBias && D == 32 ? 128 : 4];   // 4 * B'_k of the tile's keys (same parity)
-  // kBias, D = 64: table offsets B_k of the keys of K/V stage s, written by the K producer
+  // kBias: table offsets B_k of the keys of K/V stage s, written by the K producer
   // before it arms k_full[s] (read by the softmax after waiting on the same phase)
-  alignas(16) int32_t key_b[2][kBias && D == 64 ? 128 : 4];
+  alignas(16) int32_t key_b[2][kBias ? 128 : 4];
 };
 
 template <int D>
@@ -232,35 +228,6 @@ __device__ __forceinline__ int4 rpb_key_offs(const int32_t* cells, int32_t k0, i
   return make_int4(off(c.x), off(c.y), off(c.z), off(c.w));
 }
 
-// packed (row << 16) | col of the 4 sequence positions s0 + 4 lane .. + 3 (-1: phantom, >= N)
-__device__ __forceinline__ int4 rpb_rc4(const int32_t* cells, int32_t s0, int32_t N, int32_t W, int lane) {
-  const int32_t s = s0 + 4 * lane;
-  int4 c = make_int4(-1, -1, -1, -1);
-  if (s < N) c = cells ? __ldg(reinterpret_cast<const int4*>(cells + s0) + lane) : make_int4(s, s + 1, s + 2, s + 3);
-  auto rc = [&](int32_t cell) { const int32_t r = cell / W; return (r << 16) | (cell - r * W); };
-  return make_int4(rc(c.x), rc(c.y), rc(c.z), rc(c.w));   // N % 4 == 0: a lane's 4 positions are all real or all phantom
-}
-struct RcBox { int32_t r0, r1, c0, c1; };
-// row / column range of the real positions held by the warp (4 per lane), identical in every lane
-__device__ __forceinline__ RcBox rpb_box(int4 rc) {
-  RcBox bx{1 << 30, -(1 << 30), 1 << 30, -(1 << 30)};
-  const int32_t v[4] = {rc.x, rc.y, rc.z, rc.w};
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-    if (v[j] >= 0) {
-      const int32_t r = v[j] >> 16, c = v[j] & 0xffff;
-      bx.r0 = min(bx.r0, r); bx.r1 = max(bx.r1, r); bx.c0 = min(bx.c0, c); bx.c1 = max(bx.c1, c);
-    }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    bx.r0 = min(bx.r0, __shfl_xor_sync(0xffffffffu, bx.r0, o));
-    bx.r1 = max(bx.r1, __shfl_xor_sync(0xffffffffu, bx.r1, o));
-    bx.c0 = min(bx.c0, __shfl_xor_sync(0xffffffffu, bx.c0, o));
-    bx.c1 = max(bx.c1, __shfl_xor_sync(0xffffffffu, bx.c1, o));
-  }
-  return bx;
-}
-
 template <int D, bool kTwoD, bool kGather, bool kBias>
 __global__ void __launch_bounds__(kThreads, 2)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -372,7 +339,7 @@ __global__ void __launch_bounds__(kThreads, 2)
               continue;
             }
             if (s) tag1 = tag; else tag0 = tag;
-            if (kBias && D == 64 && is_k) {
+            if (kBias && is_k) {
               const int4 bk = rpb_key_offs(prm.cells, kvb * kBlock, prm.N, prm.grid_w, prm.rpb_w, lane);
               sm100::sts_u4(sm100::smem_u32(sm.key_b[s]) + 16u * lane, bk.x, bk.y, bk.z, bk.w);
               __syncwarp();   // every lane's offsets are written before lane 0 arms k_full
@@ -473,17 +440,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       meta = load_meta(prm.col_idx, prm.kind, it.rs, it.nt, lane);
       pmeta = load_meta(prm.col_idx, prm.kind, it.prs, it.pre - it.prs, lane);
     }
-    // RPB: cells (packed row / col) of the next tile's keys, loaded one tile ahead
-    // staged windows only at D = 32 (measured: cfg5 fwd 3.79 -> 3.62 ms; at D = 64 the
-    // cfg2 HWA + RPB fwd went 0.221 -> 0.244 ms, its L1 gather over compact Hilbert
-    // blocks being cheaper than the per-tile fill + barrier)
-    constexpr int32_t kWin = D == 32 ? 2048 : 0;
-    int4 krc_next = make_int4(-1, -1, -1, -1);   // kWin > 0
-    if (kBias && it.valid) {
-      const int32_t k0 = (tile_meta(meta, prm.col_idx, prm.kind, it.rs, 0) >> 2) * kBlock;
-      if constexpr (kWin > 0) krc_next = rpb_rc4(prm.cells, k0, prm.N, prm.grid_w, lane);
-
-    }
+    // RPB: the row's table offset A_q (per unit); the keys' B_k come staged with K
     while (it.valid) {
       const int32_t qb = it.u % mq, h = (it.u / mq) % prm.heads, b = it.u / (mq * prm.heads);
       const int32_t q = qb * kBlock + row;
@@ -492,66 +449,9 @@ __global__ void __launch_bounds__(kThreads, 2)
       const bool real = q < prm.N;
       const int32_t ocell = kGather ? (real ? __ldg(prm.s2c + q) : 0) : q;   // fused inverse reorder of O (used at the end)
       const float* rpbh = kBias ? prm.rpb + (int64_t)h * prm.rpb_hw : nullptr;
-      // RPB: this unit's q-block cell box; the row's cell (phantom rows: the box corner,
-      // which keeps every window index in range)
-      RcBox qbox{0, 0, 0, 0};
-      int32_t q_rc = 0;
-      const int32_t a_q = (kBias && kWin == 0) ? prm.rpb_a0 + rpb_cell_off(prm.cells, q, prm.N, prm.grid_w, prm.rpb_w) : 0;
-      if (kBias && kWin > 0) {
-        qbox = rpb_box(rpb_rc4(prm.cells, qb * kBlock, prm.N, prm.grid_w, lane));
-        if (real) {
-          const int32_t cell = prm.cells ? __ldg(prm.cells + q) : q;
-          const int32_t r = cell / prm.grid_w;
-          q_rc = (r << 16) | (cell - r * prm.grid_w);
-        } else {
-          q_rc = (qbox.r0 << 16) | qbox.c0;
-        }
-      }
+      const int32_t a_q = kBias ? prm.rpb_a0 + rpb_cell_off(prm.cells, q, prm.N, prm.grid_w, prm.rpb_w) : 0;
       if (row == 0) HLA_TR((2 << 24) | (6 << 16) | it.n);
       for (int t = 0; t < it.nt; ++t, ++g) {
-        // RPB window of this tile: offsets (dr, dc) = q cell - k cell over the two cell
-        // boxes; its table entries (x log2 e) are staged in shared memory by the 128
-        // softmax threads while the S MMA runs, so the per-element bias is a shared-memory
-        // gather instead of an L1 gather.  Windows larger than kWin use the table directly.
-        int32_t w_aq = 0;
-        int4 w_bk = make_int4(0, 0, 0, 0);
-        bool win = false;
-        if constexpr (kBias && kWin > 0) {
-          const int4 krc = krc_next;
-          const RcBox kb = rpb_box(krc);
-          const int32_t dr0 = qbox.r0 - kb.r1, dc0 = qbox.c0 - kb.c1;
-          const int32_t wc = qbox.c1 - kb.c0 - dc0 + 1, wr = qbox.r1 - kb.r0 - dr0 + 1;
-          win = wr * wc <= kWin;
-          const int32_t kfill = (kb.r0 << 16) | kb.c0;   // phantom keys -> the box corner
-          const int32_t kr4[4] = {krc.x < 0 ? kfill : krc.x, krc.y < 0 ? kfill : krc.y, krc.z < 0 ? kfill : krc.z,
-                                  krc.w < 0 ? kfill : krc.w};
-          if (win) {
-            float* wbuf = sm.bias_win[g & 1];
-            const int32_t n = wr * wc;
-            for (int i = row; i < n; i += 128) {
-              const int32_t ir = i / wc;
-              wbuf[i] = __ldg(rpbh + (dr0 + ir + prm.grid_h - 1) * prm.rpb_w + (dc0 + i - ir * wc + prm.grid_w - 1)) *
-                        1.4426950408889634f;
-            }
-            w_aq = ((q_rc >> 16) - dr0) * wc + ((q_rc & 0xffff) - dc0);
-            w_bk = make_int4((kr4[0] >> 16) * wc + (kr4[0] & 0xffff), (kr4[1] >> 16) * wc + (kr4[1] & 0xffff),
-                             (kr4[2] >> 16) * wc + (kr4[2] & 0xffff), (kr4[3] >> 16) * wc + (kr4[3] & 0xffff));
-            // byte offsets of the 128 keys, read back as warp-uniform (broadcast) 16-B loads
-            if (quarter == 0)
-              sm100::sts_u4(sm100::smem_u32(sm.key_off[g & 1]) + 16u * lane, 4 * w_bk.x, 4 * w_bk.y, 4 * w_bk.z,
-                            4 * w_bk.w);
-          } else {
-            // direct table index A_q - B_k (B_k = kr (2W - 1) + kc)
-            w_aq = prm.rpb_a0 + (q_rc >> 16) * prm.rpb_w + (q_rc & 0xffff);
-            w_bk = make_int4((kr4[0] >> 16) * prm.rpb_w + (kr4[0] & 0xffff), (kr4[1] >> 16) * prm.rpb_w + (kr4[1] & 0xffff),
-                             (kr4[2] >> 16) * prm.rpb_w + (kr4[2] & 0xffff), (kr4[3] >> 16) * prm.rpb_w + (kr4[3] & 0xffff));
-          }
-          // the next tile's key cells (this unit's next tile, else the next unit's first)
-          const int32_t nt_kvb = (t + 1 < it.nt) ? (tile_meta(meta, prm.col_idx, prm.kind, it.rs, t + 1) >> 2)
-                                                 : (__shfl_sync(0xffffffffu, pmeta, 0) >> 2);
-          krc_next = rpb_rc4(prm.cells, nt_kvb * kBlock, prm.N, prm.grid_w, lane);
-          sm100::named_bar_sync(1, 128);   // window complete (buffer g&1 of tile g-2 no longer read)
-        }
         sm100::mbar_wait(&sm.s_full, g & 1);
         if (row == 0) HLA_TR((2 << 24) | (1 << 16) | g);
         sm100::tc_fence_after();
@@ -569,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         // kBias: scores move to the log2 domain here (s = S * scale * log2e + bias * log2e)
         // so that the mask, the max and the exponentials see the biased score
         const float sl2e = kBias ? 1.f : sl2;
-        if constexpr (kBias && kWin == 0) {
+        if constexpr (kBias) {
           // key offsets B_k staged with K (warp-uniform 16-B loads); the k_full phase of this
           // tile is complete (S used it) -- the wait makes the producer's writes visible
           sm100::mbar_wait(&sm.k_full[g & 1], (g >> 1) & 1);
@@ -581,27 +481,6 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
             for (int j = 0; j < 4; ++j)
               s[4 * c4 + j] = fmaf(s[4 * c4 + j], sl2, __ldg(rpbh + (a_q - ov[j])) * 1.4426950408889634f);
-          }
-        }
-        if constexpr (kBias && kWin > 0) {
-          const int32_t bkr[4] = {w_bk.x, w_bk.y, w_bk.z, w_bk.w};
-          if (win) {
-            const uint32_t wb = sm100::smem_u32(sm.bias_win[g & 1]) + 4u * (uint32_t)w_aq;
-            const uint32_t ko = sm100::smem_u32(sm.key_off[g & 1]);
-#pragma unroll
-            for (int c4 = 0; c4 < kBlock / 4; ++c4) {
-              const float4 o = sm100::lds_f4(ko + 16u * c4);
-              const uint32_t ov[4] = {__float_as_uint(o.x), __float_as_uint(o.y), __float_as_uint(o.z),
-                                      __float_as_uint(o.w)};
-#pragma unroll
-              for (int j = 0; j < 4; ++j) s[4 * c4 + j] = fmaf(s[4 * c4 + j], sl2, sm100::lds_f32(wb - ov[j]));
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < kBlock; ++c) {
-              const int32_t b_k = __shfl_sync(0xffffffffu, bkr[c & 3], c >> 2);
-              s[c] = fmaf(s[c], sl2, __ldg(rpbh + (w_aq - b_k)) * 1.4426950408889634f);
-            }
           }
         }
         if ((tm & 3) == 2) apply_row_mask<kTwoD>(s, prm.pat, box, (tm >> 2) * kBlock);
