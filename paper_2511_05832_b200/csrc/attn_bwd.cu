@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int32_t q0 = __ldg(prm.t_col_idx + rs + t) * kBlock;
         // RPB: the tile's offset box (dr, dc) = q box - key box and whether its rows fit
         // the shared-memory dRPB window (query offsets A_q come staged with LSE / D)
-        int32_t dr0 = 0, dc0 = 0, wc = 0, wrows = 0, kwb = 0;
+        int32_t dr0 = 0, dc0 = 0, wc = 0, wrows = 0, wcols = 0, kwb = 0;
         bool win = false;
         if (kBias) {
           const CellBox qbox = rpb_block_box(prm.cells, q0, prm.N, prm.grid_w, lane);
@@ -528,6 +528,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // index (dr - dr0) * wc + (dc - dc0) = A_q - kwb (A_q staged per q-block)
           wc = prm.rpb_w;
           wrows = qbox.r1 - kbox.r0 - dr0 + 1;
+          wcols = qbox.c1 - kbox.c0 - dc0 + 1;   // offset columns actually used (<= wc)
           win = wrows * wc <= rpb_win_cap<D>();
           kwb = (prm.grid_h - 1) * prm.rpb_w + prm.grid_w - 1 + k_b + dr0 * wc + dc0;
         }
@@ -663,12 +664,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           // flush the tile's dRPB window to global (and re-zero it) -- all 256 compute threads
           sm100::named_bar_sync(3, 256);
           const int tid = (warp - 2) * 32 + lane;
-          for (int i = tid; i < wrows * wc; i += 256) {
-            const int32_t v = sm.rpb_win[i];
+          for (int i = tid; i < wrows * wcols; i += 256) {   // only the box's used columns
+            const int32_t ir = i / wcols, ic = i - ir * wcols;
+            const int32_t v = sm.rpb_win[ir * wc + ic];
             if (v != 0) {
-              const int32_t dr = dr0 + i / wc, dc = dc0 + i % wc;
-              atomicAdd(drpbh + (dr + prm.grid_h - 1) * prm.rpb_w + (dc + prm.grid_w - 1), (float)v * (1.f / kRpbFix));
-              sm.rpb_win[i] = 0;
+              atomicAdd(drpbh + (dr0 + ir + prm.grid_h - 1) * prm.rpb_w + (dc0 + ic + prm.grid_w - 1),
+                        (float)v * (1.f / kRpbFix));
+              sm.rpb_win[ir * wc + ic] = 0;
             }
           }
           sm100::named_bar_sync(3, 256);
