@@ -134,8 +134,12 @@ enum {
  * hla_hilbert_index -- the cached Hilbert path: seq_to_cell[s] = cell
  * (row*W + col) of the s-th curve position, cell_to_seq = its inverse.  Either
  * output may be NULL.  Curve: classic Hilbert d2xy with x = column, y = row,
- * starting at (0,0) (reading R1).  grid must be square 2^k with
- * 1 <= 2^k <= 32768, else HLA_ERR_UNSUPPORTED.
+ * starting at (0,0) (reading R1).  Square 2^k grids: computed on the
+ * device by a bit-loop kernel (asynchronous on `stream`).  Any other H x W
+ * (1 <= H*W < 2^30; the paper's 56^2, 96^2, 160^2, 128x256 rows): the
+ * generalized ("gilbert") curve, built on the host and copied -- this path
+ * synchronises `stream` before returning (DESIGN.md f4, reading R2).
+ * Invalid sizes: HLA_ERR_INVALID.
  */
 HLA_API hla_status hla_hilbert_index(int32_t grid_h, int32_t grid_w,
                              int32_t* seq_to_cell, int32_t* cell_to_seq,
