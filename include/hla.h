@@ -115,6 +115,11 @@ typedef struct {
   uint8_t* t_dq;                 /* [capacity] per transposed entry: HLA_DQ_* bits  */
   uint8_t* q_dq_local;           /* [n_qblocks] 1 = dQ rows written by bwd_main     */
   int32_t n_dq_nonlocal;         /* host: q-blocks with q_dq_local == 0 (-1: none)  */
+  /* Host copy of counts (nnz, n_full, n_partial, n_empty), written by the fill call of
+     hla_build_block_mask.  The backward picks its schedule from it: the full-tile
+     schedule when n_full >= n_partial, the half-tile schedule otherwise (all zero,
+     e.g. a mask not built by the library: half-tile).  The choice changes speed only. */
+  int64_t host_counts[4];
 } hla_block_mask;
 
 /* Bits of hla_block_mask.t_dq.  The backward walks the transposed lists in work

@@ -40,7 +40,8 @@ class BlockMaskC(ctypes.Structure):
                 ("row_ptr", ctypes.c_void_p), ("col_idx", ctypes.c_void_p), ("kind", ctypes.c_void_p),
                 ("t_row_ptr", ctypes.c_void_p), ("t_col_idx", ctypes.c_void_p), ("t_kind", ctypes.c_void_p),
                 ("counts", ctypes.c_void_p),
-                ("t_dq", ctypes.c_void_p), ("q_dq_local", ctypes.c_void_p), ("n_dq_nonlocal", ctypes.c_int32)]
+                ("t_dq", ctypes.c_void_p), ("q_dq_local", ctypes.c_void_p), ("n_dq_nonlocal", ctypes.c_int32),
+                ("host_counts", ctypes.c_int64 * 4)]
 
 
 class HlaError(RuntimeError):

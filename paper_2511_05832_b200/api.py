@@ -61,10 +61,11 @@ class BlockMask:
 
     @property
     def c(self):
+        hc = (ctypes.c_int64 * 4)(*(self.host_counts or (0, 0, 0, 0)))
         return BlockMaskC(self.row_ptr.numel() - 1, self.t_row_ptr.numel() - 1, self.col_idx.numel(),
                           self.row_ptr.data_ptr(), self.col_idx.data_ptr(), self.kind.data_ptr(),
                           self.t_row_ptr.data_ptr(), self.t_col_idx.data_ptr(), self.t_kind.data_ptr(),
-                          self.counts.data_ptr(), _dp(self.t_dq), _dp(self.q_dq_local), self.n_dq_nonlocal)
+                          self.counts.data_ptr(), _dp(self.t_dq), _dp(self.q_dq_local), self.n_dq_nonlocal, hc)
 
     @property
     def nnz(self):
@@ -131,7 +132,7 @@ def hla_build_block_mask(desc, device="cuda", stream=None, plan=True):
     c = m.c
     check("hla_build_block_mask", lib().hla_build_block_mask(ctypes.byref(desc), ctypes.byref(c), ctypes.byref(nnz),
                                                              _stream(stream)))
-    m.host_counts = tuple(int(x) for x in m.counts.cpu().tolist())
+    m.host_counts = tuple(int(x) for x in c.host_counts)   # written by the fill call
     if plan and desc.block_q == desc.block_k:
         hla_build_bwd_plan(m, stream)
     return m

@@ -7,250 +7,165 @@
 //   dV = P^T dO,  dS = scale P o (dO V^T - D),  dK = dS^T Q,  dQ = dS K.
 //
 // K7 bwd_preprocess : D = rowsum(dO o O) (fp32) and zero the fp32 dQ accumulator.
-// K8 attn_bwd_kernel: one CTA per (kv-block j, head, batch), walking the
-//    transposed CSR list of q-blocks i (ascending).  320 threads, 1 CTA / SM:
-//    warp 0     TMA: K_j, V_j once; per q-block Q_i, dO_i (+ LSE_i, D_i via bulk
-//               copy) into a 2-stage ring;
-//    warp 1     TMEM allocator + single-thread tcgen05.mma issuer:
-//                 S^T  = K_j Q_i^T     (SS, TMEM cols [0,128))
-//                 dP^T = V_j dO_i^T    (SS, TMEM cols [128,256))
-//                 dV  += P^T dO_i      (TS, P^T bf16 written over the first 16 columns of
-//                                       each 32-column S^T chunk; acc [384,448))
-//                 dK  += dS^T Q_i      (SS, dS^T bf16 in smem, K-major view; acc [448,512))
-//                 dQ_i (+)= dS K_j     (SS, same dS smem, MN-major view; two accumulators
-//                                       [256,320) / [320,384) chained by the mask's dQ plan)
-//    warps 2-9  thread = key row (two warps per TMEM lane quarter, one 32-column
-//               chunk each): P^T, dS^T from S^T, dP^T (mask only on partial
-//               tiles); final dK (warps 6-9), dV (warps 2-5) -> bf16;
-//    warps 10-13 thread = query row: at the end of a dQ chain, dQ_i -> bf16 dq rows
-//               (complete chains) or -> smem -> TMA reduce-add into the fp32
-//               accumulator (overlaps the next q-block's MMAs).
+// K8 attn_bwd_kernel: persistent, 1 CTA / SM, kv-major over the transposed CSR
+//    (work unit = a pair of consecutive kv-blocks of one (b, h); per kv-block the
+//    listed q-blocks i, ascending).  kThreads = 4 + kCmpWarps + 4 warps, registers
+//    redistributed with setmaxnreg (kRegsCtl / kRegsCmp / kRegsDq):
+//    warpgroup 0  warp 0 TMA K_j (+ LSE_i, D_i bulk copies), warp 2 TMA V_j, Q_i,
+//                 warp 3 TMA dO_i (Q / dO in a 2-stage ring, K / V 2 stages);
+//                 warp 1 TMEM allocator + single-thread tcgen05.mma issuer:
+//                   S^T  = K_j Q_i^T   (SS, M = kv 128, N = q 128, TMEM cols [0,128))
+//                   dP^T = V_j dO_i^T  (SS, N = 128, TMEM cols [128,256))
+//                   dV  += P^T dO_i    (TS: P^T bf16 written over S^T; acc [384,448))
+//                   dK  += dS^T Q_i    (SS: dS^T bf16 in smem, K-major view; acc [448,512))
+//                   dQ_i (+)= dS K_j   (SS: same dS^T smem tile, MN-major view; two
+//                                       accumulators [256,320) / [320,384) chained by
+//                                       the mask's dQ plan)
+//                 order per tile: dP^T(g+1) as soon as the compute warps hold S^T / dP^T(g)
+//                 in registers | dV(g) S^T(g+1) | dK(g) dQ(g); dQ(g) overlaps the compute
+//                 warps' start on tile g+1.
+//    compute warps  thread = key row, kCmpWarps / 4 warps per TMEM lane quarter:
+//                 P^T, dS^T from S^T, dP^T (element mask only on partial tiles: the
+//                 full-tile code has none); P^T packed back into TMEM, dS^T to smem.
+//    last warpgroup thread = query row: dQ_i drain at the end of a dQ
+//                 chain (complete chains -> bf16 dq rows; others -> smem -> TMA
+//                 reduce-add into the fp32 accumulator) and the dK / dV rows of
+//                 each unit.
 // K9 dq_finalize    : fp32 accumulator -> bf16 dQ.
-#include "predicates.cuh"
-#include "sm100.cuh"
-#include "tensor_map.cuh"
+#include <type_traits>
+
+#include "attn_bwd_common.cuh"
 
 namespace hla {
+#ifdef HLA_BWD_PROF
+__device__ unsigned long long g_bwd_prof[1024][24];
+#endif
+namespace bwd {
 namespace {
 
-constexpr int kBlock = 128;
-constexpr int kThreads = 512;   // 16 warps: TMA, MMA, 8 x P/dS, 4 x dQ, 2 x TMA
-constexpr uint32_t kTmemCols = 512;
+// Warp roles: warpgroup 0 = TMA producers + MMA issuer, then kCmpWarps compute warps (P / dS;
+// kCmpWarps / 4 per TMEM lane quarter, each over 128 / (kCmpWarps / 4) query columns), then
+// one warpgroup for the dQ drains and the dK / dV epilogue.
+#ifndef HLA_BWD_CMP_WARPS
+#define HLA_BWD_CMP_WARPS 8
+#endif
+constexpr int kCmpWarps = HLA_BWD_CMP_WARPS;
+static_assert(kCmpWarps == 8 || kCmpWarps == 16, "compute warps: 2 or 4 per TMEM lane quarter");
+constexpr int kCmpThreads = kCmpWarps * 32;
+constexpr int kChunks = 16 / kCmpWarps;              // 32-column chunks of S^T / dP^T per compute thread
+constexpr int kDqWarp0 = 4 + kCmpWarps;              // first dQ / epilogue warp
+constexpr int kThreads = (kDqWarp0 + 4) * 32;
+// per-warpgroup register budgets (setmaxnreg; the launch allocates 65536 / kThreads, rounded to 8)
+constexpr int kRegsCtl = kCmpWarps == 16 ? 56 : 64, kRegsCmp = kCmpWarps == 16 ? 88 : 168,
+              kRegsDq = kCmpWarps == 16 ? 56 : 104;
+// columns per TMEM load batch of the dQ drain / dK dV epilogue (a full D = 64 row needs ~96 registers)
+template <int D>
+constexpr int ep_cols() { return kRegsDq >= 96 ? D : 32; }
+static_assert(128 * (kRegsCtl + kRegsDq) + kCmpThreads * kRegsCmp <= kThreads * ((65536 / kThreads) & ~7),
+              "register budget");
 constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256, kColDV = 384, kColDK = 448;   // dQ: 2 x 64 columns
-constexpr float kLog2e = 1.4426950408889634f;
-constexpr int kHalf = 64;   // q-columns per pipeline half
+// Q / dO / LSE / D stages: tile g uses stage g & 1 (a stage that already holds the tile's
+// q-block is re-published without a reload).  A third stage (reuse-aware ring, single dS^T
+// tile) was measured slower: DESIGN.md 6f.
+constexpr int kQStages = 2;
 
-struct BwdParams {
-  Pattern pat;
-  int32_t N, heads, batch;
-  float scale, scale_log2, inv_scale;
-  const int32_t* t_row_ptr;
-  const int32_t* t_col_idx;
-  const uint8_t* t_kind;
-  const uint8_t* t_dq;     // dQ chaining plan per transposed entry (HLA_DQ_*; null = one chain per tile)
-  const float* lse2;       // LSE * log2(e), [B, H, N] (workspace, from the preprocess)
-  const float* dsum;       // D * scale, [B, H, N] (workspace, from the preprocess)
-  float* dq_acc;           // [B, N, H, Dh] fp32 (grid order when s2c != null)
-  const int32_t* s2c;      // fused reorder: seq_to_cell table (tensors in grid order), else null
-  const float* rpb;        // global RPB table [heads][2H-1][2W-1] (kBias)
-  float* drpb;             // its gradient (accumulated)
-  const int32_t* cells;    // grid cell of each sequence position (null: identity)
-  int32_t grid_h, grid_w, rpb_w, rpb_hw;
-  __nv_bfloat16* dk;
-  __nv_bfloat16* dv;
-  __nv_bfloat16* dq;       // dQ rows of LOCAL chains (bf16, same layout as dk)
-  unsigned long long* visited;
-};
+// Dev-only decomposition switches (`make VARIANT=name DEFS=-DHLA_BWD_VAR=<mask>`; results
+// are garbage, the timing is the point -- DESIGN.md 6f): 1 no MMAs (commits still arrive),
+// 2 no P / dS compute (the compute warps only wait and arrive), 4 no TMA loads (barriers
+// still arrive), 8 no dQ drain / dK dV epilogue (waits and arrives only).
+#ifndef HLA_BWD_VAR
+#define HLA_BWD_VAR 0
+#endif
+constexpr int kVar = HLA_BWD_VAR;
+
+// Dev-only wait-time accounting (`make VARIANT=prof DEFS=-DHLA_BWD_PROF`): one thread per
+// role sums the cycles it spends in each wait / work phase; hla_debug_bwd_prof() reads the
+// per-CTA sums.
+#ifdef HLA_BWD_PROF
+#define HLA_PW(slot, ...)                          \
+  do {                                             \
+    const long long _t0 = clock64();               \
+    __VA_ARGS__;                                   \
+    prof[slot] += (unsigned long long)(clock64() - _t0); \
+  } while (0)
+#define HLA_PDECL unsigned long long prof[24] = {0}
+#define HLA_PMARK(v) const long long v = clock64()
+#define HLA_PADD(slot, since) prof[slot] += (unsigned long long)(clock64() - (since))
+#define HLA_PFLUSH(lo, hi, cond)                                                  \
+  do {                                                                           \
+    if (cond)                                                                    \
+      for (int _i = (lo); _i < (hi); ++_i) ::hla::g_bwd_prof[blockIdx.x][_i] = prof[_i]; \
+  } while (0)
+#else
+#define HLA_PW(slot, ...) __VA_ARGS__
+#define HLA_PDECL do {} while (0)
+#define HLA_PMARK(v) do {} while (0)
+#define HLA_PADD(slot, since) do {} while (0)
+#define HLA_PFLUSH(lo, hi, cond) do {} while (0)
+#endif
 
 // entries of the per-tile dRPB window (offset rows of the tile's box, full table row stride
 // 2W - 1) in shared memory; more at D = 32, where the smaller tiles leave room
 template <int D>
 constexpr int rpb_win_cap() { return D == 32 ? 4096 : 2048; }
-// The window accumulates in 32-bit fixed point: shared-memory fp32 atomics are
-// compare-and-swap loops on sm_100 (ATOMS.CAST.SPIN, measured in SASS) while
-// integer ATOMS.ADD is native.  Resolution 2^-16 (absolute; dS values are
-// O(1e-2..1)), each addend saturated at +-2^14 so a tile's sum per offset (at most
-// 128 pairs) cannot overflow; converted back to fp32 when the window is flushed.
-constexpr float kRpbFix = 65536.f;
+// The window accumulates in 32-bit fixed point (shared-memory fp32 / 64-bit atomics are
+// compare-and-swap loops on sm_100, ATOMS.CAST.SPIN in SASS; 32-bit integer ATOMS.ADD is
+// native) with a per-tile power-of-two scale chosen from the tile's largest |dL/dscore|:
+// every addend is at most 2^22 in magnitude and at most 128 pairs of a 128 x 128 tile share
+// an offset (one per key), so a window entry stays below 2^29; the resolution is 2^-22 of
+// the tile's largest addend, independent of the gradient's absolute magnitude.
+constexpr int kRpbFixBits = 22;
 
 template <int D, bool kBias = false>
-struct BwdSmem {
+struct FullSmem {
   static constexpr uint32_t kTileBytes = kBlock * D * 2;
   alignas(1024) uint8_t k[2][kTileBytes];
   alignas(1024) uint8_t v[2][kTileBytes];
-  alignas(1024) uint8_t q[2][kTileBytes];
-  alignas(1024) uint8_t dO[2][kTileBytes];
+  alignas(1024) uint8_t q[kQStages][kTileBytes];
+  alignas(1024) uint8_t dO[kQStages][kTileBytes];
   alignas(1024) uint8_t ds[2][2 * 128 * 128];   // dS^T bf16 x2 (tile parity): [q/64][kv 128][64 q], SWIZZLE_128B
   alignas(1024) float dq_stage[kBlock * 32];    // fp32 dQ half tile [128][32], SWIZZLE_128B
-  alignas(16) float lse[2][kBlock];
-  alignas(16) float dd[2][kBlock];
-  alignas(16) int32_t qa[2][kBias ? kBlock : 4];   // kBias: A_q of the stage's query columns (RPB table index = A_q - B_k)
-  uint64_t kv_full[2], kv_empty[2], q_full[2], q_empty[2], s_full[2], ds_ready[2], dq_full[2], dq_free[2], dkv_full,
-      epi_done;
+  alignas(16) float lse[kQStages][kBlock];
+  alignas(16) float dd[kQStages][kBlock];
+  alignas(16) int32_t qa[kQStages][kBias ? kBlock : 4];   // kBias: A_q of the stage's query columns (RPB table index = A_q - B_k)
+  alignas(16) float rpb_wmax[kCmpWarps];            // kBias: per compute warp max |dL/dscore| of the tile
+  uint64_t kv_full[2], kv_empty[2], q_full[kQStages], q_empty[kQStages], s_full, s_read, p_ready, ds_ready,
+      dq_full[2], dq_free[2], dkv_full, epi_done;
   uint64_t dbg_bar;
   uint32_t tmem_base;
   int32_t rpb_win[kBias ? rpb_win_cap<D>() : 1];   // dRPB of the current tile's offset box, fixed point (compute warps)
 };
 
-template <int D>
-__device__ __forceinline__ uint64_t kmajor_desc(const uint8_t* tile, int kstep) {
-  constexpr uint32_t layout = D == 64 ? sm100::kSwizzle128B : sm100::kSwizzle64B;
-  return sm100::make_smem_desc(sm100::smem_u32(tile) + kstep * 32, 16, 8 * D * 2, layout);
-}
-template <int D>
-__device__ __forceinline__ uint64_t mnmajor_desc(const uint8_t* tile, int kstep) {
-  constexpr uint32_t layout = D == 64 ? sm100::kSwizzle128B : sm100::kSwizzle64B;
-  return sm100::make_smem_desc(sm100::smem_u32(tile) + kstep * 16 * D * 2, kBlock * D * 2, 8 * D * 2, layout);
-}
-// dS^T smem tile viewed as K-major A (M = kv, K = q): K step = 16 q
-__device__ __forceinline__ uint64_t ds_kmajor_desc(const uint8_t* ds, int kstep) {
-  return sm100::make_smem_desc(sm100::smem_u32(ds) + (kstep >> 2) * 16384 + (kstep & 3) * 32, 16, 1024,
-                               sm100::kSwizzle128B);
-}
-// dS^T smem tile viewed as MN-major A of dQ = dS K (M = q, K = kv): K step = 16 kv rows
-__device__ __forceinline__ uint64_t ds_mnmajor_desc(const uint8_t* ds, int kstep) {
-  return sm100::make_smem_desc(sm100::smem_u32(ds) + kstep * 2048, 16384, 1024, sm100::kSwizzle128B);
-}
-
-// Work units are pairs (2p, 2p+1) of kv-blocks of one (b, h) -- the unit of the dQ
-// plan (hla_build_bwd_plan) -- strided over the grid.  Consecutive kv-blocks share
-// q-blocks (the producer then skips reloading a Q/dO stage, and dQ partials chain in
-// TMEM), while all CTAs stay on nearby units (L2 reuse).
-constexpr int32_t kUnitEnd = 0x7fffffff, kUnitSkip = -1;
-struct UnitGeom {
-  int32_t mk, ppb, pairs;   // kv-blocks per (b, h), pairs per (b, h), pairs in total
-};
-// k-th kv-block of this CTA: flattened u = (b * heads + h) * mk + kb, kUnitSkip for
-// the missing second block of a ragged last pair, kUnitEnd past the last pair
-__device__ __forceinline__ int32_t unit_at(int32_t k, const UnitGeom& ug) {
-  const int32_t P = (int32_t)blockIdx.x + (k >> 1) * (int32_t)gridDim.x;
-  if (P >= ug.pairs) return kUnitEnd;
-  const int32_t bh = P / ug.ppb;
-  const int32_t kb = 2 * (P - bh * ug.ppb) + (k & 1);
-  return kb < ug.mk ? bh * ug.mk + kb : kUnitSkip;
-}
-
-// Iterator over the flattened (work unit, q-block tile) sequence of this CTA,
-// skipping units without tiles.  n = ordinal of the current non-empty unit.
-struct TileIter {
-  int32_t k, u, t, nt, rs;
-  uint32_t n;
-  bool valid;
-  __device__ void seek(const int32_t* t_row_ptr, const UnitGeom& ug) {
-    for (;; ++k) {
-      u = unit_at(k, ug);
-      if (u == kUnitEnd) break;
-      if (u < 0) continue;
-      const int32_t kb = u % ug.mk;
-      rs = __ldg(t_row_ptr + kb);
-      nt = __ldg(t_row_ptr + kb + 1) - rs;
-      if (nt > 0) { valid = true; return; }
-    }
-    valid = false;
-  }
-  __device__ void init(const int32_t* t_row_ptr, const UnitGeom& ug) {
-    k = 0; t = 0; n = 0;
-    seek(t_row_ptr, ug);
-  }
-  __device__ void advance(const int32_t* t_row_ptr, const UnitGeom& ug) {
-    if (++t < nt) return;
-    t = 0; ++n; ++k;
-    seek(t_row_ptr, ug);
-  }
-};
-
-// dQ plan bits of the g-th tile (transposed entry e); without a plan every tile is
-// its own chain, alternating between the two accumulators
-__device__ __forceinline__ uint32_t dq_plan(const uint8_t* t_dq, int32_t e, uint32_t g) {
-  return t_dq ? (uint32_t)__ldg(t_dq + e) : ((g & 1u) | HLA_DQ_NEW | HLA_DQ_DRAIN);
-}
-
-// Load the 128 token rows [seq0, seq0 + 128) (sequence order) of head h, batch b;
-// see attn_fwd.cu load_rows (kGather = fused reorder through s2c with .tile::gather4).
-template <int D, bool kGather>
-__device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int32_t h,
-                                          int32_t b, int32_t N, int32_t seq0, const int32_t* s2c, uint64_t pol,
-                                          int lane) {
-  if (kGather) {
-    // rows past N (ragged last tile) gather cell 0: their values are masked / discarded
-    const int4 c = seq0 + 4 * lane < N ? __ldg(reinterpret_cast<const int4*>(s2c + seq0) + lane) : make_int4(0, 0, 0, 0);
-    const int32_t base = b * N;
-    sm100::tma_gather4(dst + lane * 4 * D * 2, map, bar, h * D, base + c.x, base + c.y, base + c.z, base + c.w, pol);
-  } else if (lane == 0) {
-    sm100::tma_load_3d(dst, map, bar, 0, h, b * N + seq0, pol);
-  }
-}
-
-__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
-               : "memory");
-}
-
-// Persistent: CTA c processes kv-block work units c, c + G, ... (unit = kv-block,
-// head, batch; kv-block fastest).  K/V are double-buffered across units, so the
-// next unit's K/V (and first Q/dO) stream in while the current unit computes;
-// the dK/dV epilogue of a unit overlaps the first S/dP MMAs of the next one.
-// Phase counters: n = units with nt > 0 so far, g = (q-block) tiles so far.
-// cell -> (row << 16) | col (RPB offsets; grid sides < 2^15)
-__device__ __forceinline__ int32_t rpb_cell_rc(const int32_t* cells, int32_t seq, int32_t N, int32_t W) {
-  const int32_t cell = seq < N ? (cells ? __ldg(cells + seq) : seq) : 0;
-  const int32_t r = cell / W;
-  return (r << 16) | (cell - r * W);
-}
-// min / max of the rows and columns of the cells of sequence block [s0, s0 + 128)
-// (phantom positions >= N ignored); identical in every lane.
-struct CellBox { int32_t r0, r1, c0, c1; };
-__device__ __forceinline__ CellBox rpb_block_box(const int32_t* cells, int32_t s0, int32_t N, int32_t W, int lane) {
-  CellBox bx{1 << 30, -(1 << 30), 1 << 30, -(1 << 30)};
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int32_t sq = s0 + 32 * j + lane;
-    if (sq < N) {
-      const int32_t rc = rpb_cell_rc(cells, sq, N, W);
-      const int32_t r = rc >> 16, c = rc & 0xffff;
-      bx.r0 = min(bx.r0, r); bx.r1 = max(bx.r1, r); bx.c0 = min(bx.c0, c); bx.c1 = max(bx.c1, c);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    bx.r0 = min(bx.r0, __shfl_xor_sync(0xffffffffu, bx.r0, o));
-    bx.r1 = max(bx.r1, __shfl_xor_sync(0xffffffffu, bx.r1, o));
-    bx.c0 = min(bx.c0, __shfl_xor_sync(0xffffffffu, bx.c0, o));
-    bx.c1 = max(bx.c1, __shfl_xor_sync(0xffffffffu, bx.c1, o));
-  }
-  return bx;
-}
-
+// Persistent: CTA c processes kv-block work units c, c + G, ... (pairs of kv-blocks of
+// one (b, h)).  K/V are double-buffered across units, so the next unit's K/V (and first
+// Q/dO) stream in while the current unit computes; the dK/dV epilogue of a unit
+// overlaps the first MMAs of the next one.  Phase counters: n = units with tiles so
+// far, g = (q-block) tiles so far.
 template <int D, bool kTwoD, bool kGather, bool kBias>
 __global__ void __launch_bounds__(kThreads, 1)
-    attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+    attn_bwd_full_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                     const __grid_constant__ CUtensorMap tmDQ, const BwdParams prm) {
   extern __shared__ uint8_t smem_raw[];
-  using Smem = BwdSmem<D, kBias>;
+  using Smem = FullSmem<D, kBias>;
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  UnitGeom ug;
-  ug.mk = (prm.N + kBlock - 1) / kBlock;   // last kv-block may be ragged
-  ug.ppb = (ug.mk + 1) / 2;
-  ug.pairs = ug.ppb * prm.heads * prm.batch;
-  const int32_t mk = ug.mk;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < 2; ++s) {
-      sm100::mbar_init(&sm.kv_full[s], 2);    // producer warps 0 (K), 14 (V)
+      sm100::mbar_init(&sm.kv_full[s], 2);    // producer warps 0 (K), 2 (V)
       sm100::mbar_init(&sm.kv_empty[s], 1);
-      sm100::mbar_init(&sm.q_full[s], 3);     // producer warps 0 (LSE, D), 14 (Q), 15 (dO)
+      sm100::mbar_init(&sm.dq_full[s], 1);
+      sm100::mbar_init(&sm.dq_free[s], 128);
+    }
+    for (int s = 0; s < kQStages; ++s) {
+      sm100::mbar_init(&sm.q_full[s], 3);     // producer warps 0 (LSE, D), 2 (Q), 3 (dO)
       sm100::mbar_init(&sm.q_empty[s], 1);
     }
-    for (int hh = 0; hh < 2; ++hh) {
-      sm100::mbar_init(&sm.s_full[hh], 1);
-      sm100::mbar_init(&sm.ds_ready[hh], 256);
-    }
-    for (int bb = 0; bb < 2; ++bb) {
-      sm100::mbar_init(&sm.dq_full[bb], 1);
-      sm100::mbar_init(&sm.dq_free[bb], 128);
-    }
+    sm100::mbar_init(&sm.s_full, 1);
+    sm100::mbar_init(&sm.s_read, kCmpThreads);
+    sm100::mbar_init(&sm.p_ready, kCmpThreads);
+    sm100::mbar_init(&sm.ds_ready, kCmpThreads);
     sm100::mbar_init(&sm.dkv_full, 1);
     sm100::mbar_init(&sm.epi_done, 128);
     sm100::mbar_init(&sm.dbg_bar, 1);
@@ -264,6 +179,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     sm100::tmem_alloc(&sm.tmem_base, kTmemCols);
     sm100::tmem_relinquish();
   }
+  // LSE / D stages start zeroed: the bulk copies fill only real rows, and masked
+  // (P = 0) phantom columns of a ragged tile must see finite values (0 * NaN = NaN)
+  for (int i = threadIdx.x; i < kQStages * kBlock; i += kThreads) {
+    (&sm.lse[0][0])[i] = 0.f;
+    (&sm.dd[0][0])[i] = 0.f;
+  }
+  sm100::fence_proxy_async_smem();
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
@@ -271,16 +193,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned long long tiles_done = 0;
   HLA_TR_DECL;
 
-  if (warp == 0 || warp >= 14) {
-    // ----------------------------------------------------------- TMA producers
-    // Three warps run the same schedule and split the loads (a CTA's TMA gather4
-    // throughput grows with the number of issuing warps): warp 0 K + LSE / D,
-    // warp 14 V + Q, warp 15 dO.  Every warp arrives (with its own byte count) on
-    // the barriers it feeds, so no expect_tx has to precede another warp's copy.
-    {
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl) : "memory");
+    HLA_PDECL;
+    UnitGeom ug;
+    ug.mk = (prm.N + kBlock - 1) / kBlock;   // last kv-block may be ragged
+    ug.ppb = (ug.mk + 1) / 2;
+    ug.pairs = ug.ppb * prm.heads * prm.batch;
+    const int32_t mk = ug.mk;
+    if (warp != 1) {
+      // ----------------------------------------------------------- TMA producers
+      // Three warps run the same schedule and split the loads (a CTA's TMA gather4
+      // throughput grows with the number of issuing warps): warp 0 K + LSE / D,
+      // warp 2 V + Q, warp 3 dO.  Every warp arrives (with its own byte count) on
+      // the barriers it feeds, so no expect_tx has to precede another warp's copy.
       const uint64_t pol_kv = sm100::policy_evict_first();
       const uint64_t pol_q = sm100::policy_evict_last();
-      const int role = warp == 0 ? 0 : warp - 13;   // 0, 1, 2
+      const int role = warp == 0 ? 0 : warp - 1;   // 0, 1, 2
       constexpr uint32_t kTile = Smem::kTileBytes;
       uint32_t n = 0, g = 0;
       int64_t stage_tag0 = -1, stage_tag1 = -1;   // (b, h, q-block) held by stage 0 / 1
@@ -294,17 +223,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t bh = (int64_t)b * prm.heads + h;
         const int kvs = n & 1;
         if (role < 2) {
-          if (n >= 2) sm100::mbar_wait(&sm.kv_empty[kvs], ((n >> 1) - 1) & 1);
-          if (lane == 0) HLA_TR((3 << 24) | ((1) << 16) | (n));
-          if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.kv_full[kvs], kTile);
-          __syncwarp();
-          load_rows<D, kGather>(role == 0 ? sm.k[kvs] : sm.v[kvs], role == 0 ? &tmK : &tmV, &sm.kv_full[kvs], h, b,
-                                prm.N, kb * kBlock, prm.s2c, pol_kv, lane);
+          if (n >= 2) HLA_PW(13, sm100::mbar_wait(&sm.kv_empty[kvs], ((n >> 1) - 1) & 1));
+          if (kVar & 4) {
+            if (lane == 0) sm100::mbar_arrive(&sm.kv_full[kvs]);
+          } else {
+            if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.kv_full[kvs], kTile);
+            __syncwarp();
+            load_rows<D, kGather>(role == 0 ? sm.k[kvs] : sm.v[kvs], role == 0 ? &tmK : &tmV, &sm.kv_full[kvs], h,
+                                  b, prm.N, kb * kBlock, prm.s2c, pol_kv, lane);
+          }
         }
         for (int t = 0; t < nt; ++t, ++g) {
           const int s = g & 1;
-          if (g >= 2) sm100::mbar_wait(&sm.q_empty[s], ((g >> 1) - 1) & 1);
-          if (lane == 0 && role == 1) HLA_TR((7 << 24) | ((2) << 16) | (g));
+          if (g >= 2) HLA_PW(14, sm100::mbar_wait(&sm.q_empty[s], ((g >> 1) - 1) & 1));
           const int32_t qblk = __ldg(prm.t_col_idx + rs + t);
           const int64_t tag = bh * prm.N + qblk;     // (b, h, q-block) held by the stage
           if (tag == (s ? stage_tag1 : stage_tag0)) {
@@ -327,13 +258,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               sm100::sts_u4(sm100::smem_u32(sm.qa[s]) + 16u * lane, a_of(rc.x), a_of(rc.y), a_of(rc.z), a_of(rc.w));
               __syncwarp();   // every lane's A_q is written before lane 0 arrives on q_full
             }
-            if (lane == 0) {
+            if (lane == 0 && (kVar & 4)) {
+              sm100::mbar_arrive(&sm.q_full[s]);
+            } else if (lane == 0) {
               // LSE / D of the real rows only (ragged last tile: N % 4 == 0, so 16-B multiples)
               const uint32_t vbytes = (uint32_t)min(kBlock, prm.N - qblk * kBlock) * 4u;
               sm100::mbar_arrive_expect_tx(&sm.q_full[s], 2 * vbytes);
               sm100::bulk_load(sm.lse[s], prm.lse2 + bh * prm.N + qblk * kBlock, vbytes, &sm.q_full[s]);
               sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * kBlock, vbytes, &sm.q_full[s]);
             }
+          } else if (kVar & 4) {
+            if (lane == 0) sm100::mbar_arrive(&sm.q_full[s]);
           } else {
             if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.q_full[s], kTile);
             __syncwarp();
@@ -343,103 +278,95 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ++n;
       }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------- MMA issuer
-    // Half-tile software pipeline over the flattened (unit, q-block) sequence:
-    //   S_A,dP_A(g) S_B,dP_B(g) | dV_A dK_A(g) S_A,dP_A(g+1) | dV_B dK_B dQ(g) S_B,dP_B(g+1) | ...
-    // so the tensor core works on one q-half while the compute warps process the other.
-    if (lane == 0) {
-      constexpr uint32_t idesc_h = sm100::make_idesc_bf16(kBlock, kHalf, false, false);  // S^T, dP^T halves
-      constexpr uint32_t idesc_kv = sm100::make_idesc_bf16(kBlock, D, false, true);      // dV, dK
-      constexpr uint32_t idesc_q = sm100::make_idesc_bf16(kBlock, D, true, true);        // dQ
+      HLA_PFLUSH(13, 15, warp == 0 && lane == 0);
+    } else if (lane == 0) {
+      // ------------------------------------------------------------- MMA issuer
+      // Per tile g of the flattened (unit, q-block) sequence, driven by the compute
+      // warps' hand-offs for tile g:
+      //   s_read(g)   S^T(g), dP^T(g) are in registers -> dP^T(g+1)         (SS, N = 128)
+      //   p_ready(g)  P^T(g) is in TMEM over S^T(g)    -> dV(g) (TS), then S^T(g+1)
+      //                                                   (SS, N = 128; after dV(g) in
+      //                                                   the in-order pipe)
+      //   ds_ready(g) dS^T(g) is in smem               -> dK(g), dQ(g)      (SS)
+      // dQ(g) runs on the tensor pipe while the compute warps start tile g+1.  When tile
+      // g+1's operands have not landed, its MMAs wait behind dK / dQ(g) instead of
+      // blocking them.
+      constexpr uint32_t idesc_s = sm100::make_idesc_bf16(kBlock, kBlock, false, false);   // S^T, dP^T
+      constexpr uint32_t idesc_kv = sm100::make_idesc_bf16(kBlock, D, false, true);        // dV, dK
+      constexpr uint32_t idesc_q = sm100::make_idesc_bf16(kBlock, D, true, true);          // dQ
       const uint32_t tDQ = tmem + kColDQ, tDV = tmem + kColDV, tDK = tmem + kColDK;
       TileIter cur;
       cur.init(prm.t_row_ptr, ug);
       uint32_t g = 0;
       uint32_t dq_started0 = 0, dq_started1 = 0;   // chains begun per dQ accumulator
-      auto issue_sdp = [&](const TileIter& it, uint32_t gg, int half) {
-        const int s = gg & 1;
-        const uint8_t* sk = sm.k[it.n & 1];
-        const uint8_t* sv = sm.v[it.n & 1];
-        const uint32_t qoff = half * kHalf * D * 2;   // first row of this q half
+      auto issue_dp = [&](const TileIter& it, uint32_t gg) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          sm100::mma_ss(tmem + kColS + half * kHalf, kmajor_desc<D>(sk, kk), kmajor_desc<D>(sm.q[s] + qoff, kk),
-                        idesc_h, kk > 0);
+        for (int kk = 0; kk < D / 16 && !(kVar & 1); ++kk)
+          sm100::mma_ss(tmem + kColDP, kmajor_desc<D>(sm.v[it.n & 1], kk), kmajor_desc<D>(sm.dO[gg & 1], kk),
+                        idesc_s, kk > 0);
+      };
+      auto issue_s = [&](const TileIter& it, uint32_t gg) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          sm100::mma_ss(tmem + kColDP + half * kHalf, kmajor_desc<D>(sv, kk), kmajor_desc<D>(sm.dO[s] + qoff, kk),
-                        idesc_h, kk > 0);
-        sm100::mma_commit(&sm.s_full[half]);
+        for (int kk = 0; kk < D / 16 && !(kVar & 1); ++kk)
+          sm100::mma_ss(tmem + kColS, kmajor_desc<D>(sm.k[it.n & 1], kk), kmajor_desc<D>(sm.q[gg & 1], kk), idesc_s,
+                        kk > 0);
+        sm100::mma_commit(&sm.s_full);   // also covers the earlier dP^T(gg)
       };
-      auto issue_dvdk = [&](uint32_t gg, int half, bool first_tile) {
-        const int s = gg & 1;
-        const uint8_t* ds = sm.ds[gg & 1];
-#pragma unroll
-        for (int kk = half * 4; kk < half * 4 + 4; ++kk) {
-          const uint32_t acc = (!first_tile || kk > 0) ? 1u : 0u;
-          // P^T of q-columns [16kk, 16kk + 16): 8 packed columns at the start of S^T chunk kk/2
-          sm100::mma_ts(tDV, tmem + kColS + (kk >> 1) * 32 + (kk & 1) * 8, mnmajor_desc<D>(sm.dO[s], kk), idesc_kv,
-                        acc);
-          sm100::mma_ss(tDK, ds_kmajor_desc(ds, kk), mnmajor_desc<D>(sm.q[s], kk), idesc_kv, acc);
-        }
+      auto next_ready = [&](const TileIter& it, uint32_t gg) {
+        return (it.t != 0 || sm100::mbar_test_wait(&sm.kv_full[it.n & 1], (it.n >> 1) & 1)) &&
+               sm100::mbar_test_wait(&sm.q_full[gg & 1], (gg >> 1) & 1);
       };
-#if defined(HLA_TRACE) && defined(HLA_TRACE_MMA)
-      uint32_t dbg_phase = 0;
-      // trace builds: serialise after each MMA group and record its tensor-core time
-      auto mma_probe = [&](int ev, uint32_t gg) {
-        sm100::mma_commit(&sm.dbg_bar);
-        sm100::mbar_wait(&sm.dbg_bar, dbg_phase);
-        dbg_phase ^= 1;
-        HLA_TR((5 << 24) | (ev << 16) | gg);
-      };
-#else
-      auto mma_probe = [](int, uint32_t) {};
-#endif
-      if (cur.valid) {
-        sm100::mbar_wait(&sm.kv_full[cur.n & 1], (cur.n >> 1) & 1);
-        sm100::mbar_wait(&sm.q_full[0], 0);
+      auto wait_next = [&](const TileIter& it, uint32_t gg) {
+        HLA_PMARK(t0);
+        if (it.t == 0) sm100::mbar_wait(&sm.kv_full[it.n & 1], (it.n >> 1) & 1);
+        sm100::mbar_wait(&sm.q_full[gg & 1], (gg >> 1) & 1);
+        HLA_PADD(2, t0);
         sm100::tc_fence_after();
-        issue_sdp(cur, 0, 0);
-        issue_sdp(cur, 0, 1);
+      };
+      if (cur.valid) {
+        wait_next(cur, 0);
+        issue_dp(cur, 0);
+        issue_s(cur, 0);
       }
+      HLA_PMARK(tl0);
       while (cur.valid) {
         TileIter nxt = cur;
         nxt.advance(prm.t_row_ptr, ug);
         const uint32_t fdq = dq_plan(prm.t_dq, cur.rs + cur.t, g);
         const int kvs = cur.n & 1;
+        const int s = g & 1;
         const bool last_of_unit = cur.t == cur.nt - 1;
-        // half A of tile g
-        sm100::mbar_wait(&sm.ds_ready[0], g & 1);
-        HLA_TR((1 << 24) | ((1) << 16) | (g));
+        bool dp_next = false, s_next = false;
+        HLA_PW(0, sm100::mbar_wait(&sm.s_read, g & 1));
+        if (nxt.valid && next_ready(nxt, g + 1)) {
+          sm100::tc_fence_after();
+          issue_dp(nxt, g + 1);
+          dp_next = true;
+        }
+        HLA_PW(0, sm100::mbar_wait(&sm.p_ready, g & 1));
         sm100::tc_fence_after();
-        HLA_TR((5 << 24) | (0 << 16) | g);
         if (cur.t == 0 && cur.n > 0) {
           // the previous unit's dV / dK must have been drained from TMEM
-          sm100::mbar_wait(&sm.epi_done, (cur.n - 1) & 1);
+          HLA_PW(1, sm100::mbar_wait(&sm.epi_done, (cur.n - 1) & 1));
           sm100::tc_fence_after();
         }
-        issue_dvdk(g, 0, cur.t == 0);
-        mma_probe(1, g);
-        // S_A / dP_A of the next tile now if its operands already landed (never block
-        // here: the B half of this tile must not wait behind the next tile's loads)
-        bool next_a_issued = false;
-        if (nxt.valid && (nxt.t != 0 || sm100::mbar_test_wait(&sm.kv_full[nxt.n & 1], (nxt.n >> 1) & 1)) &&
-            sm100::mbar_test_wait(&sm.q_full[(g + 1) & 1], ((g + 1) >> 1) & 1)) {
-          HLA_TR((1 << 24) | ((4) << 16) | (g));
+#pragma unroll
+        for (int kk = 0; kk < kBlock / 16 && !(kVar & 1); ++kk)
+          sm100::mma_ts(tDV, tmem + kColS + packed_col(kk), mnmajor_desc<D>(sm.dO[s], kk), idesc_kv,
+                        (cur.t > 0 || kk > 0) ? 1u : 0u);
+        if (nxt.valid && (dp_next || next_ready(nxt, g + 1))) {
           sm100::tc_fence_after();
-          issue_sdp(nxt, g + 1, 0);
-          next_a_issued = true;
+          if (!dp_next) issue_dp(nxt, g + 1);
+          issue_s(nxt, g + 1);
+          s_next = true;
         }
-        // half B of tile g, then dQ (needs both halves of dS)
-        sm100::mbar_wait(&sm.ds_ready[1], g & 1);
-        HLA_TR((1 << 24) | ((2) << 16) | (g));
+        HLA_PW(0, sm100::mbar_wait(&sm.ds_ready, g & 1));
         sm100::tc_fence_after();
-        HLA_TR((5 << 24) | (0 << 16) | g);
-        issue_dvdk(g, 1, false);
-        mma_probe(3, g);
-        sm100::mma_commit(&sm.q_empty[g & 1]);   // Q_g / dO_g no longer read (dQ needs only dS and K)
+#pragma unroll
+        for (int kk = 0; kk < kBlock / 16 && !(kVar & 1); ++kk)
+          sm100::mma_ss(tDK, ds_kmajor_desc(sm.ds[g & 1], kk), mnmajor_desc<D>(sm.q[s], kk), idesc_kv,
+                        (cur.t > 0 || kk > 0) ? 1u : 0u);
+        sm100::mma_commit(&sm.q_empty[s]);   // Q_g / dO_g no longer read (dQ needs only dS and K)
         if (last_of_unit) sm100::mma_commit(&sm.dkv_full);
         const int dqb = (int)(fdq & HLA_DQ_BUF);
         const bool dq_new = (fdq & HLA_DQ_NEW) != 0;
@@ -447,48 +374,52 @@ __global__ void __launch_bounds__(kThreads, 1)
           // a new chain: the accumulator's previous chain must have been drained
           const uint32_t c = dqb ? dq_started1++ : dq_started0++;
           if (c > 0) {
-            sm100::mbar_wait(&sm.dq_free[dqb], (c - 1) & 1);
-            HLA_TR((1 << 24) | ((3) << 16) | (g));
+            HLA_PW(3, sm100::mbar_wait(&sm.dq_free[dqb], (c - 1) & 1));
             sm100::tc_fence_after();
           }
         }
 #pragma unroll
-        for (int kk = 0; kk < kBlock / 16; ++kk)
-          sm100::mma_ss(tDQ + dqb * 64, ds_mnmajor_desc(sm.ds[g & 1], kk), mnmajor_desc<D>(sm.k[kvs], kk), idesc_q,
-                        (kk > 0 || !dq_new) ? 1u : 0u);
-        mma_probe(4, g);
+        for (int kk = 0; kk < kBlock / 16 && !(kVar & 1); ++kk)
+          sm100::mma_ss(tDQ + dqb * 64, ds_mnmajor_desc(sm.ds[g & 1], kk), mnmajor_desc<D>(sm.k[kvs], kk),
+                        idesc_q, (kk > 0 || !dq_new) ? 1u : 0u);
         if (fdq & HLA_DQ_DRAIN) sm100::mma_commit(&sm.dq_full[dqb]);
         if (last_of_unit) sm100::mma_commit(&sm.kv_empty[kvs]);
-        if (nxt.valid) {
-          if (!next_a_issued) {
-            if (nxt.t == 0) sm100::mbar_wait(&sm.kv_full[nxt.n & 1], (nxt.n >> 1) & 1);
-            sm100::mbar_wait(&sm.q_full[(g + 1) & 1], ((g + 1) >> 1) & 1);
-            HLA_TR((1 << 24) | ((4) << 16) | (g));
-            sm100::tc_fence_after();
-            issue_sdp(nxt, g + 1, 0);
-          }
-          HLA_TR((5 << 24) | (0 << 16) | g);
-          issue_sdp(nxt, g + 1, 1);
-          mma_probe(5, g);
+        if (nxt.valid && !s_next) {
+          wait_next(nxt, g + 1);
+          if (!dp_next) issue_dp(nxt, g + 1);
+          issue_s(nxt, g + 1);
         }
         cur = nxt;
         ++g;
       }
+      HLA_PADD(4, tl0);
+#ifdef HLA_BWD_PROF
+      prof[15] = g;
+#endif
+      HLA_PFLUSH(0, 5, true);
+      HLA_PFLUSH(15, 16, true);
     }
-  } else if (warp < 10) {
+  } else if (warp < kDqWarp0) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsCmp) : "memory");
+    HLA_PDECL;
     // --------------------------------------------- P^T / dS^T (thread = key row)
-    // two warp sets (cset 0: warps 2-5, cset 1: warps 6-9) share every TMEM lane
-    // quarter; within each q-half, cset c processes the 32-column chunk 2*half + c.
+    // warp sets cset = 0 .. kCmpWarps / 4 - 1 (4 consecutive warps each) share every TMEM lane
+    // quarter; cset c processes the kChunks 32-column chunks [c * kChunks, (c + 1) * kChunks).
     const int quarter = warp & 3;
-    const int cset = (warp - 2) >> 2;
+    const int cset = (warp - 4) >> 2;
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = prm.scale_log2, scale = prm.scale;
+    UnitGeom ug;
+    ug.mk = (prm.N + kBlock - 1) / kBlock;
+    ug.ppb = (ug.mk + 1) / 2;
+    ug.pairs = ug.ppb * prm.heads * prm.batch;
+    const int32_t mk = ug.mk;
     if (kBias) {   // the dRPB window starts (and is left after every flush) zeroed
-      for (int i = (warp - 2) * 32 + lane; i < rpb_win_cap<D>(); i += 256) sm.rpb_win[i] = 0;
-      sm100::named_bar_sync(3, 256);
+      for (int i = (warp - 4) * 32 + lane; i < rpb_win_cap<D>(); i += kCmpThreads) sm.rpb_win[i] = 0;
+      sm100::named_bar_sync(3, kCmpThreads);
     }
-    uint32_t n = 0, g = 0;
+    uint32_t g = 0;
     for (int32_t kq = 0;; ++kq) {
       const int32_t u = unit_at(kq, ug);
       if (u == kUnitEnd) break;
@@ -499,23 +430,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       RowBox box = clip_box<kTwoD>(prm.pat, col_box(prm.pat, kidx));
       if (kidx >= prm.N) box.len = 0;   // phantom key row of a ragged tile: nothing allowed
       // RPB: this key row's cell, the key block's cell box, the head's table / gradient
-      int32_t k_r = 0, k_c = 0, k_b = 0;
+      int32_t k_b = 0;
       CellBox kbox{0, 0, 0, 0};
       const float* rpbh = nullptr;
       float* drpbh = nullptr;
       if (kBias) {
         const int32_t rc = rpb_cell_rc(prm.cells, kidx, prm.N, prm.grid_w);
-        k_r = rc >> 16;
-        k_c = rc & 0xffff;
-        k_b = k_r * prm.rpb_w + k_c;
+        k_b = (rc >> 16) * prm.rpb_w + (rc & 0xffff);
         kbox = rpb_block_box(prm.cells, kb * kBlock, prm.N, prm.grid_w, lane);
         rpbh = prm.rpb + (int64_t)h * prm.rpb_hw;
         drpbh = prm.drpb + (int64_t)h * prm.rpb_hw;
       }
       for (int t = 0; t < nt; ++t, ++g) {
-        const int s = g & 1;
         const uint8_t kd = __ldg(prm.t_kind + rs + t);
         const int32_t q0 = __ldg(prm.t_col_idx + rs + t) * kBlock;
+        const int s = g & 1;
         // RPB: the tile's offset box (dr, dc) = q box - key box and whether its rows fit
         // the shared-memory dRPB window (query offsets A_q come staged with LSE / D)
         int32_t dr0 = 0, dc0 = 0, wc = 0, wrows = 0, wcols = 0, kwb = 0;
@@ -532,40 +461,54 @@ __global__ void __launch_bounds__(kThreads, 1)
           win = wrows * wc <= rpb_win_cap<D>();
           kwb = (prm.grid_h - 1) * prm.rpb_w + prm.grid_w - 1 + k_b + dr0 * wc + dc0;
         }
-        sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1);
-        if (row == 0 && cset == 0) HLA_TR((2 << 24) | ((1) << 16) | (g));
+        HLA_PW(5, sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1));
         const uint32_t lse2 = sm100::smem_u32(sm.lse[s]);
         const uint32_t dd = sm100::smem_u32(sm.dd[s]);
         const uint32_t qa = sm100::smem_u32(sm.qa[s]);
         const uint32_t dsbuf = sm100::smem_u32(sm.ds[g & 1]);
-#pragma unroll 1
-        for (int half = 0; half < 2; ++half) {
-          sm100::mbar_wait(&sm.s_full[half], g & 1);
-          if (row == 0 && cset == 0) HLA_TR((2 << 24) | ((2 + 2 * half) << 16) | (g));
-          sm100::tc_fence_after();
-          {
-            const int c = 2 * half + cset;
-            uint32_t sr[32], dpr[32];
-            sm100::tmem_ld32(tmem + lane_off + kColS + c * 32, sr);
-            sm100::tmem_ld32(tmem + lane_off + kColDP + c * 32, dpr);
-            sm100::tmem_wait_ld();
+        HLA_PW(6, sm100::mbar_wait(&sm.s_full, g & 1));
+        HLA_PMARK(tc0);
+        sm100::tc_fence_after();
+        uint32_t sr[kChunks][32], dpr[kChunks][32];
+        if (!(kVar & 2)) {
+#pragma unroll
+          for (int j = 0; j < kChunks; ++j) {
+            sm100::tmem_ld32(tmem + lane_off + kColS + (cset * kChunks + j) * 32, sr[j]);
+            sm100::tmem_ld32(tmem + lane_off + kColDP + (cset * kChunks + j) * 32, dpr[j]);
+          }
+          sm100::tmem_wait_ld();
+        }
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&sm.s_read);      // dP^T(g+1) may overwrite the dP^T columns
+        HLA_PADD(16, tc0);
+        // P^T = exp2(S^T scale log2e - LSE log2e) (+ bias).  Partial tiles only: masked
+        // elements get an exponent of -inf (P = 0, hence dS = 0: D and dP^T are finite --
+        // the LSE / D stages start zeroed, phantom rows load finite data).
+        auto p_math = [&](auto partial_tag) {
+          constexpr bool kPart = decltype(partial_tag)::value;
+#pragma unroll
+          for (int j = 0; j < kChunks; ++j) {
+            const int c = cset * kChunks + j;
+            const int32_t base = q0 + c * 32;
             // [ulo, uhi): 8-column groups of this chunk that hold an allowed query of some
             // key row of this warp (partial tiles of 1D patterns: each key row's queries are
             // one interval); the other groups are all masked, their exponentials skipped
-            // (warp-uniform) and P = 0 there.  Full tiles / 2D patterns: all 4 groups.
+            // (warp-uniform) and P = 0 there.
             int ulo = 0, uhi = 4;
-            if (!kBias && kd == 2 && !kTwoD) {   // (with the RPB gather the branchy loop measured slower: cfg5 +6%)
-              const int32_t base = q0 + c * 32;
+            bool elem_mask = kPart;   // false: every element of this warp's chunk is allowed
+            if (kPart && !kTwoD) {
               const int32_t lo = min(max(box.lo - base, 0), 32), hi = min(max(box.lo + box.len - base, 0), 32);
-              const bool any = hi > lo;
-              ulo = __reduce_min_sync(0xffffffffu, any ? lo : 32) >> 3;
-              uhi = (__reduce_max_sync(0xffffffffu, any ? hi : 0) + 7) >> 3;
+              elem_mask = !__all_sync(0xffffffffu, lo == 0 && hi == 32);
+              if (!kBias) {   // (with the RPB gather the branchy loop measured slower: cfg5 +6%)
+                const bool any = hi > lo;
+                ulo = __reduce_min_sync(0xffffffffu, any ? lo : 32) >> 3;
+                uhi = (__reduce_max_sync(0xffffffffu, any ? hi : 0) + 7) >> 3;
+              }
             }
-            // P first (so its TMEM store is in flight while dS is formed)
-            float p[32];
+            float* p = reinterpret_cast<float*>(sr[j]);   // P overwrites S in place
 #pragma unroll
             for (int u4 = 0; u4 < 4; ++u4) {
-              if (u4 < ulo || u4 >= uhi) {
+              if (kPart && (u4 < ulo || u4 >= uhi)) {
 #pragma unroll
                 for (int e = 0; e < 8; ++e) p[u4 * 8 + e] = 0.f;
                 continue;
@@ -582,112 +525,168 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
-                float x = fmaf(__uint_as_float(sr[u4 * 8 + e]), sl2, -lv[e]);
+                float x = fmaf(__uint_as_float(sr[j][u4 * 8 + e]), sl2, -lv[e]);
                 if (kBias)   // + bias * log2(e), bias = table[h][dr + H - 1][dc + W - 1] = table[A_q - B_k]
-                  x = fmaf(__ldg(rpbh + (av[e] - k_b)), 1.4426950408889634f, x);
+                  x = fmaf(__ldg(rpbh + (av[e] - k_b)), kLog2e, x);
+                if (kPart && elem_mask) {
+                  const int32_t qq = base + u4 * 8 + e;
+                  bool ok;
+                  if (!kTwoD) {
+                    ok = (uint32_t)(qq - box.lo) < (uint32_t)box.len;
+                  } else {
+                    const int32_t rq = prm.pat.log2W >= 0 ? (qq >> prm.pat.log2W) : qq / prm.pat.W;
+                    const int32_t cq = qq - rq * prm.pat.W;
+                    ok = ((uint32_t)(rq - box.lo) < (uint32_t)box.len) && ((uint32_t)(cq - box.c0) < (uint32_t)box.cn);
+                  }
+                  x = ok ? x : -INFINITY;
+                }
                 p[u4 * 8 + e] = sm100::ex2(x);
               }
             }
-            uint32_t okbits = 0xffffffffu;   // element mask of this chunk (partial tiles only)
-            if (kd == 2) {
+          }
+        };
+        if (!(kVar & 2)) {
+          if (kd == 2) p_math(std::true_type{}); else p_math(std::false_type{});
+        }
+        if (!(kVar & 2)) {
+          // P^T packed to bf16 over the first 16 columns of each S^T chunk (in registers):
+          // the A operand of dV += P^T dO
 #pragma unroll
-              for (int e = 0; e < 32; ++e) {
-                const int32_t qq = q0 + c * 32 + e;
-                bool ok;
-                if (!kTwoD) {
-                  ok = (uint32_t)(qq - box.lo) < (uint32_t)box.len;
-                } else {
-                  const int32_t rq = prm.pat.log2W >= 0 ? (qq >> prm.pat.log2W) : qq / prm.pat.W;
-                  const int32_t cq = qq - rq * prm.pat.W;
-                  ok = ((uint32_t)(rq - box.lo) < (uint32_t)box.len) && ((uint32_t)(cq - box.c0) < (uint32_t)box.cn);
-                }
-                if (!ok) {
-                  p[e] = 0.f;
-                  okbits &= ~(1u << e);
-                }
-              }
-            }
-            {
-              uint32_t pk[16];
+          for (int j = 0; j < kChunks; ++j) {
+            const float* p = reinterpret_cast<const float*>(sr[j]);
+            uint32_t pk[16];
 #pragma unroll
-              for (int e = 0; e < 16; ++e) pk[e] = sm100::pack_bf16(p[2 * e], p[2 * e + 1]);
-              // over the first 16 columns of this thread's own S^T chunk (already in registers)
-              sm100::tmem_st16(tmem + lane_off + kColS + c * 32, pk);
-            }
+            for (int e = 0; e < 16; ++e) pk[e] = sm100::pack_bf16(p[2 * e], p[2 * e + 1]);
+            sm100::tmem_st16(tmem + lane_off + kColS + (cset * kChunks + j) * 32, pk);
+          }
+        }
+        sm100::tmem_wait_st();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&sm.p_ready);     // P^T(g) in TMEM: dV(g), then S^T(g+1) over it
+        // (dS^T buffer g & 1 was last read by dK / dQ(g - 2), issued before S^T(g): s_full(g)
+        // already certified their completion)
+        if (!(kVar & 2)) {
+          // dS^T = P^T o (dP^T scale - D scale) in place of dP^T, then bf16 smem tile [q/64][kv][64]
+          // with the 128B swizzle (A of dK += dS^T Q and, MN-major view, of dQ = dS K)
 #pragma unroll
-            for (int u4 = 0; u4 < 4; ++u4) {   // dS, 8 query columns (one 16B chunk) at a time
+          for (int j = 0; j < kChunks; ++j) {
+            const int c = cset * kChunks + j;
+            const float* p = reinterpret_cast<const float*>(sr[j]);
+            float* ds = reinterpret_cast<float*>(dpr[j]);
+#pragma unroll
+            for (int u4 = 0; u4 < 4; ++u4) {
               const int qc = c * 32 + u4 * 8;
               const float4 da = sm100::lds_f4(dd + qc * 4), db = sm100::lds_f4(dd + qc * 4 + 16);
               const float dv[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
-              float ds[8];
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
-                ds[e] = p[u4 * 8 + e] * fmaf(__uint_as_float(dpr[u4 * 8 + e]), scale, -dv[e]);
-                // masked: exactly 0 (the D / LSE of phantom query columns may be stale, 0 * NaN = NaN)
-                if (!((okbits >> (u4 * 8 + e)) & 1u)) ds[e] = 0.f;
+                const int i = u4 * 8 + e;
+                ds[i] = p[i] * fmaf(__uint_as_float(dpr[j][i]), scale, -dv[e]);
               }
-              if (kBias) {
-                // dRPB[offset] += dL/dscore = dS / scale: into the tile's shared-memory
-                // offset window (flushed once per tile), else straight to global
-                const float4 xa = sm100::lds_f4(qa + qc * 4), xb = sm100::lds_f4(qa + qc * 4 + 16);
-                const int32_t av[8] = {__float_as_int(xa.x), __float_as_int(xa.y), __float_as_int(xa.z),
-                                       __float_as_int(xa.w), __float_as_int(xb.x), __float_as_int(xb.y),
-                                       __float_as_int(xb.z), __float_as_int(xb.w)};
-                const uint32_t wbase = sm100::smem_u32(sm.rpb_win);
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                  if (!((okbits >> (u4 * 8 + e)) & 1u)) continue;
-                  const float gv = ds[e] * prm.inv_scale;
-                  if (win) {   // window index (dr - dr0) * (2W - 1) + (dc - dc0) = A_q - kwb
-                    const int32_t fx = __float2int_rn(fminf(fmaxf(gv, -16384.f), 16384.f) * kRpbFix);
-                    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(wbase + 4u * (uint32_t)(av[e] - kwb)), "r"(fx)
-                                 : "memory");
-                  } else {     // table index A_q - B_k
-                    atomicAdd(drpbh + (av[e] - k_b), gv);
-                  }
-                }
-              }
-              // dS^T row -> smem [q/64][kv][64] with the 128B swizzle (16B chunks)
               const uint32_t off =
                   (uint32_t)(qc >> 6) * 16384u + sm100::swz128((uint32_t)row * 128u + (uint32_t)(qc & 63) * 2u);
-              sm100::sts_u4(dsbuf + off, sm100::pack_bf16(ds[0], ds[1]), sm100::pack_bf16(ds[2], ds[3]),
-                            sm100::pack_bf16(ds[4], ds[5]), sm100::pack_bf16(ds[6], ds[7]));
+              sm100::sts_u4(dsbuf + off, sm100::pack_bf16(ds[u4 * 8 + 0], ds[u4 * 8 + 1]),
+                            sm100::pack_bf16(ds[u4 * 8 + 2], ds[u4 * 8 + 3]),
+                            sm100::pack_bf16(ds[u4 * 8 + 4], ds[u4 * 8 + 5]),
+                            sm100::pack_bf16(ds[u4 * 8 + 6], ds[u4 * 8 + 7]));
             }
           }
-          sm100::tmem_wait_st();
-          sm100::fence_proxy_async_smem();
-          sm100::tc_fence_before();
-          sm100::mbar_arrive(&sm.ds_ready[half]);
-          if (row == 0 && cset == 0) HLA_TR((2 << 24) | ((3 + 2 * half) << 16) | (g));
         }
-        if (kBias && win) {
-          // flush the tile's dRPB window to global (and re-zero it) -- all 256 compute threads
-          sm100::named_bar_sync(3, 256);
-          const int tid = (warp - 2) * 32 + lane;
-          for (int i = tid; i < wrows * wcols; i += 256) {   // only the box's used columns
-            const int32_t ir = i / wcols, ic = i - ir * wcols;
-            const int32_t v = sm.rpb_win[ir * wc + ic];
-            if (v != 0) {
-              atomicAdd(drpbh + (dr0 + ir + prm.grid_h - 1) * prm.rpb_w + (dc0 + ic + prm.grid_w - 1),
-                        (float)v * (1.f / kRpbFix));
-              sm.rpb_win[ir * wc + ic] = 0;
+        HLA_PADD(17, tc0);
+        if (kBias && !(kVar & 2)) {
+          // dRPB[offset] += dL/dscore = dS / scale (before ds_ready: the A_q staged with the
+          // tile's Q stage are reused once it is released): into the tile's shared-memory
+          // offset window at a per-tile power-of-two fixed-point scale (kRpbFixBits), flushed
+          // with fp32 global reductions; windows that do not fit go to global fp32 reductions
+          float fx = 0.f;
+          if (win) {
+            float mx = 0.f;
+#pragma unroll
+            for (int j = 0; j < kChunks; ++j)
+#pragma unroll
+              for (int i = 0; i < 32; ++i) mx = fmaxf(mx, fabsf(__uint_as_float(dpr[j][i])));
+            // non-negative floats order like their bit patterns
+            const uint32_t mb = __reduce_max_sync(0xffffffffu, __float_as_uint(mx * prm.inv_scale));
+            if (lane == 0) sm.rpb_wmax[warp - 4] = __uint_as_float(mb);
+            sm100::named_bar_sync(3, kCmpThreads);
+            float tmx = 0.f;
+#pragma unroll
+            for (int w4 = 0; w4 < kCmpWarps / 4; ++w4) {
+              const float4 m = sm100::lds_f4(sm100::smem_u32(sm.rpb_wmax) + 16 * w4);
+              tmx = fmaxf(tmx, fmaxf(fmaxf(m.x, m.y), fmaxf(m.z, m.w)));
+            }
+            // largest addend in [2^(kRpbFixBits-1), 2^kRpbFixBits)
+            fx = tmx > 0.f ? ldexpf(1.f, kRpbFixBits - 1 - ilogbf(tmx)) : 1.f;
+          }
+          const uint32_t wbase = sm100::smem_u32(sm.rpb_win);
+#pragma unroll
+          for (int j = 0; j < kChunks; ++j) {
+#pragma unroll
+            for (int u4 = 0; u4 < 4; ++u4) {
+              const int qc = (cset * kChunks + j) * 32 + u4 * 8;
+              const float4 xa = sm100::lds_f4(qa + qc * 4), xb = sm100::lds_f4(qa + qc * 4 + 16);
+              const int32_t av[8] = {__float_as_int(xa.x), __float_as_int(xa.y), __float_as_int(xa.z),
+                                     __float_as_int(xa.w), __float_as_int(xb.x), __float_as_int(xb.y),
+                                     __float_as_int(xb.z), __float_as_int(xb.w)};
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const int i = u4 * 8 + e;
+                const float gv = __uint_as_float(dpr[j][i]) * prm.inv_scale;
+                if (gv == 0.f) continue;   // masked pairs (P = 0) add nothing
+                if (win) {   // window index (dr - dr0) * (2W - 1) + (dc - dc0) = A_q - kwb
+                  const int32_t v = __float2int_rn(gv * fx);
+                  if (v != 0)   // (phantom positions: cell 0, possibly outside the box; their P is 0)
+                    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(wbase + 4u * (uint32_t)(av[e] - kwb)), "r"(v)
+                                 : "memory");
+                } else {     // table index A_q - B_k
+                  atomicAdd(drpbh + (av[e] - k_b), gv);
+                }
+              }
             }
           }
-          sm100::named_bar_sync(3, 256);
+          if (win) {
+            // flush the tile's dRPB window to global (and re-zero it) -- all compute threads
+            sm100::named_bar_sync(3, kCmpThreads);
+            const float inv_fx = 1.f / fx;
+            const int tid = (warp - 4) * 32 + lane;
+            for (int i = tid; i < wrows * wcols; i += kCmpThreads) {   // only the box's used columns
+              const int32_t ir = i / wcols, ic = i - ir * wcols;
+              const int32_t v = sm.rpb_win[ir * wc + ic];
+              if (v != 0) {
+                atomicAdd(drpbh + (dr0 + ir + prm.grid_h - 1) * prm.rpb_w + (dc0 + ic + prm.grid_w - 1),
+                          (float)v * inv_fx);
+                sm.rpb_win[ir * wc + ic] = 0;
+              }
+            }
+          }
         }
+        sm100::fence_proxy_async_smem();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&sm.ds_ready);
+        HLA_PADD(7, tc0);
       }
       tiles_done += nt;
     }
-  } else if (warp < 14) {
+    HLA_PFLUSH(5, 9, warp == 4 && lane == 0);
+    HLA_PFLUSH(16, 18, warp == 4 && lane == 0);
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsDq) : "memory");
+    HLA_PDECL;
     // ------------------------------------------ dQ partial -> fp32 accumulator
     // thread = query row: drain the dQ_i tile from TMEM (then release it), stage it
     // in shared memory (two 32-column halves, 128B swizzle) and let the TMA engine
     // add it into the fp32 accumulator (cp.reduce.async.bulk.tensor ... add) -- no
     // per-thread atomics, so the LSU stays free for the compute warps.
+    UnitGeom ug;
+    ug.mk = (prm.N + kBlock - 1) / kBlock;
+    ug.ppb = (ug.mk + 1) / 2;
+    ug.pairs = ug.ppb * prm.heads * prm.batch;
+    const int32_t mk = ug.mk;
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const bool leader = warp == 10 && lane == 0;
+    const bool leader = warp == kDqWarp0 && lane == 0;
+    constexpr int kEpCols = ep_cols<D>();
     uint32_t g = 0, n = 0;
     uint32_t dq_drained0 = 0, dq_drained1 = 0;   // chains drained per dQ accumulator
     for (int32_t kq = 0;; ++kq) {
@@ -700,51 +699,69 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t fdq = dq_plan(prm.t_dq, rs + t, g);
         if (!(fdq & HLA_DQ_DRAIN)) continue;   // the chain continues in TMEM
         const int dqb = (int)(fdq & HLA_DQ_BUF);
-        sm100::mbar_wait(&sm.dq_full[dqb], (dqb ? dq_drained1++ : dq_drained0++) & 1);
-        if (leader) HLA_TR((4 << 24) | ((1) << 16) | (g));
+        HLA_PW(9, sm100::mbar_wait(&sm.dq_full[dqb], (dqb ? dq_drained1++ : dq_drained0++) & 1));
+        HLA_PMARK(td0);
         sm100::tc_fence_after();
-        const int32_t qblk = __ldg(prm.t_col_idx + rs + t);
-        const int32_t qrow = b * prm.N + qblk * kBlock;   // sequence order
-        uint32_t r[D];
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c)
-          sm100::tmem_ld32(tmem + lane_off + kColDQ + dqb * 64 + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
-        sm100::tmem_wait_ld();
-        sm100::tc_fence_before();
-        sm100::mbar_arrive(&sm.dq_free[dqb]);     // the TMEM dQ accumulator may now be overwritten
-        if (fdq & HLA_DQ_LOCAL) {
-          // complete dQ_i (dS carries the softmax scale): bf16 rows straight to dq, to the
-          // grid cell under the fused reorder; phantom rows of a ragged tile write nothing
-          const int32_t qs = qblk * kBlock + row;
-          if (qs < prm.N) {
-            const int32_t qcell = kGather ? __ldg(prm.s2c + qs) : qs;
-            uint4* dqp = reinterpret_cast<uint4*>(prm.dq + (((int64_t)b * prm.N + qcell) * prm.heads + h) * D);
-#pragma unroll
-            for (int v4 = 0; v4 < D / 8; ++v4)
-              dqp[v4] = make_uint4(sm100::pack_bf16(__uint_as_float(r[8 * v4 + 0]), __uint_as_float(r[8 * v4 + 1])),
-                                   sm100::pack_bf16(__uint_as_float(r[8 * v4 + 2]), __uint_as_float(r[8 * v4 + 3])),
-                                   sm100::pack_bf16(__uint_as_float(r[8 * v4 + 4]), __uint_as_float(r[8 * v4 + 5])),
-                                   sm100::pack_bf16(__uint_as_float(r[8 * v4 + 6]), __uint_as_float(r[8 * v4 + 7])));
-          }
+        if (kVar & 8) {
+          sm100::mbar_arrive(&sm.dq_free[dqb]);
           continue;
         }
+        const int32_t qblk = __ldg(prm.t_col_idx + rs + t);
+        const int32_t qrow = b * prm.N + qblk * kBlock;   // sequence order
+        const bool local = (fdq & HLA_DQ_LOCAL) != 0;
+        // complete dQ_i (LOCAL; dS carries the softmax scale): bf16 rows straight to dq, to the
+        // grid cell under the fused reorder; phantom rows of a ragged tile write nothing
+        uint4* dqp = nullptr;
+        if (local && qblk * kBlock + row < prm.N) {
+          const int32_t qs = qblk * kBlock + row;
+          const int32_t qcell = kGather ? __ldg(prm.s2c + qs) : qs;
+          dqp = reinterpret_cast<uint4*>(prm.dq + (((int64_t)b * prm.N + qcell) * prm.heads + h) * D);
+        }
+        // the accumulator in kEpCols-column batches (all D columns when the register budget
+        // allows: the dq_free hand-off then follows a single TMEM round trip)
 #pragma unroll
-        for (int hh = 0; hh < D / 32; ++hh) {
-          if (leader) sm100::bulk_wait_group_read0();   // previous reduce finished reading the stage
-          sm100::named_bar_sync(2, 128);
+        for (int hb = 0; hb < D / kEpCols; ++hb) {
+          uint32_t r[kEpCols];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const uint32_t off = sm100::swz128((uint32_t)row * 128u + (uint32_t)j * 16u);
-            sm100::sts_u4(sm100::smem_u32(sm.dq_stage) + off, r[hh * 32 + 4 * j], r[hh * 32 + 4 * j + 1],
-                          r[hh * 32 + 4 * j + 2], r[hh * 32 + 4 * j + 3]);
+          for (int c = 0; c < kEpCols / 32; ++c)
+            sm100::tmem_ld32(tmem + lane_off + kColDQ + dqb * 64 + hb * kEpCols + c * 32,
+                             *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
+          sm100::tmem_wait_ld();
+          if (hb == D / kEpCols - 1) {
+            sm100::tc_fence_before();
+            sm100::mbar_arrive(&sm.dq_free[dqb]);     // the TMEM dQ accumulator may now be overwritten
           }
-          sm100::fence_proxy_async_smem();
-          sm100::named_bar_sync(2, 128);
-          if (leader) {
-            sm100::tma_reduce_add_3d(&tmDQ, sm.dq_stage, hh * 32, h, qrow);
-            sm100::bulk_commit_group();
+          if (local) {
+#pragma unroll
+            for (int v4 = 0; v4 < kEpCols / 8 && dqp; ++v4)
+              dqp[hb * (kEpCols / 8) + v4] =
+                  make_uint4(sm100::pack_bf16(__uint_as_float(r[8 * v4 + 0]), __uint_as_float(r[8 * v4 + 1])),
+                             sm100::pack_bf16(__uint_as_float(r[8 * v4 + 2]), __uint_as_float(r[8 * v4 + 3])),
+                             sm100::pack_bf16(__uint_as_float(r[8 * v4 + 4]), __uint_as_float(r[8 * v4 + 5])),
+                             sm100::pack_bf16(__uint_as_float(r[8 * v4 + 6]), __uint_as_float(r[8 * v4 + 7])));
+            continue;
+          }
+          // partial dQ_i -> smem stage (32 columns at a time, 128B swizzle) -> TMA reduce-add
+          // into the fp32 accumulator
+#pragma unroll
+          for (int hh = 0; hh < kEpCols / 32; ++hh) {
+            if (leader) sm100::bulk_wait_group_read0();   // previous reduce finished reading the stage
+            sm100::named_bar_sync(2, 128);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t off = sm100::swz128((uint32_t)row * 128u + (uint32_t)j * 16u);
+              sm100::sts_u4(sm100::smem_u32(sm.dq_stage) + off, r[hh * 32 + 4 * j], r[hh * 32 + 4 * j + 1],
+                            r[hh * 32 + 4 * j + 2], r[hh * 32 + 4 * j + 3]);
+            }
+            sm100::fence_proxy_async_smem();
+            sm100::named_bar_sync(2, 128);
+            if (leader) {
+              sm100::tma_reduce_add_3d(&tmDQ, sm.dq_stage, hb * kEpCols + hh * 32, h, qrow);
+              sm100::bulk_commit_group();
+            }
           }
         }
+        HLA_PADD(10, td0);
       }
       // final dK, dV rows of this unit -> bf16 (thread = key row; dS already carries
       // the softmax scale).  Done here, off the compute warps' critical path; the
@@ -756,33 +773,63 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint4* dkp = reinterpret_cast<uint4*>(prm.dk + grow * D);
       uint4* dvp = reinterpret_cast<uint4*>(prm.dv + grow * D);
       if (nt > 0) {
-        sm100::mbar_wait(&sm.dkv_full, n & 1);
-        if (leader) HLA_TR((4 << 24) | ((6) << 16) | (n));
+        HLA_PW(11, sm100::mbar_wait(&sm.dkv_full, n & 1));
+        HLA_PMARK(te0);
         sm100::tc_fence_after();
-        // dV then dK, each packed to bf16 right away (64 live registers, not 128)
-        uint32_t pv[D / 2], pk[D / 2];
-#pragma unroll
-        for (int which = 0; which < 2; ++which) {
-          uint32_t r[D];
+        if (kVar & 8) {
+          sm100::mbar_arrive(&sm.epi_done);
+          ++n;
+          continue;
+        }
+        if constexpr (kEpCols == D) {
+          // dV then dK: the dK load is in flight while the dV row is stored (<= 96 live registers)
+          uint32_t r[D], pv[D / 2];
 #pragma unroll
           for (int c = 0; c < D / 32; ++c)
-            sm100::tmem_ld32(tmem + lane_off + (which ? kColDK : kColDV) + c * 32,
-                             *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
+            sm100::tmem_ld32(tmem + lane_off + kColDV + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
           sm100::tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < D / 2; ++e) {
-            const uint32_t w = sm100::pack_bf16(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
-            if (which) pk[e] = w; else pv[e] = w;
+          for (int e = 0; e < D / 2; ++e)
+            pv[e] = sm100::pack_bf16(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c)
+            sm100::tmem_ld32(tmem + lane_off + kColDK + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
+#pragma unroll
+          for (int v4 = 0; v4 < D / 8 && real; ++v4)
+            dvp[v4] = make_uint4(pv[v4 * 4 + 0], pv[v4 * 4 + 1], pv[v4 * 4 + 2], pv[v4 * 4 + 3]);
+          sm100::tmem_wait_ld();
+          sm100::tc_fence_before();
+          sm100::mbar_arrive(&sm.epi_done);      // dV / dK accumulators may now be reset
+#pragma unroll
+          for (int v4 = 0; v4 < D / 8 && real; ++v4)
+            dkp[v4] = make_uint4(sm100::pack_bf16(__uint_as_float(r[8 * v4 + 0]), __uint_as_float(r[8 * v4 + 1])),
+                                 sm100::pack_bf16(__uint_as_float(r[8 * v4 + 2]), __uint_as_float(r[8 * v4 + 3])),
+                                 sm100::pack_bf16(__uint_as_float(r[8 * v4 + 4]), __uint_as_float(r[8 * v4 + 5])),
+                                 sm100::pack_bf16(__uint_as_float(r[8 * v4 + 6]), __uint_as_float(r[8 * v4 + 7])));
+        } else {
+          // dV then dK in 32-column batches (register budget kRegsDq); epi_done after the last load
+#pragma unroll
+          for (int which = 0; which < 2; ++which) {
+            uint4* dst = which ? dkp : dvp;
+#pragma unroll
+            for (int hh = 0; hh < D / 32; ++hh) {
+              uint32_t r[32];
+              sm100::tmem_ld32(tmem + lane_off + (which ? kColDK : kColDV) + hh * 32, r);
+              sm100::tmem_wait_ld();
+              if (which == 1 && hh == D / 32 - 1) {
+                sm100::tc_fence_before();
+                sm100::mbar_arrive(&sm.epi_done);      // dV / dK accumulators may now be reset
+              }
+#pragma unroll
+              for (int v4 = 0; v4 < 4 && real; ++v4)
+                dst[hh * 4 + v4] = make_uint4(sm100::pack_bf16(__uint_as_float(r[8 * v4 + 0]), __uint_as_float(r[8 * v4 + 1])),
+                                              sm100::pack_bf16(__uint_as_float(r[8 * v4 + 2]), __uint_as_float(r[8 * v4 + 3])),
+                                              sm100::pack_bf16(__uint_as_float(r[8 * v4 + 4]), __uint_as_float(r[8 * v4 + 5])),
+                                              sm100::pack_bf16(__uint_as_float(r[8 * v4 + 6]), __uint_as_float(r[8 * v4 + 7])));
+            }
           }
         }
-        sm100::tc_fence_before();
-        sm100::mbar_arrive(&sm.epi_done);      // dV / dK accumulators may now be reset
-#pragma unroll
-        for (int v4 = 0; v4 < D / 8 && real; ++v4) {
-          dvp[v4] = make_uint4(pv[v4 * 4 + 0], pv[v4 * 4 + 1], pv[v4 * 4 + 2], pv[v4 * 4 + 3]);
-          dkp[v4] = make_uint4(pk[v4 * 4 + 0], pk[v4 * 4 + 1], pk[v4 * 4 + 2], pk[v4 * 4 + 3]);
-        }
-        if (leader) HLA_TR((4 << 24) | ((7) << 16) | (n));
+        HLA_PADD(12, te0);
         ++n;
       } else {
 #pragma unroll
@@ -793,14 +840,60 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (leader) sm100::bulk_wait_group0();
+    HLA_PFLUSH(9, 13, leader);
   }
 
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
   if (warp == 1) sm100::tmem_dealloc(tmem, kTmemCols);
-  if (warp == 2 && lane == 0 && prm.visited != nullptr && tiles_done > 0) atomicAdd(prm.visited, tiles_done);
+  if (warp == 4 && lane == 0 && prm.visited != nullptr && tiles_done > 0) atomicAdd(prm.visited, tiles_done);
 }
+
+template <int D, bool kTwoD, bool kGather, bool kBias>
+hla_status launch_full_t(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mdo,
+                      const CUtensorMap& mdq, const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream) {
+  const size_t smem = sizeof(FullSmem<D, kBias>) + 1024;
+  auto* fn = attn_bwd_full_kernel<D, kTwoD, kGather, kBias>;
+  HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t pairs = (int64_t)((n_kblocks + 1) / 2) * prm.heads * prm.batch;   // work units (kv-block pairs)
+  const int grid = (int)std::min<int64_t>(pairs, (int64_t)num_sms());
+  fn<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mdo, mdq, prm);
+  HLA_CUDA_TRY(cudaGetLastError());
+  return HLA_OK;
+}
+
+static_assert(sizeof(FullSmem<64, true>) + 1024 <= 227 * 1024, "bwd shared memory (d = 64, RPB) exceeds 227 KB");
+
+template <bool kBias>
+hla_status dispatch_full(int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
+                         const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm,
+                         int32_t mkb, cudaStream_t stream) {
+  if (head_dim == 64) {
+    if (gather) return launch_full_t<64, false, true, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
+    return two_d ? launch_full_t<64, true, false, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream)
+                 : launch_full_t<64, false, false, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
+  }
+  if (gather) return launch_full_t<32, false, true, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
+  return two_d ? launch_full_t<32, true, false, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream)
+               : launch_full_t<32, false, false, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
+}
+
+}  // namespace
+
+hla_status launch_full(bool bias, int head_dim, bool gather, bool two_d, const CUtensorMap& mq,
+                       const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq,
+                       const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream) {
+  return bias ? dispatch_full<true>(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, n_kblocks, stream)
+              : dispatch_full<false>(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
+}
+
+}  // namespace bwd
+
+namespace {
+
+using bwd::kBlock;
+using bwd::kLog2e;
 
 // K7: D = rowsum(dO o O) per (b, s, h) row of head_dim bf16, fp32, in sequence order s
 // (rows read at grid cell s2c[s] under the fused reorder), stored pre-multiplied by
@@ -873,39 +966,20 @@ __global__ void __launch_bounds__(256) dq_finalize_kernel(const float4* __restri
                      sm100::pack_bf16(v1.z, v1.w));
 }
 
-template <int D, bool kTwoD, bool kGather, bool kBias>
-hla_status launch_bwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mdo,
-                      const CUtensorMap& mdq, const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream) {
-  const size_t smem = sizeof(BwdSmem<D, kBias>) + 1024;
-  auto* fn = attn_bwd_kernel<D, kTwoD, kGather, kBias>;
-  HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t pairs = (int64_t)((n_kblocks + 1) / 2) * prm.heads * prm.batch;   // work units (kv-block pairs)
-  const int grid = (int)std::min<int64_t>(pairs, (int64_t)num_sms());
-  fn<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mdo, mdq, prm);
-  HLA_CUDA_TRY(cudaGetLastError());
-  return HLA_OK;
-}
-
-static_assert(sizeof(BwdSmem<64, true>) + 1024 <= 227 * 1024, "bwd shared memory (d = 64, RPB) exceeds 227 KB");
-
-template <bool kBias>
-hla_status dispatch_bwd(int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
-                        const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm,
-                        int32_t mkb, cudaStream_t stream) {
-  if (head_dim == 64) {
-    if (gather) return launch_bwd<64, false, true, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
-    return two_d ? launch_bwd<64, true, false, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream)
-                 : launch_bwd<64, false, false, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
-  }
-  if (gather) return launch_bwd<32, false, true, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
-  return two_d ? launch_bwd<32, true, false, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream)
-               : launch_bwd<32, false, false, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
-}
-
 }  // namespace
 }  // namespace hla
 
 using namespace hla;
+
+#ifdef HLA_BWD_PROF
+// dev-only: per-CTA wait / work cycle sums of the last attn_bwd_kernel launch (HLA_BWD_PROF builds)
+extern "C" __attribute__((visibility("default"))) int hla_debug_bwd_prof(unsigned long long* host, int ctas) {
+  cudaDeviceSynchronize();
+  const int n = ctas < 1024 ? ctas : 1024;
+  cudaMemcpyFromSymbol(host, hla::g_bwd_prof, (size_t)n * 24 * sizeof(unsigned long long));
+  return n;
+}
+#endif
 
 extern "C" size_t hla_attn_bwd_workspace(int32_t batch, int32_t heads, int32_t n, int32_t head_dim) {
   const size_t acc = (size_t)batch * n * heads * head_dim * 4;
@@ -990,7 +1064,7 @@ extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_blo
   st = carve_workspace(batch, heads, pat.N, head_dim, workspace, workspace_bytes, &dq_acc, &dsum, &lse2);
   if (st != HLA_OK) return st;
   const float sc = scale > 0.f ? scale : 1.0f / sqrtf((float)head_dim);
-  BwdParams prm;
+  bwd::BwdParams prm;
   prm.pat = pat;
   prm.N = pat.N;
   prm.heads = heads;
@@ -1032,8 +1106,12 @@ extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_blo
   if ((st = make_f32_rows_map(&mdq, dq_acc, tok, heads, head_dim, 32, kBlock)) != HLA_OK) return st;
   const bool two_d = pat.kind == K_WSA || pat.kind == K_SA || pat.kind == K_NA2D;
   const int32_t mkb = (pat.N + kBlock - 1) / kBlock;
-  return prm.rpb ? dispatch_bwd<true>(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, mkb, stream)
-                 : dispatch_bwd<false>(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, mkb, stream);
+  // schedule: full-tile (attn_bwd_full_kernel) when full tiles are at least half of the
+  // mask's tiles or with the RPB score_mod; half-tile (attn_bwd_split_kernel) otherwise
+  // (the split schedule overlaps the partial tiles' masked compute better)
+  const bool full = prm.rpb != nullptr || m->host_counts[1] >= m->host_counts[2];
+  if (full) return bwd::launch_full(prm.rpb != nullptr, head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, mkb, stream);
+  return bwd::launch_split(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, mkb, stream);
 }
 
 extern "C" hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,

@@ -1,0 +1,170 @@
+// Shared pieces of the two backward schedules (attn_bwd.cu: full-tile schedule and the
+// host API; attn_bwd_split.cu: half-tile schedule).  Internal header of libhla.
+#pragma once
+
+#include "predicates.cuh"
+#include "sm100.cuh"
+#include "tensor_map.cuh"
+
+namespace hla {
+namespace bwd {
+
+constexpr int kBlock = 128;
+constexpr uint32_t kTmemCols = 512;
+constexpr float kLog2e = 1.4426950408889634f;
+
+struct BwdParams {
+  Pattern pat;
+  int32_t N, heads, batch;
+  float scale, scale_log2, inv_scale;
+  const int32_t* t_row_ptr;
+  const int32_t* t_col_idx;
+  const uint8_t* t_kind;
+  const uint8_t* t_dq;     // dQ chaining plan per transposed entry (HLA_DQ_*; null = one chain per tile)
+  const float* lse2;       // LSE * log2(e), [B, H, N] (workspace, from the preprocess)
+  const float* dsum;       // D * scale, [B, H, N] (workspace, from the preprocess)
+  float* dq_acc;           // [B, N, H, Dh] fp32 (grid order when s2c != null)
+  const int32_t* s2c;      // fused reorder: seq_to_cell table (tensors in grid order), else null
+  const float* rpb;        // global RPB table [heads][2H-1][2W-1] (kBias)
+  float* drpb;             // its gradient (accumulated)
+  const int32_t* cells;    // grid cell of each sequence position (null: identity)
+  int32_t grid_h, grid_w, rpb_w, rpb_hw;
+  __nv_bfloat16* dk;
+  __nv_bfloat16* dv;
+  __nv_bfloat16* dq;       // dQ rows of LOCAL chains (bf16, same layout as dk)
+  unsigned long long* visited;
+};
+
+// Kernel launch of one schedule for the head_dim / reorder / 2D-pattern variant; the maps
+// view Q, K, V, dO as bf16 rows and the fp32 dQ accumulator (see hla_attn_bwd_main).
+hla_status launch_full(bool bias, int head_dim, bool gather, bool two_d, const CUtensorMap& mq,
+                       const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq,
+                       const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream);
+hla_status launch_split(int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
+                        const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm,
+                        int32_t n_kblocks, cudaStream_t stream);
+
+template <int D>
+__device__ __forceinline__ uint64_t kmajor_desc(const uint8_t* tile, int kstep) {
+  constexpr uint32_t layout = D == 64 ? sm100::kSwizzle128B : sm100::kSwizzle64B;
+  return sm100::make_smem_desc(sm100::smem_u32(tile) + kstep * 32, 16, 8 * D * 2, layout);
+}
+template <int D>
+__device__ __forceinline__ uint64_t mnmajor_desc(const uint8_t* tile, int kstep) {
+  constexpr uint32_t layout = D == 64 ? sm100::kSwizzle128B : sm100::kSwizzle64B;
+  return sm100::make_smem_desc(sm100::smem_u32(tile) + kstep * 16 * D * 2, kBlock * D * 2, 8 * D * 2, layout);
+}
+// TMEM column of the packed bf16 P^T (A of dV += P^T dO) for K step kk (16 q): the compute
+// thread of 32-column chunk c writes its 32 values over the chunk's first 16 S^T columns
+__device__ __forceinline__ uint32_t packed_col(int kk) { return (uint32_t)((kk >> 1) * 32 + (kk & 1) * 8); }
+// dS^T smem tile viewed as K-major A of dK += dS^T Q (M = kv, K = q): K step = 16 q
+__device__ __forceinline__ uint64_t ds_kmajor_desc(const uint8_t* ds, int kstep) {
+  return sm100::make_smem_desc(sm100::smem_u32(ds) + (kstep >> 2) * 16384 + (kstep & 3) * 32, 16, 1024,
+                               sm100::kSwizzle128B);
+}
+// dS^T smem tile viewed as MN-major A of dQ = dS K (M = q, K = kv): K step = 16 kv rows
+__device__ __forceinline__ uint64_t ds_mnmajor_desc(const uint8_t* ds, int kstep) {
+  return sm100::make_smem_desc(sm100::smem_u32(ds) + kstep * 2048, 16384, 1024, sm100::kSwizzle128B);
+}
+
+// Work units are pairs (2p, 2p+1) of kv-blocks of one (b, h) -- the unit of the dQ
+// plan (hla_build_bwd_plan) -- strided over the grid.  Consecutive kv-blocks share
+// q-blocks (the producer then skips reloading a Q/dO stage, and dQ partials chain in
+// TMEM), while all CTAs stay on nearby units (L2 reuse).
+constexpr int32_t kUnitEnd = 0x7fffffff, kUnitSkip = -1;
+struct UnitGeom {
+  int32_t mk, ppb, pairs;   // kv-blocks per (b, h), pairs per (b, h), pairs in total
+};
+// k-th kv-block of this CTA: flattened u = (b * heads + h) * mk + kb, kUnitSkip for
+// the missing second block of a ragged last pair, kUnitEnd past the last pair
+__device__ __forceinline__ int32_t unit_at(int32_t k, const UnitGeom& ug) {
+  const int32_t P = (int32_t)blockIdx.x + (k >> 1) * (int32_t)gridDim.x;
+  if (P >= ug.pairs) return kUnitEnd;
+  const int32_t bh = P / ug.ppb;
+  const int32_t kb = 2 * (P - bh * ug.ppb) + (k & 1);
+  return kb < ug.mk ? bh * ug.mk + kb : kUnitSkip;
+}
+
+// Iterator over the flattened (work unit, q-block tile) sequence of this CTA,
+// skipping units without tiles.  n = ordinal of the current non-empty unit.
+struct TileIter {
+  int32_t k, u, t, nt, rs;
+  uint32_t n;
+  bool valid;
+  __device__ void seek(const int32_t* t_row_ptr, const UnitGeom& ug) {
+    for (;; ++k) {
+      u = unit_at(k, ug);
+      if (u == kUnitEnd) break;
+      if (u < 0) continue;
+      const int32_t kb = u % ug.mk;
+      rs = __ldg(t_row_ptr + kb);
+      nt = __ldg(t_row_ptr + kb + 1) - rs;
+      if (nt > 0) { valid = true; return; }
+    }
+    valid = false;
+  }
+  __device__ void init(const int32_t* t_row_ptr, const UnitGeom& ug) {
+    k = 0; t = 0; n = 0;
+    seek(t_row_ptr, ug);
+  }
+  __device__ void advance(const int32_t* t_row_ptr, const UnitGeom& ug) {
+    if (++t < nt) return;
+    t = 0; ++n; ++k;
+    seek(t_row_ptr, ug);
+  }
+};
+
+// dQ plan bits of the g-th tile (transposed entry e); without a plan every tile is
+// its own chain, alternating between the two accumulators
+__device__ __forceinline__ uint32_t dq_plan(const uint8_t* t_dq, int32_t e, uint32_t g) {
+  return t_dq ? (uint32_t)__ldg(t_dq + e) : ((g & 1u) | HLA_DQ_NEW | HLA_DQ_DRAIN);
+}
+
+// Load the 128 token rows [seq0, seq0 + 128) (sequence order) of head h, batch b;
+// see attn_fwd.cu load_rows (kGather = fused reorder through s2c with .tile::gather4).
+template <int D, bool kGather>
+__device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int32_t h,
+                                          int32_t b, int32_t N, int32_t seq0, const int32_t* s2c, uint64_t pol,
+                                          int lane) {
+  if (kGather) {
+    // rows past N (ragged last tile) gather cell 0: their values are masked / discarded
+    const int4 c = seq0 + 4 * lane < N ? __ldg(reinterpret_cast<const int4*>(s2c + seq0) + lane) : make_int4(0, 0, 0, 0);
+    const int32_t base = b * N;
+    sm100::tma_gather4(dst + lane * 4 * D * 2, map, bar, h * D, base + c.x, base + c.y, base + c.z, base + c.w, pol);
+  } else if (lane == 0) {
+    sm100::tma_load_3d(dst, map, bar, 0, h, b * N + seq0, pol);
+  }
+}
+
+// cell -> (row << 16) | col (RPB offsets; grid sides < 2^15)
+__device__ __forceinline__ int32_t rpb_cell_rc(const int32_t* cells, int32_t seq, int32_t N, int32_t W) {
+  const int32_t cell = seq < N ? (cells ? __ldg(cells + seq) : seq) : 0;
+  const int32_t r = cell / W;
+  return (r << 16) | (cell - r * W);
+}
+// min / max of the rows and columns of the cells of sequence block [s0, s0 + 128)
+// (phantom positions >= N ignored); identical in every lane.
+struct CellBox { int32_t r0, r1, c0, c1; };
+__device__ __forceinline__ CellBox rpb_block_box(const int32_t* cells, int32_t s0, int32_t N, int32_t W, int lane) {
+  CellBox bx{1 << 30, -(1 << 30), 1 << 30, -(1 << 30)};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int32_t sq = s0 + 32 * j + lane;
+    if (sq < N) {
+      const int32_t rc = rpb_cell_rc(cells, sq, N, W);
+      const int32_t r = rc >> 16, c = rc & 0xffff;
+      bx.r0 = min(bx.r0, r); bx.r1 = max(bx.r1, r); bx.c0 = min(bx.c0, c); bx.c1 = max(bx.c1, c);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    bx.r0 = min(bx.r0, __shfl_xor_sync(0xffffffffu, bx.r0, o));
+    bx.r1 = max(bx.r1, __shfl_xor_sync(0xffffffffu, bx.r1, o));
+    bx.c0 = min(bx.c0, __shfl_xor_sync(0xffffffffu, bx.c0, o));
+    bx.c1 = max(bx.c1, __shfl_xor_sync(0xffffffffu, bx.c1, o));
+  }
+  return bx;
+}
+
+}  // namespace bwd
+}  // namespace hla

@@ -1,0 +1,560 @@
+// K8 (half-tile schedule): block-sparse attention backward on sm_100a for masks made
+// mostly of PARTIAL tiles (slides, neighbourhoods, shifted / small windows: "partial
+// blocks require element-wise masking").  Same operation, operands and outputs as the
+// full-tile schedule in attn_bwd.cu (see its header for the gradient formulas); chosen by
+// hla_attn_bwd_main when partial tiles outnumber full ones.
+//
+// Persistent, 1 CTA / SM, kv-major over the transposed CSR (work unit = a pair of
+// consecutive kv-blocks of one (b, h)).  512 threads = 16 warps:
+//    warps 0, 14, 15  TMA producers: K_j (+ LSE_i, D_i bulk copies) / V_j, Q_i / dO_i;
+//    warp 1     TMEM allocator + single-thread tcgen05.mma issuer:
+//                 S^T  = K_j Q_i^T     (SS, N = 64 per query half, TMEM cols [0,128))
+//                 dP^T = V_j dO_i^T    (SS, N = 64 per query half, TMEM cols [128,256))
+//                 dV  += P^T dO_i      (TS, P^T bf16 written over the first 16 columns of
+//                                       each 32-column S^T chunk; acc [384,448))
+//                 dK  += dS^T Q_i      (SS, dS^T bf16 in smem, K-major view; acc [448,512))
+//                 dQ_i (+)= dS K_j     (SS, same dS smem, MN-major view; two accumulators
+//                                       [256,320) / [320,384) chained by the mask's dQ plan)
+//               half-tile software pipeline: the tensor core works on one 64-query half
+//               while the compute warps turn the other into P^T / dS^T, so the element
+//               masks of partial tiles overlap the MMAs;
+//    warps 2-9  thread = key row (two warps per TMEM lane quarter, one 32-column chunk
+//               each per half): P^T, dS^T (mask only on partial tiles);
+//    warps 10-13 thread = query row: dQ_i drains (bf16 rows for complete chains, else
+//               smem -> TMA reduce-add into the fp32 accumulator) and the dK / dV rows.
+// No global-RPB score_mod here: that runs on the full-tile schedule.
+#include "attn_bwd_common.cuh"
+
+namespace hla {
+namespace bwd {
+namespace {
+
+constexpr int kThreads = 512;   // 16 warps: TMA, MMA, 8 x P/dS, 4 x dQ, 2 x TMA
+constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256, kColDV = 384, kColDK = 448;   // dQ: 2 x 64 columns
+constexpr int kHalf = 64;       // q-columns per pipeline half
+#ifndef HLA_BWD_VAR
+#define HLA_BWD_VAR 0
+#endif
+constexpr int kVar = HLA_BWD_VAR;   // dev-only decomposition switches, see attn_bwd.cu
+
+template <int D>
+struct SplitSmem {
+  static constexpr uint32_t kTileBytes = kBlock * D * 2;
+  alignas(1024) uint8_t k[2][kTileBytes];
+  alignas(1024) uint8_t v[2][kTileBytes];
+  alignas(1024) uint8_t q[2][kTileBytes];
+  alignas(1024) uint8_t dO[2][kTileBytes];
+  alignas(1024) uint8_t ds[2][2 * 128 * 128];   // dS^T bf16 x2 (tile parity): [q/64][kv 128][64 q], SWIZZLE_128B
+  alignas(1024) float dq_stage[kBlock * 32];    // fp32 dQ half tile [128][32], SWIZZLE_128B
+  alignas(16) float lse[2][kBlock];
+  alignas(16) float dd[2][kBlock];
+  uint64_t kv_full[2], kv_empty[2], q_full[2], q_empty[2], s_full[2], ds_ready[2], dq_full[2], dq_free[2], dkv_full,
+      epi_done;
+  uint32_t tmem_base;
+};
+
+template <int D, bool kTwoD, bool kGather>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                    const __grid_constant__ CUtensorMap tmDQ, const BwdParams prm) {
+  extern __shared__ uint8_t smem_raw[];
+  using Smem = SplitSmem<D>;
+  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  UnitGeom ug;
+  ug.mk = (prm.N + kBlock - 1) / kBlock;   // last kv-block may be ragged
+  ug.ppb = (ug.mk + 1) / 2;
+  ug.pairs = ug.ppb * prm.heads * prm.batch;
+  const int32_t mk = ug.mk;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < 2; ++s) {
+      sm100::mbar_init(&sm.kv_full[s], 2);    // producer warps 0 (K), 14 (V)
+      sm100::mbar_init(&sm.kv_empty[s], 1);
+      sm100::mbar_init(&sm.q_full[s], 3);     // producer warps 0 (LSE, D), 14 (Q), 15 (dO)
+      sm100::mbar_init(&sm.q_empty[s], 1);
+    }
+    for (int hh = 0; hh < 2; ++hh) {
+      sm100::mbar_init(&sm.s_full[hh], 1);
+      sm100::mbar_init(&sm.ds_ready[hh], 256);
+    }
+    for (int bb = 0; bb < 2; ++bb) {
+      sm100::mbar_init(&sm.dq_full[bb], 1);
+      sm100::mbar_init(&sm.dq_free[bb], 128);
+    }
+    sm100::mbar_init(&sm.dkv_full, 1);
+    sm100::mbar_init(&sm.epi_done, 128);
+        sm100::fence_mbar_init();
+    sm100::tma_prefetch_desc(&tmQ);
+    sm100::tma_prefetch_desc(&tmK);
+    sm100::tma_prefetch_desc(&tmV);
+    sm100::tma_prefetch_desc(&tmDO);
+  }
+  if (warp == 1) {
+    sm100::tmem_alloc(&sm.tmem_base, kTmemCols);
+    sm100::tmem_relinquish();
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+  unsigned long long tiles_done = 0;
+
+  if (warp == 0 || warp >= 14) {
+    // ----------------------------------------------------------- TMA producers
+    // Three warps run the same schedule and split the loads (a CTA's TMA gather4
+    // throughput grows with the number of issuing warps): warp 0 K + LSE / D,
+    // warp 14 V + Q, warp 15 dO.  Every warp arrives (with its own byte count) on
+    // the barriers it feeds, so no expect_tx has to precede another warp's copy.
+    {
+      const uint64_t pol_kv = sm100::policy_evict_first();
+      const uint64_t pol_q = sm100::policy_evict_last();
+      const int role = warp == 0 ? 0 : warp - 13;   // 0, 1, 2
+      constexpr uint32_t kTile = Smem::kTileBytes;
+      uint32_t n = 0, g = 0;
+      int64_t stage_tag0 = -1, stage_tag1 = -1;   // (b, h, q-block) held by stage 0 / 1
+      for (int32_t kq = 0;; ++kq) {
+        const int32_t u = unit_at(kq, ug);
+        if (u == kUnitEnd) break;
+        if (u < 0) continue;
+        const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
+        const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
+        if (nt == 0) continue;
+        const int64_t bh = (int64_t)b * prm.heads + h;
+        const int kvs = n & 1;
+        if (role < 2) {
+          if (n >= 2) sm100::mbar_wait(&sm.kv_empty[kvs], ((n >> 1) - 1) & 1);
+          if (kVar & 4) {
+            if (lane == 0) sm100::mbar_arrive(&sm.kv_full[kvs]);
+          } else {
+            if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.kv_full[kvs], kTile);
+            __syncwarp();
+            load_rows<D, kGather>(role == 0 ? sm.k[kvs] : sm.v[kvs], role == 0 ? &tmK : &tmV, &sm.kv_full[kvs], h,
+                                  b, prm.N, kb * kBlock, prm.s2c, pol_kv, lane);
+          }
+        }
+        for (int t = 0; t < nt; ++t, ++g) {
+          const int s = g & 1;
+          if (g >= 2) sm100::mbar_wait(&sm.q_empty[s], ((g >> 1) - 1) & 1);
+          const int32_t qblk = __ldg(prm.t_col_idx + rs + t);
+          const int64_t tag = bh * prm.N + qblk;     // (b, h, q-block) held by the stage
+          if (tag == (s ? stage_tag1 : stage_tag0)) {
+            // the stage already holds this q-block (consecutive kv-blocks share
+            // q-blocks): no reload, just publish it again
+            if (lane == 0) sm100::mbar_arrive(&sm.q_full[s]);
+            continue;
+          }
+          if (s) stage_tag1 = tag; else stage_tag0 = tag;
+          if (role == 0) {
+            if (lane == 0 && (kVar & 4)) {
+              sm100::mbar_arrive(&sm.q_full[s]);
+            } else if (lane == 0) {
+              // LSE / D of the real rows only (ragged last tile: N % 4 == 0, so 16-B multiples)
+              const uint32_t vbytes = (uint32_t)min(kBlock, prm.N - qblk * kBlock) * 4u;
+              sm100::mbar_arrive_expect_tx(&sm.q_full[s], 2 * vbytes);
+              sm100::bulk_load(sm.lse[s], prm.lse2 + bh * prm.N + qblk * kBlock, vbytes, &sm.q_full[s]);
+              sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * kBlock, vbytes, &sm.q_full[s]);
+            }
+          } else if (kVar & 4) {
+            if (lane == 0) sm100::mbar_arrive(&sm.q_full[s]);
+          } else {
+            if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.q_full[s], kTile);
+            __syncwarp();
+            load_rows<D, kGather>(role == 1 ? sm.q[s] : sm.dO[s], role == 1 ? &tmQ : &tmDO, &sm.q_full[s], h, b,
+                                  prm.N, qblk * kBlock, prm.s2c, pol_q, lane);
+          }
+        }
+        ++n;
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------- MMA issuer
+    // Half-tile software pipeline over the flattened (unit, q-block) sequence:
+    //   S_A,dP_A(g) S_B,dP_B(g) | dV_A dK_A(g) S_A,dP_A(g+1) | dV_B dK_B dQ(g) S_B,dP_B(g+1) | ...
+    // so the tensor core works on one q-half while the compute warps process the other.
+    if (lane == 0) {
+      constexpr uint32_t idesc_h = sm100::make_idesc_bf16(kBlock, kHalf, false, false);  // S^T, dP^T halves
+      constexpr uint32_t idesc_kv = sm100::make_idesc_bf16(kBlock, D, false, true);      // dV, dK
+      constexpr uint32_t idesc_q = sm100::make_idesc_bf16(kBlock, D, true, true);        // dQ
+      const uint32_t tDQ = tmem + kColDQ, tDV = tmem + kColDV, tDK = tmem + kColDK;
+      TileIter cur;
+      cur.init(prm.t_row_ptr, ug);
+      uint32_t g = 0;
+      uint32_t dq_started0 = 0, dq_started1 = 0;   // chains begun per dQ accumulator
+      auto issue_sdp = [&](const TileIter& it, uint32_t gg, int half) {
+        const int s = gg & 1;
+        const uint8_t* sk = sm.k[it.n & 1];
+        const uint8_t* sv = sm.v[it.n & 1];
+        const uint32_t qoff = half * kHalf * D * 2;   // first row of this q half
+#pragma unroll
+        for (int kk = 0; kk < D / 16 && !(kVar & 1); ++kk)
+          sm100::mma_ss(tmem + kColS + half * kHalf, kmajor_desc<D>(sk, kk), kmajor_desc<D>(sm.q[s] + qoff, kk),
+                        idesc_h, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16 && !(kVar & 1); ++kk)
+          sm100::mma_ss(tmem + kColDP + half * kHalf, kmajor_desc<D>(sv, kk), kmajor_desc<D>(sm.dO[s] + qoff, kk),
+                        idesc_h, kk > 0);
+        sm100::mma_commit(&sm.s_full[half]);
+      };
+      auto issue_dvdk = [&](uint32_t gg, int half, bool first_tile) {
+        const int s = gg & 1;
+        const uint8_t* ds = sm.ds[gg & 1];
+#pragma unroll
+        for (int kk = half * 4; kk < half * 4 + 4 && !(kVar & 1); ++kk) {
+          const uint32_t acc = (!first_tile || kk > 0) ? 1u : 0u;
+          // P^T of q-columns [16kk, 16kk + 16): 8 packed columns at the start of S^T chunk kk/2
+          sm100::mma_ts(tDV, tmem + kColS + (kk >> 1) * 32 + (kk & 1) * 8, mnmajor_desc<D>(sm.dO[s], kk), idesc_kv,
+                        acc);
+          sm100::mma_ss(tDK, ds_kmajor_desc(ds, kk), mnmajor_desc<D>(sm.q[s], kk), idesc_kv, acc);
+        }
+      };
+      if (cur.valid) {
+        sm100::mbar_wait(&sm.kv_full[cur.n & 1], (cur.n >> 1) & 1);
+        sm100::mbar_wait(&sm.q_full[0], 0);
+        sm100::tc_fence_after();
+        issue_sdp(cur, 0, 0);
+        issue_sdp(cur, 0, 1);
+      }
+      while (cur.valid) {
+        TileIter nxt = cur;
+        nxt.advance(prm.t_row_ptr, ug);
+        const uint32_t fdq = dq_plan(prm.t_dq, cur.rs + cur.t, g);
+        const int kvs = cur.n & 1;
+        const bool last_of_unit = cur.t == cur.nt - 1;
+        // half A of tile g
+        sm100::mbar_wait(&sm.ds_ready[0], g & 1);
+        sm100::tc_fence_after();
+        if (cur.t == 0 && cur.n > 0) {
+          // the previous unit's dV / dK must have been drained from TMEM
+          sm100::mbar_wait(&sm.epi_done, (cur.n - 1) & 1);
+          sm100::tc_fence_after();
+        }
+        issue_dvdk(g, 0, cur.t == 0);
+        // S_A / dP_A of the next tile now if its operands already landed (never block
+        // here: the B half of this tile must not wait behind the next tile's loads)
+        bool next_a_issued = false;
+        if (nxt.valid && (nxt.t != 0 || sm100::mbar_test_wait(&sm.kv_full[nxt.n & 1], (nxt.n >> 1) & 1)) &&
+            sm100::mbar_test_wait(&sm.q_full[(g + 1) & 1], ((g + 1) >> 1) & 1)) {
+          sm100::tc_fence_after();
+          issue_sdp(nxt, g + 1, 0);
+          next_a_issued = true;
+        }
+        // half B of tile g, then dQ (needs both halves of dS)
+        sm100::mbar_wait(&sm.ds_ready[1], g & 1);
+        sm100::tc_fence_after();
+        issue_dvdk(g, 1, false);
+        sm100::mma_commit(&sm.q_empty[g & 1]);   // Q_g / dO_g no longer read (dQ needs only dS and K)
+        if (last_of_unit) sm100::mma_commit(&sm.dkv_full);
+        const int dqb = (int)(fdq & HLA_DQ_BUF);
+        const bool dq_new = (fdq & HLA_DQ_NEW) != 0;
+        if (dq_new) {
+          // a new chain: the accumulator's previous chain must have been drained
+          const uint32_t c = dqb ? dq_started1++ : dq_started0++;
+          if (c > 0) {
+            sm100::mbar_wait(&sm.dq_free[dqb], (c - 1) & 1);
+            sm100::tc_fence_after();
+          }
+        }
+#pragma unroll
+        for (int kk = 0; kk < kBlock / 16 && !(kVar & 1); ++kk)
+          sm100::mma_ss(tDQ + dqb * 64, ds_mnmajor_desc(sm.ds[g & 1], kk), mnmajor_desc<D>(sm.k[kvs], kk), idesc_q,
+                        (kk > 0 || !dq_new) ? 1u : 0u);
+        if (fdq & HLA_DQ_DRAIN) sm100::mma_commit(&sm.dq_full[dqb]);
+        if (last_of_unit) sm100::mma_commit(&sm.kv_empty[kvs]);
+        if (nxt.valid) {
+          if (!next_a_issued) {
+            if (nxt.t == 0) sm100::mbar_wait(&sm.kv_full[nxt.n & 1], (nxt.n >> 1) & 1);
+            sm100::mbar_wait(&sm.q_full[(g + 1) & 1], ((g + 1) >> 1) & 1);
+            sm100::tc_fence_after();
+            issue_sdp(nxt, g + 1, 0);
+          }
+          issue_sdp(nxt, g + 1, 1);
+        }
+        cur = nxt;
+        ++g;
+      }
+    }
+  } else if (warp < 10) {
+    // --------------------------------------------- P^T / dS^T (thread = key row)
+    // two warp sets (cset 0: warps 2-5, cset 1: warps 6-9) share every TMEM lane
+    // quarter; within each q-half, cset c processes the 32-column chunk 2*half + c.
+    const int quarter = warp & 3;
+    const int cset = (warp - 2) >> 2;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const float sl2 = prm.scale_log2, scale = prm.scale;
+    uint32_t n = 0, g = 0;
+    for (int32_t kq = 0;; ++kq) {
+      const int32_t u = unit_at(kq, ug);
+      if (u == kUnitEnd) break;
+      if (u < 0) continue;
+      const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
+      const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
+      const int32_t kidx = kb * kBlock + row;
+      RowBox box = clip_box<kTwoD>(prm.pat, col_box(prm.pat, kidx));
+      if (kidx >= prm.N) box.len = 0;   // phantom key row of a ragged tile: nothing allowed
+      for (int t = 0; t < nt; ++t, ++g) {
+        const int s = g & 1;
+        const uint8_t kd = __ldg(prm.t_kind + rs + t);
+        const int32_t q0 = __ldg(prm.t_col_idx + rs + t) * kBlock;
+        sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1);
+        const uint32_t lse2 = sm100::smem_u32(sm.lse[s]);
+        const uint32_t dd = sm100::smem_u32(sm.dd[s]);
+        const uint32_t dsbuf = sm100::smem_u32(sm.ds[g & 1]);
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+          sm100::mbar_wait(&sm.s_full[half], g & 1);
+          sm100::tc_fence_after();
+          if (!(kVar & 2)) {
+            const int c = 2 * half + cset;
+            uint32_t sr[32], dpr[32];
+            sm100::tmem_ld32(tmem + lane_off + kColS + c * 32, sr);
+            sm100::tmem_ld32(tmem + lane_off + kColDP + c * 32, dpr);
+            sm100::tmem_wait_ld();
+            // [ulo, uhi): 8-column groups of this chunk that hold an allowed query of some
+            // key row of this warp (partial tiles of 1D patterns: each key row's queries are
+            // one interval); the other groups are all masked, their exponentials skipped
+            // (warp-uniform) and P = 0 there.  Full tiles / 2D patterns: all 4 groups.
+            int ulo = 0, uhi = 4;
+            if (kd == 2 && !kTwoD) {
+              const int32_t base = q0 + c * 32;
+              const int32_t lo = min(max(box.lo - base, 0), 32), hi = min(max(box.lo + box.len - base, 0), 32);
+              const bool any = hi > lo;
+              ulo = __reduce_min_sync(0xffffffffu, any ? lo : 32) >> 3;
+              uhi = (__reduce_max_sync(0xffffffffu, any ? hi : 0) + 7) >> 3;
+            }
+            // P first (so its TMEM store is in flight while dS is formed)
+            float p[32];
+#pragma unroll
+            for (int u4 = 0; u4 < 4; ++u4) {
+              if (u4 < ulo || u4 >= uhi) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) p[u4 * 8 + e] = 0.f;
+                continue;
+              }
+              const int qc = c * 32 + u4 * 8;
+              const float4 la = sm100::lds_f4(lse2 + qc * 4), lb = sm100::lds_f4(lse2 + qc * 4 + 16);
+              const float lv[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                p[u4 * 8 + e] = sm100::ex2(fmaf(__uint_as_float(sr[u4 * 8 + e]), sl2, -lv[e]));
+              }
+            }
+            uint32_t okbits = 0xffffffffu;   // element mask of this chunk (partial tiles only)
+            if (kd == 2) {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) {
+                const int32_t qq = q0 + c * 32 + e;
+                bool ok;
+                if (!kTwoD) {
+                  ok = (uint32_t)(qq - box.lo) < (uint32_t)box.len;
+                } else {
+                  const int32_t rq = prm.pat.log2W >= 0 ? (qq >> prm.pat.log2W) : qq / prm.pat.W;
+                  const int32_t cq = qq - rq * prm.pat.W;
+                  ok = ((uint32_t)(rq - box.lo) < (uint32_t)box.len) && ((uint32_t)(cq - box.c0) < (uint32_t)box.cn);
+                }
+                if (!ok) {
+                  p[e] = 0.f;
+                  okbits &= ~(1u << e);
+                }
+              }
+            }
+            {
+              uint32_t pk[16];
+#pragma unroll
+              for (int e = 0; e < 16; ++e) pk[e] = sm100::pack_bf16(p[2 * e], p[2 * e + 1]);
+              // over the first 16 columns of this thread's own S^T chunk (already in registers)
+              sm100::tmem_st16(tmem + lane_off + kColS + c * 32, pk);
+            }
+#pragma unroll
+            for (int u4 = 0; u4 < 4; ++u4) {   // dS, 8 query columns (one 16B chunk) at a time
+              const int qc = c * 32 + u4 * 8;
+              const float4 da = sm100::lds_f4(dd + qc * 4), db = sm100::lds_f4(dd + qc * 4 + 16);
+              const float dv[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
+              float ds[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                ds[e] = p[u4 * 8 + e] * fmaf(__uint_as_float(dpr[u4 * 8 + e]), scale, -dv[e]);
+                // masked: exactly 0 (the D / LSE of phantom query columns may be stale, 0 * NaN = NaN)
+                if (!((okbits >> (u4 * 8 + e)) & 1u)) ds[e] = 0.f;
+              }
+              // dS^T row -> smem [q/64][kv][64] with the 128B swizzle (16B chunks)
+              const uint32_t off =
+                  (uint32_t)(qc >> 6) * 16384u + sm100::swz128((uint32_t)row * 128u + (uint32_t)(qc & 63) * 2u);
+              sm100::sts_u4(dsbuf + off, sm100::pack_bf16(ds[0], ds[1]), sm100::pack_bf16(ds[2], ds[3]),
+                            sm100::pack_bf16(ds[4], ds[5]), sm100::pack_bf16(ds[6], ds[7]));
+            }
+          }
+          sm100::tmem_wait_st();
+          sm100::fence_proxy_async_smem();
+          sm100::tc_fence_before();
+          sm100::mbar_arrive(&sm.ds_ready[half]);
+        }
+      }
+      tiles_done += nt;
+    }
+  } else if (warp < 14) {
+    // ------------------------------------------ dQ partial -> fp32 accumulator
+    // thread = query row: drain the dQ_i tile from TMEM (then release it), stage it
+    // in shared memory (two 32-column halves, 128B swizzle) and let the TMA engine
+    // add it into the fp32 accumulator (cp.reduce.async.bulk.tensor ... add) -- no
+    // per-thread atomics, so the LSU stays free for the compute warps.
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const bool leader = warp == 10 && lane == 0;
+    uint32_t g = 0, n = 0;
+    uint32_t dq_drained0 = 0, dq_drained1 = 0;   // chains drained per dQ accumulator
+    for (int32_t kq = 0;; ++kq) {
+      const int32_t u = unit_at(kq, ug);
+      if (u == kUnitEnd) break;
+      if (u < 0) continue;
+      const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
+      const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
+      for (int t = 0; t < nt; ++t, ++g) {
+        const uint32_t fdq = dq_plan(prm.t_dq, rs + t, g);
+        if (!(fdq & HLA_DQ_DRAIN)) continue;   // the chain continues in TMEM
+        const int dqb = (int)(fdq & HLA_DQ_BUF);
+        sm100::mbar_wait(&sm.dq_full[dqb], (dqb ? dq_drained1++ : dq_drained0++) & 1);
+        sm100::tc_fence_after();
+        if (kVar & 8) {
+          sm100::mbar_arrive(&sm.dq_free[dqb]);
+          continue;
+        }
+        const int32_t qblk = __ldg(prm.t_col_idx + rs + t);
+        const int32_t qrow = b * prm.N + qblk * kBlock;   // sequence order
+        uint32_t r[D];
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c)
+          sm100::tmem_ld32(tmem + lane_off + kColDQ + dqb * 64 + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
+        sm100::tmem_wait_ld();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&sm.dq_free[dqb]);     // the TMEM dQ accumulator may now be overwritten
+        if (fdq & HLA_DQ_LOCAL) {
+          // complete dQ_i (dS carries the softmax scale): bf16 rows straight to dq, to the
+          // grid cell under the fused reorder; phantom rows of a ragged tile write nothing
+          const int32_t qs = qblk * kBlock + row;
+          if (qs < prm.N) {
+            const int32_t qcell = kGather ? __ldg(prm.s2c + qs) : qs;
+            uint4* dqp = reinterpret_cast<uint4*>(prm.dq + (((int64_t)b * prm.N + qcell) * prm.heads + h) * D);
+#pragma unroll
+            for (int v4 = 0; v4 < D / 8; ++v4)
+              dqp[v4] = make_uint4(sm100::pack_bf16(__uint_as_float(r[8 * v4 + 0]), __uint_as_float(r[8 * v4 + 1])),
+                                   sm100::pack_bf16(__uint_as_float(r[8 * v4 + 2]), __uint_as_float(r[8 * v4 + 3])),
+                                   sm100::pack_bf16(__uint_as_float(r[8 * v4 + 4]), __uint_as_float(r[8 * v4 + 5])),
+                                   sm100::pack_bf16(__uint_as_float(r[8 * v4 + 6]), __uint_as_float(r[8 * v4 + 7])));
+          }
+          continue;
+        }
+#pragma unroll
+        for (int hh = 0; hh < D / 32; ++hh) {
+          if (leader) sm100::bulk_wait_group_read0();   // previous reduce finished reading the stage
+          sm100::named_bar_sync(2, 128);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t off = sm100::swz128((uint32_t)row * 128u + (uint32_t)j * 16u);
+            sm100::sts_u4(sm100::smem_u32(sm.dq_stage) + off, r[hh * 32 + 4 * j], r[hh * 32 + 4 * j + 1],
+                          r[hh * 32 + 4 * j + 2], r[hh * 32 + 4 * j + 3]);
+          }
+          sm100::fence_proxy_async_smem();
+          sm100::named_bar_sync(2, 128);
+          if (leader) {
+            sm100::tma_reduce_add_3d(&tmDQ, sm.dq_stage, hh * 32, h, qrow);
+            sm100::bulk_commit_group();
+          }
+        }
+      }
+      // final dK, dV rows of this unit -> bf16 (thread = key row; dS already carries
+      // the softmax scale).  Done here, off the compute warps' critical path; the
+      // next unit's first dV/dK MMA waits for epi_done.
+      const int32_t kidx = kb * kBlock + row;
+      const bool real = kidx < prm.N;   // phantom key rows of a ragged tile write nothing
+      const int32_t kcell = kGather ? (real ? __ldg(prm.s2c + kidx) : 0) : kidx;   // fused inverse reorder of dK, dV
+      const int64_t grow = ((int64_t)b * prm.N + kcell) * prm.heads + h;
+      uint4* dkp = reinterpret_cast<uint4*>(prm.dk + grow * D);
+      uint4* dvp = reinterpret_cast<uint4*>(prm.dv + grow * D);
+      if (nt > 0) {
+        sm100::mbar_wait(&sm.dkv_full, n & 1);
+        sm100::tc_fence_after();
+        if (kVar & 8) {
+          sm100::mbar_arrive(&sm.epi_done);
+          ++n;
+          continue;
+        }
+        // dV then dK, each packed to bf16 right away (64 live registers, not 128)
+        uint32_t pv[D / 2], pk[D / 2];
+#pragma unroll
+        for (int which = 0; which < 2; ++which) {
+          uint32_t r[D];
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c)
+            sm100::tmem_ld32(tmem + lane_off + (which ? kColDK : kColDV) + c * 32,
+                             *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
+          sm100::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < D / 2; ++e) {
+            const uint32_t w = sm100::pack_bf16(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
+            if (which) pk[e] = w; else pv[e] = w;
+          }
+        }
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&sm.epi_done);      // dV / dK accumulators may now be reset
+#pragma unroll
+        for (int v4 = 0; v4 < D / 8 && real; ++v4) {
+          dvp[v4] = make_uint4(pv[v4 * 4 + 0], pv[v4 * 4 + 1], pv[v4 * 4 + 2], pv[v4 * 4 + 3]);
+          dkp[v4] = make_uint4(pk[v4 * 4 + 0], pk[v4 * 4 + 1], pk[v4 * 4 + 2], pk[v4 * 4 + 3]);
+        }
+        ++n;
+      } else {
+#pragma unroll
+        for (int c = 0; c < D / 8 && real; ++c) {
+          dvp[c] = make_uint4(0, 0, 0, 0);
+          dkp[c] = make_uint4(0, 0, 0, 0);
+        }
+      }
+    }
+    if (leader) sm100::bulk_wait_group0();
+  }
+
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  if (warp == 1) sm100::tmem_dealloc(tmem, kTmemCols);
+  if (warp == 2 && lane == 0 && prm.visited != nullptr && tiles_done > 0) atomicAdd(prm.visited, tiles_done);
+}
+
+
+template <int D, bool kTwoD, bool kGather>
+hla_status launch_split_t(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                          const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm, int32_t n_kblocks,
+                          cudaStream_t stream) {
+  const size_t smem = sizeof(SplitSmem<D>) + 1024;
+  auto* fn = attn_bwd_split_kernel<D, kTwoD, kGather>;
+  HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t pairs = (int64_t)((n_kblocks + 1) / 2) * prm.heads * prm.batch;   // work units (kv-block pairs)
+  const int grid = (int)std::min<int64_t>(pairs, (int64_t)num_sms());
+  fn<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mdo, mdq, prm);
+  HLA_CUDA_TRY(cudaGetLastError());
+  return HLA_OK;
+}
+
+static_assert(sizeof(SplitSmem<64>) + 1024 <= 227 * 1024, "split bwd shared memory exceeds 227 KB");
+
+}  // namespace
+
+hla_status launch_split(int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
+                        const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm,
+                        int32_t n_kblocks, cudaStream_t stream) {
+  if (head_dim == 64) {
+    if (gather) return launch_split_t<64, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
+    return two_d ? launch_split_t<64, true, false>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream)
+                 : launch_split_t<64, false, false>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
+  }
+  if (gather) return launch_split_t<32, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
+  return two_d ? launch_split_t<32, true, false>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream)
+               : launch_split_t<32, false, false>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
+}
+
+}  // namespace bwd
+}  // namespace hla

@@ -294,6 +294,7 @@ extern "C" hla_status hla_build_block_mask(const hla_pattern_desc* d, hla_block_
                                                                   m->col_idx, m->kind, m->t_row_ptr, m->t_col_idx,
                                                                   m->t_kind, counts);
   HLA_CUDA_TRY(cudaGetLastError());
+  HLA_CUDA_TRY(cudaMemcpyAsync(m->host_counts, m->counts, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
   HLA_CUDA_TRY(cudaStreamSynchronize(stream));
   return HLA_OK;
 }
