@@ -91,9 +91,14 @@ typedef struct {
   int32_t order;            /* hla_order: sequence order the tensors are in */
   int32_t pattern;          /* hla_pattern */
   int32_t win_h, win_w;     /* window / kernel in cells; Hilbert patterns use n = win_h*win_w tokens */
-  int32_t shift;            /* HSWA 1D shift in tokens (0 <= shift < n); must be 0 otherwise */
+  int32_t shift;            /* HSWA 1D shift in tokens (0 < shift < n); must be 0 otherwise */
   int32_t block_q, block_k; /* tile shape b_q x b_k.  Mask builder: any >= 1.
-                               Attention: block_q == block_k == 128. */
+                               Attention: block_q == block_k, 64 or 128. */
+  /* Window / kernel sizes: WINDOW and SHIFTED_WINDOW need win_h | grid_h and win_w | grid_w
+     (S:L98); SLIDE / NEIGHBORHOOD accept even kernels too, with radius floor(n/2) (DESIGN.md
+     reading R5: BASELINE cfg3 uses a 16 x 16 = 256-token slide) -- an even 2D kernel then
+     spans 2*floor(k/2)+1 rows / columns (SA) or k cells with an off-centre clamped start
+     (NA2D, NATTEN's convention for the start). */
 } hla_pattern_desc;
 
 /* Block mask in CSR form (caller-allocated DEVICE arrays).  Entry kinds:
@@ -237,8 +242,9 @@ typedef struct {
  *   O = O / l (bf16), LSE = m + ln(l) (fp32, natural log).
  * q, k, v, o: bf16 [batch, N, heads, head_dim] in d->order.  lse: fp32
  * [batch, heads, N].  scale <= 0 selects 1/sqrt(head_dim).
- * Limits: head_dim in {32, 64}; block_q == block_k == 128; N % 128 == 0;
- * mask built for the same descriptor (n_qblocks == N/128).
+ * Limits: head_dim in {32, 64}; block_q == block_k in {64, 128}; N % 4 == 0 (a
+ * ragged last tile is masked); mask built for the same descriptor
+ * (n_qblocks == ceil(N / block)).
  * tiles_visited: optional device int64 counter; when non-NULL the kernel adds
  * the number of tiles it executed (must equal batch*heads*nnz: empty tiles are
  * skipped).

@@ -99,6 +99,8 @@ def validate(spec):
     if spec.kind in ("WSA", "HWA", "HSWA"):
         if spec.grid_h % spec.win_h or spec.grid_w % spec.win_w:
             raise ValueError("window does not divide the grid")
+    if spec.kind == "HSWA" and not 0 < spec.shift < spec.win_h * spec.win_w:
+        raise ValueError("HSWA shift must lie in (0, n) (S:L139-140)")
     if spec.kind in ("SA", "NA2D"):
         if spec.win_h > spec.grid_h or spec.win_w > spec.grid_w:
             raise ValueError("kernel larger than grid")

@@ -12,6 +12,7 @@ Layers:
                    one call per forward / backward step (the public API)
 """
 
+from ._lib import HlaError  # noqa: F401
 from .api import (KINDS, BlockMask, hla_attn_bwd, hla_attn_bwd_workspace, hla_attn_fwd,  # noqa: F401
                   hla_build_block_mask, hla_debug_umma, hla_hilbert_index, hla_hilbert_perm, pattern_desc,
                   version)

@@ -1,4 +1,6 @@
-"""ctypes loader for libhla.so (the C ABI declared in include/hla.h).
+"""ctypes loaders for libhla.so (the hot path: the C ABI declared in include/hla.h) and
+libhla_debug.so (tcgen05 / TMA bring-up and machine-constant probes, include/hla_debug.h;
+never loaded by the product path).
 
 Argument marshalling only.  There is deliberately no fallback: if the shared
 library is missing or fails to load, every call raises.
@@ -8,19 +10,20 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, os.environ.get("HLA_LIB_NAME", "libhla.so"))   # HLA_LIB_NAME: dev trace build
+LIB_PATH = os.path.join(_HERE, os.environ.get("HLA_LIB_NAME", "libhla.so"))   # HLA_LIB_NAME: dev variant builds
+DEBUG_LIB_PATH = os.path.join(_HERE, "libhla_debug.so")
 
 HLA_OK, HLA_ERR_INVALID, HLA_ERR_UNSUPPORTED, HLA_ERR_CAPACITY, HLA_ERR_CUDA = range(5)
 STATUS_NAMES = {0: "HLA_OK", 1: "HLA_ERR_INVALID", 2: "HLA_ERR_UNSUPPORTED", 3: "HLA_ERR_CAPACITY",
                 4: "HLA_ERR_CUDA"}
 
-# exported symbols of include/hla.h and include/hla_debug.h
+# exported symbols of include/hla.h (libhla.so) and include/hla_debug.h (libhla_debug.so)
 EXPORTED = ("hla_hilbert_index", "hla_hilbert_perm", "hla_build_block_mask", "hla_mask_ratios",
             "hla_attn_fwd", "hla_attn_bwd", "hla_attn_bwd_workspace", "hla_attn_bwd_preprocess",
-            "hla_attn_bwd_main", "hla_attn_bwd_finalize", "hla_build_bwd_plan", "hla_last_error", "hla_version",
-            "hla_debug_umma", "hla_debug_gather4", "hla_debug_mma_rate",
-            "hla_debug_tmem_rate", "hla_debug_ex2_rate", "hla_debug_xu_rate", "hla_debug_sync_latency",
-            "hla_debug_softmax_rate", "hla_debug_softmax_tile", "hla_debug_load_rate")
+            "hla_attn_bwd_main", "hla_attn_bwd_finalize", "hla_build_bwd_plan", "hla_last_error", "hla_version")
+DEBUG_EXPORTED = ("hla_debug_umma", "hla_debug_gather4", "hla_debug_mma_rate",
+                  "hla_debug_tmem_rate", "hla_debug_ex2_rate", "hla_debug_xu_rate", "hla_debug_sync_latency",
+                  "hla_debug_softmax_rate", "hla_debug_softmax_tile", "hla_debug_load_rate")
 
 
 class PatternDesc(ctypes.Structure):
@@ -51,55 +54,71 @@ class HlaError(RuntimeError):
 
 
 _lib = None
+_debug_lib = None
+
+_vp, _i32, _i64, _f32, _sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_size_t
+_pdesc, _pmask = ctypes.POINTER(PatternDesc), ctypes.POINTER(BlockMaskC)
+_SIG = {
+    "hla_hilbert_index": [_i32, _i32, _vp, _vp, _vp],
+    "hla_hilbert_perm": [_i32, _i32, _i32, _i32, _i32, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp],
+    "hla_build_block_mask": [_pdesc, _pmask, ctypes.POINTER(_i64), _vp],
+    "hla_mask_ratios": [_pdesc, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
+    "hla_attn_fwd": [_pdesc, _pmask, _i32, _i32, _i32, _f32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "hla_attn_bwd": [_pdesc, _pmask, _i32, _i32, _i32, _f32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                     _vp, _sz, _vp, _vp],
+    "hla_attn_bwd_preprocess": [_i32, _i32, _i32, _i32, _f32, _vp, _vp, _vp, _vp, _pmask, _vp, _sz, _vp],
+    "hla_attn_bwd_main": [_pdesc, _pmask, _i32, _i32, _i32, _f32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                          _sz, _vp, _vp],
+    "hla_attn_bwd_finalize": [_i32, _i32, _i32, _i32, _vp, _sz, _vp, _vp, _pmask, _vp],
+    "hla_build_bwd_plan": [_pmask, _vp],
+}
+_DEBUG_SIG = {
+    "hla_debug_umma": [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp],
+    "hla_debug_gather4": [_vp, _i64, _i32, _i32, _vp, _i32, _i32, _vp, _vp],
+    "hla_debug_mma_rate": [_i32, _i32, _i32, _i32, _i32, _vp, _vp],
+    "hla_debug_tmem_rate": [_i32, _i32, _i32, _i32, _vp, _vp],
+    "hla_debug_ex2_rate": [_i32, _i32, _vp, _vp, _vp],
+    "hla_debug_xu_rate": [_i32, _i32, _i32, _vp, _vp, _vp],
+    "hla_debug_sync_latency": [_i32, _i32, _vp, _vp],
+    "hla_debug_softmax_rate": [_i32, _i32, _vp, _vp, _vp],
+    "hla_debug_softmax_tile": [_i32, _i32, _vp, _vp, _vp],
+    "hla_debug_load_rate": [_vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _vp],
+}
 
 
-def lib():
-    global _lib
-    if _lib is not None:
-        return _lib
-    if not os.path.exists(LIB_PATH):
-        raise ImportError("libhla.so not built (%s); run __graft_entry__.build() -- there is no fallback" % LIB_PATH)
-    L = ctypes.CDLL(LIB_PATH)
-    vp, i32, i64, f32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_size_t
-    pdesc, pmask = ctypes.POINTER(PatternDesc), ctypes.POINTER(BlockMaskC)
-    sig = {
-        "hla_hilbert_index": [i32, i32, vp, vp, vp],
-        "hla_hilbert_perm": [i32, i32, i32, i32, i32, i32, ctypes.POINTER(vp), ctypes.POINTER(vp), vp, vp],
-        "hla_build_block_mask": [pdesc, pmask, ctypes.POINTER(i64), vp],
-        "hla_mask_ratios": [pdesc, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double),
-                            ctypes.POINTER(ctypes.c_double)],
-        "hla_attn_fwd": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp],
-        "hla_attn_bwd": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp,
-                         vp],
-        "hla_attn_bwd_preprocess": [i32, i32, i32, i32, f32, vp, vp, vp, vp, pmask, vp, sz, vp],
-        "hla_attn_bwd_main": [pdesc, pmask, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp],
-        "hla_attn_bwd_finalize": [i32, i32, i32, i32, vp, sz, vp, vp, pmask, vp],
-        "hla_build_bwd_plan": [pmask, vp],
-        "hla_debug_umma": [vp, vp, vp, i32, i32, i32, i32, i32, i32, vp],
-        "hla_debug_gather4": [vp, i64, i32, i32, vp, i32, i32, vp, vp],
-        "hla_debug_mma_rate": [i32, i32, i32, i32, i32, vp, vp],
-        "hla_debug_tmem_rate": [i32, i32, i32, i32, vp, vp],
-        "hla_debug_ex2_rate": [i32, i32, vp, vp, vp],
-        "hla_debug_xu_rate": [i32, i32, i32, vp, vp, vp],
-        "hla_debug_sync_latency": [i32, i32, vp, vp],
-        "hla_debug_softmax_rate": [i32, i32, vp, vp, vp],
-        "hla_debug_softmax_tile": [i32, i32, vp, vp, vp],
-        "hla_debug_load_rate": [vp, i64, i32, i32, i32, i32, i32, vp, vp],
-    }
+def _load(path, sig, what):
+    if not os.path.exists(path):
+        raise ImportError("%s not built (%s); run __graft_entry__.build() -- there is no fallback" % (what, path))
+    L = ctypes.CDLL(path)
     for name, args in sig.items():
-        if name.startswith("hla_debug_") and not hasattr(L, name):
-            continue   # bring-up probes are optional (e.g. an older dev build under HLA_LIB_NAME)
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = ctypes.c_int
-    L.hla_attn_bwd_workspace.argtypes = [i32, i32, i32, i32]
-    L.hla_attn_bwd_workspace.restype = sz
     L.hla_last_error.restype = ctypes.c_char_p
+    return L
+
+
+def lib():
+    """libhla.so: the hot path (include/hla.h)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    L = _load(LIB_PATH, _SIG, "libhla.so")
+    L.hla_attn_bwd_workspace.argtypes = [_i32, _i32, _i32, _i32]
+    L.hla_attn_bwd_workspace.restype = _sz
     L.hla_version.restype = ctypes.c_char_p
     _lib = L
     return L
 
 
-def check(name, status):
+def debug_lib():
+    """libhla_debug.so: bring-up / machine-constant probes (include/hla_debug.h); tests and tools only."""
+    global _debug_lib
+    if _debug_lib is None:
+        _debug_lib = _load(DEBUG_LIB_PATH, _DEBUG_SIG, "libhla_debug.so")
+    return _debug_lib
+
+
+def check(name, status, L=None):
     if status != HLA_OK:
-        raise HlaError(name, status, lib().hla_last_error().decode())
+        raise HlaError(name, status, (L or (debug_lib() if name.startswith("hla_debug_") else lib())).hla_last_error().decode())

@@ -25,8 +25,10 @@ KINDS = {
 }
 
 
-def _stream(stream=None):
-    s = stream if stream is not None else torch.cuda.current_stream()
+def _stream(stream=None, device=None):
+    """The launch stream: `stream`, else the current stream of `device` (the tensors' device,
+    not whichever device happens to be current)."""
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return ctypes.c_void_p(s.cuda_stream)
 
 
@@ -87,7 +89,9 @@ def hla_hilbert_index(grid_h, grid_w, device="cuda", stream=None):
     n = grid_h * grid_w
     s2c = torch.empty(n, dtype=torch.int32, device=device)
     c2s = torch.empty(n, dtype=torch.int32, device=device)
-    check("hla_hilbert_index", lib().hla_hilbert_index(grid_h, grid_w, _ptr(s2c), _ptr(c2s), _stream(stream)))
+    with torch.cuda.device(s2c.device):
+        check("hla_hilbert_index", lib().hla_hilbert_index(grid_h, grid_w, _ptr(s2c), _ptr(c2s),
+                                                           _stream(stream, s2c.device)))
     return s2c, c2s
 
 
@@ -104,8 +108,9 @@ def hla_hilbert_perm(grid_h, grid_w, direction, srcs, dsts=None, stream=None):
     n = len(srcs)
     src_arr = (ctypes.c_void_p * n)(*[s.data_ptr() for s in srcs])
     dst_arr = (ctypes.c_void_p * n)(*[d.data_ptr() for d in dsts])
-    check("hla_hilbert_perm", lib().hla_hilbert_perm(grid_h, grid_w, direction, B, row_bytes, n, src_arr, dst_arr,
-                                                     None, _stream(stream)))
+    with torch.cuda.device(srcs[0].device):
+        check("hla_hilbert_perm", lib().hla_hilbert_perm(grid_h, grid_w, direction, B, row_bytes, n, src_arr, dst_arr,
+                                                         None, _stream(stream, srcs[0].device)))
     return dsts
 
 
@@ -122,16 +127,19 @@ def hla_build_block_mask(desc, device="cuda", stream=None, plan=True):
     c = m.c
     c.col_idx = None
     nnz = ctypes.c_int64()
-    check("hla_build_block_mask", lib().hla_build_block_mask(ctypes.byref(desc), ctypes.byref(c), ctypes.byref(nnz),
-                                                             _stream(stream)))
+    dev = m.row_ptr.device
+    with torch.cuda.device(dev):
+        check("hla_build_block_mask", lib().hla_build_block_mask(ctypes.byref(desc), ctypes.byref(c),
+                                                                 ctypes.byref(nnz), _stream(stream, dev)))
     cap = max(1, nnz.value)
     m.col_idx = torch.empty(cap, **i32)
     m.kind = torch.empty(cap, dtype=torch.uint8, device=device)
     m.t_col_idx = torch.empty(cap, **i32)
     m.t_kind = torch.empty(cap, dtype=torch.uint8, device=device)
     c = m.c
-    check("hla_build_block_mask", lib().hla_build_block_mask(ctypes.byref(desc), ctypes.byref(c), ctypes.byref(nnz),
-                                                             _stream(stream)))
+    with torch.cuda.device(dev):
+        check("hla_build_block_mask", lib().hla_build_block_mask(ctypes.byref(desc), ctypes.byref(c),
+                                                                 ctypes.byref(nnz), _stream(stream, dev)))
     m.host_counts = tuple(int(x) for x in c.host_counts)   # written by the fill call
     if plan and desc.block_q == desc.block_k:
         hla_build_bwd_plan(m, stream)
@@ -144,7 +152,8 @@ def hla_build_bwd_plan(mask, stream=None):
     mask.t_dq = torch.zeros(max(1, mask.col_idx.numel()), dtype=torch.uint8, device=dev)
     mask.q_dq_local = torch.zeros(mask.row_ptr.numel() - 1, dtype=torch.uint8, device=dev)
     c = mask.c
-    check("hla_build_bwd_plan", lib().hla_build_bwd_plan(ctypes.byref(c), _stream(stream)))
+    with torch.cuda.device(dev):
+        check("hla_build_bwd_plan", lib().hla_build_bwd_plan(ctypes.byref(c), _stream(stream, dev)))
     mask.n_dq_nonlocal = int(c.n_dq_nonlocal)
     return mask
 
@@ -179,9 +188,10 @@ def hla_attn_fwd(desc, mask, q, k, v, scale=0.0, o=None, lse=None, tiles_visited
     if lse is None:
         lse = torch.empty(B, H, N, dtype=torch.float32, device=q.device)
     mc = mask.c
-    check("hla_attn_fwd", lib().hla_attn_fwd(ctypes.byref(desc), ctypes.byref(mc), B, H, D, float(scale),
-                                             _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(seq_to_cell),
-                                             _sm(mod), _ptr(tiles_visited), _stream(stream)))
+    with torch.cuda.device(q.device):
+        check("hla_attn_fwd", lib().hla_attn_fwd(ctypes.byref(desc), ctypes.byref(mc), B, H, D, float(scale),
+                                                 _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(seq_to_cell),
+                                                 _sm(mod), _ptr(tiles_visited), _stream(stream, q.device)))
     return o, lse
 
 
@@ -199,11 +209,12 @@ def hla_attn_bwd(desc, mask, q, k, v, o, lse, dout, scale=0.0, dq=None, dk=None,
     if workspace is None:
         workspace = torch.empty(nbytes, dtype=torch.uint8, device=q.device)
     mc = mask.c
-    check("hla_attn_bwd", lib().hla_attn_bwd(ctypes.byref(desc), ctypes.byref(mc), B, H, D, float(scale),
-                                             _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(dout),
-                                             _ptr(dq), _ptr(dk), _ptr(dv), _ptr(seq_to_cell), _sm(mod),
-                                             _ptr(workspace), workspace.numel(), _ptr(tiles_visited),
-                                             _stream(stream)))
+    with torch.cuda.device(q.device):
+        check("hla_attn_bwd", lib().hla_attn_bwd(ctypes.byref(desc), ctypes.byref(mc), B, H, D, float(scale),
+                                                 _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(dout),
+                                                 _ptr(dq), _ptr(dk), _ptr(dv), _ptr(seq_to_cell), _sm(mod),
+                                                 _ptr(workspace), workspace.numel(), _ptr(tiles_visited),
+                                                 _stream(stream, q.device)))
     return dq, dk, dv
 
 
@@ -214,10 +225,11 @@ def _pm(mask):
 def hla_attn_bwd_preprocess(o, dout, lse, workspace, scale=0.0, seq_to_cell=None, stream=None, mask=None):
     """mask: the mask whose dQ plan hla_attn_bwd_main will use (None = no plan)."""
     B, N, H, D = o.shape
-    check("hla_attn_bwd_preprocess", lib().hla_attn_bwd_preprocess(B, H, N, D, float(scale), _ptr(o), _ptr(dout),
-                                                                   _ptr(lse), _ptr(seq_to_cell), _pm(mask),
-                                                                   _ptr(workspace), workspace.numel(),
-                                                                   _stream(stream)))
+    with torch.cuda.device(o.device):
+        check("hla_attn_bwd_preprocess", lib().hla_attn_bwd_preprocess(B, H, N, D, float(scale), _ptr(o), _ptr(dout),
+                                                                       _ptr(lse), _ptr(seq_to_cell), _pm(mask),
+                                                                       _ptr(workspace), workspace.numel(),
+                                                                       _stream(stream, o.device)))
 
 
 def hla_attn_bwd_main(desc, mask, q, k, v, dout, dq, dk, dv, workspace, scale=0.0, tiles_visited=None,
@@ -228,24 +240,27 @@ def hla_attn_bwd_main(desc, mask, q, k, v, dout, dq, dk, dv, workspace, scale=0.
     into mod's drpb."""
     B, N, H, D = q.shape
     mc = mask.c
-    check("hla_attn_bwd_main", lib().hla_attn_bwd_main(ctypes.byref(desc), ctypes.byref(mc), B, H, D, float(scale),
-                                                       _ptr(q), _ptr(k), _ptr(v), _ptr(dout), _ptr(dq), _ptr(dk),
-                                                       _ptr(dv), _ptr(seq_to_cell), _sm(mod), _ptr(workspace),
-                                                       workspace.numel(), _ptr(tiles_visited), _stream(stream)))
+    with torch.cuda.device(q.device):
+        check("hla_attn_bwd_main", lib().hla_attn_bwd_main(ctypes.byref(desc), ctypes.byref(mc), B, H, D,
+                                                           float(scale), _ptr(q), _ptr(k), _ptr(v), _ptr(dout),
+                                                           _ptr(dq), _ptr(dk), _ptr(dv), _ptr(seq_to_cell), _sm(mod),
+                                                           _ptr(workspace), workspace.numel(), _ptr(tiles_visited),
+                                                           _stream(stream, q.device)))
 
 
 def hla_attn_bwd_finalize(workspace, dq, seq_to_cell=None, stream=None, mask=None):
     """mask: the mask whose dQ plan hla_attn_bwd_main used (None = no plan)."""
     B, N, H, D = dq.shape
-    check("hla_attn_bwd_finalize", lib().hla_attn_bwd_finalize(B, H, N, D, _ptr(workspace), workspace.numel(),
-                                                               _ptr(dq), _ptr(seq_to_cell), _pm(mask),
-                                                               _stream(stream)))
+    with torch.cuda.device(dq.device):
+        check("hla_attn_bwd_finalize", lib().hla_attn_bwd_finalize(B, H, N, D, _ptr(workspace), workspace.numel(),
+                                                                   _ptr(dq), _ptr(seq_to_cell), _pm(mask),
+                                                                   _stream(stream, dq.device)))
 
 
 def hla_debug_umma(A, B, M, N, K, a_mn=False, b_mn=False, a_tmem=False, stream=None):
     C = torch.empty(M, N, dtype=torch.float32, device=A.device)
-    check("hla_debug_umma", lib().hla_debug_umma(_ptr(A), _ptr(B), _ptr(C), M, N, K, int(a_mn), int(b_mn),
-                                                 int(a_tmem), _stream(stream)))
+    check("hla_debug_umma", _lib.debug_lib().hla_debug_umma(_ptr(A), _ptr(B), _ptr(C), M, N, K, int(a_mn),
+                                                            int(b_mn), int(a_tmem), _stream(stream, A.device)))
     return C
 
 
@@ -253,8 +268,8 @@ def hla_debug_gather4(src, idx, head, box_h=1, stream=None):
     """src: bf16 [rows, heads, d]; idx: int32[128] row indices -> bf16 [128, d] (TMA gather4 bring-up)."""
     rows, heads, d = src.shape
     out = torch.empty(128, d, dtype=torch.bfloat16, device=src.device)
-    check("hla_debug_gather4", lib().hla_debug_gather4(_ptr(src), rows, heads, d, _ptr(idx), head, box_h, _ptr(out),
-                                                       _stream(stream)))
+    check("hla_debug_gather4", _lib.debug_lib().hla_debug_gather4(_ptr(src), rows, heads, d, _ptr(idx), head, box_h,
+                                                                  _ptr(out), _stream(stream, src.device)))
     return out
 
 

@@ -25,9 +25,11 @@ whose whole kv list lies in one pair get their dQ written by the main backward k
 (no fp32 accumulator traffic, no finalize pass when that holds for all of them).
 
 rpb=True adds HWT's global relative position bias (reading R19): a table
-`self.rpb` fp32 [heads, 2H-1, 2W-1] (zero-initialised; set it as a parameter)
-whose gradient is written to `self.drpb` by backward() (one memset + the
-backward kernel's accumulation; launches_per_step counts the memset).
+`self.rpb` fp32 [heads, 2H-1, 2W-1] (zero-initialised) whose gradient is written to
+`self.drpb` by backward() (one memset + the backward kernel's accumulation;
+launches_per_step counts the memset).  The kernels hold raw pointers to these two
+buffers, so they keep their storage for the layer's lifetime: assigning `layer.rpb = t`
+copies t into the table (in place), and `drpb` is read-only.
 """
 
 import torch
@@ -60,16 +62,32 @@ class HilbertLocalAttention:
             self.qs, self.ks, self.vs, self.os = e(), e(), e(), e()
             self.dos, self.dqs, self.dks, self.dvs = e(), e(), e(), e()
         self._saved = None
-        self.rpb = self.drpb = self.mod = None
+        self._rpb = self._drpb = self.mod = None
         if rpb:
             shape = (heads, 2 * grid_h - 1, 2 * grid_w - 1)
-            self.rpb = torch.zeros(shape, dtype=torch.float32, device=device)
-            self.drpb = torch.zeros(shape, dtype=torch.float32, device=device)
+            self._rpb = torch.zeros(shape, dtype=torch.float32, device=device)
+            self._drpb = torch.zeros(shape, dtype=torch.float32, device=device)
             cells = None
             if self.hilbert:     # 2D offsets need the sequence -> cell map of the order
                 cells = self.s2c if self.s2c is not None else api.hla_hilbert_index(grid_h, grid_w, device)[0]
             self._cells = cells
-            self.mod = api.score_mod(self.rpb, self.drpb, cells)
+            self.mod = api.score_mod(self._rpb, self._drpb, cells)
+
+    @property
+    def rpb(self):
+        """The global-RPB table (None without rpb=True); its storage is fixed for the layer."""
+        return self._rpb
+
+    @rpb.setter
+    def rpb(self, value):
+        if self._rpb is None:
+            raise AttributeError("layer built without rpb=True")
+        self._rpb.copy_(value)   # in place: the kernels hold this buffer's pointer
+
+    @property
+    def drpb(self):
+        """Gradient of the RPB table written by backward() (read-only binding)."""
+        return self._drpb
 
     # tiles executed per step, per (b, h): R (P:L102 r_i summed over q-blocks)
     @property
@@ -113,8 +131,8 @@ class HilbertLocalAttention:
             dout_s, dq, dk, dv = dout, self.dq, self.dk, self.dv
         api.hla_attn_bwd_preprocess(o, dout_s, self.lse, self.workspace, self.scale, seq_to_cell=self.s2c,
                                     mask=self.mask)
-        if self.drpb is not None:
-            self.drpb.zero_()      # the kernel accumulates the table gradient
+        if self._drpb is not None:
+            self._drpb.zero_()     # the kernel accumulates the table gradient
         mark("bwd_pre")
         api.hla_attn_bwd_main(self.desc, self.mask, q, k, v, dout_s, dq, dk, dv, self.workspace, self.scale,
                               seq_to_cell=self.s2c, mod=self.mod)
@@ -131,7 +149,7 @@ class HilbertLocalAttention:
     @property
     def launches_per_step(self):
         fin = 0 if self.mask.n_dq_nonlocal == 0 else 1   # the finalize launches nothing when every dQ is local
-        return 3 + fin + (4 if (self.hilbert and not self.fused) else 0) + (1 if self.rpb is not None else 0)
+        return 3 + fin + (4 if (self.hilbert and not self.fused) else 0) + (1 if self._rpb is not None else 0)
 
     def step(self, q, k, v, dout, mark=None):
         """One pass of the whole hot path: forward then backward."""

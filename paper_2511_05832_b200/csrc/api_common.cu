@@ -58,7 +58,11 @@ hla_status make_pattern(const hla_pattern_desc* d, Pattern* p) {
         p->kind = K_HNA;
         return HLA_OK;
       case HLA_SHIFTED_WINDOW:
-        HLA_REQUIRE(d->shift >= 0 && d->shift < n, HLA_ERR_INVALID, "shift %d outside [0, n)", d->shift);
+        // windows of n tokens on a grid the 2D window divides (as HWA); the shift moves them
+        // by 0 < shift < n tokens (shift 0 would be HWA itself)
+        HLA_REQUIRE(d->grid_h % d->win_h == 0 && d->grid_w % d->win_w == 0, HLA_ERR_INVALID,
+                    "window %dx%d does not divide grid %dx%d", d->win_h, d->win_w, d->grid_h, d->grid_w);
+        HLA_REQUIRE(d->shift > 0 && d->shift < n, HLA_ERR_INVALID, "shift %d outside (0, n)", d->shift);
         p->shift = d->shift;
         p->kind = K_HSWA;
         return HLA_OK;

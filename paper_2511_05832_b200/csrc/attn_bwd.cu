@@ -1044,13 +1044,22 @@ extern "C" hla_status hla_attn_bwd_preprocess(int32_t batch, int32_t heads, int3
   return HLA_OK;
 }
 
-extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch,
-                                        int32_t heads, int32_t head_dim, float scale, const void* q, const void* k,
-                                        const void* v, const void* dout, void* dq, void* dk, void* dv,
-                                        const int32_t* seq_to_cell, const hla_score_mod* score_mod,
-                                        void* workspace, size_t workspace_bytes, int64_t* tiles_visited,
-                                        cudaStream_t stream) {
-  clear_error();
+namespace {
+
+// Everything hla_attn_bwd_main launches with: validated arguments, kernel parameters, tensor
+// maps and the schedule.  Built (and every argument checked) before anything is launched.
+struct MainPlan {
+  bwd::BwdParams prm;
+  CUtensorMap mq, mk, mv, mdo, mdq;
+  int32_t head_dim, mkb;
+  bool gather, two_d, full;
+};
+
+hla_status prepare_main(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
+                        int32_t head_dim, float scale, const void* q, const void* k, const void* v,
+                        const void* dout, void* dq, void* dk, void* dv, const int32_t* seq_to_cell,
+                        const hla_score_mod* score_mod, void* workspace, size_t workspace_bytes,
+                        int64_t* tiles_visited, MainPlan* pl) {
   Pattern pat;
   hla_status st = check_attn_args(d, m, batch, heads, head_dim, &pat);
   if (st != HLA_OK) return st;
@@ -1064,7 +1073,7 @@ extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_blo
   st = carve_workspace(batch, heads, pat.N, head_dim, workspace, workspace_bytes, &dq_acc, &dsum, &lse2);
   if (st != HLA_OK) return st;
   const float sc = scale > 0.f ? scale : 1.0f / sqrtf((float)head_dim);
-  bwd::BwdParams prm;
+  bwd::BwdParams& prm = pl->prm;
   prm.pat = pat;
   prm.N = pat.N;
   prm.heads = heads;
@@ -1089,29 +1098,54 @@ extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_blo
   prm.rpb_w = 2 * pat.W - 1;
   prm.rpb_hw = (2 * pat.H - 1) * prm.rpb_w;
   prm.inv_scale = 1.f / sc;
-  const bool gather = seq_to_cell != nullptr;
-  HLA_REQUIRE(!gather || d->order == HLA_ORDER_HILBERT, HLA_ERR_INVALID,
+  pl->gather = seq_to_cell != nullptr;
+  HLA_REQUIRE(!pl->gather || d->order == HLA_ORDER_HILBERT, HLA_ERR_INVALID,
               "seq_to_cell (fused reorder) is only meaningful for Hilbert-order patterns");
-  HLA_REQUIRE(!gather || ((uintptr_t)seq_to_cell & 15) == 0, HLA_ERR_INVALID, "seq_to_cell must be 16-byte aligned");
+  HLA_REQUIRE(!pl->gather || ((uintptr_t)seq_to_cell & 15) == 0, HLA_ERR_INVALID,
+              "seq_to_cell must be 16-byte aligned");
   const int64_t tok = (int64_t)batch * pat.N;
-  CUtensorMap mq, mk, mv, mdo;
   auto mk_map = [&](CUtensorMap* mp, const void* base) {
-    return gather ? make_gather_map(mp, base, tok, heads, head_dim) : make_rows_map(mp, base, tok, heads, head_dim, kBlock);
+    return pl->gather ? make_gather_map(mp, base, tok, heads, head_dim)
+                      : make_rows_map(mp, base, tok, heads, head_dim, kBlock);
   };
-  if ((st = mk_map(&mq, q)) != HLA_OK) return st;
-  if ((st = mk_map(&mk, k)) != HLA_OK) return st;
-  if ((st = mk_map(&mv, v)) != HLA_OK) return st;
-  if ((st = mk_map(&mdo, dout)) != HLA_OK) return st;
-  CUtensorMap mdq;   // fp32 dQ accumulator, sequence order, 32-float (128 B) boxes for the TMA reduce-add
-  if ((st = make_f32_rows_map(&mdq, dq_acc, tok, heads, head_dim, 32, kBlock)) != HLA_OK) return st;
-  const bool two_d = pat.kind == K_WSA || pat.kind == K_SA || pat.kind == K_NA2D;
-  const int32_t mkb = (pat.N + kBlock - 1) / kBlock;
+  if ((st = mk_map(&pl->mq, q)) != HLA_OK) return st;
+  if ((st = mk_map(&pl->mk, k)) != HLA_OK) return st;
+  if ((st = mk_map(&pl->mv, v)) != HLA_OK) return st;
+  if ((st = mk_map(&pl->mdo, dout)) != HLA_OK) return st;
+  // fp32 dQ accumulator, sequence order, 32-float (128 B) boxes for the TMA reduce-add
+  if ((st = make_f32_rows_map(&pl->mdq, dq_acc, tok, heads, head_dim, 32, kBlock)) != HLA_OK) return st;
+  pl->two_d = pat.kind == K_WSA || pat.kind == K_SA || pat.kind == K_NA2D;
+  pl->mkb = (pat.N + kBlock - 1) / kBlock;
+  pl->head_dim = head_dim;
   // schedule: full-tile (attn_bwd_full_kernel) when full tiles are at least half of the
   // mask's tiles or with the RPB score_mod; half-tile (attn_bwd_split_kernel) otherwise
   // (the split schedule overlaps the partial tiles' masked compute better)
-  const bool full = prm.rpb != nullptr || m->host_counts[1] >= m->host_counts[2];
-  if (full) return bwd::launch_full(prm.rpb != nullptr, head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, mkb, stream);
-  return bwd::launch_split(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, mkb, stream);
+  pl->full = prm.rpb != nullptr || m->host_counts[1] >= m->host_counts[2];
+  return HLA_OK;
+}
+
+hla_status launch_main(const MainPlan& pl, cudaStream_t stream) {
+  if (pl.full)
+    return bwd::launch_full(pl.prm.rpb != nullptr, pl.head_dim, pl.gather, pl.two_d, pl.mq, pl.mk, pl.mv, pl.mdo,
+                            pl.mdq, pl.prm, pl.mkb, stream);
+  return bwd::launch_split(pl.head_dim, pl.gather, pl.two_d, pl.mq, pl.mk, pl.mv, pl.mdo, pl.mdq, pl.prm, pl.mkb,
+                           stream);
+}
+
+}  // namespace
+
+extern "C" hla_status hla_attn_bwd_main(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch,
+                                        int32_t heads, int32_t head_dim, float scale, const void* q, const void* k,
+                                        const void* v, const void* dout, void* dq, void* dk, void* dv,
+                                        const int32_t* seq_to_cell, const hla_score_mod* score_mod,
+                                        void* workspace, size_t workspace_bytes, int64_t* tiles_visited,
+                                        cudaStream_t stream) {
+  clear_error();
+  MainPlan pl;
+  const hla_status st = prepare_main(d, m, batch, heads, head_dim, scale, q, k, v, dout, dq, dk, dv, seq_to_cell,
+                                     score_mod, workspace, workspace_bytes, tiles_visited, &pl);
+  if (st != HLA_OK) return st;
+  return launch_main(pl, stream);
 }
 
 extern "C" hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_t n, int32_t head_dim,
@@ -1143,27 +1177,23 @@ extern "C" hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_ma
                                    const int32_t* seq_to_cell, const hla_score_mod* score_mod, void* workspace,
                                    size_t workspace_bytes, int64_t* tiles_visited, cudaStream_t stream) {
   clear_error();
-  Pattern pat;
-  hla_status st = check_attn_args(d, m, batch, heads, head_dim, &pat);
+  // validate every stage's arguments (and build the main kernel's tensor maps) before
+  // launching anything: a rejected call leaves drpb and the workspace untouched
+  MainPlan pl;
+  hla_status st = prepare_main(d, m, batch, heads, head_dim, scale, q, k, v, dout, dq, dk, dv, seq_to_cell,
+                               score_mod, workspace, workspace_bytes, tiles_visited, &pl);
   if (st != HLA_OK) return st;
-  HLA_REQUIRE(o && dq, HLA_ERR_INVALID, "null pointer");
-  // validate everything before launching anything
-  float *dq_acc, *dsum;
-  st = carve_workspace(batch, heads, pat.N, head_dim, workspace, workspace_bytes, &dq_acc, &dsum);
-  if (st != HLA_OK) return st;
+  HLA_REQUIRE(o && dq && lse, HLA_ERR_INVALID, "null pointer");
   HLA_REQUIRE(((uintptr_t)o | (uintptr_t)dq) % 16 == 0, HLA_ERR_INVALID, "tensors must be 16-byte aligned");
-  const float* rpb;
-  float* drpb;
-  const int32_t* cells;
-  if ((st = parse_score_mod(d, score_mod, true, &rpb, &drpb, &cells)) != HLA_OK) return st;
-  if (drpb)   // the table gradient is accumulated: start from zero
-    HLA_CUDA_TRY(cudaMemsetAsync(drpb, 0, sizeof(float) * heads * (2 * pat.H - 1) * (2 * pat.W - 1), stream));
-  if ((st = hla_attn_bwd_preprocess(batch, heads, pat.N, head_dim, scale, o, dout, lse, seq_to_cell, m, workspace,
+  HLA_REQUIRE((int64_t)batch * pl.prm.N * heads * head_dim / 8 < (1ll << 31), HLA_ERR_UNSUPPORTED,
+              "B * N * heads * head_dim too large");
+  if (pl.prm.drpb)   // the table gradient is accumulated: start from zero
+    HLA_CUDA_TRY(cudaMemsetAsync(pl.prm.drpb, 0,
+                                 sizeof(float) * heads * (2 * pl.prm.grid_h - 1) * (2 * pl.prm.grid_w - 1), stream));
+  if ((st = hla_attn_bwd_preprocess(batch, heads, pl.prm.N, head_dim, scale, o, dout, lse, seq_to_cell, m, workspace,
                                     workspace_bytes, stream)) != HLA_OK)
     return st;
-  if ((st = hla_attn_bwd_main(d, m, batch, heads, head_dim, scale, q, k, v, dout, dq, dk, dv, seq_to_cell,
-                              score_mod, workspace, workspace_bytes, tiles_visited, stream)) != HLA_OK)
-    return st;
-  return hla_attn_bwd_finalize(batch, heads, pat.N, head_dim, workspace, workspace_bytes, dq, seq_to_cell, m,
+  if ((st = launch_main(pl, stream)) != HLA_OK) return st;
+  return hla_attn_bwd_finalize(batch, heads, pl.prm.N, head_dim, workspace, workspace_bytes, dq, seq_to_cell, m,
                                stream);
 }

@@ -506,7 +506,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         uint32_t pk[64];
 #pragma unroll
         for (int e = 0; e < 64; ++e) {
-          // MUFU for one half of the exponentials, the FMA pipe for the other (FA4's split)
+          // all exponentials on the MUFU pipe: a polynomial exp2 on the FMA pipe for part of
+          // them (FA4's split) measured slower here
           const float p0 = sm100::ex2(fmaf(s[2 * e], sl2e, -m_use));
           const float p1 = sm100::ex2(fmaf(s[2 * e + 1], sl2e, -m_use));
           l4[e & 3] += p0 + p1;

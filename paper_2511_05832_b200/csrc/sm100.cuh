@@ -323,19 +323,6 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x for x <= 0 on the FMA / ALU pipes (no MUFU): x = j + f, j = rint(x), |f| <= 1/2,
-// 2^f by its degree-4 Taylor polynomial (relative error < 5e-5, far below the bf16
-// rounding of P), j added to the exponent field; x is clamped at -126 (result < 2^-125).
-__device__ __forceinline__ float ex2_poly(float x) {
-  const float xc = fmaxf(x, -126.f);
-  const float t = xc + 12582912.f;   // 1.5 * 2^23: rint(xc) lands in the low mantissa bits
-  const float f = xc - (t - 12582912.f);
-  float p = fmaf(f, 0.0096181291f, 0.0555041087f);
-  p = fmaf(p, f, 0.2402265070f);
-  p = fmaf(p, f, 0.6931471806f);
-  p = fmaf(p, f, 1.0f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));

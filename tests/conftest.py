@@ -19,9 +19,13 @@ def golden_dir():
 
 
 def pytest_sessionstart(session):
-    # libhla.so is a build artefact (git-ignored); build it if this checkout has none.
-    lib = os.path.join(ROOT, "paper_2511_05832_b200", "libhla.so")
-    if not os.path.exists(lib):
-        import subprocess
-        subprocess.run(["make", "-C", os.path.join(ROOT, "paper_2511_05832_b200", "csrc"), "-j8"], check=True,
-                       stdout=subprocess.DEVNULL)
+    # libhla.so / libhla_debug.so are build artefacts (git-ignored); build them if this checkout
+    # has none and nvcc is available.  Without nvcc the tests that need the libraries fail
+    # with the loader's "not built" error (there is no fallback); the oracle tests still run.
+    import shutil
+    import subprocess
+    pkg = os.path.join(ROOT, "paper_2511_05832_b200")
+    libs = [os.path.join(pkg, n) for n in ("libhla.so", "libhla_debug.so")]
+    if all(os.path.exists(p) for p in libs) or shutil.which("nvcc") is None:
+        return
+    subprocess.run(["make", "-C", os.path.join(pkg, "csrc"), "-j8"], check=True, stdout=subprocess.DEVNULL)

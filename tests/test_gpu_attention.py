@@ -304,3 +304,44 @@ def test_dq_plan_matches_no_plan(kind, g, w, B, H, d, fused):
     assert torch.equal(r1[0], r2[0])
     assert torch.equal(r1[2], r2[2]) and torch.equal(r1[3], r2[3])
     assert (r1[1].float() - r2[1].float()).abs().max().item() <= 2e-3
+
+
+def test_rpb_gradient_small_upstream_gradient():
+    """the table gradient sums dL/dscore over many pairs; with a mean-reduced loss
+    dO is ~1e-6 and every per-pair term is tiny.  The per-tile power-of-two fixed-point scale
+    keeps the relative accuracy independent of that magnitude (reading R20's bound)."""
+    kind, g, w, B, H, d = "HWA", 32, 8, 2, 2, 64
+    N = g * g
+    q, k, v, do = _inputs(B, N, H, d, seed=23)
+    do = (do.float() * 1e-6).to(torch.bfloat16)
+    layer = hla.HilbertLocalAttention(kind, g, g, w, w, B, H, d, device=DEV, rpb=True)
+    table = torch.rand(layer.rpb.shape, generator=torch.Generator().manual_seed(6), dtype=torch.float64)
+    layer.rpb = (2 * table - 1).float()
+    layer.forward(q, k, v)
+    layer.backward(do)
+    torch.cuda.synchronize()
+    spec = Spec(kind, g, g, w, w)
+    s2c = hilbert.hilbert_order(g, g)[0]
+    seq = lambda t: hilbert.to_sequence(to_np(t), s2c)   # noqa: E731
+    T = layer.rpb.double().cpu().numpy()
+    _, _, _, dT_ref = oatt.attn_bwd(seq(q), seq(k), seq(v), seq(do), spec, rpb=T)
+    dT = layer.drpb.double().cpu().numpy()
+    assert np.abs(dT_ref).max() < 1e-4          # the regime of the finding
+    rel = np.linalg.norm(dT - dT_ref) / np.linalg.norm(dT_ref)
+    assert rel <= 2e-2, rel
+
+
+def test_bwd_rejects_before_launching():
+    """hla.h: on a non-OK status nothing has been launched -- hla_attn_bwd validates every
+    stage (a missing O here) before it zeroes drpb or runs the preprocess."""
+    g, w, B, H, d = 32, 8, 1, 2, 64
+    q, k, v, do = _inputs(B, g * g, H, d, seed=24)
+    layer = hla.HilbertLocalAttention("HWA", g, g, w, w, B, H, d, device=DEV, rpb=True)
+    o, lse = layer.forward(q, k, v), layer.lse
+    layer.drpb.fill_(7.0)
+    ws = torch.full((hla.hla_attn_bwd_workspace(B, H, g * g, d),), 0x5A, dtype=torch.uint8, device=DEV)
+    with pytest.raises(hla.HlaError):
+        hla.hla_attn_bwd(layer.desc, layer.mask, q, k, v, None, lse, do, workspace=ws, seq_to_cell=layer.s2c,
+                         mod=layer.mod)
+    torch.cuda.synchronize()
+    assert bool((layer.drpb == 7.0).all()) and bool((ws == 0x5A).all())

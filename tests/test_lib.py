@@ -17,23 +17,29 @@ from oracle.patterns import Spec
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _declared_symbols():
-    names = set()
-    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
-        src = open(h).read()
-        names.update(re.findall(r"HLA_API\s+[\w\s\*]+?\b(hla_\w+)\s*\(", src))
-    return names
+def _declared_symbols(header):
+    src = open(os.path.join(ROOT, "include", header)).read()
+    return set(re.findall(r"HLA_API\s+[\w\s\*]+?\b(hla_\w+)\s*\(", src))
 
 
 def test_library_exports_header_symbols():
+    """libhla.so exports exactly include/hla.h (the hot path); the bring-up probes of
+    include/hla_debug.h live in libhla_debug.so, not in the product library."""
     from paper_2511_05832_b200 import _lib
     L = _lib.lib()
-    declared = _declared_symbols()
+    declared = _declared_symbols("hla.h")
     assert len(declared) >= 10
     for name in declared:
         assert hasattr(L, name), name
     assert set(_lib.EXPORTED) == declared
+    for name in _declared_symbols("hla_debug.h"):
+        assert not hasattr(L, name), name
     assert "sm_100a" in L.hla_version().decode()
+    D = _lib.debug_lib()
+    dbg = _declared_symbols("hla_debug.h")
+    assert set(_lib.DEBUG_EXPORTED) == dbg and len(dbg) >= 5
+    for name in dbg:
+        assert hasattr(D, name), name
 
 
 def test_argument_validation_without_gpu():

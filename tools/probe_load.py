@@ -3,7 +3,7 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2511_05832_b200 import _lib
-lib = _lib.lib()
+lib = _lib.debug_lib()
 rows, heads = 16 * 4096, 8
 src = torch.randn(rows, heads, 64, device="cuda").to(torch.bfloat16)
 ctas = torch.cuda.get_device_properties(0).multi_processor_count

@@ -1,7 +1,7 @@
 import os, sys, torch, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2511_05832_b200 import _lib
-L = _lib.lib()
+L = _lib.debug_lib()
 out = torch.zeros(1, dtype=torch.int64, device="cuda")
 for N in (64, 128, 256):
     for a_mn, b_mn, a_tm in ((0, 0, 0), (0, 0, 2), (1, 1, 2), (0, 1, 1), (0, 1, 3)):

@@ -1,7 +1,7 @@
 import os, sys, torch, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2511_05832_b200 import _lib
-L = _lib.lib()
+L = _lib.debug_lib()
 out = torch.zeros(1024, dtype=torch.int64, device="cuda"); sink = torch.zeros(1, dtype=torch.int32, device="cuda")
 for blocks in (1, 148, 296, 592):
     r = []

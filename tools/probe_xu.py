@@ -2,7 +2,7 @@
 import os, sys, torch, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2511_05832_b200 import _lib
-L = _lib.lib()
+L = _lib.debug_lib()
 out = torch.zeros(1, dtype=torch.int64, device="cuda"); sink = torch.zeros(1, dtype=torch.int32, device="cuda")
 names = {0: "ex2.f32", 1: "ex2.bf16x2", 2: "ex2.f16x2", 3: "cvt.bf16x2.f32",
          4: "softmax pair (2 ex2.f32 + cvt)", 5: "softmax pair (ex2.bf16x2, ALU pack)", 6: "softmax pair (ex2.bf16x2, cvt pack)"}
