@@ -17,7 +17,7 @@ import paper_2511_05832_b200 as hla
 from oracle import attention as oatt
 from oracle import hilbert
 from oracle.patterns import Spec
-from parity import LSE_MAX_ABS, assert_close, to_np
+from parity import LSE_MAX_ABS, assert_close, emulated_slice, to_np
 
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
@@ -136,13 +136,26 @@ def test_bwd_small(case, sharp):
     torch.cuda.synchronize()
     spec = Spec(kind, gh, gw, wh, ww, shift=shift)
     dQ, dK, dV = oatt.attn_bwd(to_np(q), to_np(k), to_np(v), to_np(do), spec)
-    for name, got, ref in (("dQ", dq, dQ), ("dK", dk, dK), ("dV", dv, dV)):
-        # DESIGN.md reading R16: the north_star bound is absolute for the workload
-        # recipe (unit-variance inputs).  The sharp stress input (Q x 4) scales the
-        # gradients up to ~5x; its bound scales with the reference RMS relative to
-        # the nominal gradient RMS (0.25), i.e. the same relative accuracy.
-        f = max(1.0, float(np.sqrt((ref ** 2).mean())) / 0.25) if sharp else 1.0
-        assert_close(name, to_np(got), ref, max_abs=2e-2 * f, mean_abs=2e-3 * f)
+    if not sharp:
+        for name, got, ref in (("dQ", dq, dQ), ("dK", dk, dK), ("dV", dv, dV)):
+            assert_close(name, to_np(got), ref)            # the north_star bound
+    else:
+        # DESIGN.md reading R16: the north_star bound is absolute for the workload recipe
+        # (unit-variance inputs).  The sharp stress input (Q x 4, outside the paper's
+        # workloads) scales the gradients up to ~5x; its bound is the error of the bf16
+        # rounding model (tests/parity.py emulated_slice: fp64 with the kernels' rounding
+        # points) against the same fp64 oracle, times 1.25.
+        emu = {n: np.zeros_like(r) for n, r in (("dQ", dQ), ("dK", dK), ("dV", dV))}
+        s2c = np.arange(N)
+        for b in range(B):
+            for h in range(H):
+                _, eq, ek, ev = emulated_slice(*(to_np(t[b, :, h]) for t in (q, k, v, do)), spec)
+                emu["dQ"][b, :, h], emu["dK"][b, :, h], emu["dV"][b, :, h] = eq, ek, ev
+        for name, got, ref in (("dQ", dq, dQ), ("dK", dk, dK), ("dV", dv, dV)):
+            e_gpu = np.abs(to_np(got) - ref)
+            e_emu = np.abs(emu[name] - ref)
+            assert e_gpu.max() <= 1.25 * e_emu.max() + 1e-3, (name, e_gpu.max(), e_emu.max())
+            assert e_gpu.mean() <= 1.25 * e_emu.mean() + 1e-4, (name, e_gpu.mean(), e_emu.mean())
     assert int(visited.item()) == B * H * m.nnz
 
 
@@ -345,3 +358,39 @@ def test_bwd_rejects_before_launching():
                          mod=layer.mod)
     torch.cuda.synchronize()
     assert bool((layer.drpb == 7.0).all()) and bool((ws == 0x5A).all())
+
+
+# the HWT-T stack bench.py times as cfg5-hwt (bench.py STACK): grid, heads, window side
+CFG5_HWT = [(56, 3, 7), (28, 6, 7), (14, 12, 7), (8, 24, 8)]
+
+
+@pytest.mark.parametrize("kind", ["HWA", "HSWA"])
+@pytest.mark.parametrize("g,H,w", CFG5_HWT, ids=lambda v: str(v))
+def test_cfg5_hwt_layer_as_timed(g, H, w, kind):
+    """Every layer shape of the timed HWT stack (generalized Hilbert curve, ragged N, 49-token
+    windows, HWA / HSWA with shift = half a window, global RPB, d32) at B = 2 through the layer
+    API exactly as bench.py runs it: O, dQ, dK, dV of every (b, h) slice under the north_star
+    bound, the RPB table gradient under reading R20's relative bound."""
+    B, d = 2, 32
+    N = g * g
+    shift = (w * w) // 2 if kind == "HSWA" else 0
+    q, k, v, do = _inputs(B, N, H, d, seed=31)
+    layer = hla.HilbertLocalAttention(kind, g, g, w, w, B, H, d, shift=shift, device=DEV, rpb=True)
+    table = torch.rand(layer.rpb.shape, generator=torch.Generator().manual_seed(g), dtype=torch.float64)
+    layer.rpb = (2 * table - 1).float()
+    o = layer.forward(q, k, v).clone()
+    dq, dk, dv = (t.clone() for t in layer.backward(do))
+    torch.cuda.synchronize()
+    spec = Spec(kind, g, g, w, w, shift=shift)
+    s2c = hilbert.hilbert_order(g, g)[0]
+    T = layer.rpb.double().cpu().numpy()
+    dT_ref = np.zeros_like(T)
+    for b in range(B):
+        for h in range(H):
+            Q, K, V, DO = (to_np(t[b, :, h])[s2c] for t in (q, k, v, do))
+            dQ, dK, dV, O, _, dTh = oatt.attn_bwd_slice(Q, K, V, DO, spec, rpb=T[h])
+            dT_ref[h] += dTh
+            for name, got, ref in (("O", o, O), ("dQ", dq, dQ), ("dK", dk, dK), ("dV", dv, dV)):
+                assert_close("cfg5-hwt %s g%d b%d h%d %s" % (kind, g, b, h, name), to_np(got[b, :, h])[s2c], ref)
+    dT = layer.drpb.double().cpu().numpy()
+    assert np.linalg.norm(dT - dT_ref) / np.linalg.norm(dT_ref) <= 2e-2
