@@ -1,22 +1,28 @@
 #!/usr/bin/env python
 """bench.py -- Hilbert-guided local attention hot path on B200 (driver contract).
 
-One STEP = one pass of the whole hot path over one batch, grid-order
+One STEP = one pass of the whole hot path over one global batch, grid-order
 tensors in and out, through the public HilbertLocalAttention API:
   block-sparse fwd (Hilbert gather of Q,K,V + scatter of O fused into the kernel) ;
   bwd preprocess (D, LSE2; gather of O,dO) ; block-sparse bwd (gathers, scatter of
   dK,dV) ; dQ finalize (+ inverse reorder)
-(with HilbertLocalAttention(fused=False) the reorder runs as separate
-hla_hilbert_perm passes instead, the paper's "Reshape" step).
-The block mask and the Hilbert path are built once per shape, before timing
-(the paper caches them).  Workload (N=1): BASELINE.json configs[1]
-("cfg2": 64x64 grid, 8 heads, head_dim 64, HWA 256 tokens vs row-major 16x16
-windows, block 128), batch 16 (the paper's batch).
+(HilbertLocalAttention(fused=False) runs the reorder as separate hla_hilbert_perm passes
+instead, the paper's "Reshape" step; that variant is timed too, for perm_ms).
+The block mask and the Hilbert path are built once per shape, before timing (the paper
+caches them); their build time is reported separately (mask_build_ms).
+Workload (N=1): BASELINE.json configs[1] ("cfg2": 64x64 grid, 8 heads, head_dim 64, HWA
+256 tokens vs row-major 16x16 windows, block 128), batch 16 (the paper's batch).
 
-metric "fwd+bwd ms ...": value = step time per batch of work for the whole job
-= (max-over-ranks device time of one step) / (batches processed per step by all
-ranks).  Each rank processes its own batch (weak scaling, no collective on the
-hot path; NCCL only for the barrier and the max-reduction of timings).
+Multi-GPU (north_star "partitioned across the 8xB200 box by batch x head"):
+STRONG scaling at the fixed global batch.  plan_shards() gives every rank a contiguous
+block of (batch, head) units -- B/g whole batches, or head groups of one batch when B < g;
+the units are independent (no exchange step), so there is no collective on the hot path.
+NCCL carries only the barrier, the max-reduction of step times and, after the timed loop,
+the all_gather of per-rank statistics (times, units, backward-invariant residuals).
+value = max-over-ranks device time of one step of the whole global batch.
+
+`python bench.py --gpus N` outside torchrun re-executes itself under
+torch.distributed.run with N ranks; under torchrun WORLD_SIZE must equal --gpus.
 
 Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
 """
@@ -25,10 +31,10 @@ import argparse
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
-import tempfile
 import threading
 import time
 
@@ -47,42 +53,91 @@ CONFIGS = {
     "cfg4": dict(kind="HNA", rm="NA2D", grid=128, win=7, B=16, H=12, d=64,
                  text="128x128 grid, HNA 49 tokens vs NA2D 7x7, 12 heads, d64, block 128, batch 16"),
 }
-# cfg5: the HWT-T attention stack (SURVEY 8 cfg5 + 8(f) NEXT-1): Swin-T-like stages on the paper's
-# feature-map sizes (generalized Hilbert path, ragged N), HWA / HSWA blocks alternating (HWT
-# blocks come in pairs), each with HWT's global RPB, 7x7 = 49-token windows
-STACK = {"cfg5": dict(B=128, d=32, stages=[(56, 3, 2, 7), (28, 6, 2, 7), (14, 12, 6, 7), (8, 24, 2, 8)],
-                      text="HWT-T attention stack: stages 56x56/28x28/14x14/7x7->8x8 padded (N % 4 == 0 kernel "
-                           "limit) (generalized Hilbert, ragged N), "
-                           "heads 3/6/12/24, depths 2/2/6/2, B128, d32, 49-token windows (64 at the padded 8x8 stage), "
-                           "HWA/HSWA alternating (shift = half a window), global RPB, block 128")}
+# attention stacks of a Hilbert Window Transformer (HWT-T: Swin-T stage shapes)
+#   cfg5     BASELINE.json configs[4] as stated: 56/28/14/7 grids padded to the Hilbert grid
+#            64/32/16/8, window 49 -> 64 tokens (8 x 8), heads 3/6/12/24, batch 128, all HWA
+#            (MVP), depths 2/2/6/2, d32
+#   cfg5-hwt the HWT-T stack itself: unpadded 56/28/14 grids on the
+#            generalized Hilbert curve (ragged N; 7x7 -> 8x8 padded: the kernels need N % 4 == 0),
+#            49-token windows, HWA / HSWA alternating (shift = half a window), global RPB
+STACK = {
+    "cfg5": dict(B=128, d=32, block=128, hswa=False, rpb=False,
+                 stages=[(64, 3, 2, 8), (32, 6, 2, 8), (16, 12, 6, 8), (8, 24, 2, 8)],
+                 text="HWT-T attention stack as BASELINE states it: 56x56/28x28/14x14/7x7 padded to "
+                      "64x64/32x32/16x16/8x8 Hilbert grids, windows 49->64 tokens (8x8), heads 3/6/12/24, "
+                      "depths 2/2/6/2, all HWA, B128, d32, block 128"),
+    "cfg5-hwt": dict(B=128, d=32, block=128, hswa=True, rpb=True,
+                     stages=[(56, 3, 2, 7), (28, 6, 2, 7), (14, 12, 6, 7), (8, 24, 2, 8)],
+                     text="HWT-T attention stack: stages 56x56/28x28/14x14 (generalized Hilbert, ragged N) "
+                          "and 7x7->8x8 padded, heads 3/6/12/24, depths 2/2/6/2, B128, d32, 49-token windows "
+                          "(64 at 8x8), HWA/HSWA alternating (shift = half a window), global RPB, block 128"),
+}
 # paper's row-major-block-sparse -> Hilbert fwd+bwd speedup on the nearest shape (RTX 3080)
 PAPER_SPEEDUP = {"cfg2": (2.70, "WSA(Flex)->HWA 64x64 W8, P:L150-151"),
                  "cfg3": (1.62, "SA(Flex)->HSA 64x64 K9, P:L495-496"),
                  "cfg4": (1.58, "NA2D(Flex)->HNA 56x56 K7, P:L490-491")}
+# the paper's headline speedups, with their hardware (context, not targets)
+PAPER_HEADLINES = {
+    "window_about_4x": "dense WSA 2.74 ms / HWA(Flex) 0.68 ms, forward, 128x128 grid, 16x16 windows, "
+                       "RTX 3080 (P:L7, P:L161-163, P:L167)",
+    "slide_about_18x": "naive SA 5.85 ms / HSA(Flex) 0.32 ms, forward, 56x56 grid, 7x7 kernel, "
+                       "RTX 3080 (P:L7, P:L226-228)",
+}
+PAPER_TIMING = ("the paper: mean of 10 runs x 100 iterations, first 25% warm-up (P:L137); here: W warm-up "
+                "steps then K timed steps (driver contract)")
 L2_FLUSH_BYTES = 512 << 20
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--config", default="cfg2", choices=sorted(CONFIGS) + sorted(STACK))
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--no-variants", action="store_true", help="skip the row-major / dense comparison runs")
+    p.add_argument("--no-variants", action="store_true", help="skip the row-major / dense / RPB / unfused runs")
     p.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
     p.add_argument("--no-e2e", action="store_true")
-    return p.parse_args()
+    return p.parse_args(argv)
 
 
-# ------------------------------------------------------------------ helpers
-def bwd_bytes(T, d, mask):
-    """Algorithmic HBM bytes of attn_bwd_kernel per launch: read Q, K, V, dO (8d per token-head),
-    LSE, D (8); write dK, dV (4d); dQ: bf16 write (2d) for the q-blocks the dQ plan keeps
-    local, one fp32 read + write of the accumulator (8d, TMA reduce-add) for the others."""
-    mq = mask.row_ptr.numel() - 1
-    nl = mq if mask.n_dq_nonlocal < 0 else mask.n_dq_nonlocal
-    return int(T * (12 * d + 8) + T * (2 * d * (mq - nl) + 8 * d * nl) // mq)
+# ------------------------------------------------------------------ multi-GPU plumbing
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def launch_ranks(args, argv):
+    """--gpus N > 1 outside torchrun: re-execute under torch.distributed.run with N ranks
+    (one process per GPU, rendezvous on 127.0.0.1).  Returns the exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + argv
+    return subprocess.call(cmd)
+
+
+def plan_shards(B, H, world):
+    """Strong-scaling partition of the B x H independent (batch, head) attention units over
+    `world` ranks: rank r gets the contiguous block (b0, b1, h0, h1) --
+    B / world whole batches when world divides B; when B < world and world / B divides H,
+    each batch's heads are split into world / B contiguous groups.  Every unit belongs to
+    exactly one rank.  None: no such partition (the config runs as replicas)."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    if B % world == 0:
+        k = B // world
+        return [(r * k, (r + 1) * k, 0, H) for r in range(world)]
+    if world % B == 0 and H % (world // B) == 0:
+        g = world // B
+        hk = H // g
+        return [(r // g, r // g + 1, (r % g) * hk, (r % g + 1) * hk) for r in range(world)]
+    return None
 
 
 def reduce_max_ms(ms, dist=None, device=None):
@@ -94,14 +149,38 @@ def reduce_max_ms(ms, dist=None, device=None):
     return float(t.item())
 
 
-def job_value(step_ms, world):
-    """Weak scaling: every rank processes one batch per step, so the whole job does
-    `world` batches in step_ms (max over ranks) -> ms per batch of work."""
-    return step_ms / world
+def gather_rank_stats(values, dist=None, device=None):
+    """all_gather of a fixed-length list of floats from every rank (after the timed loop;
+    NCCL on the GPU box, gloo in the CPU tests) -> list indexed by rank."""
+    import torch
+    t = torch.tensor([float(x) for x in values], dtype=torch.float64, device=device)
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return [t.tolist()]
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return [o.tolist() for o in out]
 
 
-def dist_env():
-    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+# ------------------------------------------------------------------ helpers
+def bwd_bytes(T, d, mask):
+    """Algorithmic HBM bytes of the backward main kernel per launch: read Q, K, V, dO (8d per
+    token-head), LSE, D (8); write dK, dV (4d); dQ: bf16 write (2d) for the q-blocks the dQ
+    plan keeps local, one fp32 read + write of the accumulator (8d, TMA reduce-add) for the others."""
+    mq = mask.row_ptr.numel() - 1
+    nl = mq if mask.n_dq_nonlocal < 0 else mask.n_dq_nonlocal
+    return int(T * (12 * d + 8) + T * (2 * d * (mq - nl) + 8 * d * nl) // mq)
+
+
+def exec_flops(tiles, d, block=128):
+    """Tensor-core flops on EXECUTED tiles of one fwd+bwd: 4 b^2 d (S, PV) + 10 b^2 d (S, dP,
+    dV, dK, dQ recomputed / computed in the backward) per tile; empty tiles are never counted."""
+    return 14 * block * block * d * tiles
+
+
+def tensor_pct(flops, ms, peak_tf):
+    """Executed-tile tensor throughput as % of the peak -- the same definition for the headline
+    and every variant: flops / (fwd + bwd_pre + bwd + bwd_fin time)."""
+    return round(100 * flops / (ms * 1e-3) / (peak_tf * 1e12), 2)
 
 
 def load_peaks():
@@ -189,7 +268,7 @@ def oracle_step_sample(cfg, n_slices, seed=0):
     from oracle import attention as oatt
     from oracle import hilbert as ohil
     from oracle.patterns import Spec
-    g, B, H, d = cfg["grid"], cfg["B"], cfg["H"], cfg["d"]
+    g, d = cfg["grid"], cfg["d"]
     N = g * g
     spec = Spec(cfg["kind"], g, g, cfg["win"], cfg["win"])
     s2c, _ = ohil.hilbert_order(g, g)
@@ -220,9 +299,9 @@ def cpu_baseline(cfg, budget_s=15.0):
     t = oracle_step_sample(cfg, n, seed=1) if n > 1 else t1
     per_slice = t / n
     return {"value": round(per_slice * slices_total * 1e3, 3), "unit": "ms", "cores": blas_threads(),
-            "kind": "oracle",
-            "sample": "%d of %d (b,h) slices of one step (Hilbert reorder + fp64 fwd+bwd, numpy), "
-                      "extrapolated x%d" % (n, slices_total, slices_total // max(n, 1))}
+            "kind": "oracle", "measured_s": round(t, 3), "slices_measured": n, "slices_per_step": slices_total,
+            "sample": "%d of %d (b,h) slices of one step (Hilbert reorder + fp64 fwd+bwd, numpy), measured %.2f s, "
+                      "extrapolated x%.2f" % (n, slices_total, t, slices_total / n)}
 
 
 def run_reference(args, cfg):
@@ -236,110 +315,155 @@ def run_reference(args, cfg):
     ms = statistics.mean(times) * slices_total * 1e3
     line = {"impl": "reference", "metric": METRIC, "value": round(ms, 3), "unit": "ms", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (hla_synth)",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (hla_synth)",
             "config": {"workload": args.config + ": " + cfg["text"], "global_batch": cfg["B"],
-                       "seq_len": cfg["grid"] ** 2, "parallelism": "host cores (numpy BLAS)"},
+                       "seq_len": cfg["grid"] ** 2, "parallelism": "host cores (numpy BLAS), rank 0 only"},
             "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": blas_threads(), "kind": "oracle",
-                             "sample": "each step = 1 of %d (b,h) slices (Hilbert reorder + fp64 fwd+bwd), "
-                                       "extrapolated x%d" % (slices_total, slices_total)},
+                             "measured_s_per_slice": [round(t, 4) for t in times],
+                             "sample": "each step = 1 of %d (b,h) slices (Hilbert reorder + fp64 fwd+bwd) measured "
+                                       "(mean %.3f s), extrapolated x%d to the whole step"
+                                       % (slices_total, statistics.mean(times), slices_total)},
             "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------- GPU leg
-def run_stack(args):
-    """--config cfg5: one step = fwd + bwd of every attention layer of the HWT-T stack."""
+def _timed(step, steps, warmup, flush=None, marks=True, sampler=None, dist=None, world=1):
+    """Device-timed steps: one start/end CUDA-event pair per step (marks=False), or an event
+    after every launch for the per-launch breakdown (marks=True).  flush: L2 flush buffer
+    written between steps (untimed); None = warm L2."""
+    import torch
+    for _ in range(warmup):
+        step(None)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.start()
+    rec = []
+    for _ in range(steps):
+        if flush is not None:
+            flush.zero_()
+        ev = [("start", torch.cuda.Event(enable_timing=True))]
+        ev[0][1].record()
+
+        def mark(name, ev=ev):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            ev.append((name, e))
+        step(mark if marks else None)
+        if not marks:
+            mark("end")
+        rec.append(ev)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = sampler.stop() if sampler else None
+    total = [ev[0][1].elapsed_time(ev[-1][1]) for ev in rec]
+    stages, sums = {}, {}
+    for ev in rec:
+        for (_, a), (name, b) in zip(ev[:-1], ev[1:]):
+            stages.setdefault(name, []).append(a.elapsed_time(b))
+            sums[name] = sums.get(name, 0.0) + a.elapsed_time(b) / steps
+    # per-launch medians (single-layer steps) and, per launch name, the mean over steps of its
+    # summed time within a step (the stacks: the same name recurs once per layer)
+    return total, {kk: statistics.median(vv) for kk, vv in stages.items()}, sums, clocks
+
+
+def _init_dist(args):
     import torch
     import torch.distributed as dist
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit("bench.py: WORLD_SIZE=%d but --gpus %d (launch one process per GPU)" % (world, args.gpus))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    return rank, world, local, dev, dist
+
+
+def invariant_residuals(dk, dv, do):
+    """Backward invariants of every (b, h) slice: sum_k dK[k] = 0 and
+    sum_k dV[k] = sum_q dO[q] (exact for the fp64 oracle; softmax rows sum to one).  Returns
+    (max |sum dK|, max |sum dV - sum dO|, bound) -- bound = the bf16 rounding allowance the
+    GPU parity tests use, 8 sqrt(N) rms(dK) 2^-8."""
+    N = dk.shape[1]
+    rk = float(dk.float().sum(1).abs().max())
+    rv = float((dv.float().sum(1) - do.float().sum(1)).abs().max())
+    bound = 8 * math.sqrt(N) * float(dk.float().pow(2).mean().sqrt()) * 2 ** -8
+    return rk, rv, bound
+
+
+def run_stack(args):
+    """--config cfg5 / cfg5-hwt: one step = fwd + bwd of every attention layer of the HWT-T stack."""
+    import torch
 
     import hla_synth
     import paper_2511_05832_b200 as hla
 
     sc = STACK[args.config]
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    rank, world, local, dev, dist = _init_dist(args)
     B, d = sc["B"], sc["d"]
+    if B % world:
+        raise SystemExit("cfg5 stacks shard their batch of %d over the ranks: %d does not divide it" % (B, world))
+    b0, b1 = rank * B // world, (rank + 1) * B // world
     layers = []   # (layer, inputs) in execution order
     for si, (g, H, depth, w) in enumerate(sc["stages"]):
         N = g * g
-        ins = hla_synth.attention_inputs(B, N, H, d, seed=100 * rank + si, device=dev)
-        pair = [hla.HilbertLocalAttention(kind, g, g, w, w, B, H, d, shift=(w * w) // 2 if kind == "HSWA" else 0,
-                                          device=dev, rpb=True) for kind in ("HWA", "HSWA")]
+        ins = hla_synth.attention_inputs_block(B, N, H, d, b0, b1, 0, H, seed=100 + si, device=dev)
+        kinds = ("HWA", "HSWA") if sc["hswa"] else ("HWA",)
+        pair = [hla.HilbertLocalAttention(kind, g, g, w, w, b1 - b0, H, d, block=sc["block"],
+                                          shift=(w * w) // 2 if kind == "HSWA" else 0, device=dev, rpb=sc["rpb"])
+                for kind in kinds]
         gen = torch.Generator().manual_seed(si)
         for lay in pair:
-            lay.rpb.copy_(torch.rand(lay.rpb.shape, generator=gen) * 2 - 1)
+            if sc["rpb"]:
+                lay.rpb = torch.rand(lay.rpb.shape, generator=gen) * 2 - 1
         for i in range(depth):
-            layers.append((pair[i % 2], ins))
+            layers.append((pair[i % len(pair)], ins))
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
     def one_step(rec=None):
         for lay, (q, k, v, do) in layers:
             lay.step(q, k, v, do, rec)
 
-    for _ in range(args.warmup):
-        one_step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-
-    def run(steps, marks):
-        recs = []
-        for _ in range(steps):
-            flush.zero_()
-            ev = [("start", torch.cuda.Event(enable_timing=True))]
-            ev[0][1].record()
-
-            def mark(name, ev=ev):
-                e = torch.cuda.Event(enable_timing=True)
-                e.record()
-                ev.append((name, e))
-            one_step(mark if marks else None)
-            if not marks:
-                mark("end")
-            recs.append(ev)
-        torch.cuda.synchronize()
-        return recs
-
-    # the step: one start / end event pair; the per-stage sums: a second, instrumented run
     sampler = ClockSampler(local)
-    sampler.start()
-    totals = run(args.steps, False)
-    if world > 1:
-        dist.barrier()
-    clocks = sampler.stop()
-    step = [ev[0][1].elapsed_time(ev[-1][1]) for ev in totals]
-    per = {}
-    for ev in run(args.steps, True):
-        for (_, a), (name, b) in zip(ev[:-1], ev[1:]):
-            per[name] = per.get(name, 0.0) + a.elapsed_time(b) / args.steps
-    step_ms = reduce_max_ms(statistics.mean(step), dist if world > 1 else None, dev)
+    totals, _, _, clocks = _timed(one_step, args.steps, args.warmup, flush, False, sampler, dist, world)
+    # per-stage sums over the layers: a second, instrumented run (events after every launch)
+    _, _, per, _ = _timed(one_step, args.steps, 1, flush, True, None, dist, world)
+    my_ms = statistics.mean(totals)
+    step_ms = reduce_max_ms(my_ms, dist if world > 1 else None, dev)
+    ranks = gather_rank_stats([rank, b1 - b0, my_ms], dist if world > 1 else None, dev)
     peaks = load_peaks()
-    # roofline of the stack's dominant kernel (sum over layers): algorithmic bytes / summed time
+    # roofline of the stack's dominant kernel (summed over the layers): algorithmic bytes / summed time
     tb = {"fwd": 0, "bwd": 0}
     for lay, (q, _, _, _) in layers:
         T = q.shape[0] * q.shape[1] * q.shape[2]
         tb["fwd"] += T * (8 * d + 4)
         tb["bwd"] += bwd_bytes(T, d, lay.mask)
-    dom = max(("fwd", "bwd"), key=lambda kk: per[kk])
+    dom = max(("fwd", "bwd"), key=lambda kk: per.get(kk, 0.0))
     ach = tb[dom] / (per[dom] * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm"], "unit": "GB/s",
             "frac": round(ach / peaks["hbm"], 4), "kernel": "attn_%s_kernel" % dom, "stage": dom,
-            "share_of_step": round(per[dom] / statistics.mean(step), 4), "traffic": None,
-            "note": "summed over the %d attention layers of the stack" % len(layers), "peak_source": peaks["source"]}
-    line = {"metric": METRIC, "value": round(job_value(step_ms, world), 4), "unit": "ms", "n_gpus": world,
+            "share_of_step": round(per[dom] / my_ms, 4), "traffic": None,
+            "note": "summed over the %d attention layers of the stack (rank 0)" % len(layers),
+            "peak_source": peaks["source"]}
+    line = {"metric": METRIC, "value": round(step_ms, 4), "unit": "ms", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic: hla_synth splitmix64 uniform, unit variance, bf16 (no dataset)",
-            "config": {"workload": args.config + ": " + sc["text"], "global_batch": B * world,
-                       "layers": len(layers), "parallelism": "dp%d" % world,
-                       "l2": "flushed between timed steps (%d MiB write, untimed)" % (L2_FLUSH_BYTES >> 20)},
+            "config": {"workload": args.config + ": " + sc["text"], "global_batch": B, "layers": len(layers),
+                       "parallelism": "batch shards: rank r runs batches [r B/%d, (r+1) B/%d), all heads" % (world, world),
+                       "l2": "flushed between timed steps (%d MiB write, untimed)" % (L2_FLUSH_BYTES >> 20),
+                       "timing": PAPER_TIMING},
             "clocks": clocks, "e2e": None,
             "gpu_launches": sum(lay.launches_per_step for lay, _ in layers) * args.steps,
             "roofline": roof, "cpu_baseline": None,
-            "breakdown_ms": {kk: round(vv, 4) for kk, vv in per.items()}}
+            "breakdown_ms": {kk: round(vv, 4) for kk, vv in per.items()},
+            "ranks": [{"rank": int(r[0]), "batches": int(r[1]), "step_ms": round(r[2], 4)} for r in ranks]}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -347,115 +471,91 @@ def run_stack(args):
         dist.destroy_process_group()
 
 
-def main():
-    args = parse()
-    if args.config in STACK:
-        if args.impl == "reference":
-            print(json.dumps({"impl": "reference", "unavailable": "the oracle leg covers cfg1-cfg4 only"}))
-            return
-        run_stack(args)
-        return
-    cfg = CONFIGS[args.config]
-    if args.impl == "reference":
-        run_reference(args, cfg)
-        return
-
+def run_single(args):
     import torch
-    import torch.distributed as dist
 
     import hla_synth
     import paper_2511_05832_b200 as hla
 
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    rank, world, local, dev, dist = _init_dist(args)
     peaks = load_peaks()
-
     g, B, H, d, win = cfg["grid"], cfg["B"], cfg["H"], cfg["d"], cfg["win"]
     N = g * g
-    # each rank: its own batch shard (weak scaling); inputs resident in HBM before timing
-    q, k, v, do = hla_synth.attention_inputs(B, N, H, d, seed=rank, device=dev)
-    layer = hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, B, H, d, device=dev)
+    plan = plan_shards(B, H, world)
+    b0, b1, h0, h1 = plan[rank] if plan else (0, B, 0, H)
+    Bs, Hs = b1 - b0, h1 - h0
+    # this rank's shard of the global batch (exactly the global tensors' values), resident in HBM
+    q, k, v, do = hla_synth.attention_inputs_block(B, N, H, d, b0, b1, h0, h1, seed=0, device=dev)
+
+    # mask build (once per shape, outside the step; reported separately): host wall time of
+    # hla_build_block_mask + the bwd plan, both synchronous
+    builds = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        hla.hla_build_block_mask(hla.pattern_desc(cfg["kind"], g, g, win, win), dev)
+        builds.append((time.perf_counter() - t0) * 1e3)
+    layer = hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, Bs, Hs, d, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
-
-    def timed(lay, steps, warmup, with_marks=True, sampler=None):
-        for _ in range(warmup):
-            lay.step(q, k, v, do)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        if sampler:
-            sampler.start()
-        rec = []
-        for _ in range(steps):
-            flush.zero_()                       # L2 flush between timed steps (untimed)
-            ev = [("start", torch.cuda.Event(enable_timing=True))]
-            ev[0][1].record()
-
-            def mark(name, ev=ev):
-                e = torch.cuda.Event(enable_timing=True)
-                e.record()
-                ev.append((name, e))
-            lay.step(q, k, v, do, mark if with_marks else None)
-            if not with_marks:
-                mark("end")
-            rec.append(ev)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        clocks = sampler.stop() if sampler else None
-        total = [ev[0][1].elapsed_time(ev[-1][1]) for ev in rec]
-        stages = {}
-        for ev in rec:
-            for (_, a), (name, b) in zip(ev[:-1], ev[1:]):
-                stages.setdefault(name, []).append(a.elapsed_time(b))
-        # per-launch stages: median over the steps (robust to a single slow step)
-        return total, {kk: statistics.median(vv) for kk, vv in stages.items()}, clocks
+    step = lambda mark, lay=layer: lay.step(q, k, v, do, mark)   # noqa: E731
 
     sampler = ClockSampler(local)
     # the step is timed with one start / end event pair only; the per-kernel breakdown comes
     # from a second, instrumented run (one event after every launch: each intermediate event
     # adds ~2-3 us of GPU timeline, so it must not sit inside the headline measurement)
-    total, _, clocks = timed(layer, args.steps, args.warmup, False, sampler)
-    _, stages, _ = timed(layer, args.steps, 2, True)
+    total, _, _, clocks = _timed(step, args.steps, args.warmup, flush, False, sampler, dist, world)
+    _, stages, _, _ = _timed(step, args.steps, 2, flush, True, None, dist, world)
+    warm, _, _, _ = _timed(step, args.steps, 2, None, False, None, dist, world)
     my_ms = statistics.mean(total)
     step_ms = reduce_max_ms(my_ms, dist if world > 1 else None, dev)
-    value = job_value(step_ms, world)   # ms per batch of work for the whole job
+    warm_ms = reduce_max_ms(statistics.mean(warm), dist if world > 1 else None, dev)
+    dq, dk, dv = layer.step(q, k, v, do)
+    torch.cuda.synchronize()
+    rk, rv, rbound = invariant_residuals(dk, dv, do)
 
-    # --- row-major baseline and dense FA on the same shape (same kernels) ---
-    variants = {}
+    tiles = layer.nnz * Bs * Hs
+    attn_ms = stages["fwd"] + stages["bwd_pre"] + stages["bwd"] + stages["bwd_fin"]
+
+    # --- variants on this rank's shard (same kernels): row-major baseline, dense FA, HWT's
+    #     global RPB, and the unfused reorder (explicit hla_hilbert_perm passes: perm_ms) ---
+    variants, perm = {}, None
     if not args.no_variants:
         vsteps = max(3, min(args.steps, 10))
         for name, kind in (("row_major", cfg["rm"]), ("dense", "DENSE")):
-            lay = hla.HilbertLocalAttention(kind, g, g, win, win, B, H, d, device=dev)
-            tot, _, _ = timed(lay, vsteps, 2, False)
-            _, st, _ = timed(lay, vsteps, 1, True)
+            lay = hla.HilbertLocalAttention(kind, g, g, win, win, Bs, Hs, d, device=dev)
+            st_fn = lambda mark, lay=lay: lay.step(q, k, v, do, mark)   # noqa: E731
+            tot, _, _, _ = _timed(st_fn, vsteps, 2, flush, False, None, dist, world)
+            _, st, _, _ = _timed(st_fn, vsteps, 1, flush, True, None, dist, world)
+            a_ms = st["fwd"] + st["bwd_pre"] + st["bwd"] + st["bwd_fin"]
             variants[name] = {"pattern": kind, "ms_per_step": round(statistics.mean(tot), 4),
-                              "fwd_ms": round(st["fwd"], 4), "bwd_ms": round(st["bwd_pre"] + st["bwd"] + st["bwd_fin"], 4),
-                              "tiles_per_bh": lay.nnz}
-            exec_flops = 14 * 128 * 128 * d * lay.nnz * B * H
-            variants[name]["tensor_pct_executed"] = round(
-                100 * exec_flops / ((st["fwd"] + st["bwd"]) * 1e-3) / (peaks["tf_sus"] * 1e12), 2)
+                              "fwd_ms": round(st["fwd"], 4), "bwd_ms": round(a_ms - st["fwd"], 4),
+                              "tiles_per_bh": lay.nnz,
+                              "tensor_pct_executed": tensor_pct(exec_flops(lay.nnz * Bs * Hs, d), a_ms, peaks["tf_sus"])}
             del lay
-        # HWT's global relative position bias on the same layer (reading R19)
-        lay = hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, B, H, d, device=dev, rpb=True)
-        lay.rpb.copy_(torch.rand(lay.rpb.shape, generator=torch.Generator().manual_seed(1)) * 2 - 1)
-        tot, _, _ = timed(lay, vsteps, 2, False)
-        _, st, _ = timed(lay, vsteps, 1, True)
+        lay = hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, Bs, Hs, d, device=dev, rpb=True)
+        lay.rpb = torch.rand(lay.rpb.shape, generator=torch.Generator().manual_seed(1)) * 2 - 1
+        st_fn = lambda mark, lay=lay: lay.step(q, k, v, do, mark)   # noqa: E731
+        tot, _, _, _ = _timed(st_fn, vsteps, 2, flush, False, None, dist, world)
+        _, st, _, _ = _timed(st_fn, vsteps, 1, flush, True, None, dist, world)
         variants["global_rpb"] = {"pattern": cfg["kind"] + " + global RPB score_mod",
                                   "ms_per_step": round(statistics.mean(tot), 4), "fwd_ms": round(st["fwd"], 4),
                                   "bwd_ms": round(st["bwd_pre"] + st["bwd"] + st["bwd_fin"], 4)}
         del lay
-        ours_attn = stages["fwd"] + stages["bwd_pre"] + stages["bwd"] + stages["bwd_fin"]
+        if layer.hilbert and (g & (g - 1)) == 0:
+            lay = hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, Bs, Hs, d, device=dev, fused=False)
+            st_fn = lambda mark, lay=lay: lay.step(q, k, v, do, mark)   # noqa: E731
+            tot, _, _, _ = _timed(st_fn, vsteps, 2, flush, False, None, dist, world)
+            _, st, _, _ = _timed(st_fn, vsteps, 1, flush, True, None, dist, world)
+            perm = {kk: round(st[kk], 4) for kk in ("perm_qkv", "perm_o", "perm_do", "perm_grads")}
+            variants["unfused_reorder"] = {"pattern": cfg["kind"] + " with explicit hla_hilbert_perm passes",
+                                           "ms_per_step": round(statistics.mean(tot), 4),
+                                           "perm_ms": round(sum(perm.values()), 4), "perm_breakdown_ms": perm,
+                                           "attn_ms": round(st["fwd"] + st["bwd_pre"] + st["bwd"] + st["bwd_fin"], 4)}
+            del lay
         rm = variants["row_major"]
-        rm_attn = rm["fwd_ms"] + rm["bwd_ms"]
-        variants["speedup_attn_vs_row_major"] = round(rm_attn / ours_attn, 3)
-        variants["speedup_step_vs_row_major"] = round(rm["ms_per_step"] / step_ms, 3)
-        variants["speedup_attn_vs_dense"] = round((variants["dense"]["fwd_ms"] + variants["dense"]["bwd_ms"]) / ours_attn, 3)
+        variants["speedup_attn_vs_row_major"] = round((rm["fwd_ms"] + rm["bwd_ms"]) / attn_ms, 3)
+        variants["speedup_step_vs_row_major"] = round(rm["ms_per_step"] / my_ms, 3)
+        variants["speedup_attn_vs_dense"] = round((variants["dense"]["fwd_ms"] + variants["dense"]["bwd_ms"]) / attn_ms, 3)
         if args.config in PAPER_SPEEDUP:
             variants["paper_speedup_fwd_bwd"] = {"value": PAPER_SPEEDUP[args.config][0],
                                                  "source": PAPER_SPEEDUP[args.config][1] + " (RTX 3080, context)"}
@@ -469,7 +569,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         hin = [x.cpu().pin_memory() for x in (q, k, v, do)]
-        layers = [layer, hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, B, H, d, device=dev)]
+        layers = [layer, hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, Bs, Hs, d, device=dev)]
         din = [[torch.empty_like(x) for x in (q, k, v, do)] for _ in range(2)]
         hout = [[torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (q, q, q, q)] for _ in range(2)]
         s_in, s_out, s_cmp = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.current_stream(dev)
@@ -515,19 +615,18 @@ def main():
         torch.cuda.synchronize()
         te = reduce_max_ms(e0.elapsed_time(e1) / esteps, dist if world > 1 else None, dev)
         nbytes = sum(x.numel() * x.element_size() for x in hin)
-        e2e = {"value": round(job_value(te, world), 4), "unit": "ms", "h2d_bytes_per_step": nbytes,
-               "d2h_bytes_per_step": nbytes, "steps": esteps,
+        e2e = {"value": round(te, 4), "unit": "ms", "h2d_bytes_per_step": nbytes * world,
+               "d2h_bytes_per_step": nbytes * world, "steps": esteps,
                "path": "pinned host -> (copy stream) -> HilbertLocalAttention.forward/backward (compute stream) -> "
-                       "(copy stream) -> pinned host; two steps in flight (double-buffered device tensors)"}
+                       "(copy stream) -> pinned host; two steps in flight (double-buffered device tensors); "
+                       "per-rank shards, max over ranks; bytes = all ranks"}
 
     # --- roofline of the dominant kernel (share of the step) ---
-    T = B * H * N                               # token-heads per launch
-    tiles = layer.nnz * B * H
+    T = Bs * Hs * N                              # token-heads per launch on this rank
     kern = {
         "fwd": {"bytes": T * (8 * d + 4), "flops": 4 * 128 * 128 * d * tiles, "name": "attn_fwd_kernel"},
-        "bwd": {"bytes": bwd_bytes(T, d, layer.mask), "flops": 10 * 128 * 128 * d * tiles, "name": "attn_bwd_kernel"},
-        "perm_qkv": {"bytes": 3 * 2 * T * d * 2, "flops": 0, "name": "hilbert_perm_kernel"},
-        "perm_grads": {"bytes": 3 * 2 * T * d * 2, "flops": 0, "name": "hilbert_perm_kernel"},
+        "bwd": {"bytes": bwd_bytes(T, d, layer.mask), "flops": 10 * 128 * 128 * d * tiles,
+                "name": "attn_bwd_full_kernel / attn_bwd_split_kernel"},
     }
     dom = max((kk for kk in kern if kk in stages), key=lambda kk: stages[kk])
     ms_dom = stages[dom]
@@ -549,35 +648,49 @@ def main():
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f).get(args.config, {}).get(dom)
-        if tr:
+        if tr and world == 1:
             roof["traffic"] = tr
     except Exception:
         pass
 
-    attn_ms = stages["fwd"] + stages["bwd_pre"] + stages["bwd"] + stages["bwd_fin"]
-    exec_flops = 14 * 128 * 128 * d * tiles
+    # --- after the timed loops: per-rank statistics over NCCL (C1, C2) ---
+    ranks = gather_rank_stats([rank, b0, b1, h0, h1, my_ms, stages["fwd"], stages["bwd"], rk, rv, rbound],
+                              dist if world > 1 else None, dev)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(cfg)
 
     line = {
-        "metric": METRIC, "value": round(value, 4), "unit": "ms", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16",
+        "metric": METRIC, "value": round(step_ms, 4), "unit": "ms", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": False,
+        "scaling": "strong" if plan else "replicas", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic: hla_synth splitmix64 uniform, unit variance, bf16 (no dataset)",
-        "config": {"workload": args.config + ": " + cfg["text"], "global_batch": B * world, "seq_len": N,
-                   "parallelism": "dp%d (batch shards, no collective on the hot path)" % world,
-                   "l2": "flushed between timed steps (%d MiB write, untimed)" % (L2_FLUSH_BYTES >> 20),
+        "config": {"workload": args.config + ": " + cfg["text"], "global_batch": B, "seq_len": N,
+                   "parallelism": ("batch x head shards over %d ranks (plan_shards), no collective on the hot path"
+                                   % world) if plan else "replicas (no batch x head partition for %d ranks)" % world,
+                   "l2": "flushed between timed steps (%d MiB write, untimed); warm_l2_ms without the flush"
+                         % (L2_FLUSH_BYTES >> 20),
                    "step": ("fwd+bwd_pre+bwd+bwd_fin (Hilbert reorder fused into the kernels)" if layer.fused else
-                            "perm(qkv)+fwd+perm(o)+perm(dO)+bwd_pre+bwd+bwd_fin+perm(dq,dk,dv)"),
-                   "mask": "built once before timing (%d of %d tiles per (b,h) executed)" % (layer.nnz, (N // 128) ** 2),
-                   "timing": "CUDA events: one start/end pair per step (value = mean); breakdown_ms = per-launch "
-                             "medians from a second run with one event after every launch"},
+                            "fwd+bwd_pre+bwd+bwd_fin"),
+                   "mask": "built once before timing (%d of %d tiles per (b,h) executed)"
+                           % (layer.nnz, ((N + 127) // 128) ** 2),
+                   "timing": "CUDA events: one start/end pair per step (value = mean, max over ranks); "
+                             "breakdown_ms = per-launch medians from a second run with one event after every "
+                             "launch; " + PAPER_TIMING},
         "clocks": clocks, "e2e": e2e, "gpu_launches": layer.launches_per_step * args.steps,
         "roofline": roof, "cpu_baseline": cpu,
         "breakdown_ms": {kk: round(vv, 5) for kk, vv in stages.items()},
         "attn_ms": round(attn_ms, 4),
-        "tensor_pct_executed": round(100 * exec_flops / (attn_ms * 1e-3) / (peaks["tf_sus"] * 1e12), 2),
+        "tensor_pct_executed": tensor_pct(exec_flops(tiles, d), attn_ms, peaks["tf_sus"]),
+        "warm_l2_ms": round(warm_ms, 4),
+        "mask_build_ms": round(statistics.median(builds), 3),
+        "perm_ms": round(sum(perm.values()), 4) if perm else None,
+        "ranks": [{"rank": int(r[0]), "batches": [int(r[1]), int(r[2])], "heads": [int(r[3]), int(r[4])],
+                   "step_ms": round(r[5], 4), "fwd_ms": round(r[6], 4), "bwd_ms": round(r[7], 4),
+                   "bwd_invariants": {"max_abs_sum_dK": r[8], "max_abs_sum_dV_minus_sum_dO": r[9],
+                                      "bound": r[10], "ok": bool(r[8] <= r[10] and r[9] <= r[10])}}
+                  for r in ranks],
+        "paper_headlines": PAPER_HEADLINES,
         "variants": variants,
     }
     if rank == 0:
@@ -585,6 +698,24 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(args, argv))
+    if args.impl == "reference":
+        if args.config in STACK:
+            if dist_env()[0] == 0:
+                print(json.dumps({"impl": "reference", "unavailable": "the oracle leg covers cfg1-cfg4 only"}))
+            return
+        run_reference(args, CONFIGS[args.config])
+        return
+    if args.config in STACK:
+        run_stack(args)
+    else:
+        run_single(args)
 
 
 if __name__ == "__main__":

@@ -92,6 +92,35 @@ def uniform_torch(shape, seed, tensor_id, scale=1.0, device="cpu", chunk=1 << 26
     return out.view(*shape)
 
 
+def uniform_torch_block(shape, b0, b1, h0, h1, seed, tensor_id, scale=1.0, device="cpu"):
+    """The [b0:b1, :, h0:h1, :] block of uniform_torch(shape, ...) for shape = (B, N, H, d),
+    generated from its GLOBAL linear indices (a rank's shard holds exactly the values of the
+    global tensor -- multi-GPU shards, bench.py plan_shards)."""
+    import torch
+    B, N, H, d = shape
+    out = torch.empty((b1 - b0, N, h1 - h0, d), dtype=torch.bfloat16, device=device)
+    key = _to_signed((seed ^ (tensor_id << 56)) & 0xFFFFFFFFFFFFFFFF)
+    hd = torch.arange(h0, h1, dtype=torch.int64, device=device)[:, None] * d + torch.arange(d, device=device)[None, :]
+    rows = max(1, (1 << 24) // max(1, (h1 - h0) * d))
+    for b in range(b0, b1):
+        for n0 in range(0, N, rows):
+            n1 = min(N, n0 + rows)
+            tok = (b * N + torch.arange(n0, n1, dtype=torch.int64, device=device)) * (H * d)
+            idx = tok[:, None, None] + hd[None, :, :]
+            u = _lsr(splitmix64_torch(idx ^ key), 40)
+            x = (u.to(torch.float32) * (2.0 ** -24) * 2.0 - 1.0) * math.sqrt(3.0)
+            out[b - b0, n0:n1] = (x * scale).to(torch.bfloat16)
+    return out
+
+
+def attention_inputs_block(B, N, H, d, b0, b1, h0, h1, seed=0, sharp=False, device="cpu"):
+    """q, k, v, dO restricted to batches [b0, b1) and heads [h0, h1) of the global tensors."""
+    qscale = 4.0 if sharp else 1.0
+    shape = (B, N, H, d)
+    return tuple(uniform_torch_block(shape, b0, b1, h0, h1, seed, t, sc, device)
+                 for t, sc in ((1, qscale), (2, 1.0), (3, 1.0), (4, 1.0)))
+
+
 def attention_inputs(B, N, H, d, seed=0, sharp=False, backend="torch", device="cpu"):
     """q, k, v, dO in grid order, layout [B, N, heads, d]."""
     qscale = 4.0 if sharp else 1.0

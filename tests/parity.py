@@ -60,7 +60,8 @@ def emulated_slice(Q, K, V, dO, spec, scale=None, block=128):
         st = s2[:, k0:k0 + block]
         m_tile = st.max(axis=1)
         m_new = np.where(m_tile > m_ref + 8.0, m_tile, m_ref)
-        alpha = np.where(m_new == m_ref, 1.0, np.exp2(m_ref - m_new))
+        with np.errstate(invalid="ignore"):   # -inf - -inf where a row has no key yet (alpha unused)
+            alpha = np.where(m_new == m_ref, 1.0, np.exp2(m_ref - m_new))
         m_ref = m_new
         m_use = np.where(np.isinf(m_ref), 0.0, m_ref)
         p = np.exp2(st - m_use[:, None])

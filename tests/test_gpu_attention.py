@@ -246,7 +246,7 @@ RPB_CASES = [
     ("WSA", 56, 7, 1, 1, 32, True),        # 56x56 (paper shape), ragged last tile
     ("HWA", 56, 7, 1, 2, 32, True),        # generalized Hilbert 56x56 (fused), ragged last tile
     ("HSWA", 28, 7, 2, 6, 32, True),       # cfg5 stage 2 shape (HWT-T), 49-token shifted windows
-    ("HSWA", 8, 7, 2, 24, 32, True),       # cfg5 stage 4 (7x7 padded to 8x8: N = 64 < one tile)
+    ("HSWA", 8, 8, 2, 24, 32, True),       # cfg5 stage 4 (7x7 padded to 8x8, 8x8 windows: N = 64 < one tile)
 ]
 
 

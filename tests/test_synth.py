@@ -31,3 +31,12 @@ def test_distribution():
     assert np.abs(x).max() <= np.sqrt(3) + 1e-2
     bits = x.view(np.uint32)
     assert not (bits & 0xFFFF).any()          # exactly bf16-representable
+
+
+def test_block_generator_matches_global_tensor():
+    """A multi-GPU shard ([b0:b1, :, h0:h1]) holds exactly the global tensor's values."""
+    import torch
+    full = hla_synth.attention_inputs(3, 16, 4, 8, seed=5, sharp=True)
+    for b0, b1, h0, h1 in ((0, 3, 0, 4), (1, 3, 1, 3), (2, 3, 0, 1)):
+        blk = hla_synth.attention_inputs_block(3, 16, 4, 8, b0, b1, h0, h1, seed=5, sharp=True)
+        assert all(torch.equal(f[b0:b1, :, h0:h1], b) for f, b in zip(full, blk))
