@@ -22,7 +22,7 @@ for kind, g, w, B, H, d, fused in cases:
 # (shifted windows, all-partial tiles), HNA (clamped neighbourhoods, dQ accumulator + finalize),
 # and the generalized Hilbert curve on a non-2^k grid (56x56, ragged last tile)
 cases2 = [("HWA", 64, 16, 1, 2, 64, False), ("HWA", 56, 7, 1, 1, 32, True), ("HSWA", 32, 8, 2, 3, 32, True),
-          ("HNA", 32, 5, 1, 2, 64, False), ("HSWA", 8, 7, 2, 2, 32, True)]
+          ("HNA", 32, 5, 1, 2, 64, False), ("HSWA", 8, 8, 2, 2, 32, True)]
 for kind, g, w, B, H, d, rpb in cases2:
     q, k, v, do = (t.to(dev) for t in hla_synth.attention_inputs(B, g * g, H, d, seed=1))
     shift = (w * w) // 2 if kind == "HSWA" else 0
