@@ -104,17 +104,6 @@ constexpr int kVar = HLA_BWD_VAR;
 #define HLA_PFLUSH(lo, hi, cond) do {} while (0)
 #endif
 
-// entries of the per-tile dRPB window (offset rows of the tile's box, full table row stride
-// 2W - 1) in shared memory; more at D = 32, where the smaller tiles leave room
-template <int D>
-constexpr int rpb_win_cap() { return D == 32 ? 4096 : 2048; }
-// The window accumulates in 32-bit fixed point (shared-memory fp32 / 64-bit atomics are
-// compare-and-swap loops on sm_100, ATOMS.CAST.SPIN in SASS; 32-bit integer ATOMS.ADD is
-// native) with a per-tile power-of-two scale chosen from the tile's largest |dL/dscore|:
-// every addend is at most 2^22 in magnitude and at most 128 pairs of a 128 x 128 tile share
-// an offset (one per key), so a window entry stays below 2^29; the resolution is 2^-22 of
-// the tile's largest addend, independent of the gradient's absolute magnitude.
-constexpr int kRpbFixBits = 22;
 
 template <int D, bool kBias = false>
 struct FullSmem {
@@ -616,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               tmx = fmaxf(tmx, fmaxf(fmaxf(m.x, m.y), fmaxf(m.z, m.w)));
             }
             // largest addend in [2^(kRpbFixBits-1), 2^kRpbFixBits)
-            fx = tmx > 0.f ? ldexpf(1.f, kRpbFixBits - 1 - ilogbf(tmx)) : 1.f;
+            fx = rpb_scale_for(tmx, 1.f);
           }
           const uint32_t wbase = sm100::smem_u32(sm.rpb_win);
 #pragma unroll
@@ -1118,18 +1107,19 @@ hla_status prepare_main(const hla_pattern_desc* d, const hla_block_mask* m, int3
   pl->mkb = (pat.N + kBlock - 1) / kBlock;
   pl->head_dim = head_dim;
   // schedule: full-tile (attn_bwd_full_kernel) when full tiles are at least half of the
-  // mask's tiles or with the RPB score_mod; half-tile (attn_bwd_split_kernel) otherwise
-  // (the split schedule overlaps the partial tiles' masked compute better)
-  pl->full = prm.rpb != nullptr || m->host_counts[1] >= m->host_counts[2];
+  // mask's tiles; half-tile (attn_bwd_split_kernel) otherwise (the split
+  // schedule overlaps the partial tiles' masked compute better)
+  pl->full = m->host_counts[1] >= m->host_counts[2] && m->host_counts[1] > 0;
   return HLA_OK;
 }
 
 hla_status launch_main(const MainPlan& pl, cudaStream_t stream) {
+  const bool bias = pl.prm.rpb != nullptr;
   if (pl.full)
-    return bwd::launch_full(pl.prm.rpb != nullptr, pl.head_dim, pl.gather, pl.two_d, pl.mq, pl.mk, pl.mv, pl.mdo,
-                            pl.mdq, pl.prm, pl.mkb, stream);
-  return bwd::launch_split(pl.head_dim, pl.gather, pl.two_d, pl.mq, pl.mk, pl.mv, pl.mdo, pl.mdq, pl.prm, pl.mkb,
-                           stream);
+    return bwd::launch_full(bias, pl.head_dim, pl.gather, pl.two_d, pl.mq, pl.mk, pl.mv, pl.mdo, pl.mdq, pl.prm,
+                            pl.mkb, stream);
+  return bwd::launch_split(bias, pl.head_dim, pl.gather, pl.two_d, pl.mq, pl.mk, pl.mv, pl.mdo, pl.mdq, pl.prm,
+                           pl.mkb, stream);
 }
 
 }  // namespace

@@ -35,12 +35,38 @@ struct BwdParams {
   unsigned long long* visited;
 };
 
+// Global-RPB table gradient (reading R19/R20).  Each tile's pairs are accumulated per 2D
+// offset in a shared-memory window (the offset rows of the tile's cell box at the table's
+// row stride 2W - 1) and flushed to the table with fp32 global reductions.  Entries of
+// the window.  More at D = 32, where the smaller tiles leave room.
+template <int D>
+constexpr int rpb_win_cap() { return D == 32 ? 4096 : 2048; }
+// The window accumulates in 32-bit fixed point (shared-memory fp32 / 64-bit atomics are
+// compare-and-swap loops on sm_100, ATOMS.CAST.SPIN in SASS; 32-bit integer ATOMS.ADD is
+// native) at a power-of-two scale relative to the largest |dL/dscore| of a tile: every
+// addend below 2^22 and at most 128 pairs of a 128 x 128 tile per offset (one per key) keep
+// an entry below 2^29; the resolution is 2^-22 of that largest addend, independent of the
+// gradient's absolute magnitude.
+constexpr int kRpbFixBits = 22;
+constexpr float kRpbFixMax = 4194304.f;   // 2^kRpbFixBits: larger scaled addends go to global fp32 atomics
+// scale whose largest addend (for the maximum tmx) lies in [2^(kRpbFixBits-1), 2^kRpbFixBits)
+__device__ __forceinline__ float rpb_scale_for(float tmx, float fallback) {
+  return tmx > 0.f ? ldexpf(1.f, kRpbFixBits - 1 - ilogbf(tmx)) : fallback;
+}
+// the next tile's scale from the eight compute warps' maxima of a tile
+__device__ __forceinline__ float rpb_next_scale(const float* wmax8, float cur) {
+  float m = 0.f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) m = fmaxf(m, wmax8[w]);
+  return rpb_scale_for(m, cur);
+}
+
 // Kernel launch of one schedule for the head_dim / reorder / 2D-pattern variant; the maps
 // view Q, K, V, dO as bf16 rows and the fp32 dQ accumulator (see hla_attn_bwd_main).
 hla_status launch_full(bool bias, int head_dim, bool gather, bool two_d, const CUtensorMap& mq,
                        const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq,
                        const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream);
-hla_status launch_split(int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
+hla_status launch_split(bool bias, int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
                         const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm,
                         int32_t n_kblocks, cudaStream_t stream);
 

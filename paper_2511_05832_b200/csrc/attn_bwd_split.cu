@@ -22,7 +22,9 @@
 //               each per half): P^T, dS^T (mask only on partial tiles);
 //    warps 10-13 thread = query row: dQ_i drains (bf16 rows for complete chains, else
 //               smem -> TMA reduce-add into the fp32 accumulator) and the dK / dV rows.
-// No global-RPB score_mod here: that runs on the full-tile schedule.
+// Global-RPB score_mod (kBias): the bias joins the P recompute, and dL/dscore is
+// accumulated per 2D offset in a shared-memory window (fixed point at the previous tile's
+// scale, attn_bwd_common.cuh) flushed once per tile.
 #include "attn_bwd_common.cuh"
 
 namespace hla {
@@ -37,7 +39,7 @@ constexpr int kHalf = 64;       // q-columns per pipeline half
 #endif
 constexpr int kVar = HLA_BWD_VAR;   // dev-only decomposition switches, see attn_bwd.cu
 
-template <int D>
+template <int D, bool kBias>
 struct SplitSmem {
   static constexpr uint32_t kTileBytes = kBlock * D * 2;
   alignas(1024) uint8_t k[2][kTileBytes];
@@ -48,18 +50,21 @@ struct SplitSmem {
   alignas(1024) float dq_stage[kBlock * 32];    // fp32 dQ half tile [128][32], SWIZZLE_128B
   alignas(16) float lse[2][kBlock];
   alignas(16) float dd[2][kBlock];
+  alignas(16) int32_t qa[2][kBias ? kBlock : 4];   // kBias: A_q of the stage's query columns (RPB table index = A_q - B_k)
+  alignas(16) float rpb_wmax[2][8];                // kBias: per compute warp max |dL/dscore| of a tile (tile parity)
   uint64_t kv_full[2], kv_empty[2], q_full[2], q_empty[2], s_full[2], ds_ready[2], dq_full[2], dq_free[2], dkv_full,
       epi_done;
   uint32_t tmem_base;
+  int32_t rpb_win[kBias ? rpb_win_cap<D>() : 1];   // dRPB of the current tile's offset box, fixed point (compute warps)
 };
 
-template <int D, bool kTwoD, bool kGather>
+template <int D, bool kTwoD, bool kGather, bool kBias>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                     const __grid_constant__ CUtensorMap tmDQ, const BwdParams prm) {
   extern __shared__ uint8_t smem_raw[];
-  using Smem = SplitSmem<D>;
+  using Smem = SplitSmem<D, kBias>;
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   UnitGeom ug;
@@ -147,6 +152,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (s) stage_tag1 = tag; else stage_tag0 = tag;
           if (role == 0) {
+            if (kBias) {
+              // A_q = (qr + H - 1)(2W - 1) + qc + W - 1 of the q-block's 128 columns (phantom: cell 0),
+              // read by the compute warps as warp-uniform 16-B loads next to LSE / D
+              const int4 rc = make_int4(rpb_cell_rc(prm.cells, qblk * kBlock + 4 * lane, prm.N, prm.grid_w),
+                                        rpb_cell_rc(prm.cells, qblk * kBlock + 4 * lane + 1, prm.N, prm.grid_w),
+                                        rpb_cell_rc(prm.cells, qblk * kBlock + 4 * lane + 2, prm.N, prm.grid_w),
+                                        rpb_cell_rc(prm.cells, qblk * kBlock + 4 * lane + 3, prm.N, prm.grid_w));
+              const int32_t a0 = (prm.grid_h - 1) * prm.rpb_w + prm.grid_w - 1;
+              auto a_of = [&](int32_t v) { return a0 + (v >> 16) * prm.rpb_w + (v & 0xffff); };
+              sm100::sts_u4(sm100::smem_u32(sm.qa[s]) + 16u * lane, a_of(rc.x), a_of(rc.y), a_of(rc.z), a_of(rc.w));
+              __syncwarp();   // every lane's A_q is written before lane 0 arrives on q_full
+            }
             if (lane == 0 && (kVar & 4)) {
               sm100::mbar_arrive(&sm.q_full[s]);
             } else if (lane == 0) {
@@ -284,6 +301,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = prm.scale_log2, scale = prm.scale;
+    if (kBias) {   // the dRPB window starts (and is left after every flush) zeroed
+      for (int i = (warp - 2) * 32 + lane; i < rpb_win_cap<D>(); i += 256) sm.rpb_win[i] = 0;
+      sm100::named_bar_sync(3, 256);
+    }
+    float rpb_fx = 0.f;   // fixed-point scale of the dRPB window, from the previous tile's maximum (0: none yet)
     uint32_t n = 0, g = 0;
     for (int32_t kq = 0;; ++kq) {
       const int32_t u = unit_at(kq, ug);
@@ -294,14 +316,46 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int32_t kidx = kb * kBlock + row;
       RowBox box = clip_box<kTwoD>(prm.pat, col_box(prm.pat, kidx));
       if (kidx >= prm.N) box.len = 0;   // phantom key row of a ragged tile: nothing allowed
+      // RPB: this key row's cell, the key block's cell box, the head's table / gradient
+      int32_t k_r = 0, k_c = 0, k_b = 0;
+      CellBox kbox{0, 0, 0, 0};
+      const float* rpbh = nullptr;
+      float* drpbh = nullptr;
+      if (kBias) {
+        const int32_t rc = rpb_cell_rc(prm.cells, kidx, prm.N, prm.grid_w);
+        k_r = rc >> 16;
+        k_c = rc & 0xffff;
+        k_b = k_r * prm.rpb_w + k_c;
+        kbox = rpb_block_box(prm.cells, kb * kBlock, prm.N, prm.grid_w, lane);
+        rpbh = prm.rpb + (int64_t)h * prm.rpb_hw;
+        drpbh = prm.drpb + (int64_t)h * prm.rpb_hw;
+      }
       for (int t = 0; t < nt; ++t, ++g) {
         const int s = g & 1;
         const uint8_t kd = __ldg(prm.t_kind + rs + t);
         const int32_t q0 = __ldg(prm.t_col_idx + rs + t) * kBlock;
+        // RPB: the tile's offset box (dr, dc) = q box - key box and whether its rows fit
+        // the shared-memory dRPB window (query offsets A_q come staged with LSE / D)
+        int32_t dr0 = 0, dc0 = 0, wc = 0, wrows = 0, wcols = 0, kwb = 0;
+        bool win = false;
+        if (kBias) {
+          const CellBox qbox = rpb_block_box(prm.cells, q0, prm.N, prm.grid_w, lane);
+          dr0 = qbox.r0 - kbox.r1;
+          dc0 = qbox.c0 - kbox.c1;
+          // window = the box's offset rows at the table's own row stride, so that the element
+          // index (dr - dr0) * wc + (dc - dc0) = A_q - kwb (A_q staged per q-block)
+          wc = prm.rpb_w;
+          wrows = qbox.r1 - kbox.r0 - dr0 + 1;
+          wcols = qbox.c1 - kbox.c0 - dc0 + 1;   // offset columns actually used (<= wc)
+          win = wrows * wc <= rpb_win_cap<D>();
+          kwb = (prm.grid_h - 1) * prm.rpb_w + prm.grid_w - 1 + k_b + dr0 * wc + dc0;
+        }
         sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1);
         const uint32_t lse2 = sm100::smem_u32(sm.lse[s]);
         const uint32_t dd = sm100::smem_u32(sm.dd[s]);
+        const uint32_t qa = sm100::smem_u32(sm.qa[s]);
         const uint32_t dsbuf = sm100::smem_u32(sm.ds[g & 1]);
+        float tmax = 0.f;   // kBias: largest |dL/dscore| of the tile (this thread)
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
           sm100::mbar_wait(&sm.s_full[half], g & 1);
@@ -317,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // one interval); the other groups are all masked, their exponentials skipped
             // (warp-uniform) and P = 0 there.  Full tiles / 2D patterns: all 4 groups.
             int ulo = 0, uhi = 4;
-            if (kd == 2 && !kTwoD) {
+            if (!kBias && kd == 2 && !kTwoD) {   // (with the RPB gather the branchy loop measured slower: cfg5 +6%)
               const int32_t base = q0 + c * 32;
               const int32_t lo = min(max(box.lo - base, 0), 32), hi = min(max(box.lo + box.len - base, 0), 32);
               const bool any = hi > lo;
@@ -336,9 +390,19 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int qc = c * 32 + u4 * 8;
               const float4 la = sm100::lds_f4(lse2 + qc * 4), lb = sm100::lds_f4(lse2 + qc * 4 + 16);
               const float lv[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
+              int32_t av[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+              if (kBias) {
+                const float4 xa = sm100::lds_f4(qa + qc * 4), xb = sm100::lds_f4(qa + qc * 4 + 16);
+                av[0] = __float_as_int(xa.x); av[1] = __float_as_int(xa.y); av[2] = __float_as_int(xa.z);
+                av[3] = __float_as_int(xa.w); av[4] = __float_as_int(xb.x); av[5] = __float_as_int(xb.y);
+                av[6] = __float_as_int(xb.z); av[7] = __float_as_int(xb.w);
+              }
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
-                p[u4 * 8 + e] = sm100::ex2(fmaf(__uint_as_float(sr[u4 * 8 + e]), sl2, -lv[e]));
+                float x = fmaf(__uint_as_float(sr[u4 * 8 + e]), sl2, -lv[e]);
+                if (kBias)   // + bias * log2(e), bias = table[h][dr + H - 1][dc + W - 1] = table[A_q - B_k]
+                  x = fmaf(__ldg(rpbh + (av[e] - k_b)), 1.4426950408889634f, x);
+                p[u4 * 8 + e] = sm100::ex2(x);
               }
             }
             uint32_t okbits = 0xffffffffu;   // element mask of this chunk (partial tiles only)
@@ -379,6 +443,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // masked: exactly 0 (the D / LSE of phantom query columns may be stale, 0 * NaN = NaN)
                 if (!((okbits >> (u4 * 8 + e)) & 1u)) ds[e] = 0.f;
               }
+              if (kBias) {
+                // dRPB[offset] += dL/dscore = dS / scale: into the tile's shared-memory
+                // offset window (flushed once per tile), else straight to global
+                const float4 xa = sm100::lds_f4(qa + qc * 4), xb = sm100::lds_f4(qa + qc * 4 + 16);
+                const int32_t av[8] = {__float_as_int(xa.x), __float_as_int(xa.y), __float_as_int(xa.z),
+                                       __float_as_int(xa.w), __float_as_int(xb.x), __float_as_int(xb.y),
+                                       __float_as_int(xb.z), __float_as_int(xb.w)};
+                const uint32_t wbase = sm100::smem_u32(sm.rpb_win);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  if (!((okbits >> (u4 * 8 + e)) & 1u)) continue;
+                  const float gv = ds[e] * prm.inv_scale;
+                  tmax = fmaxf(tmax, fabsf(gv));
+                  const float sv = gv * rpb_fx;
+                  // window index (dr - dr0) * (2W - 1) + (dc - dc0) = A_q - kwb; a CTA's first tile
+                  // (no scale yet: rpb_fx == 0) and out-of-range addends take the global path
+                  if (win && rpb_fx > 0.f && fabsf(sv) < kRpbFixMax) {
+                    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(wbase + 4u * (uint32_t)(av[e] - kwb)),
+                                 "r"(__float2int_rn(sv))
+                                 : "memory");
+                  } else {     // table index A_q - B_k (no window, or outside the fixed-point range)
+                    atomicAdd(drpbh + (av[e] - k_b), gv);
+                  }
+                }
+              }
               // dS^T row -> smem [q/64][kv][64] with the 128B swizzle (16B chunks)
               const uint32_t off =
                   (uint32_t)(qc >> 6) * 16384u + sm100::swz128((uint32_t)row * 128u + (uint32_t)(qc & 63) * 2u);
@@ -390,6 +479,27 @@ __global__ void __launch_bounds__(kThreads, 1)
           sm100::fence_proxy_async_smem();
           sm100::tc_fence_before();
           sm100::mbar_arrive(&sm.ds_ready[half]);
+        }
+        if (kBias && win) {
+          // flush the tile's dRPB window to global (and re-zero it) -- all 256 compute threads;
+          // the tile's largest |dL/dscore| sets the fixed-point scale of the NEXT tile (no
+          // extra barrier; elements beyond that scale's range go to global fp32 atomics)
+          const uint32_t wm = __reduce_max_sync(0xffffffffu, __float_as_uint(tmax));   // non-negative floats
+          if (lane == 0) sm.rpb_wmax[g & 1][warp - 2] = __uint_as_float(wm);
+          sm100::named_bar_sync(3, 256);
+          const float inv_fx = rpb_fx > 0.f ? 1.f / rpb_fx : 0.f;   // (nothing accumulated without a scale)
+          const int tid = (warp - 2) * 32 + lane;
+          for (int i = tid; i < wrows * wcols; i += 256) {   // only the box's used columns
+            const int32_t ir = i / wcols, ic = i - ir * wcols;
+            const int32_t v = sm.rpb_win[ir * wc + ic];
+            if (v != 0) {
+              atomicAdd(drpbh + (dr0 + ir + prm.grid_h - 1) * prm.rpb_w + (dc0 + ic + prm.grid_w - 1),
+                        (float)v * inv_fx);
+              sm.rpb_win[ir * wc + ic] = 0;
+            }
+          }
+          rpb_fx = rpb_next_scale(sm.rpb_wmax[g & 1], rpb_fx);   // (stays 0 only for an all-zero tile)
+          sm100::named_bar_sync(3, 256);
         }
       }
       tiles_done += nt;
@@ -525,12 +635,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 
-template <int D, bool kTwoD, bool kGather>
+template <int D, bool kTwoD, bool kGather, bool kBias>
 hla_status launch_split_t(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                           const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm, int32_t n_kblocks,
                           cudaStream_t stream) {
-  const size_t smem = sizeof(SplitSmem<D>) + 1024;
-  auto* fn = attn_bwd_split_kernel<D, kTwoD, kGather>;
+  const size_t smem = sizeof(SplitSmem<D, kBias>) + 1024;
+  auto* fn = attn_bwd_split_kernel<D, kTwoD, kGather, kBias>;
   HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t pairs = (int64_t)((n_kblocks + 1) / 2) * prm.heads * prm.batch;   // work units (kv-block pairs)
   const int grid = (int)std::min<int64_t>(pairs, (int64_t)num_sms());
@@ -539,21 +649,29 @@ hla_status launch_split_t(const CUtensorMap& mq, const CUtensorMap& mk, const CU
   return HLA_OK;
 }
 
-static_assert(sizeof(SplitSmem<64>) + 1024 <= 227 * 1024, "split bwd shared memory exceeds 227 KB");
+static_assert(sizeof(SplitSmem<64, true>) + 1024 <= 227 * 1024, "split bwd shared memory exceeds 227 KB");
+
+template <bool kBias>
+hla_status dispatch_split(int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
+                          const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm,
+                          int32_t n_kblocks, cudaStream_t stream) {
+  if (head_dim == 64) {
+    if (gather) return launch_split_t<64, false, true, kBias>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
+    return two_d ? launch_split_t<64, true, false, kBias>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream)
+                 : launch_split_t<64, false, false, kBias>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
+  }
+  if (gather) return launch_split_t<32, false, true, kBias>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
+  return two_d ? launch_split_t<32, true, false, kBias>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream)
+               : launch_split_t<32, false, false, kBias>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
+}
 
 }  // namespace
 
-hla_status launch_split(int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
+hla_status launch_split(bool bias, int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
                         const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm,
                         int32_t n_kblocks, cudaStream_t stream) {
-  if (head_dim == 64) {
-    if (gather) return launch_split_t<64, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
-    return two_d ? launch_split_t<64, true, false>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream)
-                 : launch_split_t<64, false, false>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
-  }
-  if (gather) return launch_split_t<32, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
-  return two_d ? launch_split_t<32, true, false>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream)
-               : launch_split_t<32, false, false>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
+  return bias ? dispatch_split<true>(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, n_kblocks, stream)
+              : dispatch_split<false>(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
 }
 
 }  // namespace bwd
