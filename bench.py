@@ -47,11 +47,11 @@ CONFIGS = {
     "cfg1": dict(kind="HWA", rm="WSA", grid=16, win=8, B=1, H=1, d=32,
                  text="16x16 grid, HWA 64 tokens vs WSA 8x8, 1 head, d32, batch 1"),
     "cfg2": dict(kind="HWA", rm="WSA", grid=64, win=16, B=16, H=8, d=64,
-                 text="64x64 grid, HWA 256 tokens vs WSA 16x16, 8 heads, d64, block 128, batch 16"),
+                 text="64x64 grid, HWA 256 tokens vs WSA 16x16, 8 heads, d64, batch 16"),
     "cfg3": dict(kind="HSA", rm="SA", grid=64, win=16, B=16, H=8, d=64,
-                 text="64x64 grid, HSA 256 tokens vs SA 16x16, 8 heads, d64, block 128, batch 16"),
+                 text="64x64 grid, HSA 256 tokens vs SA 16x16, 8 heads, d64, batch 16"),
     "cfg4": dict(kind="HNA", rm="NA2D", grid=128, win=7, B=16, H=12, d=64,
-                 text="128x128 grid, HNA 49 tokens vs NA2D 7x7, 12 heads, d64, block 128, batch 16"),
+                 text="128x128 grid, HNA 49 tokens vs NA2D 7x7, 12 heads, d64, batch 16"),
 }
 # attention stacks of a Hilbert Window Transformer (HWT-T: Swin-T stage shapes)
 #   cfg5     BASELINE.json configs[4] as stated: 56/28/14/7 grids padded to the Hilbert grid
@@ -61,16 +61,16 @@ CONFIGS = {
 #            generalized Hilbert curve (ragged N; 7x7 -> 8x8 padded: the kernels need N % 4 == 0),
 #            49-token windows, HWA / HSWA alternating (shift = half a window), global RPB
 STACK = {
-    "cfg5": dict(B=128, d=32, block=128, hswa=False, rpb=False,
+    "cfg5": dict(B=128, d=32, block=64, hswa=False, rpb=False,
                  stages=[(64, 3, 2, 8), (32, 6, 2, 8), (16, 12, 6, 8), (8, 24, 2, 8)],
                  text="HWT-T attention stack as BASELINE states it: 56x56/28x28/14x14/7x7 padded to "
                       "64x64/32x32/16x16/8x8 Hilbert grids, windows 49->64 tokens (8x8), heads 3/6/12/24, "
-                      "depths 2/2/6/2, all HWA, B128, d32, block 128"),
+                      "depths 2/2/6/2, all HWA, B128, d32"),
     "cfg5-hwt": dict(B=128, d=32, block=128, hswa=True, rpb=True,
                      stages=[(56, 3, 2, 7), (28, 6, 2, 7), (14, 12, 6, 7), (8, 24, 2, 8)],
                      text="HWT-T attention stack: stages 56x56/28x28/14x14 (generalized Hilbert, ragged N) "
                           "and 7x7->8x8 padded, heads 3/6/12/24, depths 2/2/6/2, B128, d32, 49-token windows "
-                          "(64 at 8x8), HWA/HSWA alternating (shift = half a window), global RPB, block 128"),
+                          "(64 at 8x8), HWA/HSWA alternating (shift = half a window), global RPB"),
 }
 # paper's row-major-block-sparse -> Hilbert fwd+bwd speedup on the nearest shape (RTX 3080)
 PAPER_SPEEDUP = {"cfg2": (2.70, "WSA(Flex)->HWA 64x64 W8, P:L150-151"),
@@ -95,6 +95,8 @@ def parse(argv=None):
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--config", default="cfg2", choices=sorted(CONFIGS) + sorted(STACK))
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--block", type=int, default=None, choices=[64, 128],
+                   help="tile block b_q = b_k (default: the config's; SURVEY 8: 128, cfg5 64)")
     p.add_argument("--no-variants", action="store_true", help="skip the row-major / dense / RPB / unfused runs")
     p.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
     p.add_argument("--no-e2e", action="store_true")
@@ -405,6 +407,7 @@ def run_stack(args):
     import paper_2511_05832_b200 as hla
 
     sc = STACK[args.config]
+    blk = args.block or sc["block"]
     rank, world, local, dev, dist = _init_dist(args)
     B, d = sc["B"], sc["d"]
     if B % world:
@@ -415,7 +418,7 @@ def run_stack(args):
         N = g * g
         ins = hla_synth.attention_inputs_block(B, N, H, d, b0, b1, 0, H, seed=100 + si, device=dev)
         kinds = ("HWA", "HSWA") if sc["hswa"] else ("HWA",)
-        pair = [hla.HilbertLocalAttention(kind, g, g, w, w, b1 - b0, H, d, block=sc["block"],
+        pair = [hla.HilbertLocalAttention(kind, g, g, w, w, b1 - b0, H, d, block=blk,
                                           shift=(w * w) // 2 if kind == "HSWA" else 0, device=dev, rpb=sc["rpb"])
                 for kind in kinds]
         gen = torch.Generator().manual_seed(si)
@@ -455,7 +458,8 @@ def run_stack(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic: hla_synth splitmix64 uniform, unit variance, bf16 (no dataset)",
-            "config": {"workload": args.config + ": " + sc["text"], "global_batch": B, "layers": len(layers),
+            "config": {"workload": "%s: %s, block %d" % (args.config, sc["text"], blk), "global_batch": B,
+                       "layers": len(layers), "block": blk,
                        "parallelism": "batch shards: rank r runs batches [r B/%d, (r+1) B/%d), all heads" % (world, world),
                        "l2": "flushed between timed steps (%d MiB write, untimed)" % (L2_FLUSH_BYTES >> 20),
                        "timing": PAPER_TIMING},
@@ -478,6 +482,7 @@ def run_single(args):
     import paper_2511_05832_b200 as hla
 
     cfg = CONFIGS[args.config]
+    blk = args.block or 128
     rank, world, local, dev, dist = _init_dist(args)
     peaks = load_peaks()
     g, B, H, d, win = cfg["grid"], cfg["B"], cfg["H"], cfg["d"], cfg["win"]
@@ -493,9 +498,9 @@ def run_single(args):
     builds = []
     for _ in range(3):
         t0 = time.perf_counter()
-        hla.hla_build_block_mask(hla.pattern_desc(cfg["kind"], g, g, win, win), dev)
+        hla.hla_build_block_mask(hla.pattern_desc(cfg["kind"], g, g, win, win, block=blk), dev)
         builds.append((time.perf_counter() - t0) * 1e3)
-    layer = hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, Bs, Hs, d, device=dev)
+    layer = hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, Bs, Hs, d, block=blk, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     step = lambda mark, lay=layer: lay.step(q, k, v, do, mark)   # noqa: E731
 
@@ -513,7 +518,7 @@ def run_single(args):
     torch.cuda.synchronize()
     rk, rv, rbound = invariant_residuals(dk, dv, do)
 
-    tiles = layer.nnz * Bs * Hs
+    tiles = layer.tiles * Bs * Hs   # executed 128 x 128 tiles (block 64: windows)
     attn_ms = stages["fwd"] + stages["bwd_pre"] + stages["bwd"] + stages["bwd_fin"]
 
     # --- variants on this rank's shard (same kernels): row-major baseline, dense FA, HWT's
@@ -522,17 +527,17 @@ def run_single(args):
     if not args.no_variants:
         vsteps = max(3, min(args.steps, 10))
         for name, kind in (("row_major", cfg["rm"]), ("dense", "DENSE")):
-            lay = hla.HilbertLocalAttention(kind, g, g, win, win, Bs, Hs, d, device=dev)
+            lay = hla.HilbertLocalAttention(kind, g, g, win, win, Bs, Hs, d, block=blk, device=dev)
             st_fn = lambda mark, lay=lay: lay.step(q, k, v, do, mark)   # noqa: E731
             tot, _, _, _ = _timed(st_fn, vsteps, 2, flush, False, None, dist, world)
             _, st, _, _ = _timed(st_fn, vsteps, 1, flush, True, None, dist, world)
             a_ms = st["fwd"] + st["bwd_pre"] + st["bwd"] + st["bwd_fin"]
             variants[name] = {"pattern": kind, "ms_per_step": round(statistics.mean(tot), 4),
                               "fwd_ms": round(st["fwd"], 4), "bwd_ms": round(a_ms - st["fwd"], 4),
-                              "tiles_per_bh": lay.nnz,
-                              "tensor_pct_executed": tensor_pct(exec_flops(lay.nnz * Bs * Hs, d), a_ms, peaks["tf_sus"])}
+                              "tiles_per_bh": lay.tiles,
+                              "tensor_pct_executed": tensor_pct(exec_flops(lay.tiles * Bs * Hs, d), a_ms, peaks["tf_sus"])}
             del lay
-        lay = hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, Bs, Hs, d, device=dev, rpb=True)
+        lay = hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, Bs, Hs, d, block=blk, device=dev, rpb=True)
         lay.rpb = torch.rand(lay.rpb.shape, generator=torch.Generator().manual_seed(1)) * 2 - 1
         st_fn = lambda mark, lay=lay: lay.step(q, k, v, do, mark)   # noqa: E731
         tot, _, _, _ = _timed(st_fn, vsteps, 2, flush, False, None, dist, world)
@@ -542,7 +547,7 @@ def run_single(args):
                                   "bwd_ms": round(st["bwd_pre"] + st["bwd"] + st["bwd_fin"], 4)}
         del lay
         if layer.hilbert and (g & (g - 1)) == 0:
-            lay = hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, Bs, Hs, d, device=dev, fused=False)
+            lay = hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, Bs, Hs, d, block=blk, device=dev, fused=False)
             st_fn = lambda mark, lay=lay: lay.step(q, k, v, do, mark)   # noqa: E731
             tot, _, _, _ = _timed(st_fn, vsteps, 2, flush, False, None, dist, world)
             _, st, _, _ = _timed(st_fn, vsteps, 1, flush, True, None, dist, world)
@@ -569,7 +574,7 @@ def run_single(args):
     e2e = None
     if not args.no_e2e:
         hin = [x.cpu().pin_memory() for x in (q, k, v, do)]
-        layers = [layer, hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, Bs, Hs, d, device=dev)]
+        layers = [layer, hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, Bs, Hs, d, block=blk, device=dev)]
         din = [[torch.empty_like(x) for x in (q, k, v, do)] for _ in range(2)]
         hout = [[torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (q, q, q, q)] for _ in range(2)]
         s_in, s_out, s_cmp = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.current_stream(dev)
@@ -665,15 +670,16 @@ def run_single(args):
         "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": False,
         "scaling": "strong" if plan else "replicas", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic: hla_synth splitmix64 uniform, unit variance, bf16 (no dataset)",
-        "config": {"workload": args.config + ": " + cfg["text"], "global_batch": B, "seq_len": N,
+        "config": {"workload": "%s: %s, block %d" % (args.config, cfg["text"], blk),
+                   "global_batch": B, "seq_len": N, "block": blk,
                    "parallelism": ("batch x head shards over %d ranks (plan_shards), no collective on the hot path"
                                    % world) if plan else "replicas (no batch x head partition for %d ranks)" % world,
                    "l2": "flushed between timed steps (%d MiB write, untimed); warm_l2_ms without the flush"
                          % (L2_FLUSH_BYTES >> 20),
                    "step": ("fwd+bwd_pre+bwd+bwd_fin (Hilbert reorder fused into the kernels)" if layer.fused else
                             "fwd+bwd_pre+bwd+bwd_fin"),
-                   "mask": "built once before timing (%d of %d tiles per (b,h) executed)"
-                           % (layer.nnz, ((N + 127) // 128) ** 2),
+                   "mask": "built once before timing: %d of %d block-%d tiles per (b,h) non-empty, %d 128 x 128 "
+                           "tiles executed" % (layer.nnz, ((N + blk - 1) // blk) ** 2, blk, layer.tiles),
                    "timing": "CUDA events: one start/end pair per step (value = mean, max over ranks); "
                              "breakdown_ms = per-launch medians from a second run with one event after every "
                              "launch; " + PAPER_TIMING},

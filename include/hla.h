@@ -125,6 +125,21 @@ typedef struct {
      schedule when n_full >= n_partial, the half-tile schedule otherwise (all zero,
      e.g. a mask not built by the library: half-tile).  The choice changes speed only. */
   int64_t host_counts[4];
+  /* Attention tiling of a block-64 mask (hla_build_tile_lists; unused at block 128).  The
+     kernels run 128 x 128 MMA tiles at 64-granular offsets: each 128-row tile (64-q-blocks
+     2t, 2t+1) walks the union of the two blocks' kv lists cut into 128-key windows that
+     start on any 64-block, so the columns it executes follow the block-64 sparsity (P:L85,
+     tab:blocksize P:L172-190).  Forward lists per 128-q tile, transposed lists per 128-key
+     tile; window kind 1 = all four 64 x 64 sub-tiles full (no element mask), 2 = otherwise. */
+  int32_t* w_row_ptr;            /* [ceil(n_qblocks/2)+1]                             */
+  int32_t* w_col;                /* [w_capacity] first kv 64-block of each window      */
+  uint8_t* w_kind;               /* [w_capacity]                                       */
+  int32_t* wt_row_ptr;           /* [ceil(n_kblocks/2)+1]                             */
+  int32_t* wt_col;               /* [w_capacity] first q 64-block of each window       */
+  uint8_t* wt_kind;              /* [w_capacity]                                       */
+  int64_t w_capacity;
+  int64_t w_counts[4];           /* host: windows, full windows (forward lists), same
+                                    for the transposed lists                          */
 } hla_block_mask;
 
 /* Bits of hla_block_mask.t_dq.  The backward walks the transposed lists in work
@@ -201,6 +216,18 @@ HLA_API hla_status hla_build_block_mask(const hla_pattern_desc* d, hla_block_mas
  */
 HLA_API hla_status hla_build_bwd_plan(hla_block_mask* m, cudaStream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * hla_build_tile_lists -- the window lists (w_*, wt_*) of a filled block-64 mask
+ * (block_q == block_k == 64, fill call of hla_build_block_mask done), needed by the
+ * attention calls at block 64.  Built on the host from the CSR lists (copied back),
+ * once per mask; synchronises `stream`.  Sizing call: m->w_col == NULL -> writes
+ * m->w_counts and the needed capacity to *n_out, nothing else.  Fill call: writes
+ * all six arrays and m->w_counts; HLA_ERR_CAPACITY (with *n_out) if w_capacity is
+ * too small.  Window formation (per 128-row tile, ascending): the first kv 64-block
+ * of the two q-blocks' union not yet covered starts a window covering it and the
+ * next 64-block; repeated until the union is covered (same for the transpose). */
+HLA_API hla_status hla_build_tile_lists(hla_block_mask* m, int64_t* n_out, cudaStream_t stream);
+
 /* Host helper: the two sparsity ratios of a built mask from its integer counts
  * (host copy of m->counts): empty_tile_ratio = n_empty / (Mq*Mk); sparsity =
  * 1 - nnz*b_q*b_k / N^2, the paper's "Sparsity" column (DESIGN.md
@@ -244,7 +271,9 @@ typedef struct {
  * [batch, heads, N].  scale <= 0 selects 1/sqrt(head_dim).
  * Limits: head_dim in {32, 64}; block_q == block_k in {64, 128}; N % 4 == 0 (a
  * ragged last tile is masked); mask built for the same descriptor
- * (n_qblocks == ceil(N / block)).
+ * (n_qblocks == ceil(N / block)); block 64 also needs the mask's window lists
+ * (hla_build_tile_lists).  tiles_visited counts executed 128 x 128 tiles (block
+ * 64: windows).
  * tiles_visited: optional device int64 counter; when non-NULL the kernel adds
  * the number of tiles it executed (must equal batch*heads*nnz: empty tiles are
  * skipped).

@@ -20,7 +20,8 @@ STATUS_NAMES = {0: "HLA_OK", 1: "HLA_ERR_INVALID", 2: "HLA_ERR_UNSUPPORTED", 3: 
 # exported symbols of include/hla.h (libhla.so) and include/hla_debug.h (libhla_debug.so)
 EXPORTED = ("hla_hilbert_index", "hla_hilbert_perm", "hla_build_block_mask", "hla_mask_ratios",
             "hla_attn_fwd", "hla_attn_bwd", "hla_attn_bwd_workspace", "hla_attn_bwd_preprocess",
-            "hla_attn_bwd_main", "hla_attn_bwd_finalize", "hla_build_bwd_plan", "hla_last_error", "hla_version")
+            "hla_attn_bwd_main", "hla_attn_bwd_finalize", "hla_build_bwd_plan", "hla_build_tile_lists",
+            "hla_last_error", "hla_version")
 DEBUG_EXPORTED = ("hla_debug_umma", "hla_debug_gather4", "hla_debug_mma_rate",
                   "hla_debug_tmem_rate", "hla_debug_ex2_rate", "hla_debug_xu_rate", "hla_debug_sync_latency",
                   "hla_debug_softmax_rate", "hla_debug_softmax_tile", "hla_debug_load_rate")
@@ -44,7 +45,10 @@ class BlockMaskC(ctypes.Structure):
                 ("t_row_ptr", ctypes.c_void_p), ("t_col_idx", ctypes.c_void_p), ("t_kind", ctypes.c_void_p),
                 ("counts", ctypes.c_void_p),
                 ("t_dq", ctypes.c_void_p), ("q_dq_local", ctypes.c_void_p), ("n_dq_nonlocal", ctypes.c_int32),
-                ("host_counts", ctypes.c_int64 * 4)]
+                ("host_counts", ctypes.c_int64 * 4),
+                ("w_row_ptr", ctypes.c_void_p), ("w_col", ctypes.c_void_p), ("w_kind", ctypes.c_void_p),
+                ("wt_row_ptr", ctypes.c_void_p), ("wt_col", ctypes.c_void_p), ("wt_kind", ctypes.c_void_p),
+                ("w_capacity", ctypes.c_int64), ("w_counts", ctypes.c_int64 * 4)]
 
 
 class HlaError(RuntimeError):
@@ -71,6 +75,7 @@ _SIG = {
                           _sz, _vp, _vp],
     "hla_attn_bwd_finalize": [_i32, _i32, _i32, _i32, _vp, _sz, _vp, _vp, _pmask, _vp],
     "hla_build_bwd_plan": [_pmask, _vp],
+    "hla_build_tile_lists": [_pmask, ctypes.POINTER(_i64), _vp],
 }
 _DEBUG_SIG = {
     "hla_debug_umma": [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp],

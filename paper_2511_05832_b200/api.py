@@ -60,14 +60,32 @@ class BlockMask:
     t_dq: torch.Tensor = None     # backward dQ plan (hla_build_bwd_plan): uint8 per transposed entry
     q_dq_local: torch.Tensor = None   # uint8 per q-block: 1 = dQ written by the main backward kernel
     n_dq_nonlocal: int = -1
+    # block 64: the attention kernels' window lists (hla_build_tile_lists)
+    w_row_ptr: torch.Tensor = None
+    w_col: torch.Tensor = None
+    w_kind: torch.Tensor = None
+    wt_row_ptr: torch.Tensor = None
+    wt_col: torch.Tensor = None
+    wt_kind: torch.Tensor = None
+    w_counts: tuple = (0, 0, 0, 0)
 
     @property
     def c(self):
         hc = (ctypes.c_int64 * 4)(*(self.host_counts or (0, 0, 0, 0)))
+        wc = (ctypes.c_int64 * 4)(*self.w_counts)
+        cap = self.w_col.numel() if self.w_col is not None else 0
         return BlockMaskC(self.row_ptr.numel() - 1, self.t_row_ptr.numel() - 1, self.col_idx.numel(),
                           self.row_ptr.data_ptr(), self.col_idx.data_ptr(), self.kind.data_ptr(),
                           self.t_row_ptr.data_ptr(), self.t_col_idx.data_ptr(), self.t_kind.data_ptr(),
-                          self.counts.data_ptr(), _dp(self.t_dq), _dp(self.q_dq_local), self.n_dq_nonlocal, hc)
+                          self.counts.data_ptr(), _dp(self.t_dq), _dp(self.q_dq_local), self.n_dq_nonlocal, hc,
+                          _dp(self.w_row_ptr), _dp(self.w_col), _dp(self.w_kind), _dp(self.wt_row_ptr),
+                          _dp(self.wt_col), _dp(self.wt_kind), cap, wc)
+
+    @property
+    def tiles(self):
+        """128 x 128 tiles the attention kernels execute per (b, h): the CSR entries at block
+        128, the forward windows at block 64."""
+        return self.w_counts[0] if self.w_col is not None else self.nnz
 
     @property
     def nnz(self):
@@ -141,9 +159,31 @@ def hla_build_block_mask(desc, device="cuda", stream=None, plan=True):
         check("hla_build_block_mask", lib().hla_build_block_mask(ctypes.byref(desc), ctypes.byref(c),
                                                                  ctypes.byref(nnz), _stream(stream, dev)))
     m.host_counts = tuple(int(x) for x in c.host_counts)   # written by the fill call
-    if plan and desc.block_q == desc.block_k:
+    if desc.block_q == desc.block_k == 64:
+        hla_build_tile_lists(m, stream)      # the attention kernels' windows (no dQ plan at block 64)
+    elif plan and desc.block_q == desc.block_k:
         hla_build_bwd_plan(m, stream)
     return m
+
+
+def hla_build_tile_lists(mask, stream=None):
+    """Window lists of a filled block-64 mask (synchronous; once per mask)."""
+    dev = mask.row_ptr.device
+    c = mask.c
+    n = ctypes.c_int64()
+    with torch.cuda.device(dev):
+        check("hla_build_tile_lists", lib().hla_build_tile_lists(ctypes.byref(c), ctypes.byref(n), _stream(stream, dev)))
+    i32 = dict(dtype=torch.int32, device=dev)
+    tq, tk = (mask.row_ptr.numel() - 1 + 1) // 2, (mask.t_row_ptr.numel() - 1 + 1) // 2
+    mask.w_row_ptr, mask.wt_row_ptr = torch.zeros(tq + 1, **i32), torch.zeros(tk + 1, **i32)
+    mask.w_col, mask.wt_col = torch.empty(n.value, **i32), torch.empty(n.value, **i32)
+    mask.w_kind = torch.empty(n.value, dtype=torch.uint8, device=dev)
+    mask.wt_kind = torch.empty(n.value, dtype=torch.uint8, device=dev)
+    c = mask.c
+    with torch.cuda.device(dev):
+        check("hla_build_tile_lists", lib().hla_build_tile_lists(ctypes.byref(c), ctypes.byref(n), _stream(stream, dev)))
+    mask.w_counts = tuple(int(x) for x in c.w_counts)
+    return mask
 
 
 def hla_build_bwd_plan(mask, stream=None):

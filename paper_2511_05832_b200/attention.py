@@ -89,10 +89,15 @@ class HilbertLocalAttention:
         """Gradient of the RPB table written by backward() (read-only binding)."""
         return self._drpb
 
-    # tiles executed per step, per (b, h): R (P:L102 r_i summed over q-blocks)
+    # non-empty tiles of the mask per (b, h): R (P:L102 r_i summed over q-blocks)
     @property
     def nnz(self):
         return self.mask.nnz
+
+    # 128 x 128 tiles the kernels execute per (b, h) and per pass (block 64: windows)
+    @property
+    def tiles(self):
+        return self.mask.tiles
 
     def forward(self, q, k, v, mark=None):
         """q, k, v: bf16 [B, N, heads, d] in grid (row-major cell) order -> o (grid order).

@@ -238,10 +238,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (kBias) {
               // A_q = (qr + H - 1)(2W - 1) + qc + W - 1 of the q-block's 128 columns (phantom: cell 0),
               // read by the compute warps as warp-uniform 16-B loads next to LSE / D
-              const int4 rc = make_int4(rpb_cell_rc(prm.cells, qblk * kBlock + 4 * lane, prm.N, prm.grid_w),
-                                        rpb_cell_rc(prm.cells, qblk * kBlock + 4 * lane + 1, prm.N, prm.grid_w),
-                                        rpb_cell_rc(prm.cells, qblk * kBlock + 4 * lane + 2, prm.N, prm.grid_w),
-                                        rpb_cell_rc(prm.cells, qblk * kBlock + 4 * lane + 3, prm.N, prm.grid_w));
+              const int4 rc = make_int4(rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane, prm.N, prm.grid_w),
+                                        rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane + 1, prm.N, prm.grid_w),
+                                        rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane + 2, prm.N, prm.grid_w),
+                                        rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane + 3, prm.N, prm.grid_w));
               const int32_t a0 = (prm.grid_h - 1) * prm.rpb_w + prm.grid_w - 1;
               auto a_of = [&](int32_t v) { return a0 + (v >> 16) * prm.rpb_w + (v & 0xffff); };
               sm100::sts_u4(sm100::smem_u32(sm.qa[s]) + 16u * lane, a_of(rc.x), a_of(rc.y), a_of(rc.z), a_of(rc.w));
@@ -251,10 +251,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               sm100::mbar_arrive(&sm.q_full[s]);
             } else if (lane == 0) {
               // LSE / D of the real rows only (ragged last tile: N % 4 == 0, so 16-B multiples)
-              const uint32_t vbytes = (uint32_t)min(kBlock, prm.N - qblk * kBlock) * 4u;
+              const uint32_t vbytes = (uint32_t)min(kBlock, prm.N - qblk * prm.col_mul) * 4u;
               sm100::mbar_arrive_expect_tx(&sm.q_full[s], 2 * vbytes);
-              sm100::bulk_load(sm.lse[s], prm.lse2 + bh * prm.N + qblk * kBlock, vbytes, &sm.q_full[s]);
-              sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * kBlock, vbytes, &sm.q_full[s]);
+              sm100::bulk_load(sm.lse[s], prm.lse2 + bh * prm.N + qblk * prm.col_mul, vbytes, &sm.q_full[s]);
+              sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * prm.col_mul, vbytes, &sm.q_full[s]);
             }
           } else if (kVar & 4) {
             if (lane == 0) sm100::mbar_arrive(&sm.q_full[s]);
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.q_full[s], kTile);
             __syncwarp();
             load_rows<D, kGather>(role == 1 ? sm.q[s] : sm.dO[s], role == 1 ? &tmQ : &tmDO, &sm.q_full[s], h, b,
-                                  prm.N, qblk * kBlock, prm.s2c, pol_q, lane);
+                                  prm.N, qblk * prm.col_mul, prm.s2c, pol_q, lane);
           }
         }
         ++n;
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       for (int t = 0; t < nt; ++t, ++g) {
         const uint8_t kd = __ldg(prm.t_kind + rs + t);
-        const int32_t q0 = __ldg(prm.t_col_idx + rs + t) * kBlock;
+        const int32_t q0 = __ldg(prm.t_col_idx + rs + t) * prm.col_mul;
         const int s = g & 1;
         // RPB: the tile's offset box (dr, dc) = q box - key box and whether its rows fit
         // the shared-memory dRPB window (query offsets A_q come staged with LSE / D)
@@ -696,13 +696,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         const int32_t qblk = __ldg(prm.t_col_idx + rs + t);
-        const int32_t qrow = b * prm.N + qblk * kBlock;   // sequence order
+        const int32_t qrow = b * prm.N + qblk * prm.col_mul;   // sequence order
         const bool local = (fdq & HLA_DQ_LOCAL) != 0;
         // complete dQ_i (LOCAL; dS carries the softmax scale): bf16 rows straight to dq, to the
         // grid cell under the fused reorder; phantom rows of a ragged tile write nothing
         uint4* dqp = nullptr;
-        if (local && qblk * kBlock + row < prm.N) {
-          const int32_t qs = qblk * kBlock + row;
+        if (local && qblk * prm.col_mul + row < prm.N) {
+          const int32_t qs = qblk * prm.col_mul + row;
           const int32_t qcell = kGather ? __ldg(prm.s2c + qs) : qs;
           dqp = reinterpret_cast<uint4*>(prm.dq + (((int64_t)b * prm.N + qcell) * prm.heads + h) * D);
         }
@@ -1050,9 +1050,10 @@ hla_status prepare_main(const hla_pattern_desc* d, const hla_block_mask* m, int3
                         const hla_score_mod* score_mod, void* workspace, size_t workspace_bytes,
                         int64_t* tiles_visited, MainPlan* pl) {
   Pattern pat;
-  hla_status st = check_attn_args(d, m, batch, heads, head_dim, &pat);
+  AttnLists lists;
+  hla_status st = check_attn_args(d, m, batch, heads, head_dim, &pat, &lists);
   if (st != HLA_OK) return st;
-  HLA_REQUIRE(m->t_row_ptr && m->t_col_idx && m->t_kind, HLA_ERR_INVALID, "transposed mask arrays missing");
+  HLA_REQUIRE(lists.t_row_ptr && lists.t_col && lists.t_kind, HLA_ERR_INVALID, "transposed mask arrays missing");
   HLA_REQUIRE(q && k && v && dout && dk && dv, HLA_ERR_INVALID, "null pointer");
   HLA_REQUIRE(dq || !plan_of(m, pat.N), HLA_ERR_INVALID, "dq required: the mask's dQ plan writes local q-blocks");
   HLA_REQUIRE(((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)dout | (uintptr_t)dk | (uintptr_t)dv |
@@ -1069,9 +1070,10 @@ hla_status prepare_main(const hla_pattern_desc* d, const hla_block_mask* m, int3
   prm.batch = batch;
   prm.scale = sc;
   prm.scale_log2 = sc * kLog2e;
-  prm.t_row_ptr = m->t_row_ptr;
-  prm.t_col_idx = m->t_col_idx;
-  prm.t_kind = m->t_kind;
+  prm.t_row_ptr = lists.t_row_ptr;
+  prm.t_col_idx = lists.t_col;
+  prm.t_kind = lists.t_kind;
+  prm.col_mul = lists.col_mul;
   prm.t_dq = plan_of(m, pat.N) ? m->t_dq : nullptr;
   prm.dq = reinterpret_cast<__nv_bfloat16*>(dq);
   prm.lse2 = lse2;
@@ -1109,7 +1111,7 @@ hla_status prepare_main(const hla_pattern_desc* d, const hla_block_mask* m, int3
   // schedule: full-tile (attn_bwd_full_kernel) when full tiles are at least half of the
   // mask's tiles; half-tile (attn_bwd_split_kernel) otherwise (the split
   // schedule overlaps the partial tiles' masked compute better)
-  pl->full = m->host_counts[1] >= m->host_counts[2] && m->host_counts[1] > 0;
+  pl->full = lists.t_n_full >= lists.t_n_partial && lists.t_n_full > 0;
   return HLA_OK;
 }
 

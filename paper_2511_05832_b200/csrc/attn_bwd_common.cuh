@@ -17,9 +17,10 @@ struct BwdParams {
   Pattern pat;
   int32_t N, heads, batch;
   float scale, scale_log2, inv_scale;
-  const int32_t* t_row_ptr;
+  const int32_t* t_row_ptr;   // tile lists (AttnLists): per 128-key tile
   const int32_t* t_col_idx;
   const uint8_t* t_kind;
+  int32_t col_mul;            // start row of a list entry = column * col_mul (128, or 64: windows)
   const uint8_t* t_dq;     // dQ chaining plan per transposed entry (HLA_DQ_*; null = one chain per tile)
   const float* lse2;       // LSE * log2(e), [B, H, N] (workspace, from the preprocess)
   const float* dsum;       // D * scale, [B, H, N] (workspace, from the preprocess)

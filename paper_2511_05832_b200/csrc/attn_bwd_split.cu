@@ -155,10 +155,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (kBias) {
               // A_q = (qr + H - 1)(2W - 1) + qc + W - 1 of the q-block's 128 columns (phantom: cell 0),
               // read by the compute warps as warp-uniform 16-B loads next to LSE / D
-              const int4 rc = make_int4(rpb_cell_rc(prm.cells, qblk * kBlock + 4 * lane, prm.N, prm.grid_w),
-                                        rpb_cell_rc(prm.cells, qblk * kBlock + 4 * lane + 1, prm.N, prm.grid_w),
-                                        rpb_cell_rc(prm.cells, qblk * kBlock + 4 * lane + 2, prm.N, prm.grid_w),
-                                        rpb_cell_rc(prm.cells, qblk * kBlock + 4 * lane + 3, prm.N, prm.grid_w));
+              const int4 rc = make_int4(rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane, prm.N, prm.grid_w),
+                                        rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane + 1, prm.N, prm.grid_w),
+                                        rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane + 2, prm.N, prm.grid_w),
+                                        rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane + 3, prm.N, prm.grid_w));
               const int32_t a0 = (prm.grid_h - 1) * prm.rpb_w + prm.grid_w - 1;
               auto a_of = [&](int32_t v) { return a0 + (v >> 16) * prm.rpb_w + (v & 0xffff); };
               sm100::sts_u4(sm100::smem_u32(sm.qa[s]) + 16u * lane, a_of(rc.x), a_of(rc.y), a_of(rc.z), a_of(rc.w));
@@ -168,10 +168,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               sm100::mbar_arrive(&sm.q_full[s]);
             } else if (lane == 0) {
               // LSE / D of the real rows only (ragged last tile: N % 4 == 0, so 16-B multiples)
-              const uint32_t vbytes = (uint32_t)min(kBlock, prm.N - qblk * kBlock) * 4u;
+              const uint32_t vbytes = (uint32_t)min(kBlock, prm.N - qblk * prm.col_mul) * 4u;
               sm100::mbar_arrive_expect_tx(&sm.q_full[s], 2 * vbytes);
-              sm100::bulk_load(sm.lse[s], prm.lse2 + bh * prm.N + qblk * kBlock, vbytes, &sm.q_full[s]);
-              sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * kBlock, vbytes, &sm.q_full[s]);
+              sm100::bulk_load(sm.lse[s], prm.lse2 + bh * prm.N + qblk * prm.col_mul, vbytes, &sm.q_full[s]);
+              sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * prm.col_mul, vbytes, &sm.q_full[s]);
             }
           } else if (kVar & 4) {
             if (lane == 0) sm100::mbar_arrive(&sm.q_full[s]);
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.q_full[s], kTile);
             __syncwarp();
             load_rows<D, kGather>(role == 1 ? sm.q[s] : sm.dO[s], role == 1 ? &tmQ : &tmDO, &sm.q_full[s], h, b,
-                                  prm.N, qblk * kBlock, prm.s2c, pol_q, lane);
+                                  prm.N, qblk * prm.col_mul, prm.s2c, pol_q, lane);
           }
         }
         ++n;
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = 0; t < nt; ++t, ++g) {
         const int s = g & 1;
         const uint8_t kd = __ldg(prm.t_kind + rs + t);
-        const int32_t q0 = __ldg(prm.t_col_idx + rs + t) * kBlock;
+        const int32_t q0 = __ldg(prm.t_col_idx + rs + t) * prm.col_mul;
         // RPB: the tile's offset box (dr, dc) = q box - key box and whether its rows fit
         // the shared-memory dRPB window (query offsets A_q come staged with LSE / D)
         int32_t dr0 = 0, dc0 = 0, wc = 0, wrows = 0, wcols = 0, kwb = 0;
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         const int32_t qblk = __ldg(prm.t_col_idx + rs + t);
-        const int32_t qrow = b * prm.N + qblk * kBlock;   // sequence order
+        const int32_t qrow = b * prm.N + qblk * prm.col_mul;   // sequence order
         uint32_t r[D];
 #pragma unroll
         for (int c = 0; c < D / 32; ++c)
@@ -544,7 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (fdq & HLA_DQ_LOCAL) {
           // complete dQ_i (dS carries the softmax scale): bf16 rows straight to dq, to the
           // grid cell under the fused reorder; phantom rows of a ragged tile write nothing
-          const int32_t qs = qblk * kBlock + row;
+          const int32_t qs = qblk * prm.col_mul + row;
           if (qs < prm.N) {
             const int32_t qcell = kGather ? __ldg(prm.s2c + qs) : qs;
             uint4* dqp = reinterpret_cast<uint4*>(prm.dq + (((int64_t)b * prm.N + qcell) * prm.heads + h) * D);

@@ -41,9 +41,10 @@ struct FwdParams {
   Pattern pat;
   int32_t N, heads, batch;
   float scale_log2;
-  const int32_t* row_ptr;
+  const int32_t* row_ptr;    // tile lists (AttnLists): per 128-row q tile
   const int32_t* col_idx;
   const uint8_t* kind;
+  int32_t col_mul;           // start row of a list entry = column * col_mul (128, or 64: windows)
   const int32_t* s2c;        // fused reorder: seq_to_cell table (tensors in grid order), else null
   const float* rpb;          // global RPB table [heads][2H-1][2W-1] (kBias), else null
   const int32_t* cells;      // grid cell of each sequence position for the RPB offsets (null: identity)
@@ -330,9 +331,9 @@ __global__ void __launch_bounds__(kThreads, 2)
             const int s = g & 1;
             uint64_t* full = is_k ? &sm.k_full[s] : &sm.v_full[s];
             const int32_t kvb = tile_meta(meta, prm.col_idx, prm.kind, it.rs, t) >> 2;
-            const int64_t tag = bh * mq + kvb;
+            const int64_t tag = bh * prm.N + kvb;
             const bool reuse = tag == (s ? tag1 : tag0);   // stage already holds this K/V tile
-            const int4 cells = reuse ? make_int4(0, 0, 0, 0) : row_cells<kGather>(prm.N, kvb * kBlock, prm.s2c, lane);
+            const int4 cells = reuse ? make_int4(0, 0, 0, 0) : row_cells<kGather>(prm.N, kvb * prm.col_mul, prm.s2c, lane);
             if (g >= 2) sm100::mbar_wait(&sm.kv_empty[s], ((g >> 1) - 1) & 1);
             if (reuse) {
               if (lane == 0) sm100::mbar_arrive(full);
@@ -340,14 +341,14 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             if (s) tag1 = tag; else tag0 = tag;
             if (kBias && is_k) {
-              const int4 bk = rpb_key_offs(prm.cells, kvb * kBlock, prm.N, prm.grid_w, prm.rpb_w, lane);
+              const int4 bk = rpb_key_offs(prm.cells, kvb * prm.col_mul, prm.N, prm.grid_w, prm.rpb_w, lane);
               sm100::sts_u4(sm100::smem_u32(sm.key_b[s]) + 16u * lane, bk.x, bk.y, bk.z, bk.w);
               __syncwarp();   // every lane's offsets are written before lane 0 arms k_full
             }
             if (lane == 0) sm100::mbar_arrive_expect_tx(full, FwdSmem<D, kBias>::kTileBytes);
             __syncwarp();
-            issue_rows<D, kGather>(is_k ? sm.k[s] : sm.v[s], is_k ? &tmK : &tmV, full, h, b, prm.N, kvb * kBlock,
-                                   cells, pol_kv, lane);
+            issue_rows<D, kGather>(is_k ? sm.k[s] : sm.v[s], is_k ? &tmK : &tmV, full, h, b, prm.N,
+                                   kvb * prm.col_mul, cells, pol_kv, lane);
           }
         }
         it.t = it.nt - 1;
@@ -483,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, 2)
               s[4 * c4 + j] = fmaf(s[4 * c4 + j], sl2, __ldg(rpbh + (a_q - ov[j])) * 1.4426950408889634f);
           }
         }
-        if ((tm & 3) == 2) apply_row_mask<kTwoD>(s, prm.pat, box, (tm >> 2) * kBlock);
+        if ((tm & 3) == 2) apply_row_mask<kTwoD>(s, prm.pat, box, (tm >> 2) * prm.col_mul);
         // row max with 8 independent chains (a single dependent chain costs ~4 cycles x 128)
         float m8[8];
 #pragma unroll
@@ -631,19 +632,29 @@ hla_status dispatch_fwd(int head_dim, bool gather, bool two_d, const CUtensorMap
 
 // shared argument validation of forward and backward (declared in attn_common.cuh)
 hla_status check_attn_args(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
-                           int32_t head_dim, Pattern* pat) {
+                           int32_t head_dim, Pattern* pat, AttnLists* L) {
   hla_status st = make_pattern(d, pat);
   if (st != HLA_OK) return st;
   HLA_REQUIRE(m != nullptr && m->row_ptr && m->col_idx && m->kind, HLA_ERR_INVALID, "mask arrays missing");
   HLA_REQUIRE(head_dim == 32 || head_dim == 64, HLA_ERR_UNSUPPORTED, "head_dim %d not in {32, 64}", head_dim);
-  HLA_REQUIRE(d->block_q == kBlock && d->block_k == kBlock, HLA_ERR_UNSUPPORTED,
-              "attention needs block_q == block_k == 128 (got %d, %d)", d->block_q, d->block_k);
+  HLA_REQUIRE(d->block_q == d->block_k && (d->block_q == 128 || d->block_q == 64), HLA_ERR_UNSUPPORTED,
+              "attention needs block_q == block_k in {64, 128} (got %d, %d)", d->block_q, d->block_k);
   HLA_REQUIRE(pat->N % 4 == 0, HLA_ERR_UNSUPPORTED, "N=%d not a multiple of 4", pat->N);
-  const int32_t nb = (pat->N + kBlock - 1) / kBlock;   // ragged last block: phantom rows masked / not written
+  const int32_t b = d->block_q;
+  const int32_t nb = (pat->N + b - 1) / b;   // ragged last block: phantom rows masked / not written
   HLA_REQUIRE(m->n_qblocks == nb && m->n_kblocks == nb, HLA_ERR_INVALID,
               "mask built for a different N / block");
   HLA_REQUIRE(batch >= 1 && batch <= 65535 && heads >= 1 && heads <= 65535, HLA_ERR_INVALID,
               "batch %d / heads %d out of range", batch, heads);
+  if (b == 128) {
+    *L = AttnLists{m->row_ptr, m->col_idx, m->kind, m->t_row_ptr, m->t_col_idx, m->t_kind, 128,
+                   m->host_counts[1], m->host_counts[2], m->host_counts[1], m->host_counts[2]};
+  } else {
+    HLA_REQUIRE(m->w_row_ptr && m->w_col && m->w_kind && m->wt_row_ptr && m->wt_col && m->wt_kind, HLA_ERR_INVALID,
+                "block 64 needs the mask's window lists (hla_build_tile_lists)");
+    *L = AttnLists{m->w_row_ptr, m->w_col, m->w_kind, m->wt_row_ptr, m->wt_col, m->wt_kind, 64,
+                   m->w_counts[1], m->w_counts[0] - m->w_counts[1], m->w_counts[3], m->w_counts[2] - m->w_counts[3]};
+  }
   return HLA_OK;
 }
 
@@ -675,7 +686,8 @@ extern "C" hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_ma
                                    const hla_score_mod* score_mod, int64_t* tiles_visited, cudaStream_t stream) {
   clear_error();
   Pattern pat;
-  hla_status st = check_attn_args(d, m, batch, heads, head_dim, &pat);
+  AttnLists lists;
+  hla_status st = check_attn_args(d, m, batch, heads, head_dim, &pat, &lists);
   if (st != HLA_OK) return st;
   HLA_REQUIRE(q && k && v && o && lse, HLA_ERR_INVALID, "null tensor pointer");
   HLA_REQUIRE((((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)o) & 15) == 0, HLA_ERR_INVALID,
@@ -687,9 +699,10 @@ extern "C" hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_ma
   prm.heads = heads;
   prm.batch = batch;
   prm.scale_log2 = sc * 1.4426950408889634f;
-  prm.row_ptr = m->row_ptr;
-  prm.col_idx = m->col_idx;
-  prm.kind = m->kind;
+  prm.row_ptr = lists.row_ptr;
+  prm.col_idx = lists.col;
+  prm.kind = lists.kind;
+  prm.col_mul = lists.col_mul;
   prm.o = reinterpret_cast<__nv_bfloat16*>(o);
   prm.lse = lse;
   prm.s2c = seq_to_cell;

@@ -10,6 +10,7 @@
 // or compacted in ascending order (fill pass).  The library owns no scratch
 // memory, so lines are re-classified in each pass (not on the per-step path;
 // built once per shape like the cached Hilbert path).
+#include <algorithm>
 #include <vector>
 
 #include "predicates.cuh"
@@ -250,6 +251,98 @@ extern "C" hla_status hla_build_bwd_plan(hla_block_mask* m, cudaStream_t stream)
   int32_t n = 0;
   for (uint8_t x : loc) n += x ? 0 : 1;
   m->n_dq_nonlocal = n;
+  return HLA_OK;
+}
+
+namespace {
+
+// Windows of one 128-row tile from the CSR rows r0 (and r1 if it exists) of a block-64
+// mask: `cols` / `kinds` per row; the union is cut into windows (u, u + 1) from its
+// smallest uncovered element upward.  Kind 1 iff all four 64 x 64 sub-tiles are listed full.
+void tile_windows(const std::vector<int32_t>& rp, const std::vector<int32_t>& ci, const std::vector<uint8_t>& kd,
+                  int32_t r0, int32_t nrows, std::vector<int32_t>* wcol, std::vector<uint8_t>* wkind) {
+  auto kind_of = [&](int32_t r, int32_t c) -> int {
+    if (r >= nrows) return 0;
+    for (int32_t e = rp[r]; e < rp[r + 1]; ++e)
+      if (ci[e] == c) return kd[e];
+    return 0;
+  };
+  std::vector<int32_t> u;
+  for (int32_t r = r0; r < std::min(r0 + 2, nrows); ++r)
+    for (int32_t e = rp[r]; e < rp[r + 1]; ++e) u.push_back(ci[e]);
+  std::sort(u.begin(), u.end());
+  u.erase(std::unique(u.begin(), u.end()), u.end());
+  int32_t covered = -1;   // last 64-block covered by a window
+  for (int32_t c : u) {
+    if (c <= covered) continue;
+    const bool full = kind_of(r0, c) == 1 && kind_of(r0, c + 1) == 1 && kind_of(r0 + 1, c) == 1 &&
+                      kind_of(r0 + 1, c + 1) == 1;
+    wcol->push_back(c);
+    wkind->push_back(full ? 1 : 2);
+    covered = c + 1;
+  }
+}
+
+}  // namespace
+
+extern "C" hla_status hla_build_tile_lists(hla_block_mask* m, int64_t* n_out, cudaStream_t stream) {
+  clear_error();
+  HLA_REQUIRE(m != nullptr && n_out != nullptr, HLA_ERR_INVALID, "null mask or n_out");
+  HLA_REQUIRE(m->row_ptr && m->col_idx && m->kind && m->t_row_ptr && m->t_col_idx && m->t_kind, HLA_ERR_INVALID,
+              "the mask must be filled (hla_build_block_mask fill call) before its window lists");
+  HLA_REQUIRE(m->n_qblocks >= 1 && m->n_kblocks >= 1 && m->n_qblocks <= (1 << 20) && m->n_kblocks <= (1 << 20),
+              HLA_ERR_INVALID, "bad block counts");
+  const int32_t Mq = m->n_qblocks, Mk = m->n_kblocks;
+  std::vector<int32_t> rp(Mq + 1), trp(Mk + 1);
+  HLA_CUDA_TRY(cudaMemcpyAsync(rp.data(), m->row_ptr, sizeof(int32_t) * (Mq + 1), cudaMemcpyDeviceToHost, stream));
+  HLA_CUDA_TRY(cudaMemcpyAsync(trp.data(), m->t_row_ptr, sizeof(int32_t) * (Mk + 1), cudaMemcpyDeviceToHost, stream));
+  HLA_CUDA_TRY(cudaStreamSynchronize(stream));
+  const int64_t nnz = rp[Mq];
+  HLA_REQUIRE(nnz == trp[Mk], HLA_ERR_INVALID, "row / transposed lists disagree");
+  std::vector<int32_t> ci(nnz), tci(nnz);
+  std::vector<uint8_t> kd(nnz), tkd(nnz);
+  if (nnz > 0) {
+    HLA_CUDA_TRY(cudaMemcpyAsync(ci.data(), m->col_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, stream));
+    HLA_CUDA_TRY(cudaMemcpyAsync(kd.data(), m->kind, nnz, cudaMemcpyDeviceToHost, stream));
+    HLA_CUDA_TRY(cudaMemcpyAsync(tci.data(), m->t_col_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, stream));
+    HLA_CUDA_TRY(cudaMemcpyAsync(tkd.data(), m->t_kind, nnz, cudaMemcpyDeviceToHost, stream));
+    HLA_CUDA_TRY(cudaStreamSynchronize(stream));
+  }
+  const int32_t Tq = (Mq + 1) / 2, Tk = (Mk + 1) / 2;
+  std::vector<int32_t> wrp(Tq + 1, 0), wtrp(Tk + 1, 0), wcol, wtcol;
+  std::vector<uint8_t> wkind, wtkind;
+  for (int32_t t = 0; t < Tq; ++t) {
+    tile_windows(rp, ci, kd, 2 * t, Mq, &wcol, &wkind);
+    wrp[t + 1] = (int32_t)wcol.size();
+  }
+  for (int32_t t = 0; t < Tk; ++t) {
+    tile_windows(trp, tci, tkd, 2 * t, Mk, &wtcol, &wtkind);
+    wtrp[t + 1] = (int32_t)wtcol.size();
+  }
+  auto nfull = [](const std::vector<uint8_t>& k) { return (int64_t)std::count(k.begin(), k.end(), (uint8_t)1); };
+  m->w_counts[0] = (int64_t)wcol.size();
+  m->w_counts[1] = nfull(wkind);
+  m->w_counts[2] = (int64_t)wtcol.size();
+  m->w_counts[3] = nfull(wtkind);
+  const int64_t need = std::max<int64_t>(1, std::max(m->w_counts[0], m->w_counts[2]));
+  *n_out = need;
+  if (m->w_col == nullptr) return HLA_OK;
+  HLA_REQUIRE(m->w_row_ptr && m->w_kind && m->wt_row_ptr && m->wt_col && m->wt_kind, HLA_ERR_INVALID,
+              "fill call needs all window arrays");
+  HLA_REQUIRE(need <= m->w_capacity, HLA_ERR_CAPACITY, "window capacity %lld < %lld", (long long)m->w_capacity,
+              (long long)need);
+  HLA_CUDA_TRY(cudaMemcpyAsync(m->w_row_ptr, wrp.data(), sizeof(int32_t) * (Tq + 1), cudaMemcpyHostToDevice, stream));
+  HLA_CUDA_TRY(cudaMemcpyAsync(m->wt_row_ptr, wtrp.data(), sizeof(int32_t) * (Tk + 1), cudaMemcpyHostToDevice, stream));
+  if (!wcol.empty()) {
+    HLA_CUDA_TRY(cudaMemcpyAsync(m->w_col, wcol.data(), sizeof(int32_t) * wcol.size(), cudaMemcpyHostToDevice, stream));
+    HLA_CUDA_TRY(cudaMemcpyAsync(m->w_kind, wkind.data(), wkind.size(), cudaMemcpyHostToDevice, stream));
+  }
+  if (!wtcol.empty()) {
+    HLA_CUDA_TRY(cudaMemcpyAsync(m->wt_col, wtcol.data(), sizeof(int32_t) * wtcol.size(), cudaMemcpyHostToDevice,
+                                 stream));
+    HLA_CUDA_TRY(cudaMemcpyAsync(m->wt_kind, wtkind.data(), wtkind.size(), cudaMemcpyHostToDevice, stream));
+  }
+  HLA_CUDA_TRY(cudaStreamSynchronize(stream));
   return HLA_OK;
 }
 

@@ -52,9 +52,23 @@ struct Pattern {
 
 hla_status make_pattern(const hla_pattern_desc* d, Pattern* p);
 
-// Argument checks shared by hla_attn_fwd / hla_attn_bwd (attn_fwd.cu).
+// The tile lists an attention call walks (tiles are 128 x 128 either way): the mask's CSR
+// lists at block 128; its window lists (hla_build_tile_lists) at block 64, whose columns
+// are 64-block starts.  Start row of a list entry = column * col_mul.
+struct AttnLists {
+  const int32_t* row_ptr;     // per 128-row q tile
+  const int32_t* col;
+  const uint8_t* kind;        // 1 full, 2 element-masked
+  const int32_t* t_row_ptr;   // per 128-key tile (backward)
+  const int32_t* t_col;
+  const uint8_t* t_kind;
+  int32_t col_mul;
+  int64_t n_full, n_partial, t_n_full, t_n_partial;
+};
+
+// Argument checks shared by hla_attn_fwd / hla_attn_bwd (attn_fwd.cu); fills the lists.
 hla_status check_attn_args(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
-                           int32_t head_dim, Pattern* pat);
+                           int32_t head_dim, Pattern* pat, AttnLists* lists);
 
 // Validates an optional hla_score_mod (attn_fwd.cu): outputs stay null when the
 // score modification is off; drpb may be null for the forward.

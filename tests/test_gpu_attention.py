@@ -394,3 +394,118 @@ def test_cfg5_hwt_layer_as_timed(g, H, w, kind):
                 assert_close("cfg5-hwt %s g%d b%d h%d %s" % (kind, g, b, h, name), to_np(got[b, :, h])[s2c], ref)
     dT = layer.drpb.double().cpu().numpy()
     assert np.linalg.norm(dT - dT_ref) / np.linalg.norm(dT_ref) <= 2e-2
+
+
+# ------------------------------------------------------------------ block 64
+def _windows_ref(km):
+    """Reference window lists of a block-64 kind matrix (tests only): per 128-row tile the
+    union of the two 64-blocks' non-empty columns, cut greedily into (u, u + 1) windows;
+    kind 1 iff all four 64 x 64 sub-tiles are full (include/hla.h hla_build_tile_lists)."""
+    from oracle import blocks
+    M = km.shape[0]
+    rp, cols, kinds = [0], [], []
+    for t in range((M + 1) // 2):
+        rows = [r for r in (2 * t, 2 * t + 1) if r < M]
+        u = sorted({int(c) for r in rows for c in np.nonzero(km[r])[0]})
+        covered = -1
+        for c in u:
+            if c <= covered:
+                continue
+            sub = [km[r, cc] if (r < M and cc < km.shape[1]) else 0 for r in (2 * t, 2 * t + 1) for cc in (c, c + 1)]
+            cols.append(c)
+            kinds.append(1 if all(k == blocks.FULL for k in sub) else 2)
+            covered = c + 1
+        rp.append(len(cols))
+    return np.array(rp), np.array(cols), np.array(kinds)
+
+
+B64_MASKS = [("HNA", 128, 128, 7, 7), ("HWA", 64, 64, 8, 8), ("HWA", 56, 56, 7, 7), ("HSA", 64, 64, 16, 16),
+             ("NA2D", 56, 56, 7, 7), ("WSA", 64, 64, 8, 8), ("DENSE", 24, 20, 1, 1), ("HSWA", 32, 32, 8, 8)]
+
+
+@pytest.mark.parametrize("kind,H,W,wh,ww", B64_MASKS)
+def test_block64_window_lists(kind, H, W, wh, ww):
+    from oracle import blocks
+    shift = (wh * ww) // 2 if kind == "HSWA" else 0
+    spec = Spec(kind, H, W, wh, ww, shift=shift)
+    km = blocks.classify_spec(spec, 64, 64)
+    m = hla.hla_build_block_mask(hla.pattern_desc(kind, H, W, wh, ww, block=64, shift=shift), DEV)
+    for rows, (wrp, wcol, wkind) in (((m.w_row_ptr, m.w_col, m.w_kind), _windows_ref(km)),
+                                     ((m.wt_row_ptr, m.wt_col, m.wt_kind), _windows_ref(km.T))):
+        n = int(wrp[-1])
+        assert np.array_equal(rows[0].cpu().numpy(), wrp)
+        assert np.array_equal(rows[1].cpu().numpy()[:n], wcol)
+        assert np.array_equal(rows[2].cpu().numpy()[:n], wkind)
+    assert m.w_counts[0] == int(_windows_ref(km)[0][-1])
+
+
+B64_CASES = [
+    # kind, grid, window, B, heads, d
+    ("HWA", 32, 32, 8, 8, 2, 2, 64),      # 64-token windows: one full 64 x 64 sub-tile per q-block
+    ("HNA", 32, 32, 7, 7, 2, 2, 64),      # cfg4 family (49 tokens)
+    ("HSA", 32, 32, 9, 9, 1, 2, 32),
+    ("HSWA", 32, 32, 8, 8, 1, 2, 64),
+    ("WSA", 32, 32, 8, 8, 1, 2, 64),
+    ("NA2D", 24, 16, 5, 3, 1, 2, 32),      # 2D, non-power-of-two width
+    ("HWA", 56, 56, 7, 7, 1, 2, 32),       # ragged: N = 3136 = 49 blocks of 64 (odd: last tile one block)
+    ("DENSE", 10, 20, 1, 1, 1, 2, 64),     # N = 200
+]
+
+
+@pytest.mark.parametrize("case", B64_CASES, ids=lambda c: "%s_%dx%d_w%dx%d_d%d" % (c[0], c[1], c[2], c[3], c[4], c[7]))
+def test_block64_fwd_bwd(case):
+    kind, gh, gw, wh, ww, B, H, d = case
+    shift = (wh * ww) // 2 if kind == "HSWA" else 0
+    N = gh * gw
+    q, k, v, do = _inputs(B, N, H, d, seed=41)
+    layer = hla.HilbertLocalAttention(kind, gh, gw, wh, ww, B, H, d, block=64, shift=shift, device=DEV)
+    visited = torch.zeros(1, dtype=torch.int64, device=DEV)
+    hla.hla_attn_fwd(layer.desc, layer.mask, q, k, v, tiles_visited=visited, seq_to_cell=layer.s2c)
+    layer.forward(q, k, v)
+    dq, dk, dv = layer.backward(do)
+    torch.cuda.synchronize()
+    assert int(visited.item()) == B * H * layer.tiles
+    spec = Spec(kind, gh, gw, wh, ww, shift=shift)
+    s2c = hilbert.hilbert_order(gh, gw)[0] if layer.hilbert else np.arange(N)
+    seq = lambda t: hilbert.to_sequence(to_np(t), s2c)   # noqa: E731
+    O_ref, L_ref = oatt.attn_fwd(seq(q), seq(k), seq(v), spec)
+    dQ, dK, dV = oatt.attn_bwd(seq(q), seq(k), seq(v), seq(do), spec)
+    assert_close("b64 O", seq(layer.o), O_ref)
+    assert np.abs(to_np(layer.lse) - L_ref).max() <= LSE_MAX_ABS
+    for name, got, ref in (("dQ", dq, dQ), ("dK", dk, dK), ("dV", dv, dV)):
+        assert_close("b64 " + name, seq(got), ref)
+
+
+def test_block64_cfg4_slice_and_rpb():
+    """cfg4 at block 64 (the shape of the b = 64 bench line) on sampled slices, and the global
+    RPB score_mod at block 64 (both backward schedules see window lists)."""
+    B, H, d, g = 2, 12, 64, 128
+    q, k, v, do = _inputs(B, g * g, H, d, seed=0)
+    layer = hla.HilbertLocalAttention("HNA", g, g, 7, 7, B, H, d, block=64, device=DEV)
+    o = layer.forward(q, k, v).clone()
+    dq, dk, dv = (t.clone() for t in layer.backward(do))
+    torch.cuda.synchronize()
+    spec = Spec("HNA", g, g, 7, 7)
+    s2c = hilbert.hilbert_order(g, g)[0]
+    b, h = B - 1, 5
+    Q, K, V, DO = (to_np(t[b, :, h])[s2c] for t in (q, k, v, do))
+    dQ, dK, dV, O, _ = oatt.attn_bwd_slice(Q, K, V, DO, spec, chunk=512)
+    for name, got, ref in (("O", o, O), ("dQ", dq, dQ), ("dK", dk, dK), ("dV", dv, dV)):
+        assert_close("cfg4-b64 " + name, to_np(got[b, :, h])[s2c], ref)
+    g2, w2 = 32, 8
+    q, k, v, do = _inputs(1, g2 * g2, 2, 32, seed=42)
+    lay = hla.HilbertLocalAttention("HWA", g2, g2, w2, w2, 1, 2, 32, block=64, device=DEV, rpb=True)
+    table = torch.rand(lay.rpb.shape, generator=torch.Generator().manual_seed(7), dtype=torch.float64)
+    lay.rpb = (2 * table - 1).float()
+    lay.forward(q, k, v)
+    lay.backward(do)
+    torch.cuda.synchronize()
+    spec = Spec("HWA", g2, g2, w2, w2)
+    s2c = hilbert.hilbert_order(g2, g2)[0]
+    seq = lambda t: hilbert.to_sequence(to_np(t), s2c)   # noqa: E731
+    T = lay.rpb.double().cpu().numpy()
+    O_ref, _ = oatt.attn_fwd(seq(q), seq(k), seq(v), spec, rpb=T)
+    _, _, _, dT_ref = oatt.attn_bwd(seq(q), seq(k), seq(v), seq(do), spec, rpb=T)
+    assert_close("b64 rpb O", seq(lay.o), O_ref)
+    dT = lay.drpb.double().cpu().numpy()
+    assert np.linalg.norm(dT - dT_ref) / np.linalg.norm(dT_ref) <= 2e-2

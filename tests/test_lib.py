@@ -58,12 +58,17 @@ def test_argument_validation_without_gpu():
     m = _lib.BlockMaskC()
     nnz = ctypes.c_int64()
     assert L.hla_build_block_mask(ctypes.byref(d), ctypes.byref(m), ctypes.byref(nnz), None) == _lib.HLA_ERR_INVALID
-    # attention limits
+    # attention limits: tiles of 64 or 128; block 64 runs on the mask's window lists
+    d = api.pattern_desc("HWA", 64, 64, 16, 16, block=32)
+    m = _lib.BlockMaskC(128, 128, 1, 8, 8, 8, 8, 8, 8, 8)
+    st = L.hla_attn_fwd(ctypes.byref(d), ctypes.byref(m), 1, 1, 64, 0.0, 16, 16, 16, 16, 16, None, None, None,
+                        None)
+    assert st == _lib.HLA_ERR_UNSUPPORTED
     d = api.pattern_desc("HWA", 64, 64, 16, 16, block=64)
     m = _lib.BlockMaskC(64, 64, 1, 8, 8, 8, 8, 8, 8, 8)
     st = L.hla_attn_fwd(ctypes.byref(d), ctypes.byref(m), 1, 1, 64, 0.0, 16, 16, 16, 16, 16, None, None, None,
                         None)
-    assert st == _lib.HLA_ERR_UNSUPPORTED
+    assert st == _lib.HLA_ERR_INVALID and b"window lists" in L.hla_last_error()
     d = api.pattern_desc("HWA", 64, 64, 16, 16)
     m = _lib.BlockMaskC(32, 32, 1, 8, 8, 8, 8, 8, 8, 8)
     st = L.hla_attn_fwd(ctypes.byref(d), ctypes.byref(m), 1, 1, 128, 0.0, 16, 16, 16, 16, 16, None, None, None,
