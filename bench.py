@@ -185,6 +185,16 @@ def tensor_pct(flops, ms, peak_tf):
     return round(100 * flops / (ms * 1e-3) / (peak_tf * 1e12), 2)
 
 
+def _ncu_traffic(key, stage):
+    """DRAM bytes per launch of the stage's kernel from the committed ncu launch lists
+    (profiles/ncu_traffic.json; dram__bytes_read.sum + dram__bytes_write.sum), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(key, {}).get(stage)
+    except Exception:
+        return None
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -451,7 +461,9 @@ def run_stack(args):
     ach = tb[dom] / (per[dom] * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm"], "unit": "GB/s",
             "frac": round(ach / peaks["hbm"], 4), "kernel": "attn_%s_kernel" % dom, "stage": dom,
-            "share_of_step": round(per[dom] / my_ms, 4), "traffic": None,
+            "share_of_step": round(per[dom] / my_ms, 4),
+            "traffic": (lambda t: t * len(layers) if t and world == 1 else None)(
+                _ncu_traffic(args.config + ("@64" if blk == 64 else ""), dom)),
             "note": "summed over the %d attention layers of the stack (rank 0)" % len(layers),
             "peak_source": peaks["source"]}
     line = {"metric": METRIC, "value": round(step_ms, 4), "unit": "ms", "n_gpus": world,
@@ -650,13 +662,9 @@ def run_single(args):
                  "ms_per_launch": round(ms_dom, 5), "algorithmic_bytes_per_launch": kd["bytes"],
                  "algorithmic_flops_per_launch": kd["flops"], "arith_intensity": round(ai, 1),
                  "peak_source": peaks["source"], "traffic": None})
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f).get(args.config, {}).get(dom)
-        if tr and world == 1:
-            roof["traffic"] = tr
-    except Exception:
-        pass
+    tr = _ncu_traffic(args.config + ("@64" if blk == 64 else ""), dom)
+    if tr and world == 1:
+        roof["traffic"] = tr
 
     # --- after the timed loops: per-rank statistics over NCCL (C1, C2) ---
     ranks = gather_rank_stats([rank, b0, b1, h0, h1, my_ms, stages["fwd"], stages["bwd"], rk, rv, rbound],

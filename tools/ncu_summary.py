@@ -5,7 +5,8 @@ import csv, io, json, subprocess, sys
 KEYS = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "dram read"),
         ("dram__bytes_write.sum", "dram write"), ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram %peak"),
         ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM %peak"),
-        ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor pipe %"),
+        ("sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32.sum", "tensor ops (bf16 tcgen05 MMA flops)"),
+        ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe cycles active %"),
         ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "TMEM/tensor mem %"),
         ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
         ("launch__grid_size", "grid"), ("launch__block_size", "block"), ("launch__registers_per_thread", "regs"),
