@@ -537,6 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!(kVar & 2)) {
           if (kd == 2) p_math(std::true_type{}); else p_math(std::false_type{});
         }
+        HLA_PADD(18, tc0);
         if (!(kVar & 2)) {
           // P^T packed to bf16 over the first 16 columns of each S^T chunk (in registers):
           // the A operand of dV += P^T dO
@@ -552,6 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         sm100::tmem_wait_st();
         sm100::tc_fence_before();
         sm100::mbar_arrive(&sm.p_ready);     // P^T(g) in TMEM: dV(g), then S^T(g+1) over it
+        HLA_PADD(19, tc0);
         // (dS^T buffer g & 1 was last read by dK / dQ(g - 2), issued before S^T(g): s_full(g)
         // already certified their completion)
         if (!(kVar & 2)) {
@@ -657,7 +659,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tiles_done += nt;
     }
     HLA_PFLUSH(5, 9, warp == 4 && lane == 0);
-    HLA_PFLUSH(16, 18, warp == 4 && lane == 0);
+    HLA_PFLUSH(16, 20, warp == 4 && lane == 0);
   } else {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsDq) : "memory");
     HLA_PDECL;

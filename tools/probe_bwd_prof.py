@@ -17,7 +17,8 @@ CASES = {"cfg2": ("HWA", 64, 16, 16, 8), "cfg3": ("HSA", 64, 16, 16, 8), "cfg4":
          "dense2": ("DENSE", 64, 1, 16, 8)}
 SLOTS = ["mma:ds_ready", "mma:epi_done", "mma:next_operands", "mma:dq_free", "mma:loop_total",
          "cmp:q_full", "cmp:s_full", "cmp:work", "cmp:-", "dq:dq_full", "dq:drain", "dq:dkv_full", "dq:epilogue",
-         "tma:kv_empty", "tma:q_empty", "-", "cmp:until_loads_done", "cmp:until_math_done"]
+         "tma:kv_empty", "tma:q_empty", "-", "cmp:until_loads_done", "cmp:until_dS_done", "cmp:until_P_done",
+         "cmp:until_p_ready"]
 L = _lib.lib()
 for name in (sys.argv[1:] or ["cfg2", "cfg3", "cfg4"]):
     kind, g, w, B, H = CASES[name]
@@ -31,7 +32,7 @@ for name in (sys.argv[1:] or ["cfg2", "cfg3", "cfg4"]):
     n = L.hla_debug_bwd_prof(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), 148)
     P = buf[:n].astype(np.float64)
     tiles = P[:, 15].sum()
-    per = P[:, :18].sum(0) / max(tiles, 1)
+    per = P[:, :20].sum(0) / max(tiles, 1)
     print("%s: %d tiles over %d CTAs; cycles per tile: %s" % (
         name, int(tiles), n, ", ".join("%s %.0f" % (s, x) for s, x in zip(SLOTS, per) if s[-1] != "-")), flush=True)
     del lay
