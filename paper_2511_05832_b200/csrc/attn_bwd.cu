@@ -105,7 +105,7 @@ constexpr int kVar = HLA_BWD_VAR;
 #endif
 
 
-template <int D, bool kBias = false>
+template <int D>
 struct FullSmem {
   static constexpr uint32_t kTileBytes = kBlock * D * 2;
   alignas(1024) uint8_t k[2][kTileBytes];
@@ -116,13 +116,10 @@ struct FullSmem {
   alignas(1024) float dq_stage[kBlock * 32];    // fp32 dQ half tile [128][32], SWIZZLE_128B
   alignas(16) float lse[kQStages][kBlock];
   alignas(16) float dd[kQStages][kBlock];
-  alignas(16) int32_t qa[kQStages][kBias ? kBlock : 4];   // kBias: A_q of the stage's query columns (RPB table index = A_q - B_k)
-  alignas(16) float rpb_wmax[kCmpWarps];            // kBias: per compute warp max |dL/dscore| of the tile
   uint64_t kv_full[2], kv_empty[2], q_full[kQStages], q_empty[kQStages], s_full, s_read, p_ready, ds_ready,
       dq_full[2], dq_free[2], dkv_full, epi_done;
   uint64_t dbg_bar;
   uint32_t tmem_base;
-  int32_t rpb_win[kBias ? rpb_win_cap<D>() : 1];   // dRPB of the current tile's offset box, fixed point (compute warps)
 };
 
 // Persistent: CTA c processes kv-block work units c, c + G, ... (pairs of kv-blocks of
@@ -130,13 +127,13 @@ struct FullSmem {
 // Q/dO) stream in while the current unit computes; the dK/dV epilogue of a unit
 // overlaps the first MMAs of the next one.  Phase counters: n = units with tiles so
 // far, g = (q-block) tiles so far.
-template <int D, bool kTwoD, bool kGather, bool kBias>
+template <int D, bool kTwoD, bool kGather>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_full_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                     const __grid_constant__ CUtensorMap tmDQ, const BwdParams prm) {
   extern __shared__ uint8_t smem_raw[];
-  using Smem = FullSmem<D, kBias>;
+  using Smem = FullSmem<D>;
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -235,18 +232,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (s) stage_tag1 = tag; else stage_tag0 = tag;
           if (role == 0) {
-            if (kBias) {
-              // A_q = (qr + H - 1)(2W - 1) + qc + W - 1 of the q-block's 128 columns (phantom: cell 0),
-              // read by the compute warps as warp-uniform 16-B loads next to LSE / D
-              const int4 rc = make_int4(rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane, prm.N, prm.grid_w),
-                                        rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane + 1, prm.N, prm.grid_w),
-                                        rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane + 2, prm.N, prm.grid_w),
-                                        rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane + 3, prm.N, prm.grid_w));
-              const int32_t a0 = (prm.grid_h - 1) * prm.rpb_w + prm.grid_w - 1;
-              auto a_of = [&](int32_t v) { return a0 + (v >> 16) * prm.rpb_w + (v & 0xffff); };
-              sm100::sts_u4(sm100::smem_u32(sm.qa[s]) + 16u * lane, a_of(rc.x), a_of(rc.y), a_of(rc.z), a_of(rc.w));
-              __syncwarp();   // every lane's A_q is written before lane 0 arrives on q_full
-            }
             if (lane == 0 && (kVar & 4)) {
               sm100::mbar_arrive(&sm.q_full[s]);
             } else if (lane == 0) {
@@ -404,10 +389,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     ug.ppb = (ug.mk + 1) / 2;
     ug.pairs = ug.ppb * prm.heads * prm.batch;
     const int32_t mk = ug.mk;
-    if (kBias) {   // the dRPB window starts (and is left after every flush) zeroed
-      for (int i = (warp - 4) * 32 + lane; i < rpb_win_cap<D>(); i += kCmpThreads) sm.rpb_win[i] = 0;
-      sm100::named_bar_sync(3, kCmpThreads);
-    }
     uint32_t g = 0;
     for (int32_t kq = 0;; ++kq) {
       const int32_t u = unit_at(kq, ug);
@@ -418,42 +399,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int32_t kidx = kb * kBlock + row;
       RowBox box = clip_box<kTwoD>(prm.pat, col_box(prm.pat, kidx));
       if (kidx >= prm.N) box.len = 0;   // phantom key row of a ragged tile: nothing allowed
-      // RPB: this key row's cell, the key block's cell box, the head's table / gradient
-      int32_t k_b = 0;
-      CellBox kbox{0, 0, 0, 0};
-      const float* rpbh = nullptr;
-      float* drpbh = nullptr;
-      if (kBias) {
-        const int32_t rc = rpb_cell_rc(prm.cells, kidx, prm.N, prm.grid_w);
-        k_b = (rc >> 16) * prm.rpb_w + (rc & 0xffff);
-        kbox = rpb_block_box(prm.cells, kb * kBlock, prm.N, prm.grid_w, lane);
-        rpbh = prm.rpb + (int64_t)h * prm.rpb_hw;
-        drpbh = prm.drpb + (int64_t)h * prm.rpb_hw;
-      }
       for (int t = 0; t < nt; ++t, ++g) {
         const uint8_t kd = __ldg(prm.t_kind + rs + t);
         const int32_t q0 = __ldg(prm.t_col_idx + rs + t) * prm.col_mul;
         const int s = g & 1;
-        // RPB: the tile's offset box (dr, dc) = q box - key box and whether its rows fit
-        // the shared-memory dRPB window (query offsets A_q come staged with LSE / D)
-        int32_t dr0 = 0, dc0 = 0, wc = 0, wrows = 0, wcols = 0, kwb = 0;
-        bool win = false;
-        if (kBias) {
-          const CellBox qbox = rpb_block_box(prm.cells, q0, prm.N, prm.grid_w, lane);
-          dr0 = qbox.r0 - kbox.r1;
-          dc0 = qbox.c0 - kbox.c1;
-          // window = the box's offset rows at the table's own row stride, so that the element
-          // index (dr - dr0) * wc + (dc - dc0) = A_q - kwb (A_q staged per q-block)
-          wc = prm.rpb_w;
-          wrows = qbox.r1 - kbox.r0 - dr0 + 1;
-          wcols = qbox.c1 - kbox.c0 - dc0 + 1;   // offset columns actually used (<= wc)
-          win = wrows * wc <= rpb_win_cap<D>();
-          kwb = (prm.grid_h - 1) * prm.rpb_w + prm.grid_w - 1 + k_b + dr0 * wc + dc0;
-        }
         HLA_PW(5, sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1));
         const uint32_t lse2 = sm100::smem_u32(sm.lse[s]);
         const uint32_t dd = sm100::smem_u32(sm.dd[s]);
-        const uint32_t qa = sm100::smem_u32(sm.qa[s]);
         const uint32_t dsbuf = sm100::smem_u32(sm.ds[g & 1]);
         HLA_PW(6, sm100::mbar_wait(&sm.s_full, g & 1));
         HLA_PMARK(tc0);
@@ -488,11 +440,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (kPart && !kTwoD) {
               const int32_t lo = min(max(box.lo - base, 0), 32), hi = min(max(box.lo + box.len - base, 0), 32);
               elem_mask = !__all_sync(0xffffffffu, lo == 0 && hi == 32);
-              if (!kBias) {   // (with the RPB gather the branchy loop measured slower: cfg5 +6%)
-                const bool any = hi > lo;
-                ulo = __reduce_min_sync(0xffffffffu, any ? lo : 32) >> 3;
-                uhi = (__reduce_max_sync(0xffffffffu, any ? hi : 0) + 7) >> 3;
-              }
+              const bool any = hi > lo;
+              ulo = __reduce_min_sync(0xffffffffu, any ? lo : 32) >> 3;
+              uhi = (__reduce_max_sync(0xffffffffu, any ? hi : 0) + 7) >> 3;
             }
             float* p = reinterpret_cast<float*>(sr[j]);   // P overwrites S in place
 #pragma unroll
@@ -505,18 +455,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int qc = c * 32 + u4 * 8;
               const float4 la = sm100::lds_f4(lse2 + qc * 4), lb = sm100::lds_f4(lse2 + qc * 4 + 16);
               const float lv[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
-              int32_t av[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-              if (kBias) {
-                const float4 xa = sm100::lds_f4(qa + qc * 4), xb = sm100::lds_f4(qa + qc * 4 + 16);
-                av[0] = __float_as_int(xa.x); av[1] = __float_as_int(xa.y); av[2] = __float_as_int(xa.z);
-                av[3] = __float_as_int(xa.w); av[4] = __float_as_int(xb.x); av[5] = __float_as_int(xb.y);
-                av[6] = __float_as_int(xb.z); av[7] = __float_as_int(xb.w);
-              }
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
                 float x = fmaf(__uint_as_float(sr[j][u4 * 8 + e]), sl2, -lv[e]);
-                if (kBias)   // + bias * log2(e), bias = table[h][dr + H - 1][dc + W - 1] = table[A_q - B_k]
-                  x = fmaf(__ldg(rpbh + (av[e] - k_b)), kLog2e, x);
                 if (kPart && elem_mask) {
                   const int32_t qq = base + u4 * 8 + e;
                   bool ok;
@@ -584,73 +525,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         HLA_PADD(17, tc0);
-        if (kBias && !(kVar & 2)) {
-          // dRPB[offset] += dL/dscore = dS / scale (before ds_ready: the A_q staged with the
-          // tile's Q stage are reused once it is released): into the tile's shared-memory
-          // offset window at a per-tile power-of-two fixed-point scale (kRpbFixBits), flushed
-          // with fp32 global reductions; windows that do not fit go to global fp32 reductions
-          float fx = 0.f;
-          if (win) {
-            float mx = 0.f;
-#pragma unroll
-            for (int j = 0; j < kChunks; ++j)
-#pragma unroll
-              for (int i = 0; i < 32; ++i) mx = fmaxf(mx, fabsf(__uint_as_float(dpr[j][i])));
-            // non-negative floats order like their bit patterns
-            const uint32_t mb = __reduce_max_sync(0xffffffffu, __float_as_uint(mx * prm.inv_scale));
-            if (lane == 0) sm.rpb_wmax[warp - 4] = __uint_as_float(mb);
-            sm100::named_bar_sync(3, kCmpThreads);
-            float tmx = 0.f;
-#pragma unroll
-            for (int w4 = 0; w4 < kCmpWarps / 4; ++w4) {
-              const float4 m = sm100::lds_f4(sm100::smem_u32(sm.rpb_wmax) + 16 * w4);
-              tmx = fmaxf(tmx, fmaxf(fmaxf(m.x, m.y), fmaxf(m.z, m.w)));
-            }
-            // largest addend in [2^(kRpbFixBits-1), 2^kRpbFixBits)
-            fx = rpb_scale_for(tmx, 1.f);
-          }
-          const uint32_t wbase = sm100::smem_u32(sm.rpb_win);
-#pragma unroll
-          for (int j = 0; j < kChunks; ++j) {
-#pragma unroll
-            for (int u4 = 0; u4 < 4; ++u4) {
-              const int qc = (cset * kChunks + j) * 32 + u4 * 8;
-              const float4 xa = sm100::lds_f4(qa + qc * 4), xb = sm100::lds_f4(qa + qc * 4 + 16);
-              const int32_t av[8] = {__float_as_int(xa.x), __float_as_int(xa.y), __float_as_int(xa.z),
-                                     __float_as_int(xa.w), __float_as_int(xb.x), __float_as_int(xb.y),
-                                     __float_as_int(xb.z), __float_as_int(xb.w)};
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const int i = u4 * 8 + e;
-                const float gv = __uint_as_float(dpr[j][i]) * prm.inv_scale;
-                if (gv == 0.f) continue;   // masked pairs (P = 0) add nothing
-                if (win) {   // window index (dr - dr0) * (2W - 1) + (dc - dc0) = A_q - kwb
-                  const int32_t v = __float2int_rn(gv * fx);
-                  if (v != 0)   // (phantom positions: cell 0, possibly outside the box; their P is 0)
-                    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(wbase + 4u * (uint32_t)(av[e] - kwb)), "r"(v)
-                                 : "memory");
-                } else {     // table index A_q - B_k
-                  atomicAdd(drpbh + (av[e] - k_b), gv);
-                }
-              }
-            }
-          }
-          if (win) {
-            // flush the tile's dRPB window to global (and re-zero it) -- all compute threads
-            sm100::named_bar_sync(3, kCmpThreads);
-            const float inv_fx = 1.f / fx;
-            const int tid = (warp - 4) * 32 + lane;
-            for (int i = tid; i < wrows * wcols; i += kCmpThreads) {   // only the box's used columns
-              const int32_t ir = i / wcols, ic = i - ir * wcols;
-              const int32_t v = sm.rpb_win[ir * wc + ic];
-              if (v != 0) {
-                atomicAdd(drpbh + (dr0 + ir + prm.grid_h - 1) * prm.rpb_w + (dc0 + ic + prm.grid_w - 1),
-                          (float)v * inv_fx);
-                sm.rpb_win[ir * wc + ic] = 0;
-              }
-            }
-          }
-        }
         sm100::fence_proxy_async_smem();
         sm100::tc_fence_before();
         sm100::mbar_arrive(&sm.ds_ready);
@@ -841,11 +715,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 4 && lane == 0 && prm.visited != nullptr && tiles_done > 0) atomicAdd(prm.visited, tiles_done);
 }
 
-template <int D, bool kTwoD, bool kGather, bool kBias>
+template <int D, bool kTwoD, bool kGather>
 hla_status launch_full_t(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mdo,
                       const CUtensorMap& mdq, const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream) {
-  const size_t smem = sizeof(FullSmem<D, kBias>) + 1024;
-  auto* fn = attn_bwd_full_kernel<D, kTwoD, kGather, kBias>;
+  const size_t smem = sizeof(FullSmem<D>) + 1024;
+  auto* fn = attn_bwd_full_kernel<D, kTwoD, kGather>;
   HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t pairs = (int64_t)((n_kblocks + 1) / 2) * prm.heads * prm.batch;   // work units (kv-block pairs)
   const int grid = (int)std::min<int64_t>(pairs, (int64_t)num_sms());
@@ -854,29 +728,21 @@ hla_status launch_full_t(const CUtensorMap& mq, const CUtensorMap& mk, const CUt
   return HLA_OK;
 }
 
-static_assert(sizeof(FullSmem<64, true>) + 1024 <= 227 * 1024, "bwd shared memory (d = 64, RPB) exceeds 227 KB");
-
-template <bool kBias>
-hla_status dispatch_full(int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
-                         const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm,
-                         int32_t mkb, cudaStream_t stream) {
-  if (head_dim == 64) {
-    if (gather) return launch_full_t<64, false, true, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
-    return two_d ? launch_full_t<64, true, false, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream)
-                 : launch_full_t<64, false, false, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
-  }
-  if (gather) return launch_full_t<32, false, true, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
-  return two_d ? launch_full_t<32, true, false, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream)
-               : launch_full_t<32, false, false, kBias>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
-}
+static_assert(sizeof(FullSmem<64>) + 1024 <= 227 * 1024, "bwd shared memory (d = 64) exceeds 227 KB");
 
 }  // namespace
 
-hla_status launch_full(bool bias, int head_dim, bool gather, bool two_d, const CUtensorMap& mq,
-                       const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq,
-                       const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream) {
-  return bias ? dispatch_full<true>(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, n_kblocks, stream)
-              : dispatch_full<false>(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
+hla_status launch_full(int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
+                       const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm,
+                       int32_t mkb, cudaStream_t stream) {
+  if (head_dim == 64) {
+    if (gather) return launch_full_t<64, false, true>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
+    return two_d ? launch_full_t<64, true, false>(mq, mk, mv, mdo, mdq, prm, mkb, stream)
+                 : launch_full_t<64, false, false>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
+  }
+  if (gather) return launch_full_t<32, false, true>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
+  return two_d ? launch_full_t<32, true, false>(mq, mk, mv, mdo, mdq, prm, mkb, stream)
+               : launch_full_t<32, false, false>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
 }
 
 }  // namespace bwd
@@ -1112,15 +978,16 @@ hla_status prepare_main(const hla_pattern_desc* d, const hla_block_mask* m, int3
   pl->head_dim = head_dim;
   // schedule: full-tile (attn_bwd_full_kernel) when full tiles are at least half of the
   // mask's tiles; half-tile (attn_bwd_split_kernel) otherwise (the split
-  // schedule overlaps the partial tiles' masked compute better)
-  pl->full = lists.t_n_full >= lists.t_n_partial && lists.t_n_full > 0;
+  // schedule overlaps the partial tiles' masked compute better) and with the global RPB (only
+  // the half-tile schedule has the dRPB window: at the previous tile's scale, no extra barrier)
+  pl->full = prm.rpb == nullptr && lists.t_n_full >= lists.t_n_partial && lists.t_n_full > 0;
   return HLA_OK;
 }
 
 hla_status launch_main(const MainPlan& pl, cudaStream_t stream) {
   const bool bias = pl.prm.rpb != nullptr;
   if (pl.full)
-    return bwd::launch_full(bias, pl.head_dim, pl.gather, pl.two_d, pl.mq, pl.mk, pl.mv, pl.mdo, pl.mdq, pl.prm,
+    return bwd::launch_full(pl.head_dim, pl.gather, pl.two_d, pl.mq, pl.mk, pl.mv, pl.mdo, pl.mdq, pl.prm,
                             pl.mkb, stream);
   return bwd::launch_split(bias, pl.head_dim, pl.gather, pl.two_d, pl.mq, pl.mk, pl.mv, pl.mdo, pl.mdq, pl.prm,
                            pl.mkb, stream);

@@ -54,7 +54,7 @@ constexpr float kRpbFixMax = 4194304.f;   // 2^kRpbFixBits: larger scaled addend
 __device__ __forceinline__ float rpb_scale_for(float tmx, float fallback) {
   return tmx > 0.f ? ldexpf(1.f, kRpbFixBits - 1 - ilogbf(tmx)) : fallback;
 }
-// the next tile's scale from the eight compute warps' maxima of a tile
+// the next tile's scale from the eight compute warps' maxima of a tile (half-tile schedule)
 __device__ __forceinline__ float rpb_next_scale(const float* wmax8, float cur) {
   float m = 0.f;
 #pragma unroll
@@ -64,9 +64,10 @@ __device__ __forceinline__ float rpb_next_scale(const float* wmax8, float cur) {
 
 // Kernel launch of one schedule for the head_dim / reorder / 2D-pattern variant; the maps
 // view Q, K, V, dO as bf16 rows and the fp32 dQ accumulator (see hla_attn_bwd_main).
-hla_status launch_full(bool bias, int head_dim, bool gather, bool two_d, const CUtensorMap& mq,
-                       const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq,
-                       const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream);
+// (the full-tile schedule has no global-RPB path: RPB layers take the half-tile schedule)
+hla_status launch_full(int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
+                       const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm,
+                       int32_t n_kblocks, cudaStream_t stream);
 hla_status launch_split(bool bias, int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
                         const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm,
                         int32_t n_kblocks, cudaStream_t stream);
