@@ -32,6 +32,9 @@
 //                 reduce-add into the fp32 accumulator) and the dK / dV rows of
 //                 each unit.
 // K9 dq_finalize    : fp32 accumulator -> bf16 dQ.
+#ifdef HLA_BWD_PROF
+#define HLA_PROF_ON
+#endif
 #include <type_traits>
 
 #include "attn_bwd_common.cuh"
@@ -39,6 +42,7 @@
 namespace hla {
 #ifdef HLA_BWD_PROF
 __device__ unsigned long long g_bwd_prof[1024][24];
+#define HLA_PROF_ARRAY g_bwd_prof
 #endif
 namespace bwd {
 namespace {
@@ -78,31 +82,6 @@ constexpr int kQStages = 2;
 #endif
 constexpr int kVar = HLA_BWD_VAR;
 
-// Dev-only wait-time accounting (`make VARIANT=prof DEFS=-DHLA_BWD_PROF`): one thread per
-// role sums the cycles it spends in each wait / work phase; hla_debug_bwd_prof() reads the
-// per-CTA sums.
-#ifdef HLA_BWD_PROF
-#define HLA_PW(slot, ...)                          \
-  do {                                             \
-    const long long _t0 = clock64();               \
-    __VA_ARGS__;                                   \
-    prof[slot] += (unsigned long long)(clock64() - _t0); \
-  } while (0)
-#define HLA_PDECL unsigned long long prof[24] = {0}
-#define HLA_PMARK(v) const long long v = clock64()
-#define HLA_PADD(slot, since) prof[slot] += (unsigned long long)(clock64() - (since))
-#define HLA_PFLUSH(lo, hi, cond)                                                  \
-  do {                                                                           \
-    if (cond)                                                                    \
-      for (int _i = (lo); _i < (hi); ++_i) ::hla::g_bwd_prof[blockIdx.x][_i] = prof[_i]; \
-  } while (0)
-#else
-#define HLA_PW(slot, ...) __VA_ARGS__
-#define HLA_PDECL do {} while (0)
-#define HLA_PMARK(v) do {} while (0)
-#define HLA_PADD(slot, since) do {} while (0)
-#define HLA_PFLUSH(lo, hi, cond) do {} while (0)
-#endif
 
 
 template <int D>

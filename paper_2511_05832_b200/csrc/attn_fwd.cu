@@ -25,11 +25,18 @@
 // released it (p_full); P has its own region, so S_{t+1} overlaps nothing the
 // PV MMA still reads.  Every commit tracks all earlier MMAs, so s_full(t) also
 // certifies that PV_{t-1} finished (O may then be rescaled safely).
+#ifdef HLA_FWD_PROF
+#define HLA_PROF_ON
+#endif
 #include "predicates.cuh"
 #include "sm100.cuh"
 #include "tensor_map.cuh"
 
 namespace hla {
+#ifdef HLA_FWD_PROF
+__device__ unsigned long long g_fwd_prof[1024][24];
+#define HLA_PROF_ARRAY g_fwd_prof
+#endif
 namespace {
 
 constexpr int kBlock = 128;
@@ -265,12 +272,18 @@ __global__ void __launch_bounds__(kThreads, 2)
   sm100::tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
   unsigned long long tiles_done = 0;
+#ifdef HLA_FWD_PROF
+  const long long prof_c0 = clock64();
+  unsigned long long prof_g0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof_g0));
+#endif
   HLA_TR_DECL;
 
   // register split (setmaxnreg acts per warpgroup): the control warpgroup gives its
   // registers to the softmax warpgroup (one thread per row keeps a 128-wide S row)
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
+    HLA_PDECL;
     // (derived after the register split, so they are not spilled across it)
     const int32_t mq = (prm.N + kBlock - 1) / kBlock;   // last q-block may be ragged
     const int32_t units = mq * prm.heads * prm.batch;
@@ -316,8 +329,8 @@ __global__ void __launch_bounds__(kThreads, 2)
           const int qs = it.n & 1;
           const int4 cells = row_cells<kGather>(prm.N, qb * kBlock, prm.s2c, lane);
           if (it.n >= 2) {
-            sm100::mbar_wait(&sm.o_staged[qs], ((it.n >> 1) - 1) & 1);
-            store_o(qs, qs ? staged1 : staged0);
+            HLA_PW(11, sm100::mbar_wait(&sm.o_staged[qs], ((it.n >> 1) - 1) & 1));
+            HLA_PW(12, store_o(qs, qs ? staged1 : staged0));
           }
           if (qs) staged1 = it.u; else staged0 = it.u;
           if (lane == 0) HLA_TR((3 << 24) | (1 << 16) | it.n);
@@ -366,6 +379,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         sm100::bulk_wait_group0();
       }
+      HLA_PFLUSH(11, 13, warp == 0 && lane == 0);
+      HLA_PFLUSH(13, 14, warp == 2 && lane == 0);
     } else if (warp == 1 && lane == 0) {
       // ----------------------------------------------------------- MMA issuer
       constexpr uint32_t idesc_s = sm100::make_idesc_bf16(kBlock, kBlock, false, false);
@@ -388,6 +403,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         sm100::tc_fence_after();
         issue_s(0, 0);
       }
+      HLA_PMARK(tl0);
       while (it.valid) {
         const int32_t ct = it.t, cnt = it.nt;
         it.advance(prm.row_ptr, mq, units);
@@ -396,7 +412,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         // ready first goes first: waiting for one in a fixed order stalls the other
         // (S first stalls PV behind late K loads; PV first stalls S behind the softmax).
         bool s_pending = it.valid, pv_pending = true;
-        if (s_pending) sm100::mbar_wait(&sm.s_free, g & 1);
+        if (s_pending) HLA_PW(0, sm100::mbar_wait(&sm.s_free, g & 1));
+        HLA_PMARK(tp0);
         while (s_pending || pv_pending) {
           if (s_pending && (it.t != 0 || sm100::mbar_test_wait(&sm.q_full[it.n & 1], (it.n >> 1) & 1)) &&
               sm100::mbar_test_wait(&sm.k_full[(g + 1) & 1], ((g + 1) >> 1) & 1)) {
@@ -421,11 +438,23 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
           __nanosleep(32);
         }
+        HLA_PADD(1, tp0);
         ++g;
       }
+      HLA_PADD(2, tl0);
+#ifdef HLA_FWD_PROF
+      prof[15] = g;
+      prof[16] = (unsigned long long)(clock64() - prof_c0);   // this CTA's cycles until its last PV issue
+      prof[17] = prof_g0;                                       // globaltimer (ns) at start / end
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof[18]));
+#endif
+      HLA_PFLUSH(0, 3, true);
+      HLA_PFLUSH(15, 19, true);
+      HLA_PFLUSH(20, 22, true);
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
+    HLA_PDECL;
     const int32_t mq = (prm.N + kBlock - 1) / kBlock;
     const int32_t units = mq * prm.heads * prm.batch;
     // --------------------------------------------------- softmax + epilogue
@@ -453,7 +482,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int32_t a_q = kBias ? prm.rpb_a0 + rpb_cell_off(prm.cells, q, prm.N, prm.grid_w, prm.rpb_w) : 0;
       if (row == 0) HLA_TR((2 << 24) | (6 << 16) | it.n);
       for (int t = 0; t < it.nt; ++t, ++g) {
-        sm100::mbar_wait(&sm.s_full, g & 1);
+        HLA_PMARK(tw0);
+        HLA_PW(3, sm100::mbar_wait(&sm.s_full, g & 1));
+        HLA_PMARK(ts0);
+        if (t == 0) HLA_PADD(19, tw0);
         if (row == 0) HLA_TR((2 << 24) | (1 << 16) | g);
         sm100::tc_fence_after();
         // the whole S row: four loads in flight, one wait (TMEM round trip ~200 cycles)
@@ -465,6 +497,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (row == 0) HLA_TR((6 << 24) | (1 << 16) | g);
         sm100::tc_fence_before();
         sm100::mbar_arrive(&sm.s_free);          // the MMA may overwrite S with S(g+1)
+        HLA_PADD(4, ts0);
         float (&s)[kBlock] = *reinterpret_cast<float(*)[kBlock]>(sr);
         const int32_t tm = tile_meta(meta, prm.col_idx, prm.kind, it.rs, t);
         // kBias: scores move to the log2 domain here (s = S * scale * log2e + bias * log2e)
@@ -517,10 +550,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
         if (row == 0) HLA_TR((6 << 24) | (3 << 16) | g);
         // P(g-1) / O are read by PV(g-1): wait for it before writing P(g) or rescaling O
+        HLA_PADD(5, ts0);
         if (g > 0) {
-          sm100::mbar_wait(&sm.pv_done, (g - 1) & 1);
+          HLA_PW(6, sm100::mbar_wait(&sm.pv_done, (g - 1) & 1));
           sm100::tc_fence_after();
         }
+        HLA_PMARK(tst0);
         if (row == 0) HLA_TR((6 << 24) | (4 << 16) | g);
         if (__any_sync(0xffffffffu, t > 0 && alpha != 1.f)) {
 #pragma unroll
@@ -540,6 +575,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         sm100::tmem_wait_st();
         sm100::tc_fence_before();
         sm100::mbar_arrive(&sm.p_full);
+        HLA_PADD(7, tst0);
         if (row == 0) HLA_TR((2 << 24) | (2 << 16) | g);
       }
 
@@ -547,7 +583,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int64_t orow = ((int64_t)b * prm.N + ocell) * prm.heads + h;
       uint4* optr = reinterpret_cast<uint4*>(prm.o + orow * D);
       const float inv_l = l > 0.f ? 1.f / l : 0.f;
-      sm100::mbar_wait(&sm.o_full, it.n & 1);
+      HLA_PW(8, sm100::mbar_wait(&sm.o_full, it.n & 1));
+      HLA_PMARK(te0);
       if (row == 0) HLA_TR((2 << 24) | (3 << 16) | it.n);
       sm100::tc_fence_after();
       uint32_t o[D];
@@ -583,6 +620,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (real)
         prm.lse[((int64_t)b * prm.heads + h) * prm.N + q] =
             l > 0.f ? (m_use + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+      HLA_PADD(9, te0);
       tiles_done += it.nt;
       it.t = it.nt - 1;
       it.advance(prm.row_ptr, mq, units);
@@ -590,8 +628,11 @@ __global__ void __launch_bounds__(kThreads, 2)
         meta = it.from_pf ? pmeta : load_meta(prm.col_idx, prm.kind, it.rs, it.nt, lane);
         pmeta = load_meta(prm.col_idx, prm.kind, it.prs, it.pre - it.prs, lane);
       }
+      HLA_PADD(10, te0);
       if (row == 0) HLA_TR((2 << 24) | (5 << 16) | it.n);
     }
+    HLA_PFLUSH(3, 11, warp == 4 && lane == 0);
+    HLA_PFLUSH(19, 20, warp == 4 && lane == 0);
   }
 
   sm100::tc_fence_before();
@@ -679,6 +720,16 @@ hla_status parse_score_mod(const hla_pattern_desc* d, const hla_score_mod* mod, 
 }  // namespace hla
 
 using namespace hla;
+
+#ifdef HLA_FWD_PROF
+// dev-only: per-CTA wait / work cycle sums of the last attn_fwd_kernel launch (HLA_FWD_PROF builds)
+extern "C" __attribute__((visibility("default"))) int hla_debug_fwd_prof(unsigned long long* host, int ctas) {
+  cudaDeviceSynchronize();
+  const int n = ctas < 1024 ? ctas : 1024;
+  cudaMemcpyFromSymbol(host, hla::g_fwd_prof, (size_t)n * 24 * sizeof(unsigned long long));
+  return n;
+}
+#endif
 
 extern "C" hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
                                    int32_t head_dim, float scale, const void* q, const void* k, const void* v,

@@ -113,4 +113,32 @@ extern __device__ unsigned long long g_hla_trace[8 * 1024 * 2];
   } while (0)
 #endif
 
+// ---- dev-only wait-time accounting (variant builds) --------------------
+// Build with the kernel's switch (HLA_BWD_PROF / HLA_FWD_PROF; its .cu file then defines
+// HLA_PROF_ON before its includes and HLA_PROF_ARRAY after them): one thread per role sums
+// the cycles it spends in each wait / work phase into prof[slot]; HLA_PFLUSH writes the
+// sums to HLA_PROF_ARRAY[blockIdx.x].
+#ifdef HLA_PROF_ON
+#define HLA_PW(slot, ...)                                \
+  do {                                                   \
+    const long long _t0 = clock64();                     \
+    __VA_ARGS__;                                         \
+    prof[slot] += (unsigned long long)(clock64() - _t0); \
+  } while (0)
+#define HLA_PDECL unsigned long long prof[24] = {0}
+#define HLA_PMARK(v) const long long v = clock64()
+#define HLA_PADD(slot, since) prof[slot] += (unsigned long long)(clock64() - (since))
+#define HLA_PFLUSH(lo, hi, cond)                                                   \
+  do {                                                                             \
+    if (cond)                                                                      \
+      for (int _i = (lo); _i < (hi); ++_i) HLA_PROF_ARRAY[blockIdx.x][_i] = prof[_i]; \
+  } while (0)
+#else
+#define HLA_PW(slot, ...) __VA_ARGS__
+#define HLA_PDECL do {} while (0)
+#define HLA_PMARK(v) do {} while (0)
+#define HLA_PADD(slot, since) do {} while (0)
+#define HLA_PFLUSH(lo, hi, cond) do {} while (0)
+#endif
+
 }  // namespace hla

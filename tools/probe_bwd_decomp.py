@@ -37,7 +37,7 @@ for name, kind, g, w, B, H in CASES:
     L = hla.HilbertLocalAttention(kind, g, g, w, w, B, H, d, device="cuda")
     L.forward(q, k, v)
     L.backward(do)
-    s2c = L.s2c
+    s2c = None if os.environ.get("HLA_NO_GATHER") else L.s2c
 
     def b():
         api.hla_attn_bwd_main(L.desc, L.mask, q, k, v, do, L.dq, L.dk, L.dv, L.workspace, 0.0, seq_to_cell=s2c)

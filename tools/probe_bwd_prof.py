@@ -1,6 +1,6 @@
 """Dev probe: per-role wait / work cycles of attn_bwd_kernel, averaged over
 the CTAs and divided by the tiles each CTA ran.  Needs the HLA_BWD_PROF build:
-  make VARIANT=prof DEFS=-DHLA_BWD_PROF ; HLA_LIB_NAME=libhla_prof.so python tools/probe_bwd_prof.py cfg2"""
+  make VARIANT=bprof DEFS=-DHLA_BWD_PROF ; HLA_LIB_NAME=libhla_bprof.so python tools/probe_bwd_prof.py cfg2"""
 import ctypes
 import os
 import sys
