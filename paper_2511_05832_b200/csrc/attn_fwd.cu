@@ -44,8 +44,26 @@ constexpr int kThreads = 256;   // warpgroup 0: TMA (Q), MMA, TMA (K), TMA (V); 
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kColS = 0, kColP = 128, kColO = 192;
 
+// floor(n / d) for 0 <= n < 2^31 as one wide multiply and a shift (Granlund-Montgomery:
+// m = ceil(2^(31+l) / d), l = ceil(log2 d)); the unit decode at every unit boundary of
+// every role otherwise runs three integer divisions on its critical path
+struct FastDiv {
+  uint32_t m, s;
+  int32_t d;
+  __device__ __forceinline__ int32_t div(int32_t n) const {
+    return (int32_t)(((uint64_t)(uint32_t)n * m) >> s);
+  }
+};
+inline FastDiv make_fastdiv(int32_t d) {
+  uint32_t l = 0;
+  while ((1ll << l) < d) ++l;
+  const uint64_t p = 1ull << (31 + l);
+  return FastDiv{(uint32_t)((p + (uint64_t)d - 1) / (uint64_t)d), 31 + l, d};
+}
+
 struct FwdParams {
   Pattern pat;
+  FastDiv mq_div, heads_div;   // q-blocks per (b, h); heads
   int32_t N, heads, batch;
   float scale_log2;
   const int32_t* row_ptr;    // tile lists (AttnLists): per 128-row q tile
@@ -143,6 +161,18 @@ __device__ __forceinline__ void apply_row_mask(float (&s)[kBlock], const Pattern
   }
 }
 
+// True when no key of the partial tile [k0, k0 + 128) is allowed for query row `box`:
+// the 1D interval (clipped to [0, N)) or the 2D box's grid-row range misses the tile.
+// A warp whose 32 rows all miss skips the tile's softmax (its P rows are zero).
+template <bool kTwoD>
+__device__ __forceinline__ bool row_misses_tile(const Pattern& pat, const RowBox& box_in, int32_t k0) {
+  const RowBox box = clip_box<kTwoD>(pat, box_in);
+  if (box.len <= 0) return true;
+  if (!kTwoD) return box.lo + box.len <= k0 || box.lo >= k0 + kBlock;
+  const int32_t r0 = k0 / pat.W, r1 = (k0 + kBlock - 1) / pat.W;   // grid rows the tile's keys lie in
+  return box.lo + box.len <= r0 || box.lo > r1;
+}
+
 // k-th work unit of this CTA: pairs of consecutive q-blocks (2p, 2p+1) of one
 // (b, h), pairs strided over the grid.  Neighbouring q-blocks list the same
 // kv-blocks (HWA: exactly), so the producer can skip reloading a K/V stage.
@@ -159,32 +189,32 @@ struct FwdIter {
   bool valid;
   bool from_pf;          // the current unit came from the prefetch (its per-lane metadata too)
   int32_t pu, prs, pre;  // prefetched unit k + 1 and its CSR row [prs, pre)
-  __device__ void seek(const int32_t* row_ptr, int32_t mq, int32_t units) {
+  __device__ void seek(const int32_t* row_ptr, const FastDiv& mq, int32_t units) {
     for (;; ++k) {
       u = fwd_unit_at(k);
       if (u >= units) break;
-      const int32_t qb = u % mq;
+      const int32_t qb = u - mq.div(u) * mq.d;
       rs = __ldg(row_ptr + qb);
       nt = __ldg(row_ptr + qb + 1) - rs;
       if (nt > 0) { valid = true; return; }
     }
     valid = false;
   }
-  __device__ void prefetch(const int32_t* row_ptr, int32_t mq, int32_t units) {
+  __device__ void prefetch(const int32_t* row_ptr, const FastDiv& mq, int32_t units) {
     pu = fwd_unit_at(k + 1);
     prs = pre = 0;
     if (pu < units) {
-      const int32_t qb = pu % mq;
+      const int32_t qb = pu - mq.div(pu) * mq.d;
       prs = __ldg(row_ptr + qb);
       pre = __ldg(row_ptr + qb + 1);
     }
   }
-  __device__ void init(const int32_t* row_ptr, int32_t mq, int32_t units) {
+  __device__ void init(const int32_t* row_ptr, const FastDiv& mq, int32_t units) {
     k = 0; t = 0; n = 0; from_pf = false;
     seek(row_ptr, mq, units);
     if (valid) prefetch(row_ptr, mq, units);
   }
-  __device__ void advance(const int32_t* row_ptr, int32_t mq, int32_t units) {
+  __device__ void advance(const int32_t* row_ptr, const FastDiv& mq, int32_t units) {
     if (++t < nt) return;
     t = 0; ++n; ++k;
     if (pu >= units) { valid = false; return; }
@@ -299,7 +329,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       // O tile of unit us (staged in Q stage qs, swizzled like a loaded tile) -> global;
       // ragged tiles were written row by row by the softmax warps
       auto store_o = [&](int qs, int32_t us) {
-        const int32_t sqb = us % mq, sh = (us / mq) % prm.heads, sb = us / (mq * prm.heads);
+        const int32_t bh_s = prm.mq_div.div(us), sqb = us - bh_s * mq;
+        const int32_t sb = prm.heads_div.div(bh_s), sh = bh_s - sb * prm.heads;
         if ((sqb + 1) * kBlock > prm.N) return;
         if (kGather) {
           const int4 c = row_cells<true>(prm.N, sqb * kBlock, prm.s2c, lane);
@@ -314,14 +345,15 @@ __global__ void __launch_bounds__(kThreads, 2)
         __syncwarp();
       };
       FwdIter it;
-      it.init(prm.row_ptr, mq, units);
+      it.init(prm.row_ptr, prm.mq_div, units);
       int32_t meta = 0, pmeta = 0;
       if (warp != 0 && it.valid) {
         meta = load_meta(prm.col_idx, prm.kind, it.rs, it.nt, lane);
         pmeta = load_meta(prm.col_idx, prm.kind, it.prs, it.pre - it.prs, lane);
       }
       while (it.valid) {
-        const int32_t qb = it.u % mq, h = (it.u / mq) % prm.heads, b = it.u / (mq * prm.heads);
+        const int32_t bh_u = prm.mq_div.div(it.u), qb = it.u - bh_u * mq;
+        const int32_t b = prm.heads_div.div(bh_u), h = bh_u - b * prm.heads;
         const int64_t bh = (int64_t)b * prm.heads + h;
         if (warp == 0) {
           // Q(n) goes into stage n&1, which holds O(n-2) staged by the softmax warps:
@@ -365,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
         }
         it.t = it.nt - 1;
-        it.advance(prm.row_ptr, mq, units);
+        it.advance(prm.row_ptr, prm.mq_div, units);
         if (warp != 0 && it.valid) {
           meta = it.from_pf ? pmeta : load_meta(prm.col_idx, prm.kind, it.rs, it.nt, lane);
           pmeta = load_meta(prm.col_idx, prm.kind, it.prs, it.pre - it.prs, lane);
@@ -395,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         sm100::mma_commit(&sm.s_full);
       };
       FwdIter it;   // always one tile ahead of the PV being issued
-      it.init(prm.row_ptr, mq, units);
+      it.init(prm.row_ptr, prm.mq_div, units);
       uint32_t g = 0;
       if (it.valid) {
         sm100::mbar_wait(&sm.q_full[0], 0);
@@ -406,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       HLA_PMARK(tl0);
       while (it.valid) {
         const int32_t ct = it.t, cnt = it.nt;
-        it.advance(prm.row_ptr, mq, units);
+        it.advance(prm.row_ptr, prm.mq_div, units);
         // Two independent issues: S(g+1) (needs the softmax to have pulled S(g) into
         // registers, and the next Q / K landed) and PV(g) (needs P(g)).  Whichever is
         // ready first goes first: waiting for one in a fixed order stalls the other
@@ -447,10 +479,16 @@ __global__ void __launch_bounds__(kThreads, 2)
       prof[16] = (unsigned long long)(clock64() - prof_c0);   // this CTA's cycles until its last PV issue
       prof[17] = prof_g0;                                       // globaltimer (ns) at start / end
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof[18]));
+      {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        prof[23] = smid;
+      }
 #endif
       HLA_PFLUSH(0, 3, true);
       HLA_PFLUSH(15, 19, true);
       HLA_PFLUSH(20, 22, true);
+      HLA_PFLUSH(23, 24, true);
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
@@ -464,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const float sl2 = prm.scale_log2;
     uint32_t g = 0;
     FwdIter it;
-    it.init(prm.row_ptr, mq, units);
+    it.init(prm.row_ptr, prm.mq_div, units);
     int32_t meta = 0, pmeta = 0;
     if (it.valid) {
       meta = load_meta(prm.col_idx, prm.kind, it.rs, it.nt, lane);
@@ -472,7 +510,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     // RPB: the row's table offset A_q (per unit); the keys' B_k come staged with K
     while (it.valid) {
-      const int32_t qb = it.u % mq, h = (it.u / mq) % prm.heads, b = it.u / (mq * prm.heads);
+      const int32_t bh_u = prm.mq_div.div(it.u), qb = it.u - bh_u * mq;
+      const int32_t b = prm.heads_div.div(bh_u), h = bh_u - b * prm.heads;
       const int32_t q = qb * kBlock + row;
       float m_ref = -INFINITY, l = 0.f;
       const RowBox box = row_box(prm.pat, q);
@@ -488,6 +527,27 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (t == 0) HLA_PADD(19, tw0);
         if (row == 0) HLA_TR((2 << 24) | (1 << 16) | g);
         sm100::tc_fence_after();
+        const int32_t tm = tile_meta(meta, prm.col_idx, prm.kind, it.rs, t);
+        // partial tile that misses all 32 rows of this warp (1D windows: the warps away
+        // from the window's edge): no S load, mask or exponentials -- P rows of zero
+        if ((tm & 3) == 2 &&
+            __all_sync(0xffffffffu, !real || row_misses_tile<kTwoD>(prm.pat, box, (tm >> 2) * prm.col_mul))) {
+          sm100::tc_fence_before();
+          sm100::mbar_arrive(&sm.s_free);   // after s_full(g): phases of the S handshake stay in step
+          if (g > 0) {
+            sm100::mbar_wait(&sm.pv_done, (g - 1) & 1);
+            sm100::tc_fence_after();
+          }
+          uint32_t z[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) z[e] = 0u;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) sm100::tmem_st16(tmem + lane_off + kColP + c * 16, z);
+          sm100::tmem_wait_st();
+          sm100::tc_fence_before();
+          sm100::mbar_arrive(&sm.p_full);
+          continue;
+        }
         // the whole S row: four loads in flight, one wait (TMEM round trip ~200 cycles)
         uint32_t sr[kBlock];
 #pragma unroll
@@ -499,7 +559,6 @@ __global__ void __launch_bounds__(kThreads, 2)
         sm100::mbar_arrive(&sm.s_free);          // the MMA may overwrite S with S(g+1)
         HLA_PADD(4, ts0);
         float (&s)[kBlock] = *reinterpret_cast<float(*)[kBlock]>(sr);
-        const int32_t tm = tile_meta(meta, prm.col_idx, prm.kind, it.rs, t);
         // kBias: scores move to the log2 domain here (s = S * scale * log2e + bias * log2e)
         // so that the mask, the max and the exponentials see the biased score
         const float sl2e = kBias ? 1.f : sl2;
@@ -623,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       HLA_PADD(9, te0);
       tiles_done += it.nt;
       it.t = it.nt - 1;
-      it.advance(prm.row_ptr, mq, units);
+      it.advance(prm.row_ptr, prm.mq_div, units);
       if (it.valid) {
         meta = it.from_pf ? pmeta : load_meta(prm.col_idx, prm.kind, it.rs, it.nt, lane);
         pmeta = load_meta(prm.col_idx, prm.kind, it.prs, it.pre - it.prs, lane);
@@ -749,6 +808,8 @@ extern "C" hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_ma
   prm.N = pat.N;
   prm.heads = heads;
   prm.batch = batch;
+  prm.mq_div = make_fastdiv((pat.N + kBlock - 1) / kBlock);
+  prm.heads_div = make_fastdiv(heads);
   prm.scale_log2 = sc * 1.4426950408889634f;
   prm.row_ptr = lists.row_ptr;
   prm.col_idx = lists.col;
