@@ -165,6 +165,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     ug.mk = (prm.N + kBlock - 1) / kBlock;   // last kv-block may be ragged
     ug.ppb = (ug.mk + 1) / 2;
     ug.pairs = ug.ppb * prm.heads * prm.batch;
+    ug.mkd = prm.mk_div;
+    ug.ppbd = prm.ppb_div;
     const int32_t mk = ug.mk;
     if (warp != 1) {
       // ----------------------------------------------------------- TMA producers
@@ -182,7 +184,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int32_t u = unit_at(kq, ug);
         if (u == kUnitEnd) break;
         if (u < 0) continue;
-        const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
+        const int32_t bh_u = prm.mk_div.div(u), kb = u - bh_u * mk;
+        const int32_t b = prm.heads_div.div(bh_u), h = bh_u - b * prm.heads;
         const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
         if (nt == 0) continue;
         const int64_t bh = (int64_t)b * prm.heads + h;
@@ -367,13 +370,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     ug.mk = (prm.N + kBlock - 1) / kBlock;
     ug.ppb = (ug.mk + 1) / 2;
     ug.pairs = ug.ppb * prm.heads * prm.batch;
+    ug.mkd = prm.mk_div;
+    ug.ppbd = prm.ppb_div;
     const int32_t mk = ug.mk;
     uint32_t g = 0;
     for (int32_t kq = 0;; ++kq) {
       const int32_t u = unit_at(kq, ug);
       if (u == kUnitEnd) break;
       if (u < 0) continue;
-      const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
+      const int32_t bh_u = prm.mk_div.div(u), kb = u - bh_u * mk;
+      const int32_t b = prm.heads_div.div(bh_u), h = bh_u - b * prm.heads;
       const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
       const int32_t kidx = kb * kBlock + row;
       RowBox box = clip_box<kTwoD>(prm.pat, col_box(prm.pat, kidx));
@@ -525,6 +531,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     ug.mk = (prm.N + kBlock - 1) / kBlock;
     ug.ppb = (ug.mk + 1) / 2;
     ug.pairs = ug.ppb * prm.heads * prm.batch;
+    ug.mkd = prm.mk_div;
+    ug.ppbd = prm.ppb_div;
     const int32_t mk = ug.mk;
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
@@ -537,7 +545,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int32_t u = unit_at(kq, ug);
       if (u == kUnitEnd) break;
       if (u < 0) continue;
-      const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
+      const int32_t bh_u = prm.mk_div.div(u), kb = u - bh_u * mk;
+      const int32_t b = prm.heads_div.div(bh_u), h = bh_u - b * prm.heads;
       const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
       for (int t = 0; t < nt; ++t, ++g) {
         const uint32_t fdq = dq_plan(prm.t_dq, rs + t, g);
@@ -915,6 +924,12 @@ hla_status prepare_main(const hla_pattern_desc* d, const hla_block_mask* m, int3
   prm.N = pat.N;
   prm.heads = heads;
   prm.batch = batch;
+  {
+    const int32_t mkb = (pat.N + bwd::kBlock - 1) / bwd::kBlock;
+    prm.mk_div = make_fastdiv(mkb);
+    prm.ppb_div = make_fastdiv((mkb + 1) / 2);
+    prm.heads_div = make_fastdiv(heads);
+  }
   prm.scale = sc;
   prm.scale_log2 = sc * kLog2e;
   prm.t_row_ptr = lists.t_row_ptr;

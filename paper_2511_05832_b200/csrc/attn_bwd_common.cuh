@@ -16,6 +16,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 struct BwdParams {
   Pattern pat;
   int32_t N, heads, batch;
+  FastDiv mk_div, ppb_div, heads_div;   // kv-blocks per (b, h), kv-block pairs per (b, h), heads
   float scale, scale_log2, inv_scale;
   const int32_t* t_row_ptr;   // tile lists (AttnLists): per 128-key tile
   const int32_t* t_col_idx;
@@ -102,13 +103,14 @@ __device__ __forceinline__ uint64_t ds_mnmajor_desc(const uint8_t* ds, int kstep
 constexpr int32_t kUnitEnd = 0x7fffffff, kUnitSkip = -1;
 struct UnitGeom {
   int32_t mk, ppb, pairs;   // kv-blocks per (b, h), pairs per (b, h), pairs in total
+  FastDiv mkd, ppbd;        // division by mk / ppb (multiply-shift)
 };
 // k-th kv-block of this CTA: flattened u = (b * heads + h) * mk + kb, kUnitSkip for
 // the missing second block of a ragged last pair, kUnitEnd past the last pair
 __device__ __forceinline__ int32_t unit_at(int32_t k, const UnitGeom& ug) {
   const int32_t P = (int32_t)blockIdx.x + (k >> 1) * (int32_t)gridDim.x;
   if (P >= ug.pairs) return kUnitEnd;
-  const int32_t bh = P / ug.ppb;
+  const int32_t bh = ug.ppbd.div(P);
   const int32_t kb = 2 * (P - bh * ug.ppb) + (k & 1);
   return kb < ug.mk ? bh * ug.mk + kb : kUnitSkip;
 }
@@ -124,7 +126,7 @@ struct TileIter {
       u = unit_at(k, ug);
       if (u == kUnitEnd) break;
       if (u < 0) continue;
-      const int32_t kb = u % ug.mk;
+      const int32_t kb = u - ug.mkd.div(u) * ug.mk;
       rs = __ldg(t_row_ptr + kb);
       nt = __ldg(t_row_ptr + kb + 1) - rs;
       if (nt > 0) { valid = true; return; }

@@ -71,6 +71,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   ug.mk = (prm.N + kBlock - 1) / kBlock;   // last kv-block may be ragged
   ug.ppb = (ug.mk + 1) / 2;
   ug.pairs = ug.ppb * prm.heads * prm.batch;
+    ug.mkd = prm.mk_div;
+    ug.ppbd = prm.ppb_div;
   const int32_t mk = ug.mk;
 
   if (warp == 0 && lane == 0) {
@@ -123,7 +125,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int32_t u = unit_at(kq, ug);
         if (u == kUnitEnd) break;
         if (u < 0) continue;
-        const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
+        const int32_t bh_u = prm.mk_div.div(u), kb = u - bh_u * mk;
+        const int32_t b = prm.heads_div.div(bh_u), h = bh_u - b * prm.heads;
         const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
         if (nt == 0) continue;
         const int64_t bh = (int64_t)b * prm.heads + h;
@@ -311,7 +314,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int32_t u = unit_at(kq, ug);
       if (u == kUnitEnd) break;
       if (u < 0) continue;
-      const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
+      const int32_t bh_u = prm.mk_div.div(u), kb = u - bh_u * mk;
+      const int32_t b = prm.heads_div.div(bh_u), h = bh_u - b * prm.heads;
       const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
       const int32_t kidx = kb * kBlock + row;
       RowBox box = clip_box<kTwoD>(prm.pat, col_box(prm.pat, kidx));
@@ -520,7 +524,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int32_t u = unit_at(kq, ug);
       if (u == kUnitEnd) break;
       if (u < 0) continue;
-      const int32_t kb = u % mk, h = (u / mk) % prm.heads, b = u / (mk * prm.heads);
+      const int32_t bh_u = prm.mk_div.div(u), kb = u - bh_u * mk;
+      const int32_t b = prm.heads_div.div(bh_u), h = bh_u - b * prm.heads;
       const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
       for (int t = 0; t < nt; ++t, ++g) {
         const uint32_t fdq = dq_plan(prm.t_dq, rs + t, g);

@@ -44,23 +44,6 @@ constexpr int kThreads = 256;   // warpgroup 0: TMA (Q), MMA, TMA (K), TMA (V); 
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kColS = 0, kColP = 128, kColO = 192;
 
-// floor(n / d) for 0 <= n < 2^31 as one wide multiply and a shift (Granlund-Montgomery:
-// m = ceil(2^(31+l) / d), l = ceil(log2 d)); the unit decode at every unit boundary of
-// every role otherwise runs three integer divisions on its critical path
-struct FastDiv {
-  uint32_t m, s;
-  int32_t d;
-  __device__ __forceinline__ int32_t div(int32_t n) const {
-    return (int32_t)(((uint64_t)(uint32_t)n * m) >> s);
-  }
-};
-inline FastDiv make_fastdiv(int32_t d) {
-  uint32_t l = 0;
-  while ((1ll << l) < d) ++l;
-  const uint64_t p = 1ull << (31 + l);
-  return FastDiv{(uint32_t)((p + (uint64_t)d - 1) / (uint64_t)d), 31 + l, d};
-}
-
 struct FwdParams {
   Pattern pat;
   FastDiv mq_div, heads_div;   // q-blocks per (b, h); heads

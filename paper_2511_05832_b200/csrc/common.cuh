@@ -113,6 +113,23 @@ extern __device__ unsigned long long g_hla_trace[8 * 1024 * 2];
   } while (0)
 #endif
 
+// floor(n / d) for 0 <= n < 2^31 as one wide multiply and a shift (Granlund-Montgomery:
+// m = ceil(2^(31+l) / d), l = ceil(log2 d)); the unit decode at every unit boundary of
+// every role otherwise runs three integer divisions on its critical path (fwd + bwd)
+struct FastDiv {
+  uint32_t m, s;
+  int32_t d;
+  __device__ __forceinline__ int32_t div(int32_t n) const {
+    return (int32_t)(((uint64_t)(uint32_t)n * m) >> s);
+  }
+};
+inline FastDiv make_fastdiv(int32_t d) {
+  uint32_t l = 0;
+  while ((1ll << l) < d) ++l;
+  const uint64_t p = 1ull << (31 + l);
+  return FastDiv{(uint32_t)((p + (uint64_t)d - 1) / (uint64_t)d), 31 + l, d};
+}
+
 // ---- dev-only wait-time accounting (variant builds) --------------------
 // Build with the kernel's switch (HLA_BWD_PROF / HLA_FWD_PROF; its .cu file then defines
 // HLA_PROF_ON before its includes and HLA_PROF_ARRAY after them): one thread per role sums
