@@ -19,7 +19,8 @@ void clear_error() { g_err[0] = 0; }
 
 // Validate a pattern descriptor (S:L98-100 argument rules) and lower it to the
 // device predicate parameters.
-hla_status make_pattern(const hla_pattern_desc* d, Pattern* p) {
+namespace {
+hla_status make_pattern_fields(const hla_pattern_desc* d, Pattern* p) {
   HLA_REQUIRE(d != nullptr && p != nullptr, HLA_ERR_INVALID, "null descriptor");
   HLA_REQUIRE(d->grid_h >= 1 && d->grid_w >= 1, HLA_ERR_INVALID, "grid %dx%d invalid", d->grid_h, d->grid_w);
   int64_t N = (int64_t)d->grid_h * d->grid_w;
@@ -91,6 +92,17 @@ hla_status make_pattern(const hla_pattern_desc* d, Pattern* p) {
     default: break;
   }
   HLA_REQUIRE(false, HLA_ERR_INVALID, "pattern %d invalid", d->pattern);
+}
+}  // namespace
+
+hla_status make_pattern(const hla_pattern_desc* d, Pattern* p) {
+  const hla_status st = make_pattern_fields(d, p);
+  if (st != HLA_OK) return st;
+  p->n_div = make_fastdiv(p->n > 0 ? p->n : 1);
+  p->w_div = make_fastdiv(p->W);
+  p->kh_div = make_fastdiv(p->kh > 0 ? p->kh : 1);
+  p->kw_div = make_fastdiv(p->kw > 0 ? p->kw : 1);
+  return HLA_OK;
 }
 
 }  // namespace hla

@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   if (!kTwoD) {
                     ok = (uint32_t)(qq - box.lo) < (uint32_t)box.len;
                   } else {
-                    const int32_t rq = prm.pat.log2W >= 0 ? (qq >> prm.pat.log2W) : qq / prm.pat.W;
+                    const int32_t rq = prm.pat.log2W >= 0 ? (qq >> prm.pat.log2W) : prm.pat.w_div.div(qq);
                     const int32_t cq = qq - rq * prm.pat.W;
                     ok = ((uint32_t)(rq - box.lo) < (uint32_t)box.len) && ((uint32_t)(cq - box.c0) < (uint32_t)box.cn);
                   }

@@ -167,15 +167,16 @@ __device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* map, 
 }
 
 // cell -> (row << 16) | col (RPB offsets; grid sides < 2^15)
-__device__ __forceinline__ int32_t rpb_cell_rc(const int32_t* cells, int32_t seq, int32_t N, int32_t W) {
+__device__ __forceinline__ int32_t rpb_cell_rc(const int32_t* cells, int32_t seq, int32_t N, const FastDiv& W) {
   const int32_t cell = seq < N ? (cells ? __ldg(cells + seq) : seq) : 0;
-  const int32_t r = cell / W;
-  return (r << 16) | (cell - r * W);
+  const int32_t r = W.div(cell);
+  return (r << 16) | (cell - r * W.d);
 }
 // min / max of the rows and columns of the cells of sequence block [s0, s0 + 128)
 // (phantom positions >= N ignored); identical in every lane.
 struct CellBox { int32_t r0, r1, c0, c1; };
-__device__ __forceinline__ CellBox rpb_block_box(const int32_t* cells, int32_t s0, int32_t N, int32_t W, int lane) {
+__device__ __forceinline__ CellBox rpb_block_box(const int32_t* cells, int32_t s0, int32_t N, const FastDiv& W,
+                                                 int lane) {
   CellBox bx{1 << 30, -(1 << 30), 1 << 30, -(1 << 30)};
 #pragma unroll
   for (int j = 0; j < 4; ++j) {

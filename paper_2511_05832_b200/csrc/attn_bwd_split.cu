@@ -158,10 +158,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (kBias) {
               // A_q = (qr + H - 1)(2W - 1) + qc + W - 1 of the q-block's 128 columns (phantom: cell 0),
               // read by the compute warps as warp-uniform 16-B loads next to LSE / D
-              const int4 rc = make_int4(rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane, prm.N, prm.grid_w),
-                                        rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane + 1, prm.N, prm.grid_w),
-                                        rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane + 2, prm.N, prm.grid_w),
-                                        rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane + 3, prm.N, prm.grid_w));
+              const int4 rc = make_int4(rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane, prm.N, prm.pat.w_div),
+                                        rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane + 1, prm.N, prm.pat.w_div),
+                                        rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane + 2, prm.N, prm.pat.w_div),
+                                        rpb_cell_rc(prm.cells, qblk * prm.col_mul + 4 * lane + 3, prm.N, prm.pat.w_div));
               const int32_t a0 = (prm.grid_h - 1) * prm.rpb_w + prm.grid_w - 1;
               auto a_of = [&](int32_t v) { return a0 + (v >> 16) * prm.rpb_w + (v & 0xffff); };
               sm100::sts_u4(sm100::smem_u32(sm.qa[s]) + 16u * lane, a_of(rc.x), a_of(rc.y), a_of(rc.z), a_of(rc.w));
@@ -326,11 +326,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float* rpbh = nullptr;
       float* drpbh = nullptr;
       if (kBias) {
-        const int32_t rc = rpb_cell_rc(prm.cells, kidx, prm.N, prm.grid_w);
+        const int32_t rc = rpb_cell_rc(prm.cells, kidx, prm.N, prm.pat.w_div);
         k_r = rc >> 16;
         k_c = rc & 0xffff;
         k_b = k_r * prm.rpb_w + k_c;
-        kbox = rpb_block_box(prm.cells, kb * kBlock, prm.N, prm.grid_w, lane);
+        kbox = rpb_block_box(prm.cells, kb * kBlock, prm.N, prm.pat.w_div, lane);
         rpbh = prm.rpb + (int64_t)h * prm.rpb_hw;
         drpbh = prm.drpb + (int64_t)h * prm.rpb_hw;
       }
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int32_t dr0 = 0, dc0 = 0, wc = 0, wrows = 0, wcols = 0, kwb = 0;
         bool win = false;
         if (kBias) {
-          const CellBox qbox = rpb_block_box(prm.cells, q0, prm.N, prm.grid_w, lane);
+          const CellBox qbox = rpb_block_box(prm.cells, q0, prm.N, prm.pat.w_div, lane);
           dr0 = qbox.r0 - kbox.r1;
           dc0 = qbox.c0 - kbox.c1;
           // window = the box's offset rows at the table's own row stride, so that the element
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (!kTwoD) {
                   ok = (uint32_t)(qq - box.lo) < (uint32_t)box.len;
                 } else {
-                  const int32_t rq = prm.pat.log2W >= 0 ? (qq >> prm.pat.log2W) : qq / prm.pat.W;
+                  const int32_t rq = prm.pat.log2W >= 0 ? (qq >> prm.pat.log2W) : prm.pat.w_div.div(qq);
                   const int32_t cq = qq - rq * prm.pat.W;
                   ok = ((uint32_t)(rq - box.lo) < (uint32_t)box.len) && ((uint32_t)(cq - box.c0) < (uint32_t)box.cn);
                 }
@@ -493,8 +493,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           sm100::named_bar_sync(3, 256);
           const float inv_fx = rpb_fx > 0.f ? 1.f / rpb_fx : 0.f;   // (nothing accumulated without a scale)
           const int tid = (warp - 2) * 32 + lane;
-          for (int i = tid; i < wrows * wcols; i += 256) {   // only the box's used columns
-            const int32_t ir = i / wcols, ic = i - ir * wcols;
+          // only the box's used columns: entries i = tid, tid + 256, ... as (ir, ic), stepped
+          // without a division per entry
+          const int32_t wcs = wcols > 0 ? wcols : 1;
+          const int32_t step_r = 256 / wcs, step_c = 256 - step_r * wcs;
+          int32_t ir = wcols > 0 ? tid / wcs : wrows, ic = tid - (tid / wcs) * wcs;
+          for (; ir < wrows; ir += step_r, ic += step_c) {
+            if (ic >= wcols) { ic -= wcols; ++ir; if (ir >= wrows) break; }
             const int32_t v = sm.rpb_win[ir * wc + ic];
             if (v != 0) {
               atomicAdd(drpbh + (dr0 + ir + prm.grid_h - 1) * prm.rpb_w + (dc0 + ic + prm.grid_w - 1),

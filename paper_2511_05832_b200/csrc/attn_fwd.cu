@@ -136,7 +136,7 @@ __device__ __forceinline__ void apply_row_mask(float (&s)[kBlock], const Pattern
 #pragma unroll
     for (int c = 0; c < kBlock; ++c) {
       const int32_t k = k0 + c;
-      const int32_t rk = k / W, ck = k - rk * W;
+      const int32_t rk = pat.w_div.div(k), ck = k - rk * W;
       const bool ok = ((uint32_t)(rk - box.lo) < (uint32_t)box.len) &&
                       ((uint32_t)(ck - box.c0) < (uint32_t)box.cn);
       if (!ok) s[c] = -INFINITY;
@@ -152,7 +152,7 @@ __device__ __forceinline__ bool row_misses_tile(const Pattern& pat, const RowBox
   const RowBox box = clip_box<kTwoD>(pat, box_in);
   if (box.len <= 0) return true;
   if (!kTwoD) return box.lo + box.len <= k0 || box.lo >= k0 + kBlock;
-  const int32_t r0 = k0 / pat.W, r1 = (k0 + kBlock - 1) / pat.W;   // grid rows the tile's keys lie in
+  const int32_t r0 = pat.w_div.div(k0), r1 = pat.w_div.div(k0 + kBlock - 1);   // grid rows the tile's keys lie in
   return box.lo + box.len <= r0 || box.lo > r1;
 }
 
@@ -234,18 +234,19 @@ __device__ __forceinline__ int32_t tile_meta(int32_t meta, const int32_t* col, c
 //             P(g) (and before rescaling O) it waits pv_done(g-1)
 // Global RPB (reading R19): the table index of the pair (q, k) is
 // A_q - B_k with A_q = (qr + H - 1)(2W - 1) + qc + W - 1, B_k = kr (2W - 1) + kc.
-__device__ __forceinline__ int32_t rpb_cell_off(const int32_t* cells, int32_t seq, int32_t N, int32_t W, int32_t rw) {
+__device__ __forceinline__ int32_t rpb_cell_off(const int32_t* cells, int32_t seq, int32_t N, const FastDiv& W,
+                                                int32_t rw) {
   const int32_t cell = seq < N ? (cells ? __ldg(cells + seq) : seq) : 0;
-  const int32_t r = cell / W;
-  return r * rw + (cell - r * W);
+  const int32_t r = W.div(cell);
+  return r * rw + (cell - r * W.d);
 }
 // B_k of the 4 keys k0 + 4 lane .. + 3 of a kv tile (lane-distributed; 16-B loads)
-__device__ __forceinline__ int4 rpb_key_offs(const int32_t* cells, int32_t k0, int32_t N, int32_t W, int32_t rw,
-                                             int lane) {
+__device__ __forceinline__ int4 rpb_key_offs(const int32_t* cells, int32_t k0, int32_t N, const FastDiv& W,
+                                             int32_t rw, int lane) {
   const int32_t k = k0 + 4 * lane;
   int4 c = make_int4(0, 0, 0, 0);
   if (k < N) c = cells ? __ldg(reinterpret_cast<const int4*>(cells + k0) + lane) : make_int4(k, k + 1, k + 2, k + 3);
-  auto off = [&](int32_t cell) { const int32_t r = cell / W; return r * rw + (cell - r * W); };
+  auto off = [&](int32_t cell) { const int32_t r = W.div(cell); return r * rw + (cell - r * W.d); };
   return make_int4(off(c.x), off(c.y), off(c.z), off(c.w));
 }
 
@@ -369,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             if (s) tag1 = tag; else tag0 = tag;
             if (kBias && is_k) {
-              const int4 bk = rpb_key_offs(prm.cells, kvb * prm.col_mul, prm.N, prm.grid_w, prm.rpb_w, lane);
+              const int4 bk = rpb_key_offs(prm.cells, kvb * prm.col_mul, prm.N, prm.pat.w_div, prm.rpb_w, lane);
               sm100::sts_u4(sm100::smem_u32(sm.key_b[s]) + 16u * lane, bk.x, bk.y, bk.z, bk.w);
               __syncwarp();   // every lane's offsets are written before lane 0 arms k_full
             }
@@ -501,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       const bool real = q < prm.N;
       const int32_t ocell = kGather ? (real ? __ldg(prm.s2c + q) : 0) : q;   // fused inverse reorder of O (used at the end)
       const float* rpbh = kBias ? prm.rpb + (int64_t)h * prm.rpb_hw : nullptr;
-      const int32_t a_q = kBias ? prm.rpb_a0 + rpb_cell_off(prm.cells, q, prm.N, prm.grid_w, prm.rpb_w) : 0;
+      const int32_t a_q = kBias ? prm.rpb_a0 + rpb_cell_off(prm.cells, q, prm.N, prm.pat.w_div, prm.rpb_w) : 0;
       if (row == 0) HLA_TR((2 << 24) | (6 << 16) | it.n);
       for (int t = 0; t < it.nt; ++t, ++g) {
         HLA_PMARK(tw0);

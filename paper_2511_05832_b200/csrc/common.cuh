@@ -42,12 +42,30 @@ enum Kind : int32_t {
 };
 
 // Device-side description of the allowed(q, k) predicate.
+// floor(n / d) for 0 <= n < 2^31 as one wide multiply and a shift (Granlund-Montgomery:
+// m = ceil(2^(31+l) / d), l = ceil(log2 d)); the unit decode at every unit boundary of
+// every role otherwise runs three integer divisions on its critical path (fwd + bwd)
+struct FastDiv {
+  uint32_t m, s;
+  int32_t d;
+  __device__ __forceinline__ int32_t div(int32_t n) const {
+    return (int32_t)(((uint64_t)(uint32_t)n * m) >> s);
+  }
+};
+inline FastDiv make_fastdiv(int32_t d) {
+  uint32_t l = 0;
+  while ((1ll << l) < d) ++l;
+  const uint64_t p = 1ull << (31 + l);
+  return FastDiv{(uint32_t)((p + (uint64_t)d - 1) / (uint64_t)d), 31 + l, d};
+}
+
 struct Pattern {
   int32_t kind;
   int32_t N, H, W;
   int32_t n, r, L, shift;   // 1D (Hilbert) parameters: window n, radius r, HNA length L
   int32_t kh, kw;           // 2D (row-major) window / kernel
   int32_t log2W;            // log2(W) if W is a power of two, else -1
+  FastDiv n_div, w_div, kh_div, kw_div;   // division by n, W, kh, kw (multiply-shift)
 };
 
 hla_status make_pattern(const hla_pattern_desc* d, Pattern* p);
@@ -112,23 +130,6 @@ extern __device__ unsigned long long g_hla_trace[8 * 1024 * 2];
   do {              \
   } while (0)
 #endif
-
-// floor(n / d) for 0 <= n < 2^31 as one wide multiply and a shift (Granlund-Montgomery:
-// m = ceil(2^(31+l) / d), l = ceil(log2 d)); the unit decode at every unit boundary of
-// every role otherwise runs three integer divisions on its critical path (fwd + bwd)
-struct FastDiv {
-  uint32_t m, s;
-  int32_t d;
-  __device__ __forceinline__ int32_t div(int32_t n) const {
-    return (int32_t)(((uint64_t)(uint32_t)n * m) >> s);
-  }
-};
-inline FastDiv make_fastdiv(int32_t d) {
-  uint32_t l = 0;
-  while ((1ll << l) < d) ++l;
-  const uint64_t p = 1ull << (31 + l);
-  return FastDiv{(uint32_t)((p + (uint64_t)d - 1) / (uint64_t)d), 31 + l, d};
-}
 
 // ---- dev-only wait-time accounting (variant builds) --------------------
 // Build with the kernel's switch (HLA_BWD_PROF / HLA_FWD_PROF; its .cu file then defines

@@ -52,17 +52,18 @@ struct RowBox {
 __device__ __forceinline__ RowBox row_box(const Pattern& p, int32_t q) {
   RowBox b;
   switch (p.kind) {
-    case K_HWA: b.lo = (q / p.n) * p.n; b.len = p.n; b.c0 = 0; b.cn = 0; return b;
+    case K_HWA: b.lo = p.n_div.div(q) * p.n; b.len = p.n; b.c0 = 0; b.cn = 0; return b;
     case K_HSA: b.lo = q - p.r; b.len = 2 * p.r + 1; b.c0 = 0; b.cn = 0; return b;
     case K_HNA: b.lo = clampi(q - p.r, 0, p.N - p.L); b.len = p.L; b.c0 = 0; b.cn = 0; return b;
-    case K_HSWA: b.lo = floordiv(q - p.shift, p.n) * p.n + p.shift; b.len = p.n; b.c0 = 0; b.cn = 0; return b;
+    case K_HSWA:   // floor((q - shift) / n) with q - shift + n > 0 (0 < shift < n)
+      b.lo = (p.n_div.div(q - p.shift + p.n) - 1) * p.n + p.shift; b.len = p.n; b.c0 = 0; b.cn = 0; return b;
     case K_DENSE: b.lo = 0; b.len = p.N; b.c0 = 0; b.cn = 0; return b;
     default: break;
   }
-  int32_t rq = q / p.W, cq = q - rq * p.W;
+  int32_t rq = p.w_div.div(q), cq = q - rq * p.W;
   switch (p.kind) {
     case K_WSA:
-      b.lo = (rq / p.kh) * p.kh; b.len = p.kh; b.c0 = (cq / p.kw) * p.kw; b.cn = p.kw; return b;
+      b.lo = p.kh_div.div(rq) * p.kh; b.len = p.kh; b.c0 = p.kw_div.div(cq) * p.kw; b.cn = p.kw; return b;
     case K_SA:
       b.lo = rq - p.kh / 2; b.len = 2 * (p.kh / 2) + 1; b.c0 = cq - p.kw / 2; b.cn = 2 * (p.kw / 2) + 1; return b;
     default:  // K_NA2D
@@ -95,7 +96,7 @@ __device__ __forceinline__ RowBox col_box(const Pattern& p, int32_t k) {
   }
   if (p.kind == K_NA2D) {
     RowBox b;
-    const int32_t rk = k / p.W, ck = k - rk * p.W;
+    const int32_t rk = p.w_div.div(k), ck = k - rk * p.W;
     clamped_col_range(rk, p.kh / 2, p.kh, p.H, &b.lo, &b.len);
     clamped_col_range(ck, p.kw / 2, p.kw, p.W, &b.c0, &b.cn);
     return b;
