@@ -751,8 +751,8 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
                                                              float* __restrict__ dsum, float* __restrict__ lse2,
                                                              float* __restrict__ dq_acc,
                                                              const int32_t* __restrict__ s2c,
-                                                             const uint8_t* __restrict__ q_local, int32_t N,
-                                                             int32_t heads, int32_t rows) {
+                                                             const uint8_t* __restrict__ q_local, FastDiv N,
+                                                             FastDiv heads, int32_t rows) {
   // one thread per 8 elements (16 B of O and of dO); 32-bit index math (rows * D / 8 < 2^31).
   // Threads walk the OUTPUT order (b, h, s): D / LSE are written as contiguous runs (in
   // token order the 4-byte results of one warp land in `heads` different sectors).
@@ -761,10 +761,10 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
   const int32_t i = gid / kLanes;             // (b * heads + h) * N + s
   const int part = gid - i * kLanes;
   if (i >= rows) return;
-  const int32_t bh = i / N, s = i - bh * N;
-  const int32_t bb = bh / heads, hq = bh - bb * heads;
-  const int32_t r = (bb * N + s) * heads + hq;   // sequence-order row (b * N + s) * heads + h
-  const int64_t src = s2c ? ((int64_t)(bb * N + __ldg(s2c + s)) * heads + hq) : (int64_t)r;
+  const int32_t bh = N.div(i), s = i - bh * N.d;
+  const int32_t bb = heads.div(bh), hq = bh - bb * heads.d;
+  const int32_t r = (bb * N.d + s) * heads.d + hq;   // sequence-order row (b * N + s) * heads + h
+  const int64_t src = s2c ? ((int64_t)(bb * N.d + __ldg(s2c + s)) * heads.d + hq) : (int64_t)r;
   const uint4 a = __ldg(reinterpret_cast<const uint4*>(o + src * D + part * 8));
   const uint4 g = __ldg(reinterpret_cast<const uint4*>(dout + src * D + part * 8));
   const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
@@ -795,16 +795,16 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
 // Rows of local q-blocks (q_local: written by the main kernel) are left alone.
 __global__ void __launch_bounds__(256) dq_finalize_kernel(const float4* __restrict__ acc, uint4* __restrict__ dq,
                                                           const int32_t* __restrict__ s2c,
-                                                          const uint8_t* __restrict__ q_local, int32_t N,
-                                                          int32_t row_v, int32_t n_v) {
+                                                          const uint8_t* __restrict__ q_local, FastDiv N,
+                                                          FastDiv row_v, int32_t n_v) {
   const int32_t t = (int32_t)blockIdx.x * blockDim.x + threadIdx.x;   // n_v = B * N * row_v < 2^31
   if (t >= n_v) return;
   int64_t o = t;
   if (s2c || q_local) {   // t = (b * N + s) * row_v + part, row_v = heads * D / 8
-    const int32_t bs = t / row_v, part = t - bs * row_v;
-    const int32_t b = bs / N, s = bs - b * N;
+    const int32_t bs = row_v.div(t), part = t - bs * row_v.d;
+    const int32_t b = N.div(bs), s = bs - b * N.d;
     if (q_local && __ldg(q_local + (s >> 7))) return;
-    if (s2c) o = (int64_t)(b * N + __ldg(s2c + s)) * row_v + part;
+    if (s2c) o = (int64_t)(b * N.d + __ldg(s2c + s)) * row_v.d + part;
   }
   const float4 v0 = __ldcs(acc + 2 * (int64_t)t), v1 = __ldcs(acc + 2 * (int64_t)t + 1);
   dq[o] = make_uint4(sm100::pack_bf16(v0.x, v0.y), sm100::pack_bf16(v0.z, v0.w), sm100::pack_bf16(v1.x, v1.y),
@@ -878,13 +878,13 @@ extern "C" hla_status hla_attn_bwd_preprocess(int32_t batch, int32_t heads, int3
   if (head_dim == 64)
     bwd_preprocess_kernel<64><<<blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
                                                           reinterpret_cast<const __nv_bfloat16*>(dout), lse, sc,
-                                                          dsum, lse2, dq_acc, seq_to_cell, q_local, n, heads,
-                                                          (int32_t)rows);
+                                                          dsum, lse2, dq_acc, seq_to_cell, q_local, make_fastdiv(n),
+                                                          make_fastdiv(heads), (int32_t)rows);
   else
     bwd_preprocess_kernel<32><<<blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(o),
                                                           reinterpret_cast<const __nv_bfloat16*>(dout), lse, sc,
-                                                          dsum, lse2, dq_acc, seq_to_cell, q_local, n, heads,
-                                                          (int32_t)rows);
+                                                          dsum, lse2, dq_acc, seq_to_cell, q_local, make_fastdiv(n),
+                                                          make_fastdiv(heads), (int32_t)rows);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
 }
@@ -1020,8 +1020,8 @@ extern "C" hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_
   if (q_local && plan_mask->n_dq_nonlocal == 0) return HLA_OK;   // every dQ row written by the main kernel
   const unsigned blocks = (unsigned)((n_v + 255) / 256);
   dq_finalize_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const float4*>(dq_acc),
-                                                 reinterpret_cast<uint4*>(dq), seq_to_cell, q_local, n,
-                                                 heads * head_dim / 8, (int32_t)n_v);
+                                                 reinterpret_cast<uint4*>(dq), seq_to_cell, q_local, make_fastdiv(n),
+                                                 make_fastdiv(heads * head_dim / 8), (int32_t)n_v);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
 }
