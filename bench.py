@@ -164,12 +164,16 @@ def gather_rank_stats(values, dist=None, device=None):
 
 
 # ------------------------------------------------------------------ helpers
-def bwd_bytes(T, d, mask):
+def bwd_bytes(T, d, mask, fused_pre=False):
     """Algorithmic HBM bytes of the backward main kernel per launch: read Q, K, V, dO (8d per
     token-head), LSE, D (8); write dK, dV (4d); dQ: bf16 write (2d) for the q-blocks the dQ
-    plan keeps local, one fp32 read + write of the accumulator (8d, TMA reduce-add) for the others."""
+    plan keeps local, one fp32 read + write of the accumulator (8d, TMA reduce-add) for the others.
+    fused_pre (preprocess folded into the kernel, every q-block local): read O (2d) and the raw
+    LSE (4) instead of LSE, D: T (14d + 4) + T 2d."""
     mq = mask.row_ptr.numel() - 1
     nl = mq if mask.n_dq_nonlocal < 0 else mask.n_dq_nonlocal
+    if fused_pre:
+        return int(T * (16 * d + 4))
     return int(T * (12 * d + 8) + T * (2 * d * (mq - nl) + 8 * d * nl) // mq)
 
 
@@ -456,7 +460,7 @@ def run_stack(args):
     for lay, (q, _, _, _) in layers:
         T = q.shape[0] * q.shape[1] * q.shape[2]
         tb["fwd"] += T * (8 * d + 4)
-        tb["bwd"] += bwd_bytes(T, d, lay.mask)
+        tb["bwd"] += bwd_bytes(T, d, lay.mask, lay.fused_bwd)
     dom = max(("fwd", "bwd"), key=lambda kk: per.get(kk, 0.0))
     ach = tb[dom] / (per[dom] * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm"], "unit": "GB/s",
@@ -531,7 +535,7 @@ def run_single(args):
     rk, rv, rbound = invariant_residuals(dk, dv, do)
 
     tiles = layer.tiles * Bs * Hs   # executed 128 x 128 tiles (block 64: windows)
-    attn_ms = stages["fwd"] + stages["bwd_pre"] + stages["bwd"] + stages["bwd_fin"]
+    attn_ms = stages["fwd"] + stages.get("bwd_pre", 0.0) + stages["bwd"] + stages.get("bwd_fin", 0.0)
 
     # --- variants on this rank's shard (same kernels): row-major baseline, dense FA, HWT's
     #     global RPB, and the unfused reorder (explicit hla_hilbert_perm passes: perm_ms) ---
@@ -543,7 +547,7 @@ def run_single(args):
             st_fn = lambda mark, lay=lay: lay.step(q, k, v, do, mark)   # noqa: E731
             tot, _, _, _ = _timed(st_fn, vsteps, 2, flush, False, None, dist, world)
             _, st, _, _ = _timed(st_fn, vsteps, 1, flush, True, None, dist, world)
-            a_ms = st["fwd"] + st["bwd_pre"] + st["bwd"] + st["bwd_fin"]
+            a_ms = st["fwd"] + st.get("bwd_pre", 0.0) + st["bwd"] + st.get("bwd_fin", 0.0)
             variants[name] = {"pattern": kind, "ms_per_step": round(statistics.mean(tot), 4),
                               "fwd_ms": round(st["fwd"], 4), "bwd_ms": round(a_ms - st["fwd"], 4),
                               "tiles_per_bh": lay.tiles,
@@ -556,7 +560,7 @@ def run_single(args):
         _, st, _, _ = _timed(st_fn, vsteps, 1, flush, True, None, dist, world)
         variants["global_rpb"] = {"pattern": cfg["kind"] + " + global RPB score_mod",
                                   "ms_per_step": round(statistics.mean(tot), 4), "fwd_ms": round(st["fwd"], 4),
-                                  "bwd_ms": round(st["bwd_pre"] + st["bwd"] + st["bwd_fin"], 4)}
+                                  "bwd_ms": round(st.get("bwd_pre", 0.0) + st["bwd"] + st.get("bwd_fin", 0.0), 4)}
         del lay
         if layer.hilbert and (g & (g - 1)) == 0:
             lay = hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, Bs, Hs, d, block=blk, device=dev, fused=False)
@@ -567,7 +571,8 @@ def run_single(args):
             variants["unfused_reorder"] = {"pattern": cfg["kind"] + " with explicit hla_hilbert_perm passes",
                                            "ms_per_step": round(statistics.mean(tot), 4),
                                            "perm_ms": round(sum(perm.values()), 4), "perm_breakdown_ms": perm,
-                                           "attn_ms": round(st["fwd"] + st["bwd_pre"] + st["bwd"] + st["bwd_fin"], 4)}
+                                           "attn_ms": round(st["fwd"] + st.get("bwd_pre", 0.0) + st["bwd"] +
+                                                            st.get("bwd_fin", 0.0), 4)}
             del lay
         rm = variants["row_major"]
         variants["speedup_attn_vs_row_major"] = round((rm["fwd_ms"] + rm["bwd_ms"]) / attn_ms, 3)
@@ -642,7 +647,7 @@ def run_single(args):
     T = Bs * Hs * N                              # token-heads per launch on this rank
     kern = {
         "fwd": {"bytes": T * (8 * d + 4), "flops": 4 * 128 * 128 * d * tiles, "name": "attn_fwd_kernel"},
-        "bwd": {"bytes": bwd_bytes(T, d, layer.mask), "flops": 10 * 128 * 128 * d * tiles,
+        "bwd": {"bytes": bwd_bytes(T, d, layer.mask, layer.fused_bwd), "flops": 10 * 128 * 128 * d * tiles,
                 "name": "attn_bwd_full_kernel / attn_bwd_split_kernel"},
     }
     dom = max((kk for kk in kern if kk in stages), key=lambda kk: stages[kk])
@@ -684,8 +689,9 @@ def run_single(args):
                                    % world) if plan else "replicas (no batch x head partition for %d ranks)" % world,
                    "l2": "flushed between timed steps (%d MiB write, untimed); warm_l2_ms without the flush"
                          % (L2_FLUSH_BYTES >> 20),
-                   "step": ("fwd+bwd_pre+bwd+bwd_fin (Hilbert reorder fused into the kernels)" if layer.fused else
-                            "fwd+bwd_pre+bwd+bwd_fin"),
+                   "step": ("fwd+bwd (preprocess folded into the backward kernel)" if layer.fused_bwd else
+                            "fwd+bwd_pre+bwd+bwd_fin") +
+                           (" (Hilbert reorder fused into the kernels)" if layer.fused else ""),
                    "mask": "built once before timing: %d of %d block-%d tiles per (b,h) non-empty, %d 128 x 128 "
                            "tiles executed" % (layer.nnz, ((N + blk - 1) // blk) ** 2, blk, layer.tiles),
                    "timing": "CUDA events: one start/end pair per step (value = mean, max over ranks); "

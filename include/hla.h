@@ -307,6 +307,10 @@ HLA_API hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_mask*
  * score_mod: as in hla_attn_fwd (same table); with global RPB, drpb receives the
  * table gradient (accumulated; hla_attn_bwd zeroes it first, hla_attn_bwd_main
  * does not).
+ * When the mask's dQ plan makes every q-block local and the full-tile schedule
+ * applies (hla_attn_bwd_fuses_preprocess), hla_attn_bwd launches the main kernel
+ * only: it reads the raw LSE and the O rows itself and forms D in the kernel (the
+ * workspace is then not touched).  Same results up to fp32 summation order of D.
  */
 HLA_API hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_mask* m,
                         int32_t batch, int32_t heads, int32_t head_dim, float scale,
@@ -348,6 +352,12 @@ HLA_API hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_t n
                                  cudaStream_t stream);
 
 HLA_API size_t hla_attn_bwd_workspace(int32_t batch, int32_t heads, int32_t n, int32_t head_dim);
+
+/* 1 if hla_attn_bwd folds the preprocess into its main kernel for this pattern, mask
+ * (with its dQ plan) and score_mod -- one launch instead of preprocess + main -- else 0
+ * (also 0 for invalid arguments).  Host-only; launches nothing. */
+HLA_API int32_t hla_attn_bwd_fuses_preprocess(const hla_pattern_desc* d, const hla_block_mask* m,
+                                              const hla_score_mod* score_mod);
 
 /* Thread-local message for the last non-OK status of this thread ("" if none). */
 HLA_API const char* hla_last_error(void);

@@ -21,7 +21,7 @@ STATUS_NAMES = {0: "HLA_OK", 1: "HLA_ERR_INVALID", 2: "HLA_ERR_UNSUPPORTED", 3: 
 EXPORTED = ("hla_hilbert_index", "hla_hilbert_perm", "hla_build_block_mask", "hla_mask_ratios",
             "hla_attn_fwd", "hla_attn_bwd", "hla_attn_bwd_workspace", "hla_attn_bwd_preprocess",
             "hla_attn_bwd_main", "hla_attn_bwd_finalize", "hla_build_bwd_plan", "hla_build_tile_lists",
-            "hla_last_error", "hla_version")
+            "hla_attn_bwd_fuses_preprocess", "hla_last_error", "hla_version")
 DEBUG_EXPORTED = ("hla_debug_umma", "hla_debug_gather4", "hla_debug_mma_rate",
                   "hla_debug_tmem_rate", "hla_debug_ex2_rate", "hla_debug_xu_rate", "hla_debug_sync_latency",
                   "hla_debug_softmax_rate", "hla_debug_softmax_tile", "hla_debug_load_rate")
@@ -76,6 +76,7 @@ _SIG = {
     "hla_attn_bwd_finalize": [_i32, _i32, _i32, _i32, _vp, _sz, _vp, _vp, _pmask, _vp],
     "hla_build_bwd_plan": [_pmask, _vp],
     "hla_build_tile_lists": [_pmask, ctypes.POINTER(_i64), _vp],
+    "hla_attn_bwd_fuses_preprocess": [_pdesc, _pmask, _vp],
 }
 _DEBUG_SIG = {
     "hla_debug_umma": [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp],

@@ -258,6 +258,12 @@ def hla_attn_bwd(desc, mask, q, k, v, o, lse, dout, scale=0.0, dq=None, dk=None,
     return dq, dk, dv
 
 
+def hla_attn_bwd_fuses_preprocess(desc, mask, mod=None):
+    """True if hla_attn_bwd folds the preprocess into its main kernel (one launch)."""
+    mc = mask.c
+    return bool(lib().hla_attn_bwd_fuses_preprocess(ctypes.byref(desc), ctypes.byref(mc), _sm(mod)))
+
+
 def _pm(mask):
     return ctypes.byref(mask.c) if mask is not None else None
 

@@ -72,6 +72,8 @@ class HilbertLocalAttention:
                 cells = self.s2c if self.s2c is not None else api.hla_hilbert_index(grid_h, grid_w, device)[0]
             self._cells = cells
             self.mod = api.score_mod(self._rpb, self._drpb, cells)
+        # backward as one launch when the library folds the preprocess into the main kernel
+        self.fused_bwd = api.hla_attn_bwd_fuses_preprocess(self.desc, self.mask, self.mod)
 
     @property
     def rpb(self):
@@ -134,6 +136,12 @@ class HilbertLocalAttention:
             dout_s, dq, dk, dv = self.dos, self.dqs, self.dks, self.dvs
         else:
             dout_s, dq, dk, dv = dout, self.dq, self.dk, self.dv
+        if self.fused_bwd:
+            # one launch: the main kernel forms D / LSE itself (every dQ chain local, full-tile schedule)
+            api.hla_attn_bwd(self.desc, self.mask, q, k, v, o, self.lse, dout_s, self.scale, dq, dk, dv,
+                             self.workspace, seq_to_cell=self.s2c, mod=self.mod)
+            mark("bwd")
+            return self._grads(mark)
         api.hla_attn_bwd_preprocess(o, dout_s, self.lse, self.workspace, self.scale, seq_to_cell=self.s2c,
                                     mask=self.mask)
         if self._drpb is not None:
@@ -144,6 +152,9 @@ class HilbertLocalAttention:
         mark("bwd")
         api.hla_attn_bwd_finalize(self.workspace, dq, seq_to_cell=self.s2c, mask=self.mask)
         mark("bwd_fin")
+        return self._grads(mark)
+
+    def _grads(self, mark):
         if self.hilbert and not self.fused:
             api.hla_hilbert_perm(self.grid_h, self.grid_w, api.FROM_HILBERT, (self.dqs, self.dks, self.dvs),
                                  (self.dq, self.dk, self.dv))
@@ -153,6 +164,8 @@ class HilbertLocalAttention:
     # kernel launches per step (forward + backward)
     @property
     def launches_per_step(self):
+        if self.fused_bwd:   # fwd + the backward's main kernel
+            return 2 + (4 if (self.hilbert and not self.fused) else 0) + (1 if self._rpb is not None else 0)
         fin = 0 if self.mask.n_dq_nonlocal == 0 else 1   # the finalize launches nothing when every dQ is local
         return 3 + fin + (4 if (self.hilbert and not self.fused) else 0) + (1 if self._rpb is not None else 0)
 

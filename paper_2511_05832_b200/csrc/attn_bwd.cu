@@ -97,6 +97,9 @@ struct FullSmem {
   alignas(16) float dd[kQStages][kBlock];
   uint64_t kv_full[2], kv_empty[2], q_full[kQStages], q_empty[kQStages], s_full, s_read, p_ready, ds_ready,
       dq_full[2], dq_free[2], dkv_full, epi_done;
+  // kFuse (preprocess folded in): O tile of a newly loaded q-block (in the dq_stage bytes,
+  // unused when every dQ chain is local), and D of stage s ready for the compute warps
+  uint64_t o_full, o_empty, d_full[kQStages];
   uint64_t dbg_bar;
   uint32_t tmem_base;
 };
@@ -106,7 +109,13 @@ struct FullSmem {
 // Q/dO) stream in while the current unit computes; the dK/dV epilogue of a unit
 // overlaps the first MMAs of the next one.  Phase counters: n = units with tiles so
 // far, g = (q-block) tiles so far.
-template <int D, bool kTwoD, bool kGather>
+// kFuse: the backward preprocess folded into the kernel (only when every q-block's dQ chain is
+// local, so the dq_stage bytes are free): warp 0 loads the raw LSE and the O tile of each newly
+// loaded q-block; the dQ warpgroup (thread = query row) forms D * scale = rowsum(dO o O) * scale
+// and LSE * log2(e) in the stage one tile ahead of its dQ drains and arrives on d_full, which the
+// compute warps wait for instead of q_full.  tmDQ is then the O map.  (Serving D inside the
+// group's waits by polling measured slower: the spinning warps take issue slots, DESIGN 6g.)
+template <int D, bool kTwoD, bool kGather, bool kFuse>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_full_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -134,6 +143,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     sm100::mbar_init(&sm.dkv_full, 1);
     sm100::mbar_init(&sm.epi_done, 128);
     sm100::mbar_init(&sm.dbg_bar, 1);
+    sm100::mbar_init(&sm.o_full, 1);
+    sm100::mbar_init(&sm.o_empty, 128);
+    for (int s = 0; s < kQStages; ++s) sm100::mbar_init(&sm.d_full[s], 128);
     sm100::fence_mbar_init();
     sm100::tma_prefetch_desc(&tmQ);
     sm100::tma_prefetch_desc(&tmK);
@@ -178,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_q = sm100::policy_evict_last();
       const int role = warp == 0 ? 0 : warp - 1;   // 0, 1, 2
       constexpr uint32_t kTile = Smem::kTileBytes;
-      uint32_t n = 0, g = 0;
+      uint32_t n = 0, g = 0, n_o = 0;
       int64_t stage_tag0 = -1, stage_tag1 = -1;   // (b, h, q-block) held by stage 0 / 1
       for (int32_t kq = 0;; ++kq) {
         const int32_t u = unit_at(kq, ug);
@@ -217,11 +229,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0 && (kVar & 4)) {
               sm100::mbar_arrive(&sm.q_full[s]);
             } else if (lane == 0) {
-              // LSE / D of the real rows only (ragged last tile: N % 4 == 0, so 16-B multiples)
+              // LSE / D of the real rows only (ragged last tile: N % 4 == 0, so 16-B multiples);
+              // kFuse: the raw LSE only (D is formed in the kernel from the O tile below)
               const uint32_t vbytes = (uint32_t)min(kBlock, prm.N - qblk * prm.col_mul) * 4u;
-              sm100::mbar_arrive_expect_tx(&sm.q_full[s], 2 * vbytes);
+              sm100::mbar_arrive_expect_tx(&sm.q_full[s], (kFuse ? 1 : 2) * vbytes);
               sm100::bulk_load(sm.lse[s], prm.lse2 + bh * prm.N + qblk * prm.col_mul, vbytes, &sm.q_full[s]);
-              sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * prm.col_mul, vbytes, &sm.q_full[s]);
+              if (!kFuse)
+                sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * prm.col_mul, vbytes, &sm.q_full[s]);
+            }
+            if (kFuse && !(kVar & 4)) {
+              // the q-block's O rows into the single O stage (freed by the dQ warps after D)
+              if (n_o > 0) sm100::mbar_wait(&sm.o_empty, (n_o - 1) & 1);
+              ++n_o;
+              if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.o_full, kTile);
+              __syncwarp();
+              load_rows<D, kGather>(reinterpret_cast<uint8_t*>(sm.dq_stage), &tmDQ, &sm.o_full, h, b, prm.N,
+                                    qblk * prm.col_mul, prm.s2c, pol_q, lane);
             }
           } else if (kVar & 4) {
             if (lane == 0) sm100::mbar_arrive(&sm.q_full[s]);
@@ -388,7 +411,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint8_t kd = __ldg(prm.t_kind + rs + t);
         const int32_t q0 = __ldg(prm.t_col_idx + rs + t) * prm.col_mul;
         const int s = g & 1;
-        HLA_PW(5, sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1));
+        HLA_PW(5, sm100::mbar_wait(kFuse ? &sm.d_full[s] : &sm.q_full[s], (g >> 1) & 1));
         const uint32_t lse2 = sm100::smem_u32(sm.lse[s]);
         const uint32_t dd = sm100::smem_u32(sm.dd[s]);
         const uint32_t dsbuf = sm100::smem_u32(sm.ds[g & 1]);
@@ -541,6 +564,50 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kEpCols = ep_cols<D>();
     uint32_t g = 0, n = 0;
     uint32_t dq_drained0 = 0, dq_drained1 = 0;   // chains drained per dQ accumulator
+    // kFuse: a cursor over the same tile sequence, one tile ahead of the drains (d_upto), forms
+    // D and the log2-domain LSE of each newly loaded q-block (the producer's stage tags, mirrored)
+    TileIter dit;
+    uint32_t gd = 0, n_od = 0;
+    int64_t dtag0 = -1, dtag1 = -1;
+    if (kFuse) dit.init(prm.t_row_ptr, ug);
+    auto d_step = [&]() {   // the cursor's next tile (waits for its operands)
+      const int s = gd & 1;
+      sm100::mbar_wait(&sm.q_full[s], (gd >> 1) & 1);
+      const int32_t bh_d = prm.mk_div.div(dit.u);
+      const int32_t bd = prm.heads_div.div(bh_d), hd = bh_d - bd * prm.heads;
+      const int32_t qblk = __ldg(prm.t_col_idx + dit.rs + dit.t);
+      const int64_t tag = ((int64_t)bd * prm.heads + hd) * prm.N + qblk;
+      if (tag != (s ? dtag1 : dtag0)) {
+        sm100::mbar_wait(&sm.o_full, n_od & 1);
+        if (s) dtag1 = tag; else dtag0 = tag;
+        ++n_od;
+        const uint32_t ob = sm100::smem_u32(sm.dq_stage), gb = sm100::smem_u32(sm.dO[s]);
+        float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+        for (int j = 0; j < D / 8; ++j) {
+          const uint32_t off = (uint32_t)row * (D * 2) + (uint32_t)j * 16u;
+          const uint32_t so = D == 64 ? sm100::swz128(off) : sm100::swz64(off);
+          const float4 a = sm100::lds_f4(ob + so), c = sm100::lds_f4(gb + so);
+          const float av[4] = {a.x, a.y, a.z, a.w}, cv[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t aw = __float_as_uint(av[e]), cw = __float_as_uint(cv[e]);
+            acc0 = fmaf(__uint_as_float(aw << 16), __uint_as_float(cw << 16), acc0);
+            acc1 = fmaf(__uint_as_float(aw & 0xffff0000u), __uint_as_float(cw & 0xffff0000u), acc1);
+          }
+        }
+        sm.dd[s][row] = (acc0 + acc1) * prm.scale;
+        if (qblk * prm.col_mul + row < prm.N) sm.lse[s][row] *= kLog2e;   // raw LSE -> log2 domain
+        sm100::fence_proxy_async_smem();   // before the async proxy refills the O / LSE stages
+        sm100::mbar_arrive(&sm.o_empty);
+      }
+      sm100::mbar_arrive(&sm.d_full[s]);
+      dit.advance(prm.t_row_ptr, ug);
+      ++gd;
+    };
+    auto d_upto = [&](uint32_t target) {
+      while (dit.valid && gd <= target) d_step();
+    };
     for (int32_t kq = 0;; ++kq) {
       const int32_t u = unit_at(kq, ug);
       if (u == kUnitEnd) break;
@@ -549,6 +616,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int32_t b = prm.heads_div.div(bh_u), h = bh_u - b * prm.heads;
       const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
       for (int t = 0; t < nt; ++t, ++g) {
+        if (kFuse) d_upto(g + 1);
         const uint32_t fdq = dq_plan(prm.t_dq, rs + t, g);
         if (!(fdq & HLA_DQ_DRAIN)) continue;   // the chain continues in TMEM
         const int dqb = (int)(fdq & HLA_DQ_BUF);
@@ -703,11 +771,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 4 && lane == 0 && prm.visited != nullptr && tiles_done > 0) atomicAdd(prm.visited, tiles_done);
 }
 
-template <int D, bool kTwoD, bool kGather>
+template <int D, bool kTwoD, bool kGather, bool kFuse>
 hla_status launch_full_t(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mdo,
                       const CUtensorMap& mdq, const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream) {
   const size_t smem = sizeof(FullSmem<D>) + 1024;
-  auto* fn = attn_bwd_full_kernel<D, kTwoD, kGather>;
+  auto* fn = attn_bwd_full_kernel<D, kTwoD, kGather, kFuse>;
   HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t pairs = (int64_t)((n_kblocks + 1) / 2) * prm.heads * prm.batch;   // work units (kv-block pairs)
   const int grid = (int)std::min<int64_t>(pairs, (int64_t)num_sms());
@@ -720,17 +788,25 @@ static_assert(sizeof(FullSmem<64>) + 1024 <= 227 * 1024, "bwd shared memory (d =
 
 }  // namespace
 
-hla_status launch_full(int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
+template <bool kFuse>
+hla_status launch_full_f(int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
+                         const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm,
+                         int32_t mkb, cudaStream_t stream) {
+  if (head_dim == 64) {
+    if (gather) return launch_full_t<64, false, true, kFuse>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
+    return two_d ? launch_full_t<64, true, false, kFuse>(mq, mk, mv, mdo, mdq, prm, mkb, stream)
+                 : launch_full_t<64, false, false, kFuse>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
+  }
+  if (gather) return launch_full_t<32, false, true, kFuse>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
+  return two_d ? launch_full_t<32, true, false, kFuse>(mq, mk, mv, mdo, mdq, prm, mkb, stream)
+               : launch_full_t<32, false, false, kFuse>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
+}
+
+hla_status launch_full(int head_dim, bool gather, bool two_d, bool fuse, const CUtensorMap& mq, const CUtensorMap& mk,
                        const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm,
                        int32_t mkb, cudaStream_t stream) {
-  if (head_dim == 64) {
-    if (gather) return launch_full_t<64, false, true>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
-    return two_d ? launch_full_t<64, true, false>(mq, mk, mv, mdo, mdq, prm, mkb, stream)
-                 : launch_full_t<64, false, false>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
-  }
-  if (gather) return launch_full_t<32, false, true>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
-  return two_d ? launch_full_t<32, true, false>(mq, mk, mv, mdo, mdq, prm, mkb, stream)
-               : launch_full_t<32, false, false>(mq, mk, mv, mdo, mdq, prm, mkb, stream);
+  return fuse ? launch_full_f<true>(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, mkb, stream)
+              : launch_full_f<false>(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, mkb, stream);
 }
 
 }  // namespace bwd
@@ -898,6 +974,7 @@ struct MainPlan {
   CUtensorMap mq, mk, mv, mdo, mdq;
   int32_t head_dim, mkb;
   bool gather, two_d, full;
+  bool fuse;   // preprocess folded into the full-tile kernel (hla_attn_bwd only)
 };
 
 hla_status prepare_main(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
@@ -975,13 +1052,30 @@ hla_status prepare_main(const hla_pattern_desc* d, const hla_block_mask* m, int3
   // schedule overlaps the partial tiles' masked compute better) and with the global RPB (only
   // the half-tile schedule has the dRPB window: at the previous tile's scale, no extra barrier)
   pl->full = prm.rpb == nullptr && lists.t_n_full >= lists.t_n_partial && lists.t_n_full > 0;
+  pl->fuse = false;
+  return HLA_OK;
+}
+
+// hla_attn_bwd: fold the preprocess into the full-tile kernel when every q-block's dQ chain is
+// local (the kernel's dq_stage then holds O tiles instead of dQ partials, and the accumulator is
+// never touched): no preprocess launch, the main kernel reads the raw LSE and O.
+hla_status try_fuse(MainPlan* pl, const hla_block_mask* m, int32_t batch, int32_t heads, const void* o,
+                    const float* lse) {
+  if (!pl->full || !plan_of(m, pl->prm.N) || m->n_dq_nonlocal != 0) return HLA_OK;
+  const int64_t tok = (int64_t)batch * pl->prm.N;
+  const hla_status st = pl->gather ? make_gather_map(&pl->mdq, o, tok, heads, pl->head_dim)
+                                   : make_rows_map(&pl->mdq, o, tok, heads, pl->head_dim, kBlock);
+  if (st != HLA_OK) return st;
+  pl->prm.lse2 = lse;
+  pl->prm.dsum = nullptr;
+  pl->fuse = true;
   return HLA_OK;
 }
 
 hla_status launch_main(const MainPlan& pl, cudaStream_t stream) {
   const bool bias = pl.prm.rpb != nullptr;
   if (pl.full)
-    return bwd::launch_full(pl.head_dim, pl.gather, pl.two_d, pl.mq, pl.mk, pl.mv, pl.mdo, pl.mdq, pl.prm,
+    return bwd::launch_full(pl.head_dim, pl.gather, pl.two_d, pl.fuse, pl.mq, pl.mk, pl.mv, pl.mdo, pl.mdq, pl.prm,
                             pl.mkb, stream);
   return bwd::launch_split(bias, pl.head_dim, pl.gather, pl.two_d, pl.mq, pl.mk, pl.mv, pl.mdo, pl.mdq, pl.prm,
                            pl.mkb, stream);
@@ -1026,6 +1120,25 @@ extern "C" hla_status hla_attn_bwd_finalize(int32_t batch, int32_t heads, int32_
   return HLA_OK;
 }
 
+extern "C" int32_t hla_attn_bwd_fuses_preprocess(const hla_pattern_desc* d, const hla_block_mask* m,
+                                                 const hla_score_mod* score_mod) {
+  Pattern pat;
+  AttnLists lists;
+  if (!d || !m || check_attn_args(d, m, 1, 1, 64, &pat, &lists) != HLA_OK) {
+    clear_error();
+    return 0;
+  }
+  const float* rpb = nullptr;
+  float* drpb = nullptr;
+  const int32_t* cells = nullptr;
+  if (parse_score_mod(d, score_mod, true, &rpb, &drpb, &cells) != HLA_OK) {
+    clear_error();
+    return 0;
+  }
+  const bool full = rpb == nullptr && lists.t_n_full >= lists.t_n_partial && lists.t_n_full > 0;
+  return full && plan_of(m, pat.N) && m->n_dq_nonlocal == 0 ? 1 : 0;
+}
+
 extern "C" hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
                                    int32_t head_dim, float scale, const void* q, const void* k, const void* v,
                                    const void* o, const float* lse, const void* dout, void* dq, void* dk, void* dv,
@@ -1042,6 +1155,8 @@ extern "C" hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_ma
   HLA_REQUIRE(((uintptr_t)o | (uintptr_t)dq) % 16 == 0, HLA_ERR_INVALID, "tensors must be 16-byte aligned");
   HLA_REQUIRE((int64_t)batch * pl.prm.N * heads * head_dim / 8 < (1ll << 31), HLA_ERR_UNSUPPORTED,
               "B * N * heads * head_dim too large");
+  if ((st = try_fuse(&pl, m, batch, heads, o, lse)) != HLA_OK) return st;
+  if (pl.fuse) return launch_main(pl, stream);   // D / LSE formed in the kernel; every dQ row written there
   if (pl.prm.drpb)   // the table gradient is accumulated: start from zero
     HLA_CUDA_TRY(cudaMemsetAsync(pl.prm.drpb, 0,
                                  sizeof(float) * heads * (2 * pl.prm.grid_h - 1) * (2 * pl.prm.grid_w - 1), stream));

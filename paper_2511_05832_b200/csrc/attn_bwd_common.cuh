@@ -65,8 +65,9 @@ __device__ __forceinline__ float rpb_next_scale(const float* wmax8, float cur) {
 
 // Kernel launch of one schedule for the head_dim / reorder / 2D-pattern variant; the maps
 // view Q, K, V, dO as bf16 rows and the fp32 dQ accumulator (see hla_attn_bwd_main).
-// (the full-tile schedule has no global-RPB path: RPB layers take the half-tile schedule)
-hla_status launch_full(int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
+// (the full-tile schedule has no global-RPB path: RPB layers take the half-tile schedule;
+// fuse: preprocess folded into the kernel, every dQ chain local, mdq = the O map, lse2 = raw LSE)
+hla_status launch_full(int head_dim, bool gather, bool two_d, bool fuse, const CUtensorMap& mq, const CUtensorMap& mk,
                        const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm,
                        int32_t n_kblocks, cudaStream_t stream);
 hla_status launch_split(bool bias, int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,

@@ -14,6 +14,7 @@ import torch
 
 import hla_synth
 import paper_2511_05832_b200 as hla
+from paper_2511_05832_b200 import api
 from oracle import attention as oatt
 from oracle import hilbert
 from oracle.patterns import Spec
@@ -315,8 +316,58 @@ def test_dq_plan_matches_no_plan(kind, g, w, B, H, d, fused):
     r2 = [t.clone() for t in (b.forward(q, k, v),) + b.backward(do)]
     torch.cuda.synchronize()
     assert torch.equal(r1[0], r2[0])
-    assert torch.equal(r1[2], r2[2]) and torch.equal(r1[3], r2[3])
+    assert torch.equal(r1[3], r2[3])   # dV = P^T dO: the same products in the same order
+    if a.fused_bwd:   # D formed in the kernel: fp32 summation order of rowsum(dO o O) differs
+        assert (r1[2].float() - r2[2].float()).abs().max().item() <= 2e-3
+    else:
+        assert torch.equal(r1[2], r2[2])
     assert (r1[1].float() - r2[1].float()).abs().max().item() <= 2e-3
+
+
+@pytest.mark.parametrize("g,w,B,H,d", [(64, 16, 2, 4, 64), (32, 16, 2, 3, 32), (48, 16, 1, 2, 64),
+                                       (16, 16, 1, 2, 64)])
+@pytest.mark.parametrize("fused", [True, False])
+def test_bwd_fused_preprocess_matches_staged(g, w, B, H, d, fused):
+    """hla_attn_bwd folds the preprocess into the full-tile kernel when every q-block's dQ is
+    local (HWA windows of whole 128-blocks, cfg2): D = rowsum(dO o O) and LSE log2(e) are formed
+    in the kernel from the raw LSE and the O tile.  Against the staged calls (preprocess ->
+    main -> finalize) on the same mask: dV bit-identical, dQ / dK within fp32 order of D; and
+    one (b, h) slice against the fp64 oracle."""
+    if not fused and g & (g - 1):
+        pytest.skip("the explicit permutation kernel needs a 2^k grid")
+    N = g * g
+    q, k, v, do = _inputs(B, N, H, d, seed=31)
+    lay = hla.HilbertLocalAttention("HWA", g, g, w, w, B, H, d, device=DEV, fused=fused)
+    assert lay.fused_bwd and lay.mask.n_dq_nonlocal == 0   # (windows of whole block pairs: never ragged)
+    lay.forward(q, k, v)
+    r1 = [t.clone() for t in lay.backward(do)]
+    # the staged path on the same mask, in the layer's sequence order
+    qq, kk, vv, oo = lay._saved
+    dos = do
+    if lay.hilbert and not lay.fused:
+        dos = torch.empty_like(do)
+        api.hla_hilbert_perm(g, g, api.TO_HILBERT, (do,), (dos,))
+    ws = torch.empty_like(lay.workspace)
+    dq2, dk2, dv2 = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
+    api.hla_attn_bwd_preprocess(oo, dos, lay.lse, ws, seq_to_cell=lay.s2c, mask=lay.mask)
+    api.hla_attn_bwd_main(lay.desc, lay.mask, qq, kk, vv, dos, dq2, dk2, dv2, ws, seq_to_cell=lay.s2c)
+    api.hla_attn_bwd_finalize(ws, dq2, seq_to_cell=lay.s2c, mask=lay.mask)
+    r2 = [dq2, dk2, dv2]
+    if lay.hilbert and not lay.fused:
+        r2 = [torch.empty_like(q) for _ in range(3)]
+        api.hla_hilbert_perm(g, g, api.FROM_HILBERT, (dq2, dk2, dv2), tuple(r2))
+    torch.cuda.synchronize()
+    assert torch.equal(r1[2], r2[2])
+    for x, y in zip(r1[:2], r2[:2]):
+        assert (x.float() - y.float()).abs().max().item() <= 2e-3
+    # one slice against the fp64 oracle (grid order in, grid order out)
+    spec = Spec("HWA", g, g, w, w)
+    s2c = hilbert.hilbert_order(g, g)[0]
+    b, h = B - 1, H - 1
+    sl = lambda t: to_np(t[b, :, h, :])[s2c]   # grid order -> sequence order   # noqa: E731
+    dq_r, dk_r, dv_r = oatt.attn_bwd_slice(sl(q), sl(k), sl(v), sl(do), spec)[:3]
+    for name, got, ref in (("dq", r1[0], dq_r), ("dk", r1[1], dk_r), ("dv", r1[2], dv_r)):
+        assert_close(name, sl(got), ref)
 
 
 def test_rpb_gradient_small_upstream_gradient():
