@@ -213,6 +213,64 @@ struct FwdIter {
   }
 };
 
+// FwdIter with the CSR row pointers loaded two units ahead (the softmax warpgroup, which has
+// the registers for it): at unit k those of unit k + 1 are already in registers, so the per-lane
+// CSR entries of k + 1 can be requested without an L2 round trip first; those of k + 2 are in
+// flight.  (The producer / MMA warps keep FwdIter: at 48 registers the extra state spills.)
+struct FwdIter2 : FwdIter {
+  int32_t qu, qrs, qre;  // unit k + 2
+  __device__ static void load_rp(const int32_t* row_ptr, const FastDiv& mq, int32_t units, int32_t kk, int32_t& uu,
+                                 int32_t& b0, int32_t& b1) {
+    uu = fwd_unit_at(kk);
+    b0 = b1 = 0;
+    if (uu < units) {
+      const int32_t qb = uu - mq.div(uu) * mq.d;
+      b0 = __ldg(row_ptr + qb);
+      b1 = __ldg(row_ptr + qb + 1);
+    }
+  }
+  __device__ void init(const int32_t* row_ptr, const FastDiv& mq, int32_t units) {
+    k = 0; t = 0; n = 0; from_pf = false;
+    seek(row_ptr, mq, units);
+    if (valid) {
+      load_rp(row_ptr, mq, units, k + 1, pu, prs, pre);
+      load_rp(row_ptr, mq, units, k + 2, qu, qrs, qre);
+    }
+  }
+  __device__ void advance(const int32_t* row_ptr, const FastDiv& mq, int32_t units) {
+    if (++t < nt) return;
+    t = 0; ++n; ++k;
+    if (pu >= units) { valid = false; return; }
+    if (pre > prs) {
+      u = pu; rs = prs; nt = pre - prs; valid = true; from_pf = true;
+      pu = qu; prs = qrs; pre = qre;
+      load_rp(row_ptr, mq, units, k + 2, qu, qrs, qre);
+    } else {
+      ++k;
+      seek(row_ptr, mq, units);
+      from_pf = false;
+      if (!valid) return;
+      load_rp(row_ptr, mq, units, k + 1, pu, prs, pre);
+      load_rp(row_ptr, mq, units, k + 2, qu, qrs, qre);
+    }
+  }
+};
+
+// A unit's CSR entries as loaded (lane i: tile i), packed only when the unit starts, so the
+// loads of the next unit's entries have no consumer (no scoreboard wait) before then.
+struct MetaRaw {
+  int32_t c, k;
+};
+__device__ __forceinline__ MetaRaw load_meta_raw(const int32_t* col, const uint8_t* kind, int32_t rs, int32_t nt,
+                                                 int lane) {
+  MetaRaw m{0, 0};
+  if (lane < nt) {
+    m.c = __ldg(col + rs + lane);
+    m.k = (int32_t)__ldg(kind + rs + lane);
+  }
+  return m;
+}
+
 // Per-lane copy of a unit's CSR entries (lane i holds tile i), packed col * 4 + kind;
 // tiles past 32 fall back to direct loads.
 __device__ __forceinline__ int32_t load_meta(const int32_t* col, const uint8_t* kind, int32_t rs, int32_t nt,
@@ -263,8 +321,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int s = 0; s < 2; ++s) {
       sm100::mbar_init(&sm.q_full[s], 1);
       sm100::mbar_init(&sm.o_staged[s], 128);   // softmax threads: O(n) staged in Q stage n&1
-      sm100::mbar_init(&sm.k_full[s], 1);
-      sm100::mbar_init(&sm.v_full[s], 1);
+      sm100::mbar_init(&sm.k_full[s], 2);   // producer warps 2 and 3
+      sm100::mbar_init(&sm.v_full[s], 2);
       sm100::mbar_init(&sm.kv_empty[s], 1);
     }
     sm100::mbar_init(&sm.s_full, 1);
@@ -355,17 +413,28 @@ __global__ void __launch_bounds__(kThreads, 2)
           issue_rows<D, kGather>(sm.q[qs], &tmQ, &sm.q_full[qs], h, b, prm.N, qb * kBlock, cells, pol_q, lane);
           ++n_units;
         } else {
+          // warps 2 and 3 both feed every K / V stage (k_full / v_full count 2).  Fused reorder:
+          // warp 2 + hh gathers rows [64 hh, 64 hh + 64) of K (lanes 0-15) and of V (lanes 16-31),
+          // so each tile's 32 gather4 ops are spread over two issuing warps (a warp's gather4 stream
+          // is rate-limited) and K's go first.  Plain order: warp 2 loads K, warp 3 V (one box each)
+          // and each arrives on the other barrier without bytes.
           const bool is_k = warp == 2;
+          const int hh = warp - 2;
+          constexpr uint32_t kTile = FwdSmem<D, kBias>::kTileBytes;
           for (int t = 0; t < it.nt; ++t, ++g) {
             const int s = g & 1;
-            uint64_t* full = is_k ? &sm.k_full[s] : &sm.v_full[s];
             const int32_t kvb = tile_meta(meta, prm.col_idx, prm.kind, it.rs, t) >> 2;
             const int64_t tag = bh * prm.N + kvb;
             const bool reuse = tag == (s ? tag1 : tag0);   // stage already holds this K/V tile
-            const int4 cells = reuse ? make_int4(0, 0, 0, 0) : row_cells<kGather>(prm.N, kvb * prm.col_mul, prm.s2c, lane);
+            const int32_t r0 = kvb * prm.col_mul + hh * 64 + 4 * (lane & 15);   // this lane's 4 rows (gather)
+            const int4 cells = (reuse || !kGather) ? make_int4(0, 0, 0, 0)
+                               : (r0 < prm.N ? __ldg(reinterpret_cast<const int4*>(prm.s2c + r0)) : make_int4(0, 0, 0, 0));
             if (g >= 2) sm100::mbar_wait(&sm.kv_empty[s], ((g >> 1) - 1) & 1);
             if (reuse) {
-              if (lane == 0) sm100::mbar_arrive(full);
+              if (lane == 0) {
+                sm100::mbar_arrive(&sm.k_full[s]);
+                sm100::mbar_arrive(&sm.v_full[s]);
+              }
               continue;
             }
             if (s) tag1 = tag; else tag0 = tag;
@@ -374,10 +443,25 @@ __global__ void __launch_bounds__(kThreads, 2)
               sm100::sts_u4(sm100::smem_u32(sm.key_b[s]) + 16u * lane, bk.x, bk.y, bk.z, bk.w);
               __syncwarp();   // every lane's offsets are written before lane 0 arms k_full
             }
-            if (lane == 0) sm100::mbar_arrive_expect_tx(full, FwdSmem<D, kBias>::kTileBytes);
-            __syncwarp();
-            issue_rows<D, kGather>(is_k ? sm.k[s] : sm.v[s], is_k ? &tmK : &tmV, full, h, b, prm.N,
-                                   kvb * prm.col_mul, cells, pol_kv, lane);
+            if (kGather) {
+              if (lane == 0) {
+                sm100::mbar_arrive_expect_tx(&sm.k_full[s], kTile / 2);
+                sm100::mbar_arrive_expect_tx(&sm.v_full[s], kTile / 2);
+              }
+              __syncwarp();
+              const bool lk = lane < 16;
+              const int32_t base = b * prm.N;
+              const int row = hh * 64 + 4 * (lane & 15);
+              sm100::tma_gather4((lk ? sm.k[s] : sm.v[s]) + row * D * 2, lk ? &tmK : &tmV,
+                                 lk ? &sm.k_full[s] : &sm.v_full[s], h * D, base + cells.x, base + cells.y,
+                                 base + cells.z, base + cells.w, pol_kv);
+            } else if (lane == 0) {
+              uint64_t* full = is_k ? &sm.k_full[s] : &sm.v_full[s];
+              sm100::mbar_arrive_expect_tx(full, kTile);
+              sm100::tma_load_3d(is_k ? sm.k[s] : sm.v[s], is_k ? &tmK : &tmV, full, 0, h, b * prm.N + kvb * prm.col_mul,
+                                 pol_kv);
+              sm100::mbar_arrive(is_k ? &sm.v_full[s] : &sm.k_full[s]);
+            }
           }
         }
         it.t = it.nt - 1;
@@ -485,12 +569,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = prm.scale_log2;
     uint32_t g = 0;
-    FwdIter it;
+    FwdIter2 it;
     it.init(prm.row_ptr, prm.mq_div, units);
-    int32_t meta = 0, pmeta = 0;
+    int32_t meta = 0;
+    MetaRaw pm{0, 0};
     if (it.valid) {
       meta = load_meta(prm.col_idx, prm.kind, it.rs, it.nt, lane);
-      pmeta = load_meta(prm.col_idx, prm.kind, it.prs, it.pre - it.prs, lane);
+      pm = load_meta_raw(prm.col_idx, prm.kind, it.prs, it.pre - it.prs, lane);
     }
     // RPB: the row's table offset A_q (per unit); the keys' B_k come staged with K
     while (it.valid) {
@@ -668,8 +753,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       it.t = it.nt - 1;
       it.advance(prm.row_ptr, prm.mq_div, units);
       if (it.valid) {
-        meta = it.from_pf ? pmeta : load_meta(prm.col_idx, prm.kind, it.rs, it.nt, lane);
-        pmeta = load_meta(prm.col_idx, prm.kind, it.prs, it.pre - it.prs, lane);
+        meta = it.from_pf ? (pm.c << 2) | pm.k : load_meta(prm.col_idx, prm.kind, it.rs, it.nt, lane);
+        pm = load_meta_raw(prm.col_idx, prm.kind, it.prs, it.pre - it.prs, lane);
       }
       HLA_PADD(10, te0);
       if (row == 0) HLA_TR((2 << 24) | (5 << 16) | it.n);

@@ -200,7 +200,7 @@ def test_fused_reorder_matches_explicit_permutation(kind, g, w, B, H, d):
     r1 = [t.clone() for t in (fused.forward(q, k, v),) + fused.backward(do)]
     r2 = [t.clone() for t in (plain.forward(q, k, v),) + plain.backward(do)]
     torch.cuda.synchronize()
-    assert plain.launches_per_step == fused.launches_per_step + 4 and fused.launches_per_step in (3, 4)
+    assert plain.launches_per_step == fused.launches_per_step + 4 and fused.launches_per_step in (2, 3, 4)
     assert torch.equal(r1[0], r2[0])                       # O
     assert torch.equal(fused.lse, plain.lse)
     assert torch.equal(r1[2], r2[2]) and torch.equal(r1[3], r2[3])   # dK, dV
