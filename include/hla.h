@@ -118,7 +118,7 @@ typedef struct {
   /* Optional backward dQ plan (hla_build_bwd_plan).  In effect only when t_dq and
      q_dq_local are non-NULL and n_dq_nonlocal >= 0 (zero-initialised = no plan). */
   uint8_t* t_dq;                 /* [capacity] per transposed entry: HLA_DQ_* bits  */
-  uint8_t* q_dq_local;           /* [n_qblocks] 1 = dQ rows written by bwd_main     */
+  uint8_t* q_dq_local;           /* [n_qblocks] (block 64: per 128-row tile) 1 = dQ rows written by bwd_main */
   int32_t n_dq_nonlocal;         /* host: q-blocks with q_dq_local == 0 (-1: none)  */
   /* Host copy of counts (nnz, n_full, n_partial, n_empty), written by the fill call of
      hla_build_block_mask.  The backward picks its schedule from it: the full-tile
@@ -213,6 +213,11 @@ HLA_API hla_status hla_build_block_mask(const hla_pattern_desc* d, hla_block_mas
  * products are summed.  Chains never cross a work unit; within a unit each
  * accumulator holds one chain at a time (a chain that would need a busy
  * accumulator is drained early through the fp32 workspace instead).
+ * Block-64 masks (window lists built first, hla_build_tile_lists): the plan is over
+ * the window lists -- t_dq per wt_col entry, q_dq_local per 128-row tile -- and is
+ * built only when every window starts on a 128-row boundary (e.g. HWA with 64-token
+ * windows); otherwise windows overlap in rows and the call leaves n_dq_nonlocal = -1
+ * (no plan) and returns HLA_OK.
  */
 HLA_API hla_status hla_build_bwd_plan(hla_block_mask* m, cudaStream_t stream);
 

@@ -160,9 +160,9 @@ def hla_build_block_mask(desc, device="cuda", stream=None, plan=True):
                                                                  ctypes.byref(nnz), _stream(stream, dev)))
     m.host_counts = tuple(int(x) for x in c.host_counts)   # written by the fill call
     if desc.block_q == desc.block_k == 64:
-        hla_build_tile_lists(m, stream)      # the attention kernels' windows (no dQ plan at block 64)
-    elif plan and desc.block_q == desc.block_k:
-        hla_build_bwd_plan(m, stream)
+        hla_build_tile_lists(m, stream)      # the attention kernels' windows
+    if plan and desc.block_q == desc.block_k:
+        hla_build_bwd_plan(m, stream)        # block 64: only when every window is 128-aligned
     return m
 
 
@@ -189,8 +189,9 @@ def hla_build_tile_lists(mask, stream=None):
 def hla_build_bwd_plan(mask, stream=None):
     """The backward's dQ chaining plan of a filled mask (synchronous; once per mask)."""
     dev = mask.row_ptr.device
-    mask.t_dq = torch.zeros(max(1, mask.col_idx.numel()), dtype=torch.uint8, device=dev)
-    mask.q_dq_local = torch.zeros(mask.row_ptr.numel() - 1, dtype=torch.uint8, device=dev)
+    win = mask.w_row_ptr is not None      # block 64: per window-list entry / 128-row tile
+    mask.t_dq = torch.zeros(max(1, (mask.wt_col if win else mask.col_idx).numel()), dtype=torch.uint8, device=dev)
+    mask.q_dq_local = torch.zeros((mask.w_row_ptr if win else mask.row_ptr).numel() - 1, dtype=torch.uint8, device=dev)
     c = mask.c
     with torch.cuda.device(dev):
         check("hla_build_bwd_plan", lib().hla_build_bwd_plan(ctypes.byref(c), _stream(stream, dev)))

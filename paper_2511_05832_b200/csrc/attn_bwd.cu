@@ -913,7 +913,8 @@ namespace {
 // q_dq_local of a mask with a complete dQ plan (else null: every q-block via the accumulator)
 const uint8_t* plan_of(const hla_block_mask* m, int32_t n) {
   if (!m || !m->t_dq || !m->q_dq_local || m->n_dq_nonlocal < 0) return nullptr;
-  return m->n_qblocks == (n + kBlock - 1) / kBlock ? m->q_dq_local : nullptr;
+  const int32_t tiles = m->w_row_ptr ? (m->n_qblocks + 1) / 2 : m->n_qblocks;   // block 64: per 128-row tile
+  return tiles == (n + kBlock - 1) / kBlock ? m->q_dq_local : nullptr;
 }
 
 // workspace carve-up: [fp32 dQ accumulator][fp32 D*scale][fp32 LSE*log2e], 256-aligned regions

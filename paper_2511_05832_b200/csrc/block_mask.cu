@@ -159,14 +159,18 @@ __global__ void __launch_bounds__(1024) scan_lines_kernel(int32_t* row_ptr, int3
 // TMEM accumulators: a q-block listed by both kv-blocks is held across the pair;
 // a new chain takes a free accumulator (alternating), and if both are held the
 // older hold is cut (its first tile drains through the fp32 workspace instead).
+// (Block-64 masks: the plan runs over the attention kernels' window lists when every window
+// starts on a 128-row boundary -- list entries are then 64-unit columns, col >> col_shift
+// the 128-tile; see hla_build_bwd_plan.)
 __global__ void bwd_plan_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ t_row_ptr,
-                                const int32_t* __restrict__ t_col_idx, int32_t Mk, uint8_t* __restrict__ t_dq) {
+                                const int32_t* __restrict__ t_col_idx, int32_t Mk, uint8_t* __restrict__ t_dq,
+                                int col_shift) {
   const int32_t p = (int32_t)(blockIdx.x * blockDim.x + threadIdx.x);
   const int32_t j0 = 2 * p, j1 = 2 * p + 1;
   if (j0 >= Mk) return;
   const int32_t a0 = t_row_ptr[j0], a1 = t_row_ptr[j0 + 1];
   const int32_t b0 = j1 < Mk ? t_row_ptr[j1] : 0, b1 = j1 < Mk ? t_row_ptr[j1 + 1] : 0;
-  auto row_len = [&](int32_t i) { return row_ptr[i + 1] - row_ptr[i]; };
+  auto row_len = [&](int32_t i) { return row_ptr[(i >> col_shift) + 1] - row_ptr[i >> col_shift]; };
   int32_t held_q[2] = {-1, -1}, held_e[2] = {-1, -1};
   int nb = 0;
   // a new chain's accumulator: prefer the alternate one, take the other if only it is
@@ -214,15 +218,16 @@ __global__ void bwd_plan_kernel(const int32_t* __restrict__ row_ptr, const int32
 // is LOCAL only if it covers i's whole forward list)
 __global__ void bwd_plan_local_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                                       const int32_t* __restrict__ t_row_ptr, const int32_t* __restrict__ t_col_idx,
-                                      const uint8_t* __restrict__ t_dq, int32_t Mq, uint8_t* __restrict__ q_local) {
+                                      const uint8_t* __restrict__ t_dq, int32_t Mq, uint8_t* __restrict__ q_local,
+                                      int col_shift) {
   const int32_t i = (int32_t)(blockIdx.x * blockDim.x + threadIdx.x);
   if (i >= Mq) return;
   uint8_t loc = 0;
   const int32_t r0 = row_ptr[i], r1 = row_ptr[i + 1];
   if (r1 > r0) {
-    const int32_t jl = col_idx[r1 - 1];
+    const int32_t jl = col_idx[r1 - 1] >> col_shift;
     for (int32_t e = t_row_ptr[jl]; e < t_row_ptr[jl + 1]; ++e)
-      if (t_col_idx[e] == i) { loc = (t_dq[e] & HLA_DQ_LOCAL) ? 1 : 0; break; }
+      if (t_col_idx[e] == (i << col_shift)) { loc = (t_dq[e] & HLA_DQ_LOCAL) ? 1 : 0; break; }
   }
   q_local[i] = loc;
 }
@@ -238,12 +243,34 @@ extern "C" hla_status hla_build_bwd_plan(hla_block_mask* m, cudaStream_t stream)
               "the mask must be filled (hla_build_block_mask fill call) before its plan");
   HLA_REQUIRE(m->t_dq && m->q_dq_local, HLA_ERR_INVALID, "t_dq / q_dq_local arrays required");
   HLA_REQUIRE(m->n_qblocks == m->n_kblocks, HLA_ERR_UNSUPPORTED, "dQ plan needs block_q == block_k");
-  const int32_t Mq = m->n_qblocks, Mk = m->n_kblocks;
-  HLA_REQUIRE(Mq >= 1 && Mq <= 65536, HLA_ERR_INVALID, "bad n_qblocks");
+  HLA_REQUIRE(m->n_qblocks >= 1 && m->n_qblocks <= 65536, HLA_ERR_INVALID, "bad n_qblocks");
+  // block 64 (window lists present): the plan is over the attention kernels' window lists and
+  // exists only when every window starts on a 128-row boundary (windows = 128-row tiles, e.g.
+  // HWA with 64-token windows); otherwise windows overlap in rows and there is no plan
+  // (n_dq_nonlocal = -1: every dQ through the fp32 accumulator)
+  const bool win = m->w_row_ptr != nullptr;
+  const int32_t* rp = win ? m->w_row_ptr : m->row_ptr;
+  const int32_t* ci = win ? m->w_col : m->col_idx;
+  const int32_t* trp = win ? m->wt_row_ptr : m->t_row_ptr;
+  const int32_t* tci = win ? m->wt_col : m->t_col_idx;
+  const int32_t Mq = win ? (m->n_qblocks + 1) / 2 : m->n_qblocks, Mk = win ? (m->n_kblocks + 1) / 2 : m->n_kblocks;
+  if (win) {
+    HLA_REQUIRE(ci && trp && tci, HLA_ERR_INVALID, "block-64 mask without its window lists");
+    std::vector<int32_t> hc((size_t)std::max<int64_t>(m->w_counts[0], 0)), htc((size_t)std::max<int64_t>(m->w_counts[2], 0));
+    if (!hc.empty())
+      HLA_CUDA_TRY(cudaMemcpyAsync(hc.data(), ci, sizeof(int32_t) * hc.size(), cudaMemcpyDeviceToHost, stream));
+    if (!htc.empty())
+      HLA_CUDA_TRY(cudaMemcpyAsync(htc.data(), tci, sizeof(int32_t) * htc.size(), cudaMemcpyDeviceToHost, stream));
+    HLA_CUDA_TRY(cudaStreamSynchronize(stream));
+    for (int32_t c : hc)
+      if (c & 1) { m->n_dq_nonlocal = -1; return HLA_OK; }
+    for (int32_t c : htc)
+      if (c & 1) { m->n_dq_nonlocal = -1; return HLA_OK; }
+  }
+  const int col_shift = win ? 1 : 0;
   const int32_t pairs = (Mk + 1) / 2;
-  bwd_plan_kernel<<<(pairs + 127) / 128, 128, 0, stream>>>(m->row_ptr, m->t_row_ptr, m->t_col_idx, Mk, m->t_dq);
-  bwd_plan_local_kernel<<<(Mq + 127) / 128, 128, 0, stream>>>(m->row_ptr, m->col_idx, m->t_row_ptr, m->t_col_idx,
-                                                              m->t_dq, Mq, m->q_dq_local);
+  bwd_plan_kernel<<<(pairs + 127) / 128, 128, 0, stream>>>(rp, trp, tci, Mk, m->t_dq, col_shift);
+  bwd_plan_local_kernel<<<(Mq + 127) / 128, 128, 0, stream>>>(rp, ci, trp, tci, m->t_dq, Mq, m->q_dq_local, col_shift);
   HLA_CUDA_TRY(cudaGetLastError());
   std::vector<uint8_t> loc((size_t)Mq);
   HLA_CUDA_TRY(cudaMemcpyAsync(loc.data(), m->q_dq_local, (size_t)Mq, cudaMemcpyDeviceToHost, stream));

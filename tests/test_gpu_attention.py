@@ -527,6 +527,31 @@ def test_block64_fwd_bwd(case):
         assert_close("b64 " + name, seq(got), ref)
 
 
+@pytest.mark.parametrize("case", B64_CASES, ids=lambda c: "%s_%dx%d_w%dx%d_d%d" % (c[0], c[1], c[2], c[3], c[4], c[7]))
+def test_block64_dq_plan_matches_no_plan(case):
+    """Block 64: the dQ plan runs over the window lists when every window starts on a 128-row
+    boundary (HWA with 64-token windows: cfg5 at block 64) -- then every q tile's dQ is local and
+    written directly; otherwise there is no plan.  Same contract as test_dq_plan_matches_no_plan."""
+    kind, gh, gw, wh, ww, B, H, d = case
+    shift = (wh * ww) // 2 if kind == "HSWA" else 0
+    q, k, v, do = _inputs(B, gh * gw, H, d, seed=43)
+    a = hla.HilbertLocalAttention(kind, gh, gw, wh, ww, B, H, d, block=64, shift=shift, device=DEV)
+    b = hla.HilbertLocalAttention(kind, gh, gw, wh, ww, B, H, d, block=64, shift=shift, device=DEV, dq_plan=False)
+    aligned = bool((a.mask.w_col[:a.mask.w_counts[0]] % 2 == 0).all()) and \
+        bool((a.mask.wt_col[:a.mask.w_counts[2]] % 2 == 0).all())
+    assert (a.mask.n_dq_nonlocal >= 0) == aligned and b.mask.n_dq_nonlocal == -1
+    if kind == "HWA" and wh * ww == 64:
+        assert a.mask.n_dq_nonlocal == 0        # every 64-token window inside one 128-row tile
+    r1 = [t.clone() for t in (a.forward(q, k, v),) + a.backward(do)]
+    r2 = [t.clone() for t in (b.forward(q, k, v),) + b.backward(do)]
+    torch.cuda.synchronize()
+    assert torch.equal(r1[0], r2[0])
+    assert torch.equal(r1[3], r2[3])
+    tol = 2e-3 if a.fused_bwd else 0.0
+    assert (r1[2].float() - r2[2].float()).abs().max().item() <= tol
+    assert (r1[1].float() - r2[1].float()).abs().max().item() <= 2e-3
+
+
 def test_block64_cfg4_slice_and_rpb():
     """cfg4 at block 64 (the shape of the b = 64 bench line) on sampled slices, and the global
     RPB score_mod at block 64 (both backward schedules see window lists)."""
