@@ -312,8 +312,8 @@ HLA_API hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_mask*
  * score_mod: as in hla_attn_fwd (same table); with global RPB, drpb receives the
  * table gradient (accumulated; hla_attn_bwd zeroes it first, hla_attn_bwd_main
  * does not).
- * When the mask's dQ plan makes every q-block local and the full-tile schedule
- * applies (hla_attn_bwd_fuses_preprocess), hla_attn_bwd launches the main kernel
+ * When the mask's dQ plan makes every q-block local and there is no global RPB
+ * (hla_attn_bwd_fuses_preprocess), hla_attn_bwd launches the main kernel
  * only: it reads the raw LSE and the O rows itself and forms D in the kernel (the
  * workspace is then not touched).  Same results up to fp32 summation order of D.
  */

@@ -975,7 +975,7 @@ struct MainPlan {
   CUtensorMap mq, mk, mv, mdo, mdq;
   int32_t head_dim, mkb;
   bool gather, two_d, full;
-  bool fuse;   // preprocess folded into the full-tile kernel (hla_attn_bwd only)
+  bool fuse;   // preprocess folded into the main kernel (hla_attn_bwd only)
 };
 
 hla_status prepare_main(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
@@ -1057,12 +1057,13 @@ hla_status prepare_main(const hla_pattern_desc* d, const hla_block_mask* m, int3
   return HLA_OK;
 }
 
-// hla_attn_bwd: fold the preprocess into the full-tile kernel when every q-block's dQ chain is
-// local (the kernel's dq_stage then holds O tiles instead of dQ partials, and the accumulator is
-// never touched): no preprocess launch, the main kernel reads the raw LSE and O.
+// hla_attn_bwd: fold the preprocess into the main kernel (either schedule, no global RPB) when
+// every q-block's dQ chain is local (the kernel's dq_stage then holds O tiles instead of dQ
+// partials, and the accumulator is never touched): no preprocess launch, the main kernel reads
+// the raw LSE and O.
 hla_status try_fuse(MainPlan* pl, const hla_block_mask* m, int32_t batch, int32_t heads, const void* o,
                     const float* lse) {
-  if (!pl->full || !plan_of(m, pl->prm.N) || m->n_dq_nonlocal != 0) return HLA_OK;
+  if (pl->prm.rpb != nullptr || !plan_of(m, pl->prm.N) || m->n_dq_nonlocal != 0) return HLA_OK;
   const int64_t tok = (int64_t)batch * pl->prm.N;
   const hla_status st = pl->gather ? make_gather_map(&pl->mdq, o, tok, heads, pl->head_dim)
                                    : make_rows_map(&pl->mdq, o, tok, heads, pl->head_dim, kBlock);
@@ -1078,7 +1079,7 @@ hla_status launch_main(const MainPlan& pl, cudaStream_t stream) {
   if (pl.full)
     return bwd::launch_full(pl.head_dim, pl.gather, pl.two_d, pl.fuse, pl.mq, pl.mk, pl.mv, pl.mdo, pl.mdq, pl.prm,
                             pl.mkb, stream);
-  return bwd::launch_split(bias, pl.head_dim, pl.gather, pl.two_d, pl.mq, pl.mk, pl.mv, pl.mdo, pl.mdq, pl.prm,
+  return bwd::launch_split(bias, pl.head_dim, pl.gather, pl.two_d, pl.fuse, pl.mq, pl.mk, pl.mv, pl.mdo, pl.mdq, pl.prm,
                            pl.mkb, stream);
 }
 
@@ -1136,8 +1137,7 @@ extern "C" int32_t hla_attn_bwd_fuses_preprocess(const hla_pattern_desc* d, cons
     clear_error();
     return 0;
   }
-  const bool full = rpb == nullptr && lists.t_n_full >= lists.t_n_partial && lists.t_n_full > 0;
-  return full && plan_of(m, pat.N) && m->n_dq_nonlocal == 0 ? 1 : 0;
+  return rpb == nullptr && plan_of(m, pat.N) && m->n_dq_nonlocal == 0 ? 1 : 0;
 }
 
 extern "C" hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,

@@ -54,11 +54,16 @@ struct SplitSmem {
   alignas(16) float rpb_wmax[2][8];                // kBias: per compute warp max |dL/dscore| of a tile (tile parity)
   uint64_t kv_full[2], kv_empty[2], q_full[2], q_empty[2], s_full[2], ds_ready[2], dq_full[2], dq_free[2], dkv_full,
       epi_done;
+  uint64_t o_full, o_empty, d_full[2];   // kFuse (preprocess folded in), as in attn_bwd.cu
   uint32_t tmem_base;
   int32_t rpb_win[kBias ? rpb_win_cap<D>() : 1];   // dRPB of the current tile's offset box, fixed point (compute warps)
 };
 
-template <int D, bool kTwoD, bool kGather, bool kBias>
+// kFuse: the preprocess folded into the kernel (every dQ chain local, no bias) exactly as in the
+// full-tile schedule (attn_bwd.cu): warp 0 loads the raw LSE and the O tile into the dq_stage
+// bytes, the dQ warpgroup forms D * scale and LSE * log2(e) one tile ahead of its drains, the
+// compute warps wait d_full instead of q_full; tmDQ is the O map.
+template <int D, bool kTwoD, bool kGather, bool kBias, bool kFuse>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -92,6 +97,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     sm100::mbar_init(&sm.dkv_full, 1);
     sm100::mbar_init(&sm.epi_done, 128);
+    sm100::mbar_init(&sm.o_full, 1);
+    sm100::mbar_init(&sm.o_empty, 128);
+    for (int s = 0; s < 2; ++s) sm100::mbar_init(&sm.d_full[s], 128);
         sm100::fence_mbar_init();
     sm100::tma_prefetch_desc(&tmQ);
     sm100::tma_prefetch_desc(&tmK);
@@ -119,7 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_q = sm100::policy_evict_last();
       const int role = warp == 0 ? 0 : warp - 13;   // 0, 1, 2
       constexpr uint32_t kTile = Smem::kTileBytes;
-      uint32_t n = 0, g = 0;
+      uint32_t n = 0, g = 0, n_o = 0;
       int64_t stage_tag0 = -1, stage_tag1 = -1;   // (b, h, q-block) held by stage 0 / 1
       for (int32_t kq = 0;; ++kq) {
         const int32_t u = unit_at(kq, ug);
@@ -172,9 +180,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else if (lane == 0) {
               // LSE / D of the real rows only (ragged last tile: N % 4 == 0, so 16-B multiples)
               const uint32_t vbytes = (uint32_t)min(kBlock, prm.N - qblk * prm.col_mul) * 4u;
-              sm100::mbar_arrive_expect_tx(&sm.q_full[s], 2 * vbytes);
+              sm100::mbar_arrive_expect_tx(&sm.q_full[s], (kFuse ? 1 : 2) * vbytes);
               sm100::bulk_load(sm.lse[s], prm.lse2 + bh * prm.N + qblk * prm.col_mul, vbytes, &sm.q_full[s]);
-              sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * prm.col_mul, vbytes, &sm.q_full[s]);
+              if (!kFuse)
+                sm100::bulk_load(sm.dd[s], prm.dsum + bh * prm.N + qblk * prm.col_mul, vbytes, &sm.q_full[s]);
+            }
+            if (kFuse && !(kVar & 4)) {
+              // the q-block's O rows into the single O stage (freed by the dQ warps after D)
+              if (n_o > 0) sm100::mbar_wait(&sm.o_empty, (n_o - 1) & 1);
+              ++n_o;
+              if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.o_full, kTile);
+              __syncwarp();
+              load_rows<D, kGather>(reinterpret_cast<uint8_t*>(sm.dq_stage), &tmDQ, &sm.o_full, h, b, prm.N,
+                                    qblk * prm.col_mul, prm.s2c, pol_q, lane);
             }
           } else if (kVar & 4) {
             if (lane == 0) sm100::mbar_arrive(&sm.q_full[s]);
@@ -354,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           win = wrows * wc <= rpb_win_cap<D>();
           kwb = (prm.grid_h - 1) * prm.rpb_w + prm.grid_w - 1 + k_b + dr0 * wc + dc0;
         }
-        sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1);
+        sm100::mbar_wait(kFuse ? &sm.d_full[s] : &sm.q_full[s], (g >> 1) & 1);
         const uint32_t lse2 = sm100::smem_u32(sm.lse[s]);
         const uint32_t dd = sm100::smem_u32(sm.dd[s]);
         const uint32_t qa = sm100::smem_u32(sm.qa[s]);
@@ -525,6 +543,49 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool leader = warp == 10 && lane == 0;
     uint32_t g = 0, n = 0;
     uint32_t dq_drained0 = 0, dq_drained1 = 0;   // chains drained per dQ accumulator
+    // kFuse: the D / log2-LSE cursor, one tile ahead of the drains (as in attn_bwd.cu)
+    TileIter dit;
+    uint32_t gd = 0, n_od = 0;
+    int64_t dtag0 = -1, dtag1 = -1;
+    if (kFuse) dit.init(prm.t_row_ptr, ug);
+    auto d_step = [&]() {
+      const int s = gd & 1;
+      sm100::mbar_wait(&sm.q_full[s], (gd >> 1) & 1);
+      const int32_t bh_d = prm.mk_div.div(dit.u);
+      const int32_t bd = prm.heads_div.div(bh_d), hd = bh_d - bd * prm.heads;
+      const int32_t qblk = __ldg(prm.t_col_idx + dit.rs + dit.t);
+      const int64_t tag = ((int64_t)bd * prm.heads + hd) * prm.N + qblk;
+      if (tag != (s ? dtag1 : dtag0)) {
+        sm100::mbar_wait(&sm.o_full, n_od & 1);
+        if (s) dtag1 = tag; else dtag0 = tag;
+        ++n_od;
+        const uint32_t ob = sm100::smem_u32(sm.dq_stage), gb = sm100::smem_u32(sm.dO[s]);
+        float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+        for (int j = 0; j < D / 8; ++j) {
+          const uint32_t off = (uint32_t)row * (D * 2) + (uint32_t)j * 16u;
+          const uint32_t so = D == 64 ? sm100::swz128(off) : sm100::swz64(off);
+          const float4 a = sm100::lds_f4(ob + so), c = sm100::lds_f4(gb + so);
+          const float av[4] = {a.x, a.y, a.z, a.w}, cv[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t aw = __float_as_uint(av[e]), cw = __float_as_uint(cv[e]);
+            acc0 = fmaf(__uint_as_float(aw << 16), __uint_as_float(cw << 16), acc0);
+            acc1 = fmaf(__uint_as_float(aw & 0xffff0000u), __uint_as_float(cw & 0xffff0000u), acc1);
+          }
+        }
+        sm.dd[s][row] = (acc0 + acc1) * prm.scale;
+        if (qblk * prm.col_mul + row < prm.N) sm.lse[s][row] *= kLog2e;   // raw LSE -> log2 domain
+        sm100::fence_proxy_async_smem();   // before the async proxy refills the O / LSE stages
+        sm100::mbar_arrive(&sm.o_empty);
+      }
+      sm100::mbar_arrive(&sm.d_full[s]);
+      dit.advance(prm.t_row_ptr, ug);
+      ++gd;
+    };
+    auto d_upto = [&](uint32_t target) {
+      while (dit.valid && gd <= target) d_step();
+    };
     for (int32_t kq = 0;; ++kq) {
       const int32_t u = unit_at(kq, ug);
       if (u == kUnitEnd) break;
@@ -533,6 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int32_t b = prm.heads_div.div(bh_u), h = bh_u - b * prm.heads;
       const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
       for (int t = 0; t < nt; ++t, ++g) {
+        if (kFuse) d_upto(g + 1);
         const uint32_t fdq = dq_plan(prm.t_dq, rs + t, g);
         if (!(fdq & HLA_DQ_DRAIN)) continue;   // the chain continues in TMEM
         const int dqb = (int)(fdq & HLA_DQ_BUF);
@@ -645,12 +707,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 
-template <int D, bool kTwoD, bool kGather, bool kBias>
+template <int D, bool kTwoD, bool kGather, bool kBias, bool kFuse = false>
 hla_status launch_split_t(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                           const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm, int32_t n_kblocks,
                           cudaStream_t stream) {
   const size_t smem = sizeof(SplitSmem<D, kBias>) + 1024;
-  auto* fn = attn_bwd_split_kernel<D, kTwoD, kGather, kBias>;
+  auto* fn = attn_bwd_split_kernel<D, kTwoD, kGather, kBias, kFuse>;
   HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t pairs = (int64_t)((n_kblocks + 1) / 2) * prm.heads * prm.batch;   // work units (kv-block pairs)
   const int grid = (int)std::min<int64_t>(pairs, (int64_t)num_sms());
@@ -675,11 +737,26 @@ hla_status dispatch_split(int head_dim, bool gather, bool two_d, const CUtensorM
                : launch_split_t<32, false, false, kBias>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
 }
 
+// preprocess folded in (no bias): every dQ chain local, mdq = the O map, lse2 = raw LSE
+hla_status dispatch_split_fused(int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
+                                const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq,
+                                const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream) {
+  if (head_dim == 64) {
+    if (gather) return launch_split_t<64, false, true, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
+    return two_d ? launch_split_t<64, true, false, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream)
+                 : launch_split_t<64, false, false, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
+  }
+  if (gather) return launch_split_t<32, false, true, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
+  return two_d ? launch_split_t<32, true, false, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream)
+               : launch_split_t<32, false, false, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
+}
+
 }  // namespace
 
-hla_status launch_split(bool bias, int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
-                        const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm,
-                        int32_t n_kblocks, cudaStream_t stream) {
+hla_status launch_split(bool bias, int head_dim, bool gather, bool two_d, bool fuse, const CUtensorMap& mq,
+                        const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq,
+                        const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream) {
+  if (fuse && !bias) return dispatch_split_fused(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
   return bias ? dispatch_split<true>(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, n_kblocks, stream)
               : dispatch_split<false>(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
 }

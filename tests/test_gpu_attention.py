@@ -324,12 +324,14 @@ def test_dq_plan_matches_no_plan(kind, g, w, B, H, d, fused):
     assert (r1[1].float() - r2[1].float()).abs().max().item() <= 2e-3
 
 
-@pytest.mark.parametrize("g,w,B,H,d", [(64, 16, 2, 4, 64), (32, 16, 2, 3, 32), (48, 16, 1, 2, 64),
-                                       (16, 16, 1, 2, 64)])
+@pytest.mark.parametrize("g,w,B,H,d,blk", [(64, 16, 2, 4, 64, 128), (32, 16, 2, 3, 32, 128), (48, 16, 1, 2, 64, 128),
+                                           (16, 16, 1, 2, 64, 128), (32, 8, 2, 3, 32, 128), (32, 8, 2, 3, 32, 64),
+                                           (16, 8, 2, 2, 64, 64)])
 @pytest.mark.parametrize("fused", [True, False])
-def test_bwd_fused_preprocess_matches_staged(g, w, B, H, d, fused):
-    """hla_attn_bwd folds the preprocess into the full-tile kernel when every q-block's dQ is
-    local (HWA windows of whole 128-blocks, cfg2): D = rowsum(dO o O) and LSE log2(e) are formed
+def test_bwd_fused_preprocess_matches_staged(g, w, B, H, d, blk, fused):
+    """hla_attn_bwd folds the preprocess into the main kernel when every q-block's dQ is local
+    (HWA windows of whole 128-blocks, cfg2: full-tile schedule; 64-token windows, cfg5: half-tile
+    schedule, block 128 or 64): D = rowsum(dO o O) and LSE log2(e) are formed
     in the kernel from the raw LSE and the O tile.  Against the staged calls (preprocess ->
     main -> finalize) on the same mask: dV bit-identical, dQ / dK within fp32 order of D; and
     one (b, h) slice against the fp64 oracle."""
@@ -337,7 +339,7 @@ def test_bwd_fused_preprocess_matches_staged(g, w, B, H, d, fused):
         pytest.skip("the explicit permutation kernel needs a 2^k grid")
     N = g * g
     q, k, v, do = _inputs(B, N, H, d, seed=31)
-    lay = hla.HilbertLocalAttention("HWA", g, g, w, w, B, H, d, device=DEV, fused=fused)
+    lay = hla.HilbertLocalAttention("HWA", g, g, w, w, B, H, d, block=blk, device=DEV, fused=fused)
     assert lay.fused_bwd and lay.mask.n_dq_nonlocal == 0   # (windows of whole block pairs: never ragged)
     lay.forward(q, k, v)
     r1 = [t.clone() for t in lay.backward(do)]
