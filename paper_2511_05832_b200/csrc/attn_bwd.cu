@@ -166,12 +166,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
-  const uint32_t tmem = sm.tmem_base;
-  unsigned long long tiles_done = 0;
   HLA_TR_DECL;
 
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl) : "memory");
+    const uint32_t tmem = sm.tmem_base;   // read after the register split (not spilled across it)
     HLA_PDECL;
     UnitGeom ug;
     ug.mk = (prm.N + kBlock - 1) / kBlock;   // last kv-block may be ragged
@@ -380,6 +379,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp < kDqWarp0) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsCmp) : "memory");
+    const uint32_t tmem = sm.tmem_base;   // read after the register split (not spilled across it)
+    unsigned long long tiles_done = 0;
     HLA_PDECL;
     // --------------------------------------------- P^T / dS^T (thread = key row)
     // warp sets cset = 0 .. kCmpWarps / 4 - 1 (4 consecutive warps each) share every TMEM lane
@@ -540,10 +541,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tiles_done += nt;
     }
+    if (warp == 4 && lane == 0 && prm.visited != nullptr && tiles_done > 0) atomicAdd(prm.visited, tiles_done);
     HLA_PFLUSH(5, 9, warp == 4 && lane == 0);
     HLA_PFLUSH(16, 20, warp == 4 && lane == 0);
   } else {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsDq) : "memory");
+    const uint32_t tmem = sm.tmem_base;   // read after the register split (not spilled across it)
     HLA_PDECL;
     // ------------------------------------------ dQ partial -> fp32 accumulator
     // thread = query row: drain the dQ_i tile from TMEM (then release it), stage it
@@ -767,8 +770,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
-  if (warp == 1) sm100::tmem_dealloc(tmem, kTmemCols);
-  if (warp == 4 && lane == 0 && prm.visited != nullptr && tiles_done > 0) atomicAdd(prm.visited, tiles_done);
+  if (warp == 1) sm100::tmem_dealloc(sm.tmem_base, kTmemCols);
 }
 
 template <int D, bool kTwoD, bool kGather, bool kFuse>

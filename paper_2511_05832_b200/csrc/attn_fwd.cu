@@ -342,8 +342,6 @@ __global__ void __launch_bounds__(kThreads, 2)
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
-  const uint32_t tmem = sm.tmem_base;
-  unsigned long long tiles_done = 0;
 #ifdef HLA_FWD_PROF
   const long long prof_c0 = clock64();
   unsigned long long prof_g0;
@@ -355,6 +353,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   // registers to the softmax warpgroup (one thread per row keeps a 128-wide S row)
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
+    const uint32_t tmem = sm.tmem_base;   // read after the register split (not spilled across it)
     HLA_PDECL;
     // (derived after the register split, so they are not spilled across it)
     const int32_t mq = (prm.N + kBlock - 1) / kBlock;   // last q-block may be ragged
@@ -560,6 +559,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
+    const uint32_t tmem = sm.tmem_base;   // read after the register split (not spilled across it)
+    unsigned long long tiles_done = 0;
     HLA_PDECL;
     const int32_t mq = (prm.N + kBlock - 1) / kBlock;
     const int32_t units = mq * prm.heads * prm.batch;
@@ -761,13 +762,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     HLA_PFLUSH(3, 11, warp == 4 && lane == 0);
     HLA_PFLUSH(19, 20, warp == 4 && lane == 0);
+    if (warp == 4 && lane == 0 && prm.visited != nullptr && tiles_done > 0) atomicAdd(prm.visited, tiles_done);
   }
 
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
-  if (warp == 1) sm100::tmem_dealloc(tmem, kTmemCols);
-  if (warp == 4 && lane == 0 && prm.visited != nullptr && tiles_done > 0) atomicAdd(prm.visited, tiles_done);
+  if (warp == 1) sm100::tmem_dealloc(sm.tmem_base, kTmemCols);
 }
 
 template <int D, bool kTwoD, bool kGather, bool kBias>
