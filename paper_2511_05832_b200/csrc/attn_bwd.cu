@@ -60,7 +60,10 @@ constexpr int kChunks = 16 / kCmpWarps;              // 32-column chunks of S^T 
 constexpr int kDqWarp0 = 4 + kCmpWarps;              // first dQ / epilogue warp
 constexpr int kThreads = (kDqWarp0 + 4) * 32;
 // per-warpgroup register budgets (setmaxnreg; the launch allocates 65536 / kThreads, rounded to 8)
-constexpr int kRegsCtl = kCmpWarps == 16 ? 56 : 64, kRegsCmp = kCmpWarps == 16 ? 88 : 168,
+#ifndef HLA_BWD_REGS_CTL
+#define HLA_BWD_REGS_CTL 64
+#endif
+constexpr int kRegsCtl = kCmpWarps == 16 ? 56 : HLA_BWD_REGS_CTL, kRegsCmp = kCmpWarps == 16 ? 88 : 168,
               kRegsDq = kCmpWarps == 16 ? 56 : 104;
 // columns per TMEM load batch of the dQ drain / dK dV epilogue (a full D = 64 row needs ~96 registers)
 template <int D>

@@ -43,6 +43,11 @@ constexpr int kBlock = 128;
 constexpr int kThreads = 256;   // warpgroup 0: TMA (Q), MMA, TMA (K), TMA (V); warpgroup 1: softmax
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kColS = 0, kColP = 128, kColO = 192;
+// per-warpgroup register budgets (setmaxnreg) at 2 CTAs / SM: 128 (kRegsCtl + kRegsSm) <= 32768
+#ifndef HLA_FWD_REGS_CTL
+#define HLA_FWD_REGS_CTL 56
+#endif
+constexpr int kRegsCtl = HLA_FWD_REGS_CTL, kRegsSm = 256 - HLA_FWD_REGS_CTL;
 
 struct FwdParams {
   Pattern pat;
@@ -352,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   // register split (setmaxnreg acts per warpgroup): the control warpgroup gives its
   // registers to the softmax warpgroup (one thread per row keeps a 128-wide S row)
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl) : "memory");
     const uint32_t tmem = sm.tmem_base;   // read after the register split (not spilled across it)
     HLA_PDECL;
     // (derived after the register split, so they are not spilled across it)
@@ -558,7 +563,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       HLA_PFLUSH(23, 24, true);
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSm) : "memory");
     const uint32_t tmem = sm.tmem_base;   // read after the register split (not spilled across it)
     unsigned long long tiles_done = 0;
     HLA_PDECL;
