@@ -98,6 +98,7 @@ struct FullSmem {
   alignas(1024) float dq_stage[kBlock * 32];    // fp32 dQ half tile [128][32], SWIZZLE_128B
   alignas(16) float lse[kQStages][kBlock];
   alignas(16) float dd[kQStages][kBlock];
+  alignas(128) uint8_t epi_stage[4][2048];        // per dQ warp: row-store transpose (store_rows_t)
   uint64_t kv_full[2], kv_empty[2], q_full[kQStages], q_empty[kQStages], s_full, s_read, p_ready, ds_ready,
       dq_full[2], dq_free[2], dkv_full, epi_done;
   // kFuse (preprocess folded in): O tile of a newly loaded q-block (in the dq_stage bytes,
@@ -658,6 +659,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             sm100::tc_fence_before();
             sm100::mbar_arrive(&sm.dq_free[dqb]);     // the TMEM dQ accumulator may now be overwritten
           }
+          if (local && kEpCols == D) {
+            uint32_t w[D / 2];
+#pragma unroll
+            for (int e = 0; e < D / 2; ++e) w[e] = sm100::pack_bf16(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
+            store_rows_t<D>(w, dqp, sm100::smem_u32(sm.epi_stage[quarter]), lane);
+            continue;
+          }
           if (local) {
 #pragma unroll
             for (int v4 = 0; v4 < kEpCols / 8 && dqp; ++v4)
@@ -721,18 +729,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int c = 0; c < D / 32; ++c)
             sm100::tmem_ld32(tmem + lane_off + kColDK + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
-#pragma unroll
-          for (int v4 = 0; v4 < D / 8 && real; ++v4)
-            dvp[v4] = make_uint4(pv[v4 * 4 + 0], pv[v4 * 4 + 1], pv[v4 * 4 + 2], pv[v4 * 4 + 3]);
+          const uint32_t stg = sm100::smem_u32(sm.epi_stage[quarter]);
+          store_rows_t<D>(pv, real ? dvp : nullptr, stg, lane);
           sm100::tmem_wait_ld();
           sm100::tc_fence_before();
           sm100::mbar_arrive(&sm.epi_done);      // dV / dK accumulators may now be reset
 #pragma unroll
-          for (int v4 = 0; v4 < D / 8 && real; ++v4)
-            dkp[v4] = make_uint4(sm100::pack_bf16(__uint_as_float(r[8 * v4 + 0]), __uint_as_float(r[8 * v4 + 1])),
-                                 sm100::pack_bf16(__uint_as_float(r[8 * v4 + 2]), __uint_as_float(r[8 * v4 + 3])),
-                                 sm100::pack_bf16(__uint_as_float(r[8 * v4 + 4]), __uint_as_float(r[8 * v4 + 5])),
-                                 sm100::pack_bf16(__uint_as_float(r[8 * v4 + 6]), __uint_as_float(r[8 * v4 + 7])));
+          for (int e = 0; e < D / 2; ++e) pv[e] = sm100::pack_bf16(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
+          store_rows_t<D>(pv, real ? dkp : nullptr, stg, lane);
         } else {
           // dV then dK in 32-column batches (register budget kRegsDq); epi_done after the last load
 #pragma unroll

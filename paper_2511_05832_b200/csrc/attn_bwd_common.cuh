@@ -167,6 +167,35 @@ __device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* map, 
   }
 }
 
+// Rows held by one warp (thread = row: D / 2 packed bf16x2 words, one 2D-byte row at `rowp`, null
+// = phantom row) stored through a per-warp shared-memory transpose, so that every STG.128 of the
+// warp writes 8 rows x 64 contiguous bytes instead of 32 rows x 16 bytes (the row stores were
+// bound by 16-byte segments, ~1 per cycle).  stage: this warp's 2 KB (shared address).
+template <int D>
+__device__ __forceinline__ void store_rows_t(const uint32_t* w, uint4* rowp, uint32_t stage, int lane) {
+  const unsigned long long pr = reinterpret_cast<unsigned long long>(rowp);
+#pragma unroll
+  for (int seg = 0; seg < D / 32; ++seg) {
+    // this lane's 64-byte segment -> stage row `lane`, 16-byte slots rotated by lane / 2 (the 8
+    // lanes of each STS.128 / LDS.128 phase hit 8 distinct slots of 128 bytes: no bank conflict)
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      sm100::sts_u4(stage + lane * 64 + 16 * ((c + (lane >> 1)) & 3), w[seg * 16 + 4 * c], w[seg * 16 + 4 * c + 1],
+                    w[seg * 16 + 4 * c + 2], w[seg * 16 + 4 * c + 3]);
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = (lane >> 2) + 8 * k, c = lane & 3;
+      const float4 v = sm100::lds_f4(stage + r * 64 + 16 * ((c + (r >> 1)) & 3));
+      const unsigned long long p = __shfl_sync(0xffffffffu, pr, r);
+      if (p)
+        reinterpret_cast<uint4*>(p)[seg * 4 + c] =
+            make_uint4(__float_as_uint(v.x), __float_as_uint(v.y), __float_as_uint(v.z), __float_as_uint(v.w));
+    }
+    __syncwarp();
+  }
+}
+
 // cell -> (row << 16) | col (RPB offsets; grid sides < 2^15)
 __device__ __forceinline__ int32_t rpb_cell_rc(const int32_t* cells, int32_t seq, int32_t N, const FastDiv& W) {
   const int32_t cell = seq < N ? (cells ? __ldg(cells + seq) : seq) : 0;

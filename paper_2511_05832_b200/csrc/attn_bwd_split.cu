@@ -57,6 +57,8 @@ struct SplitSmem {
   uint64_t o_full, o_empty, d_full[2];   // kFuse (preprocess folded in), as in attn_bwd.cu
   uint32_t tmem_base;
   int32_t rpb_win[kBias ? rpb_win_cap<D>() : 1];   // dRPB of the current tile's offset box, fixed point (compute warps)
+  // per dQ warp: row-store transpose (store_rows_t); no room next to the dRPB window
+  alignas(128) uint8_t epi_stage[kBias ? 1 : 4][kBias ? 16 : 2048];
 };
 
 // kFuse: the preprocess folded into the kernel (every dQ chain local, no bias) exactly as in the
@@ -617,7 +619,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           // complete dQ_i (dS carries the softmax scale): bf16 rows straight to dq, to the
           // grid cell under the fused reorder; phantom rows of a ragged tile write nothing
           const int32_t qs = qblk * prm.col_mul + row;
-          if (qs < prm.N) {
+          if (!kBias) {
+            uint4* dqp = nullptr;
+            if (qs < prm.N) {
+              const int32_t qcell = kGather ? __ldg(prm.s2c + qs) : qs;
+              dqp = reinterpret_cast<uint4*>(prm.dq + (((int64_t)b * prm.N + qcell) * prm.heads + h) * D);
+            }
+            uint32_t w[D / 2];
+#pragma unroll
+            for (int e = 0; e < D / 2; ++e) w[e] = sm100::pack_bf16(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
+            store_rows_t<D>(w, dqp, sm100::smem_u32(sm.epi_stage[kBias ? 0 : quarter]), lane);
+          } else if (qs < prm.N) {
             const int32_t qcell = kGather ? __ldg(prm.s2c + qs) : qs;
             uint4* dqp = reinterpret_cast<uint4*>(prm.dq + (((int64_t)b * prm.N + qcell) * prm.heads + h) * D);
 #pragma unroll
@@ -682,10 +694,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         sm100::tc_fence_before();
         sm100::mbar_arrive(&sm.epi_done);      // dV / dK accumulators may now be reset
+        if (!kBias) {
+          const uint32_t stg = sm100::smem_u32(sm.epi_stage[kBias ? 0 : quarter]);
+          store_rows_t<D>(pv, real ? dvp : nullptr, stg, lane);
+          store_rows_t<D>(pk, real ? dkp : nullptr, stg, lane);
+        } else {
 #pragma unroll
-        for (int v4 = 0; v4 < D / 8 && real; ++v4) {
-          dvp[v4] = make_uint4(pv[v4 * 4 + 0], pv[v4 * 4 + 1], pv[v4 * 4 + 2], pv[v4 * 4 + 3]);
-          dkp[v4] = make_uint4(pk[v4 * 4 + 0], pk[v4 * 4 + 1], pk[v4 * 4 + 2], pk[v4 * 4 + 3]);
+          for (int v4 = 0; v4 < D / 8 && real; ++v4) {
+            dvp[v4] = make_uint4(pv[v4 * 4 + 0], pv[v4 * 4 + 1], pv[v4 * 4 + 2], pv[v4 * 4 + 3]);
+            dkp[v4] = make_uint4(pk[v4 * 4 + 0], pk[v4 * 4 + 1], pk[v4 * 4 + 2], pk[v4 * 4 + 3]);
+          }
         }
         ++n;
       } else {
