@@ -48,6 +48,16 @@ constexpr uint32_t kColS = 0, kColP = 128, kColO = 192;
 #define HLA_FWD_REGS_CTL 56
 #endif
 constexpr int kRegsCtl = HLA_FWD_REGS_CTL, kRegsSm = 256 - HLA_FWD_REGS_CTL;
+// O tile stores: the softmax warps read their staged rows back transposed and write them with
+// coalesced STG.128 (each instruction 8 whole 64-B rows at d = 32), or warp 0 TMA-stores the
+// staged tile (store / scatter4) before it reloads the Q stage.  Measured (DESIGN 6g): the warp
+// stores win at d = 32 (cfg5 fwd -20 %), the TMA stores at d = 64 (cfg3 / cfg4 fwd -3 %).
+// HLA_FWD_OSTORE: 0 = TMA always, 1 = warps always, 2 = warps at d = 32 only (default).
+#ifndef HLA_FWD_OSTORE
+#define HLA_FWD_OSTORE 2
+#endif
+template <int D>
+constexpr bool warp_ostore() { return HLA_FWD_OSTORE == 1 || (HLA_FWD_OSTORE == 2 && D == 32); }
 
 struct FwdParams {
   Pattern pat;
@@ -408,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           const int4 cells = row_cells<kGather>(prm.N, qb * kBlock, prm.s2c, lane);
           if (it.n >= 2) {
             HLA_PW(11, sm100::mbar_wait(&sm.o_staged[qs], ((it.n >> 1) - 1) & 1));
-            HLA_PW(12, store_o(qs, qs ? staged1 : staged0));
+            if (!warp_ostore<D>()) HLA_PW(12, store_o(qs, qs ? staged1 : staged0));
           }
           if (qs) staged1 = it.u; else staged0 = it.u;
           if (lane == 0) HLA_TR((3 << 24) | (1 << 16) | it.n);
@@ -475,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           pmeta = load_meta(prm.col_idx, prm.kind, it.prs, it.pre - it.prs, lane);
         }
       }
-      if (warp == 0) {
+      if (warp == 0 && !warp_ostore<D>()) {
         // the last (up to) two units' O tiles are still staged
         for (uint32_t m = n_units >= 2 ? n_units - 2 : 0; m < n_units; ++m) {
           sm100::mbar_wait(&sm.o_staged[m & 1], (m >> 1) & 1);
@@ -747,8 +757,26 @@ __global__ void __launch_bounds__(kThreads, 2)
           optr[v4] = w;
         }
       }
+      if (warp_ostore<D>() && staged) {
+        // this warp's 32 staged rows back, transposed: lanes 8j .. 8j + 7 (d = 64; 4j .. 4j + 3 at
+        // d = 32) hold one row's 16-B chunks, so each STG.128 writes whole 128-B (64-B) rows
+        __syncwarp();
+        constexpr int kCh = D / 8;                 // 16-B chunks per row
+        constexpr int kRowsPer = 32 / kCh;         // rows per warp instruction
+        const unsigned long long op = real ? reinterpret_cast<unsigned long long>(optr) : 0ull;
+#pragma unroll
+        for (int k = 0; k < 32 / kRowsPer; ++k) {
+          const int rl = lane / kCh + kRowsPer * k, c = lane % kCh;
+          const uint32_t off = (uint32_t)(quarter * 32 + rl) * (D * 2) + (uint32_t)c * 16u;
+          const float4 v = sm100::lds_f4(stage + (D == 64 ? sm100::swz128(off) : sm100::swz64(off)));
+          const unsigned long long p = __shfl_sync(0xffffffffu, op, rl);
+          if (p)
+            reinterpret_cast<uint4*>(p)[c] =
+                make_uint4(__float_as_uint(v.x), __float_as_uint(v.y), __float_as_uint(v.z), __float_as_uint(v.w));
+        }
+      }
       sm100::fence_proxy_async_smem();
-      sm100::mbar_arrive(&sm.o_staged[it.n & 1]);
+      sm100::mbar_arrive(&sm.o_staged[it.n & 1]);   // (warp_ostore<D>(): the Q stage is free again)
       if (row == 0) HLA_TR((2 << 24) | (4 << 16) | it.n);
       const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
       if (real)
