@@ -102,8 +102,8 @@ struct FullSmem {
   uint64_t kv_full[2], kv_empty[2], q_full[kQStages], q_empty[kQStages], s_full, s_read, p_ready, ds_ready,
       dq_full[2], dq_free[2], dkv_full, epi_done;
   // kFuse (preprocess folded in): O tile of a newly loaded q-block (in the dq_stage bytes,
-  // unused when every dQ chain is local), and D of stage s ready for the compute warps
-  uint64_t o_full, o_empty, d_full[kQStages];
+  // unused when every dQ chain is local) landed / consumed
+  uint64_t o_full, o_empty;
   uint64_t dbg_bar;
   uint32_t tmem_base;
 };
@@ -115,10 +115,11 @@ struct FullSmem {
 // far, g = (q-block) tiles so far.
 // kFuse: the backward preprocess folded into the kernel (only when every q-block's dQ chain is
 // local, so the dq_stage bytes are free): warp 0 loads the raw LSE and the O tile of each newly
-// loaded q-block; the dQ warpgroup (thread = query row) forms D * scale = rowsum(dO o O) * scale
-// and LSE * log2(e) in the stage one tile ahead of its dQ drains and arrives on d_full, which the
-// compute warps wait for instead of q_full.  tmDQ is then the O map.  (Serving D inside the
-// group's waits by polling measured slower: the spinning warps take issue slots, DESIGN 6g.)
+// loaded q-block; the 256 compute warps' threads form D * scale = rowsum(dO o O) * scale and
+// LSE * log2(e) in the stage (form_d) when they first meet the q-block, before its S^T lands.
+// tmDQ is then the O map.  (D formed by the dQ warpgroup -- one tile ahead of its drains, or
+// serviced inside its waits -- measured slower: that group is busy with drains and epilogues
+// exactly when the next unit's q-blocks land, DESIGN 6g.)
 template <int D, bool kTwoD, bool kGather, bool kFuse>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_full_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -148,8 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     sm100::mbar_init(&sm.epi_done, 128);
     sm100::mbar_init(&sm.dbg_bar, 1);
     sm100::mbar_init(&sm.o_full, 1);
-    sm100::mbar_init(&sm.o_empty, 128);
-    for (int s = 0; s < kQStages; ++s) sm100::mbar_init(&sm.d_full[s], 128);
+    sm100::mbar_init(&sm.o_empty, 1);
     sm100::fence_mbar_init();
     sm100::tma_prefetch_desc(&tmQ);
     sm100::tma_prefetch_desc(&tmK);
@@ -392,6 +392,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;
     const int cset = (warp - 4) >> 2;
     const int row = quarter * 32 + lane;
+    const int cth = (warp - 4) * 32 + lane;   // compute thread 0 .. 255
+    uint32_t n_od = 0;                          // kFuse: O tiles consumed
+    int64_t dtag0 = -1, dtag1 = -1;             // kFuse: q-block held by stage 0 / 1
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = prm.scale_log2, scale = prm.scale;
     UnitGeom ug;
@@ -416,7 +419,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint8_t kd = __ldg(prm.t_kind + rs + t);
         const int32_t q0 = __ldg(prm.t_col_idx + rs + t) * prm.col_mul;
         const int s = g & 1;
-        HLA_PW(5, sm100::mbar_wait(kFuse ? &sm.d_full[s] : &sm.q_full[s], (g >> 1) & 1));
+        HLA_PW(5, sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1));
+        if (kFuse) {   // a newly loaded q-block (the producer's stage tags, mirrored): form D and the
+                       // log2-domain LSE in its stage from the O tile (form_d), then free the O tile
+          const int64_t tag = ((int64_t)b * prm.heads + h) * prm.N + q0;
+          if (tag != (s ? dtag1 : dtag0)) {
+            if (s) dtag1 = tag; else dtag0 = tag;
+            sm100::mbar_wait(&sm.o_full, n_od & 1);
+            ++n_od;
+            form_d<D>(sm100::smem_u32(sm.dq_stage), sm100::smem_u32(sm.dO[s]), sm.dd[s], sm.lse[s], cth, prm.N - q0,
+                      prm.scale);
+            sm100::fence_proxy_async_smem();   // O-stage reads before the next TMA write into it
+            sm100::named_bar_sync(kBarFormD, kCmpThreads);
+            if (cth == 0) sm100::mbar_arrive(&sm.o_empty);
+          }
+        }
         const uint32_t lse2 = sm100::smem_u32(sm.lse[s]);
         const uint32_t dd = sm100::smem_u32(sm.dd[s]);
         const uint32_t dsbuf = sm100::smem_u32(sm.ds[g & 1]);
@@ -571,50 +588,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kEpCols = ep_cols<D>();
     uint32_t g = 0, n = 0;
     uint32_t dq_drained0 = 0, dq_drained1 = 0;   // chains drained per dQ accumulator
-    // kFuse: a cursor over the same tile sequence, one tile ahead of the drains (d_upto), forms
-    // D and the log2-domain LSE of each newly loaded q-block (the producer's stage tags, mirrored)
-    TileIter dit;
-    uint32_t gd = 0, n_od = 0;
-    int64_t dtag0 = -1, dtag1 = -1;
-    if (kFuse) dit.init(prm.t_row_ptr, ug);
-    auto d_step = [&]() {   // the cursor's next tile (waits for its operands)
-      const int s = gd & 1;
-      sm100::mbar_wait(&sm.q_full[s], (gd >> 1) & 1);
-      const int32_t bh_d = prm.mk_div.div(dit.u);
-      const int32_t bd = prm.heads_div.div(bh_d), hd = bh_d - bd * prm.heads;
-      const int32_t qblk = __ldg(prm.t_col_idx + dit.rs + dit.t);
-      const int64_t tag = ((int64_t)bd * prm.heads + hd) * prm.N + qblk;
-      if (tag != (s ? dtag1 : dtag0)) {
-        sm100::mbar_wait(&sm.o_full, n_od & 1);
-        if (s) dtag1 = tag; else dtag0 = tag;
-        ++n_od;
-        const uint32_t ob = sm100::smem_u32(sm.dq_stage), gb = sm100::smem_u32(sm.dO[s]);
-        float acc0 = 0.f, acc1 = 0.f;
-#pragma unroll
-        for (int j = 0; j < D / 8; ++j) {
-          const uint32_t off = (uint32_t)row * (D * 2) + (uint32_t)j * 16u;
-          const uint32_t so = D == 64 ? sm100::swz128(off) : sm100::swz64(off);
-          const float4 a = sm100::lds_f4(ob + so), c = sm100::lds_f4(gb + so);
-          const float av[4] = {a.x, a.y, a.z, a.w}, cv[4] = {c.x, c.y, c.z, c.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const uint32_t aw = __float_as_uint(av[e]), cw = __float_as_uint(cv[e]);
-            acc0 = fmaf(__uint_as_float(aw << 16), __uint_as_float(cw << 16), acc0);
-            acc1 = fmaf(__uint_as_float(aw & 0xffff0000u), __uint_as_float(cw & 0xffff0000u), acc1);
-          }
-        }
-        sm.dd[s][row] = (acc0 + acc1) * prm.scale;
-        if (qblk * prm.col_mul + row < prm.N) sm.lse[s][row] *= kLog2e;   // raw LSE -> log2 domain
-        sm100::fence_proxy_async_smem();   // before the async proxy refills the O / LSE stages
-        sm100::mbar_arrive(&sm.o_empty);
-      }
-      sm100::mbar_arrive(&sm.d_full[s]);
-      dit.advance(prm.t_row_ptr, ug);
-      ++gd;
-    };
-    auto d_upto = [&](uint32_t target) {
-      while (dit.valid && gd <= target) d_step();
-    };
     for (int32_t kq = 0;; ++kq) {
       const int32_t u = unit_at(kq, ug);
       if (u == kUnitEnd) break;
@@ -623,7 +596,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int32_t b = prm.heads_div.div(bh_u), h = bh_u - b * prm.heads;
       const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
       for (int t = 0; t < nt; ++t, ++g) {
-        if (kFuse) d_upto(g + 1);
         const uint32_t fdq = dq_plan(prm.t_dq, rs + t, g);
         if (!(fdq & HLA_DQ_DRAIN)) continue;   // the chain continues in TMEM
         const int dqb = (int)(fdq & HLA_DQ_BUF);

@@ -196,6 +196,37 @@ __device__ __forceinline__ void store_rows_t(const uint32_t* w, uint4* rowp, uin
   }
 }
 
+// Preprocess folded into the kernel (kFuse): D * scale = rowsum(dO o O) * scale and the log2-domain
+// LSE of a newly loaded q-block, formed in place in its stage by the 256 compute threads (two per
+// query row, half a row each; t = 0 .. 255) from the O tile and the stage's dO tile (swizzled rows
+// as loaded by TMA).  The caller synchronises the 256 threads afterwards.
+template <int D>
+__device__ __forceinline__ void form_d(uint32_t ostage, uint32_t dostage, float* dd, float* lse, int t,
+                                       int32_t real_rows, float scale) {
+  const int r = t >> 1, hf = t & 1;
+  float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+  for (int j = 0; j < D / 16; ++j) {
+    const uint32_t off = (uint32_t)r * (D * 2) + (uint32_t)(hf * (D / 16) + j) * 16u;
+    const uint32_t so = D == 64 ? sm100::swz128(off) : sm100::swz64(off);
+    const float4 a = sm100::lds_f4(ostage + so), c = sm100::lds_f4(dostage + so);
+    const float av[4] = {a.x, a.y, a.z, a.w}, cv[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t aw = __float_as_uint(av[e]), cw = __float_as_uint(cv[e]);
+      acc0 = fmaf(__uint_as_float(aw << 16), __uint_as_float(cw << 16), acc0);
+      acc1 = fmaf(__uint_as_float(aw & 0xffff0000u), __uint_as_float(cw & 0xffff0000u), acc1);
+    }
+  }
+  float acc = acc0 + acc1;
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  if (hf == 0) {
+    dd[r] = acc * scale;
+    if (r < real_rows) lse[r] *= kLog2e;   // raw LSE -> log2 domain (phantom rows: never loaded)
+  }
+}
+constexpr uint32_t kBarFormD = 4;   // named barrier of the 256 compute threads after form_d
+
 // cell -> (row << 16) | col (RPB offsets; grid sides < 2^15)
 __device__ __forceinline__ int32_t rpb_cell_rc(const int32_t* cells, int32_t seq, int32_t N, const FastDiv& W) {
   const int32_t cell = seq < N ? (cells ? __ldg(cells + seq) : seq) : 0;

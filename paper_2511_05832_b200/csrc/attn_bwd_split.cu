@@ -54,7 +54,7 @@ struct SplitSmem {
   alignas(16) float rpb_wmax[2][8];                // kBias: per compute warp max |dL/dscore| of a tile (tile parity)
   uint64_t kv_full[2], kv_empty[2], q_full[2], q_empty[2], s_full[2], ds_ready[2], dq_full[2], dq_free[2], dkv_full,
       epi_done;
-  uint64_t o_full, o_empty, d_full[2];   // kFuse (preprocess folded in), as in attn_bwd.cu
+  uint64_t o_full, o_empty;   // kFuse (preprocess folded in), as in attn_bwd.cu
   uint32_t tmem_base;
   int32_t rpb_win[kBias ? rpb_win_cap<D>() : 1];   // dRPB of the current tile's offset box, fixed point (compute warps)
   // per dQ warp: row-store transpose (store_rows_t); no room next to the dRPB window
@@ -63,8 +63,8 @@ struct SplitSmem {
 
 // kFuse: the preprocess folded into the kernel (every dQ chain local, no bias) exactly as in the
 // full-tile schedule (attn_bwd.cu): warp 0 loads the raw LSE and the O tile into the dq_stage
-// bytes, the dQ warpgroup forms D * scale and LSE * log2(e) one tile ahead of its drains, the
-// compute warps wait d_full instead of q_full; tmDQ is the O map.
+// bytes, the compute threads form D * scale and LSE * log2(e) (form_d) when they first meet a
+// q-block; tmDQ is the O map.
 template <int D, bool kTwoD, bool kGather, bool kBias, bool kFuse>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -100,8 +100,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     sm100::mbar_init(&sm.dkv_full, 1);
     sm100::mbar_init(&sm.epi_done, 128);
     sm100::mbar_init(&sm.o_full, 1);
-    sm100::mbar_init(&sm.o_empty, 128);
-    for (int s = 0; s < 2; ++s) sm100::mbar_init(&sm.d_full[s], 128);
+    sm100::mbar_init(&sm.o_empty, 1);
         sm100::fence_mbar_init();
     sm100::tma_prefetch_desc(&tmQ);
     sm100::tma_prefetch_desc(&tmK);
@@ -322,6 +321,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;
     const int cset = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;
+    const int cth = (warp - 2) * 32 + lane;   // compute thread 0 .. 255
+    uint32_t n_od = 0;                          // kFuse: O tiles consumed
+    int64_t dtag0 = -1, dtag1 = -1;             // kFuse: q-block held by stage 0 / 1
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = prm.scale_log2, scale = prm.scale;
     if (kBias) {   // the dRPB window starts (and is left after every flush) zeroed
@@ -374,7 +376,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           win = wrows * wc <= rpb_win_cap<D>();
           kwb = (prm.grid_h - 1) * prm.rpb_w + prm.grid_w - 1 + k_b + dr0 * wc + dc0;
         }
-        sm100::mbar_wait(kFuse ? &sm.d_full[s] : &sm.q_full[s], (g >> 1) & 1);
+        sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1);
+        if (kFuse) {   // a newly loaded q-block (the producer's stage tags, mirrored): form D and the
+                       // log2-domain LSE in its stage from the O tile (form_d), then free the O tile
+          const int64_t tag = ((int64_t)b * prm.heads + h) * prm.N + q0;
+          if (tag != (s ? dtag1 : dtag0)) {
+            if (s) dtag1 = tag; else dtag0 = tag;
+            sm100::mbar_wait(&sm.o_full, n_od & 1);
+            ++n_od;
+            form_d<D>(sm100::smem_u32(sm.dq_stage), sm100::smem_u32(sm.dO[s]), sm.dd[s], sm.lse[s], cth, prm.N - q0,
+                      prm.scale);
+            sm100::fence_proxy_async_smem();   // O-stage reads before the next TMA write into it
+            sm100::named_bar_sync(kBarFormD, 256);
+            if (cth == 0) sm100::mbar_arrive(&sm.o_empty);
+          }
+        }
         const uint32_t lse2 = sm100::smem_u32(sm.lse[s]);
         const uint32_t dd = sm100::smem_u32(sm.dd[s]);
         const uint32_t qa = sm100::smem_u32(sm.qa[s]);
@@ -545,49 +561,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool leader = warp == 10 && lane == 0;
     uint32_t g = 0, n = 0;
     uint32_t dq_drained0 = 0, dq_drained1 = 0;   // chains drained per dQ accumulator
-    // kFuse: the D / log2-LSE cursor, one tile ahead of the drains (as in attn_bwd.cu)
-    TileIter dit;
-    uint32_t gd = 0, n_od = 0;
-    int64_t dtag0 = -1, dtag1 = -1;
-    if (kFuse) dit.init(prm.t_row_ptr, ug);
-    auto d_step = [&]() {
-      const int s = gd & 1;
-      sm100::mbar_wait(&sm.q_full[s], (gd >> 1) & 1);
-      const int32_t bh_d = prm.mk_div.div(dit.u);
-      const int32_t bd = prm.heads_div.div(bh_d), hd = bh_d - bd * prm.heads;
-      const int32_t qblk = __ldg(prm.t_col_idx + dit.rs + dit.t);
-      const int64_t tag = ((int64_t)bd * prm.heads + hd) * prm.N + qblk;
-      if (tag != (s ? dtag1 : dtag0)) {
-        sm100::mbar_wait(&sm.o_full, n_od & 1);
-        if (s) dtag1 = tag; else dtag0 = tag;
-        ++n_od;
-        const uint32_t ob = sm100::smem_u32(sm.dq_stage), gb = sm100::smem_u32(sm.dO[s]);
-        float acc0 = 0.f, acc1 = 0.f;
-#pragma unroll
-        for (int j = 0; j < D / 8; ++j) {
-          const uint32_t off = (uint32_t)row * (D * 2) + (uint32_t)j * 16u;
-          const uint32_t so = D == 64 ? sm100::swz128(off) : sm100::swz64(off);
-          const float4 a = sm100::lds_f4(ob + so), c = sm100::lds_f4(gb + so);
-          const float av[4] = {a.x, a.y, a.z, a.w}, cv[4] = {c.x, c.y, c.z, c.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const uint32_t aw = __float_as_uint(av[e]), cw = __float_as_uint(cv[e]);
-            acc0 = fmaf(__uint_as_float(aw << 16), __uint_as_float(cw << 16), acc0);
-            acc1 = fmaf(__uint_as_float(aw & 0xffff0000u), __uint_as_float(cw & 0xffff0000u), acc1);
-          }
-        }
-        sm.dd[s][row] = (acc0 + acc1) * prm.scale;
-        if (qblk * prm.col_mul + row < prm.N) sm.lse[s][row] *= kLog2e;   // raw LSE -> log2 domain
-        sm100::fence_proxy_async_smem();   // before the async proxy refills the O / LSE stages
-        sm100::mbar_arrive(&sm.o_empty);
-      }
-      sm100::mbar_arrive(&sm.d_full[s]);
-      dit.advance(prm.t_row_ptr, ug);
-      ++gd;
-    };
-    auto d_upto = [&](uint32_t target) {
-      while (dit.valid && gd <= target) d_step();
-    };
     for (int32_t kq = 0;; ++kq) {
       const int32_t u = unit_at(kq, ug);
       if (u == kUnitEnd) break;
@@ -596,7 +569,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int32_t b = prm.heads_div.div(bh_u), h = bh_u - b * prm.heads;
       const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
       for (int t = 0; t < nt; ++t, ++g) {
-        if (kFuse) d_upto(g + 1);
         const uint32_t fdq = dq_plan(prm.t_dq, rs + t, g);
         if (!(fdq & HLA_DQ_DRAIN)) continue;   // the chain continues in TMEM
         const int dqb = (int)(fdq & HLA_DQ_BUF);
