@@ -14,15 +14,16 @@ import paper_2511_05832_b200 as hla
 from paper_2511_05832_b200 import _lib, api
 
 CASES = {"cfg2": ("HWA", 64, 16, 16, 8), "cfg3": ("HSA", 64, 16, 16, 8), "cfg4": ("HNA", 128, 7, 16, 12),
-         "dense2": ("DENSE", 64, 1, 16, 8)}
+         "dense2": ("DENSE", 64, 1, 16, 8), "cfg5s1": ("HWA", 64, 8, 128, 3, 32), "cfg5s2": ("HWA", 32, 8, 128, 6, 32)}
 SLOTS = ["mma:s_free", "mma:poll_loop", "mma:loop_total", "sm:s_full", "sm:S_load", "sm:compute", "sm:pv_done",
          "sm:P_store", "sm:o_full", "sm:epilogue", "sm:epi+meta", "tma:o_staged", "tma:store_o", "tma:kv_empty",
          "-", "-", "-", "-", "-", "sm:s_full@t0", "-", "-", "-"]
 L = _lib.lib()
 for name in (sys.argv[1:] or ["cfg2", "cfg3", "cfg4"]):
-    kind, g, w, B, H = CASES[name]
-    q, k, v, do = hla_synth.attention_inputs(B, g * g, H, 64, device="cuda")
-    lay = hla.HilbertLocalAttention(kind, g, g, w, w, B, H, 64, device="cuda")
+    kind, g, w, B, H = CASES[name][:5]
+    d = CASES[name][5] if len(CASES[name]) > 5 else 64
+    q, k, v, do = hla_synth.attention_inputs(B, g * g, H, d, device="cuda")
+    lay = hla.HilbertLocalAttention(kind, g, g, w, w, B, H, d, device="cuda")
     s2c = None if os.environ.get("HLA_NO_GATHER") else lay.s2c
     lay.forward(q, k, v)
     for _ in range(3):   # the fused-reorder attention call of the layer (HLA_NO_GATHER=1: plain order)
