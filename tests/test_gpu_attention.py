@@ -326,7 +326,7 @@ def test_dq_plan_matches_no_plan(kind, g, w, B, H, d, fused):
 
 @pytest.mark.parametrize("g,w,B,H,d,blk", [(64, 16, 2, 4, 64, 128), (32, 16, 2, 3, 32, 128), (48, 16, 1, 2, 64, 128),
                                            (16, 16, 1, 2, 64, 128), (32, 8, 2, 3, 32, 128), (32, 8, 2, 3, 32, 64),
-                                           (16, 8, 2, 2, 64, 64)])
+                                           (16, 8, 2, 2, 64, 64), (8, 8, 2, 3, 32, 64), (8, 8, 1, 2, 32, 128)])
 @pytest.mark.parametrize("fused", [True, False])
 def test_bwd_fused_preprocess_matches_staged(g, w, B, H, d, blk, fused):
     """hla_attn_bwd folds the preprocess into the main kernel when every q-block's dQ is local
