@@ -58,6 +58,16 @@ constexpr int kRegsCtl = HLA_FWD_REGS_CTL, kRegsSm = 256 - HLA_FWD_REGS_CTL;
 #endif
 template <int D>
 constexpr bool warp_ostore() { return HLA_FWD_OSTORE == 1 || (HLA_FWD_OSTORE == 2 && D == 32); }
+// d = 32: S 128 + P 64 + O 32 leave 32 TMEM columns, so O is double-buffered by unit parity
+// (columns 192 / 224) and a unit's epilogue is deferred until the next unit's first P is in
+// TMEM: it then overlaps that tile's PV / next S on the tensor pipe instead of waiting for
+// the unit's last PV (cfg5 runs one tile per unit).  O is staged in its own shared-memory tile.
+#ifndef HLA_FWD_ODB
+#define HLA_FWD_ODB 1
+#endif
+
+template <int D>
+constexpr bool o_double() { return HLA_FWD_ODB != 0 && D == 32 && warp_ostore<D>(); }
 
 struct FwdParams {
   Pattern pat;
@@ -89,6 +99,7 @@ struct FwdSmem {
   // kBias: table offsets B_k of the keys of K/V stage s, written by the K producer
   // before it arms k_full[s] (read by the softmax after waiting on the same phase)
   alignas(16) int32_t key_b[2][kBias ? 128 : 4];
+  alignas(1024) uint8_t ostage[o_double<D>() ? kBlock * D * 2 : 16];   // deferred O epilogue staging (d = 32)
 };
 
 template <int D>
@@ -520,6 +531,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       HLA_PMARK(tl0);
       while (it.valid) {
         const int32_t ct = it.t, cnt = it.nt;
+        const uint32_t tOb = tO + (o_double<D>() ? 32u * (it.n & 1u) : 0u);   // this unit's O buffer
         it.advance(prm.row_ptr, prm.mq_div, units);
         // Two independent issues: S(g+1) (needs the softmax to have pulled S(g) into
         // registers, and the next Q / K landed) and PV(g) (needs P(g)).  Whichever is
@@ -542,7 +554,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             sm100::tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < kBlock / 16; ++kk)
-              sm100::mma_ts(tO, tP + kk * 8, mnmajor_desc<D>(sm.v[g & 1], kk), idesc_o,
+              sm100::mma_ts(tOb, tP + kk * 8, mnmajor_desc<D>(sm.v[g & 1], kk), idesc_o,
                             (ct > 0 || kk > 0) ? 1u : 0u);
             sm100::mma_commit(&sm.kv_empty[g & 1]);
             sm100::mma_commit(&sm.pv_done);
@@ -593,6 +605,51 @@ __global__ void __launch_bounds__(kThreads, 2)
       meta = load_meta(prm.col_idx, prm.kind, it.rs, it.nt, lane);
       pm = load_meta_raw(prm.col_idx, prm.kind, it.prs, it.pre - it.prs, lane);
     }
+    // o_double<D>(): the deferred epilogue of the previous unit (its O buffer, normalisation and
+    // destination row) runs right after the next unit's first P store (pv_done of its last tile
+    // has been waited by then, so its O is complete)
+    bool pend = false;
+    uint32_t pend_ob = 0;
+    float pend_inv_l = 0.f;
+    unsigned long long pend_optr = 0;   // 0: phantom row
+    bool pend_staged = false;
+    auto run_pending = [&]() {
+      uint32_t o[D];
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c)
+        sm100::tmem_ld32(tmem + lane_off + kColO + pend_ob + c * 32, *reinterpret_cast<uint32_t(*)[32]>(o + c * 32));
+      sm100::tmem_wait_ld();
+      const uint32_t stage = sm100::smem_u32(sm.ostage);
+#pragma unroll
+      for (int v4 = 0; v4 < D / 8; ++v4) {
+        uint4 w;
+        w.x = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 0]) * pend_inv_l, __uint_as_float(o[v4 * 8 + 1]) * pend_inv_l);
+        w.y = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 2]) * pend_inv_l, __uint_as_float(o[v4 * 8 + 3]) * pend_inv_l);
+        w.z = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 4]) * pend_inv_l, __uint_as_float(o[v4 * 8 + 5]) * pend_inv_l);
+        w.w = sm100::pack_bf16(__uint_as_float(o[v4 * 8 + 6]) * pend_inv_l, __uint_as_float(o[v4 * 8 + 7]) * pend_inv_l);
+        if (pend_staged) {
+          const uint32_t off = (uint32_t)row * (D * 2) + v4 * 16;
+          sm100::sts_u4(stage + sm100::swz64(off), w.x, w.y, w.z, w.w);
+        } else if (pend_optr) {
+          reinterpret_cast<uint4*>(pend_optr)[v4] = w;
+        }
+      }
+      if (pend_staged) {   // this warp's rows back transposed: each STG.128 writes 8 whole 64-B rows
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int rl = lane / 4 + 8 * k, c = lane % 4;
+          const uint32_t off = (uint32_t)(quarter * 32 + rl) * (D * 2) + (uint32_t)c * 16u;
+          const float4 v = sm100::lds_f4(stage + sm100::swz64(off));
+          const unsigned long long p = __shfl_sync(0xffffffffu, pend_optr, rl);
+          if (p)
+            reinterpret_cast<uint4*>(p)[c] =
+                make_uint4(__float_as_uint(v.x), __float_as_uint(v.y), __float_as_uint(v.z), __float_as_uint(v.w));
+        }
+        __syncwarp();   // (the staging rows are rewritten by the next deferred epilogue)
+      }
+      pend = false;
+    };
     // RPB: the row's table offset A_q (per unit); the keys' B_k come staged with K
     while (it.valid) {
       const int32_t bh_u = prm.mq_div.div(it.u), qb = it.u - bh_u * mq;
@@ -605,6 +662,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       const float* rpbh = kBias ? prm.rpb + (int64_t)h * prm.rpb_hw : nullptr;
       const int32_t a_q = kBias ? prm.rpb_a0 + rpb_cell_off(prm.cells, q, prm.N, prm.pat.w_div, prm.rpb_w) : 0;
       if (row == 0) HLA_TR((2 << 24) | (6 << 16) | it.n);
+      const uint32_t obuf = o_double<D>() ? 32u * (it.n & 1u) : 0u;   // this unit's O columns
       for (int t = 0; t < it.nt; ++t, ++g) {
         HLA_PMARK(tw0);
         HLA_PW(3, sm100::mbar_wait(&sm.s_full, g & 1));
@@ -631,6 +689,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           sm100::tmem_wait_st();
           sm100::tc_fence_before();
           sm100::mbar_arrive(&sm.p_full);
+          if (o_double<D>() && pend) run_pending();
           continue;
         }
         // the whole S row: four loads in flight, one wait (TMEM round trip ~200 cycles)
@@ -705,13 +764,13 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
             uint32_t o[32];
-            sm100::tmem_ld16(tmem + lane_off + kColO + c * 32, o);
-            sm100::tmem_ld16(tmem + lane_off + kColO + c * 32 + 16, o + 16);
+            sm100::tmem_ld16(tmem + lane_off + kColO + obuf + c * 32, o);
+            sm100::tmem_ld16(tmem + lane_off + kColO + obuf + c * 32 + 16, o + 16);
             sm100::tmem_wait_ld();
 #pragma unroll
             for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            sm100::tmem_st16(tmem + lane_off + kColO + c * 32, o);
-            sm100::tmem_st16(tmem + lane_off + kColO + c * 32 + 16, o + 16);
+            sm100::tmem_st16(tmem + lane_off + kColO + obuf + c * 32, o);
+            sm100::tmem_st16(tmem + lane_off + kColO + obuf + c * 32 + 16, o + 16);
           }
         }
 #pragma unroll
@@ -719,6 +778,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         sm100::tmem_wait_st();
         sm100::tc_fence_before();
         sm100::mbar_arrive(&sm.p_full);
+        if (o_double<D>() && pend) run_pending();
         HLA_PADD(7, tst0);
         if (row == 0) HLA_TR((2 << 24) | (2 << 16) | g);
       }
@@ -727,6 +787,27 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int64_t orow = ((int64_t)b * prm.N + ocell) * prm.heads + h;
       uint4* optr = reinterpret_cast<uint4*>(prm.o + orow * D);
       const float inv_l = l > 0.f ? 1.f / l : 0.f;
+      if constexpr (o_double<D>()) {
+        // deferred (run_pending after the next unit's first P store); the Q stage is free now
+        pend = true;
+        pend_ob = obuf;
+        pend_inv_l = inv_l;
+        pend_optr = real ? reinterpret_cast<unsigned long long>(optr) : 0ull;
+        pend_staged = (qb + 1) * kBlock <= prm.N;
+        sm100::mbar_arrive(&sm.o_staged[it.n & 1]);
+        const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
+        if (real)
+          prm.lse[((int64_t)b * prm.heads + h) * prm.N + q] =
+              l > 0.f ? (m_use + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+        tiles_done += it.nt;
+        it.t = it.nt - 1;
+        it.advance(prm.row_ptr, prm.mq_div, units);
+        if (it.valid) {
+          meta = it.from_pf ? (pm.c << 2) | pm.k : load_meta(prm.col_idx, prm.kind, it.rs, it.nt, lane);
+          pm = load_meta_raw(prm.col_idx, prm.kind, it.prs, it.pre - it.prs, lane);
+        }
+        continue;
+      }
       HLA_PW(8, sm100::mbar_wait(&sm.o_full, it.n & 1));
       HLA_PMARK(te0);
       if (row == 0) HLA_TR((2 << 24) | (3 << 16) | it.n);
@@ -792,6 +873,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
       HLA_PADD(10, te0);
       if (row == 0) HLA_TR((2 << 24) | (5 << 16) | it.n);
+    }
+    if (o_double<D>() && pend) {   // the last unit: its final PV (tile g - 1) must be complete
+      sm100::mbar_wait(&sm.pv_done, (g - 1) & 1);
+      sm100::tc_fence_after();
+      run_pending();
     }
     HLA_PFLUSH(3, 11, warp == 4 && lane == 0);
     HLA_PFLUSH(19, 20, warp == 4 && lane == 0);
