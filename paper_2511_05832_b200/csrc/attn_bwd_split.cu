@@ -25,9 +25,16 @@
 // Global-RPB score_mod (kBias): the bias joins the P recompute, and dL/dscore is
 // accumulated per 2D offset in a shared-memory window (fixed point at the previous tile's
 // scale, attn_bwd_common.cuh) flushed once per tile.
+#ifdef HLA_BWD_PROF
+#define HLA_PROF_ON
+#endif
 #include "attn_bwd_common.cuh"
 
 namespace hla {
+#ifdef HLA_BWD_PROF
+__device__ unsigned long long g_bwd_split_prof[1024][24];
+#define HLA_PROF_ARRAY g_bwd_split_prof
+#endif
 namespace bwd {
 namespace {
 
@@ -118,6 +125,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned long long tiles_done = 0;
 
   if (warp == 0 || warp >= 14) {
+    HLA_PDECL;
     // ----------------------------------------------------------- TMA producers
     // Three warps run the same schedule and split the loads (a CTA's TMA gather4
     // throughput grows with the number of issuing warps): warp 0 K + LSE / D,
@@ -141,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t bh = (int64_t)b * prm.heads + h;
         const int kvs = n & 1;
         if (role < 2) {
-          if (n >= 2) sm100::mbar_wait(&sm.kv_empty[kvs], ((n >> 1) - 1) & 1);
+          if (n >= 2) HLA_PW(13, sm100::mbar_wait(&sm.kv_empty[kvs], ((n >> 1) - 1) & 1));
           if (kVar & 4) {
             if (lane == 0) sm100::mbar_arrive(&sm.kv_full[kvs]);
           } else {
@@ -153,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int t = 0; t < nt; ++t, ++g) {
           const int s = g & 1;
-          if (g >= 2) sm100::mbar_wait(&sm.q_empty[s], ((g >> 1) - 1) & 1);
+          if (g >= 2) HLA_PW(14, sm100::mbar_wait(&sm.q_empty[s], ((g >> 1) - 1) & 1));
           const int32_t qblk = __ldg(prm.t_col_idx + rs + t);
           const int64_t tag = bh * prm.N + qblk;     // (b, h, q-block) held by the stage
           if (tag == (s ? stage_tag1 : stage_tag0)) {
@@ -207,11 +215,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++n;
       }
     }
+    HLA_PFLUSH(13, 15, warp == 0 && lane == 0);
   } else if (warp == 1) {
     // ------------------------------------------------------------- MMA issuer
     // Half-tile software pipeline over the flattened (unit, q-block) sequence:
     //   S_A,dP_A(g) S_B,dP_B(g) | dV_A dK_A(g) S_A,dP_A(g+1) | dV_B dK_B dQ(g) S_B,dP_B(g+1) | ...
     // so the tensor core works on one q-half while the compute warps process the other.
+    HLA_PDECL;
     if (lane == 0) {
       constexpr uint32_t idesc_h = sm100::make_idesc_bf16(kBlock, kHalf, false, false);  // S^T, dP^T halves
       constexpr uint32_t idesc_kv = sm100::make_idesc_bf16(kBlock, D, false, true);      // dV, dK
@@ -255,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         issue_sdp(cur, 0, 0);
         issue_sdp(cur, 0, 1);
       }
+      HLA_PMARK(tl0);
       while (cur.valid) {
         TileIter nxt = cur;
         nxt.advance(prm.t_row_ptr, ug);
@@ -262,11 +273,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kvs = cur.n & 1;
         const bool last_of_unit = cur.t == cur.nt - 1;
         // half A of tile g
-        sm100::mbar_wait(&sm.ds_ready[0], g & 1);
+        HLA_PW(0, sm100::mbar_wait(&sm.ds_ready[0], g & 1));
         sm100::tc_fence_after();
         if (cur.t == 0 && cur.n > 0) {
           // the previous unit's dV / dK must have been drained from TMEM
-          sm100::mbar_wait(&sm.epi_done, (cur.n - 1) & 1);
+          HLA_PW(1, sm100::mbar_wait(&sm.epi_done, (cur.n - 1) & 1));
           sm100::tc_fence_after();
         }
         issue_dvdk(g, 0, cur.t == 0);
@@ -280,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           next_a_issued = true;
         }
         // half B of tile g, then dQ (needs both halves of dS)
-        sm100::mbar_wait(&sm.ds_ready[1], g & 1);
+        HLA_PW(0, sm100::mbar_wait(&sm.ds_ready[1], g & 1));
         sm100::tc_fence_after();
         issue_dvdk(g, 1, false);
         sm100::mma_commit(&sm.q_empty[g & 1]);   // Q_g / dO_g no longer read (dQ needs only dS and K)
@@ -291,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // a new chain: the accumulator's previous chain must have been drained
           const uint32_t c = dqb ? dq_started1++ : dq_started0++;
           if (c > 0) {
-            sm100::mbar_wait(&sm.dq_free[dqb], (c - 1) & 1);
+            HLA_PW(3, sm100::mbar_wait(&sm.dq_free[dqb], (c - 1) & 1));
             sm100::tc_fence_after();
           }
         }
@@ -303,8 +314,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (last_of_unit) sm100::mma_commit(&sm.kv_empty[kvs]);
         if (nxt.valid) {
           if (!next_a_issued) {
-            if (nxt.t == 0) sm100::mbar_wait(&sm.kv_full[nxt.n & 1], (nxt.n >> 1) & 1);
-            sm100::mbar_wait(&sm.q_full[(g + 1) & 1], ((g + 1) >> 1) & 1);
+            if (nxt.t == 0) HLA_PW(2, sm100::mbar_wait(&sm.kv_full[nxt.n & 1], (nxt.n >> 1) & 1));
+            HLA_PW(2, sm100::mbar_wait(&sm.q_full[(g + 1) & 1], ((g + 1) >> 1) & 1));
             sm100::tc_fence_after();
             issue_sdp(nxt, g + 1, 0);
           }
@@ -313,8 +324,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         cur = nxt;
         ++g;
       }
+      HLA_PADD(4, tl0);
+#ifdef HLA_BWD_PROF
+      prof[15] = g;
+#endif
+      HLA_PFLUSH(0, 5, true);
+      HLA_PFLUSH(15, 16, true);
     }
   } else if (warp < 10) {
+    HLA_PDECL;
     // --------------------------------------------- P^T / dS^T (thread = key row)
     // two warp sets (cset 0: warps 2-5, cset 1: warps 6-9) share every TMEM lane
     // quarter; within each q-half, cset c processes the 32-column chunk 2*half + c.
@@ -376,7 +394,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           win = wrows * wc <= rpb_win_cap<D>();
           kwb = (prm.grid_h - 1) * prm.rpb_w + prm.grid_w - 1 + k_b + dr0 * wc + dc0;
         }
-        sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1);
+        HLA_PW(5, sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1));
+        HLA_PMARK(tc0);
         if (kFuse) {   // a newly loaded q-block (the producer's stage tags, mirrored): form D and the
                        // log2-domain LSE in its stage from the O tile (form_d), then free the O tile
           const int64_t tag = ((int64_t)b * prm.heads + h) * prm.N + q0;
@@ -398,26 +417,43 @@ __global__ void __launch_bounds__(kThreads, 1)
         float tmax = 0.f;   // kBias: largest |dL/dscore| of the tile (this thread)
 #pragma unroll 1
         for (int half = 0; half < 2; ++half) {
-          sm100::mbar_wait(&sm.s_full[half], g & 1);
+          HLA_PW(6, sm100::mbar_wait(&sm.s_full[half], g & 1));
           sm100::tc_fence_after();
-          if (!(kVar & 2)) {
-            const int c = 2 * half + cset;
+          const int c = 2 * half + cset;
+          // [ulo, uhi): 8-column groups of this chunk that hold an allowed query of some key row
+          // of this warp (partial tiles of 1D patterns: each key row's queries are one interval);
+          // the other groups are all masked, their exponentials skipped (warp-uniform) and P = 0
+          // there.  elem: some row of the warp has a masked query in the chunk (else no element
+          // mask).  Full tiles / 2D patterns: all 4 groups, element mask on partial tiles.
+          int ulo = 0, uhi = 4;
+          bool elem = kd == 2;
+          if (!kBias && kd == 2 && !kTwoD) {   // (with the RPB gather the branchy loop measured slower: cfg5 +6%)
+            const int32_t base = q0 + c * 32;
+            const int32_t lo = min(max(box.lo - base, 0), 32), hi = min(max(box.lo + box.len - base, 0), 32);
+            const bool any = hi > lo;
+            ulo = __reduce_min_sync(0xffffffffu, any ? lo : 32) >> 3;
+            uhi = (__reduce_max_sync(0xffffffffu, any ? hi : 0) + 7) >> 3;
+            elem = !__all_sync(0xffffffffu, lo == 0 && hi == 32);
+          }
+          if (!(kVar & 2) && ulo >= uhi) {
+            // no key row of this warp meets a query of this chunk (e.g. the other window of an
+            // HWA-64 tile): no TMEM loads or math -- P^T and dS^T are zero there
+            uint32_t z[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) z[e] = 0u;
+            sm100::tmem_st16(tmem + lane_off + kColS + c * 32, z);
+#pragma unroll
+            for (int u4 = 0; u4 < 4; ++u4) {
+              const int qc = c * 32 + u4 * 8;
+              const uint32_t off =
+                  (uint32_t)(qc >> 6) * 16384u + sm100::swz128((uint32_t)row * 128u + (uint32_t)(qc & 63) * 2u);
+              sm100::sts_u4(dsbuf + off, 0u, 0u, 0u, 0u);
+            }
+          } else if (!(kVar & 2)) {
             uint32_t sr[32], dpr[32];
             sm100::tmem_ld32(tmem + lane_off + kColS + c * 32, sr);
             sm100::tmem_ld32(tmem + lane_off + kColDP + c * 32, dpr);
             sm100::tmem_wait_ld();
-            // [ulo, uhi): 8-column groups of this chunk that hold an allowed query of some
-            // key row of this warp (partial tiles of 1D patterns: each key row's queries are
-            // one interval); the other groups are all masked, their exponentials skipped
-            // (warp-uniform) and P = 0 there.  Full tiles / 2D patterns: all 4 groups.
-            int ulo = 0, uhi = 4;
-            if (!kBias && kd == 2 && !kTwoD) {   // (with the RPB gather the branchy loop measured slower: cfg5 +6%)
-              const int32_t base = q0 + c * 32;
-              const int32_t lo = min(max(box.lo - base, 0), 32), hi = min(max(box.lo + box.len - base, 0), 32);
-              const bool any = hi > lo;
-              ulo = __reduce_min_sync(0xffffffffu, any ? lo : 32) >> 3;
-              uhi = (__reduce_max_sync(0xffffffffu, any ? hi : 0) + 7) >> 3;
-            }
             // P first (so its TMEM store is in flight while dS is formed)
             float p[32];
 #pragma unroll
@@ -446,7 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             uint32_t okbits = 0xffffffffu;   // element mask of this chunk (partial tiles only)
-            if (kd == 2) {
+            if (elem) {
 #pragma unroll
               for (int e = 0; e < 32; ++e) {
                 const int32_t qq = q0 + c * 32 + e;
@@ -546,10 +582,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           rpb_fx = rpb_next_scale(sm.rpb_wmax[g & 1], rpb_fx);   // (stays 0 only for an all-zero tile)
           sm100::named_bar_sync(3, 256);
         }
+        HLA_PADD(7, tc0);
       }
       tiles_done += nt;
     }
+    HLA_PFLUSH(5, 8, warp == 2 && lane == 0);
   } else if (warp < 14) {
+    HLA_PDECL;
     // ------------------------------------------ dQ partial -> fp32 accumulator
     // thread = query row: drain the dQ_i tile from TMEM (then release it), stage it
     // in shared memory (two 32-column halves, 128B swizzle) and let the TMA engine
@@ -572,7 +611,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t fdq = dq_plan(prm.t_dq, rs + t, g);
         if (!(fdq & HLA_DQ_DRAIN)) continue;   // the chain continues in TMEM
         const int dqb = (int)(fdq & HLA_DQ_BUF);
-        sm100::mbar_wait(&sm.dq_full[dqb], (dqb ? dq_drained1++ : dq_drained0++) & 1);
+        HLA_PW(9, sm100::mbar_wait(&sm.dq_full[dqb], (dqb ? dq_drained1++ : dq_drained0++) & 1));
+        HLA_PMARK(td0);
         sm100::tc_fence_after();
         if (kVar & 8) {
           sm100::mbar_arrive(&sm.dq_free[dqb]);
@@ -641,7 +681,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint4* dkp = reinterpret_cast<uint4*>(prm.dk + grow * D);
       uint4* dvp = reinterpret_cast<uint4*>(prm.dv + grow * D);
       if (nt > 0) {
-        sm100::mbar_wait(&sm.dkv_full, n & 1);
+        HLA_PW(11, sm100::mbar_wait(&sm.dkv_full, n & 1));
+        HLA_PMARK(te0);
         sm100::tc_fence_after();
         if (kVar & 8) {
           sm100::mbar_arrive(&sm.epi_done);
@@ -677,6 +718,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             dkp[v4] = make_uint4(pk[v4 * 4 + 0], pk[v4 * 4 + 1], pk[v4 * 4 + 2], pk[v4 * 4 + 3]);
           }
         }
+        HLA_PADD(12, te0);
         ++n;
       } else {
 #pragma unroll
@@ -687,6 +729,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (leader) sm100::bulk_wait_group0();
+    HLA_PFLUSH(9, 13, leader);
   }
 
   sm100::tc_fence_before();
@@ -753,3 +796,13 @@ hla_status launch_split(bool bias, int head_dim, bool gather, bool two_d, bool f
 
 }  // namespace bwd
 }  // namespace hla
+
+#ifdef HLA_BWD_PROF
+// dev-only: per-CTA wait / work cycle sums of the last attn_bwd_split_kernel launch (HLA_BWD_PROF builds)
+extern "C" __attribute__((visibility("default"))) int hla_debug_bwd_split_prof(unsigned long long* host, int ctas) {
+  cudaDeviceSynchronize();
+  const int n = ctas < 1024 ? ctas : 1024;
+  cudaMemcpyFromSymbol(host, hla::g_bwd_split_prof, (size_t)n * 24 * sizeof(unsigned long long));
+  return n;
+}
+#endif

@@ -14,22 +14,27 @@ import paper_2511_05832_b200 as hla
 from paper_2511_05832_b200 import _lib
 
 CASES = {"cfg2": ("HWA", 64, 16, 16, 8), "cfg3": ("HSA", 64, 16, 16, 8), "cfg4": ("HNA", 128, 7, 16, 12),
-         "dense2": ("DENSE", 64, 1, 16, 8)}
+         "dense2": ("DENSE", 64, 1, 16, 8), "cfg5s1": ("HWA", 64, 8, 128, 3, 32), "cfg5s2": ("HWA", 32, 8, 128, 6, 32)}
 SLOTS = ["mma:ds_ready", "mma:epi_done", "mma:next_operands", "mma:dq_free", "mma:loop_total",
          "cmp:q_full", "cmp:s_full", "cmp:work", "cmp:-", "dq:dq_full", "dq:drain", "dq:dkv_full", "dq:epilogue",
          "tma:kv_empty", "tma:q_empty", "-", "cmp:until_loads_done", "cmp:until_dS_done", "cmp:until_P_done",
          "cmp:until_p_ready"]
 L = _lib.lib()
 for name in (sys.argv[1:] or ["cfg2", "cfg3", "cfg4"]):
-    kind, g, w, B, H = CASES[name]
-    q, k, v, do = hla_synth.attention_inputs(B, g * g, H, 64, device="cuda")
-    lay = hla.HilbertLocalAttention(kind, g, g, w, w, B, H, 64, device="cuda")
+    kind, g, w, B, H = CASES[name][:5]
+    d = CASES[name][5] if len(CASES[name]) > 5 else 64
+    q, k, v, do = hla_synth.attention_inputs(B, g * g, H, d, device="cuda")
+    lay = hla.HilbertLocalAttention(kind, g, g, w, w, B, H, d, device="cuda")
     for _ in range(3):
         lay.forward(q, k, v)
         lay.backward(do)
     torch.cuda.synchronize()
     buf = np.zeros((1024, 24), dtype=np.uint64)
-    n = L.hla_debug_bwd_prof(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), 148)
+    if name in ("cfg2", "dense2"):   # full-tile schedule
+        n = L.hla_debug_bwd_prof(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), 148)
+    else:                            # half-tile schedule (its own counters)
+        n = L.hla_debug_bwd_split_prof(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), 148)
+        name += " (half-tile schedule)"
     P = buf[:n].astype(np.float64)
     tiles = P[:, 15].sum()
     per = P[:, :20].sum(0) / max(tiles, 1)
