@@ -427,13 +427,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           // mask).  Full tiles / 2D patterns: all 4 groups, element mask on partial tiles.
           int ulo = 0, uhi = 4;
           bool elem = kd == 2;
-          if (!kBias && kd == 2 && !kTwoD) {   // (with the RPB gather the branchy loop measured slower: cfg5 +6%)
+          if (kd == 2 && !kTwoD) {
             const int32_t base = q0 + c * 32;
             const int32_t lo = min(max(box.lo - base, 0), 32), hi = min(max(box.lo + box.len - base, 0), 32);
             const bool any = hi > lo;
             ulo = __reduce_min_sync(0xffffffffu, any ? lo : 32) >> 3;
             uhi = (__reduce_max_sync(0xffffffffu, any ? hi : 0) + 7) >> 3;
             elem = !__all_sync(0xffffffffu, lo == 0 && hi == 32);
+            // kBias: only the whole-chunk skip (the group-skipping loop around the RPB gather
+            // measured slower: cfg5-hwt +6%)
+            if (kBias && ulo < uhi) { ulo = 0; uhi = 4; }
           }
           if (!(kVar & 2) && ulo >= uhi) {
             // no key row of this warp meets a query of this chunk (e.g. the other window of an
