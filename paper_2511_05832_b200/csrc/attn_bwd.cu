@@ -1033,7 +1033,11 @@ hla_status prepare_main(const hla_pattern_desc* d, const hla_block_mask* m, int3
   // mask's tiles; half-tile (attn_bwd_split_kernel) otherwise (the split
   // schedule overlaps the partial tiles' masked compute better) and with the global RPB (only
   // the half-tile schedule has the dRPB window: at the previous tile's scale, no extra barrier)
-  pl->full = prm.rpb == nullptr && lists.t_n_full >= lists.t_n_partial && lists.t_n_full > 0;
+#ifndef HLA_BWD_SCHED
+#define HLA_BWD_SCHED 0   // dev A/B: 0 = by tile mix, 1 = full-tile whenever possible, 2 = half-tile always
+#endif
+  pl->full = prm.rpb == nullptr && (HLA_BWD_SCHED == 1 || (HLA_BWD_SCHED == 0 && lists.t_n_full >= lists.t_n_partial &&
+                                                            lists.t_n_full > 0));
   pl->fuse = false;
   return HLA_OK;
 }
