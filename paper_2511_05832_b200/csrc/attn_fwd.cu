@@ -94,7 +94,10 @@ struct FwdSmem {
   alignas(1024) uint8_t q[2][kTileBytes];
   alignas(1024) uint8_t k[2][kTileBytes];
   alignas(1024) uint8_t v[2][kTileBytes];
-  uint64_t q_full[2], o_staged[2], k_full[2], v_full[2], kv_empty[2], s_full, s_free, p_full, pv_done, o_full;
+  // k_empty: the stage's K was read by its S MMA (K may reload while P / PV still run; with the
+  // RPB bias the key offsets are read by the softmax, so K waits for v_empty there), v_empty: PV done
+  uint64_t q_full[2], o_staged[2], k_full[2], v_full[2], k_empty[2], v_empty[2], s_full, s_free, p_full, pv_done,
+      o_full;
   uint32_t tmem_base;
   // kBias: table offsets B_k of the keys of K/V stage s, written by the K producer
   // before it arms k_full[s] (read by the softmax after waiting on the same phase)
@@ -349,7 +352,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       sm100::mbar_init(&sm.o_staged[s], 128);   // softmax threads: O(n) staged in Q stage n&1
       sm100::mbar_init(&sm.k_full[s], 2);   // producer warps 2 and 3
       sm100::mbar_init(&sm.v_full[s], 2);
-      sm100::mbar_init(&sm.kv_empty[s], 1);
+      sm100::mbar_init(&sm.k_empty[s], 1);
+      sm100::mbar_init(&sm.v_empty[s], 1);
     }
     sm100::mbar_init(&sm.s_full, 1);
     sm100::mbar_init(&sm.s_free, 128);
@@ -454,38 +458,54 @@ __global__ void __launch_bounds__(kThreads, 2)
             const int32_t r0 = kvb * prm.col_mul + hh * 64 + 4 * (lane & 15);   // this lane's 4 rows (gather)
             const int4 cells = (reuse || !kGather) ? make_int4(0, 0, 0, 0)
                                : (r0 < prm.N ? __ldg(reinterpret_cast<const int4*>(prm.s2c + r0)) : make_int4(0, 0, 0, 0));
-            if (g >= 2) sm100::mbar_wait(&sm.kv_empty[s], ((g >> 1) - 1) & 1);
+            // every arrival on k_full / v_full follows the wait on the matching empty barrier,
+            // so it always lands in this tile's phase
+            uint64_t* kfree = kBias ? &sm.v_empty[s] : &sm.k_empty[s];
+            const uint32_t par = ((g >> 1) - 1) & 1;
             if (reuse) {
-              if (lane == 0) {
-                sm100::mbar_arrive(&sm.k_full[s]);
-                sm100::mbar_arrive(&sm.v_full[s]);
-              }
+              if (g >= 2) sm100::mbar_wait(kfree, par);
+              if (lane == 0) sm100::mbar_arrive(&sm.k_full[s]);
+              if (g >= 2) sm100::mbar_wait(&sm.v_empty[s], par);
+              if (lane == 0) sm100::mbar_arrive(&sm.v_full[s]);
               continue;
             }
             if (s) tag1 = tag; else tag0 = tag;
+            if (g >= 2) sm100::mbar_wait(kfree, par);
             if (kBias && is_k) {
               const int4 bk = rpb_key_offs(prm.cells, kvb * prm.col_mul, prm.N, prm.pat.w_div, prm.rpb_w, lane);
               sm100::sts_u4(sm100::smem_u32(sm.key_b[s]) + 16u * lane, bk.x, bk.y, bk.z, bk.w);
               __syncwarp();   // every lane's offsets are written before lane 0 arms k_full
             }
-            if (kGather) {
-              if (lane == 0) {
-                sm100::mbar_arrive_expect_tx(&sm.k_full[s], kTile / 2);
-                sm100::mbar_arrive_expect_tx(&sm.v_full[s], kTile / 2);
-              }
+            const int32_t base = b * prm.N;
+            const int row = hh * 64 + 4 * (lane & 15);
+            if (kGather) {   // this warp's half of K (lanes 0-15), then, once PV freed the stage, of V
+              if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.k_full[s], kTile / 2);
               __syncwarp();
-              const bool lk = lane < 16;
-              const int32_t base = b * prm.N;
-              const int row = hh * 64 + 4 * (lane & 15);
-              sm100::tma_gather4((lk ? sm.k[s] : sm.v[s]) + row * D * 2, lk ? &tmK : &tmV,
-                                 lk ? &sm.k_full[s] : &sm.v_full[s], h * D, base + cells.x, base + cells.y,
-                                 base + cells.z, base + cells.w, pol_kv);
-            } else if (lane == 0) {
-              uint64_t* full = is_k ? &sm.k_full[s] : &sm.v_full[s];
-              sm100::mbar_arrive_expect_tx(full, kTile);
-              sm100::tma_load_3d(is_k ? sm.k[s] : sm.v[s], is_k ? &tmK : &tmV, full, 0, h, b * prm.N + kvb * prm.col_mul,
-                                 pol_kv);
-              sm100::mbar_arrive(is_k ? &sm.v_full[s] : &sm.k_full[s]);
+              if (lane < 16)
+                sm100::tma_gather4(sm.k[s] + row * D * 2, &tmK, &sm.k_full[s], h * D, base + cells.x, base + cells.y,
+                                   base + cells.z, base + cells.w, pol_kv);
+              if (g >= 2) sm100::mbar_wait(&sm.v_empty[s], par);
+              if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.v_full[s], kTile / 2);
+              __syncwarp();
+              if (lane < 16)
+                sm100::tma_gather4(sm.v[s] + row * D * 2, &tmV, &sm.v_full[s], h * D, base + cells.x, base + cells.y,
+                                   base + cells.z, base + cells.w, pol_kv);
+            } else {   // warp 2: K box, warp 3: V box; each arrives (no bytes) on the other barrier
+              if (is_k) {
+                if (lane == 0) {
+                  sm100::mbar_arrive_expect_tx(&sm.k_full[s], kTile);
+                  sm100::tma_load_3d(sm.k[s], &tmK, &sm.k_full[s], 0, h, b * prm.N + kvb * prm.col_mul, pol_kv);
+                }
+                if (g >= 2) sm100::mbar_wait(&sm.v_empty[s], par);
+                if (lane == 0) sm100::mbar_arrive(&sm.v_full[s]);
+              } else {
+                if (lane == 0) sm100::mbar_arrive(&sm.k_full[s]);
+                if (g >= 2) sm100::mbar_wait(&sm.v_empty[s], par);
+                if (lane == 0) {
+                  sm100::mbar_arrive_expect_tx(&sm.v_full[s], kTile);
+                  sm100::tma_load_3d(sm.v[s], &tmV, &sm.v_full[s], 0, h, b * prm.N + kvb * prm.col_mul, pol_kv);
+                }
+              }
             }
           }
         }
@@ -518,6 +538,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int kk = 0; kk < D / 16; ++kk)
           sm100::mma_ss(tS, kmajor_desc<D>(q, kk), kmajor_desc<D>(k, kk), idesc_s, kk > 0);
         sm100::mma_commit(&sm.s_full);
+        sm100::mma_commit(&sm.k_empty[gg & 1]);   // K(gg) read: the stage may reload its K
       };
       FwdIter it;   // always one tile ahead of the PV being issued
       it.init(prm.row_ptr, prm.mq_div, units);
@@ -556,7 +577,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int kk = 0; kk < kBlock / 16; ++kk)
               sm100::mma_ts(tOb, tP + kk * 8, mnmajor_desc<D>(sm.v[g & 1], kk), idesc_o,
                             (ct > 0 || kk > 0) ? 1u : 0u);
-            sm100::mma_commit(&sm.kv_empty[g & 1]);
+            sm100::mma_commit(&sm.v_empty[g & 1]);
             sm100::mma_commit(&sm.pv_done);
             if (ct == cnt - 1) sm100::mma_commit(&sm.o_full);
             pv_pending = false;
