@@ -168,12 +168,12 @@ def bwd_bytes(T, d, mask, fused_pre=False):
     """Algorithmic HBM bytes of the backward main kernel per launch: read Q, K, V, dO (8d per
     token-head), LSE, D (8); write dK, dV (4d); dQ: bf16 write (2d) for the q-blocks the dQ
     plan keeps local, one fp32 read + write of the accumulator (8d, TMA reduce-add) for the others.
-    fused_pre (preprocess folded into the kernel, every q-block local): read O (2d) and the raw
-    LSE (4) instead of LSE, D: T (14d + 4) + T 2d."""
+    fused_pre (preprocess folded into the kernel): read O (2d) and the raw LSE (4) instead of
+    LSE, D (8): T (14d + 4) + the dQ part (all local: T (16d + 4))."""
     mq = mask.row_ptr.numel() - 1
     nl = mq if mask.n_dq_nonlocal < 0 else mask.n_dq_nonlocal
-    if fused_pre:
-        return int(T * (16 * d + 4))
+    if fused_pre:   # O (2d) and the raw LSE (4) instead of LSE, D (8); dQ as above
+        return int(T * (14 * d + 4) + T * (2 * d * (mq - nl) + 8 * d * nl) // mq)
     return int(T * (12 * d + 8) + T * (2 * d * (mq - nl) + 8 * d * nl) // mq)
 
 

@@ -312,10 +312,12 @@ HLA_API hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_mask*
  * score_mod: as in hla_attn_fwd (same table); with global RPB, drpb receives the
  * table gradient (accumulated; hla_attn_bwd zeroes it first, hla_attn_bwd_main
  * does not).
- * When the mask's dQ plan makes every q-block local and there is no global RPB
- * (hla_attn_bwd_fuses_preprocess), hla_attn_bwd launches the main kernel
- * only: it reads the raw LSE and the O rows itself and forms D in the kernel (the
- * workspace is then not touched).  Same results up to fp32 summation order of D.
+ * Without a global RPB, when the mask's dQ plan makes every q-block local -- or the
+ * mask is a block-64 one with non-local q-blocks (half-tile schedule) -- hla_attn_bwd
+ * folds the preprocess into the main kernel (hla_attn_bwd_fuses_preprocess): it reads
+ * the raw LSE and the O rows itself and forms D in the kernel; non-local dQ rows are
+ * zeroed by a write-only pass and finalized as usual.  Same results up to the fp32
+ * summation order of D.
  */
 HLA_API hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_mask* m,
                         int32_t batch, int32_t heads, int32_t head_dim, float scale,

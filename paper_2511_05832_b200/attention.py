@@ -137,7 +137,8 @@ class HilbertLocalAttention:
         else:
             dout_s, dq, dk, dv = dout, self.dq, self.dk, self.dv
         if self.fused_bwd:
-            # one launch: the main kernel forms D / LSE itself (every dQ chain local, full-tile schedule)
+            # the main kernel forms D / LSE itself (hla_attn_bwd_fuses_preprocess; non-local dQ rows:
+            # zeroing before, finalize after, inside the same call)
             api.hla_attn_bwd(self.desc, self.mask, q, k, v, o, self.lse, dout_s, self.scale, dq, dk, dv,
                              self.workspace, seq_to_cell=self.s2c, mod=self.mod)
             mark("bwd")
@@ -164,8 +165,9 @@ class HilbertLocalAttention:
     # kernel launches per step (forward + backward)
     @property
     def launches_per_step(self):
-        if self.fused_bwd:   # fwd + the backward's main kernel
-            return 2 + (4 if (self.hilbert and not self.fused) else 0) + (1 if self._rpb is not None else 0)
+        if self.fused_bwd:   # fwd + the backward's main kernel (+ zeroing / finalize of non-local dQ rows)
+            nl = 0 if self.mask.n_dq_nonlocal == 0 else 2
+            return 2 + nl + (4 if (self.hilbert and not self.fused) else 0) + (1 if self._rpb is not None else 0)
         fin = 0 if self.mask.n_dq_nonlocal == 0 else 1   # the finalize launches nothing when every dQ is local
         return 3 + fin + (4 if (self.hilbert and not self.fused) else 0) + (1 if self._rpb is not None else 0)
 

@@ -846,6 +846,21 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
   }
 }
 
+// Folded preprocess with non-local dQ chains: the accumulator rows of non-local q-blocks := 0
+// (sequence order, 32 B per thread; rows of local q-blocks -- q_local -- are never read)
+__global__ void __launch_bounds__(256) dq_zero_kernel(float4* __restrict__ acc, const uint8_t* __restrict__ q_local,
+                                                      FastDiv N, FastDiv row_v, int32_t n_v) {
+  const int32_t t = (int32_t)blockIdx.x * blockDim.x + threadIdx.x;   // (b * N + s) * row_v + part
+  if (t >= n_v) return;
+  if (q_local) {
+    const int32_t bs = row_v.div(t);
+    const int32_t s = bs - N.div(bs) * N.d;
+    if (__ldg(q_local + (s >> 7))) return;
+  }
+  acc[2 * (int64_t)t] = make_float4(0.f, 0.f, 0.f, 0.f);
+  acc[2 * (int64_t)t + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
 // K9: dQ = bf16(accumulator) -- the accumulator is in sequence order; under the
 // fused reorder each row is written to its grid cell s2c[s] (SURVEY 8(a) a8:
 // "dQ finalize + inverse permutation").  One thread per 8 elements (32 B in, 16 B out).
@@ -896,6 +911,16 @@ const uint8_t* plan_of(const hla_block_mask* m, int32_t n) {
   if (!m || !m->t_dq || !m->q_dq_local || m->n_dq_nonlocal < 0) return nullptr;
   const int32_t tiles = m->w_row_ptr ? (m->n_qblocks + 1) / 2 : m->n_qblocks;   // block 64: per 128-row tile
   return tiles == (n + kBlock - 1) / kBlock ? m->q_dq_local : nullptr;
+}
+
+// the backward schedule: full-tile (attn_bwd_full_kernel) when full tiles are at least half of the
+// mask's tiles, half-tile (attn_bwd_split_kernel) otherwise and with the global RPB
+#ifndef HLA_BWD_SCHED
+#define HLA_BWD_SCHED 0   // dev A/B: 0 = by tile mix, 1 = full-tile whenever possible, 2 = half-tile always
+#endif
+bool full_schedule(bool rpb, const AttnLists& lists) {
+  return !rpb && (HLA_BWD_SCHED == 1 ||
+                  (HLA_BWD_SCHED == 0 && lists.t_n_full >= lists.t_n_partial && lists.t_n_full > 0));
 }
 
 // workspace carve-up: [fp32 dQ accumulator][fp32 D*scale][fp32 LSE*log2e], 256-aligned regions
@@ -953,10 +978,11 @@ namespace {
 // maps and the schedule.  Built (and every argument checked) before anything is launched.
 struct MainPlan {
   bwd::BwdParams prm;
-  CUtensorMap mq, mk, mv, mdo, mdq;
+  CUtensorMap mq, mk, mv, mdo, mdq, mo;
   int32_t head_dim, mkb;
   bool gather, two_d, full;
-  bool fuse;   // preprocess folded into the main kernel (hla_attn_bwd only)
+  bool fuse;       // preprocess folded into the main kernel (hla_attn_bwd only)
+  bool zero_acc;   // fuse with non-local dQ chains: the accumulator rows still need zeroing
 };
 
 hla_status prepare_main(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
@@ -1033,29 +1059,43 @@ hla_status prepare_main(const hla_pattern_desc* d, const hla_block_mask* m, int3
   // mask's tiles; half-tile (attn_bwd_split_kernel) otherwise (the split
   // schedule overlaps the partial tiles' masked compute better) and with the global RPB (only
   // the half-tile schedule has the dRPB window: at the previous tile's scale, no extra barrier)
-#ifndef HLA_BWD_SCHED
-#define HLA_BWD_SCHED 0   // dev A/B: 0 = by tile mix, 1 = full-tile whenever possible, 2 = half-tile always
-#endif
-  pl->full = prm.rpb == nullptr && (HLA_BWD_SCHED == 1 || (HLA_BWD_SCHED == 0 && lists.t_n_full >= lists.t_n_partial &&
-                                                            lists.t_n_full > 0));
+  pl->full = full_schedule(prm.rpb != nullptr, lists);
   pl->fuse = false;
+  pl->zero_acc = false;
   return HLA_OK;
 }
 
-// hla_attn_bwd: fold the preprocess into the main kernel (either schedule, no global RPB) when
-// every q-block's dQ chain is local (the kernel's dq_stage then holds O tiles instead of dQ
-// partials, and the accumulator is never touched): no preprocess launch, the main kernel reads
-// the raw LSE and O.
+// hla_attn_bwd: fold the preprocess into the main kernel (no global RPB) when every q-block's
+// dQ chain is local (either schedule: the kernel's dq_stage then holds O tiles instead of dQ
+// partials, and the accumulator is never touched), or with the half-tile schedule for any plan
+// (its dQ reduce-adds are then staged in 16-column quarters through the epi_stage; the
+// accumulator rows of non-local q-blocks are zeroed by dq_zero_kernel, a pure write).  The main
+// kernel reads the raw LSE and O; no preprocess launch.
+// Non-local masks are folded only with the block-64 window lists: measured (DESIGN 6g) cfg4 @ b64
+// 1.634 -> 1.549 ms, but cfg4 @ b128 1.913 -> 1.961 and cfg3 0.356 -> 0.361 ms (the folded kernel
+// reloads O with every stage load, and q-blocks are reloaded by several units there).
+bool fusable(bool full, bool rpb, const hla_block_mask* m, int32_t n, int32_t col_mul) {
+  if (rpb) return false;
+  const bool all_local = plan_of(m, n) && m->n_dq_nonlocal == 0;
+  return all_local || (!full && col_mul == 64);
+}
+
 hla_status try_fuse(MainPlan* pl, const hla_block_mask* m, int32_t batch, int32_t heads, const void* o,
                     const float* lse) {
-  if (pl->prm.rpb != nullptr || !plan_of(m, pl->prm.N) || m->n_dq_nonlocal != 0) return HLA_OK;
+  if (!fusable(pl->full, pl->prm.rpb != nullptr, m, pl->prm.N, pl->prm.col_mul)) return HLA_OK;
+  const bool all_local = plan_of(m, pl->prm.N) && m->n_dq_nonlocal == 0;
   const int64_t tok = (int64_t)batch * pl->prm.N;
-  const hla_status st = pl->gather ? make_gather_map(&pl->mdq, o, tok, heads, pl->head_dim)
-                                   : make_rows_map(&pl->mdq, o, tok, heads, pl->head_dim, kBlock);
+  CUtensorMap* om = pl->full ? &pl->mdq : &pl->mo;   // (the full-tile kernel takes O in the dQ slot)
+  hla_status st = pl->gather ? make_gather_map(om, o, tok, heads, pl->head_dim)
+                             : make_rows_map(om, o, tok, heads, pl->head_dim, kBlock);
   if (st != HLA_OK) return st;
+  if (!pl->full && !all_local &&
+      (st = make_f32_rows_map(&pl->mdq, pl->prm.dq_acc, tok, heads, pl->head_dim, 16, kBlock)) != HLA_OK)
+    return st;
   pl->prm.lse2 = lse;
   pl->prm.dsum = nullptr;
   pl->fuse = true;
+  pl->zero_acc = !all_local;
   return HLA_OK;
 }
 
@@ -1064,8 +1104,8 @@ hla_status launch_main(const MainPlan& pl, cudaStream_t stream) {
   if (pl.full)
     return bwd::launch_full(pl.head_dim, pl.gather, pl.two_d, pl.fuse, pl.mq, pl.mk, pl.mv, pl.mdo, pl.mdq, pl.prm,
                             pl.mkb, stream);
-  return bwd::launch_split(bias, pl.head_dim, pl.gather, pl.two_d, pl.fuse, pl.mq, pl.mk, pl.mv, pl.mdo, pl.mdq, pl.prm,
-                           pl.mkb, stream);
+  return bwd::launch_split(bias, pl.head_dim, pl.gather, pl.two_d, pl.fuse, pl.mq, pl.mk, pl.mv, pl.mdo, pl.mdq,
+                           pl.fuse ? pl.mo : pl.mdq, pl.prm, pl.mkb, stream);
 }
 
 }  // namespace
@@ -1122,7 +1162,7 @@ extern "C" int32_t hla_attn_bwd_fuses_preprocess(const hla_pattern_desc* d, cons
     clear_error();
     return 0;
   }
-  return rpb == nullptr && plan_of(m, pat.N) && m->n_dq_nonlocal == 0 ? 1 : 0;
+  return fusable(full_schedule(rpb != nullptr, lists), rpb != nullptr, m, pat.N, lists.col_mul) ? 1 : 0;
 }
 
 extern "C" hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_mask* m, int32_t batch, int32_t heads,
@@ -1142,7 +1182,19 @@ extern "C" hla_status hla_attn_bwd(const hla_pattern_desc* d, const hla_block_ma
   HLA_REQUIRE((int64_t)batch * pl.prm.N * heads * head_dim / 8 < (1ll << 31), HLA_ERR_UNSUPPORTED,
               "B * N * heads * head_dim too large");
   if ((st = try_fuse(&pl, m, batch, heads, o, lse)) != HLA_OK) return st;
-  if (pl.fuse) return launch_main(pl, stream);   // D / LSE formed in the kernel; every dQ row written there
+  if (pl.fuse) {   // D / LSE formed in the kernel
+    if (pl.zero_acc) {   // non-local chains reduce into the accumulator: zero their rows first
+      const int64_t n_v = (int64_t)batch * pl.prm.N * heads * head_dim / 8;
+      dq_zero_kernel<<<(unsigned)((n_v + 255) / 256), 256, 0, stream>>>(
+          reinterpret_cast<float4*>(pl.prm.dq_acc), plan_of(m, pl.prm.N), make_fastdiv(pl.prm.N),
+          make_fastdiv(heads * head_dim / 8), (int32_t)n_v);
+      HLA_CUDA_TRY(cudaGetLastError());
+    }
+    if ((st = launch_main(pl, stream)) != HLA_OK) return st;
+    if (!pl.zero_acc) return HLA_OK;   // every dQ row written by the main kernel
+    return hla_attn_bwd_finalize(batch, heads, pl.prm.N, head_dim, workspace, workspace_bytes, dq, seq_to_cell, m,
+                                 stream);
+  }
   if (pl.prm.drpb)   // the table gradient is accumulated: start from zero
     HLA_CUDA_TRY(cudaMemsetAsync(pl.prm.drpb, 0,
                                  sizeof(float) * heads * (2 * pl.prm.grid_h - 1) * (2 * pl.prm.grid_w - 1), stream));

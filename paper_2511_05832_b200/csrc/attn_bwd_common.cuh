@@ -72,7 +72,7 @@ hla_status launch_full(int head_dim, bool gather, bool two_d, bool fuse, const C
                        int32_t n_kblocks, cudaStream_t stream);
 hla_status launch_split(bool bias, int head_dim, bool gather, bool two_d, bool fuse, const CUtensorMap& mq,
                         const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq,
-                        const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream);
+                        const CUtensorMap& mo, const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream);
 
 template <int D>
 __device__ __forceinline__ uint64_t kmajor_desc(const uint8_t* tile, int kstep) {

@@ -65,18 +65,20 @@ struct SplitSmem {
   uint32_t tmem_base;
   int32_t rpb_win[kBias ? rpb_win_cap<D>() : 1];   // dRPB of the current tile's offset box, fixed point (compute warps)
   // per dQ warp: row-store transpose (store_rows_t); no room next to the dRPB window
-  alignas(128) uint8_t epi_stage[kBias ? 1 : 4][kBias ? 16 : 2048];
+  alignas(1024) uint8_t epi_stage[kBias ? 1 : 4][kBias ? 16 : 2048];   // (also a 64B-swizzled TMA source)
 };
 
 // kFuse: the preprocess folded into the kernel (every dQ chain local, no bias) exactly as in the
 // full-tile schedule (attn_bwd.cu): warp 0 loads the raw LSE and the O tile into the dq_stage
 // bytes, the compute threads form D * scale and LSE * log2(e) (form_d) when they first meet a
-// q-block; tmDQ is the O map.
+// q-block; tmO is the O map.  Non-local dQ chains still reduce into the fp32 accumulator (zeroed
+// by dq_zero_kernel), staged in 16-column quarters through the epi_stage (tmDQ: 16-float boxes).
 template <int D, bool kTwoD, bool kGather, bool kBias, bool kFuse>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                    const __grid_constant__ CUtensorMap tmDQ, const BwdParams prm) {
+                    const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ CUtensorMap tmO,
+                    const BwdParams prm) {
   extern __shared__ uint8_t smem_raw[];
   using Smem = SplitSmem<D, kBias>;
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -200,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               ++n_o;
               if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.o_full, kTile);
               __syncwarp();
-              load_rows<D, kGather>(reinterpret_cast<uint8_t*>(sm.dq_stage), &tmDQ, &sm.o_full, h, b, prm.N,
+              load_rows<D, kGather>(reinterpret_cast<uint8_t*>(sm.dq_stage), &tmO, &sm.o_full, h, b, prm.N,
                                     qblk * prm.col_mul, prm.s2c, pol_q, lane);
             }
           } else if (kVar & 4) {
@@ -643,6 +645,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t w[D / 2];
 #pragma unroll
             for (int e = 0; e < D / 2; ++e) w[e] = sm100::pack_bf16(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
+            if (kFuse) {   // (the stage also carries the reduce-adds: the last one must have read it)
+              if (leader) sm100::bulk_wait_group_read0();
+              sm100::named_bar_sync(2, 128);
+            }
             store_rows_t<D>(w, dqp, sm100::smem_u32(sm.epi_stage[kBias ? 0 : quarter]), lane);
           } else if (qs < prm.N) {
             const int32_t qcell = kGather ? __ldg(prm.s2c + qs) : qs;
@@ -656,21 +662,44 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           continue;
         }
+        if constexpr (kFuse && !kBias) {
+          // the dq_stage holds O tiles: 16-column quarters through the 8 KB epi_stage instead
+          // (64-B rows, 64B swizzle; tmDQ has 16-float boxes in this mode)
 #pragma unroll
-        for (int hh = 0; hh < D / 32; ++hh) {
-          if (leader) sm100::bulk_wait_group_read0();   // previous reduce finished reading the stage
-          sm100::named_bar_sync(2, 128);
+          for (int hh = 0; hh < D / 16; ++hh) {
+            if (leader) sm100::bulk_wait_group_read0();   // previous reduce finished reading the stage
+            sm100::named_bar_sync(2, 128);
+            const uint32_t st = sm100::smem_u32(sm.epi_stage[0]);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const uint32_t off = sm100::swz128((uint32_t)row * 128u + (uint32_t)j * 16u);
-            sm100::sts_u4(sm100::smem_u32(sm.dq_stage) + off, r[hh * 32 + 4 * j], r[hh * 32 + 4 * j + 1],
-                          r[hh * 32 + 4 * j + 2], r[hh * 32 + 4 * j + 3]);
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t off = sm100::swz64((uint32_t)row * 64u + (uint32_t)j * 16u);
+              sm100::sts_u4(st + off, r[hh * 16 + 4 * j], r[hh * 16 + 4 * j + 1], r[hh * 16 + 4 * j + 2],
+                            r[hh * 16 + 4 * j + 3]);
+            }
+            sm100::fence_proxy_async_smem();
+            sm100::named_bar_sync(2, 128);
+            if (leader) {
+              sm100::tma_reduce_add_3d(&tmDQ, sm.epi_stage[0], hh * 16, h, qrow);
+              sm100::bulk_commit_group();
+            }
           }
-          sm100::fence_proxy_async_smem();
-          sm100::named_bar_sync(2, 128);
-          if (leader) {
-            sm100::tma_reduce_add_3d(&tmDQ, sm.dq_stage, hh * 32, h, qrow);
-            sm100::bulk_commit_group();
+        } else {
+#pragma unroll
+          for (int hh = 0; hh < D / 32; ++hh) {
+            if (leader) sm100::bulk_wait_group_read0();   // previous reduce finished reading the stage
+            sm100::named_bar_sync(2, 128);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t off = sm100::swz128((uint32_t)row * 128u + (uint32_t)j * 16u);
+              sm100::sts_u4(sm100::smem_u32(sm.dq_stage) + off, r[hh * 32 + 4 * j], r[hh * 32 + 4 * j + 1],
+                            r[hh * 32 + 4 * j + 2], r[hh * 32 + 4 * j + 3]);
+            }
+            sm100::fence_proxy_async_smem();
+            sm100::named_bar_sync(2, 128);
+            if (leader) {
+              sm100::tma_reduce_add_3d(&tmDQ, sm.dq_stage, hh * 32, h, qrow);
+              sm100::bulk_commit_group();
+            }
           }
         }
       }
@@ -711,6 +740,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         sm100::tc_fence_before();
         sm100::mbar_arrive(&sm.epi_done);      // dV / dK accumulators may now be reset
         if (!kBias) {
+          if (kFuse) {   // (the stage also carries the reduce-adds)
+            if (leader) sm100::bulk_wait_group_read0();
+            sm100::named_bar_sync(2, 128);
+          }
           const uint32_t stg = sm100::smem_u32(sm.epi_stage[kBias ? 0 : quarter]);
           store_rows_t<D>(pv, real ? dvp : nullptr, stg, lane);
           store_rows_t<D>(pk, real ? dkp : nullptr, stg, lane);
@@ -746,13 +779,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int D, bool kTwoD, bool kGather, bool kBias, bool kFuse = false>
 hla_status launch_split_t(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                           const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm, int32_t n_kblocks,
-                          cudaStream_t stream) {
+                          cudaStream_t stream, const CUtensorMap* mo = nullptr) {
   const size_t smem = sizeof(SplitSmem<D, kBias>) + 1024;
   auto* fn = attn_bwd_split_kernel<D, kTwoD, kGather, kBias, kFuse>;
   HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t pairs = (int64_t)((n_kblocks + 1) / 2) * prm.heads * prm.batch;   // work units (kv-block pairs)
   const int grid = (int)std::min<int64_t>(pairs, (int64_t)num_sms());
-  fn<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mdo, mdq, prm);
+  fn<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mdo, mdq, mo ? *mo : mdq, prm);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
 }
@@ -776,23 +809,24 @@ hla_status dispatch_split(int head_dim, bool gather, bool two_d, const CUtensorM
 // preprocess folded in (no bias): every dQ chain local, mdq = the O map, lse2 = raw LSE
 hla_status dispatch_split_fused(int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
                                 const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq,
-                                const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream) {
+                                const CUtensorMap& mo, const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream) {
   if (head_dim == 64) {
-    if (gather) return launch_split_t<64, false, true, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
-    return two_d ? launch_split_t<64, true, false, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream)
-                 : launch_split_t<64, false, false, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
+    if (gather) return launch_split_t<64, false, true, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream, &mo);
+    return two_d ? launch_split_t<64, true, false, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream, &mo)
+                 : launch_split_t<64, false, false, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream, &mo);
   }
-  if (gather) return launch_split_t<32, false, true, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
-  return two_d ? launch_split_t<32, true, false, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream)
-               : launch_split_t<32, false, false, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
+  if (gather) return launch_split_t<32, false, true, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream, &mo);
+  return two_d ? launch_split_t<32, true, false, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream, &mo)
+               : launch_split_t<32, false, false, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream, &mo);
 }
 
 }  // namespace
 
 hla_status launch_split(bool bias, int head_dim, bool gather, bool two_d, bool fuse, const CUtensorMap& mq,
                         const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq,
-                        const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream) {
-  if (fuse && !bias) return dispatch_split_fused(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
+                        const CUtensorMap& mo, const BwdParams& prm, int32_t n_kblocks, cudaStream_t stream) {
+  if (fuse && !bias)
+    return dispatch_split_fused(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, mo, prm, n_kblocks, stream);
   return bias ? dispatch_split<true>(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, n_kblocks, stream)
               : dispatch_split<false>(head_dim, gather, two_d, mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
 }

@@ -71,6 +71,7 @@ inline hla_status make_gather_map(CUtensorMap* map, const void* base, int64_t ro
 
 // fp32 tensor [rows_total, heads, head_dim] as 3-D (head_dim, heads, rows); box =
 // (box_cols, 1, box_rows), SWIZZLE_128B (box_cols * 4 == 128).
+// box_cols 32 (128-B rows, 128B swizzle) or 16 (64-B rows, 64B swizzle)
 inline hla_status make_f32_rows_map(CUtensorMap* map, const void* base, int64_t rows_total, int heads, int head_dim,
                                     int box_cols, int box_rows) {
   EncodeTiledFn enc;
@@ -81,8 +82,8 @@ inline hla_status make_f32_rows_map(CUtensorMap* map, const void* base, int64_t 
   cuuint32_t box[3] = {(cuuint32_t)box_cols, 1, (cuuint32_t)box_rows};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, box_cols == 16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   HLA_REQUIRE(r == CUDA_SUCCESS, HLA_ERR_CUDA, "cuTensorMapEncodeTiled (f32) failed (%d)", (int)r);
   return HLA_OK;
 }
