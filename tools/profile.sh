@@ -13,7 +13,7 @@ M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 M=$M,sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32.sum,sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32.avg.pct_of_peak_sustained_elapsed
 M=$M,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__inst_executed_pipe_tensor.sum
 ncu --metrics $M --clock-control none \
-    -k "regex:attn_|hilbert_|bwd_pre|dq_fin" -c 400 --csv --log-file gpurun_out/launches_${CFG}_${TAG}.csv $B > /dev/null 2>&1
+    -k "regex:attn_|hilbert_|bwd_pre|dq_fin|dq_zero" -c 400 --csv --log-file gpurun_out/launches_${CFG}_${TAG}.csv $B > /dev/null 2>&1
 for k in ${KERNELS:-attn_bwd_full_kernel attn_bwd_split_kernel attn_fwd_kernel}; do
   ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 -o gpurun_out/prof_${CFG}_${k}_${TAG} -f $B > /dev/null 2>&1
 done
