@@ -561,6 +561,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           sm100::tc_fence_before();
           sm100::mbar_arrive(&sm.ds_ready[half]);
         }
+        HLA_PMARK(tf0);
         if (kBias && win) {
           // flush the tile's dRPB window to global (and re-zero it) -- all 256 compute threads;
           // the tile's largest |dL/dscore| sets the fixed-point scale of the NEXT tile (no
@@ -587,11 +588,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           rpb_fx = rpb_next_scale(sm.rpb_wmax[g & 1], rpb_fx);   // (stays 0 only for an all-zero tile)
           sm100::named_bar_sync(3, 256);
         }
+        HLA_PADD(8, tf0);
         HLA_PADD(7, tc0);
       }
       tiles_done += nt;
     }
-    HLA_PFLUSH(5, 8, warp == 2 && lane == 0);
+    HLA_PFLUSH(5, 9, warp == 2 && lane == 0);
   } else if (warp < 14) {
     HLA_PDECL;
     // ------------------------------------------ dQ partial -> fp32 accumulator

@@ -14,17 +14,22 @@ import paper_2511_05832_b200 as hla
 from paper_2511_05832_b200 import _lib
 
 CASES = {"cfg2": ("HWA", 64, 16, 16, 8), "cfg3": ("HSA", 64, 16, 16, 8), "cfg4": ("HNA", 128, 7, 16, 12),
-         "dense2": ("DENSE", 64, 1, 16, 8), "cfg5s1": ("HWA", 64, 8, 128, 3, 32), "cfg5s2": ("HWA", 32, 8, 128, 6, 32)}
+         "dense2": ("DENSE", 64, 1, 16, 8), "cfg5s1": ("HWA", 64, 8, 128, 3, 32), "cfg5s2": ("HWA", 32, 8, 128, 6, 32),
+         "cfg4b64": ("HNA", 128, 7, 16, 12, 64, 64), "hwt1": ("HWA", 56, 7, 128, 3, 32, 128, True),
+         "hwt1s": ("HSWA", 56, 7, 128, 3, 32, 128, True)}
 SLOTS = ["mma:ds_ready", "mma:epi_done", "mma:next_operands", "mma:dq_free", "mma:loop_total",
-         "cmp:q_full", "cmp:s_full", "cmp:work", "cmp:-", "dq:dq_full", "dq:drain", "dq:dkv_full", "dq:epilogue",
+         "cmp:q_full", "cmp:s_full", "cmp:work", "cmp:rpb_flush", "dq:dq_full", "dq:drain", "dq:dkv_full", "dq:epilogue",
          "tma:kv_empty", "tma:q_empty", "-", "cmp:until_loads_done", "cmp:until_dS_done", "cmp:until_P_done",
          "cmp:until_p_ready"]
 L = _lib.lib()
 for name in (sys.argv[1:] or ["cfg2", "cfg3", "cfg4"]):
     kind, g, w, B, H = CASES[name][:5]
     d = CASES[name][5] if len(CASES[name]) > 5 else 64
+    blk = CASES[name][6] if len(CASES[name]) > 6 else 128
+    rpb = CASES[name][7] if len(CASES[name]) > 7 else False
     q, k, v, do = hla_synth.attention_inputs(B, g * g, H, d, device="cuda")
-    lay = hla.HilbertLocalAttention(kind, g, g, w, w, B, H, d, device="cuda")
+    lay = hla.HilbertLocalAttention(kind, g, g, w, w, B, H, d, block=blk, device="cuda", rpb=rpb,
+                                    shift=(w * w) // 2 if kind == "HSWA" else 0)
     for _ in range(3):
         lay.forward(q, k, v)
         lay.backward(do)
