@@ -46,6 +46,14 @@ constexpr int kHalf = 64;       // q-columns per pipeline half
 #endif
 constexpr int kVar = HLA_BWD_VAR;   // dev-only decomposition switches, see attn_bwd.cu
 
+// Global RPB at d = 32 (the HWT stack): the compute warps hand each tile's dRPB window to the dQ
+// warpgroup (win_full) instead of flushing it behind two 256-thread barriers; the window of tile g
+// is reused by tile g + 2 after win_free, which also publishes the fixed-point scale of tile g + 2
+// (from the maxima of tile g).  d = 64 keeps the synchronous flush (no shared memory for a second
+// window).
+template <int D, bool kBias>
+constexpr bool async_flush() { return kBias && D == 32; }
+
 template <int D, bool kBias>
 struct SplitSmem {
   static constexpr uint32_t kTileBytes = kBlock * D * 2;
@@ -63,7 +71,12 @@ struct SplitSmem {
       epi_done;
   uint64_t o_full, o_empty;   // kFuse (preprocess folded in), as in attn_bwd.cu
   uint32_t tmem_base;
-  int32_t rpb_win[kBias ? rpb_win_cap<D>() : 1];   // dRPB of the current tile's offset box, fixed point (compute warps)
+  // dRPB of a tile's offset box, fixed point: one window flushed by the compute warps after each
+  // tile (d = 64), or two (tile parity) flushed asynchronously by the dQ warpgroup (d = 32, kAsyncFlush)
+  int32_t rpb_win[async_flush<D, kBias>() ? 2 : 1][kBias ? rpb_win_cap<D>() : 1];
+  struct RpbGeo { int32_t dr0, dc0, wrows, wcols, win, head; float fx; } rpb_geo[2];   // (async flush)
+  float rpb_scale[2];                                                                // (async flush)
+  uint64_t win_full[2], win_free[2];                                                 // (async flush)
   // per dQ warp: row-store transpose (store_rows_t); no room next to the dRPB window
   alignas(1024) uint8_t epi_stage[kBias ? 1 : 4][kBias ? 16 : 2048];   // (also a 64B-swizzled TMA source)
 };
@@ -81,6 +94,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const BwdParams prm) {
   extern __shared__ uint8_t smem_raw[];
   using Smem = SplitSmem<D, kBias>;
+  constexpr bool kAsyncFlush = async_flush<D, kBias>();
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   UnitGeom ug;
@@ -110,6 +124,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     sm100::mbar_init(&sm.epi_done, 128);
     sm100::mbar_init(&sm.o_full, 1);
     sm100::mbar_init(&sm.o_empty, 1);
+    for (int s = 0; s < 2; ++s) {
+      sm100::mbar_init(&sm.win_full[s], 256);
+      sm100::mbar_init(&sm.win_free[s], 128);
+    }
         sm100::fence_mbar_init();
     sm100::tma_prefetch_desc(&tmQ);
     sm100::tma_prefetch_desc(&tmK);
@@ -347,7 +365,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = prm.scale_log2, scale = prm.scale;
     if (kBias) {   // the dRPB window starts (and is left after every flush) zeroed
-      for (int i = (warp - 2) * 32 + lane; i < rpb_win_cap<D>(); i += 256) sm.rpb_win[i] = 0;
+      for (int i = (warp - 2) * 32 + lane; i < (kAsyncFlush ? 2 : 1) * rpb_win_cap<D>(); i += 256)
+        (&sm.rpb_win[0][0])[i] = 0;
       sm100::named_bar_sync(3, 256);
     }
     float rpb_fx = 0.f;   // fixed-point scale of the dRPB window, from the previous tile's maximum (0: none yet)
@@ -398,6 +417,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         HLA_PW(5, sm100::mbar_wait(&sm.q_full[s], (g >> 1) & 1));
         HLA_PMARK(tc0);
+        if (kAsyncFlush) {   // window g & 1 flushed (tile g - 2) and this tile's scale published
+          if (g >= 2) {
+            sm100::mbar_wait(&sm.win_free[g & 1], ((g >> 1) - 1) & 1);
+            rpb_fx = sm.rpb_scale[g & 1];
+          } else {
+            rpb_fx = 0.f;   // (no scale yet: a CTA's first two tiles take the global path)
+          }
+        }
         if (kFuse) {   // a newly loaded q-block (the producer's stage tags, mirrored): form D and the
                        // log2-domain LSE in its stage from the O tile (form_d), then free the O tile
           const int64_t tag = ((int64_t)b * prm.heads + h) * prm.N + q0;
@@ -531,7 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int32_t av[8] = {__float_as_int(xa.x), __float_as_int(xa.y), __float_as_int(xa.z),
                                        __float_as_int(xa.w), __float_as_int(xb.x), __float_as_int(xb.y),
                                        __float_as_int(xb.z), __float_as_int(xb.w)};
-                const uint32_t wbase = sm100::smem_u32(sm.rpb_win);
+                const uint32_t wbase = sm100::smem_u32(sm.rpb_win[kAsyncFlush ? (g & 1) : 0]);
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                   if (!((okbits >> (u4 * 8 + e)) & 1u)) continue;
@@ -562,7 +589,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           sm100::mbar_arrive(&sm.ds_ready[half]);
         }
         HLA_PMARK(tf0);
-        if (kBias && win) {
+        if (kAsyncFlush) {
+          // hand the window to the dQ warpgroup: this warp's maximum, the tile's geometry, arrive
+          const uint32_t wm = __reduce_max_sync(0xffffffffu, __float_as_uint(tmax));   // non-negative floats
+          if (lane == 0) sm.rpb_wmax[g & 1][warp - 2] = __uint_as_float(wm);
+          if (cth == 0) sm.rpb_geo[g & 1] = {dr0, dc0, wrows, wcols, win ? 1 : 0, h, rpb_fx};
+          sm100::mbar_arrive(&sm.win_full[g & 1]);
+        } else if (kBias && win) {
           // flush the tile's dRPB window to global (and re-zero it) -- all 256 compute threads;
           // the tile's largest |dL/dscore| sets the fixed-point scale of the NEXT tile (no
           // extra barrier; elements beyond that scale's range go to global fp32 atomics)
@@ -578,11 +611,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           int32_t ir = wcols > 0 ? tid / wcs : wrows, ic = tid - (tid / wcs) * wcs;
           for (; ir < wrows; ir += step_r, ic += step_c) {
             if (ic >= wcols) { ic -= wcols; ++ir; if (ir >= wrows) break; }
-            const int32_t v = sm.rpb_win[ir * wc + ic];
+            const int32_t v = sm.rpb_win[0][ir * wc + ic];
             if (v != 0) {
               atomicAdd(drpbh + (dr0 + ir + prm.grid_h - 1) * prm.rpb_w + (dc0 + ic + prm.grid_w - 1),
                         (float)v * inv_fx);
-              sm.rpb_win[ir * wc + ic] = 0;
+              sm.rpb_win[0][ir * wc + ic] = 0;
             }
           }
           rpb_fx = rpb_next_scale(sm.rpb_wmax[g & 1], rpb_fx);   // (stays 0 only for an all-zero tile)
@@ -615,6 +648,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int32_t b = prm.heads_div.div(bh_u), h = bh_u - b * prm.heads;
       const int32_t rs = __ldg(prm.t_row_ptr + kb), nt = __ldg(prm.t_row_ptr + kb + 1) - rs;
       for (int t = 0; t < nt; ++t, ++g) {
+        if (kAsyncFlush) {
+          // tile g's dRPB window: flush its box to the table (and re-zero it), publish the scale
+          // of tile g + 2 from the tile's per-warp maxima, free the window
+          sm100::mbar_wait(&sm.win_full[g & 1], (g >> 1) & 1);
+          const auto geo = sm.rpb_geo[g & 1];
+          if (geo.win && geo.fx > 0.f) {
+            const float inv_fx = 1.f / geo.fx;
+            float* drp = prm.drpb + (int64_t)geo.head * prm.rpb_hw;
+            int32_t* w = sm.rpb_win[g & 1];
+            const int tid = row;   // 0 .. 127
+            const int32_t wcs = geo.wcols > 0 ? geo.wcols : 1;
+            const int32_t step_r = 128 / wcs, step_c = 128 - step_r * wcs;
+            int32_t ir = geo.wcols > 0 ? tid / wcs : geo.wrows, ic = tid - (tid / wcs) * wcs;
+            for (; ir < geo.wrows; ir += step_r, ic += step_c) {
+              if (ic >= geo.wcols) { ic -= geo.wcols; ++ir; if (ir >= geo.wrows) break; }
+              const int32_t v = w[ir * prm.rpb_w + ic];
+              if (v != 0) {
+                atomicAdd(drp + (geo.dr0 + ir + prm.grid_h - 1) * prm.rpb_w + (geo.dc0 + ic + prm.grid_w - 1),
+                          (float)v * inv_fx);
+                w[ir * prm.rpb_w + ic] = 0;
+              }
+            }
+          }
+          if (row == 0) sm.rpb_scale[g & 1] = rpb_next_scale(sm.rpb_wmax[g & 1], geo.fx);
+          sm100::mbar_arrive(&sm.win_free[g & 1]);
+        }
         const uint32_t fdq = dq_plan(prm.t_dq, rs + t, g);
         if (!(fdq & HLA_DQ_DRAIN)) continue;   // the chain continues in TMEM
         const int dqb = (int)(fdq & HLA_DQ_BUF);
