@@ -6,8 +6,11 @@
 //   P = exp(scale S - LSE) (0 where masked),  D = rowsum(dO o O)
 //   dV = P^T dO,  dS = scale P o (dO V^T - D),  dK = dS^T Q,  dQ = dS K.
 //
-// K7 bwd_preprocess : D = rowsum(dO o O) (fp32) and zero the fp32 dQ accumulator.
-// K8 attn_bwd_kernel: persistent, 1 CTA / SM, kv-major over the transposed CSR
+// K7 bwd_preprocess : D = rowsum(dO o O) (fp32) and zero the fp32 dQ accumulator -- or folded
+//    into K8 by hla_attn_bwd (kFuse: the compute warps form D and the log2 LSE from an O tile,
+//    form_d; non-local accumulator rows are then zeroed by the write-only dq_zero_kernel).
+// K8 attn_bwd_full_kernel (this file; attn_bwd_split.cu holds the half-tile schedule):
+//    persistent, 1 CTA / SM, kv-major over the transposed CSR
 //    (work unit = a pair of consecutive kv-blocks of one (b, h); per kv-block the
 //    listed q-blocks i, ascending).  kThreads = 4 + kCmpWarps + 4 warps, registers
 //    redistributed with setmaxnreg (kRegsCtl / kRegsCmp / kRegsDq):
@@ -30,7 +33,7 @@
 //    last warpgroup thread = query row: dQ_i drain at the end of a dQ
 //                 chain (complete chains -> bf16 dq rows; others -> smem -> TMA
 //                 reduce-add into the fp32 accumulator) and the dK / dV rows of
-//                 each unit.
+//                 each unit (row stores through a per-warp smem transpose, store_rows_t).
 // K9 dq_finalize    : fp32 accumulator -> bf16 dQ.
 #ifdef HLA_BWD_PROF
 #define HLA_PROF_ON
