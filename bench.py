@@ -585,23 +585,26 @@ def run_single(args):
     # --- end to end through the public API: host -> device -> step -> host ---
     # Every step copies its inputs (Q, K, V, dO) from pinned host memory and reads its
     # results (O, dQ, dK, dV) back to pinned host memory inside the timed region.  The
-    # copies run on two copy streams and the step on the compute stream, two steps in
-    # flight (two layer instances = two sets of device buffers): step i+1's host->device
-    # copies overlap step i's compute and device->host copies (full-duplex link).
+    # copies run on two copy streams and the step on the compute stream, three steps in
+    # flight (three layer instances = three sets of device buffers): step i+1's host->device
+    # copies overlap step i's compute and step i-1's device->host copies (full-duplex link;
+    # with two slots the next upload waited for the previous download, tools/probe_pcie.py).
     e2e = None
     if not args.no_e2e:
+        R = 3
         hin = [x.cpu().pin_memory() for x in (q, k, v, do)]
-        layers = [layer, hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, Bs, Hs, d, block=blk, device=dev)]
-        din = [[torch.empty_like(x) for x in (q, k, v, do)] for _ in range(2)]
-        hout = [[torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (q, q, q, q)] for _ in range(2)]
+        layers = [layer] + [hla.HilbertLocalAttention(cfg["kind"], g, g, win, win, Bs, Hs, d, block=blk, device=dev)
+                            for _ in range(R - 1)]
+        din = [[torch.empty_like(x) for x in (q, k, v, do)] for _ in range(R)]
+        hout = [[torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (q, q, q, q)] for _ in range(R)]
         s_in, s_out, s_cmp = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.current_stream(dev)
-        ev_free = [None, None]
+        ev_free = [None] * R
 
         def e2e_step(i):
-            j = i % 2
+            j = i % R
             with torch.cuda.stream(s_in):
                 if ev_free[j] is not None:
-                    s_in.wait_event(ev_free[j])       # slot j's buffers: step i-2 fully read back
+                    s_in.wait_event(ev_free[j])       # slot j's buffers: step i-R fully read back
                 for dst, src in zip(din[j], hin):
                     dst.copy_(src, non_blocking=True)
                 ev_in = torch.cuda.Event()
@@ -622,15 +625,15 @@ def run_single(args):
                 ev_free[j] = torch.cuda.Event()
                 ev_free[j].record(s_out)
 
-        esteps = max(4, min(args.steps, 10))
-        for i in range(2):                          # warm-up (untimed)
+        esteps = max(4, args.steps)   # the pipeline fill (first upload, last download) amortised like the device loop
+        for i in range(R):                          # warm-up (untimed)
             e2e_step(i)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s_in)
-        for i in range(2, 2 + esteps):
+        for i in range(R, R + esteps):
             e2e_step(i)
         s_out.wait_stream(s_cmp)
         e1.record(s_out)
@@ -640,7 +643,7 @@ def run_single(args):
         e2e = {"value": round(te, 4), "unit": "ms", "h2d_bytes_per_step": nbytes * world,
                "d2h_bytes_per_step": nbytes * world, "steps": esteps,
                "path": "pinned host -> (copy stream) -> HilbertLocalAttention.forward/backward (compute stream) -> "
-                       "(copy stream) -> pinned host; two steps in flight (double-buffered device tensors); "
+                       "(copy stream) -> pinned host; three steps in flight (triple-buffered device tensors); "
                        "per-rank shards, max over ranks; bytes = all ranks"}
 
     # --- roofline of the dominant kernel (share of the step) ---
