@@ -88,6 +88,20 @@ def hilbert_order(grid_h, grid_w):
     return seq_to_cell, cell_to_seq
 
 
+def hilbert_tiled_order(grid_h, grid_w, seg=64):
+    """(seq_to_cell, cell_to_seq) of the implementation's tiled Hilbert order (include/hla.h
+    HLA_ORDER_HILBERT_TILED; reading R23 -- NOT a curve of the paper): the Hilbert
+    order with the cells of every aligned `seg`-token segment listed in row-major order
+    (ascending cell id = (row, col) order).  Written from that definition: sort each segment."""
+    s2c, _ = hilbert_order(grid_h, grid_w)
+    n = grid_h * grid_w
+    assert n % seg == 0
+    seq_to_cell = np.sort(s2c.reshape(-1, seg), axis=1).reshape(-1)
+    cell_to_seq = np.empty(n, dtype=np.int64)
+    cell_to_seq[seq_to_cell] = np.arange(n, dtype=np.int64)
+    return seq_to_cell, cell_to_seq
+
+
 def row_major_order(grid_h, grid_w):
     """(seq_to_cell, cell_to_seq) of the conventional row-major order."""
     n = grid_h * grid_w

@@ -100,3 +100,35 @@ def test_to_sequence_roundtrip():
     y = hilbert.to_sequence(x, s2c)
     assert np.array_equal(y[:, 5], x[:, s2c[5]])
     assert np.array_equal(hilbert.to_grid(y, s2c), x)
+
+
+# ---------------------------------------------------------------- tiled order (R23)
+@pytest.mark.parametrize("k", [3, 4, 5, 6, 7])
+def test_tiled_order_segments_are_squares(k):
+    """The tiled order relabels inside aligned 64-token segments; it is well formed because
+    every such segment of the curve is an aligned 8 x 8 square (the quadrant property at
+    j = 3), so each aligned 8 positions of the tiled order are 8 consecutive cells of one row."""
+    n = 2 ** k
+    s2c, c2s = hilbert.hilbert_tiled_order(n, n)
+    h2c, _ = hilbert.hilbert_order(n, n)
+    assert sorted(s2c.tolist()) == list(range(n * n))
+    assert np.array_equal(c2s[s2c], np.arange(n * n))
+    for s0 in range(0, n * n, 64):
+        rows, cols = s2c[s0:s0 + 64] // n, s2c[s0:s0 + 64] % n
+        # the same cells as the Hilbert segment (a relabeling inside the segment only)
+        assert set(s2c[s0:s0 + 64].tolist()) == set(h2c[s0:s0 + 64].tolist())
+        assert rows.min() % 8 == 0 and cols.min() % 8 == 0
+        assert np.array_equal(rows, rows.min() + np.repeat(np.arange(8), 8))
+        assert np.array_equal(cols, cols.min() + np.tile(np.arange(8), 8))
+
+
+@pytest.mark.parametrize("k,win", [(3, 8), (5, 8), (6, 16), (7, 8), (7, 32)])
+def test_tiled_order_keeps_hwa_windows(k, win):
+    """HWA with n = win^2 tokens (a multiple of 64): window(s) = s // n holds the same set of
+    cells under both orders, so the attention of every cell is unchanged (reading R23)."""
+    n = 2 ** k
+    t2c, _ = hilbert.hilbert_tiled_order(n, n)
+    h2c, _ = hilbert.hilbert_order(n, n)
+    nt = win * win
+    for w0 in range(0, n * n, nt):
+        assert set(t2c[w0:w0 + nt].tolist()) == set(h2c[w0:w0 + nt].tolist())
