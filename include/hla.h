@@ -57,7 +57,16 @@ typedef enum {
 
 typedef enum {
   HLA_ORDER_ROW_MAJOR = 0,  /* token t = row*W + col */
-  HLA_ORDER_HILBERT = 1     /* token s = position on the Hilbert curve */
+  HLA_ORDER_HILBERT = 1,    /* token s = position on the Hilbert curve */
+  HLA_ORDER_HILBERT_TILED = 2
+  /* The Hilbert order with every aligned 64-token segment (an aligned 8 x 8 cell square of
+   * a square 2^k grid, k >= 3) relabeled in raster order (hla_hilbert_tiled_index).  Not a
+   * curve of the paper: an implementation order that is the SAME attention for the patterns
+   * whose predicates only see whole 64-token segments -- HWA with n a multiple of 64 tokens
+   * (the window of position s is s/n, unchanged by a relabeling inside a segment) and DENSE
+   * (reading R23).  Any other pattern or grid: HLA_ERR_UNSUPPORTED.  With head_dim
+   * 32 and the fused reorder the kernels load every 8 positions (8 consecutive cells of a
+   * grid row) as one TMA box instead of two .tile::gather4 ops. */
 } hla_order;
 
 /* Pattern families.  With order = HILBERT they are the paper's HWA / HSA / HNA /
@@ -169,6 +178,16 @@ enum {
 HLA_API hla_status hla_hilbert_index(int32_t grid_h, int32_t grid_w,
                              int32_t* seq_to_cell, int32_t* cell_to_seq,
                              cudaStream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * hla_hilbert_tiled_index -- seq_to_cell / cell_to_seq of HLA_ORDER_HILBERT_TILED:
+ * position s of the Hilbert curve (hla_hilbert_index) with cell (row, col) moves to
+ * (s & ~63) + 8 * (row & 7) + (col & 7).  Square 2^k grids with k >= 3 only (else
+ * HLA_ERR_UNSUPPORTED); device kernel, asynchronous on `stream`; either output may be NULL.
+ */
+HLA_API hla_status hla_hilbert_tiled_index(int32_t grid_h, int32_t grid_w,
+                                   int32_t* seq_to_cell, int32_t* cell_to_seq,
+                                   cudaStream_t stream);
 
 /* ---------------------------------------------------------------------------
  * hla_hilbert_perm -- reorder token rows between grid order and Hilbert order
@@ -288,7 +307,8 @@ typedef struct {
  * order; the kernel gathers each 128-token Hilbert tile with TMA .tile::gather4
  * row loads and writes O rows back to their grid cells, so the separate
  * "Reshape" passes of P:L196 disappear.  LSE stays in
- * sequence order.
+ * sequence order.  For d->order == HLA_ORDER_HILBERT_TILED the table must come from
+ * hla_hilbert_tiled_index (its aligned 8 positions are assumed to be 8 consecutive cells).
  */
 HLA_API hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_mask* m,
                         int32_t batch, int32_t heads, int32_t head_dim, float scale,

@@ -14,6 +14,7 @@ Layers:
 
 from ._lib import HlaError  # noqa: F401
 from .api import (KINDS, BlockMask, hla_attn_bwd, hla_attn_bwd_workspace, hla_attn_fwd,  # noqa: F401
-                  hla_build_block_mask, hla_debug_umma, hla_hilbert_index, hla_hilbert_perm, pattern_desc,
+                  hla_build_block_mask, hla_debug_umma, hla_hilbert_index, hla_hilbert_perm,
+                  hla_hilbert_tiled_index, pattern_desc,
                   version)
 from .attention import HilbertLocalAttention  # noqa: F401

@@ -18,7 +18,7 @@ STATUS_NAMES = {0: "HLA_OK", 1: "HLA_ERR_INVALID", 2: "HLA_ERR_UNSUPPORTED", 3: 
                 4: "HLA_ERR_CUDA"}
 
 # exported symbols of include/hla.h (libhla.so) and include/hla_debug.h (libhla_debug.so)
-EXPORTED = ("hla_hilbert_index", "hla_hilbert_perm", "hla_build_block_mask", "hla_mask_ratios",
+EXPORTED = ("hla_hilbert_index", "hla_hilbert_tiled_index", "hla_hilbert_perm", "hla_build_block_mask", "hla_mask_ratios",
             "hla_attn_fwd", "hla_attn_bwd", "hla_attn_bwd_workspace", "hla_attn_bwd_preprocess",
             "hla_attn_bwd_main", "hla_attn_bwd_finalize", "hla_build_bwd_plan", "hla_build_tile_lists",
             "hla_attn_bwd_fuses_preprocess", "hla_last_error", "hla_version")
@@ -64,6 +64,7 @@ _vp, _i32, _i64, _f32, _sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ct
 _pdesc, _pmask = ctypes.POINTER(PatternDesc), ctypes.POINTER(BlockMaskC)
 _SIG = {
     "hla_hilbert_index": [_i32, _i32, _vp, _vp, _vp],
+    "hla_hilbert_tiled_index": [_i32, _i32, _vp, _vp, _vp],
     "hla_hilbert_perm": [_i32, _i32, _i32, _i32, _i32, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp],
     "hla_build_block_mask": [_pdesc, _pmask, ctypes.POINTER(_i64), _vp],
     "hla_mask_ratios": [_pdesc, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],

@@ -13,7 +13,7 @@ import torch
 from . import _lib
 from ._lib import BlockMaskC, PatternDesc, check, lib
 
-ORDER_ROW_MAJOR, ORDER_HILBERT = 0, 1
+ORDER_ROW_MAJOR, ORDER_HILBERT, ORDER_HILBERT_TILED = 0, 1, 2
 WINDOW, SLIDE, NEIGHBORHOOD, DENSE, SHIFTED_WINDOW = 0, 1, 2, 3, 4
 TO_HILBERT, FROM_HILBERT = 0, 1
 
@@ -36,13 +36,25 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else None
 
 
-def pattern_desc(kind, grid_h, grid_w, win_h=1, win_w=1, block=128, shift=0):
+def pattern_desc(kind, grid_h, grid_w, win_h=1, win_w=1, block=128, shift=0, tiled=False):
+    """tiled=True: HLA_ORDER_HILBERT_TILED (HWA with a multiple of 64 tokens per window on a square
+    2^k grid: the same attention, 64-token segments relabeled in raster order; include/hla.h)."""
     order, pattern = KINDS[kind]
+    if tiled:
+        if order != ORDER_HILBERT:
+            raise ValueError("tiled order is a Hilbert order: %s is not a Hilbert pattern" % kind)
+        order = ORDER_HILBERT_TILED
     return PatternDesc(grid_h, grid_w, order, pattern, win_h, win_w, shift, block, block)
 
 
 def is_hilbert(desc):
-    return desc.order == ORDER_HILBERT
+    return desc.order != ORDER_ROW_MAJOR
+
+
+def tiled_order_applies(kind, grid_h, grid_w, win_h, win_w):
+    """The shapes HLA_ORDER_HILBERT_TILED accepts (api_common.cu make_pattern_fields)."""
+    return (kind == "HWA" and (win_h * win_w) % 64 == 0 and grid_h == grid_w and grid_h >= 8
+            and grid_h & (grid_h - 1) == 0)
 
 
 @dataclass
@@ -110,6 +122,17 @@ def hla_hilbert_index(grid_h, grid_w, device="cuda", stream=None):
     with torch.cuda.device(s2c.device):
         check("hla_hilbert_index", lib().hla_hilbert_index(grid_h, grid_w, _ptr(s2c), _ptr(c2s),
                                                            _stream(stream, s2c.device)))
+    return s2c, c2s
+
+
+def hla_hilbert_tiled_index(grid_h, grid_w, device="cuda", stream=None):
+    """seq_to_cell / cell_to_seq of HLA_ORDER_HILBERT_TILED (include/hla.h)."""
+    n = grid_h * grid_w
+    s2c = torch.empty(n, dtype=torch.int32, device=device)
+    c2s = torch.empty(n, dtype=torch.int32, device=device)
+    with torch.cuda.device(s2c.device):
+        check("hla_hilbert_tiled_index", lib().hla_hilbert_tiled_index(grid_h, grid_w, _ptr(s2c), _ptr(c2s),
+                                                                       _stream(stream, s2c.device)))
     return s2c, c2s
 
 

@@ -39,13 +39,21 @@ from . import api
 
 class HilbertLocalAttention:
     def __init__(self, kind, grid_h, grid_w, win_h=1, win_w=1, batch=1, heads=1, head_dim=64, block=128,
-                 shift=0, scale=0.0, device="cuda", fused=True, rpb=False, dq_plan=True):
+                 shift=0, scale=0.0, device="cuda", fused=True, rpb=False, dq_plan=True, tiled=None):
         self.kind = kind
         self.grid_h, self.grid_w = grid_h, grid_w
         self.N = grid_h * grid_w
         self.shape = (batch, self.N, heads, head_dim)
         self.scale = float(scale)
-        self.desc = api.pattern_desc(kind, grid_h, grid_w, win_h, win_w, block, shift)
+        # tiled Hilbert order (include/hla.h HLA_ORDER_HILBERT_TILED; R23): the same
+        # attention for HWA with 64-token-multiple windows on square 2^k grids; at head_dim 32 the
+        # fused loads then move 8-row boxes instead of gather4 ops.  None = where it applies and pays.
+        ok = api.tiled_order_applies(kind, grid_h, grid_w, win_h, win_w) and fused and not rpb
+        self.tiled = ok and head_dim == 32 if tiled is None else bool(tiled)
+        if self.tiled and not ok:
+            raise ValueError("tiled order needs fused HWA, a multiple of 64 tokens per window, a square 2^k "
+                             "grid >= 8 and no RPB")
+        self.desc = api.pattern_desc(kind, grid_h, grid_w, win_h, win_w, block, shift, tiled=self.tiled)
         self.mask = api.hla_build_block_mask(self.desc, device, plan=dq_plan)   # + the backward's dQ plan
         self.hilbert = api.is_hilbert(self.desc)
         bf = dict(dtype=torch.bfloat16, device=device)
@@ -57,7 +65,8 @@ class HilbertLocalAttention:
         self.fused = bool(fused) and self.hilbert
         self.s2c = None
         if self.fused:
-            self.s2c, _ = api.hla_hilbert_index(grid_h, grid_w, device)     # the cached path
+            index = api.hla_hilbert_tiled_index if self.tiled else api.hla_hilbert_index
+            self.s2c, _ = index(grid_h, grid_w, device)     # the cached path; the sequence order of lse
         elif self.hilbert:
             self.qs, self.ks, self.vs, self.os = e(), e(), e(), e()
             self.dos, self.dqs, self.dks, self.dvs = e(), e(), e(), e()

@@ -26,14 +26,22 @@ hla_status make_pattern_fields(const hla_pattern_desc* d, Pattern* p) {
   int64_t N = (int64_t)d->grid_h * d->grid_w;
   HLA_REQUIRE(N <= (1 << 24), HLA_ERR_UNSUPPORTED, "N=%lld too large", (long long)N);
   HLA_REQUIRE(d->block_q >= 1 && d->block_k >= 1, HLA_ERR_INVALID, "block must be >= 1");
-  HLA_REQUIRE(d->order == HLA_ORDER_ROW_MAJOR || d->order == HLA_ORDER_HILBERT, HLA_ERR_INVALID,
-              "order %d invalid", d->order);
+  HLA_REQUIRE(d->order == HLA_ORDER_ROW_MAJOR || d->order == HLA_ORDER_HILBERT || d->order == HLA_ORDER_HILBERT_TILED,
+              HLA_ERR_INVALID, "order %d invalid", d->order);
+  // the tiled order relabels positions inside aligned 64-token segments only: the patterns whose
+  // predicates see a 64-segment as a unit (windows of a multiple of 64 tokens, dense) are the same
+  // attention under it (reading R23)
+  HLA_REQUIRE(d->order != HLA_ORDER_HILBERT_TILED || d->pattern == HLA_DENSE ||
+                  (d->pattern == HLA_WINDOW && ((int64_t)d->win_h * d->win_w) % 64 == 0),
+              HLA_ERR_UNSUPPORTED, "HLA_ORDER_HILBERT_TILED needs HLA_WINDOW with a multiple of 64 tokens, or HLA_DENSE");
+  HLA_REQUIRE(d->order != HLA_ORDER_HILBERT_TILED || (d->grid_h == d->grid_w && is_pow2(d->grid_h) && d->grid_h >= 8),
+              HLA_ERR_UNSUPPORTED, "HLA_ORDER_HILBERT_TILED needs a square 2^k grid, k >= 3");
   std::memset(p, 0, sizeof(*p));
   p->N = (int32_t)N;
   p->H = d->grid_h;
   p->W = d->grid_w;
   p->log2W = is_pow2(d->grid_w) ? ilog2(d->grid_w) : -1;
-  const bool hil = d->order == HLA_ORDER_HILBERT;
+  const bool hil = d->order != HLA_ORDER_ROW_MAJOR;
   if (d->pattern == HLA_DENSE) {
     p->kind = K_DENSE;
     return HLA_OK;

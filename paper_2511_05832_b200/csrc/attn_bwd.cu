@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.kv_full[kvs], kTile);
             __syncwarp();
             load_rows<D, kGather>(role == 0 ? sm.k[kvs] : sm.v[kvs], role == 0 ? &tmK : &tmV, &sm.kv_full[kvs], h,
-                                  b, prm.N, kb * kBlock, prm.s2c, pol_kv, lane);
+                                  b, prm.N, kb * kBlock, prm.s2c, pol_kv, lane, prm.box8);
           }
         }
         for (int t = 0; t < nt; ++t, ++g) {
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.o_full, kTile);
               __syncwarp();
               load_rows<D, kGather>(reinterpret_cast<uint8_t*>(sm.dq_stage), &tmDQ, &sm.o_full, h, b, prm.N,
-                                    qblk * prm.col_mul, prm.s2c, pol_q, lane);
+                                    qblk * prm.col_mul, prm.s2c, pol_q, lane, prm.box8);
             }
           } else if (kVar & 4) {
             if (lane == 0) sm100::mbar_arrive(&sm.q_full[s]);
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.q_full[s], kTile);
             __syncwarp();
             load_rows<D, kGather>(role == 1 ? sm.q[s] : sm.dO[s], role == 1 ? &tmQ : &tmDO, &sm.q_full[s], h, b,
-                                  prm.N, qblk * prm.col_mul, prm.s2c, pol_q, lane);
+                                  prm.N, qblk * prm.col_mul, prm.s2c, pol_q, lane, prm.box8);
           }
         }
         ++n;
@@ -1040,13 +1040,14 @@ hla_status prepare_main(const hla_pattern_desc* d, const hla_block_mask* m, int3
   prm.rpb_hw = (2 * pat.H - 1) * prm.rpb_w;
   prm.inv_scale = 1.f / sc;
   pl->gather = seq_to_cell != nullptr;
-  HLA_REQUIRE(!pl->gather || d->order == HLA_ORDER_HILBERT, HLA_ERR_INVALID,
+  HLA_REQUIRE(!pl->gather || d->order != HLA_ORDER_ROW_MAJOR, HLA_ERR_INVALID,
               "seq_to_cell (fused reorder) is only meaningful for Hilbert-order patterns");
+  prm.box8 = pl->gather && d->order == HLA_ORDER_HILBERT_TILED && head_dim == 32;
   HLA_REQUIRE(!pl->gather || ((uintptr_t)seq_to_cell & 15) == 0, HLA_ERR_INVALID,
               "seq_to_cell must be 16-byte aligned");
   const int64_t tok = (int64_t)batch * pat.N;
   auto mk_map = [&](CUtensorMap* mp, const void* base) {
-    return pl->gather ? make_gather_map(mp, base, tok, heads, head_dim)
+    return pl->gather ? make_gather_map(mp, base, tok, heads, head_dim, prm.box8 ? 8 : 1)
                       : make_rows_map(mp, base, tok, heads, head_dim, kBlock);
   };
   if ((st = mk_map(&pl->mq, q)) != HLA_OK) return st;
@@ -1089,7 +1090,7 @@ hla_status try_fuse(MainPlan* pl, const hla_block_mask* m, int32_t batch, int32_
   const bool all_local = plan_of(m, pl->prm.N) && m->n_dq_nonlocal == 0;
   const int64_t tok = (int64_t)batch * pl->prm.N;
   CUtensorMap* om = pl->full ? &pl->mdq : &pl->mo;   // (the full-tile kernel takes O in the dQ slot)
-  hla_status st = pl->gather ? make_gather_map(om, o, tok, heads, pl->head_dim)
+  hla_status st = pl->gather ? make_gather_map(om, o, tok, heads, pl->head_dim, pl->prm.box8 ? 8 : 1)
                              : make_rows_map(om, o, tok, heads, pl->head_dim, kBlock);
   if (st != HLA_OK) return st;
   if (!pl->full && !all_local &&

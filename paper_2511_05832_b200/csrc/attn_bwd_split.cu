@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.kv_full[kvs], kTile);
             __syncwarp();
             load_rows<D, kGather>(role == 0 ? sm.k[kvs] : sm.v[kvs], role == 0 ? &tmK : &tmV, &sm.kv_full[kvs], h,
-                                  b, prm.N, kb * kBlock, prm.s2c, pol_kv, lane);
+                                  b, prm.N, kb * kBlock, prm.s2c, pol_kv, lane, prm.box8);
           }
         }
         for (int t = 0; t < nt; ++t, ++g) {
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.o_full, kTile);
               __syncwarp();
               load_rows<D, kGather>(reinterpret_cast<uint8_t*>(sm.dq_stage), &tmO, &sm.o_full, h, b, prm.N,
-                                    qblk * prm.col_mul, prm.s2c, pol_q, lane);
+                                    qblk * prm.col_mul, prm.s2c, pol_q, lane, prm.box8);
             }
           } else if (kVar & 4) {
             if (lane == 0) sm100::mbar_arrive(&sm.q_full[s]);
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.q_full[s], kTile);
             __syncwarp();
             load_rows<D, kGather>(role == 1 ? sm.q[s] : sm.dO[s], role == 1 ? &tmQ : &tmDO, &sm.q_full[s], h, b,
-                                  prm.N, qblk * prm.col_mul, prm.s2c, pol_q, lane);
+                                  prm.N, qblk * prm.col_mul, prm.s2c, pol_q, lane, prm.box8);
           }
         }
         ++n;

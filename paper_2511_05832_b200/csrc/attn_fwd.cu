@@ -79,6 +79,7 @@ struct FwdParams {
   const uint8_t* kind;
   int32_t col_mul;           // start row of a list entry = column * col_mul (128, or 64: windows)
   const int32_t* s2c;        // fused reorder: seq_to_cell table (tensors in grid order), else null
+  int32_t box8;              // d = 32, tiled Hilbert order: Q / K / V rows as 8-row boxes (issue_rows)
   const float* rpb;          // global RPB table [heads][2H-1][2W-1] (kBias), else null
   const int32_t* cells;      // grid cell of each sequence position for the RPB offsets (null: identity)
   int32_t grid_h, grid_w, rpb_w, rpb_hw;   // H, W, 2W-1, (2H-1)(2W-1)
@@ -132,10 +133,16 @@ __device__ __forceinline__ int4 row_cells(int32_t N, int32_t seq0, const int32_t
 }
 template <int D, bool kGather>
 __device__ __forceinline__ void issue_rows(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int32_t h, int32_t b,
-                                           int32_t N, int32_t seq0, int4 c, uint64_t pol, int lane) {
+                                           int32_t N, int32_t seq0, int4 c, uint64_t pol, int lane, bool box8) {
   if (kGather) {
     const int32_t base = b * N;
-    sm100::tma_gather4(dst + lane * 4 * D * 2, map, bar, h * D, base + c.x, base + c.y, base + c.z, base + c.w, pol);
+    if (D == 32 && box8) {   // see attn_bwd_common.cuh load_rows: lane 2l holds row 8l's cell
+      const int32_t c8 = __shfl_sync(0xffffffffu, c.x, (2 * lane) & 31);
+      if (lane < 16) sm100::tma_load_2d(dst + lane * 8 * D * 2, map, bar, h * D, base + c8, pol);
+    } else {
+      sm100::tma_gather4(dst + lane * 4 * D * 2, map, bar, h * D, base + c.x, base + c.y, base + c.z, base + c.w,
+                         pol);
+    }
   } else if (lane == 0) {
     sm100::tma_load_3d(dst, map, bar, 0, h, b * N + seq0, pol);
   }
@@ -439,7 +446,8 @@ __global__ void __launch_bounds__(kThreads, 2)
           if (lane == 0) HLA_TR((3 << 24) | (1 << 16) | it.n);
           if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.q_full[qs], FwdSmem<D, kBias>::kTileBytes);
           __syncwarp();
-          issue_rows<D, kGather>(sm.q[qs], &tmQ, &sm.q_full[qs], h, b, prm.N, qb * kBlock, cells, pol_q, lane);
+          issue_rows<D, kGather>(sm.q[qs], &tmQ, &sm.q_full[qs], h, b, prm.N, qb * kBlock, cells, pol_q, lane,
+                                 prm.box8);
           ++n_units;
         } else {
           // warps 2 and 3 both feed every K / V stage (k_full / v_full count 2).  Fused reorder:
@@ -481,15 +489,27 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (kGather) {   // this warp's half of K (lanes 0-15), then, once PV freed the stage, of V
               if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.k_full[s], kTile / 2);
               __syncwarp();
-              if (lane < 16)
+              const bool b8 = D == 32 && prm.box8;   // 8-row boxes: lanes 0-7, row 8l's cell from lane 2l
+              const int32_t c8 = b8 ? __shfl_sync(0xffffffffu, cells.x, (2 * lane) & 31) : 0;
+              if (b8) {
+                if (lane < 8)
+                  sm100::tma_load_2d(sm.k[s] + (hh * 64 + 8 * lane) * D * 2, &tmK, &sm.k_full[s], h * D, base + c8,
+                                     pol_kv);
+              } else if (lane < 16) {
                 sm100::tma_gather4(sm.k[s] + row * D * 2, &tmK, &sm.k_full[s], h * D, base + cells.x, base + cells.y,
                                    base + cells.z, base + cells.w, pol_kv);
+              }
               if (g >= 2) sm100::mbar_wait(&sm.v_empty[s], par);
               if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.v_full[s], kTile / 2);
               __syncwarp();
-              if (lane < 16)
+              if (b8) {
+                if (lane < 8)
+                  sm100::tma_load_2d(sm.v[s] + (hh * 64 + 8 * lane) * D * 2, &tmV, &sm.v_full[s], h * D, base + c8,
+                                     pol_kv);
+              } else if (lane < 16) {
                 sm100::tma_gather4(sm.v[s] + row * D * 2, &tmV, &sm.v_full[s], h * D, base + cells.x, base + cells.y,
                                    base + cells.z, base + cells.w, pol_kv);
+              }
             } else {   // warp 2: K box, warp 3: V box; each arrives (no bytes) on the other barrier
               if (is_k) {
                 if (lane == 0) {
@@ -976,7 +996,7 @@ hla_status parse_score_mod(const hla_pattern_desc* d, const hla_score_mod* mod, 
   if (mod == nullptr || mod->kind == HLA_SCORE_NONE) return HLA_OK;
   HLA_REQUIRE(mod->kind == HLA_SCORE_GLOBAL_RPB, HLA_ERR_UNSUPPORTED, "score_mod kind %d not supported", mod->kind);
   HLA_REQUIRE(mod->rpb != nullptr, HLA_ERR_INVALID, "score_mod: rpb table is null");
-  HLA_REQUIRE(d->order != HLA_ORDER_HILBERT || mod->seq_to_cell != nullptr, HLA_ERR_INVALID,
+  HLA_REQUIRE(d->order == HLA_ORDER_ROW_MAJOR || mod->seq_to_cell != nullptr, HLA_ERR_INVALID,
               "score_mod: Hilbert order needs seq_to_cell for the 2D offsets");
   HLA_REQUIRE(((uintptr_t)mod->seq_to_cell & 15) == 0, HLA_ERR_INVALID, "score_mod: seq_to_cell must be 16-byte aligned");
   HLA_REQUIRE(!bwd || mod->drpb != nullptr, HLA_ERR_INVALID, "score_mod: drpb (table gradient) is null");
@@ -1037,16 +1057,18 @@ extern "C" hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_ma
   prm.visited = reinterpret_cast<unsigned long long*>(tiles_visited);
   const bool two_d = pat.kind == K_WSA || pat.kind == K_SA || pat.kind == K_NA2D;
   const bool gather = seq_to_cell != nullptr;
-  HLA_REQUIRE(!gather || d->order == HLA_ORDER_HILBERT, HLA_ERR_INVALID,
+  HLA_REQUIRE(!gather || d->order != HLA_ORDER_ROW_MAJOR, HLA_ERR_INVALID,
               "seq_to_cell (fused reorder) is only meaningful for Hilbert-order patterns");
   HLA_REQUIRE(!gather || ((uintptr_t)seq_to_cell & 15) == 0, HLA_ERR_INVALID, "seq_to_cell must be 16-byte aligned");
+  prm.box8 = gather && d->order == HLA_ORDER_HILBERT_TILED && head_dim == 32;
   const int64_t rows = (int64_t)batch * pat.N;
   CUtensorMap mq, mk, mv, mo;
   if (gather) {
     if ((st = make_gather_map(&mo, o, rows, heads, head_dim)) != HLA_OK) return st;
-    if ((st = make_gather_map(&mq, q, rows, heads, head_dim)) != HLA_OK) return st;
-    if ((st = make_gather_map(&mk, k, rows, heads, head_dim)) != HLA_OK) return st;
-    if ((st = make_gather_map(&mv, v, rows, heads, head_dim)) != HLA_OK) return st;
+    const int kBoxH = prm.box8 ? 8 : 1;
+    if ((st = make_gather_map(&mq, q, rows, heads, head_dim, kBoxH)) != HLA_OK) return st;
+    if ((st = make_gather_map(&mk, k, rows, heads, head_dim, kBoxH)) != HLA_OK) return st;
+    if ((st = make_gather_map(&mv, v, rows, heads, head_dim, kBoxH)) != HLA_OK) return st;
   } else {
     if ((st = make_rows_map(&mo, o, rows, heads, head_dim, kBlock)) != HLA_OK) return st;
     if ((st = make_rows_map(&mq, q, rows, heads, head_dim, kBlock)) != HLA_OK) return st;

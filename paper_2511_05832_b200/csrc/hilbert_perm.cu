@@ -59,6 +59,21 @@ __global__ void hilbert_index_kernel(int32_t N, int log2n, int32_t* __restrict__
   }
 }
 
+// HLA_ORDER_HILBERT_TILED (reading R23): on a 2^k grid (k >= 3) every aligned 64-token
+// segment of the curve is an aligned 8 x 8 cell square (the curve finishes each aligned 2^j
+// square before it leaves it); inside each segment the cells are renumbered in raster order,
+// s' = (s & ~63) + 8 * (row & 7) + (col & 7), so that every aligned 8 positions are 8
+// consecutive cells of one grid row (one 8-row TMA box instead of two gather4 ops).
+__global__ void hilbert_tiled_index_kernel(int32_t N, int log2n, int32_t* __restrict__ seq_to_cell,
+                                           int32_t* __restrict__ cell_to_seq) {
+  for (int32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < N; s += gridDim.x * blockDim.x) {
+    const int32_t cell = hilbert_d2cell((uint32_t)s, log2n);
+    const int32_t t = (s & ~63) | (((cell >> log2n) & 7) << 3) | (cell & 7);
+    if (seq_to_cell) seq_to_cell[t] = cell;
+    if (cell_to_seq) cell_to_seq[cell] = t;
+  }
+}
+
 struct PermPtrs {
   const uint4* src[4];
   uint4* dst[4];
@@ -188,6 +203,23 @@ extern "C" hla_status hla_hilbert_index(int32_t grid_h, int32_t grid_w, int32_t*
   if (!seq_to_cell && !cell_to_seq) return HLA_OK;
   const int blocks = (N + 255) / 256;
   hilbert_index_kernel<<<blocks, 256, 0, stream>>>(N, log2n, seq_to_cell, cell_to_seq);
+  HLA_CUDA_TRY(cudaGetLastError());
+  return HLA_OK;
+}
+
+extern "C" hla_status hla_hilbert_tiled_index(int32_t grid_h, int32_t grid_w, int32_t* seq_to_cell,
+                                              int32_t* cell_to_seq, cudaStream_t stream) {
+  clear_error();
+  HLA_REQUIRE(grid_h >= 1 && grid_w >= 1 && (int64_t)grid_h * grid_w < (1ll << 30), HLA_ERR_INVALID,
+              "grid %dx%d invalid", grid_h, grid_w);
+  HLA_REQUIRE(grid_h == grid_w && is_pow2(grid_h) && grid_h >= 8, HLA_ERR_UNSUPPORTED,
+              "tiled Hilbert order needs a square 2^k grid, k >= 3 (got %dx%d)", grid_h, grid_w);
+  int log2n = 0;
+  hla_status st = check_grid(grid_h, grid_w, &log2n);
+  if (st != HLA_OK) return st;
+  if (!seq_to_cell && !cell_to_seq) return HLA_OK;
+  const int32_t N = grid_h * grid_w;
+  hilbert_tiled_index_kernel<<<(N + 255) / 256, 256, 0, stream>>>(N, log2n, seq_to_cell, cell_to_seq);
   HLA_CUDA_TRY(cudaGetLastError());
   return HLA_OK;
 }

@@ -171,6 +171,7 @@ def test_cfg5_stage(g, H):
     N = g * g
     q, k, v, do = _inputs(B, N, H, d, seed=21)
     layer = hla.HilbertLocalAttention("HWA", g, g, 8, 8, B, H, d, device=DEV)
+    assert layer.tiled          # d = 32, 64-token windows: the tiled order and 8-row box loads
     o = layer.forward(q, k, v).clone()
     dq, dk, dv = (t.clone() for t in layer.backward(do))
     torch.cuda.synchronize()
@@ -181,6 +182,36 @@ def test_cfg5_stage(g, H):
     dQ, dK, dV, O, _ = oatt.attn_bwd_slice(Q, K, V, DO, spec)
     for name, got, ref in (("O", o, O), ("dQ", dq, dQ), ("dK", dk, dK), ("dV", dv, dV)):
         assert_close("cfg5 g%d %s" % (g, name), to_np(got[b, :, h])[s2c], ref)
+
+
+@pytest.mark.parametrize("g,w,B,H,d,blk", [(64, 8, 4, 3, 32, 64), (64, 8, 2, 3, 32, 128), (32, 16, 2, 2, 32, 64),
+                                          (16, 8, 3, 2, 32, 128), (64, 16, 2, 2, 64, 128), (8, 8, 2, 2, 32, 64)])
+def test_tiled_order_vs_oracle_and_hilbert_order(g, w, B, H, d, blk):
+    """HLA_ORDER_HILBERT_TILED (reading R23) through the layer: O, dQ, dK, dV equal the fp64
+    oracle of the paper's Hilbert-order HWA on every checked slice, agree with the same layer in
+    Hilbert order to bf16 rounding, and the LSE (kept in the tiled sequence order) is the oracle's
+    LSE relabeled.  d = 32 runs the 8-row box loads, d = 64 the gather4 loads over the tiled table."""
+    N = g * g
+    q, k, v, do = _inputs(B, N, H, d, seed=23)
+    til = hla.HilbertLocalAttention("HWA", g, g, w, w, B, H, d, block=blk, device=DEV, tiled=True)
+    hil = hla.HilbertLocalAttention("HWA", g, g, w, w, B, H, d, block=blk, device=DEV, tiled=False)
+    r1 = [t.clone() for t in (til.forward(q, k, v),) + til.backward(do)]
+    r2 = [t.clone() for t in (hil.forward(q, k, v),) + hil.backward(do)]
+    torch.cuda.synchronize()
+    assert til.tiled and not hil.tiled
+    for a, b in zip(r1, r2):
+        assert (a.float() - b.float()).abs().max().item() <= 2e-2 * max(b.float().abs().max().item(), 1.0)
+    spec = Spec("HWA", g, g, w, w)
+    h2c, _ = hilbert.hilbert_order(g, g)
+    t2c, _ = hilbert.hilbert_tiled_order(g, g)
+    _, c2h = hilbert.hilbert_order(g, g)
+    for b, h in [(0, 0), (B - 1, H - 1)]:
+        Q, K, V, DO = (to_np(t[b, :, h])[h2c] for t in (q, k, v, do))
+        dQ, dK, dV, O, L = oatt.attn_bwd_slice(Q, K, V, DO, spec)
+        for name, got, ref in zip(("O", "dQ", "dK", "dV"), r1, (O, dQ, dK, dV)):
+            assert_close("tiled g%d b%d %s" % (g, blk, name), to_np(got[b, :, h])[h2c], ref)
+        got_lse = to_np(til.lse[b, h])           # position t of the tiled order = cell t2c[t]
+        assert_close("tiled LSE", got_lse, L[c2h[t2c]], max_abs=LSE_MAX_ABS, mean_abs=LSE_MAX_ABS)
 
 
 FULL_BWD = [c for c in FULL if c[0] in ("cfg2", "cfg2-rm", "cfg3", "cfg3-rm", "cfg4", "cfg4-rm")]
@@ -195,7 +226,7 @@ def test_fused_reorder_matches_explicit_permutation(kind, g, w, B, H, d):
     dQ within atomics-order rounding."""
     q, k, v, do = _inputs(B, g * g, H, d, seed=11)
     shift = (w * w) // 2 if kind == "HSWA" else 0
-    fused = hla.HilbertLocalAttention(kind, g, g, w, w, B, H, d, shift=shift, device=DEV, fused=True)
+    fused = hla.HilbertLocalAttention(kind, g, g, w, w, B, H, d, shift=shift, device=DEV, fused=True, tiled=False)
     plain = hla.HilbertLocalAttention(kind, g, g, w, w, B, H, d, shift=shift, device=DEV, fused=False)
     r1 = [t.clone() for t in (fused.forward(q, k, v),) + fused.backward(do)]
     r2 = [t.clone() for t in (plain.forward(q, k, v),) + plain.backward(do)]

@@ -40,6 +40,32 @@ def test_hilbert_index_bit_exact(k):
     assert np.array_equal(c2s.cpu().numpy(), ref_c2s)
 
 
+@pytest.mark.parametrize("k", range(3, 10))
+def test_hilbert_tiled_index_bit_exact(k):
+    """HLA_ORDER_HILBERT_TILED (reading R23): the device kernel's closed-form relabeling
+    (s & ~63) + 8 (row & 7) + (col & 7) == the oracle's sort of every 64-token segment."""
+    n = 1 << k
+    s2c, c2s = hla.hla_hilbert_tiled_index(n, n, DEV)
+    ref_s2c, ref_c2s = hilbert.hilbert_tiled_order(n, n)
+    assert np.array_equal(s2c.cpu().numpy(), ref_s2c)
+    assert np.array_equal(c2s.cpu().numpy(), ref_c2s)
+
+
+def test_tiled_order_rejections():
+    """Tiled order only where it is the same attention (square 2^k grid >= 8; HWA with a
+    multiple of 64 tokens or DENSE): anything else is HLA_ERR_UNSUPPORTED, nothing built."""
+    for h, w in [(4, 4), (56, 56), (64, 32)]:
+        with pytest.raises(hla.HlaError) as e:
+            hla.hla_hilbert_tiled_index(h, w, DEV)
+        assert "HLA_ERR_UNSUPPORTED" in str(e.value)
+    for kind, g, w in [("HSA", 64, 16), ("HNA", 64, 8), ("HWA", 64, 4), ("HSWA", 64, 8), ("HWA", 56, 8)]:
+        desc = hla.pattern_desc(kind, g, g, w, w, 128, (w * w) // 2 if kind == "HSWA" else 0, tiled=True)
+        with pytest.raises(hla.HlaError):
+            hla.hla_build_block_mask(desc, DEV)
+    with pytest.raises(ValueError):
+        hla.HilbertLocalAttention("HSA", 64, 64, 16, 16, 1, 1, 32, device=DEV, tiled=True)
+
+
 @pytest.mark.parametrize("h,w", [(56, 56), (28, 28), (14, 14), (7, 7), (96, 96), (160, 160), (16, 24), (24, 16),
                                  (1, 9), (5, 3), (128, 256)])
 def test_generalized_hilbert_index_bit_exact(h, w):
