@@ -344,7 +344,10 @@ __device__ __forceinline__ int4 rpb_key_offs(const int32_t* cells, int32_t k0, i
   return make_int4(off(c.x), off(c.y), off(c.z), off(c.w));
 }
 
-template <int D, bool kTwoD, bool kGather, bool kBias>
+// kHalf: HWA with 64-token windows (launch_fwd checks it): every tile pairs the two windows of its
+// 128 query rows with the same two windows of keys, so each softmax warp's 32 rows see exactly one
+// unmasked 64-column half of S -- half the S loads, exponentials and P stores.
+template <int D, bool kTwoD, bool kGather, bool kBias, bool kHalf = false>
 __global__ void __launch_bounds__(kThreads, 2)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
@@ -712,6 +715,75 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (row == 0) HLA_TR((2 << 24) | (1 << 16) | g);
         sm100::tc_fence_after();
         const int32_t tm = tile_meta(meta, prm.col_idx, prm.kind, it.rs, t);
+        if constexpr (kHalf) {
+          const uint32_t hc = (uint32_t)(row >> 6) * 64u;   // this warp's key columns [hc, hc + 64)
+          uint32_t sr[64];
+          sm100::tmem_ld32(tmem + lane_off + kColS + hc, *reinterpret_cast<uint32_t(*)[32]>(sr));
+          sm100::tmem_ld32(tmem + lane_off + kColS + hc + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+          sm100::tmem_wait_ld();
+          sm100::tc_fence_before();
+          sm100::mbar_arrive(&sm.s_free);
+          HLA_PADD(4, ts0);
+          const float* s = reinterpret_cast<const float*>(sr);
+          float m8[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) m8[j] = s[j];
+#pragma unroll
+          for (int c = 8; c < 64; ++c) m8[c & 7] = fmaxf(m8[c & 7], s[c]);
+#pragma unroll
+          for (int j = 4; j > 0; j >>= 1)
+#pragma unroll
+            for (int i = 0; i < j; ++i) m8[i] = fmaxf(m8[i], m8[i + j]);
+          const float m_tile = m8[0] * sl2;
+          const float m_new = (m_tile > m_ref + 8.f) ? m_tile : m_ref;
+          const float alpha = (m_new == m_ref) ? 1.f : sm100::ex2(m_ref - m_new);
+          m_ref = m_new;
+          l *= alpha;
+          const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
+          float l4[4] = {0.f, 0.f, 0.f, 0.f};
+          uint32_t pk[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const float p0 = sm100::ex2(fmaf(s[2 * e], sl2, -m_use));
+            const float p1 = sm100::ex2(fmaf(s[2 * e + 1], sl2, -m_use));
+            l4[e & 3] += p0 + p1;
+            pk[e] = sm100::pack_bf16(p0, p1);
+          }
+          l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
+          HLA_PADD(5, ts0);
+          if (g > 0) {
+            HLA_PW(6, sm100::mbar_wait(&sm.pv_done, (g - 1) & 1));
+            sm100::tc_fence_after();
+          }
+          HLA_PMARK(tst0);
+          if (__any_sync(0xffffffffu, t > 0 && alpha != 1.f)) {
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+              uint32_t o[32];
+              sm100::tmem_ld16(tmem + lane_off + kColO + obuf + c * 32, o);
+              sm100::tmem_ld16(tmem + lane_off + kColO + obuf + c * 32 + 16, o + 16);
+              sm100::tmem_wait_ld();
+#pragma unroll
+              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+              sm100::tmem_st16(tmem + lane_off + kColO + obuf + c * 32, o);
+              sm100::tmem_st16(tmem + lane_off + kColO + obuf + c * 32 + 16, o + 16);
+            }
+          }
+          uint32_t z[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) z[e] = 0u;
+          const uint32_t pl = kColP + hc / 2, pd = kColP + (64u - hc) / 2;   // live / dead P columns
+          sm100::tmem_st16(tmem + lane_off + pl, pk);
+          sm100::tmem_st16(tmem + lane_off + pl + 16, pk + 16);
+          sm100::tmem_st16(tmem + lane_off + pd, z);
+          sm100::tmem_st16(tmem + lane_off + pd + 16, z);
+          sm100::tmem_wait_st();
+          sm100::tc_fence_before();
+          sm100::mbar_arrive(&sm.p_full);
+          if (o_double<D>() && pend) run_pending();
+          HLA_PADD(7, tst0);
+          continue;
+        }
         // partial tile that misses all 32 rows of this warp (1D windows: the warps away
         // from the window's edge): no S load, mask or exponentials -- P rows of zero
         if ((tm & 3) == 2 &&
@@ -931,11 +1003,11 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (warp == 1) sm100::tmem_dealloc(sm.tmem_base, kTmemCols);
 }
 
-template <int D, bool kTwoD, bool kGather, bool kBias>
+template <int D, bool kTwoD, bool kGather, bool kBias, bool kHalf = false>
 hla_status launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mo,
                       const FwdParams& prm, int32_t n_qblocks, cudaStream_t stream) {
   const size_t smem = sizeof(FwdSmem<D, kBias>) + 1024;
-  auto* fn = attn_fwd_kernel<D, kTwoD, kGather, kBias>;
+  auto* fn = attn_fwd_kernel<D, kTwoD, kGather, kBias, kHalf>;
   HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t units = (int64_t)n_qblocks * prm.heads * prm.batch;
   const int grid = (int)std::min<int64_t>((units + 1) / 2, 2 * (int64_t)num_sms());   // pairs of units
@@ -952,6 +1024,13 @@ hla_status dispatch_fwd(int head_dim, bool gather, bool two_d, const CUtensorMap
     if (gather) return launch_fwd<64, false, true, kBias>(mq, mk, mv, mo, prm, mqb, stream);
     return two_d ? launch_fwd<64, true, false, kBias>(mq, mk, mv, mo, prm, mqb, stream)
                  : launch_fwd<64, false, false, kBias>(mq, mk, mv, mo, prm, mqb, stream);
+  }
+  if constexpr (!kBias) {
+    // HWA with 64-token windows: the half-row softmax instantiation (attn_fwd_kernel kHalf); every
+    // list entry is then the diagonal window pair of its 128-row tile (block 128: kv-block i of
+    // q-block i; block 64: the window (2t, 2t + 1) of tile t)
+    if (gather && prm.pat.kind == K_HWA && prm.pat.n == 64)
+      return launch_fwd<32, false, true, false, true>(mq, mk, mv, mo, prm, mqb, stream);
   }
   if (gather) return launch_fwd<32, false, true, kBias>(mq, mk, mv, mo, prm, mqb, stream);
   return two_d ? launch_fwd<32, true, false, kBias>(mq, mk, mv, mo, prm, mqb, stream)
