@@ -1021,6 +1021,10 @@ hla_status dispatch_fwd(int head_dim, bool gather, bool two_d, const CUtensorMap
                         const CUtensorMap& mv, const CUtensorMap& mo, const FwdParams& prm, int32_t mqb,
                         cudaStream_t stream) {
   if (head_dim == 64) {
+    if constexpr (!kBias) {
+      if (gather && prm.pat.kind == K_HWA && prm.pat.n == 64)   // half-row softmax (see below)
+        return launch_fwd<64, false, true, false, true>(mq, mk, mv, mo, prm, mqb, stream);
+    }
     if (gather) return launch_fwd<64, false, true, kBias>(mq, mk, mv, mo, prm, mqb, stream);
     return two_d ? launch_fwd<64, true, false, kBias>(mq, mk, mv, mo, prm, mqb, stream)
                  : launch_fwd<64, false, false, kBias>(mq, mk, mv, mo, prm, mqb, stream);

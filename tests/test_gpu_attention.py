@@ -185,7 +185,8 @@ def test_cfg5_stage(g, H):
 
 
 @pytest.mark.parametrize("g,w,B,H,d,blk", [(64, 8, 4, 3, 32, 64), (64, 8, 2, 3, 32, 128), (32, 16, 2, 2, 32, 64),
-                                          (16, 8, 3, 2, 32, 128), (64, 16, 2, 2, 64, 128), (8, 8, 2, 2, 32, 64)])
+                                          (16, 8, 3, 2, 32, 128), (64, 16, 2, 2, 64, 128), (8, 8, 2, 2, 32, 64),
+                                          (32, 8, 2, 2, 64, 64), (16, 8, 2, 3, 64, 128)])
 def test_tiled_order_vs_oracle_and_hilbert_order(g, w, B, H, d, blk):
     """HLA_ORDER_HILBERT_TILED (reading R23) through the layer: O, dQ, dK, dV equal the fp64
     oracle of the paper's Hilbert-order HWA on every checked slice, agree with the same layer in
