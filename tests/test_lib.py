@@ -95,6 +95,28 @@ def test_argument_validation_without_gpu():
     assert L.hla_build_bwd_plan(ctypes.byref(m), None) == _lib.HLA_ERR_UNSUPPORTED
 
 
+def test_tiled_order_validation_without_gpu():
+    """HLA_ORDER_HILBERT_TILED (reading R23) is accepted only where it is the same attention:
+    host-side checks before any CUDA call, and the layer's selection rule agrees with them."""
+    from paper_2511_05832_b200 import _lib, api
+    L = _lib.lib()
+    assert L.hla_hilbert_tiled_index(4, 4, None, None, None) == _lib.HLA_ERR_UNSUPPORTED
+    assert L.hla_hilbert_tiled_index(56, 56, None, None, None) == _lib.HLA_ERR_UNSUPPORTED
+    assert L.hla_hilbert_tiled_index(64, 32, None, None, None) == _lib.HLA_ERR_UNSUPPORTED
+    assert L.hla_hilbert_tiled_index(64, 64, None, None, None) == _lib.HLA_OK   # no outputs: no work
+    m = _lib.BlockMaskC()
+    nnz = ctypes.c_int64()
+    for kind, g, w, want in (("HSA", 64, 16, _lib.HLA_ERR_UNSUPPORTED), ("HWA", 64, 4, _lib.HLA_ERR_UNSUPPORTED),
+                             ("HNA", 64, 8, _lib.HLA_ERR_UNSUPPORTED), ("HWA", 56, 8, _lib.HLA_ERR_UNSUPPORTED)):
+        d = api.pattern_desc(kind, g, g, w, w, tiled=True)
+        assert L.hla_build_block_mask(ctypes.byref(d), ctypes.byref(m), ctypes.byref(nnz), None) == want, kind
+        assert not api.tiled_order_applies(kind, g, g, w, w)
+    with pytest.raises(ValueError):
+        api.pattern_desc("WSA", 64, 64, 8, 8, tiled=True)      # row-major: not a Hilbert order
+    assert api.tiled_order_applies("HWA", 64, 64, 8, 8) and api.tiled_order_applies("HWA", 8, 8, 8, 8)
+    assert api.tiled_order_applies("HWA", 128, 128, 16, 16) and not api.tiled_order_applies("HWA", 64, 64, 7, 7)
+
+
 @pytest.mark.parametrize("kind,H,W,wh,ww,b", [("HWA", 56, 56, 7, 7, 128), ("SA", 56, 56, 7, 7, 128),
                                              ("HNA", 128, 128, 17, 17, 128), ("WSA", 128, 128, 16, 16, 512),
                                              ("HWA", 16, 16, 8, 8, 16)])
