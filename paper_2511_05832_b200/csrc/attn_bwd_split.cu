@@ -86,7 +86,12 @@ struct SplitSmem {
 // bytes, the compute threads form D * scale and LSE * log2(e) (form_d) when they first meet a
 // q-block; tmO is the O map.  Non-local dQ chains still reduce into the fp32 accumulator (zeroed
 // by dq_zero_kernel), staged in 16-column quarters through the epi_stage (tmDQ: 16-float boxes).
-template <int D, bool kTwoD, bool kGather, bool kBias, bool kFuse>
+// kDiag: HWA with 64-token windows, N % 128 == 0 (the launcher checks): every tile pairs the two
+// windows of its 128 key rows with the same two windows of queries, so key rows 0-63 (TMEM lane
+// quarters 0, 1) meet only q-half A, unmasked, and rows 64-127 only q-half B.  The liveness of a
+// warp's chunk is then known without the per-half interval reductions, and the dS^T quadrants no
+// key row meets are zeroed once at the start (they are never written again).
+template <int D, bool kTwoD, bool kGather, bool kBias, bool kFuse, bool kDiag = false>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -369,6 +374,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         (&sm.rpb_win[0][0])[i] = 0;
       sm100::named_bar_sync(3, 256);
     }
+    if constexpr (kDiag) {   // both dS^T tiles start zeroed (the dead quadrants stay so)
+      const uint32_t ds0 = sm100::smem_u32(sm.ds[0]);
+      for (uint32_t i = (uint32_t)cth * 16u; i < 2u * sizeof(sm.ds[0]); i += 256u * 16u)
+        sm100::sts_u4(ds0 + i, 0u, 0u, 0u, 0u);
+      sm100::fence_proxy_async_smem();
+      sm100::named_bar_sync(3, 256);
+    }
     float rpb_fx = 0.f;   // fixed-point scale of the dRPB window, from the previous tile's maximum (0: none yet)
     uint32_t n = 0, g = 0;
     for (int32_t kq = 0;; ++kq) {
@@ -456,7 +468,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           // mask).  Full tiles / 2D patterns: all 4 groups, element mask on partial tiles.
           int ulo = 0, uhi = 4;
           bool elem = kd == 2;
-          if (kd == 2 && !kTwoD) {
+          if constexpr (kDiag) {
+            const bool live = (quarter >> 1) == half;
+            ulo = live ? 0 : 4;
+            uhi = live ? 4 : 0;
+            elem = false;
+          } else if (kd == 2 && !kTwoD) {
             const int32_t base = q0 + c * 32;
             const int32_t lo = min(max(box.lo - base, 0), 32), hi = min(max(box.lo + box.len - base, 0), 32);
             const bool any = hi > lo;
@@ -475,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int e = 0; e < 16; ++e) z[e] = 0u;
             sm100::tmem_st16(tmem + lane_off + kColS + c * 32, z);
 #pragma unroll
-            for (int u4 = 0; u4 < 4; ++u4) {
+            for (int u4 = 0; u4 < 4 && !kDiag; ++u4) {
               const int qc = c * 32 + u4 * 8;
               const uint32_t off =
                   (uint32_t)(qc >> 6) * 16384u + sm100::swz128((uint32_t)row * 128u + (uint32_t)(qc & 63) * 2u);
@@ -837,12 +854,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 
-template <int D, bool kTwoD, bool kGather, bool kBias, bool kFuse = false>
+template <int D, bool kTwoD, bool kGather, bool kBias, bool kFuse = false, bool kDiag = false>
 hla_status launch_split_t(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                           const CUtensorMap& mdo, const CUtensorMap& mdq, const BwdParams& prm, int32_t n_kblocks,
                           cudaStream_t stream, const CUtensorMap* mo = nullptr) {
   const size_t smem = sizeof(SplitSmem<D, kBias>) + 1024;
-  auto* fn = attn_bwd_split_kernel<D, kTwoD, kGather, kBias, kFuse>;
+  auto* fn = attn_bwd_split_kernel<D, kTwoD, kGather, kBias, kFuse, kDiag>;
   HLA_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t pairs = (int64_t)((n_kblocks + 1) / 2) * prm.heads * prm.batch;   // work units (kv-block pairs)
   const int grid = (int)std::min<int64_t>(pairs, (int64_t)num_sms());
@@ -867,6 +884,9 @@ hla_status dispatch_split(int head_dim, bool gather, bool two_d, const CUtensorM
                : launch_split_t<32, false, false, kBias>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream);
 }
 
+// HWA with 64-token windows and no ragged tile: the kDiag instantiation applies
+inline bool diag64(const BwdParams& prm) { return prm.pat.kind == K_HWA && prm.pat.n == 64 && prm.N % 128 == 0; }
+
 // preprocess folded in (no bias): every dQ chain local, mdq = the O map, lse2 = raw LSE
 hla_status dispatch_split_fused(int head_dim, bool gather, bool two_d, const CUtensorMap& mq, const CUtensorMap& mk,
                                 const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq,
@@ -876,6 +896,8 @@ hla_status dispatch_split_fused(int head_dim, bool gather, bool two_d, const CUt
     return two_d ? launch_split_t<64, true, false, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream, &mo)
                  : launch_split_t<64, false, false, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream, &mo);
   }
+  if (gather && diag64(prm))
+    return launch_split_t<32, false, true, false, true, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream, &mo);
   if (gather) return launch_split_t<32, false, true, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream, &mo);
   return two_d ? launch_split_t<32, true, false, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream, &mo)
                : launch_split_t<32, false, false, false, true>(mq, mk, mv, mdo, mdq, prm, n_kblocks, stream, &mo);
