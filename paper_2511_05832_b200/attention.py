@@ -47,7 +47,7 @@ class HilbertLocalAttention:
         self.scale = float(scale)
         # tiled Hilbert order (include/hla.h HLA_ORDER_HILBERT_TILED; R23): the same
         # attention for HWA with 64-token-multiple windows on square 2^k grids; at head_dim 32 the
-        # fused loads then move 8-row boxes instead of gather4 ops.  None = where it applies and pays.
+        # fused loads then move one TMA box per 8 x 8 cell square.  None = where it applies and pays.
         ok = api.tiled_order_applies(kind, grid_h, grid_w, win_h, win_w) and fused and not rpb
         self.tiled = ok and head_dim == 32 if tiled is None else bool(tiled)
         if self.tiled and not ok:

@@ -1042,12 +1042,13 @@ hla_status prepare_main(const hla_pattern_desc* d, const hla_block_mask* m, int3
   pl->gather = seq_to_cell != nullptr;
   HLA_REQUIRE(!pl->gather || d->order != HLA_ORDER_ROW_MAJOR, HLA_ERR_INVALID,
               "seq_to_cell (fused reorder) is only meaningful for Hilbert-order patterns");
-  prm.box8 = pl->gather && d->order == HLA_ORDER_HILBERT_TILED && head_dim == 32;
+  prm.box8 = (pl->gather && d->order == HLA_ORDER_HILBERT_TILED && head_dim == 32) ? ilog2(pat.W) + 1 : 0;
   HLA_REQUIRE(!pl->gather || ((uintptr_t)seq_to_cell & 15) == 0, HLA_ERR_INVALID,
               "seq_to_cell must be 16-byte aligned");
   const int64_t tok = (int64_t)batch * pat.N;
   auto mk_map = [&](CUtensorMap* mp, const void* base) {
-    return pl->gather ? make_gather_map(mp, base, tok, heads, head_dim, prm.box8 ? 8 : 1)
+    if (prm.box8) return make_square_map(mp, base, batch, pat.H, pat.W, heads, head_dim);
+    return pl->gather ? make_gather_map(mp, base, tok, heads, head_dim)
                       : make_rows_map(mp, base, tok, heads, head_dim, kBlock);
   };
   if ((st = mk_map(&pl->mq, q)) != HLA_OK) return st;
@@ -1090,7 +1091,8 @@ hla_status try_fuse(MainPlan* pl, const hla_block_mask* m, int32_t batch, int32_
   const bool all_local = plan_of(m, pl->prm.N) && m->n_dq_nonlocal == 0;
   const int64_t tok = (int64_t)batch * pl->prm.N;
   CUtensorMap* om = pl->full ? &pl->mdq : &pl->mo;   // (the full-tile kernel takes O in the dQ slot)
-  hla_status st = pl->gather ? make_gather_map(om, o, tok, heads, pl->head_dim, pl->prm.box8 ? 8 : 1)
+  hla_status st = pl->prm.box8 ? make_square_map(om, o, batch, pl->prm.pat.H, pl->prm.pat.W, heads, pl->head_dim)
+                 : pl->gather ? make_gather_map(om, o, tok, heads, pl->head_dim)
                              : make_rows_map(om, o, tok, heads, pl->head_dim, kBlock);
   if (st != HLA_OK) return st;
   if (!pl->full && !all_local &&

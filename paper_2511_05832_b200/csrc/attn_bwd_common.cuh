@@ -27,7 +27,7 @@ struct BwdParams {
   const float* dsum;       // D * scale, [B, H, N] (workspace, from the preprocess)
   float* dq_acc;           // [B, N, H, Dh] fp32 (grid order when s2c != null)
   const int32_t* s2c;      // fused reorder: seq_to_cell table (tensors in grid order), else null
-  int32_t box8;            // d = 32, tiled Hilbert order: rows loaded as 8-row boxes (see load_rows)
+  int32_t box8;            // d = 32, tiled Hilbert order: log2(W) + 1 (0 = off): square-box loads (load_rows)
   const float* rpb;        // global RPB table [heads][2H-1][2W-1] (kBias)
   float* drpb;             // its gradient (accumulated)
   const int32_t* cells;    // grid cell of each sequence position (null: identity)
@@ -154,18 +154,21 @@ __device__ __forceinline__ uint32_t dq_plan(const uint8_t* t_dq, int32_t e, uint
 
 // Load the 128 token rows [seq0, seq0 + 128) (sequence order) of head h, batch b;
 // see attn_fwd.cu load_rows (kGather = fused reorder through s2c with .tile::gather4).
-// box8 (d = 32, HLA_ORDER_HILBERT_TILED: every aligned 8 sequence positions are 8 consecutive
-// cells of one grid row): 16 lanes each load an 8-row box (512 B) instead of 32 gather4 ops of
-// 4 x 64-B rows -- at d = 32 the per-op cost of the TMA unit, not the bytes, bounds the loads.
+// sq (d = 32, HLA_ORDER_HILBERT_TILED; log2(grid_w) + 1, 0 = off): every aligned 64 sequence
+// positions are an aligned 8 x 8 cell square in raster order, so 2 lanes each move one square with
+// a 5-D box (`map` from make_square_map) instead of 32 gather4 ops of 4 x 64-B rows -- at d = 32
+// the per-op cost of the TMA unit, not the bytes, bounds the loads.  A square past N (ragged
+// last tile) loads the square at cell 0.
 template <int D, bool kGather>
 __device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int32_t h,
                                           int32_t b, int32_t N, int32_t seq0, const int32_t* s2c, uint64_t pol,
-                                          int lane, bool box8) {
+                                          int lane, int sq) {
   if (kGather) {
-    if (D == 32 && box8) {
-      if (lane < 16) {
-        const int32_t c = seq0 + 8 * lane < N ? __ldg(s2c + seq0 + 8 * lane) : 0;
-        sm100::tma_load_2d(dst + lane * 8 * D * 2, map, bar, h * D, b * N + c, pol);
+    if (D == 32 && sq) {
+      if (lane < 2) {
+        const int32_t c = seq0 + 64 * lane < N ? __ldg(s2c + seq0 + 64 * lane) : 0;
+        const int32_t lw = sq - 1;
+        sm100::tma_load_5d(dst + lane * 64 * D * 2, map, bar, 0, h, c & ((1 << lw) - 1), c >> lw, b, pol);
       }
       return;
     }

@@ -79,7 +79,7 @@ struct FwdParams {
   const uint8_t* kind;
   int32_t col_mul;           // start row of a list entry = column * col_mul (128, or 64: windows)
   const int32_t* s2c;        // fused reorder: seq_to_cell table (tensors in grid order), else null
-  int32_t box8;              // d = 32, tiled Hilbert order: Q / K / V rows as 8-row boxes (issue_rows)
+  int32_t box8;              // d = 32, tiled Hilbert order: log2(W) + 1 (0 = off): Q / K / V as 8 x 8-cell square boxes
   const float* rpb;          // global RPB table [heads][2H-1][2W-1] (kBias), else null
   const int32_t* cells;      // grid cell of each sequence position for the RPB offsets (null: identity)
   int32_t grid_h, grid_w, rpb_w, rpb_hw;   // H, W, 2W-1, (2H-1)(2W-1)
@@ -133,12 +133,14 @@ __device__ __forceinline__ int4 row_cells(int32_t N, int32_t seq0, const int32_t
 }
 template <int D, bool kGather>
 __device__ __forceinline__ void issue_rows(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int32_t h, int32_t b,
-                                           int32_t N, int32_t seq0, int4 c, uint64_t pol, int lane, bool box8) {
+                                           int32_t N, int32_t seq0, int4 c, uint64_t pol, int lane, int sq) {
   if (kGather) {
     const int32_t base = b * N;
-    if (D == 32 && box8) {   // see attn_bwd_common.cuh load_rows: lane 2l holds row 8l's cell
-      const int32_t c8 = __shfl_sync(0xffffffffu, c.x, (2 * lane) & 31);
-      if (lane < 16) sm100::tma_load_2d(dst + lane * 8 * D * 2, map, bar, h * D, base + c8, pol);
+    if (D == 32 && sq) {   // see attn_bwd_common.cuh load_rows: lane 16l holds row 64l's cell
+      const int32_t c64 = __shfl_sync(0xffffffffu, c.x, (16 * lane) & 31);
+      const int lw = sq - 1;
+      if (lane < 2)
+        sm100::tma_load_5d(dst + lane * 64 * D * 2, map, bar, 0, h, c64 & ((1 << lw) - 1), c64 >> lw, b, pol);
     } else {
       sm100::tma_gather4(dst + lane * 4 * D * 2, map, bar, h * D, base + c.x, base + c.y, base + c.z, base + c.w,
                          pol);
@@ -492,12 +494,14 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (kGather) {   // this warp's half of K (lanes 0-15), then, once PV freed the stage, of V
               if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.k_full[s], kTile / 2);
               __syncwarp();
-              const bool b8 = D == 32 && prm.box8;   // 8-row boxes: lanes 0-7, row 8l's cell from lane 2l
-              const int32_t c8 = b8 ? __shfl_sync(0xffffffffu, cells.x, (2 * lane) & 31) : 0;
+              // square boxes: this warp's 64 rows are one 8 x 8 cell square (its first cell: lane 0)
+              const bool b8 = D == 32 && prm.box8;
+              const int lw = prm.box8 - 1;
+              const int32_t c8 = b8 ? __shfl_sync(0xffffffffu, cells.x, 0) : 0;
               if (b8) {
-                if (lane < 8)
-                  sm100::tma_load_2d(sm.k[s] + (hh * 64 + 8 * lane) * D * 2, &tmK, &sm.k_full[s], h * D, base + c8,
-                                     pol_kv);
+                if (lane == 0)
+                  sm100::tma_load_5d(sm.k[s] + hh * 64 * D * 2, &tmK, &sm.k_full[s], 0, h, c8 & ((1 << lw) - 1),
+                                     c8 >> lw, b, pol_kv);
               } else if (lane < 16) {
                 sm100::tma_gather4(sm.k[s] + row * D * 2, &tmK, &sm.k_full[s], h * D, base + cells.x, base + cells.y,
                                    base + cells.z, base + cells.w, pol_kv);
@@ -506,9 +510,9 @@ __global__ void __launch_bounds__(kThreads, 2)
               if (lane == 0) sm100::mbar_arrive_expect_tx(&sm.v_full[s], kTile / 2);
               __syncwarp();
               if (b8) {
-                if (lane < 8)
-                  sm100::tma_load_2d(sm.v[s] + (hh * 64 + 8 * lane) * D * 2, &tmV, &sm.v_full[s], h * D, base + c8,
-                                     pol_kv);
+                if (lane == 0)
+                  sm100::tma_load_5d(sm.v[s] + hh * 64 * D * 2, &tmV, &sm.v_full[s], 0, h, c8 & ((1 << lw) - 1),
+                                     c8 >> lw, b, pol_kv);
               } else if (lane < 16) {
                 sm100::tma_gather4(sm.v[s] + row * D * 2, &tmV, &sm.v_full[s], h * D, base + cells.x, base + cells.y,
                                    base + cells.z, base + cells.w, pol_kv);
@@ -1143,15 +1147,18 @@ extern "C" hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_ma
   HLA_REQUIRE(!gather || d->order != HLA_ORDER_ROW_MAJOR, HLA_ERR_INVALID,
               "seq_to_cell (fused reorder) is only meaningful for Hilbert-order patterns");
   HLA_REQUIRE(!gather || ((uintptr_t)seq_to_cell & 15) == 0, HLA_ERR_INVALID, "seq_to_cell must be 16-byte aligned");
-  prm.box8 = gather && d->order == HLA_ORDER_HILBERT_TILED && head_dim == 32;
+  prm.box8 = (gather && d->order == HLA_ORDER_HILBERT_TILED && head_dim == 32) ? ilog2(pat.W) + 1 : 0;
   const int64_t rows = (int64_t)batch * pat.N;
   CUtensorMap mq, mk, mv, mo;
   if (gather) {
     if ((st = make_gather_map(&mo, o, rows, heads, head_dim)) != HLA_OK) return st;
-    const int kBoxH = prm.box8 ? 8 : 1;
-    if ((st = make_gather_map(&mq, q, rows, heads, head_dim, kBoxH)) != HLA_OK) return st;
-    if ((st = make_gather_map(&mk, k, rows, heads, head_dim, kBoxH)) != HLA_OK) return st;
-    if ((st = make_gather_map(&mv, v, rows, heads, head_dim, kBoxH)) != HLA_OK) return st;
+    auto mk_map = [&](CUtensorMap* mp, const void* base) {
+      return prm.box8 ? make_square_map(mp, base, batch, pat.H, pat.W, heads, head_dim)
+                      : make_gather_map(mp, base, rows, heads, head_dim);
+    };
+    if ((st = mk_map(&mq, q)) != HLA_OK) return st;
+    if ((st = mk_map(&mk, k)) != HLA_OK) return st;
+    if ((st = mk_map(&mv, v)) != HLA_OK) return st;
   } else {
     if ((st = make_rows_map(&mo, o, rows, heads, head_dim, kBlock)) != HLA_OK) return st;
     if ((st = make_rows_map(&mq, q, rows, heads, head_dim, kBlock)) != HLA_OK) return st;

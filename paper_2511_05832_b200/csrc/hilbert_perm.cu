@@ -63,7 +63,8 @@ __global__ void hilbert_index_kernel(int32_t N, int log2n, int32_t* __restrict__
 // segment of the curve is an aligned 8 x 8 cell square (the curve finishes each aligned 2^j
 // square before it leaves it); inside each segment the cells are renumbered in raster order,
 // s' = (s & ~63) + 8 * (row & 7) + (col & 7), so that every aligned 8 positions are 8
-// consecutive cells of one grid row (one 8-row TMA box instead of two gather4 ops).
+// consecutive cells of one grid row and every aligned 64 one aligned square in raster order (one
+// 5-D TMA box per square instead of 16 gather4 ops, attn_bwd_common.cuh load_rows).
 __global__ void hilbert_tiled_index_kernel(int32_t N, int log2n, int32_t* __restrict__ seq_to_cell,
                                            int32_t* __restrict__ cell_to_seq) {
   for (int32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < N; s += gridDim.x * blockDim.x) {

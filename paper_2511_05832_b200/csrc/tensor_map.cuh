@@ -48,6 +48,30 @@ inline hla_status make_rows_map(CUtensorMap* map, const void* base, int64_t rows
   return HLA_OK;
 }
 
+// bf16 tensor [batch, grid_h * grid_w cells, heads, head_dim] viewed as 5-D (head_dim, heads,
+// grid_w, grid_h, batch); box = (head_dim, 1, 8, 8, 1): one op moves an aligned 8 x 8 cell square
+// of one head, 64 rows in raster order -- a 64-token segment of the tiled Hilbert order.
+inline hla_status make_square_map(CUtensorMap* map, const void* base, int batch, int grid_h, int grid_w, int heads,
+                                  int head_dim) {
+  EncodeTiledFn enc;
+  hla_status st = get_encode_fn(&enc);
+  if (st != HLA_OK) return st;
+  const cuuint64_t row = (cuuint64_t)heads * head_dim * 2;
+  cuuint64_t dims[5] = {(cuuint64_t)head_dim, (cuuint64_t)heads, (cuuint64_t)grid_w, (cuuint64_t)grid_h,
+                        (cuuint64_t)batch};
+  cuuint64_t strides[4] = {(cuuint64_t)head_dim * 2, row, row * grid_w, row * grid_w * grid_h};
+  cuuint32_t box[5] = {(cuuint32_t)head_dim, 1, 8, 8, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUtensorMapSwizzle swz = head_dim * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                           : head_dim * 2 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                : CU_TENSOR_MAP_SWIZZLE_32B;
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  HLA_REQUIRE(r == CUDA_SUCCESS, HLA_ERR_CUDA, "cuTensorMapEncodeTiled (square) failed (%d)", (int)r);
+  return HLA_OK;
+}
+
 // bf16 tensor [rows_total, heads * head_dim] viewed as 2-D (heads*head_dim, rows) for
 // .tile::gather4 loads of single token rows: box = (head_dim, box_h).
 inline hla_status make_gather_map(CUtensorMap* map, const void* base, int64_t rows_total, int heads, int head_dim,

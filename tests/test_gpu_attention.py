@@ -171,7 +171,7 @@ def test_cfg5_stage(g, H):
     N = g * g
     q, k, v, do = _inputs(B, N, H, d, seed=21)
     layer = hla.HilbertLocalAttention("HWA", g, g, 8, 8, B, H, d, device=DEV)
-    assert layer.tiled          # d = 32, 64-token windows: the tiled order and 8-row box loads
+    assert layer.tiled          # d = 32, 64-token windows: the tiled order and square-box loads
     o = layer.forward(q, k, v).clone()
     dq, dk, dv = (t.clone() for t in layer.backward(do))
     torch.cuda.synchronize()
@@ -191,7 +191,7 @@ def test_tiled_order_vs_oracle_and_hilbert_order(g, w, B, H, d, blk):
     """HLA_ORDER_HILBERT_TILED (reading R23) through the layer: O, dQ, dK, dV equal the fp64
     oracle of the paper's Hilbert-order HWA on every checked slice, agree with the same layer in
     Hilbert order to bf16 rounding, and the LSE (kept in the tiled sequence order) is the oracle's
-    LSE relabeled.  d = 32 runs the 8-row box loads, d = 64 the gather4 loads over the tiled table."""
+    LSE relabeled.  d = 32 runs the square-box loads, d = 64 the gather4 loads over the tiled table."""
     N = g * g
     q, k, v, do = _inputs(B, N, H, d, seed=23)
     til = hla.HilbertLocalAttention("HWA", g, g, w, w, B, H, d, block=blk, device=DEV, tiled=True)
