@@ -65,9 +65,8 @@ typedef enum {
    * whose predicates only see whole 64-token segments -- HWA with n a multiple of 64 tokens
    * (the window of position s is s/n, unchanged by a relabeling inside a segment) and DENSE
    * (reading R23).  Any other pattern or grid: HLA_ERR_UNSUPPORTED.  With head_dim
-   * 32 and the fused reorder the kernels load every 8 positions (8 consecutive cells of a
-   * grid row; every aligned 64 an aligned 8 x 8 square) as one 5-D TMA box per square instead of
-   * 16 .tile::gather4 ops. */
+   * 32 and the fused reorder the kernels load every aligned 64 positions (an aligned 8 x 8
+   * cell square, raster order) with one 5-D TMA box instead of 16 .tile::gather4 ops. */
 } hla_order;
 
 /* Pattern families.  With order = HILBERT they are the paper's HWA / HSA / HNA /
