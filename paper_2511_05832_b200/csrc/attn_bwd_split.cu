@@ -271,6 +271,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                         idesc_h, kk > 0);
         sm100::mma_commit(&sm.s_full[half]);
       };
+      // kDiag: both halves' S^T / dP^T as one N = 128 product each (the two lane-quarter pairs
+      // compute their halves concurrently anyway): half the instructions of the half-tile issue
+      constexpr uint32_t idesc_f = sm100::make_idesc_bf16(kBlock, kBlock, false, false);
+      auto issue_sdp_full = [&](const TileIter& it, uint32_t gg) {
+        const int s = gg & 1;
+        const uint8_t* sk = sm.k[it.n & 1];
+        const uint8_t* sv = sm.v[it.n & 1];
+#pragma unroll
+        for (int kk = 0; kk < D / 16 && !(kVar & 1); ++kk)
+          sm100::mma_ss(tmem + kColS, kmajor_desc<D>(sk, kk), kmajor_desc<D>(sm.q[s], kk), idesc_f, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16 && !(kVar & 1); ++kk)
+          sm100::mma_ss(tmem + kColDP, kmajor_desc<D>(sv, kk), kmajor_desc<D>(sm.dO[s], kk), idesc_f, kk > 0);
+        sm100::mma_commit(&sm.s_full[0]);
+        sm100::mma_commit(&sm.s_full[1]);
+      };
       auto issue_dvdk = [&](uint32_t gg, int half, bool first_tile) {
         const int s = gg & 1;
         const uint8_t* ds = sm.ds[gg & 1];
@@ -287,8 +303,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         sm100::mbar_wait(&sm.kv_full[cur.n & 1], (cur.n >> 1) & 1);
         sm100::mbar_wait(&sm.q_full[0], 0);
         sm100::tc_fence_after();
-        issue_sdp(cur, 0, 0);
-        issue_sdp(cur, 0, 1);
+        if constexpr (kDiag) {
+          issue_sdp_full(cur, 0);
+        } else {
+          issue_sdp(cur, 0, 0);
+          issue_sdp(cur, 0, 1);
+        }
       }
       HLA_PMARK(tl0);
       while (cur.valid) {
@@ -309,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // S_A / dP_A of the next tile now if its operands already landed (never block
         // here: the B half of this tile must not wait behind the next tile's loads)
         bool next_a_issued = false;
-        if (nxt.valid && (nxt.t != 0 || sm100::mbar_test_wait(&sm.kv_full[nxt.n & 1], (nxt.n >> 1) & 1)) &&
+        if (!kDiag && nxt.valid && (nxt.t != 0 || sm100::mbar_test_wait(&sm.kv_full[nxt.n & 1], (nxt.n >> 1) & 1)) &&
             sm100::mbar_test_wait(&sm.q_full[(g + 1) & 1], ((g + 1) >> 1) & 1)) {
           sm100::tc_fence_after();
           issue_sdp(nxt, g + 1, 0);
@@ -342,9 +362,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (nxt.t == 0) HLA_PW(2, sm100::mbar_wait(&sm.kv_full[nxt.n & 1], (nxt.n >> 1) & 1));
             HLA_PW(2, sm100::mbar_wait(&sm.q_full[(g + 1) & 1], ((g + 1) >> 1) & 1));
             sm100::tc_fence_after();
-            issue_sdp(nxt, g + 1, 0);
+            if (!kDiag) issue_sdp(nxt, g + 1, 0);
           }
-          issue_sdp(nxt, g + 1, 1);
+          if (kDiag) issue_sdp_full(nxt, g + 1);
+          else issue_sdp(nxt, g + 1, 1);
         }
         cur = nxt;
         ++g;
