@@ -661,7 +661,15 @@ __global__ void __launch_bounds__(kThreads, 2)
     float pend_inv_l = 0.f;
     unsigned long long pend_optr = 0;   // 0: phantom row
     bool pend_staged = false;
+    // square mode (tiled order, prm.box8): this warp's 32 staged rows = 4 grid rows of 8 cells of one
+    // square, stored with one TMA box (tmO: 8 x 4 cells) from the first row's cell
+    int32_t pend_c = 0, pend_h = 0, pend_b = 0;
+    const bool sq_store = prm.box8 != 0;
     auto run_pending = [&]() {
+      if (sq_store && pend_staged) {   // the previous store has read its staging rows
+        if (lane == 0) sm100::bulk_wait_group_read0();
+        __syncwarp();
+      }
       uint32_t o[D];
 #pragma unroll
       for (int c = 0; c < D / 32; ++c)
@@ -682,7 +690,16 @@ __global__ void __launch_bounds__(kThreads, 2)
           reinterpret_cast<uint4*>(pend_optr)[v4] = w;
         }
       }
-      if (pend_staged) {   // this warp's rows back transposed: each STG.128 writes 8 whole 64-B rows
+      if (pend_staged && sq_store) {
+        sm100::fence_proxy_async_smem();   // the staged rows before the TMA engine reads them
+        __syncwarp();
+        if (lane == 0) {
+          const int lw = prm.box8 - 1;
+          sm100::tma_store_5d(&tmO, sm.ostage + quarter * 32 * D * 2, 0, pend_h, pend_c & ((1 << lw) - 1),
+                              pend_c >> lw, pend_b);
+          sm100::bulk_commit_group();
+        }
+      } else if (pend_staged) {   // this warp's rows back transposed: each STG.128 writes 8 whole 64-B rows
         __syncwarp();
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -911,6 +928,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         pend_inv_l = inv_l;
         pend_optr = real ? reinterpret_cast<unsigned long long>(optr) : 0ull;
         pend_staged = (qb + 1) * kBlock <= prm.N;
+        pend_c = __shfl_sync(0xffffffffu, ocell, 0);
+        pend_h = h;
+        pend_b = b;
         sm100::mbar_arrive(&sm.o_staged[it.n & 1]);
         const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
         if (real)
@@ -996,6 +1016,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       sm100::tc_fence_after();
       run_pending();
     }
+    if (o_double<D>() && sq_store && lane == 0) sm100::bulk_wait_group0();   // stores done before exit
     HLA_PFLUSH(3, 11, warp == 4 && lane == 0);
     HLA_PFLUSH(19, 20, warp == 4 && lane == 0);
     if (warp == 4 && lane == 0 && prm.visited != nullptr && tiles_done > 0) atomicAdd(prm.visited, tiles_done);
@@ -1151,7 +1172,9 @@ extern "C" hla_status hla_attn_fwd(const hla_pattern_desc* d, const hla_block_ma
   const int64_t rows = (int64_t)batch * pat.N;
   CUtensorMap mq, mk, mv, mo;
   if (gather) {
-    if ((st = make_gather_map(&mo, o, rows, heads, head_dim)) != HLA_OK) return st;
+    if ((st = prm.box8 ? make_square_map(&mo, o, batch, pat.H, pat.W, heads, head_dim, 4)
+                       : make_gather_map(&mo, o, rows, heads, head_dim)) != HLA_OK)
+      return st;
     auto mk_map = [&](CUtensorMap* mp, const void* base) {
       return prm.box8 ? make_square_map(mp, base, batch, pat.H, pat.W, heads, head_dim)
                       : make_gather_map(mp, base, rows, heads, head_dim);

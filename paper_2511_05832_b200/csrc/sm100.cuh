@@ -160,6 +160,14 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
                "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
                : "memory");
 }
+// 5-D tile store shared -> global (bulk async group)
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, const void* src, int32_t c0, int32_t c1,
+                                             int32_t c2, int32_t c3, int32_t c4) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+               : "memory");
+}
 // 2-D scatter of 4 rows (sm_100 .tile::scatter4): 4 consecutive box rows in shared
 // memory to rows y0..y3 at column x of a 2-D tensor map (bulk async group)
 __device__ __forceinline__ void tma_scatter4(const CUtensorMap* map, const void* src, int32_t x, int32_t y0,

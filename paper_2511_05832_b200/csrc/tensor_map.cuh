@@ -52,7 +52,7 @@ inline hla_status make_rows_map(CUtensorMap* map, const void* base, int64_t rows
 // grid_w, grid_h, batch); box = (head_dim, 1, 8, 8, 1): one op moves an aligned 8 x 8 cell square
 // of one head, 64 rows in raster order -- a 64-token segment of the tiled Hilbert order.
 inline hla_status make_square_map(CUtensorMap* map, const void* base, int batch, int grid_h, int grid_w, int heads,
-                                  int head_dim) {
+                                  int head_dim, int box_rows = 8) {
   EncodeTiledFn enc;
   hla_status st = get_encode_fn(&enc);
   if (st != HLA_OK) return st;
@@ -60,7 +60,7 @@ inline hla_status make_square_map(CUtensorMap* map, const void* base, int batch,
   cuuint64_t dims[5] = {(cuuint64_t)head_dim, (cuuint64_t)heads, (cuuint64_t)grid_w, (cuuint64_t)grid_h,
                         (cuuint64_t)batch};
   cuuint64_t strides[4] = {(cuuint64_t)head_dim * 2, row, row * grid_w, row * grid_w * grid_h};
-  cuuint32_t box[5] = {(cuuint32_t)head_dim, 1, 8, 8, 1};
+  cuuint32_t box[5] = {(cuuint32_t)head_dim, 1, 8, (cuuint32_t)box_rows, 1};   // box_rows < 8: part of a square
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   CUtensorMapSwizzle swz = head_dim * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
                            : head_dim * 2 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
